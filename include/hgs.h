@@ -1,0 +1,177 @@
+/*
+ * hgs.h -- C ABI of libhgs.so, the sm_100a hybrid 2D/3D Gaussian rasterizer.
+ *
+ * This is the drop-in boundary.  It replaces the reference's native blend seam
+ * `hybridsplat.raster._blend_cy` (declared in pkg/setup.py:5-13, bound at
+ * raster/render.py:73-80 and grad/backward.py:19-30) -- and, because
+ * preprocess and binning are hot too, the whole of
+ *   build_frame            raster/project.py:360-379
+ *   forward_blend          raster/_blend_py.py:55-123
+ *   backward_blend         raster/_blend_py.py:126-242
+ *   backward chain rule    grad/backward.py:68-178
+ *   exchange_pass          exchange.py:137-155
+ * All paths below are relative to /root/reference/pkg/src/hybridsplat.
+ *
+ * Conventions
+ *  - Plain C types only.  Every pointer in hgs_scene / hgs_images / grads is a
+ *    DEVICE pointer (cudaMalloc / PyTorch caching allocator); structs passed
+ *    by pointer live in HOST memory.
+ *  - The library never allocates or frees device memory and keeps no global
+ *    state: the caller provides a frame buffer (hgs_frame_bytes) that holds
+ *    everything a forward produces and a backward consumes.
+ *  - Work is enqueued on the caller's stream (a cudaStream_t passed as void*).
+ *    hgs_forward synchronises that stream once, to read the number of
+ *    tile/splat pairs K (data dependent) before binning.
+ *  - Errors are returned as hgs_status codes; the Python layer maps them to
+ *    the reference exception classes (hybridsplat/errors.py).
+ */
+#ifndef HGS_H_
+#define HGS_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HGS_ABI_VERSION 1
+
+typedef enum hgs_status {
+  HGS_OK = 0,
+  HGS_ERR_CONFIG = 1,            /* ConfigError: bad camera / settings / shapes  */
+  HGS_ERR_INVALID_PARAMETER = 2, /* InvalidParameterError: |q| <= 1e-8 (rotation.py:19-20) */
+  HGS_ERR_INTEGRITY = 3,         /* IntegrityError: frame / scene / grad mismatch */
+  HGS_ERR_DEGENERATE_SCALE = 4,  /* DegenerateScaleError (exchange.py:67-68)      */
+  HGS_ERR_PAIR_CAPACITY = 5,     /* frame buffer too small for K pairs: grow + retry */
+  HGS_ERR_CUDA = 6               /* a CUDA launch / copy failed                   */
+} hgs_status;
+
+/* Scene in structure-of-arrays layout, float32 (reference: core/types.py:32-50,
+ * float64 there).  sh is (n, 3, sh_bases) channel-major; type_spec 0 = 2D surfel,
+ * 1 = 3D Gaussian. */
+typedef struct hgs_scene {
+  int64_t n;
+  int32_t sh_bases; /* (degree + 1)^2, degree <= 3 */
+  int32_t reserved;
+  const float *center;        /* (n, 3) */
+  const float *log_scale;     /* (n, 3) */
+  const float *rotation;      /* (n, 4) w-first, not necessarily unit */
+  const float *opacity_logit; /* (n) */
+  const float *sh;            /* (n, 3, sh_bases) */
+  const uint8_t *type_spec;   /* (n) */
+} hgs_scene;
+
+/* Pinhole camera (core/types.py:145-197); pixel (ix, iy) samples (ix+.5, iy+.5). */
+typedef struct hgs_camera {
+  double fx, fy, cx, cy;
+  int32_t width, height;
+  double world_to_camera[16]; /* row-major 4x4 */
+  double near_plane, far_plane;
+} hgs_camera;
+
+/* RenderSettings (raster/project.py:34-45) + mode flags. */
+typedef struct hgs_settings {
+  float background[3];
+  int32_t tile_size; /* must be 16 */
+  double theta_z, t_z, lambda_z;
+  uint32_t flags;
+  uint32_t reserved;
+} hgs_settings;
+
+#define HGS_FLAG_NAIVE 0x1u /* render_naive: every splat for every pixel, no tiles, no bbox test (render.py:101-118) */
+#define HGS_FLAG_FAST 0x2u  /* skip the float64 re-evaluation of near-threshold decisions */
+
+/* Output images (device, row-major).  Any of normal / alpha may be NULL. */
+typedef struct hgs_images {
+  float *color;         /* (H, W, 3): blend + background * T (render.py:54-61) */
+  float *depth;         /* (H, W): sum w * z_center (_blend_py.py:105) */
+  float *transmittance; /* (H, W) */
+  float *alpha;         /* (H, W): 1 - T                      [extension] */
+  float *normal;        /* (H, W, 3): sum w * n_camera         [extension] */
+} hgs_images;
+
+/* Filled by hgs_forward, consumed by hgs_backward / hgs_frame_export. */
+typedef struct hgs_frame_info {
+  int64_t n;          /* Gaussians in the scene */
+  int64_t m;          /* splats kept (near + singular-conic cull), SplatFrame.count */
+  int64_t k;          /* tile/splat pairs = len(tile_ids) */
+  int64_t n_tiles;
+  int32_t width, height, tiles_x, tiles_y;
+  int64_t pair_capacity;
+  int32_t sh_bases;
+  uint32_t flags;
+  uint64_t counters[4]; /* diagnostics: f64 re-checks taken in the last composite */
+} hgs_frame_info;
+
+/* Bytes of device memory hgs_forward needs for n Gaussians at W x H and room
+ * for pair_capacity tile/splat pairs. */
+size_t hgs_frame_bytes(int64_t n, int32_t width, int32_t height, int32_t tile_size, int64_t pair_capacity);
+
+/* render (raster/render.py:83-98): project, depth-sort, bin, composite.
+ * Returns HGS_ERR_PAIR_CAPACITY (info->k = required pairs) if the frame buffer
+ * cannot hold K pairs; the caller grows the buffer and calls again. */
+int hgs_forward(const hgs_scene *scene, const hgs_camera *camera, const hgs_settings *settings, void *frame,
+                size_t frame_bytes, const hgs_images *out, hgs_frame_info *info, void *stream);
+
+/* Scratch bytes for hgs_backward with kg stacked upstream gradients. */
+size_t hgs_backward_scratch_bytes(int64_t n, int32_t kg);
+
+/* backward (grad/backward.py:37-181).
+ *   pixel_grads  (kg, H, W, 3) dL/dcolor, required
+ *   depth_grads  (kg, H, W)    dL/ddepth,  nullable   [extension]
+ *   normal_grads (kg, H, W, 3) dL/dnormal, nullable   [extension]
+ *   alpha_grads  (kg, H, W)    dL/dalpha,  nullable   [extension]
+ *   grads        (kg, n * P) out, P = 11 + 3 * sh_bases, each kg block laid out
+ *                field-major: center (n,3) | log_scale (n,3) | rotation (n,4) |
+ *                opacity_logit (n) | sh (n,3,B)  (ParamGrads, grad/bundle.py:11-30)
+ *   touched      (n) uint8 out, 1 = the Gaussian contributed to some pixel
+ * The frame buffer must hold the hgs_forward result for the same scene. */
+int hgs_backward(const hgs_scene *scene, const hgs_camera *camera, const hgs_settings *settings, const void *frame,
+                 const hgs_frame_info *info, int32_t kg, const float *pixel_grads, const float *depth_grads,
+                 const float *normal_grads, const float *alpha_grads, void *scratch, size_t scratch_bytes,
+                 float *grads, uint8_t *touched, void *stream);
+
+/* Adaptive type exchange (exchange.py:137-155), in place on log_scale, rotation
+ * and type_spec (device).  eranks (n) float out (nullable).  report (host) =
+ * {n_3d_to_2d, n_2d_to_3d, n_2d, n_3d, hist[20] over [1, 3]}.  scratch: 256 B. */
+typedef struct hgs_exchange_report {
+  int64_t n_3d_to_2d, n_2d_to_3d, n_2d, n_3d;
+  int64_t erank_hist[20];
+} hgs_exchange_report;
+
+int hgs_exchange(int64_t n, float *log_scale, float *rotation, uint8_t *type_spec, double theta_e, float *eranks,
+                 void *scratch, hgs_exchange_report *report, void *stream);
+
+/* Test / API-parity export of the sorted SplatFrame (raster/project.py:60-90)
+ * into caller device buffers (each nullable): idx (m) i32, typ (m) u8,
+ * depth (m), center2d (m,2), cov2d (m,3), conic (m,3), mrow (m,3,4),
+ * alpha_eff (m), color (m,3), bbox (m,4) i32, radius (m), tile_offsets
+ * (n_tiles+1) i64, tile_ids (k) i32.  Values are the float64 preprocess
+ * results (bit-for-bit what the binning used). */
+typedef struct hgs_frame_export {
+  int32_t *idx;
+  uint8_t *typ;
+  double *depth, *center2d, *cov2d, *conic, *mrow, *alpha_eff, *color, *radius, *normal;
+  int32_t *bbox;
+  int64_t *tile_offsets;
+  int32_t *tile_ids;
+  int32_t *pixel_count; /* (H, W) blend-log entries per pixel */
+} hgs_frame_export;
+
+int hgs_frame_export_arrays(const hgs_scene *scene, const hgs_camera *camera, const hgs_settings *settings,
+                            const void *frame, const hgs_frame_info *info, const hgs_frame_export *out, void *stream);
+
+/* Blend log (raster/render.py:30-51) for small frames: offsets (H*W+1) i64 from
+ * the pixel counts, position (total) i32, alpha / u / v (total) float. */
+int hgs_blend_log(const hgs_scene *scene, const hgs_camera *camera, const hgs_settings *settings, const void *frame,
+                  const hgs_frame_info *info, const int64_t *offsets, int32_t *position, float *alpha, float *u,
+                  float *v, void *stream);
+
+const char *hgs_status_string(int status);
+int hgs_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HGS_H_ */

@@ -1,0 +1,175 @@
+"""Generate golden fixtures by running the REFERENCE implementation.
+
+Run in the build container (where /root/reference exists):
+
+    PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_golden.py
+
+It imports the reference package ``hybridsplat`` from
+/root/reference/pkg/src, renders / back-propagates / exchanges a set of seeded
+scenes, and writes compressed ``.npz`` fixtures next to this script.  The
+fixtures pin the CPU oracle (tests/test_oracle_golden.py) and, on the GPU box
+where the reference is absent, the CUDA path (tests/test_gpu_*.py).
+
+Scene inputs are float32-representable (synthetic_scene rounds them), so they
+are stored as float32 without loss; reference outputs are stored as float64.
+"""
+
+import os
+import sys
+import time
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+REPO = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, "/root/reference/pkg/src")
+sys.path.insert(0, REPO)
+
+import hybridsplat as hs  # noqa: E402  (the reference)
+from hybridsplat.grad import backward as ref_backward  # noqa: E402
+from hybridsplat.raster import RenderSettings, render as ref_render  # noqa: E402
+from hybridsplat.raster import render_naive as ref_render_naive  # noqa: E402
+
+from paper_2512_02932_b200.synthetic import f32_exact, synthetic_scene  # noqa: E402
+
+
+def to_ref(scene, cam):
+    rs = hs.core.GaussianSet(scene.center, scene.log_scale, scene.rotation,
+                             scene.opacity_logit, scene.sh_coeffs, scene.type_spec)
+    rc = hs.core.CameraView(cam.fx, cam.fy, cam.cx, cam.cy, cam.width, cam.height,
+                            cam.world_to_camera, near=cam.near, far=cam.far)
+    return rs, rc
+
+
+def scene_arrays(scene, cam, st):
+    return dict(
+        in_center=scene.center.astype(np.float32), in_log_scale=scene.log_scale.astype(np.float32),
+        in_rotation=scene.rotation.astype(np.float32),
+        in_opacity_logit=scene.opacity_logit.astype(np.float32),
+        in_sh=scene.sh_coeffs.astype(np.float32), in_type=scene.type_spec,
+        cam_intr=np.array([cam.fx, cam.fy, cam.cx, cam.cy, cam.near, cam.far]),
+        cam_size=np.array([cam.width, cam.height]), cam_w2c=cam.world_to_camera,
+        background=np.array(st.background, np.float64),
+        modulation=np.array([st.theta_z, st.t_z, st.lambda_z]))
+
+
+def render_fixture(name, scene, cam, st, kg=1, with_log=True, naive=False, seed=11):
+    rs, rc = to_ref(scene, cam)
+    t0 = time.time()
+    out = ref_render(rs, rc, st)
+    t_fwd = time.time() - t0
+    f = out.frame
+    data = scene_arrays(scene, cam, st)
+    data.update(
+        f_idx=f.idx, f_typ=f.typ, f_depth=f.depth, f_center2d=f.center2d, f_cov2d=f.cov2d,
+        f_conic=f.conic, f_mrow=f.mrow, f_alpha=f.alpha, f_alpha_eff=f.alpha_eff,
+        f_color=f.color, f_bbox=f.bbox, f_radius=f.radius, f_tile_offsets=f.tile_offsets,
+        f_tile_ids=f.tile_ids, color=out.color, depth=out.depth,
+        transmittance=out.transmittance)
+    if with_log:
+        lg = out.blend_log
+        data.update(log_offsets=lg.offsets, log_pos=lg.position, log_alpha=lg.alpha,
+                    log_u=lg.u, log_v=lg.v)
+    else:
+        data.update(log_counts=np.diff(out.blend_log.offsets).astype(np.int32))
+    if naive:
+        nv = ref_render_naive(rs, rc, st)
+        data.update(naive_color=nv.color, naive_depth=nv.depth,
+                    naive_transmittance=nv.transmittance)
+    rng = np.random.default_rng(seed)
+    pg = f32_exact(rng.normal(size=(kg, cam.height, cam.width, 3)))
+    t0 = time.time()
+    grads, touched = ref_backward(rs, rc, out, pg)
+    t_bwd = time.time() - t0
+    data.update(pixel_grad=pg.astype(np.float32),
+                grads=np.stack([g.flat() for g in grads]), touched=touched)
+    path = os.path.join(HERE, name + ".npz")
+    np.savez_compressed(path, **data)
+    print("%-14s N=%-6d M=%-6d K=%-7d fwd %.1fs bwd %.1fs -> %s (%.0f kB)"
+          % (name, scene.count, f.count, f.tile_ids.size, t_fwd, t_bwd, os.path.basename(path),
+             os.path.getsize(path) / 1024))
+
+
+def stress2d_scene(seed=5, n=60, size=48):
+    """Large, tilted, near-camera 2D surfels: exercises the dual-conic AABB and
+    its full-screen fallback ('Hard parts')."""
+    from paper_2512_02932_b200.core import GaussianSet
+    from paper_2512_02932_b200.synthetic import synthetic_camera
+    rng = np.random.default_rng(seed)
+    cam = synthetic_camera(size, size)
+    z = rng.uniform(0.3, 3.0, n)
+    px = rng.uniform(-0.2 * size, 1.2 * size, n)
+    py = rng.uniform(-0.2 * size, 1.2 * size, n)
+    center = np.stack([(px - cam.cx) * z / cam.fx, (py - cam.cy) * z / cam.fy, z], 1)
+    ls = np.log(rng.uniform(0.05, 0.8, (n, 3)))
+    rot = rng.normal(size=(n, 4))
+    rot /= np.linalg.norm(rot, axis=1, keepdims=True)
+    sc = GaussianSet(f32_exact(center), f32_exact(ls), f32_exact(rot),
+                     f32_exact(rng.normal(size=n)), f32_exact(rng.normal(0, .3, (n, 3, 4))),
+                     np.zeros(n, np.uint8))
+    return sc, cam
+
+
+def rotated_camera_scene(seed=7):
+    """Non-identity world-to-camera: exercises V in projection and chain rule."""
+    from paper_2512_02932_b200.synthetic import synthetic_camera
+    sc, cam = synthetic_scene(500, 64, 48, 2, seed=seed)
+    ang = 0.3
+    Rz = np.array([[np.cos(ang), -np.sin(ang), 0], [np.sin(ang), np.cos(ang), 0], [0, 0, 1]])
+    Rx = np.array([[1, 0, 0], [0, np.cos(0.2), -np.sin(0.2)], [0, np.sin(0.2), np.cos(0.2)]])
+    R = Rx @ Rz
+    w2c = np.eye(4)
+    w2c[:3, :3] = R
+    w2c[:3, 3] = [0.05, -0.1, 0.2]
+    # Move the scene so it stays in view: x_world = R^T (x_cam - t)
+    xc = sc.center
+    sc.center[:] = f32_exact((xc - w2c[:3, 3]) @ R)
+    return sc, synthetic_camera(64, 48, w2c)
+
+
+def exchange_fixture():
+    rng = np.random.default_rng(13)
+    n = 4000
+    ls = f32_exact(rng.normal(0.0, 1.0, (n, 3)) * rng.uniform(0.05, 1.5, (n, 1)) - 2.0)
+    # a block of near-threshold rows and exact ties for choose_permutation
+    ls[:50] = f32_exact(np.log([[1.0, 1.0, 2.6]] * 50) + rng.normal(0, 0.01, (50, 3)))
+    ls[50:60] = f32_exact(np.log(np.array([[0.5, 0.5, 2.0]] * 10)))
+    ls[60:70] = f32_exact(np.log(np.array([[2.0, 0.5, 0.5]] * 10)))
+    rot = rng.normal(size=(n, 4))
+    rot = f32_exact(rot / np.linalg.norm(rot, axis=1, keepdims=True))
+    ty = (rng.random(n) < 0.5).astype(np.uint8)
+    sc = hs.core.GaussianSet(np.zeros((n, 3)), ls.copy(), rot.copy(), np.zeros(n),
+                             np.zeros((n, 3, 1)), ty.copy())  # the reference aliases f64 inputs
+    rep = hs.exchange.exchange_pass(sc, hs.exchange.ExchangeConfig())
+    np.savez_compressed(os.path.join(HERE, "exchange.npz"),
+                        in_log_scale=ls.astype(np.float32), in_rotation=rot.astype(np.float32),
+                        in_type=ty, out_log_scale=sc.log_scale, out_rotation=sc.rotation,
+                        out_type=sc.type_spec, eranks=hs.exchange.effective_rank(ls),
+                        counts=np.array([rep.n_3d_to_2d, rep.n_2d_to_3d, rep.n_2d, rep.n_3d]),
+                        hist=rep.erank_hist, edges=rep.erank_edges)
+    print("exchange: demoted %d promoted %d" % (rep.n_3d_to_2d, rep.n_2d_to_3d))
+
+
+def main(which=None):
+    jobs = {
+        "tiny_sh3": lambda: render_fixture(
+            "tiny_sh3", *synthetic_scene(400, 64, 48, 3, seed=1),
+            RenderSettings(background=(0.1, 0.2, 0.3)), kg=2, naive=True),
+        "stress2d": lambda: render_fixture(
+            "stress2d", *stress2d_scene(), RenderSettings(background=(0.0, 0.5, 1.0)), kg=1,
+            naive=True),
+        "rotcam_sh2": lambda: render_fixture(
+            "rotcam_sh2", *rotated_camera_scene(), RenderSettings(), kg=3),
+        "c1": lambda: render_fixture(
+            "c1", *synthetic_scene(10_000, 256, 256, 0, seed=0), RenderSettings(), kg=1,
+            with_log=False),
+        "exchange": exchange_fixture,
+    }
+    for name, fn in jobs.items():
+        if which and name not in which:
+            continue
+        fn()
+
+
+if __name__ == "__main__":
+    main(sys.argv[1:])
