@@ -101,7 +101,7 @@ typedef struct hgs_frame_info {
   int64_t pair_capacity;
   int32_t sh_bases;
   uint32_t flags;
-  uint64_t counters[4]; /* diagnostics: f64 re-checks taken in the last composite */
+  uint32_t internal[4]; /* library bookkeeping (which ping-pong buffer holds the tile lists) */
 } hgs_frame_info;
 
 /* Bytes of device memory hgs_forward needs for n Gaussians at W x H and room

@@ -1,0 +1,177 @@
+"""ctypes binding of libhgs.so (include/hgs.h).
+
+The extension is mandatory: if libhgs.so is missing or fails to load, every
+entry point raises ExtensionError.  There is no CPU fallback.
+"""
+
+import ctypes
+import os
+
+from .errors import (ConfigError, DegenerateScaleError, ExtensionError, IntegrityError,
+                     InvalidParameterError, SplatError)
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libhgs.so")
+
+HGS_OK = 0
+HGS_ERR_CONFIG = 1
+HGS_ERR_INVALID_PARAMETER = 2
+HGS_ERR_INTEGRITY = 3
+HGS_ERR_DEGENERATE_SCALE = 4
+HGS_ERR_PAIR_CAPACITY = 5
+HGS_ERR_CUDA = 6
+
+HGS_FLAG_NAIVE = 0x1
+HGS_FLAG_FAST = 0x2
+
+# Every symbol include/hgs.h declares.
+EXPORTS = ("hgs_abi_version", "hgs_status_string", "hgs_frame_bytes", "hgs_forward",
+           "hgs_backward_scratch_bytes", "hgs_backward", "hgs_exchange",
+           "hgs_frame_export_arrays", "hgs_blend_log")
+
+_vp = ctypes.c_void_p
+_i64 = ctypes.c_int64
+_i32 = ctypes.c_int32
+
+
+class Scene(ctypes.Structure):
+    _fields_ = [("n", _i64), ("sh_bases", _i32), ("reserved", _i32),
+                ("center", _vp), ("log_scale", _vp), ("rotation", _vp),
+                ("opacity_logit", _vp), ("sh", _vp), ("type_spec", _vp)]
+
+
+class Camera(ctypes.Structure):
+    _fields_ = [("fx", ctypes.c_double), ("fy", ctypes.c_double), ("cx", ctypes.c_double),
+                ("cy", ctypes.c_double), ("width", _i32), ("height", _i32),
+                ("world_to_camera", ctypes.c_double * 16), ("near_plane", ctypes.c_double),
+                ("far_plane", ctypes.c_double)]
+
+
+class Settings(ctypes.Structure):
+    _fields_ = [("background", ctypes.c_float * 3), ("tile_size", _i32),
+                ("theta_z", ctypes.c_double), ("t_z", ctypes.c_double),
+                ("lambda_z", ctypes.c_double), ("flags", ctypes.c_uint32),
+                ("reserved", ctypes.c_uint32)]
+
+
+class Images(ctypes.Structure):
+    _fields_ = [("color", _vp), ("depth", _vp), ("transmittance", _vp), ("alpha", _vp),
+                ("normal", _vp)]
+
+
+class FrameInfo(ctypes.Structure):
+    _fields_ = [("n", _i64), ("m", _i64), ("k", _i64), ("n_tiles", _i64),
+                ("width", _i32), ("height", _i32), ("tiles_x", _i32), ("tiles_y", _i32),
+                ("pair_capacity", _i64), ("sh_bases", _i32), ("flags", ctypes.c_uint32),
+                ("internal", ctypes.c_uint32 * 4)]
+
+
+class ExchangeReport(ctypes.Structure):
+    _fields_ = [("n_3d_to_2d", _i64), ("n_2d_to_3d", _i64), ("n_2d", _i64), ("n_3d", _i64),
+                ("erank_hist", _i64 * 20)]
+
+
+class FrameExport(ctypes.Structure):
+    _fields_ = [("idx", _vp), ("typ", _vp), ("depth", _vp), ("center2d", _vp), ("cov2d", _vp),
+                ("conic", _vp), ("mrow", _vp), ("alpha_eff", _vp), ("color", _vp),
+                ("radius", _vp), ("normal", _vp), ("bbox", _vp), ("tile_offsets", _vp),
+                ("tile_ids", _vp), ("pixel_count", _vp)]
+
+
+_lib = None
+_load_error = None
+
+
+def lib():
+    """The loaded libhgs.so; raises ExtensionError if it is unavailable."""
+    global _lib, _load_error
+    if _lib is not None:
+        return _lib
+    if _load_error is not None:
+        raise ExtensionError(_load_error)
+    if not os.path.exists(LIB_PATH):
+        _load_error = ("libhgs.so not built (%s); run __graft_entry__.build() or "
+                       "make -C paper_2512_02932_b200/csrc" % LIB_PATH)
+        raise ExtensionError(_load_error)
+    try:
+        L = ctypes.CDLL(LIB_PATH)
+    except OSError as e:  # pragma: no cover - depends on the machine
+        _load_error = "failed to load libhgs.so: %s" % e
+        raise ExtensionError(_load_error)
+    P = ctypes.POINTER
+    L.hgs_abi_version.restype = ctypes.c_int
+    L.hgs_status_string.restype = ctypes.c_char_p
+    L.hgs_status_string.argtypes = [ctypes.c_int]
+    L.hgs_frame_bytes.restype = ctypes.c_size_t
+    L.hgs_frame_bytes.argtypes = [_i64, _i32, _i32, _i32, _i64]
+    L.hgs_forward.argtypes = [P(Scene), P(Camera), P(Settings), _vp, ctypes.c_size_t, P(Images),
+                              P(FrameInfo), _vp]
+    L.hgs_backward_scratch_bytes.restype = ctypes.c_size_t
+    L.hgs_backward_scratch_bytes.argtypes = [_i64, _i32]
+    L.hgs_backward.argtypes = [P(Scene), P(Camera), P(Settings), _vp, P(FrameInfo), _i32, _vp, _vp,
+                               _vp, _vp, _vp, ctypes.c_size_t, _vp, _vp, _vp]
+    L.hgs_exchange.argtypes = [_i64, _vp, _vp, _vp, ctypes.c_double, _vp, _vp, P(ExchangeReport),
+                               _vp]
+    L.hgs_frame_export_arrays.argtypes = [P(Scene), P(Camera), P(Settings), _vp, P(FrameInfo),
+                                          P(FrameExport), _vp]
+    L.hgs_blend_log.argtypes = [P(Scene), P(Camera), P(Settings), _vp, P(FrameInfo), _vp, _vp,
+                                _vp, _vp, _vp, _vp]
+    if L.hgs_abi_version() != 1:
+        _load_error = "libhgs.so ABI version mismatch"
+        raise ExtensionError(_load_error)
+    _lib = L
+    return _lib
+
+
+def available():
+    try:
+        lib()
+        return True
+    except ExtensionError:
+        return False
+
+
+_STATUS_EXC = {
+    HGS_ERR_CONFIG: ConfigError,
+    HGS_ERR_INVALID_PARAMETER: InvalidParameterError,
+    HGS_ERR_INTEGRITY: IntegrityError,
+    HGS_ERR_DEGENERATE_SCALE: DegenerateScaleError,
+    HGS_ERR_CUDA: ExtensionError,
+}
+
+
+def check(status, what):
+    if status == HGS_OK:
+        return
+    msg = "%s: %s" % (what, lib().hgs_status_string(status).decode())
+    raise _STATUS_EXC.get(status, SplatError)(msg)
+
+
+def ptr(t):
+    """Device pointer of a torch tensor (or None)."""
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def current_stream_handle(device=None):
+    import torch
+    return ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)
+
+
+def scene_struct(ds):
+    return Scene(ds.count, ds.sh_bases, 0, ds.center.data_ptr(), ds.log_scale.data_ptr(),
+                 ds.rotation.data_ptr(), ds.opacity_logit.data_ptr(), ds.sh_coeffs.data_ptr(),
+                 ds.type_spec.data_ptr())
+
+
+def camera_struct(cam):
+    w2c = [float(v) for v in cam.world_to_camera.reshape(16)]
+    return Camera(float(cam.fx), float(cam.fy), float(cam.cx), float(cam.cy), int(cam.width),
+                  int(cam.height), (ctypes.c_double * 16)(*w2c), float(cam.near), float(cam.far))
+
+
+def settings_struct(st, flags=0):
+    bg = [float(b) for b in st.background]
+    if len(bg) != 3:
+        raise ConfigError("background must have 3 channels")
+    return Settings((ctypes.c_float * 3)(*bg), int(st.tile_size), float(st.theta_z),
+                    float(st.t_z), float(st.lambda_z), int(flags), 0)

@@ -1,0 +1,552 @@
+// hgs_api.cu -- the C ABI declared in include/hgs.h: frame-buffer layout,
+// launch orchestration, error mapping.  No device allocation happens here;
+// every buffer is carved out of caller memory.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+#include "hgs_kernels.cuh"
+
+namespace hgs {
+
+namespace {
+
+constexpr int kMaxGrid = 148 * 8;
+
+struct Layout {
+  size_t state, hist_d, off_d, hist_p, off_p, keys_a, keys_b, vals_a, vals_b, lb_sort, lb_scan, recs, pair_off,
+      pk_a, pk_b, pv_a, pv_b, tile_off, pix_T, pix_last, pix_count, total;
+  size_t small_end;  // [state, small_end) is zeroed at the start of a forward
+  size_t lb_sort_bytes, lb_scan_bytes;
+};
+
+int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+Layout make_layout(int64_t n, int W, int H, int64_t cap) {
+  Layout L;
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    size_t o = off;
+    off += (bytes + 255) & ~(size_t)255;
+    return o;
+  };
+  const int64_t n_tiles = ceil_div(W, kTile) * ceil_div(H, kTile);
+  const int64_t nn = std::max<int64_t>(n, 1), cc = std::max<int64_t>(cap, 1);
+  L.state = take(sizeof(FrameState));
+  L.hist_d = take(8 * kRadix * 4);
+  L.off_d = take(8 * kRadix * 4);
+  L.hist_p = take(2 * kRadix * 4);
+  L.off_p = take(2 * kRadix * 4);
+  L.small_end = off;
+  L.lb_sort_bytes = (size_t)std::max<int64_t>(8 * ceil_div(nn, kSortTile), 2 * ceil_div(cc, kSortTile)) * kRadix * 4;
+  L.lb_sort = take(L.lb_sort_bytes);
+  L.lb_scan_bytes = (size_t)ceil_div(nn, kScanThreads) * 8;
+  L.lb_scan = take(L.lb_scan_bytes);
+  L.keys_a = take(nn * 8);
+  L.keys_b = take(nn * 8);
+  L.vals_a = take(nn * 4);
+  L.vals_b = take(nn * 4);
+  L.recs = take(nn * sizeof(SplatRec));
+  L.pair_off = take(nn * 8);
+  L.tile_off = take((n_tiles + 1) * 4);
+  L.pix_T = take((size_t)W * H * 4);
+  L.pix_last = take((size_t)W * H * 4);
+  L.pix_count = take((size_t)W * H * 4);
+  L.pk_a = take(cc * 4);
+  L.pk_b = take(cc * 4);
+  L.pv_a = take(cc * 4);
+  L.pv_b = take(cc * 4);
+  L.total = off;
+  return L;
+}
+
+template <typename T>
+T *at(void *base, size_t off) {
+  return reinterpret_cast<T *>(static_cast<char *>(base) + off);
+}
+template <typename T>
+const T *at(const void *base, size_t off) {
+  return reinterpret_cast<const T *>(static_cast<const char *>(base) + off);
+}
+
+CamD make_cam(const hgs_camera &c) {
+  CamD d;
+  for (int r = 0; r < 3; ++r) {
+    for (int k = 0; k < 3; ++k) d.V[r * 3 + k] = c.world_to_camera[r * 4 + k];
+    d.tv[r] = c.world_to_camera[r * 4 + 3];
+  }
+  const double K[16] = {c.fx, 0, c.cx, 0, 0, c.fy, c.cy, 0, 0, 0, 1, 0, 0, 0, 1, 0};
+  for (int r = 0; r < 4; ++r)
+    for (int k = 0; k < 4; ++k)
+      d.T[r * 4 + k] = ((K[r * 4] * c.world_to_camera[k] + K[r * 4 + 1] * c.world_to_camera[4 + k]) +
+                        K[r * 4 + 2] * c.world_to_camera[8 + k]) +
+                       K[r * 4 + 3] * c.world_to_camera[12 + k];
+  for (int k = 0; k < 3; ++k) d.campos[k] = -((d.V[k] * d.tv[0] + d.V[3 + k] * d.tv[1]) + d.V[6 + k] * d.tv[2]);
+  d.fx = c.fx; d.fy = c.fy; d.cx = c.cx; d.cy = c.cy; d.near_plane = c.near_plane;
+  d.width = c.width; d.height = c.height;
+  d.tiles_x = (int)ceil_div(c.width, kTile);
+  d.tiles_y = (int)ceil_div(c.height, kTile);
+  return d;
+}
+
+SceneView make_scene(const hgs_scene &s) {
+  SceneView v;
+  v.center = s.center; v.log_scale = s.log_scale; v.rotation = s.rotation; v.opacity_logit = s.opacity_logit;
+  v.sh = s.sh; v.type_spec = s.type_spec; v.n = s.n; v.sh_bases = s.sh_bases;
+  return v;
+}
+
+int check_common(const hgs_scene *sc, const hgs_camera *cam, const hgs_settings *st) {
+  if (!sc || !cam || !st) return HGS_ERR_CONFIG;
+  if (st->tile_size != kTile) return HGS_ERR_CONFIG;
+  if (cam->width <= 0 || cam->height <= 0 || cam->width > 65535 || cam->height > 65535) return HGS_ERR_CONFIG;
+  if (!(cam->fx > 0) || !(cam->fy > 0) || !(cam->near_plane > 0) || !(cam->near_plane < cam->far_plane))
+    return HGS_ERR_CONFIG;
+  const int b = sc->sh_bases;
+  if (b != 1 && b != 4 && b != 9 && b != 16) return HGS_ERR_CONFIG;
+  if (sc->n < 0 || sc->n >= (1ll << 31)) return HGS_ERR_CONFIG;
+  if (!(st->t_z > 0)) return HGS_ERR_CONFIG;
+  return HGS_OK;
+}
+
+#define HGS_CUDA(x)                                         \
+  do {                                                      \
+    cudaError_t e_ = (x);                                   \
+    if (e_ != cudaSuccess) return HGS_ERR_CUDA;             \
+  } while (0)
+
+#define HGS_LAUNCHED() HGS_CUDA(cudaGetLastError())
+
+int grid_for(int64_t work, int block) {
+  return (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(work, block), kMaxGrid));
+}
+
+// Stable LSD radix sort of (key, value) pairs over the listed 8-bit digit
+// passes; returns true if the result landed in the *_b buffers.
+template <typename K>
+int radix_sort(K *ka, K *kb, uint32_t *va, uint32_t *vb, int64_t n, const int *passes, int npass,
+               const uint32_t *offsets, uint32_t *lookback, uint32_t *counters, cudaStream_t s, bool *in_b) {
+  *in_b = false;
+  if (n == 0 || npass == 0) return HGS_OK;
+  const int64_t tiles = ceil_div(n, kSortTile);
+  HGS_CUDA(cudaMemsetAsync(lookback, 0, (size_t)tiles * kRadix * 4 * npass, s));
+  HGS_CUDA(cudaMemsetAsync(counters, 0, 4 * npass, s));
+  K *src = ka, *dst = kb;
+  uint32_t *vs = va, *vd = vb;
+  for (int i = 0; i < npass; ++i) {
+    const int p = passes[i];
+    k_onesweep<K><<<(unsigned)tiles, kSortThreads, 0, s>>>(src, vs, dst, vd, n, p * kRadixBits, offsets + p * kRadix,
+                                                           lookback + (size_t)i * tiles * kRadix, counters + i);
+    HGS_LAUNCHED();
+    std::swap(src, dst);
+    std::swap(vs, vd);
+    *in_b = !*in_b;
+  }
+  return HGS_OK;
+}
+
+}  // namespace
+}  // namespace hgs
+
+using namespace hgs;
+
+extern "C" {
+
+int hgs_abi_version(void) { return HGS_ABI_VERSION; }
+
+const char *hgs_status_string(int status) {
+  switch (status) {
+    case HGS_OK: return "ok";
+    case HGS_ERR_CONFIG: return "invalid configuration (camera, settings or shapes)";
+    case HGS_ERR_INVALID_PARAMETER: return "invalid primitive parameters (quaternion norm below 1e-8)";
+    case HGS_ERR_INTEGRITY: return "frame / scene / gradient mismatch";
+    case HGS_ERR_DEGENERATE_SCALE: return "squared scales sum to zero or overflow";
+    case HGS_ERR_PAIR_CAPACITY: return "frame buffer too small for the tile/splat pairs";
+    case HGS_ERR_CUDA: return "CUDA error";
+    default: return "unknown status";
+  }
+}
+
+size_t hgs_frame_bytes(int64_t n, int32_t width, int32_t height, int32_t tile_size, int64_t pair_capacity) {
+  if (tile_size != kTile || width <= 0 || height <= 0 || n < 0 || pair_capacity < 0) return 0;
+  return make_layout(n, width, height, pair_capacity).total;
+}
+
+static int64_t capacity_of(size_t frame_bytes, int64_t n, int W, int H) {
+  // largest capacity whose layout fits in frame_bytes (layout is affine in cap)
+  size_t base = make_layout(n, W, H, 0).total;
+  if (frame_bytes < base) return -1;
+  int64_t lo = 0, hi = (int64_t)((frame_bytes - base) / 16) + 1;
+  while (lo < hi) {
+    int64_t mid = (lo + hi + 1) / 2;
+    if (make_layout(n, W, H, mid).total <= frame_bytes) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+int hgs_forward(const hgs_scene *scene, const hgs_camera *camera, const hgs_settings *settings, void *frame,
+                size_t frame_bytes, const hgs_images *out, hgs_frame_info *info, void *stream) {
+  int rc = check_common(scene, camera, settings);
+  if (rc) return rc;
+  if (!out || !out->color || !out->depth || !out->transmittance || !info || !frame) return HGS_ERR_CONFIG;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int W = camera->width, H = camera->height;
+  const int64_t n = scene->n;
+  const int64_t cap = capacity_of(frame_bytes, n, W, H);
+  if (cap < 0) return HGS_ERR_PAIR_CAPACITY;
+  const Layout L = make_layout(n, W, H, cap);
+  const CamD cam = make_cam(*camera);
+  const SceneView sc = make_scene(*scene);
+  const ModD mod{settings->theta_z, settings->t_z, settings->lambda_z};
+  const int64_t n_tiles = (int64_t)cam.tiles_x * cam.tiles_y;
+  FrameState *st = at<FrameState>(frame, L.state);
+
+  memset(info, 0, sizeof(*info));
+  info->n = n; info->width = W; info->height = H; info->tiles_x = cam.tiles_x; info->tiles_y = cam.tiles_y;
+  info->n_tiles = n_tiles; info->pair_capacity = cap; info->sh_bases = scene->sh_bases; info->flags = settings->flags;
+
+  HGS_CUDA(cudaMemsetAsync(frame, 0, L.small_end, s));
+  // 1. depth keys + digit histograms
+  uint32_t *vals_sorted = at<uint32_t>(frame, L.vals_a);
+  int64_t m = 0;
+  if (n > 0) {
+    k_depth_keys<<<grid_for(n, 256), 256, 0, s>>>(sc, cam, at<unsigned long long>(frame, L.keys_a),
+                                                  at<uint32_t>(frame, L.vals_a), at<uint32_t>(frame, L.hist_d), st);
+    HGS_LAUNCHED();
+    k_radix_offsets<<<8, kRadix, 0, s>>>(at<uint32_t>(frame, L.hist_d), at<uint32_t>(frame, L.off_d));
+    HGS_LAUNCHED();
+    uint32_t hist[8 * kRadix];
+    FrameState hst;
+    HGS_CUDA(cudaMemcpyAsync(hist, at<uint32_t>(frame, L.hist_d), sizeof(hist), cudaMemcpyDeviceToHost, s));
+    HGS_CUDA(cudaMemcpyAsync(&hst, st, sizeof(hst), cudaMemcpyDeviceToHost, s));
+    HGS_CUDA(cudaStreamSynchronize(s));
+    if (hst.status) return (int)hst.status;
+    m = hst.m_count;
+    // 2. depth sort over the digit passes that are not constant
+    int passes[8], np = 0;
+    for (int p = 0; p < 8; ++p) {
+      bool trivial = false;
+      for (int d = 0; d < kRadix; ++d)
+        if (hist[p * kRadix + d] == (uint32_t)n) trivial = true;
+      if (!trivial) passes[np++] = p;
+    }
+    bool in_b;
+    rc = radix_sort<unsigned long long>(at<unsigned long long>(frame, L.keys_a), at<unsigned long long>(frame, L.keys_b),
+                                        at<uint32_t>(frame, L.vals_a), at<uint32_t>(frame, L.vals_b), n, passes, np,
+                                        at<uint32_t>(frame, L.off_d), at<uint32_t>(frame, L.lb_sort),
+                                        st->tile_counters + 1, s, &in_b);
+    if (rc) return rc;
+    vals_sorted = at<uint32_t>(frame, in_b ? L.vals_b : L.vals_a);
+  }
+  info->m = m;
+  // 3. float64 preprocess per rank + pair-offset scan
+  int64_t K = 0;
+  if (m > 0) {
+    HGS_CUDA(cudaMemsetAsync(at<char>(frame, L.lb_scan), 0, L.lb_scan_bytes, s));
+    k_preprocess<<<(unsigned)ceil_div(m, kScanThreads), kScanThreads, 0, s>>>(
+        sc, cam, mod, vals_sorted, m, at<SplatRec>(frame, L.recs), at<unsigned long long>(frame, L.pair_off),
+        at<unsigned long long>(frame, L.lb_scan), st);
+    HGS_LAUNCHED();
+    unsigned long long kt;
+    HGS_CUDA(cudaMemcpyAsync(&kt, &st->k_total, 8, cudaMemcpyDeviceToHost, s));
+    HGS_CUDA(cudaStreamSynchronize(s));
+    K = (int64_t)kt;
+  }
+  info->k = K;
+  if (K > cap || K >= (1ll << 32)) return HGS_ERR_PAIR_CAPACITY;
+  // 4. duplicate + tile sort + ranges
+  const uint32_t *tile_vals = at<uint32_t>(frame, L.pv_a);
+  const uint32_t *tile_keys = at<uint32_t>(frame, L.pk_a);
+  if (K > 0) {
+    const int nd = n_tiles > kRadix ? 2 : 1;
+    k_duplicate<<<grid_for(m, 256), 256, 0, s>>>(at<SplatRec>(frame, L.recs), at<unsigned long long>(frame, L.pair_off),
+                                                 m, cam.tiles_x, at<uint32_t>(frame, L.pk_a), at<uint32_t>(frame, L.pv_a),
+                                                 nd, at<uint32_t>(frame, L.hist_p));
+    HGS_LAUNCHED();
+    k_radix_offsets<<<nd, kRadix, 0, s>>>(at<uint32_t>(frame, L.hist_p), at<uint32_t>(frame, L.off_p));
+    HGS_LAUNCHED();
+    int passes[2] = {0, 1};
+    bool in_b;
+    rc = radix_sort<uint32_t>(at<uint32_t>(frame, L.pk_a), at<uint32_t>(frame, L.pk_b), at<uint32_t>(frame, L.pv_a),
+                              at<uint32_t>(frame, L.pv_b), K, passes, nd, at<uint32_t>(frame, L.off_p),
+                              at<uint32_t>(frame, L.lb_sort), st->tile_counters + 12, s, &in_b);
+    if (rc) return rc;
+    tile_vals = at<uint32_t>(frame, in_b ? L.pv_b : L.pv_a);
+    tile_keys = at<uint32_t>(frame, in_b ? L.pk_b : L.pk_a);
+    info->internal[0] = in_b ? 1u : 0u;
+  }
+  k_tile_ranges<<<(unsigned)std::max<int64_t>(1, ceil_div(std::max<int64_t>(K, n_tiles + 1), 256)), 256, 0, s>>>(
+      tile_keys, K, n_tiles, at<uint32_t>(frame, L.tile_off));
+  HGS_LAUNCHED();
+  // 5. composite
+  CompositeArgs a;
+  a.recs = at<SplatRec>(frame, L.recs);
+  a.tile_off = at<uint32_t>(frame, L.tile_off);
+  a.tile_vals = tile_vals;
+  a.m = m;
+  a.tiles_x = cam.tiles_x; a.width = W; a.height = H;
+  a.flags = settings->flags;
+  for (int c = 0; c < 3; ++c) a.bg[c] = settings->background[c];
+  a.color = out->color; a.depth = out->depth; a.trans = out->transmittance; a.alpha = out->alpha;
+  a.normal = out->normal;
+  a.pix_T = at<float>(frame, L.pix_T);
+  a.pix_last = at<uint32_t>(frame, L.pix_last);
+  a.pix_count = at<uint32_t>(frame, L.pix_count);
+  a.sc = sc; a.cam = cam; a.mod = mod; a.st = st;
+  if (settings->flags & HGS_FLAG_NAIVE)
+    k_composite_fwd<true><<<(unsigned)n_tiles, kBlock, 0, s>>>(a);
+  else
+    k_composite_fwd<false><<<(unsigned)n_tiles, kBlock, 0, s>>>(a);
+  HGS_LAUNCHED();
+  return HGS_OK;
+}
+
+static CompositeArgs composite_args_for(const hgs_scene *scene, const hgs_camera *camera,
+                                        const hgs_settings *settings, const void *frame, const hgs_frame_info *info) {
+  const Layout L = make_layout(info->n, info->width, info->height, info->pair_capacity);
+  void *fr = const_cast<void *>(frame);
+  CompositeArgs a;
+  memset(&a, 0, sizeof(a));
+  a.recs = at<SplatRec>(fr, L.recs);
+  a.tile_off = at<uint32_t>(fr, L.tile_off);
+  a.tile_vals = at<uint32_t>(fr, info->internal[0] ? L.pv_b : L.pv_a);
+  a.m = info->m;
+  a.tiles_x = info->tiles_x; a.width = info->width; a.height = info->height;
+  a.flags = info->flags;
+  for (int c = 0; c < 3; ++c) a.bg[c] = settings->background[c];
+  a.pix_T = at<float>(fr, L.pix_T);
+  a.pix_last = at<uint32_t>(fr, L.pix_last);
+  a.pix_count = at<uint32_t>(fr, L.pix_count);
+  a.sc = make_scene(*scene);
+  a.cam = make_cam(*camera);
+  a.mod = ModD{settings->theta_z, settings->t_z, settings->lambda_z};
+  a.st = at<FrameState>(fr, L.state);
+  return a;
+}
+
+static int check_frame(const hgs_scene *scene, const hgs_camera *camera, const hgs_frame_info *info) {
+  if (!info) return HGS_ERR_INTEGRITY;
+  if (info->n != scene->n || info->width != camera->width || info->height != camera->height ||
+      info->sh_bases != scene->sh_bases)
+    return HGS_ERR_INTEGRITY;
+  return HGS_OK;
+}
+
+size_t hgs_backward_scratch_bytes(int64_t n, int32_t kg) {
+  if (n < 0 || kg < 1) return 0;
+  const int64_t kc = std::min<int32_t>(kg, 4);
+  const int64_t nn = std::max<int64_t>(n, 1);
+  return (size_t)(((nn * kc * 16 * 4 + 255) & ~255ll) + ((nn * kc * 4 * 4 + 255) & ~255ll) + ((nn + 255) & ~255ll));
+}
+
+}  // extern "C"
+
+template <int KG>
+static void launch_bwd(const BwdArgs &b, int64_t n_tiles, bool ext, cudaStream_t s) {
+  if (ext)
+    k_composite_bwd<KG, true><<<(unsigned)n_tiles, kBlock, 0, s>>>(b);
+  else
+    k_composite_bwd<KG, false><<<(unsigned)n_tiles, kBlock, 0, s>>>(b);
+}
+
+extern "C" {
+
+int hgs_backward(const hgs_scene *scene, const hgs_camera *camera, const hgs_settings *settings, const void *frame,
+                 const hgs_frame_info *info, int32_t kg, const float *pixel_grads, const float *depth_grads,
+                 const float *normal_grads, const float *alpha_grads, void *scratch, size_t scratch_bytes,
+                 float *grads, uint8_t *touched, void *stream) {
+  int rc = check_common(scene, camera, settings);
+  if (rc) return rc;
+  rc = check_frame(scene, camera, info);
+  if (rc) return rc;
+  if (kg < 1 || !pixel_grads || !grads || !touched) return HGS_ERR_CONFIG;
+  if (scratch_bytes < hgs_backward_scratch_bytes(scene->n, kg)) return HGS_ERR_CONFIG;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int64_t n = scene->n, m = info->m;
+  const int64_t P = 11 + 3 * (int64_t)scene->sh_bases;
+  const int64_t HW = (int64_t)info->width * info->height;
+  const bool ext = depth_grads || normal_grads || alpha_grads;
+  const int kc_max = std::min<int32_t>(kg, 4);
+  const int64_t nn = std::max<int64_t>(n, 1);
+  float *acc = static_cast<float *>(scratch);
+  float *acc_ext = reinterpret_cast<float *>(static_cast<char *>(scratch) + ((nn * kc_max * 16 * 4 + 255) & ~255ll));
+  uint8_t *touched_rank = reinterpret_cast<uint8_t *>(reinterpret_cast<char *>(acc_ext) +
+                                                      ((nn * kc_max * 4 * 4 + 255) & ~255ll));
+  HGS_CUDA(cudaMemsetAsync(touched, 0, (size_t)nn, s));
+  BwdArgs b;
+  b.c = composite_args_for(scene, camera, settings, frame, info);
+  const ChainArgs c0{b.c.sc, b.c.cam, b.c.mod, acc, ext ? acc_ext : nullptr, 0, nullptr};
+  for (int k0 = 0; k0 < kg; k0 += 4) {
+    const int kc = std::min(4, kg - k0);
+    HGS_CUDA(cudaMemsetAsync(acc, 0, (size_t)nn * kc * 16 * 4, s));
+    if (ext) HGS_CUDA(cudaMemsetAsync(acc_ext, 0, (size_t)nn * kc * 4 * 4, s));
+    HGS_CUDA(cudaMemsetAsync(touched_rank, 0, (size_t)std::max<int64_t>(m, 1), s));
+    b.pix_grad = pixel_grads + (int64_t)k0 * HW * 3;
+    b.depth_grad = depth_grads ? depth_grads + (int64_t)k0 * HW : nullptr;
+    b.normal_grad = normal_grads ? normal_grads + (int64_t)k0 * HW * 3 : nullptr;
+    b.alpha_grad = alpha_grads ? alpha_grads + (int64_t)k0 * HW : nullptr;
+    b.acc = acc;
+    b.acc_ext = ext ? acc_ext : nullptr;
+    b.touched_rank = touched_rank;
+    if (m > 0) {
+      switch (kc) {
+        case 1: launch_bwd<1>(b, info->n_tiles, ext, s); break;
+        case 2: launch_bwd<2>(b, info->n_tiles, ext, s); break;
+        case 3: launch_bwd<3>(b, info->n_tiles, ext, s); break;
+        default: launch_bwd<4>(b, info->n_tiles, ext, s); break;
+      }
+      HGS_LAUNCHED();
+      if (k0 == 0) {
+        k_touched_scatter<<<grid_for(m, 256), 256, 0, s>>>(b.c.recs, touched_rank, m, touched);
+        HGS_LAUNCHED();
+      }
+    }
+    ChainArgs c = c0;
+    c.kg = kc;
+    c.grads = grads + (int64_t)k0 * n * P;
+    if (n > 0) {
+      k_chain_rule<<<grid_for(n, 128), 128, 0, s>>>(c);
+      HGS_LAUNCHED();
+    }
+  }
+  return HGS_OK;
+}
+
+int hgs_exchange(int64_t n, float *log_scale, float *rotation, uint8_t *type_spec, double theta_e, float *eranks,
+                 void *scratch, hgs_exchange_report *report, void *stream) {
+  if (n < 0 || !report || !scratch || !(theta_e > 1.0 && theta_e < 3.0)) return HGS_ERR_CONFIG;
+  memset(report, 0, sizeof(*report));
+  if (n == 0) return HGS_OK;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  ExchangeState *st = static_cast<ExchangeState *>(scratch);
+  HGS_CUDA(cudaMemsetAsync(st, 0, sizeof(ExchangeState), s));
+  k_exchange_scan<<<grid_for(n, 256), 256, 0, s>>>(n, log_scale, type_spec, theta_e, eranks, st);
+  HGS_LAUNCHED();
+  ExchangeState h;
+  HGS_CUDA(cudaMemcpyAsync(&h, st, sizeof(h), cudaMemcpyDeviceToHost, s));
+  HGS_CUDA(cudaStreamSynchronize(s));
+  if (h.counts[3]) return HGS_ERR_DEGENERATE_SCALE;
+  k_exchange_apply<<<grid_for(n, 256), 256, 0, s>>>(n, log_scale, rotation, type_spec, theta_e);
+  HGS_LAUNCHED();
+  report->n_3d_to_2d = (int64_t)h.counts[0];
+  report->n_2d_to_3d = (int64_t)h.counts[1];
+  report->n_3d = (int64_t)h.counts[2] - (int64_t)h.counts[0] + (int64_t)h.counts[1];
+  report->n_2d = n - report->n_3d;
+  for (int b = 0; b < 20; ++b) report->erank_hist[b] = (int64_t)h.hist[b];
+  return HGS_OK;
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------- export
+
+namespace hgs {
+
+__global__ void k_export_frame(SceneView sc, CamD cam, ModD mod, const SplatRec *__restrict__ recs, int64_t m,
+                               hgs_frame_export o) {
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < m; r += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t i = __float_as_uint(recs[r].r4.w) & 0x7fffffffu;
+    ProjD p;
+    project_d(sc, i, cam, mod, p);
+    bbox_d(p, cam.width, cam.height);
+    if (o.idx) o.idx[r] = (int32_t)i;
+    if (o.typ) o.typ[r] = (uint8_t)p.typ;
+    if (o.depth) o.depth[r] = p.t[2];
+    if (o.center2d) { o.center2d[2 * r] = p.ctr[0]; o.center2d[2 * r + 1] = p.ctr[1]; }
+    for (int k = 0; k < 3; ++k) {
+      if (o.cov2d) o.cov2d[3 * r + k] = p.cov[k];
+      if (o.conic) o.conic[3 * r + k] = p.conic[k];
+      if (o.color) o.color[3 * r + k] = p.color[k];
+      if (o.normal) o.normal[3 * r + k] = p.normal[k];
+    }
+    if (o.mrow)
+      for (int k = 0; k < 12; ++k) o.mrow[12 * r + k] = p.mrow[k];
+    if (o.alpha_eff) o.alpha_eff[r] = p.alpha_eff;
+    if (o.radius) o.radius[r] = p.radius;
+    if (o.bbox)
+      for (int k = 0; k < 4; ++k) o.bbox[4 * r + k] = p.bbox[k];
+  }
+}
+
+__global__ void k_export_u32_to_i64(const uint32_t *__restrict__ src, int64_t *__restrict__ dst, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = src[i];
+}
+
+// Blend log (render.py:30-51): one thread per pixel re-walks its tile list
+// with the forward's exact decisions and writes (position, alpha, u, v).
+__global__ void k_blend_log(CompositeArgs a, const int64_t *__restrict__ offsets, int32_t *__restrict__ pos,
+                            float *__restrict__ alpha, float *__restrict__ u, float *__restrict__ v) {
+  const int64_t HW = (int64_t)a.width * a.height;
+  const bool naive = a.flags & HGS_FLAG_NAIVE;
+  for (int64_t pix = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; pix < HW; pix += (int64_t)gridDim.x * blockDim.x) {
+    const int ix = (int)(pix % a.width), iy = (int)(pix / a.width);
+    const int tile = (iy / kTile) * a.tiles_x + ix / kTile;
+    const int64_t lo = naive ? 0 : a.tile_off[tile];
+    const int64_t end = lo + a.pix_last[pix];
+    int64_t o = offsets[pix];
+    for (int64_t j = lo; j < end; ++j) {
+      const uint32_t rk = naive ? (uint32_t)j : a.tile_vals[j];
+      const SplatRec r = a.recs[rk];
+      if (!naive) {
+        const int4 q = r.r5;
+        const int x0 = q.x & 0xffff, y0 = (int)((uint32_t)q.x >> 16);
+        const int x1 = q.y & 0xffff, y1 = (int)((uint32_t)q.y >> 16);
+        if (ix < x0 || ix > x1 || iy < y0 || iy > y1) continue;
+      }
+      PairEval p;
+      if (!eval_pair<false>(r, ix, iy, a, p)) continue;
+      pos[o] = (int32_t)rk;
+      alpha[o] = p.at;
+      u[o] = p.u;
+      v[o] = p.v;
+      ++o;
+    }
+  }
+}
+
+}  // namespace hgs
+
+extern "C" {
+
+int hgs_frame_export_arrays(const hgs_scene *scene, const hgs_camera *camera, const hgs_settings *settings,
+                            const void *frame, const hgs_frame_info *info, const hgs_frame_export *out, void *stream) {
+  int rc = check_common(scene, camera, settings);
+  if (rc) return rc;
+  rc = check_frame(scene, camera, info);
+  if (rc) return rc;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const CompositeArgs a = composite_args_for(scene, camera, settings, frame, info);
+  if (info->m > 0) {
+    k_export_frame<<<grid_for(info->m, 128), 128, 0, s>>>(a.sc, a.cam, a.mod, a.recs, info->m, *out);
+    HGS_LAUNCHED();
+  }
+  if (out->tile_offsets) {
+    k_export_u32_to_i64<<<grid_for(info->n_tiles + 1, 256), 256, 0, s>>>(a.tile_off, out->tile_offsets,
+                                                                        info->n_tiles + 1);
+    HGS_LAUNCHED();
+  }
+  if (out->tile_ids && info->k > 0)
+    HGS_CUDA(cudaMemcpyAsync(out->tile_ids, a.tile_vals, (size_t)info->k * 4, cudaMemcpyDeviceToDevice, s));
+  if (out->pixel_count)
+    HGS_CUDA(cudaMemcpyAsync(out->pixel_count, a.pix_count, (size_t)info->width * info->height * 4,
+                             cudaMemcpyDeviceToDevice, s));
+  return HGS_OK;
+}
+
+int hgs_blend_log(const hgs_scene *scene, const hgs_camera *camera, const hgs_settings *settings, const void *frame,
+                  const hgs_frame_info *info, const int64_t *offsets, int32_t *position, float *alpha, float *u,
+                  float *v, void *stream) {
+  int rc = check_common(scene, camera, settings);
+  if (rc) return rc;
+  rc = check_frame(scene, camera, info);
+  if (rc) return rc;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const CompositeArgs a = composite_args_for(scene, camera, settings, frame, info);
+  const int64_t HW = (int64_t)info->width * info->height;
+  k_blend_log<<<grid_for(HW, 128), 128, 0, s>>>(a, offsets, position, alpha, u, v);
+  HGS_LAUNCHED();
+  return HGS_OK;
+}
+
+}  // extern "C"

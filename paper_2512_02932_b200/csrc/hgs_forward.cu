@@ -1,0 +1,263 @@
+// hgs_forward.cu -- forward kernels: depth keys, float64 preprocess + pair
+// scan, tile duplication, tile ranges and the per-tile front-to-back
+// compositor.  Semantics: raster/project.py:169-379 and
+// raster/_blend_py.py:55-123 (paths relative to the reference package).
+#include "hgs_kernels.cuh"
+
+namespace hgs {
+
+// ------------------------------------------------------------ depth keys
+// Per Gaussian: view depth in float64, near cull (project.py:181-185),
+// singular-conic validity for 3D (project.py:225), |q| check (rotation.py:
+// 19-20).  key = bits(z) for kept splats, ~0 otherwise (they sort last and
+// are not counted in M).  Also accumulates the 8 digit histograms.
+__global__ void __launch_bounds__(256) k_depth_keys(SceneView sc, CamD cam, unsigned long long *__restrict__ keys,
+                                                    uint32_t *__restrict__ vals, uint32_t *__restrict__ hist,
+                                                    FrameState *__restrict__ st) {
+  __shared__ uint32_t sh[8 * kRadix];
+  __shared__ uint32_t s_m;
+  for (int i = threadIdx.x; i < 8 * kRadix; i += blockDim.x) sh[i] = 0;
+  if (threadIdx.x == 0) s_m = 0;
+  __syncthreads();
+  uint32_t bad = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < sc.n; i += (int64_t)gridDim.x * blockDim.x) {
+    double p[3], t[3];
+    load_center_d(sc, i, p);
+    t_cam_d(cam, p, t);
+    bool keep = t[2] > cam.near_plane;
+    if (keep) {
+      double R[9];
+      bool qok = quat_to_matrix_d(sc.rotation[4 * i], sc.rotation[4 * i + 1], sc.rotation[4 * i + 2],
+                                  sc.rotation[4 * i + 3], R);
+      if (!qok) {
+        bad = 1;
+        keep = false;
+      } else if (sc.type_spec[i] == 1) {
+        double s[3] = {exp((double)sc.log_scale[3 * i]), exp((double)sc.log_scale[3 * i + 1]),
+                       exp((double)sc.log_scale[3 * i + 2])};
+        double a, b, c;
+        cov2d_3d(cam, t, R, s, a, b, c);
+        keep = (a * c - b * b) > 1e-18;
+      }
+    }
+    unsigned long long k = keep ? (unsigned long long)__double_as_longlong(t[2]) : ~0ull;
+    keys[i] = k;
+    vals[i] = (uint32_t)i;
+    if (keep) atomicAdd(&s_m, 1u);
+#pragma unroll
+    for (int pss = 0; pss < 8; ++pss) atomicAdd(&sh[pss * kRadix + digit_of(k, pss * 8)], 1u);
+  }
+  if (bad) atomicOr(&st->status, (uint32_t)HGS_ERR_INVALID_PARAMETER);
+  __syncthreads();
+  for (int i = threadIdx.x; i < 8 * kRadix; i += blockDim.x)
+    if (sh[i]) atomicAdd(&hist[i], sh[i]);
+  if (threadIdx.x == 0 && s_m) atomicAdd(&st->m_count, s_m);
+}
+
+// ---------------------------------------------------- preprocess + scan
+__device__ __forceinline__ uint32_t tile_count_of(const int *bb) {
+  if (bb[2] < bb[0]) return 0u;
+  uint32_t tx = (uint32_t)(bb[2] / kTile - bb[0] / kTile + 1);
+  uint32_t ty = (uint32_t)(bb[3] / kTile - bb[1] / kTile + 1);
+  return tx * ty;
+}
+
+__device__ __forceinline__ void write_record(const ProjD &o, uint32_t idx, SplatRec *__restrict__ rec) {
+  // anchor pixel = floor(centre), kept within +-2^30 so (ix - ax) stays exact
+  double axd = floor(o.ctr[0]), ayd = floor(o.ctr[1]);
+  axd = fmin(fmax(axd, -1073741824.0), 1073741824.0);
+  ayd = fmin(fmax(ayd, -1073741824.0), 1073741824.0);
+  if (isnan(axd)) axd = 0.0;
+  if (isnan(ayd)) ayd = 0.0;
+  SplatRec r;
+  r.r0 = make_float4((float)(o.ctr[0] - axd), (float)(o.ctr[1] - ayd), (float)o.t[2], (float)log2(o.alpha_eff));
+  if (o.typ == 1) {
+    // relative float32 error amplification of the conic quadratic form
+    r.r1 = make_float4((float)o.conic[0], (float)o.conic[1], (float)o.conic[2], 0.f);
+    r.r2 = make_float4(0.f, 0.f, 0.f, 0.f);
+    r.r3 = make_float4(0.f, (float)o.color[0], (float)o.color[1], (float)o.color[2]);
+  } else {
+    const double *m = o.mrow;  // rows x(0..3), y(4..7), w(8..11)
+    double m00 = m[0] - axd * m[8], m01 = m[1] - axd * m[9], m03 = m[3] - axd * m[11];
+    double m10 = m[4] - ayd * m[8], m11 = m[5] - ayd * m[9], m13 = m[7] - ayd * m[11];
+    r.r1 = make_float4((float)m00, (float)m01, (float)m03, (float)m10);
+    r.r2 = make_float4((float)m11, (float)m13, (float)m[8], (float)m[9]);
+    r.r3 = make_float4((float)m[11], (float)o.color[0], (float)o.color[1], (float)o.color[2]);
+  }
+  uint32_t tag = idx | ((uint32_t)(o.typ == 1) << 31);
+  r.r4 = make_float4((float)o.normal[0], (float)o.normal[1], (float)o.normal[2], __uint_as_float(tag));
+  int x0 = o.bbox[0], y0 = o.bbox[1], x1 = o.bbox[2], y1 = o.bbox[3];
+  if (x1 < x0) {  // off screen: empty box, never binned
+    x0 = 1; x1 = 0; y0 = 1; y1 = 0;
+  }
+  r.r5 = make_int4((int)((uint32_t)x0 | ((uint32_t)y0 << 16)), (int)((uint32_t)x1 | ((uint32_t)y1 << 16)), (int)axd,
+                   (int)ayd);
+  *rec = r;
+}
+
+// One thread per depth rank r < M: float64 projection of Gaussian
+// sorted_idx[r], record write, tile count, exclusive scan -> pair offsets.
+__global__ void __launch_bounds__(kScanThreads) k_preprocess(SceneView sc, CamD cam, ModD mod,
+                                                             const uint32_t *__restrict__ sorted_idx, int64_t m,
+                                                             SplatRec *__restrict__ recs,
+                                                             unsigned long long *__restrict__ pair_off,
+                                                             unsigned long long *__restrict__ scan_lb,
+                                                             FrameState *__restrict__ st) {
+  __shared__ uint32_t s_tile;
+  __shared__ unsigned long long s_warp[32];
+  __shared__ unsigned long long s_excl;
+  if (threadIdx.x == 0) s_tile = atomicAdd(&st->tile_counters[0], 1u);
+  __syncthreads();
+  const uint32_t tile = s_tile;
+  const int64_t base = (int64_t)tile * kScanThreads;
+  const int64_t r = base + threadIdx.x;
+  uint32_t cnt = 0;
+  if (r < m) {
+    uint32_t i = sorted_idx[r];
+    ProjD o;
+    project_d(sc, i, cam, mod, o);
+    bbox_d(o, cam.width, cam.height);
+    write_record(o, i, recs + r);
+    cnt = tile_count_of(o.bbox);
+  }
+  unsigned long long total;
+  unsigned long long ex = block_exclusive_scan_u64(cnt, s_warp, total);
+  if (threadIdx.x == 0) s_excl = scan_lookback(scan_lb, tile, total);
+  __syncthreads();
+  if (r < m) pair_off[r] = s_excl + ex;
+  if (base + kScanThreads >= m && threadIdx.x == 0) st->k_total = s_excl + total;
+}
+
+// ------------------------------------------------------------ duplicate
+// Emit (tile id, rank) pairs in rank order at the scanned offsets and build
+// the tile-id digit histograms for the pair sort.
+__global__ void __launch_bounds__(256) k_duplicate(const SplatRec *__restrict__ recs,
+                                                   const unsigned long long *__restrict__ pair_off, int64_t m,
+                                                   int tiles_x, uint32_t *__restrict__ pkeys,
+                                                   uint32_t *__restrict__ pvals, int n_digits,
+                                                   uint32_t *__restrict__ hist) {
+  __shared__ uint32_t sh[2 * kRadix];
+  for (int i = threadIdx.x; i < 2 * kRadix; i += blockDim.x) sh[i] = 0;
+  __syncthreads();
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < m; r += (int64_t)gridDim.x * blockDim.x) {
+    int4 q = recs[r].r5;
+    int x0 = q.x & 0xffff, y0 = (int)((uint32_t)q.x >> 16), x1 = q.y & 0xffff, y1 = (int)((uint32_t)q.y >> 16);
+    if (x1 < x0) continue;
+    unsigned long long o = pair_off[r];
+    int tx0 = x0 / kTile, tx1 = x1 / kTile, ty0 = y0 / kTile, ty1 = y1 / kTile;
+    for (int ty = ty0; ty <= ty1; ++ty)
+      for (int tx = tx0; tx <= tx1; ++tx) {
+        uint32_t t = (uint32_t)(ty * tiles_x + tx);
+        pkeys[o] = t;
+        pvals[o] = (uint32_t)r;
+        ++o;
+        atomicAdd(&sh[t & 0xff], 1u);
+        if (n_digits > 1) atomicAdd(&sh[kRadix + ((t >> 8) & 0xff)], 1u);
+      }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < n_digits * kRadix; i += blockDim.x)
+    if (sh[i]) atomicAdd(&hist[i], sh[i]);
+}
+
+// tile_offsets (n_tiles + 1) from the tile-sorted keys (project.py:344-345).
+__global__ void k_tile_ranges(const uint32_t *__restrict__ skeys, int64_t k, int64_t n_tiles,
+                              uint32_t *__restrict__ tile_off) {
+  int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k == 0) {
+    for (int64_t t = p; t <= n_tiles; t += (int64_t)gridDim.x * blockDim.x) tile_off[t] = 0;
+    return;
+  }
+  if (p >= k) return;
+  int64_t t = skeys[p];
+  int64_t prev = p ? (int64_t)skeys[p - 1] : -1;
+  for (int64_t tt = prev + 1; tt <= t; ++tt) tile_off[tt] = (uint32_t)p;
+  if (p == k - 1)
+    for (int64_t tt = t + 1; tt <= n_tiles; ++tt) tile_off[tt] = (uint32_t)k;
+}
+
+// -------------------------------------------------------------- composite
+
+// Per-tile front-to-back compositor (_blend_py.py:76-117).  One CTA per
+// 16 x 16 tile, one thread per pixel; warps own 8 x 4 pixel blocks.  Splat
+// records are staged in shared memory in batches of 256; every lane of a
+// warp walks the same splat so the 2D / 3D branch is warp-uniform.
+template <bool NAIVE>
+__global__ void __launch_bounds__(kBlock) k_composite_fwd(CompositeArgs a) {
+  __shared__ SplatRec s_rec[kBlock];
+  const int tile = blockIdx.x;
+  const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ix = tx * kTile + (warp & 1) * 8 + (lane & 7);
+  const int iy = ty * kTile + (warp >> 1) * 4 + (lane >> 3);
+  const bool inside = ix < a.width && iy < a.height;
+  int64_t lo, hi;
+  if (NAIVE) {
+    lo = 0;
+    hi = a.m;
+  } else {
+    lo = a.tile_off[tile];
+    hi = a.tile_off[tile + 1];
+  }
+  float T = 1.f, cr = 0.f, cg = 0.f, cb = 0.f, dep = 0.f, n0 = 0.f, n1 = 0.f, n2 = 0.f;
+  uint32_t cnt = 0, last = 0;
+  bool done = !inside;
+  const FwdGuard guard(a, ix, iy);
+  for (int64_t base = lo; base < hi; base += kBlock) {
+    __syncthreads();
+    int64_t j = base + threadIdx.x;
+    if (j < hi) {
+      uint32_t rk = NAIVE ? (uint32_t)j : a.tile_vals[j];
+      s_rec[threadIdx.x] = a.recs[rk];
+    }
+    __syncthreads();
+    const int nb = (int)(hi - base < kBlock ? hi - base : kBlock);
+    for (int e = 0; e < nb && !done; ++e) {
+      const SplatRec &r = s_rec[e];
+      const int4 q = r.r5;
+      if (!NAIVE) {
+        const int x0 = q.x & 0xffff, y0 = (int)((uint32_t)q.x >> 16);
+        const int x1 = q.y & 0xffff, y1 = (int)((uint32_t)q.y >> 16);
+        if (ix < x0 || ix > x1 || iy < y0 || iy > y1) continue;
+      }
+      float at;
+      if (!eval_alpha(r, ix, iy, guard, at)) continue;
+      const float w = at * T;
+      const float4 c3 = r.r3, c4 = r.r4, c0 = r.r0;
+      cr = fmaf(w, c3.y, cr);
+      cg = fmaf(w, c3.z, cg);
+      cb = fmaf(w, c3.w, cb);
+      dep = fmaf(w, c0.z, dep);
+      n0 = fmaf(w, c4.x, n0);
+      n1 = fmaf(w, c4.y, n1);
+      n2 = fmaf(w, c4.z, n2);
+      ++cnt;
+      last = (uint32_t)(base + e - lo) + 1u;
+      const float Tn = T * (1.f - at);
+      if (guard.early_stop(Tn, T, lo, base + e)) done = true;
+      T = Tn;
+    }
+    if (__syncthreads_count(done) == kBlock) break;
+  }
+  if (!inside) return;
+  const int64_t pix = (int64_t)iy * a.width + ix;
+  a.color[3 * pix + 0] = cr + a.bg[0] * T;
+  a.color[3 * pix + 1] = cg + a.bg[1] * T;
+  a.color[3 * pix + 2] = cb + a.bg[2] * T;
+  a.depth[pix] = dep;
+  a.trans[pix] = T;
+  if (a.alpha) a.alpha[pix] = 1.f - T;
+  if (a.normal) {
+    a.normal[3 * pix + 0] = n0;
+    a.normal[3 * pix + 1] = n1;
+    a.normal[3 * pix + 2] = n2;
+  }
+  a.pix_T[pix] = T;
+  a.pix_last[pix] = last;
+  a.pix_count[pix] = cnt;
+}
+
+template __global__ void k_composite_fwd<false>(CompositeArgs);
+template __global__ void k_composite_fwd<true>(CompositeArgs);
+
+}  // namespace hgs

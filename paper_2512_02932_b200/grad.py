@@ -1,0 +1,181 @@
+"""Backward API -- drop-in for the reference's ``hybridsplat.grad``
+(grad/backward.py:37-181, grad/bundle.py:11-88).
+
+``backward(scene, camera, output, pixel_grad)`` replays the GPU frame of
+``output`` back to front (k_composite_bwd) and runs the float64 per-Gaussian
+chain rule (k_chain_rule).  Like the reference it returns one ParamGrads (or a
+list of KG) plus the per-Gaussian ``touched`` mask.  Optional extension
+gradients: ``depth_grad`` (H,W), ``normal_grad`` (H,W,3), ``alpha_grad``
+(H,W), each with the same leading KG dimension as ``pixel_grad`` if stacked.
+"""
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .core import DeviceGaussians, GaussianSet
+from .errors import IntegrityError
+
+__all__ = ["backward", "ParamGrads", "GradientBundle", "param_labels"]
+
+
+@dataclass
+class ParamGrads:
+    """Gradients for every trainable array of a scene (grad/bundle.py:11-63).
+    Arrays are numpy float64 for host scenes, CUDA float32 views of one flat
+    buffer for device scenes."""
+    center: object
+    log_scale: object
+    rotation: object
+    opacity_logit: object
+    sh_coeffs: object
+
+    @classmethod
+    def zeros_like(cls, scene):
+        if isinstance(scene, DeviceGaussians):
+            import torch
+            return cls(*(torch.zeros_like(getattr(scene, f)) for f in
+                         ("center", "log_scale", "rotation", "opacity_logit", "sh_coeffs")))
+        return cls(np.zeros_like(scene.center), np.zeros_like(scene.log_scale),
+                   np.zeros_like(scene.rotation), np.zeros_like(scene.opacity_logit),
+                   np.zeros_like(scene.sh_coeffs))
+
+    @property
+    def count(self):
+        return self.center.shape[0]
+
+    def flat(self):
+        """(N, P) rows: center(3), log_scale(3), rotation(4), opacity(1), sh(3B)."""
+        n = self.count
+        parts = [self.center.reshape(n, -1), self.log_scale.reshape(n, -1),
+                 self.rotation.reshape(n, -1), self.opacity_logit.reshape(n, 1),
+                 self.sh_coeffs.reshape(n, -1)]
+        if isinstance(self.center, np.ndarray):
+            return np.concatenate(parts, axis=1)
+        import torch
+        return torch.cat(parts, dim=1)
+
+    @classmethod
+    def from_flat(cls, flat, template):
+        n = template.count
+        b = template.sh_coeffs.shape[2]
+        if tuple(flat.shape) != (n, 11 + 3 * b):
+            raise IntegrityError("flat gradient shape %s does not match scene" % (flat.shape,))
+        return cls(flat[:, 0:3], flat[:, 3:6], flat[:, 6:10], flat[:, 10],
+                   flat[:, 11:].reshape(n, 3, b))
+
+    def assert_finite(self):
+        for name in ("center", "log_scale", "rotation", "opacity_logit", "sh_coeffs"):
+            a = getattr(self, name)
+            ok = np.all(np.isfinite(a)) if isinstance(a, np.ndarray) else bool(a.isfinite().all())
+            if not ok:
+                raise IntegrityError("non-finite gradient in %s" % name)
+
+
+@dataclass
+class GradientBundle:
+    """grad/bundle.py:66-76"""
+    g_color: ParamGrads
+    g_low: ParamGrads
+    g_high: ParamGrads
+
+
+def param_labels(scene):
+    b = scene.sh_coeffs.shape[2]
+    per = (["center.%d" % i for i in range(3)] + ["log_scale.%d" % i for i in range(3)]
+           + ["rotation.%d" % i for i in range(4)] + ["opacity_logit"]
+           + ["sh.%d.%d" % (c, k) for c in range(3) for k in range(b)])
+    return [("g%d.%s" % (g, p)) for g in range(scene.count) for p in per]
+
+
+def _views(flat_block, n, B):
+    """ParamGrads views of one field-major (n*P,) block (include/hgs.h)."""
+    o = 0
+    out = []
+    for shape in ((n, 3), (n, 3), (n, 4), (n,), (n, 3, B)):
+        size = int(np.prod(shape))
+        out.append(flat_block[o:o + size].view(*shape))
+        o += size
+    return ParamGrads(*out)
+
+
+def _as_device(a, dev, name, shape):
+    import torch
+    if a is None:
+        return None
+    t = a if isinstance(a, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(a))
+    t = t.to(device=dev, dtype=torch.float32)
+    if t.dim() == len(shape) - 1:
+        t = t.unsqueeze(0)
+    if tuple(t.shape[1:]) != shape[1:]:
+        raise IntegrityError("%s shape %s does not match the camera" % (name, tuple(a.shape)))
+    return t.contiguous()
+
+
+def backward_device(frame, pixel_grads, depth_grads=None, normal_grads=None, alpha_grads=None,
+                    grads_out=None, touched_out=None):
+    """Device-level backward.  pixel_grads (KG,H,W,3) float32 CUDA; returns
+    (grads (KG, n*P) float32, touched (n,) uint8)."""
+    import torch
+    L = _lib.lib()
+    ds = frame.scene
+    dev = ds.device
+    kg = pixel_grads.shape[0]
+    n, B = ds.count, ds.sh_bases
+    P = 11 + 3 * B
+    if grads_out is None:
+        grads_out = torch.empty((kg, n * P), dtype=torch.float32, device=dev)
+    if touched_out is None:
+        touched_out = torch.empty(max(n, 1), dtype=torch.uint8, device=dev)
+    nscr = L.hgs_backward_scratch_bytes(n, kg)
+    scratch = torch.empty(nscr, dtype=torch.uint8, device=dev)
+    _lib.check(L.hgs_backward(
+        _lib.scene_struct(ds), _lib.camera_struct(frame.camera),
+        _lib.settings_struct(frame.settings, frame.flags), _lib.ptr(frame.buf), frame.info, kg,
+        _lib.ptr(pixel_grads), _lib.ptr(depth_grads), _lib.ptr(normal_grads),
+        _lib.ptr(alpha_grads), _lib.ptr(scratch), nscr, _lib.ptr(grads_out), _lib.ptr(touched_out),
+        _lib.current_stream_handle(dev)), "hgs_backward")
+    return grads_out, touched_out[:n]
+
+
+def backward(scene, camera, output, pixel_grad, depth_grad=None, normal_grad=None,
+             alpha_grad=None, validate=True):
+    """Gradients of a scalar image loss with upstream dL/d(color image)
+    (grad/backward.py:37-181).  pixel_grad (H,W,3) or (KG,H,W,3).  Returns a
+    ParamGrads (or a list of KG) and the per-Gaussian touched mask."""
+    import torch
+    single = pixel_grad.ndim == 3
+    H, W = int(camera.height), int(camera.width)
+    shape = tuple(pixel_grad.shape[1:]) if not single else tuple(pixel_grad.shape)
+    if shape != (H, W, 3):
+        raise IntegrityError("pixel_grad shape %s does not match the camera"
+                             % (tuple(pixel_grad.shape),))
+    frame = output.frame
+    dev = frame.scene.device
+    pg = _as_device(pixel_grad, dev, "pixel_grad", (0, H, W, 3))
+    dg = _as_device(depth_grad, dev, "depth_grad", (0, H, W))
+    ng = _as_device(normal_grad, dev, "normal_grad", (0, H, W, 3))
+    ag = _as_device(alpha_grad, dev, "alpha_grad", (0, H, W))
+    kg = pg.shape[0]
+    for t in (dg, ng, ag):
+        if t is not None and t.shape[0] != kg:
+            raise IntegrityError("extension gradients must have the same KG as pixel_grad")
+    if validate:
+        bad = [~torch.isfinite(t).all() for t in (pg, dg, ng, ag) if t is not None]
+        if bool(torch.stack(bad).any()):
+            raise IntegrityError("pixel_grad contains non-finite values")
+    output.check_scene(scene)
+    host = isinstance(scene, GaussianSet)
+    grads, touched = backward_device(frame, pg, dg, ng, ag)
+    n, B = frame.scene.count, frame.scene.sh_bases
+    if host:
+        g = grads.double().cpu()
+        out = [ParamGrads(*(x.numpy() for x in (lambda v: (v.center, v.log_scale, v.rotation,
+                                                            v.opacity_logit, v.sh_coeffs))(
+            _views(g[k], n, B)))) for k in range(kg)]
+        touched = touched.cpu().numpy().astype(bool)
+    else:
+        out = [_views(grads[k], n, B) for k in range(kg)]
+        touched = touched.bool()
+    return (out[0] if single else out), touched

@@ -1,0 +1,319 @@
+"""Forward rendering API -- drop-in for the reference's ``hybridsplat.raster``
+(raster/render.py:83-118, raster/project.py:34-90).
+
+``render(scene, camera, settings)`` runs the whole hot path on the B200 through
+libhgs.so: float64 preprocess, onesweep depth sort, tile binning, and the
+per-tile compositor.  It accepts the reference-style host ``GaussianSet``
+(float64 numpy; outputs come back as float64 numpy, like the reference) or a
+device-resident ``DeviceGaussians`` (float32 CUDA tensors; outputs stay on the
+GPU as torch tensors).  There is no CPU backend.
+"""
+
+from dataclasses import dataclass
+from typing import Optional
+
+import numpy as np
+
+from . import _lib
+from .core import CameraView, DeviceGaussians, GaussianSet
+from .errors import ConfigError, IntegrityError
+from .settings import (ALPHA_CLAMP, EARLY_STOP_T, LOWPASS_SIGMA, MIN_ALPHA, SCREEN_DILATION,
+                       TILE_SIZE, RenderSettings)
+
+HAVE_EXT = _lib.available()
+
+__all__ = ["ALPHA_CLAMP", "EARLY_STOP_T", "LOWPASS_SIGMA", "MIN_ALPHA", "ProjectedSplat",
+           "RenderSettings", "SCREEN_DILATION", "SplatFrame", "HAVE_EXT", "BlendLog",
+           "RenderOutput", "active_backend", "render", "render_naive", "scene_fingerprint"]
+
+
+def active_backend(settings: RenderSettings):
+    """Backend selection (raster/render.py:20-27).  Only the sm_100a kernels
+    exist here; the reference's CPU backends are rejected rather than
+    silently substituted."""
+    b = settings.backend
+    if b in ("auto", "cuda"):
+        _lib.lib()
+        return "cuda"
+    if b in ("cython", "python"):
+        raise ConfigError("backend %r is a CPU backend of the reference; this package only "
+                          "provides the sm_100a CUDA rasterizer" % b)
+    raise ConfigError("backend must be auto or cuda")
+
+
+def scene_fingerprint(scene):
+    """Identity of the scene a RenderOutput was produced from
+    (raster/render.py:67-70).  Host scenes use the reference's sums; device
+    scenes use tensor version counters (no device sync)."""
+    if isinstance(scene, DeviceGaussians):
+        return ("device", scene.count) + scene.versions()
+    return (scene.count, float(scene.center.sum()), float(scene.opacity_logit.sum()),
+            float(scene.log_scale.sum()))
+
+
+@dataclass
+class ProjectedSplat:
+    """raster/project.py:48-57"""
+    gaussian_index: int
+    type_spec: int
+    screen_center: np.ndarray
+    depth_key: float
+    radius: float
+    conic: Optional[np.ndarray] = None
+    plane_params: Optional[np.ndarray] = None
+
+
+@dataclass
+class BlendLog:
+    """Per-pixel ordered record of every composited contribution
+    (raster/render.py:30-51); materialised on demand from the GPU frame."""
+    offsets: np.ndarray
+    position: np.ndarray
+    gaussian_index: np.ndarray
+    alpha: np.ndarray
+    u: np.ndarray
+    v: np.ndarray
+
+    def entries(self, ix, iy, width):
+        lo = self.offsets[iy * width + ix]
+        hi = self.offsets[iy * width + ix + 1]
+        return [(int(self.gaussian_index[e]), float(self.alpha[e]),
+                 (float(self.u[e]), float(self.v[e]))) for e in range(lo, hi)]
+
+
+_FRAME_FIELDS = ("idx", "typ", "depth", "center2d", "cov2d", "conic", "mrow", "alpha_eff",
+                 "color", "radius", "normal", "bbox", "tile_offsets", "tile_ids", "pixel_count")
+
+
+class SplatFrame:
+    """The device frame of one render: sorted splat records, tile lists and
+    per-pixel replay state, living in one caller-owned CUDA buffer.  The
+    reference's SplatFrame arrays (raster/project.py:60-90) are exported on
+    first access (float64, exactly the values the binning used)."""
+
+    def __init__(self, scene, camera, settings, buf, info, flags):
+        self.scene = scene
+        self.camera = camera
+        self.settings = settings
+        self.buf = buf
+        self.info = info
+        self.flags = flags
+        self.height = camera.height
+        self.width = camera.width
+        self.tile_size = settings.tile_size
+        self._host = None
+
+    @property
+    def count(self):
+        return int(self.info.m)
+
+    @property
+    def pair_count(self):
+        return int(self.info.k)
+
+    def export(self):
+        """Dict of float64 / int numpy arrays (reference SplatFrame fields)."""
+        if self._host is not None:
+            return self._host
+        import torch
+        m, k = self.count, self.pair_count
+        dev = self.buf.device
+        W, H = self.width, self.height
+        d = dict(
+            idx=torch.empty(max(m, 1), dtype=torch.int32, device=dev),
+            typ=torch.empty(max(m, 1), dtype=torch.uint8, device=dev),
+            depth=torch.empty(max(m, 1), dtype=torch.float64, device=dev),
+            center2d=torch.empty((max(m, 1), 2), dtype=torch.float64, device=dev),
+            cov2d=torch.empty((max(m, 1), 3), dtype=torch.float64, device=dev),
+            conic=torch.empty((max(m, 1), 3), dtype=torch.float64, device=dev),
+            mrow=torch.empty((max(m, 1), 3, 4), dtype=torch.float64, device=dev),
+            alpha_eff=torch.empty(max(m, 1), dtype=torch.float64, device=dev),
+            color=torch.empty((max(m, 1), 3), dtype=torch.float64, device=dev),
+            radius=torch.empty(max(m, 1), dtype=torch.float64, device=dev),
+            normal=torch.empty((max(m, 1), 3), dtype=torch.float64, device=dev),
+            bbox=torch.empty((max(m, 1), 4), dtype=torch.int32, device=dev),
+            tile_offsets=torch.empty(int(self.info.n_tiles) + 1, dtype=torch.int64, device=dev),
+            tile_ids=torch.empty(max(k, 1), dtype=torch.int32, device=dev),
+            pixel_count=torch.empty((H, W), dtype=torch.int32, device=dev),
+        )
+        ex = _lib.FrameExport(*(_lib.ptr(d[f]) for f in _FRAME_FIELDS))
+        ds = self.scene
+        sc = _lib.scene_struct(ds)
+        _lib.check(_lib.lib().hgs_frame_export_arrays(
+            sc, _lib.camera_struct(self.camera), _lib.settings_struct(self.settings, self.flags),
+            _lib.ptr(self.buf), self.info, ex, _lib.current_stream_handle(dev)), "frame export")
+        out = {f: t.cpu().numpy() for f, t in d.items()}
+        for f in _FRAME_FIELDS:
+            if f in ("tile_offsets", "pixel_count"):
+                continue
+            out[f] = out[f][:k] if f == "tile_ids" else out[f][:m]
+        self._host = out
+        return out
+
+    def __getattr__(self, name):
+        if name in _FRAME_FIELDS:
+            return self.export()[name]
+        raise AttributeError(name)
+
+    def splat(self, k):
+        f = self.export()
+        typ = int(f["typ"][k])
+        c = f["conic"][k]
+        return ProjectedSplat(
+            gaussian_index=int(f["idx"][k]), type_spec=typ, screen_center=f["center2d"][k].copy(),
+            depth_key=float(f["depth"][k]), radius=float(f["radius"][k]),
+            conic=np.array([[c[0], c[1]], [c[1], c[2]]]) if typ == 1 else None,
+            plane_params=f["mrow"][k].copy() if typ == 0 else None)
+
+
+class RenderOutput:
+    """raster/render.py:54-65.  ``color``/``depth``/``transmittance`` are numpy
+    float64 for host scenes and float32 CUDA tensors for device scenes;
+    ``alpha`` (1 - T) and ``normal`` are the extension images."""
+
+    def __init__(self, color, depth, transmittance, alpha, normal, frame, fingerprint,
+                 host_scene=None):
+        self.color = color
+        self.depth = depth
+        self.transmittance = transmittance
+        self.alpha = alpha
+        self.normal = normal
+        self.frame = frame
+        self.scene_fingerprint = fingerprint
+        self._host_scene = host_scene
+        self._log = None
+
+    def check_scene(self, scene):
+        if scene_fingerprint(scene) != self.scene_fingerprint:
+            raise IntegrityError("blend log does not match this scene")
+
+    @property
+    def blend_log(self):
+        if self._log is None:
+            self._log = _materialise_log(self.frame)
+        return self._log
+
+
+def _materialise_log(frame):
+    import torch
+    fx = frame.export()
+    counts = fx["pixel_count"].reshape(-1).astype(np.int64)
+    offsets = np.zeros(counts.size + 1, np.int64)
+    np.cumsum(counts, out=offsets[1:])
+    tot = int(offsets[-1])
+    dev = frame.buf.device
+    d_off = torch.from_numpy(offsets).to(dev)
+    pos = torch.empty(max(tot, 1), dtype=torch.int32, device=dev)
+    al = torch.empty(max(tot, 1), dtype=torch.float32, device=dev)
+    u = torch.empty_like(al)
+    v = torch.empty_like(al)
+    _lib.check(_lib.lib().hgs_blend_log(
+        _lib.scene_struct(frame.scene), _lib.camera_struct(frame.camera),
+        _lib.settings_struct(frame.settings, frame.flags), _lib.ptr(frame.buf), frame.info,
+        _lib.ptr(d_off), _lib.ptr(pos), _lib.ptr(al), _lib.ptr(u), _lib.ptr(v),
+        _lib.current_stream_handle(dev)), "blend log")
+    pos = pos.cpu().numpy()[:tot]
+    idx = fx["idx"]
+    return BlendLog(offsets, pos, idx[pos] if tot else pos,
+                    al.double().cpu().numpy()[:tot], u.double().cpu().numpy()[:tot],
+                    v.double().cpu().numpy()[:tot])
+
+
+# pair-capacity hints per (n, W, H): K of the last frame, so steady-state
+# frames allocate once and never retry.
+_pair_hint = {}
+
+
+def _check_camera(camera):
+    if not isinstance(camera, CameraView):
+        for a in ("fx", "fy", "cx", "cy", "width", "height", "world_to_camera"):
+            if not hasattr(camera, a):
+                raise ConfigError("camera lacks %s" % a)
+    if int(camera.width) > 65535 or int(camera.height) > 65535:
+        raise ConfigError("image dimensions above 65535 are not supported")
+
+
+def rasterize(ds, camera, settings, flags=0, outputs=None):
+    """Device-level forward: DeviceGaussians -> (images dict, SplatFrame).
+
+    ``outputs`` may pass preallocated image tensors (keys color, depth,
+    transmittance, alpha, normal) to avoid per-frame allocation."""
+    import torch
+    L = _lib.lib()
+    _check_camera(camera)
+    if settings.tile_size != TILE_SIZE:
+        raise ConfigError("tile_size must be %d for the CUDA compositor" % TILE_SIZE)
+    dev = ds.device
+    W, H = int(camera.width), int(camera.height)
+    n = ds.count
+    if outputs is None:
+        outputs = dict(
+            color=torch.empty((H, W, 3), dtype=torch.float32, device=dev),
+            depth=torch.empty((H, W), dtype=torch.float32, device=dev),
+            transmittance=torch.empty((H, W), dtype=torch.float32, device=dev),
+            alpha=torch.empty((H, W), dtype=torch.float32, device=dev),
+            normal=torch.empty((H, W, 3), dtype=torch.float32, device=dev))
+    imgs = _lib.Images(*(_lib.ptr(outputs.get(k)) for k in
+                         ("color", "depth", "transmittance", "alpha", "normal")))
+    sc = _lib.scene_struct(ds)
+    cam = _lib.camera_struct(camera)
+    st = _lib.settings_struct(settings, flags)
+    stream = _lib.current_stream_handle(dev)
+    key = (n, W, H)
+    cap = _pair_hint.get(key, max(8 * n, 1 << 16))
+    for _ in range(3):
+        nbytes = L.hgs_frame_bytes(n, W, H, TILE_SIZE, cap)
+        buf = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+        info = _lib.FrameInfo()
+        rc = L.hgs_forward(sc, cam, st, _lib.ptr(buf), nbytes, imgs, info, stream)
+        if rc == _lib.HGS_ERR_PAIR_CAPACITY:
+            cap = int(info.k * 1.25) + 1024
+            _pair_hint[key] = cap
+            continue
+        _lib.check(rc, "hgs_forward")
+        if info.k > cap * 0.9 or key not in _pair_hint:
+            _pair_hint[key] = max(cap, int(info.k * 1.25) + 1024)
+        return outputs, SplatFrame(ds, camera, settings, buf, info, flags)
+    raise ConfigError("could not size the pair buffer")
+
+
+def _flags(settings, naive=False, fast=False):
+    active_backend(settings)
+    f = 0
+    if naive:
+        f |= _lib.HGS_FLAG_NAIVE
+    if fast:
+        f |= _lib.HGS_FLAG_FAST
+    return f
+
+
+def _render(scene, camera, settings, naive, fast):
+    if settings is None:
+        settings = RenderSettings()
+    flags = _flags(settings, naive, fast)
+    if isinstance(scene, DeviceGaussians):
+        imgs, frame = rasterize(scene, camera, settings, flags)
+        return RenderOutput(imgs["color"], imgs["depth"], imgs["transmittance"], imgs["alpha"],
+                            imgs["normal"], frame, scene_fingerprint(scene))
+    if not isinstance(scene, GaussianSet):
+        scene = GaussianSet(scene.center, scene.log_scale, scene.rotation, scene.opacity_logit,
+                            scene.sh_coeffs, scene.type_spec)
+    ds = DeviceGaussians.from_host(scene)
+    imgs, frame = rasterize(ds, camera, settings, flags)
+    host = {k: v.double().cpu().numpy() for k, v in imgs.items()}
+    return RenderOutput(host["color"], host["depth"], host["transmittance"], host["alpha"],
+                        host["normal"], frame, scene_fingerprint(scene), host_scene=scene)
+
+
+def render(scene, camera, settings: RenderSettings = None, *, fast=False) -> RenderOutput:
+    """Rasterize the scene for one view in a single alpha-blending pass
+    (raster/render.py:83-98).  ``fast=True`` skips the float64 re-evaluation
+    of near-threshold decisions (HGS_FLAG_FAST)."""
+    return _render(scene, camera, settings, False, fast)
+
+
+def render_naive(scene, camera, settings: RenderSettings = None) -> RenderOutput:
+    """All-pairs compositor without tiles or bounding boxes, on the GPU
+    (raster/render.py:101-118) -- the oracle the tile renderer is checked
+    against."""
+    return _render(scene, camera, settings, True, False)

@@ -1,0 +1,70 @@
+"""CPU-side checks of the drop-in boundary: libhgs.so loads, exports every
+symbol include/hgs.h declares, and its host-only entry points (sizes, status
+strings) behave.  No kernel is launched here."""
+
+import ctypes
+import os
+import re
+
+import pytest
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _header_symbols():
+    src = open(os.path.join(REPO, "include", "hgs.h")).read()
+    return sorted(set(re.findall(r"^\s*(?:int|size_t|const char \*)\s*(hgs_\w+)\s*\(", src, re.M)))
+
+
+@pytest.fixture(scope="module")
+def L():
+    from paper_2512_02932_b200 import _lib
+    so = _lib.LIB_PATH
+    if not os.path.exists(so):
+        import __graft_entry__
+        __graft_entry__.build()
+    return _lib.lib()
+
+
+def test_exports_every_declared_symbol(L):
+    from paper_2512_02932_b200 import _lib
+    syms = _header_symbols()
+    assert len(syms) >= 9
+    assert set(syms) == set(_lib.EXPORTS)
+    for s in syms:
+        assert hasattr(L, s), s
+
+
+def test_abi_version_and_status_strings(L):
+    assert L.hgs_abi_version() == 1
+    for code in range(0, 7):
+        assert L.hgs_status_string(code)
+    assert b"pairs" in L.hgs_status_string(5)
+
+
+def test_frame_bytes_monotone(L):
+    a = L.hgs_frame_bytes(1000, 64, 48, 16, 10000)
+    b = L.hgs_frame_bytes(1000, 64, 48, 16, 20000)
+    c = L.hgs_frame_bytes(2000, 64, 48, 16, 20000)
+    assert 0 < a < b < c
+    assert L.hgs_frame_bytes(1000, 64, 48, 8, 10) == 0  # tile size must be 16
+    assert L.hgs_backward_scratch_bytes(1000, 1) < L.hgs_backward_scratch_bytes(1000, 3)
+
+
+def test_struct_sizes_match_header():
+    from paper_2512_02932_b200 import _lib
+    assert ctypes.sizeof(_lib.Scene) == 8 + 4 + 4 + 6 * 8
+    assert ctypes.sizeof(_lib.Camera) == 4 * 8 + 8 + 16 * 8 + 2 * 8
+    assert ctypes.sizeof(_lib.FrameInfo) == 4 * 8 + 4 * 4 + 8 + 4 + 4 + 16
+
+
+def test_errors_are_reference_classes():
+    from paper_2512_02932_b200 import _lib, errors
+    with pytest.raises(errors.ConfigError):
+        _lib.check(1, "x")
+    with pytest.raises(errors.InvalidParameterError):
+        _lib.check(2, "x")
+    with pytest.raises(errors.IntegrityError):
+        _lib.check(3, "x")
+    with pytest.raises(errors.DegenerateScaleError):
+        _lib.check(4, "x")
