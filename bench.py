@@ -1,0 +1,409 @@
+"""Benchmark: hybrid-GS fwd+bwd iters/s (and fwd frames/s) at 1M Gaussians, 1080p.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (BASELINE.json configs[1]): synthetic 1M-Gaussian mixed
+2D/3D scene, SH degree 3, 1920x1080, seeded generator; one step = forward
+render + backward (KG = 1 colour gradient) of one view, inputs resident in HBM.
+Under torchrun (N > 1) every rank renders its own view of the replicated scene
+(camera sharding, weak scaling) and the per-Gaussian gradient buffer is
+all-reduced over NCCL each step -- the multi-view training exchange.
+
+One JSON line on rank 0 (see the keys below).  Timing: W untimed warm-up
+steps; K timed steps, each bracketed by CUDA events on the launching stream
+with an L2 flush (256 MiB write) between steps outside the events; barrier +
+synchronize around the timed region; the max over ranks is reported.
+"""
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+MEASURED_PEAKS = os.path.join(REPO, "MEASURED_PEAKS.json")
+METRIC = "hybrid-GS frames/s fwd & iters/s fwd+bwd at 1M Gaussians 1080p; 1/2/4/8 B200"
+N_SM = 148
+FMA_PER_SM_CLK = 128
+MUFU_PER_SM_CLK = 16
+
+# Algorithmic work per pair (_blend_py.py:17-44, 96-113, 149-240)
+FLOP_EVAL_3D = 13       # distance + alpha of a bbox-passing 3D pair
+FLOP_EVAL_2D = 34       # ray-splat solve + low-pass + alpha of a 2D pair
+FLOP_CONTRIB = 11       # weight, colour, depth, transmittance update
+FLOP_BWD_3D = 60        # per contributing pair per KG
+FLOP_BWD_2D_RAY = 115
+FLOP_BWD_2D_LP = 40
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=1_000_000)
+    ap.add_argument("--width", type=int, default=1920)
+    ap.add_argument("--height", type=int, default=1080)
+    ap.add_argument("--sh-degree", type=int, default=3)
+    ap.add_argument("--kg", type=int, default=1)
+    ap.add_argument("--fast", action="store_true", help="HGS_FLAG_FAST (skip f64 re-checks)")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-crop", type=int, default=4, help="cpu sample = 1/crop^2 of the frame")
+    return ap.parse_args()
+
+
+def workload_config(a, n_gpus):
+    return {"workload": "synthetic %d-Gaussian mixed 2D/3D scene (50/50), SH deg %d, %dx%d, "
+                        "fwd + bwd (KG=%d) per view, one view per GPU per step"
+                        % (a.n, a.sh_degree, a.width, a.height, a.kg),
+            "n_gaussians": a.n, "width": a.width, "height": a.height, "sh_degree": a.sh_degree,
+            "kg": a.kg, "views_per_gpu_per_step": 1,
+            "parallelism": "camera-sharded dp%d + NCCL all-reduce of the gradient buffer" % n_gpus
+            if n_gpus > 1 else "single GPU",
+            "l2": "flushed between timed steps (256 MiB write); scene (237 MB) > L2 (126 MB)",
+            "decisions": "fast (f32 only)" if a.fast else "exact (f64 re-check near thresholds)"}
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), "--query-gpu=" + self.Q,
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            self.t.join(timeout=2)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            for nm, v in zip(names, r[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(self.rows)}
+
+
+# ------------------------------------------------------------ CPU baseline
+def cpu_baseline(scene, cam, st, crop, kg=1):
+    """The oracle port on all host cores: full build_frame + fwd/bwd blend of a
+    centred 1/crop^2 crop, extrapolated linearly in pixel count."""
+    import oracle
+    from paper_2512_02932_b200.synthetic import synthetic_camera
+    W, H = cam.width, cam.height
+    cw, ch = W // crop, H // crop
+    ccam = synthetic_camera(cw, ch)
+    ccam.fx, ccam.fy = cam.fx, cam.fy
+    ccam.cx, ccam.cy = cam.cx - (W - cw) / 2.0, cam.cy - (H - ch) / 2.0
+    t0 = time.perf_counter()
+    oracle.build_frame(scene, cam, st)
+    t_build = time.perf_counter() - t0
+    fc = oracle.build_frame(scene, ccam, st)
+    rng = np.random.default_rng(0)
+    pg = rng.normal(size=(kg, ch, cw, 3))
+    t0 = time.perf_counter()
+    oracle.render(scene, ccam, st, frame=fc)
+    t_fwd = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    oracle.backward(scene, ccam, st, pg, frame=fc)
+    t_bwd = time.perf_counter() - t0
+    scale = (W * H) / float(cw * ch)
+    t_iter = t_build + (t_fwd + t_bwd) * scale
+    t_frame = t_build + t_fwd * scale
+    return {"value": 1.0 / t_iter, "unit": "iters/s", "cores": oracle.num_threads(),
+            "kind": "port", "fwd_frames_per_s": 1.0 / t_frame,
+            "sample": "oracle/hgs_oracle.c (float64, OpenMP): build_frame on all %d Gaussians "
+                      "(%.2fs) + fwd (%.2fs) + bwd (%.2fs) blend of a centred %dx%d crop, "
+                      "extrapolated x%.1f in pixel count" % (scene.count, t_build, t_fwd, t_bwd,
+                                                             cw, ch, scale)}
+
+
+def run_reference(a):
+    """--impl reference: the reference's CPU path (oracle port, all host
+    threads) on the same workload; rank 0 only."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from paper_2512_02932_b200.settings import RenderSettings
+    from paper_2512_02932_b200.synthetic import synthetic_scene
+    scene, cam = synthetic_scene(a.n, a.width, a.height, a.sh_degree, seed=0)
+    st = RenderSettings()
+    vals = []
+    for i in range(a.warmup + a.steps):
+        cb = cpu_baseline(scene, cam, st, a.cpu_crop, a.kg)
+        if i >= a.warmup:
+            vals.append(cb["value"])
+    v = float(np.mean(vals))
+    cb["value"] = v
+    line = {"metric": METRIC, "value": v, "unit": "iters/s", "n_gpus": a.gpus, "steps": a.steps,
+            "warmup": a.warmup, "ms_per_step": 1000.0 / v, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": workload_config(a, 1), "impl": "reference", "cpu_baseline": cb,
+            "e2e": {"value": v, "unit": "iters/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------- our arm
+def main():
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+        return
+    import torch
+    import torch.distributed as dist
+
+    from paper_2512_02932_b200 import _lib, grad, raster
+    from paper_2512_02932_b200.core import DeviceGaussians
+    from paper_2512_02932_b200.settings import RenderSettings
+    from paper_2512_02932_b200.synthetic import synthetic_scene
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    scene, cam = synthetic_scene(a.n, a.width, a.height, a.sh_degree, seed=0)
+    st = RenderSettings()
+    ds = DeviceGaussians.from_host(scene, dev)
+    flags = _lib.HGS_FLAG_FAST if a.fast else 0
+    H, W = a.height, a.width
+    g = torch.Generator(device=dev).manual_seed(1234 + rank)
+    pg = torch.randn((a.kg, H, W, 3), device=dev, generator=g)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    n, P = ds.count, 11 + 3 * ds.sh_bases
+    grads_buf = torch.empty((a.kg, n * P), dtype=torch.float32, device=dev)
+    touched_buf = torch.empty(n, dtype=torch.uint8, device=dev)
+    scratch = torch.empty(_lib.lib().hgs_backward_scratch_bytes(n, a.kg), dtype=torch.uint8,
+                          device=dev)
+    imgs = dict(color=torch.empty((H, W, 3), device=dev), depth=torch.empty((H, W), device=dev),
+                transmittance=torch.empty((H, W), device=dev), alpha=torch.empty((H, W), device=dev),
+                normal=torch.empty((H, W, 3), device=dev))
+
+    def ev():
+        return torch.cuda.Event(enable_timing=True)
+
+    def step(fe=None, be=None):
+        _, frame = raster.rasterize(ds, cam, st, flags, outputs=imgs, events=fe)
+        grad.backward_device(frame, pg, grads_out=grads_buf, touched_out=touched_buf, events=be,
+                             scratch=scratch)
+        if world > 1:
+            dist.all_reduce(grads_buf)
+        return frame
+
+    def fwd_only(fe=None):
+        _, frame = raster.rasterize(ds, cam, st, flags, outputs=imgs, events=fe)
+        return frame
+
+    # ---- counting pass (outside timing): algorithmic work per launch
+    _, cframe = raster.rasterize(ds, cam, st, flags | _lib.HGS_FLAG_COUNT, outputs=imgs)
+    grad.backward_device(cframe, pg, grads_out=grads_buf, touched_out=touched_buf,
+                         flags=flags | _lib.HGS_FLAG_COUNT, scratch=scratch)
+    stats = _lib.frame_stats(cframe).astype(np.int64)
+    M, K = cframe.count, cframe.pair_count
+    n_depth_passes, n_tile_passes = int(cframe.info.internal[2]), int(cframe.info.internal[3])
+    del cframe
+
+    for _ in range(a.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    # ---- timed fwd+bwd steps
+    K_ = a.steps
+    s_ev = [ev() for _ in range(K_)]
+    e_ev = [ev() for _ in range(K_)]
+    f_ev = [[ev() for _ in range(5)] for _ in range(K_)]
+    b_ev = [[ev() for _ in range(3)] for _ in range(K_)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clocks:
+        for i in range(K_):
+            flush.fill_(i & 0xff)
+            s_ev[i].record()
+            step(f_ev[i], b_ev[i])
+            e_ev[i].record()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        # fwd-only frames/s
+        fs = [ev() for _ in range(K_)]
+        fe = [ev() for _ in range(K_)]
+        for i in range(K_):
+            flush.fill_(i & 0xff)
+            fs[i].record()
+            fwd_only()
+            fe[i].record()
+        torch.cuda.synchronize()
+    step_ms = float(np.mean([s_ev[i].elapsed_time(e_ev[i]) for i in range(K_)]))
+    fwd_ms = float(np.mean([fs[i].elapsed_time(fe[i]) for i in range(K_)]))
+    stage_names = ["depth_keys+sort", "preprocess_f64+scan", "binning(dup+tile sort+ranges)",
+                   "composite_fwd"]
+    stages = {}
+    for j, nm in enumerate(stage_names):
+        stages[nm] = float(np.mean([f_ev[i][j].elapsed_time(f_ev[i][j + 1]) for i in range(K_)]))
+    stages["composite_bwd"] = float(np.mean([b_ev[i][0].elapsed_time(b_ev[i][1]) for i in range(K_)]))
+    stages["chain_rule(+touched)"] = float(np.mean([b_ev[i][1].elapsed_time(b_ev[i][2])
+                                                   for i in range(K_)]))
+    if world > 1:
+        t = torch.tensor([step_ms, fwd_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        step_ms, fwd_ms = float(t[0]), float(t[1])
+
+    clk = clocks.summary()
+    sm_mhz = clk["sm_mhz"] or 1965.0
+    fp32_peak = N_SM * FMA_PER_SM_CLK * 2 * sm_mhz * 1e6 / 1e12
+    mufu_peak = N_SM * MUFU_PER_SM_CLK * sm_mhz * 1e6 / 1e12
+
+    # ---- roofline of the dominant kernel
+    ev3, ev2, c3, c2 = (int(x) for x in stats[2:6])
+    b3, br, bl, bev = (int(x) for x in stats[6:10])
+    dom = max(stages, key=stages.get)
+    flops = {
+        "composite_fwd": FLOP_EVAL_3D * ev3 + FLOP_EVAL_2D * ev2 + FLOP_CONTRIB * (c3 + c2),
+        "composite_bwd": (FLOP_EVAL_3D * ev3 + FLOP_EVAL_2D * ev2) * bev / max(ev3 + ev2, 1)
+        + a.kg * (FLOP_BWD_3D * b3 + FLOP_BWD_2D_RAY * br + FLOP_BWD_2D_LP * bl),
+    }
+    mufu = {"composite_fwd": ev3 + 2 * ev2, "composite_bwd": bev + 2 * (b3 + br + bl)}
+    hbm_bytes = {
+        "depth_keys+sort": a.n * (40 + 1) + a.n * 12 * 2 * n_depth_passes,
+        "preprocess_f64+scan": M * (237 + 4 + 96 + 8),
+        "binning(dup+tile sort+ranges)": M * 104 + K * (8 + 16 * n_tile_passes + 4),
+        "chain_rule(+touched)": a.n * (4 * (11 + 3 * ds.sh_bases) + 1 + 64 * a.kg
+                                       + 4 * P * a.kg),
+    }
+    peaks = json.load(open(MEASURED_PEAKS)) if os.path.exists(MEASURED_PEAKS) else {}
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    t_dom = stages[dom] * 1e-3
+    if dom in flops:
+        ach = flops[dom] / t_dom / 1e12
+        roof = {"kernel": dom, "bound": "fp32", "achieved": ach, "peak": fp32_peak,
+                "unit": "TFLOP/s", "frac": ach / fp32_peak,
+                "mufu_frac": mufu[dom] / t_dom / 1e12 / mufu_peak,
+                "peak_source": "148 SM x 128 FFMA/clk x 2 x median SM clock under load "
+                               "(%.0f MHz, nvidia-smi during the timed region)" % sm_mhz,
+                "work": "%d 3D + %d 2D bbox-passing pairs, %d contributing (fwd); bwd contributing "
+                        "3D %d, 2D-ray %d, 2D-lowpass %d" % (ev3, ev2, c3 + c2, b3, br, bl)}
+    else:
+        ach = hbm_bytes[dom] / t_dom / 1e9
+        roof = {"kernel": dom, "bound": "hbm", "achieved": ach, "peak": hbm_peak, "unit": "GB/s",
+                "frac": ach / hbm_peak, "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
+    traffic_file = os.path.join(REPO, "profiles", "traffic.json")
+    roof["traffic"] = None
+    if os.path.exists(traffic_file):
+        tr = json.load(open(traffic_file))
+        if dom in tr:
+            roof["traffic"] = tr[dom]
+    stage_roofs = {}
+    for nm, t_ms in stages.items():
+        if nm in flops:
+            stage_roofs[nm] = {"ms": t_ms, "TFLOP/s": flops[nm] / (t_ms * 1e-3) / 1e12,
+                               "fp32_frac": flops[nm] / (t_ms * 1e-3) / 1e12 / fp32_peak}
+        elif nm in hbm_bytes:
+            gbs = hbm_bytes[nm] / (t_ms * 1e-3) / 1e9
+            stage_roofs[nm] = {"ms": t_ms, "GB/s": gbs, "hbm_frac": gbs / hbm_peak}
+
+    launches_fwd = 1 + 1 + n_depth_passes + 1 + 1 + 1 + n_tile_passes + 1 + 1
+    launches_bwd = 1 + 1 + 2 * ((a.kg + 3) // 4)
+    value = world * 1000.0 / step_ms
+
+    # ---- e2e through the public API with host buffers (rank-local)
+    e2e = None
+    if not a.no_e2e:
+        from paper_2512_02932_b200.core import GaussianSet
+        host_scene = GaussianSet(scene.center, scene.log_scale, scene.rotation, scene.opacity_logit,
+                                 scene.sh_coeffs, scene.type_spec)
+        pg_host = pg[0].double().cpu().numpy()
+        h2d = sum(getattr(host_scene, f).nbytes for f in GaussianSet.FIELDS) + pg_host.nbytes
+        ts = []
+        for i in range(a.e2e_steps + 1):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            out = raster.render(host_scene, cam, st, fast=a.fast)
+            gr, touched = grad.backward(host_scene, cam, out, pg_host)
+            torch.cuda.synchronize()
+            if i:
+                ts.append(time.perf_counter() - t0)
+        d2h = (out.color.nbytes + out.depth.nbytes + out.transmittance.nbytes + out.alpha.nbytes
+               + out.normal.nbytes + gr.flat().nbytes + touched.nbytes)
+        tt = float(np.mean(ts))
+        if world > 1:
+            t = torch.tensor([tt], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            tt = float(t[0])
+        e2e = {"value": world / tt, "unit": "iters/s", "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h),
+               "path": "raster.render(GaussianSet float64 numpy) + grad.backward(numpy pixel_grad)"
+                       " -> numpy float64 images and ParamGrads; wall clock with device syncs"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        cpu = cpu_baseline(scene, cam, st, a.cpu_crop, a.kg)
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": "iters/s", "n_gpus": world,
+                "steps": a.steps, "warmup": a.warmup, "ms_per_step": step_ms,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "fp32",
+                "data": "synthetic (seeded generator, SURVEY.md 8d)",
+                "config": workload_config(a, world),
+                "fwd_frames_per_s": world * 1000.0 / fwd_ms, "fwd_ms": fwd_ms,
+                "stages_ms": stages, "stage_rooflines": stage_roofs, "roofline": roof,
+                "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
+                "gpu_launches": (launches_fwd + launches_bwd) * a.steps,
+                "frame": {"M": M, "K_pairs": K, "depth_sort_passes": n_depth_passes,
+                          "f64_rechecks": int(stats[0]), "f64_T_replays": int(stats[1]),
+                          "fwd_pairs_evaluated": ev3 + ev2, "fwd_pairs_contributing": c3 + c2}}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -76,11 +76,19 @@ typedef struct hgs_settings {
   int32_t tile_size; /* must be 16 */
   double theta_z, t_z, lambda_z;
   uint32_t flags;
-  uint32_t reserved;
+  int32_t n_timing_events;     /* 0, or the length of timing_events            */
+  void *const *timing_events;  /* nullable: caller-created cudaEvent_t handles
+                                * recorded on the stream at stage boundaries:
+                                * forward  [0] start [1] depth keys+sort
+                                *          [2] f64 preprocess+scan [3] binning
+                                *          [4] composite
+                                * backward [0] start [1] composite replay
+                                *          [2] chain rule                     */
 } hgs_settings;
 
 #define HGS_FLAG_NAIVE 0x1u /* render_naive: every splat for every pixel, no tiles, no bbox test (render.py:101-118) */
 #define HGS_FLAG_FAST 0x2u  /* skip the float64 re-evaluation of near-threshold decisions */
+#define HGS_FLAG_COUNT 0x4u /* count evaluated / contributing pairs per type (hgs_frame_stats) */
 
 /* Output images (device, row-major).  Any of normal / alpha may be NULL. */
 typedef struct hgs_images {
@@ -167,6 +175,14 @@ int hgs_frame_export_arrays(const hgs_scene *scene, const hgs_camera *camera, co
 int hgs_blend_log(const hgs_scene *scene, const hgs_camera *camera, const hgs_settings *settings, const void *frame,
                   const hgs_frame_info *info, const int64_t *offsets, int32_t *position, float *alpha, float *u,
                   float *v, void *stream);
+
+/* Diagnostics of the last forward / backward on this frame (synchronous):
+ *  [0] float64 pair re-evaluations  [1] float64 transmittance replays
+ *  with HGS_FLAG_COUNT: forward [2] 3D pairs evaluated (bbox pass) [3] 2D pairs
+ *  evaluated [4] 3D contributing [5] 2D contributing; backward [6] 3D
+ *  contributing [7] 2D ray-branch contributing [8] 2D low-pass contributing
+ *  [9] pairs evaluated. */
+int hgs_frame_stats(const void *frame, const hgs_frame_info *info, uint64_t *out16, void *stream);
 
 const char *hgs_status_string(int status);
 int hgs_abi_version(void);

@@ -23,11 +23,12 @@ HGS_ERR_CUDA = 6
 
 HGS_FLAG_NAIVE = 0x1
 HGS_FLAG_FAST = 0x2
+HGS_FLAG_COUNT = 0x4
 
 # Every symbol include/hgs.h declares.
 EXPORTS = ("hgs_abi_version", "hgs_status_string", "hgs_frame_bytes", "hgs_forward",
            "hgs_backward_scratch_bytes", "hgs_backward", "hgs_exchange",
-           "hgs_frame_export_arrays", "hgs_blend_log")
+           "hgs_frame_export_arrays", "hgs_blend_log", "hgs_frame_stats")
 
 _vp = ctypes.c_void_p
 _i64 = ctypes.c_int64
@@ -51,7 +52,7 @@ class Settings(ctypes.Structure):
     _fields_ = [("background", ctypes.c_float * 3), ("tile_size", _i32),
                 ("theta_z", ctypes.c_double), ("t_z", ctypes.c_double),
                 ("lambda_z", ctypes.c_double), ("flags", ctypes.c_uint32),
-                ("reserved", ctypes.c_uint32)]
+                ("n_timing_events", _i32), ("timing_events", ctypes.POINTER(_vp))]
 
 
 class Images(ctypes.Structure):
@@ -116,6 +117,7 @@ def lib():
                                           P(FrameExport), _vp]
     L.hgs_blend_log.argtypes = [P(Scene), P(Camera), P(Settings), _vp, P(FrameInfo), _vp, _vp,
                                 _vp, _vp, _vp, _vp]
+    L.hgs_frame_stats.argtypes = [_vp, P(FrameInfo), _vp, _vp]
     if L.hgs_abi_version() != 1:
         _load_error = "libhgs.so ABI version mismatch"
         raise ExtensionError(_load_error)
@@ -169,9 +171,32 @@ def camera_struct(cam):
                   int(cam.height), (ctypes.c_double * 16)(*w2c), float(cam.near), float(cam.far))
 
 
-def settings_struct(st, flags=0):
+def settings_struct(st, flags=0, events=None):
+    """hgs_settings; ``events`` = list of torch.cuda.Event(enable_timing=True)
+    recorded by the library at its stage boundaries (include/hgs.h)."""
     bg = [float(b) for b in st.background]
     if len(bg) != 3:
         raise ConfigError("background must have 3 channels")
-    return Settings((ctypes.c_float * 3)(*bg), int(st.tile_size), float(st.theta_z),
-                    float(st.t_z), float(st.lambda_z), int(flags), 0)
+    s = Settings((ctypes.c_float * 3)(*bg), int(st.tile_size), float(st.theta_z),
+                 float(st.t_z), float(st.lambda_z), int(flags), 0, None)
+    if events:
+        arr = (_vp * len(events))(*[event_handle(e) for e in events])
+        s.n_timing_events = len(events)
+        s.timing_events = ctypes.cast(arr, ctypes.POINTER(_vp))
+        s._keep = arr
+    return s
+
+
+def event_handle(ev):
+    """Raw cudaEvent_t of a torch.cuda.Event (created on first record)."""
+    if not ev.cuda_event:
+        ev.record()
+    return ev.cuda_event
+
+
+def frame_stats(frame):
+    import numpy as np
+    out = np.zeros(16, np.uint64)
+    check(lib().hgs_frame_stats(ptr(frame.buf), frame.info, out.ctypes.data_as(ctypes.c_void_p),
+                                current_stream_handle(frame.buf.device)), "hgs_frame_stats")
+    return out

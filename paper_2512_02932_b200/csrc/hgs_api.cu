@@ -117,6 +117,11 @@ int check_common(const hgs_scene *sc, const hgs_camera *cam, const hgs_settings 
 
 #define HGS_LAUNCHED() HGS_CUDA(cudaGetLastError())
 
+cudaError_t record_event(const hgs_settings *st, int i, cudaStream_t s) {
+  if (!st->timing_events || i >= st->n_timing_events || !st->timing_events[i]) return cudaSuccess;
+  return cudaEventRecord(static_cast<cudaEvent_t>(st->timing_events[i]), s);
+}
+
 int grid_for(int64_t work, int block) {
   return (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(work, block), kMaxGrid));
 }
@@ -205,7 +210,10 @@ int hgs_forward(const hgs_scene *scene, const hgs_camera *camera, const hgs_sett
   info->n = n; info->width = W; info->height = H; info->tiles_x = cam.tiles_x; info->tiles_y = cam.tiles_y;
   info->n_tiles = n_tiles; info->pair_capacity = cap; info->sh_bases = scene->sh_bases; info->flags = settings->flags;
 
+  HGS_CUDA(record_event(settings, 0, s));
   HGS_CUDA(cudaMemsetAsync(frame, 0, L.small_end, s));
+  k_init_state<<<1, 1, 0, s>>>(sc, cam, mod, st);
+  HGS_LAUNCHED();
   // 1. depth keys + digit histograms
   uint32_t *vals_sorted = at<uint32_t>(frame, L.vals_a);
   int64_t m = 0;
@@ -237,8 +245,10 @@ int hgs_forward(const hgs_scene *scene, const hgs_camera *camera, const hgs_sett
                                         st->tile_counters + 1, s, &in_b);
     if (rc) return rc;
     vals_sorted = at<uint32_t>(frame, in_b ? L.vals_b : L.vals_a);
+    info->internal[2] = (uint32_t)np;  // depth-sort passes (diagnostics / launch count)
   }
   info->m = m;
+  HGS_CUDA(record_event(settings, 1, s));
   // 3. float64 preprocess per rank + pair-offset scan
   int64_t K = 0;
   if (m > 0) {
@@ -253,6 +263,7 @@ int hgs_forward(const hgs_scene *scene, const hgs_camera *camera, const hgs_sett
     K = (int64_t)kt;
   }
   info->k = K;
+  HGS_CUDA(record_event(settings, 2, s));
   if (K > cap || K >= (1ll << 32)) return HGS_ERR_PAIR_CAPACITY;
   // 4. duplicate + tile sort + ranges
   const uint32_t *tile_vals = at<uint32_t>(frame, L.pv_a);
@@ -274,10 +285,12 @@ int hgs_forward(const hgs_scene *scene, const hgs_camera *camera, const hgs_sett
     tile_vals = at<uint32_t>(frame, in_b ? L.pv_b : L.pv_a);
     tile_keys = at<uint32_t>(frame, in_b ? L.pk_b : L.pk_a);
     info->internal[0] = in_b ? 1u : 0u;
+    info->internal[3] = (uint32_t)nd;  // tile-sort passes
   }
   k_tile_ranges<<<(unsigned)std::max<int64_t>(1, ceil_div(std::max<int64_t>(K, n_tiles + 1), 256)), 256, 0, s>>>(
       tile_keys, K, n_tiles, at<uint32_t>(frame, L.tile_off));
   HGS_LAUNCHED();
+  HGS_CUDA(record_event(settings, 3, s));
   // 5. composite
   CompositeArgs a;
   a.recs = at<SplatRec>(frame, L.recs);
@@ -292,12 +305,14 @@ int hgs_forward(const hgs_scene *scene, const hgs_camera *camera, const hgs_sett
   a.pix_T = at<float>(frame, L.pix_T);
   a.pix_last = at<uint32_t>(frame, L.pix_last);
   a.pix_count = at<uint32_t>(frame, L.pix_count);
-  a.sc = sc; a.cam = cam; a.mod = mod; a.st = st;
-  if (settings->flags & HGS_FLAG_NAIVE)
-    k_composite_fwd<true><<<(unsigned)n_tiles, kBlock, 0, s>>>(a);
-  else
-    k_composite_fwd<false><<<(unsigned)n_tiles, kBlock, 0, s>>>(a);
+  a.st = st;
+  const bool naive = settings->flags & HGS_FLAG_NAIVE, count = settings->flags & HGS_FLAG_COUNT;
+  if (naive && count) k_composite_fwd<true, true><<<(unsigned)n_tiles, kBlock, 0, s>>>(a);
+  else if (naive) k_composite_fwd<true, false><<<(unsigned)n_tiles, kBlock, 0, s>>>(a);
+  else if (count) k_composite_fwd<false, true><<<(unsigned)n_tiles, kBlock, 0, s>>>(a);
+  else k_composite_fwd<false, false><<<(unsigned)n_tiles, kBlock, 0, s>>>(a);
   HGS_LAUNCHED();
+  HGS_CUDA(record_event(settings, 4, s));
   return HGS_OK;
 }
 
@@ -317,10 +332,9 @@ static CompositeArgs composite_args_for(const hgs_scene *scene, const hgs_camera
   a.pix_T = at<float>(fr, L.pix_T);
   a.pix_last = at<uint32_t>(fr, L.pix_last);
   a.pix_count = at<uint32_t>(fr, L.pix_count);
-  a.sc = make_scene(*scene);
-  a.cam = make_cam(*camera);
-  a.mod = ModD{settings->theta_z, settings->t_z, settings->lambda_z};
   a.st = at<FrameState>(fr, L.state);
+  (void)scene;
+  (void)camera;
   return a;
 }
 
@@ -372,10 +386,17 @@ int hgs_backward(const hgs_scene *scene, const hgs_camera *camera, const hgs_set
   float *acc_ext = reinterpret_cast<float *>(static_cast<char *>(scratch) + ((nn * kc_max * 16 * 4 + 255) & ~255ll));
   uint8_t *touched_rank = reinterpret_cast<uint8_t *>(reinterpret_cast<char *>(acc_ext) +
                                                       ((nn * kc_max * 4 * 4 + 255) & ~255ll));
+  HGS_CUDA(record_event(settings, 0, s));
   HGS_CUDA(cudaMemsetAsync(touched, 0, (size_t)nn, s));
   BwdArgs b;
   b.c = composite_args_for(scene, camera, settings, frame, info);
-  const ChainArgs c0{b.c.sc, b.c.cam, b.c.mod, acc, ext ? acc_ext : nullptr, 0, nullptr};
+  HGS_CUDA(cudaMemsetAsync(&b.c.st->diag[6], 0, 4 * sizeof(unsigned long long), s));
+  const SceneView sc = make_scene(*scene);
+  const CamD cam = make_cam(*camera);
+  const ModD mod{settings->theta_z, settings->t_z, settings->lambda_z};
+  k_init_state<<<1, 1, 0, s>>>(sc, cam, mod, b.c.st);
+  HGS_LAUNCHED();
+  const ChainArgs c0{sc, cam, mod, acc, ext ? acc_ext : nullptr, 0, nullptr};
   for (int k0 = 0; k0 < kg; k0 += 4) {
     const int kc = std::min(4, kg - k0);
     HGS_CUDA(cudaMemsetAsync(acc, 0, (size_t)nn * kc * 16 * 4, s));
@@ -396,6 +417,7 @@ int hgs_backward(const hgs_scene *scene, const hgs_camera *camera, const hgs_set
         default: launch_bwd<4>(b, info->n_tiles, ext, s); break;
       }
       HGS_LAUNCHED();
+      if (k0 == 0) HGS_CUDA(record_event(settings, 1, s));
       if (k0 == 0) {
         k_touched_scatter<<<grid_for(m, 256), 256, 0, s>>>(b.c.recs, touched_rank, m, touched);
         HGS_LAUNCHED();
@@ -409,6 +431,7 @@ int hgs_backward(const hgs_scene *scene, const hgs_camera *camera, const hgs_set
       HGS_LAUNCHED();
     }
   }
+  HGS_CUDA(record_event(settings, 2, s));
   return HGS_OK;
 }
 
@@ -495,7 +518,7 @@ __global__ void k_blend_log(CompositeArgs a, const int64_t *__restrict__ offsets
         if (ix < x0 || ix > x1 || iy < y0 || iy > y1) continue;
       }
       PairEval p;
-      if (!eval_pair<false>(r, ix, iy, a, p)) continue;
+      if (!eval_pair<true>(r, a.recs + rk, ix, iy, a.flags, a.st, p)) continue;
       pos[o] = (int32_t)rk;
       alpha[o] = p.at;
       u[o] = p.u;
@@ -518,7 +541,8 @@ int hgs_frame_export_arrays(const hgs_scene *scene, const hgs_camera *camera, co
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const CompositeArgs a = composite_args_for(scene, camera, settings, frame, info);
   if (info->m > 0) {
-    k_export_frame<<<grid_for(info->m, 128), 128, 0, s>>>(a.sc, a.cam, a.mod, a.recs, info->m, *out);
+    k_export_frame<<<grid_for(info->m, 128), 128, 0, s>>>(make_scene(*scene), make_cam(*camera),
+        ModD{settings->theta_z, settings->t_z, settings->lambda_z}, a.recs, info->m, *out);
     HGS_LAUNCHED();
   }
   if (out->tile_offsets) {
@@ -531,6 +555,16 @@ int hgs_frame_export_arrays(const hgs_scene *scene, const hgs_camera *camera, co
   if (out->pixel_count)
     HGS_CUDA(cudaMemcpyAsync(out->pixel_count, a.pix_count, (size_t)info->width * info->height * 4,
                              cudaMemcpyDeviceToDevice, s));
+  return HGS_OK;
+}
+
+int hgs_frame_stats(const void *frame, const hgs_frame_info *info, uint64_t *out16, void *stream) {
+  if (!frame || !info || !out16) return HGS_ERR_CONFIG;
+  const Layout L = make_layout(info->n, info->width, info->height, info->pair_capacity);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const FrameState *st = at<FrameState>(frame, L.state);
+  HGS_CUDA(cudaMemcpyAsync(out16, st->diag, 16 * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+  HGS_CUDA(cudaStreamSynchronize(s));
   return HGS_OK;
 }
 

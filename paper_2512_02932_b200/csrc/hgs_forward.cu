@@ -6,6 +6,12 @@
 
 namespace hgs {
 
+__global__ void k_init_state(SceneView sc, CamD cam, ModD mod, FrameState *st) {
+  st->sc = sc;
+  st->cam = cam;
+  st->mod = mod;
+}
+
 // ------------------------------------------------------------ depth keys
 // Per Gaussian: view depth in float64, near cull (project.py:181-185),
 // singular-conic validity for 3D (project.py:225), |q| check (rotation.py:
@@ -180,16 +186,18 @@ __global__ void k_tile_ranges(const uint32_t *__restrict__ skeys, int64_t k, int
 
 // Per-tile front-to-back compositor (_blend_py.py:76-117).  One CTA per
 // 16 x 16 tile, one thread per pixel; warps own 8 x 4 pixel blocks.  Splat
-// records are staged in shared memory in batches of 256; every lane of a
-// warp walks the same splat so the 2D / 3D branch is warp-uniform.
-template <bool NAIVE>
-__global__ void __launch_bounds__(kBlock) k_composite_fwd(CompositeArgs a) {
+// records are staged in shared memory in batches of 256.  Each warp first
+// culls the batch against its 8 x 4 block (one rect test per lane, ballot),
+// then walks only the relevant splats, in order; all lanes of the warp see
+// the same splat, so the 2D / 3D branch is warp-uniform.
+template <bool NAIVE, bool COUNT>
+__global__ void __launch_bounds__(kBlock, 3) k_composite_fwd(CompositeArgs a) {
   __shared__ SplatRec s_rec[kBlock];
   const int tile = blockIdx.x;
   const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int ix = tx * kTile + (warp & 1) * 8 + (lane & 7);
-  const int iy = ty * kTile + (warp >> 1) * 4 + (lane >> 3);
+  const int wx0 = tx * kTile + (warp & 1) * 8, wy0 = ty * kTile + (warp >> 1) * 4;
+  const int ix = wx0 + (lane & 7), iy = wy0 + (lane >> 3);
   const bool inside = ix < a.width && iy < a.height;
   int64_t lo, hi;
   if (NAIVE) {
@@ -202,42 +210,66 @@ __global__ void __launch_bounds__(kBlock) k_composite_fwd(CompositeArgs a) {
   float T = 1.f, cr = 0.f, cg = 0.f, cb = 0.f, dep = 0.f, n0 = 0.f, n1 = 0.f, n2 = 0.f;
   uint32_t cnt = 0, last = 0;
   bool done = !inside;
-  const FwdGuard guard(a, ix, iy);
+  uint32_t n_ev3 = 0, n_ev2 = 0, n_c3 = 0, n_c2 = 0;  // HGS_FLAG_COUNT
   for (int64_t base = lo; base < hi; base += kBlock) {
     __syncthreads();
-    int64_t j = base + threadIdx.x;
+    const int64_t j = base + threadIdx.x;
     if (j < hi) {
-      uint32_t rk = NAIVE ? (uint32_t)j : a.tile_vals[j];
+      const uint32_t rk = NAIVE ? (uint32_t)j : a.tile_vals[j];
       s_rec[threadIdx.x] = a.recs[rk];
     }
     __syncthreads();
     const int nb = (int)(hi - base < kBlock ? hi - base : kBlock);
-    for (int e = 0; e < nb && !done; ++e) {
-      const SplatRec &r = s_rec[e];
-      const int4 q = r.r5;
-      if (!NAIVE) {
-        const int x0 = q.x & 0xffff, y0 = (int)((uint32_t)q.x >> 16);
-        const int x1 = q.y & 0xffff, y1 = (int)((uint32_t)q.y >> 16);
-        if (ix < x0 || ix > x1 || iy < y0 || iy > y1) continue;
+    for (int w0 = 0; w0 < nb && !__all_sync(0xffffffffu, done); w0 += 32) {
+      const int el = w0 + lane;
+      bool rel = el < nb;
+      if (!NAIVE && rel) rel = bbox_overlaps(s_rec[el].r5, wx0, wy0, wx0 + 7, wy0 + 3);
+      uint32_t mask = __ballot_sync(0xffffffffu, rel);
+      while (mask) {
+        const int e = w0 + __ffs(mask) - 1;
+        mask &= mask - 1;
+        if (done) continue;
+        const SplatRec &r = s_rec[e];
+        if (!NAIVE && !in_bbox(r.r5, ix, iy)) continue;
+        const bool is3d = rec_is3d(r);
+        if (COUNT) (is3d ? n_ev3 : n_ev2) += 1;
+        PairEval p;
+        const uint32_t rk = NAIVE ? (uint32_t)(base + e) : a.tile_vals[base + e];
+        if (!eval_pair<false>(r, a.recs + rk, ix, iy, a.flags, a.st, p)) continue;
+        if (COUNT) (is3d ? n_c3 : n_c2) += 1;
+        const float at = p.at;
+        const float w = at * T;
+        const float4 c3 = r.r3, c4 = r.r4;
+        cr = fmaf(w, c3.y, cr);
+        cg = fmaf(w, c3.z, cg);
+        cb = fmaf(w, c3.w, cb);
+        dep = fmaf(w, r.r0.z, dep);
+        n0 = fmaf(w, c4.x, n0);
+        n1 = fmaf(w, c4.y, n1);
+        n2 = fmaf(w, c4.z, n2);
+        ++cnt;
+        last = (uint32_t)(base + e - lo) + 1u;
+        const float Tn = T * (1.f - at);
+        if (early_stop(Tn, a, lo, base + e, ix, iy)) done = true;
+        T = Tn;
       }
-      float at;
-      if (!eval_alpha(r, ix, iy, guard, at)) continue;
-      const float w = at * T;
-      const float4 c3 = r.r3, c4 = r.r4, c0 = r.r0;
-      cr = fmaf(w, c3.y, cr);
-      cg = fmaf(w, c3.z, cg);
-      cb = fmaf(w, c3.w, cb);
-      dep = fmaf(w, c0.z, dep);
-      n0 = fmaf(w, c4.x, n0);
-      n1 = fmaf(w, c4.y, n1);
-      n2 = fmaf(w, c4.z, n2);
-      ++cnt;
-      last = (uint32_t)(base + e - lo) + 1u;
-      const float Tn = T * (1.f - at);
-      if (guard.early_stop(Tn, T, lo, base + e)) done = true;
-      T = Tn;
     }
     if (__syncthreads_count(done) == kBlock) break;
+  }
+  if (COUNT) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      n_ev3 += __shfl_xor_sync(0xffffffffu, n_ev3, o);
+      n_ev2 += __shfl_xor_sync(0xffffffffu, n_ev2, o);
+      n_c3 += __shfl_xor_sync(0xffffffffu, n_c3, o);
+      n_c2 += __shfl_xor_sync(0xffffffffu, n_c2, o);
+    }
+    if (lane == 0) {
+      atomicAdd(&a.st->diag[2], (unsigned long long)n_ev3);
+      atomicAdd(&a.st->diag[3], (unsigned long long)n_ev2);
+      atomicAdd(&a.st->diag[4], (unsigned long long)n_c3);
+      atomicAdd(&a.st->diag[5], (unsigned long long)n_c2);
+    }
   }
   if (!inside) return;
   const int64_t pix = (int64_t)iy * a.width + ix;
@@ -257,7 +289,9 @@ __global__ void __launch_bounds__(kBlock) k_composite_fwd(CompositeArgs a) {
   a.pix_count[pix] = cnt;
 }
 
-template __global__ void k_composite_fwd<false>(CompositeArgs);
-template __global__ void k_composite_fwd<true>(CompositeArgs);
+template __global__ void k_composite_fwd<false, false>(CompositeArgs);
+template __global__ void k_composite_fwd<true, false>(CompositeArgs);
+template __global__ void k_composite_fwd<false, true>(CompositeArgs);
+template __global__ void k_composite_fwd<true, true>(CompositeArgs);
 
 }  // namespace hgs

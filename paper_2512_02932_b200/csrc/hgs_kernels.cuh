@@ -7,13 +7,18 @@
 
 namespace hgs {
 
-// Small device-side state at the head of the frame buffer.
+// Device-side state at the head of the frame buffer.  The scene / camera
+// copies serve the rare float64 re-evaluation paths, which read them through
+// a global pointer instead of (large) kernel parameters.
 struct FrameState {
   uint32_t status;
   uint32_t m_count;
   unsigned long long k_total;
   uint32_t tile_counters[24];
-  unsigned long long diag[4];  // [0] f64 pair re-checks, [1] f64 T replays
+  unsigned long long diag[16];  // see hgs_frame_stats in include/hgs.h
+  SceneView sc;
+  CamD cam;
+  ModD mod;
 };
 
 struct CompositeArgs {
@@ -29,11 +34,7 @@ struct CompositeArgs {
   float *color, *depth, *trans, *alpha, *normal;
   float *pix_T;
   uint32_t *pix_last, *pix_count;
-  // float64 re-evaluation of near-threshold decisions
-  SceneView sc;
-  CamD cam;
-  ModD mod;
-  FrameState *st;
+  FrameState *st;  // diagnostics + scene / camera for float64 re-checks
 };
 
 // log2 domain constants: at = ex2(arg), arg = log2(alpha_eff) - d * 0.5 log2(e)
@@ -41,6 +42,24 @@ constexpr float kHalfLog2e = 0.72134752044448170f;
 constexpr float kArgMinAlpha = -7.99435343685885793f;  // log2(1/255)
 constexpr float kArgClamp = -0.01449956969511509f;     // log2(0.99)
 constexpr float kEps = 5.96046448e-8f;                 // 2^-24
+constexpr float kCoarse2D = 0.05f;                     // log2 units; 2D precise bounds only inside
+
+__device__ __forceinline__ bool rec_is3d(const SplatRec &r) { return __float_as_uint(r.r4.w) >> 31; }
+__device__ __forceinline__ uint32_t rec_idx(const SplatRec &r) { return __float_as_uint(r.r4.w) & 0x7fffffffu; }
+
+// inclusive pixel bbox (raster/_blend_py.py:89-91)
+__device__ __forceinline__ bool in_bbox(const int4 q, int ix, int iy) {
+  const int x0 = q.x & 0xffff, y0 = (int)((uint32_t)q.x >> 16);
+  const int x1 = q.y & 0xffff, y1 = (int)((uint32_t)q.y >> 16);
+  return !(ix < x0 || ix > x1 || iy < y0 || iy > y1);
+}
+
+// bbox overlaps the pixel rectangle [rx0, rx1] x [ry0, ry1]
+__device__ __forceinline__ bool bbox_overlaps(const int4 q, int rx0, int ry0, int rx1, int ry1) {
+  const int x0 = q.x & 0xffff, y0 = (int)((uint32_t)q.x >> 16);
+  const int x1 = q.y & 0xffff, y1 = (int)((uint32_t)q.y >> 16);
+  return !(x1 < rx0 || x0 > rx1 || y1 < ry0 || y0 > ry1);
+}
 
 // Result of evaluating one (pixel, splat) pair.
 struct PairEval {
@@ -55,8 +74,8 @@ struct PairEval {
 
 // float64 re-evaluation of one pair exactly as the reference does it
 // (_blend_py.py:17-44, 96-100).  Returns false if the pair is skipped.
-static __device__ __noinline__ bool pair_f64(const SceneView &sc, const CamD &cam, const ModD &mod, uint32_t idx, int ix,
-                                      int iy, double *at_out, bool *ray_out, bool *clamped_out) {
+static __device__ __noinline__ bool pair_f64(const SceneView &sc, const CamD &cam, const ModD &mod, uint32_t idx,
+                                             int ix, int iy, double *at_out, bool *ray_out, bool *clamped_out) {
   ProjD o;
   project_d(sc, idx, cam, mod, o);
   const double px = ix + 0.5, py = iy + 0.5;
@@ -84,159 +103,210 @@ static __device__ __noinline__ bool pair_f64(const SceneView &sc, const CamD &ca
   return at >= kMinAlpha;
 }
 
-// Evaluate a pair in float32.  BWD additionally resolves the backward-only
-// decisions (ray branch, clamp) exactly.  Returns false if the pair does not
-// contribute.  Decisions whose float32 error bound straddles the threshold
-// are re-evaluated in float64 (pair_f64) unless HGS_FLAG_FAST.
-template <bool BWD>
-__device__ __forceinline__ bool eval_pair(const SplatRec &r, int ix, int iy, const CompositeArgs &a, PairEval &p) {
-  const float4 r0 = r.r0;
+// The float32 pair geometry.  Explicit fmaf / __fmul_rn / __fadd_rn so the
+// inline fast path and the out-of-line resolver compute identical bits.
+struct Geom {
+  float dx, dy, pxl, pyl;
+  float d, arg, S;                               // 3D: S bounds |terms| of d
+  float hu0, hu1, hu3, hv0, hv1, hv3, den, dmag;  // 2D
+  float inv_den, u, v, dray, dscr;               // 2D
+  bool ray;
+};
+
+__device__ __forceinline__ void geom_common(const SplatRec &r, int ix, int iy, Geom &g) {
   const int4 q = r.r5;
-  const uint32_t tag = __float_as_uint(r.r4.w);
-  const bool is3d = tag >> 31;
-  p.pxl = (float)(ix - q.z) + 0.5f;
-  p.pyl = (float)(iy - q.w) + 0.5f;
-  p.dx = p.pxl - r0.x;
-  p.dy = p.pyl - r0.y;
-  const bool exact = !(a.flags & HGS_FLAG_FAST);
-  bool ambiguous = false;
-  float arg = 0.f;
-  p.ray = false;
-  if (is3d) {
-    const float4 cn = r.r1;
-    const float t = cn.y * p.dx * p.dy;
-    const float d = fmaf(cn.x * p.dx, p.dx, fmaf(cn.z * p.dy, p.dy, 2.f * t));
-    p.u = p.dx;
-    p.v = p.dy;
-    arg = fmaf(d, -kHalfLog2e, r0.w);
-    // |d error| <= 16 eps S, S = a dx^2 + c dy^2 + 2|b dx dy| (>= every term)
-    const float S = d + 2.f * (fabsf(t) - t);
-    const float margin = fmaf(S, 16.f * kEps * kHalfLog2e, 1e-5f);
-    if (arg < kArgMinAlpha - margin) return false;  // cheap cull: no ex2
-    if (exact && (arg <= kArgMinAlpha + margin || (BWD && fabsf(arg - kArgClamp) <= margin))) ambiguous = true;
-  } else {
-    const float4 m1 = r.r1, m2 = r.r2;
-    const float m23 = r.r3.x;
-    // rows re-based at the anchor: hu = pxl m2 - m0', hv = pyl m2 - m1'
-    p.hu0 = fmaf(p.pxl, m2.z, -m1.x);
-    p.hu1 = fmaf(p.pxl, m2.w, -m1.y);
-    p.hu3 = fmaf(p.pxl, m23, -m1.z);
-    p.hv0 = fmaf(p.pyl, m2.z, -m1.w);
-    p.hv1 = fmaf(p.pyl, m2.w, -m2.x);
-    p.hv3 = fmaf(p.pyl, m23, -m2.y);
-    const float den = p.hu0 * p.hv1 - p.hu1 * p.hv0;
-    const float dmag = fabsf(p.hu0 * p.hv1) + fabsf(p.hu1 * p.hv0);
-    if (fabsf(den) <= fmaf(dmag, 1e-4f, (float)kDegenerateDen)) {
-      // (near-)degenerate ray/plane intersection (_blend_py.py:36-37)
-      if (!exact) {
-        if (fabsf(den) < (float)kDegenerateDen) return false;
-      } else {
-        ambiguous = true;
-      }
-    }
-    if (!ambiguous) {
-      p.inv_den = 1.f / den;
-      p.u = (p.hu1 * p.hv3 - p.hu3 * p.hv1) * p.inv_den;
-      p.v = (p.hu3 * p.hv0 - p.hu0 * p.hv3) * p.inv_den;
-      const float dray = fmaf(p.u, p.u, p.v * p.v);
-      const float dscr = (p.dx * p.dx + p.dy * p.dy) * 4.f;
-      p.ray = dray <= dscr;
-      const float d = p.ray ? dray : dscr;
-      arg = fmaf(d, -kHalfLog2e, r0.w);
-      constexpr float kCoarse = 0.05f;  // log2 units; precise bounds only inside
-      if (arg < kArgMinAlpha - kCoarse) return false;
-      const bool near = exact && (arg <= kArgMinAlpha + kCoarse ||
-                                  (BWD && (fabsf(arg - kArgClamp) <= kCoarse ||
-                                           fabsf(dray - dscr) <= 0.02f * (dray + dscr))));
-      if (near) {
-        // first-order error bounds of the float32 2x2 solve
-        const float A0 = fabsf(p.pxl * m2.z) + fabsf(m1.x), A1 = fabsf(p.pxl * m2.w) + fabsf(m1.y);
-        const float A3 = fabsf(p.pxl * m23) + fabsf(m1.z);
-        const float B0 = fabsf(p.pyl * m2.z) + fabsf(m1.w), B1 = fabsf(p.pyl * m2.w) + fabsf(m2.x);
-        const float B3 = fabsf(p.pyl * m23) + fabsf(m2.y);
-        const float ad = fabsf(den);
-        const float dden = 6.f * kEps * (A0 * B1 + A1 * B0);
-        const float du = (6.f * kEps * (A1 * B3 + A3 * B1) + fabsf(p.u) * dden) / ad + 4.f * kEps * fabsf(p.u);
-        const float dv = (6.f * kEps * (A3 * B0 + A0 * B3) + fabsf(p.v) * dden) / ad + 4.f * kEps * fabsf(p.v);
-        const float e_ray = 2.f * (fabsf(p.u) * du + fabsf(p.v) * dv) + 4.f * kEps * dray;
-        const float e_scr = 8.f * kEps * dscr + 1e-6f * (fabsf(p.dx) + fabsf(p.dy));
-        const float margin = fmaf(p.ray ? e_ray : e_scr, kHalfLog2e, 1e-5f);
-        if (arg < kArgMinAlpha - margin) return false;
-        if (arg <= kArgMinAlpha + margin) ambiguous = true;
-        if (BWD && (fabsf(arg - kArgClamp) <= margin || fabsf(dray - dscr) <= e_ray + e_scr)) ambiguous = true;
+  g.pxl = __fadd_rn((float)(ix - q.z), 0.5f);
+  g.pyl = __fadd_rn((float)(iy - q.w), 0.5f);
+  g.dx = __fsub_rn(g.pxl, r.r0.x);
+  g.dy = __fsub_rn(g.pyl, r.r0.y);
+}
+
+__device__ __forceinline__ void geom_3d(const SplatRec &r, Geom &g) {
+  const float4 cn = r.r1;
+  const float t = __fmul_rn(__fmul_rn(cn.y, g.dx), g.dy);
+  g.d = fmaf(__fmul_rn(cn.x, g.dx), g.dx, fmaf(__fmul_rn(cn.z, g.dy), g.dy, __fmul_rn(2.f, t)));
+  g.arg = fmaf(g.d, -kHalfLog2e, r.r0.w);
+  g.S = __fadd_rn(g.d, __fmul_rn(2.f, __fsub_rn(fabsf(t), t)));
+}
+
+__device__ __forceinline__ void geom_2d_rows(const SplatRec &r, Geom &g) {
+  const float4 m1 = r.r1, m2 = r.r2;
+  const float m23 = r.r3.x;
+  // rows re-based at the anchor: hu = pxl m2 - m0', hv = pyl m2 - m1'
+  g.hu0 = fmaf(g.pxl, m2.z, -m1.x);
+  g.hu1 = fmaf(g.pxl, m2.w, -m1.y);
+  g.hu3 = fmaf(g.pxl, m23, -m1.z);
+  g.hv0 = fmaf(g.pyl, m2.z, -m1.w);
+  g.hv1 = fmaf(g.pyl, m2.w, -m2.x);
+  g.hv3 = fmaf(g.pyl, m23, -m2.y);
+  const float a = __fmul_rn(g.hu0, g.hv1), b = __fmul_rn(g.hu1, g.hv0);
+  g.den = __fsub_rn(a, b);
+  g.dmag = __fadd_rn(fabsf(a), fabsf(b));
+}
+
+__device__ __forceinline__ void geom_2d_solve(const SplatRec &r, Geom &g) {
+  g.inv_den = __frcp_rn(g.den);
+  g.u = __fmul_rn(__fsub_rn(__fmul_rn(g.hu1, g.hv3), __fmul_rn(g.hu3, g.hv1)), g.inv_den);
+  g.v = __fmul_rn(__fsub_rn(__fmul_rn(g.hu3, g.hv0), __fmul_rn(g.hu0, g.hv3)), g.inv_den);
+  g.dray = fmaf(g.u, g.u, __fmul_rn(g.v, g.v));
+  g.dscr = __fmul_rn(fmaf(g.dx, g.dx, __fmul_rn(g.dy, g.dy)), 4.f);
+  g.ray = g.dray <= g.dscr;
+  g.d = g.ray ? g.dray : g.dscr;
+  g.arg = fmaf(g.d, -kHalfLog2e, r.r0.w);
+}
+
+__device__ __forceinline__ bool near_degenerate(const Geom &g) {
+  return fabsf(g.den) <= fmaf(g.dmag, 1e-4f, (float)kDegenerateDen);
+}
+
+// Outcome of the out-of-line resolver.
+struct Resolved {
+  float at;
+  uint32_t flags;  // bit0 contributes, bit1 clamped, bit2 ray branch
+};
+
+// Out-of-line: exact decisions for a pair the fast path found ambiguous.
+// 2D pairs first get a first-order float32 error bound of the 2x2 solve;
+// anything still ambiguous is re-evaluated in float64 (pair_f64).
+static __device__ __noinline__ Resolved resolve_pair(const SplatRec *rp, int ix, int iy, FrameState *st, bool bwd) {
+  const SplatRec r = *rp;
+  Geom g;
+  geom_common(r, ix, iy, g);
+  bool amb = true;
+  Resolved out{0.f, 0u};
+  if (!rec_is3d(r)) {
+    geom_2d_rows(r, g);
+    if (!near_degenerate(g)) {
+      geom_2d_solve(r, g);
+      const float4 m1 = r.r1, m2 = r.r2;
+      const float m23 = r.r3.x;
+      const float A0 = fabsf(g.pxl * m2.z) + fabsf(m1.x), A1 = fabsf(g.pxl * m2.w) + fabsf(m1.y);
+      const float A3 = fabsf(g.pxl * m23) + fabsf(m1.z);
+      const float B0 = fabsf(g.pyl * m2.z) + fabsf(m1.w), B1 = fabsf(g.pyl * m2.w) + fabsf(m2.x);
+      const float B3 = fabsf(g.pyl * m23) + fabsf(m2.y);
+      const float ad = fabsf(g.den);
+      const float dden = 6.f * kEps * (A0 * B1 + A1 * B0);
+      const float du = (6.f * kEps * (A1 * B3 + A3 * B1) + fabsf(g.u) * dden) / ad + 4.f * kEps * fabsf(g.u);
+      const float dv = (6.f * kEps * (A3 * B0 + A0 * B3) + fabsf(g.v) * dden) / ad + 4.f * kEps * fabsf(g.v);
+      const float e_ray = 2.f * (fabsf(g.u) * du + fabsf(g.v) * dv) + 4.f * kEps * g.dray;
+      const float e_scr = 8.f * kEps * g.dscr + 1e-6f * (fabsf(g.dx) + fabsf(g.dy));
+      const float margin = fmaf(g.ray ? e_ray : e_scr, kHalfLog2e, 1e-5f);
+      const bool deg_ok = ad > (float)kDegenerateDen + dden;
+      if (deg_ok && margin < kCoarse2D) {
+        if (g.arg < kArgMinAlpha - margin) return out;  // skip
+        amb = g.arg <= kArgMinAlpha + margin;
+        if (bwd && (fabsf(g.arg - kArgClamp) <= margin || fabsf(g.dray - g.dscr) <= e_ray + e_scr)) amb = true;
+        if (!amb) {
+          const bool cl = g.arg > kArgClamp;
+          out.at = cl ? 0.99f : ex2_approx(g.arg);
+          out.flags = 1u | (cl ? 2u : 0u) | (g.ray ? 4u : 0u);
+          return out;
+        }
       }
     }
   }
-  if (ambiguous) {
-    double at64;
-    bool ray64, cl64;
-    atomicAdd(&a.st->diag[0], 1ull);
-    if (!pair_f64(a.sc, a.cam, a.mod, tag & 0x7fffffffu, ix, iy, &at64, &ray64, &cl64)) return false;
-    p.at = (float)at64;
-    p.clamped = cl64;
-    if (!is3d) {
-      p.ray = ray64;
-      const float den = p.hu0 * p.hv1 - p.hu1 * p.hv0;
-      p.inv_den = 1.f / den;
-      p.u = (p.hu1 * p.hv3 - p.hu3 * p.hv1) * p.inv_den;
-      p.v = (p.hu3 * p.hv0 - p.hu0 * p.hv3) * p.inv_den;
+  atomicAdd(&st->diag[0], 1ull);
+  double at64;
+  bool ray64, cl64;
+  if (!pair_f64(st->sc, st->cam, st->mod, rec_idx(r), ix, iy, &at64, &ray64, &cl64)) return out;
+  out.at = (float)at64;
+  out.flags = 1u | (cl64 ? 2u : 0u) | (ray64 ? 4u : 0u);
+  return out;
+}
+
+// Evaluate a pair in float32 (fast path inline).  BWD additionally needs the
+// backward-only decisions (ray branch, clamp) exactly and the 2D solve
+// quantities.  Returns false if the pair does not contribute.
+template <bool BWD>
+__device__ __forceinline__ bool eval_pair(const SplatRec &r, const SplatRec *rp, int ix, int iy, uint32_t flags,
+                                          FrameState *st, PairEval &p) {
+  Geom g;
+  geom_common(r, ix, iy, g);
+  p.dx = g.dx;
+  p.dy = g.dy;
+  p.pxl = g.pxl;
+  p.pyl = g.pyl;
+  const bool exact = !(flags & HGS_FLAG_FAST);
+  bool amb = false;
+  p.ray = false;
+  if (rec_is3d(r)) {
+    geom_3d(r, g);
+    p.u = g.dx;
+    p.v = g.dy;
+    // |d error| <= 16 eps S, S = a dx^2 + c dy^2 + 2|b dx dy| (>= every term)
+    const float margin = fmaf(g.S, 16.f * kEps * kHalfLog2e, 1e-5f);
+    if (g.arg < kArgMinAlpha - margin) return false;  // cheap cull: no ex2
+    if (exact && (g.arg <= kArgMinAlpha + margin || (BWD && fabsf(g.arg - kArgClamp) <= margin))) amb = true;
+  } else {
+    geom_2d_rows(r, g);
+    if (near_degenerate(g)) {  // (near-)degenerate ray/plane intersection (_blend_py.py:36-37)
+      if (!exact) {
+        if (fabsf(g.den) < (float)kDegenerateDen) return false;
+      } else {
+        amb = true;
+      }
     }
+    if (!amb) {
+      geom_2d_solve(r, g);
+      if (g.arg < kArgMinAlpha - kCoarse2D) return false;
+      if (exact && (g.arg <= kArgMinAlpha + kCoarse2D ||
+                    (BWD && (fabsf(g.arg - kArgClamp) <= kCoarse2D ||
+                             fabsf(g.dray - g.dscr) <= 0.02f * (g.dray + g.dscr)))))
+        amb = true;
+      p.ray = g.ray;
+    }
+    if (BWD) {
+      p.hu0 = g.hu0; p.hu1 = g.hu1; p.hu3 = g.hu3;
+      p.hv0 = g.hv0; p.hv1 = g.hv1; p.hv3 = g.hv3;
+      if (amb && near_degenerate(g)) geom_2d_solve(r, g);
+      p.inv_den = g.inv_den;
+      p.u = g.u;
+      p.v = g.v;
+    }
+  }
+  if (amb) {
+    const Resolved rs = resolve_pair(rp, ix, iy, st, BWD);
+    if (!(rs.flags & 1u)) return false;
+    p.at = rs.at;
+    p.clamped = rs.flags & 2u;
+    p.ray = rs.flags & 4u;
     return true;
   }
-  p.clamped = arg > kArgClamp;
-  p.at = p.clamped ? 0.99f : ex2_approx(arg);
+  p.clamped = g.arg > kArgClamp;
+  p.at = p.clamped ? 0.99f : ex2_approx(g.arg);
   return true;
 }
 
-// Early-stop decision T < 1e-4 (_blend_py.py:111-113).  Near the threshold
-// the pixel's transmittance is replayed in float64 over the tile list.
-static __device__ __noinline__ bool replay_T_below(const CompositeArgs &a, int64_t lo, int64_t upto, int ix, int iy,
-                                            bool naive) {
-  atomicAdd(&a.st->diag[1], 1ull);
+// Early-stop decision T < 1e-4 (_blend_py.py:111-113).  Near the threshold the
+// pixel's transmittance is replayed in float64 over its tile list.
+static __device__ __noinline__ bool replay_T_below(const SplatRec *recs, const uint32_t *tile_vals, uint32_t flags,
+                                                   FrameState *st, int64_t lo, int64_t upto, int ix, int iy) {
+  atomicAdd(&st->diag[1], 1ull);
+  const bool naive = flags & HGS_FLAG_NAIVE;
   double T = 1.0;
   for (int64_t j = lo; j <= upto; ++j) {
-    uint32_t rk = naive ? (uint32_t)j : a.tile_vals[j];
-    const SplatRec r = a.recs[rk];
-    if (!naive) {
-      const int4 q = r.r5;
-      const int x0 = q.x & 0xffff, y0 = (int)((uint32_t)q.x >> 16);
-      const int x1 = q.y & 0xffff, y1 = (int)((uint32_t)q.y >> 16);
-      if (ix < x0 || ix > x1 || iy < y0 || iy > y1) continue;
-    }
+    const uint32_t rk = naive ? (uint32_t)j : tile_vals[j];
+    const SplatRec r = recs[rk];
+    if (!naive && !in_bbox(r.r5, ix, iy)) continue;
     PairEval p;
-    if (!eval_pair<false>(r, ix, iy, a, p)) continue;
+    if (!eval_pair<false>(r, recs + rk, ix, iy, flags, st, p)) continue;
     double at64;
     bool ray64, cl64;
-    if (!pair_f64(a.sc, a.cam, a.mod, __float_as_uint(r.r4.w) & 0x7fffffffu, ix, iy, &at64, &ray64, &cl64))
-      continue;
+    if (!pair_f64(st->sc, st->cam, st->mod, rec_idx(r), ix, iy, &at64, &ray64, &cl64)) continue;
     T *= 1.0 - at64;
   }
   return T < kEarlyStopT;
 }
 
-struct FwdGuard {
-  const CompositeArgs &a;
-  int ix, iy;
-  bool exact, naive;
-  __device__ FwdGuard(const CompositeArgs &a_, int ix_, int iy_)
-      : a(a_), ix(ix_), iy(iy_), exact(!(a_.flags & HGS_FLAG_FAST)), naive(a_.flags & HGS_FLAG_NAIVE) {}
-  // Tn = transmittance after the splat at tile-list entry e.
-  __device__ __forceinline__ bool early_stop(float Tn, float Tprev, int64_t lo, int64_t e) const {
-    const float thr = (float)kEarlyStopT;
-    if (exact && fabsf(Tn - thr) <= 2e-5f * thr) return replay_T_below(a, lo, e, ix, iy, naive);
-    return Tn < thr;
-  }
-};
-
-__device__ __forceinline__ bool eval_alpha(const SplatRec &r, int ix, int iy, const FwdGuard &g, float &at) {
-  PairEval p;
-  if (!eval_pair<false>(r, ix, iy, g.a, p)) return false;
-  at = p.at;
-  return true;
+__device__ __forceinline__ bool early_stop(float Tn, const CompositeArgs &a, int64_t lo, int64_t e, int ix, int iy) {
+  const float thr = (float)kEarlyStopT;
+  if (!(a.flags & HGS_FLAG_FAST) && fabsf(Tn - thr) <= 2e-5f * thr)
+    return replay_T_below(a.recs, a.tile_vals, a.flags, a.st, lo, e, ix, iy);
+  return Tn < thr;
 }
 
 struct BwdArgs {
-  CompositeArgs c;          // recs, tile lists, flags, bg, scene / camera for f64 checks
+  CompositeArgs c;          // recs, tile lists, flags, bg, state
   const float *pix_grad;    // (KG, H, W, 3)
   const float *depth_grad;  // (KG, H, W) or null
   const float *normal_grad; // (KG, H, W, 3) or null
@@ -262,6 +332,7 @@ struct ExchangeState {
 };
 
 // kernels (defined in hgs_forward.cu / hgs_backward.cu / hgs_exchange.cu)
+__global__ void k_init_state(SceneView sc, CamD cam, ModD mod, FrameState *st);
 __global__ void k_depth_keys(SceneView sc, CamD cam, unsigned long long *keys, uint32_t *vals, uint32_t *hist,
                              FrameState *st);
 __global__ void k_preprocess(SceneView sc, CamD cam, ModD mod, const uint32_t *sorted_idx, int64_t m, SplatRec *recs,
@@ -269,7 +340,7 @@ __global__ void k_preprocess(SceneView sc, CamD cam, ModD mod, const uint32_t *s
 __global__ void k_duplicate(const SplatRec *recs, const unsigned long long *pair_off, int64_t m, int tiles_x,
                             uint32_t *pkeys, uint32_t *pvals, int n_digits, uint32_t *hist);
 __global__ void k_tile_ranges(const uint32_t *skeys, int64_t k, int64_t n_tiles, uint32_t *tile_off);
-template <bool NAIVE>
+template <bool NAIVE, bool COUNT>
 __global__ void k_composite_fwd(CompositeArgs a);
 template <int KG, bool EXT>
 __global__ void k_composite_bwd(BwdArgs b);

@@ -114,9 +114,10 @@ def _as_device(a, dev, name, shape):
 
 
 def backward_device(frame, pixel_grads, depth_grads=None, normal_grads=None, alpha_grads=None,
-                    grads_out=None, touched_out=None):
+                    grads_out=None, touched_out=None, events=None, flags=None, scratch=None):
     """Device-level backward.  pixel_grads (KG,H,W,3) float32 CUDA; returns
-    (grads (KG, n*P) float32, touched (n,) uint8)."""
+    (grads (KG, n*P) float32, touched (n,) uint8).  ``events`` (3
+    torch.cuda.Event) are recorded at the library's stage boundaries."""
     import torch
     L = _lib.lib()
     ds = frame.scene
@@ -129,10 +130,12 @@ def backward_device(frame, pixel_grads, depth_grads=None, normal_grads=None, alp
     if touched_out is None:
         touched_out = torch.empty(max(n, 1), dtype=torch.uint8, device=dev)
     nscr = L.hgs_backward_scratch_bytes(n, kg)
-    scratch = torch.empty(nscr, dtype=torch.uint8, device=dev)
+    if scratch is None or scratch.numel() < nscr:
+        scratch = torch.empty(nscr, dtype=torch.uint8, device=dev)
+    fl = frame.flags if flags is None else flags
     _lib.check(L.hgs_backward(
         _lib.scene_struct(ds), _lib.camera_struct(frame.camera),
-        _lib.settings_struct(frame.settings, frame.flags), _lib.ptr(frame.buf), frame.info, kg,
+        _lib.settings_struct(frame.settings, fl, events), _lib.ptr(frame.buf), frame.info, kg,
         _lib.ptr(pixel_grads), _lib.ptr(depth_grads), _lib.ptr(normal_grads),
         _lib.ptr(alpha_grads), _lib.ptr(scratch), nscr, _lib.ptr(grads_out), _lib.ptr(touched_out),
         _lib.current_stream_handle(dev)), "hgs_backward")

@@ -233,11 +233,12 @@ def _check_camera(camera):
         raise ConfigError("image dimensions above 65535 are not supported")
 
 
-def rasterize(ds, camera, settings, flags=0, outputs=None):
+def rasterize(ds, camera, settings, flags=0, outputs=None, events=None):
     """Device-level forward: DeviceGaussians -> (images dict, SplatFrame).
 
     ``outputs`` may pass preallocated image tensors (keys color, depth,
-    transmittance, alpha, normal) to avoid per-frame allocation."""
+    transmittance, alpha, normal) to avoid per-frame allocation; ``events``
+    (5 torch.cuda.Event) are recorded at the library's stage boundaries."""
     import torch
     L = _lib.lib()
     _check_camera(camera)
@@ -257,7 +258,7 @@ def rasterize(ds, camera, settings, flags=0, outputs=None):
                          ("color", "depth", "transmittance", "alpha", "normal")))
     sc = _lib.scene_struct(ds)
     cam = _lib.camera_struct(camera)
-    st = _lib.settings_struct(settings, flags)
+    st = _lib.settings_struct(settings, flags, events)
     stream = _lib.current_stream_handle(dev)
     key = (n, W, H)
     cap = _pair_hint.get(key, max(8 * n, 1 << 16))
