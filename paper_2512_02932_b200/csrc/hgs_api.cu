@@ -384,8 +384,6 @@ int hgs_backward(const hgs_scene *scene, const hgs_camera *camera, const hgs_set
   const int64_t nn = std::max<int64_t>(n, 1);
   float *acc = static_cast<float *>(scratch);
   float *acc_ext = reinterpret_cast<float *>(static_cast<char *>(scratch) + ((nn * kc_max * 16 * 4 + 255) & ~255ll));
-  uint8_t *touched_rank = reinterpret_cast<uint8_t *>(reinterpret_cast<char *>(acc_ext) +
-                                                      ((nn * kc_max * 4 * 4 + 255) & ~255ll));
   HGS_CUDA(record_event(settings, 0, s));
   HGS_CUDA(cudaMemsetAsync(touched, 0, (size_t)nn, s));
   BwdArgs b;
@@ -401,14 +399,13 @@ int hgs_backward(const hgs_scene *scene, const hgs_camera *camera, const hgs_set
     const int kc = std::min(4, kg - k0);
     HGS_CUDA(cudaMemsetAsync(acc, 0, (size_t)nn * kc * 16 * 4, s));
     if (ext) HGS_CUDA(cudaMemsetAsync(acc_ext, 0, (size_t)nn * kc * 4 * 4, s));
-    HGS_CUDA(cudaMemsetAsync(touched_rank, 0, (size_t)std::max<int64_t>(m, 1), s));
     b.pix_grad = pixel_grads + (int64_t)k0 * HW * 3;
     b.depth_grad = depth_grads ? depth_grads + (int64_t)k0 * HW : nullptr;
     b.normal_grad = normal_grads ? normal_grads + (int64_t)k0 * HW * 3 : nullptr;
     b.alpha_grad = alpha_grads ? alpha_grads + (int64_t)k0 * HW : nullptr;
     b.acc = acc;
     b.acc_ext = ext ? acc_ext : nullptr;
-    b.touched_rank = touched_rank;
+    b.touched = touched;
     if (m > 0) {
       switch (kc) {
         case 1: launch_bwd<1>(b, info->n_tiles, ext, s); break;
@@ -418,10 +415,6 @@ int hgs_backward(const hgs_scene *scene, const hgs_camera *camera, const hgs_set
       }
       HGS_LAUNCHED();
       if (k0 == 0) HGS_CUDA(record_event(settings, 1, s));
-      if (k0 == 0) {
-        k_touched_scatter<<<grid_for(m, 256), 256, 0, s>>>(b.c.recs, touched_rank, m, touched);
-        HGS_LAUNCHED();
-      }
     }
     ChainArgs c = c0;
     c.kg = kc;

@@ -75,20 +75,19 @@ __global__ void __launch_bounds__(kBlock, 2) k_composite_bwd(BwdArgs b) {
   const int64_t lo = naive ? 0 : (int64_t)a.tile_off[tile];
   const int64_t HW = (int64_t)a.width * a.height;
   const int64_t pix = (int64_t)iy * a.width + ix;
+  __shared__ float s_park[8][kBlock];
   uint32_t last = 0;
   float T_fin = 1.f;
   float gp[KG][3], gd[KG], gn[KG][3], ga[KG];
-#pragma unroll
-  for (int k = 0; k < KG; ++k) {
-    gp[k][0] = gp[k][1] = gp[k][2] = 0.f;
-    gd[k] = ga[k] = 0.f;
-    gn[k][0] = gn[k][1] = gn[k][2] = 0.f;
-  }
-  if (inside) {
-    last = a.pix_last[pix];
-    T_fin = a.pix_T[pix];
+  // upstream gradients of this pixel (reloaded after out-of-line calls so
+  // they are never live across one)
+  auto load_grads = [&]() {
 #pragma unroll
     for (int k = 0; k < KG; ++k) {
+      gp[k][0] = gp[k][1] = gp[k][2] = 0.f;
+      gd[k] = ga[k] = 0.f;
+      gn[k][0] = gn[k][1] = gn[k][2] = 0.f;
+      if (!inside) continue;
       const float *g = b.pix_grad + ((int64_t)k * HW + pix) * 3;
       gp[k][0] = g[0]; gp[k][1] = g[1]; gp[k][2] = g[2];
       if (EXT) {
@@ -100,6 +99,11 @@ __global__ void __launch_bounds__(kBlock, 2) k_composite_bwd(BwdArgs b) {
         }
       }
     }
+  };
+  load_grads();
+  if (inside) {
+    last = a.pix_last[pix];
+    T_fin = a.pix_T[pix];
   }
   if (threadIdx.x == 0) s_max_last = 0;
   __syncthreads();
@@ -145,8 +149,24 @@ __global__ void __launch_bounds__(kBlock, 2) k_composite_bwd(BwdArgs b) {
         if (act && !naive) act = in_bbox(r.r5, ix, iy);
         PairEval p;
         if (count && act) ++n_ev;
-        const uint32_t rk = naive ? (uint32_t)j : a.tile_vals[j];
-        if (act) act = eval_pair<true>(r, a.recs + rk, ix, iy, a.flags, a.st, p);
+        const int c = act ? eval_fast<true>(r, ix, iy, a.flags, p) : kSkip;
+        if (c == kAmbiguous) {
+          // rare: park the per-pixel state in shared memory, resolve out of
+          // line, reload (nothing accumulated stays live across the call)
+          s_park[0][threadIdx.x] = T_run; s_park[1][threadIdx.x] = S0;
+          s_park[2][threadIdx.x] = S1; s_park[3][threadIdx.x] = S2;
+          s_park[4][threadIdx.x] = SD; s_park[5][threadIdx.x] = SN0;
+          s_park[6][threadIdx.x] = SN1; s_park[7][threadIdx.x] = SN2;
+          const Resolved rs = resolve_pair(&s_rec[e], ix, iy, a.st, true);
+          T_run = s_park[0][threadIdx.x]; S0 = s_park[1][threadIdx.x];
+          S1 = s_park[2][threadIdx.x]; S2 = s_park[3][threadIdx.x];
+          SD = s_park[4][threadIdx.x]; SN0 = s_park[5][threadIdx.x];
+          SN1 = s_park[6][threadIdx.x]; SN2 = s_park[7][threadIdx.x];
+          load_grads();
+          act = finish_resolved(rs, p);
+        } else {
+          act = c == kContrib;
+        }
         if (!__any_sync(0xffffffffu, act)) continue;
         const bool is3d = rec_is3d(r);
         const uint32_t gidx = rec_idx(r);
@@ -231,7 +251,7 @@ __global__ void __launch_bounds__(kBlock, 2) k_composite_bwd(BwdArgs b) {
             SN2 = fmaf(c4.z, w, SN2);
           }
         }
-        if (lane == 0) b.touched_rank[rk] = 1;
+        if (lane == 0) b.touched[gidx] = 1;
 #pragma unroll
         for (int k = 0; k < KG; ++k) {
           const float tot = warp_transpose_reduce16(v[k], lane);

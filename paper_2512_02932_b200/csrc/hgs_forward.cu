@@ -4,6 +4,10 @@
 // raster/_blend_py.py:55-123 (paths relative to the reference package).
 #include "hgs_kernels.cuh"
 
+#ifndef HGS_FWD_MINB
+#define HGS_FWD_MINB 2  // CTAs per SM the forward compositor is register-budgeted for
+#endif
+
 namespace hgs {
 
 __global__ void k_init_state(SceneView sc, CamD cam, ModD mod, FrameState *st) {
@@ -190,9 +194,29 @@ __global__ void k_tile_ranges(const uint32_t *__restrict__ skeys, int64_t k, int
 // culls the batch against its 8 x 4 block (one rect test per lane, ballot),
 // then walks only the relevant splats, in order; all lanes of the warp see
 // the same splat, so the 2D / 3D branch is warp-uniform.
+#define PARK_STATE()                                                                   \
+  do {                                                                                 \
+    s_park[0][threadIdx.x] = T; s_park[1][threadIdx.x] = cr;                           \
+    s_park[2][threadIdx.x] = cg; s_park[3][threadIdx.x] = cb;                          \
+    s_park[4][threadIdx.x] = dep; s_park[5][threadIdx.x] = n0;                         \
+    s_park[6][threadIdx.x] = n1; s_park[7][threadIdx.x] = n2;                          \
+    s_park[8][threadIdx.x] = __uint_as_float(cnt);                                     \
+    s_park[9][threadIdx.x] = __uint_as_float(last);                                    \
+  } while (0)
+#define UNPARK_STATE()                                                                 \
+  do {                                                                                 \
+    T = s_park[0][threadIdx.x]; cr = s_park[1][threadIdx.x];                           \
+    cg = s_park[2][threadIdx.x]; cb = s_park[3][threadIdx.x];                          \
+    dep = s_park[4][threadIdx.x]; n0 = s_park[5][threadIdx.x];                         \
+    n1 = s_park[6][threadIdx.x]; n2 = s_park[7][threadIdx.x];                          \
+    cnt = __float_as_uint(s_park[8][threadIdx.x]);                                     \
+    last = __float_as_uint(s_park[9][threadIdx.x]);                                    \
+  } while (0)
+
 template <bool NAIVE, bool COUNT>
-__global__ void __launch_bounds__(kBlock, 3) k_composite_fwd(CompositeArgs a) {
+__global__ void __launch_bounds__(kBlock, HGS_FWD_MINB) k_composite_fwd(CompositeArgs a) {
   __shared__ SplatRec s_rec[kBlock];
+  __shared__ float s_park[10][kBlock];
   const int tile = blockIdx.x;
   const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -234,8 +258,16 @@ __global__ void __launch_bounds__(kBlock, 3) k_composite_fwd(CompositeArgs a) {
         const bool is3d = rec_is3d(r);
         if (COUNT) (is3d ? n_ev3 : n_ev2) += 1;
         PairEval p;
-        const uint32_t rk = NAIVE ? (uint32_t)(base + e) : a.tile_vals[base + e];
-        if (!eval_pair<false>(r, a.recs + rk, ix, iy, a.flags, a.st, p)) continue;
+        int c = eval_fast<false>(r, ix, iy, a.flags, p);
+        if (c == kAmbiguous) {
+          // rare: park the loop-carried state in shared memory so nothing
+          // accumulated is live across the out-of-line call
+          PARK_STATE();
+          const Resolved rs = resolve_pair(&s_rec[e], ix, iy, a.st, false);
+          UNPARK_STATE();
+          c = finish_resolved(rs, p) ? kContrib : kSkip;
+        }
+        if (c == kSkip) continue;
         if (COUNT) (is3d ? n_c3 : n_c2) += 1;
         const float at = p.at;
         const float w = at * T;
@@ -250,8 +282,17 @@ __global__ void __launch_bounds__(kBlock, 3) k_composite_fwd(CompositeArgs a) {
         ++cnt;
         last = (uint32_t)(base + e - lo) + 1u;
         const float Tn = T * (1.f - at);
-        if (early_stop(Tn, a, lo, base + e, ix, iy)) done = true;
-        T = Tn;
+        bool stop;
+        if (!(a.flags & HGS_FLAG_FAST) && fabsf(Tn - (float)kEarlyStopT) <= 2e-5f * (float)kEarlyStopT) {
+          T = Tn;
+          PARK_STATE();
+          stop = replay_T_below(a.recs, a.tile_vals, a.flags, a.st, lo, base + e, ix, iy);
+          UNPARK_STATE();
+        } else {
+          stop = Tn < (float)kEarlyStopT;
+          T = Tn;
+        }
+        if (stop) done = true;
       }
     }
     if (__syncthreads_count(done) == kBlock) break;

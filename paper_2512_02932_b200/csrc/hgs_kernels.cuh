@@ -145,7 +145,7 @@ __device__ __forceinline__ void geom_2d_rows(const SplatRec &r, Geom &g) {
 }
 
 __device__ __forceinline__ void geom_2d_solve(const SplatRec &r, Geom &g) {
-  g.inv_den = __frcp_rn(g.den);
+  g.inv_den = rcp_approx(g.den);  // MUFU.RCP: no out-of-line slow path in the hot loop
   g.u = __fmul_rn(__fsub_rn(__fmul_rn(g.hu1, g.hv3), __fmul_rn(g.hu3, g.hv1)), g.inv_den);
   g.v = __fmul_rn(__fsub_rn(__fmul_rn(g.hu3, g.hv0), __fmul_rn(g.hu0, g.hv3)), g.inv_den);
   g.dray = fmaf(g.u, g.u, __fmul_rn(g.v, g.v));
@@ -214,12 +214,14 @@ static __device__ __noinline__ Resolved resolve_pair(const SplatRec *rp, int ix,
   return out;
 }
 
-// Evaluate a pair in float32 (fast path inline).  BWD additionally needs the
-// backward-only decisions (ray branch, clamp) exactly and the 2D solve
-// quantities.  Returns false if the pair does not contribute.
+enum : int { kSkip = 0, kContrib = 1, kAmbiguous = 2 };
+
+// Evaluate a pair in float32 (fast path, no calls).  BWD additionally needs
+// the backward-only decisions (ray branch, clamp) and the 2D solve
+// quantities.  Returns kSkip, kContrib, or kAmbiguous -- the caller then runs
+// resolve_pair (out of line) and applies finish_resolved.
 template <bool BWD>
-__device__ __forceinline__ bool eval_pair(const SplatRec &r, const SplatRec *rp, int ix, int iy, uint32_t flags,
-                                          FrameState *st, PairEval &p) {
+__device__ __forceinline__ int eval_fast(const SplatRec &r, int ix, int iy, uint32_t flags, PairEval &p) {
   Geom g;
   geom_common(r, ix, iy, g);
   p.dx = g.dx;
@@ -235,20 +237,20 @@ __device__ __forceinline__ bool eval_pair(const SplatRec &r, const SplatRec *rp,
     p.v = g.dy;
     // |d error| <= 16 eps S, S = a dx^2 + c dy^2 + 2|b dx dy| (>= every term)
     const float margin = fmaf(g.S, 16.f * kEps * kHalfLog2e, 1e-5f);
-    if (g.arg < kArgMinAlpha - margin) return false;  // cheap cull: no ex2
+    if (g.arg < kArgMinAlpha - margin) return kSkip;  // cheap cull: no ex2
     if (exact && (g.arg <= kArgMinAlpha + margin || (BWD && fabsf(g.arg - kArgClamp) <= margin))) amb = true;
   } else {
     geom_2d_rows(r, g);
     if (near_degenerate(g)) {  // (near-)degenerate ray/plane intersection (_blend_py.py:36-37)
       if (!exact) {
-        if (fabsf(g.den) < (float)kDegenerateDen) return false;
+        if (fabsf(g.den) < (float)kDegenerateDen) return kSkip;
       } else {
         amb = true;
       }
     }
     if (!amb) {
       geom_2d_solve(r, g);
-      if (g.arg < kArgMinAlpha - kCoarse2D) return false;
+      if (g.arg < kArgMinAlpha - kCoarse2D) return kSkip;
       if (exact && (g.arg <= kArgMinAlpha + kCoarse2D ||
                     (BWD && (fabsf(g.arg - kArgClamp) <= kCoarse2D ||
                              fabsf(g.dray - g.dscr) <= 0.02f * (g.dray + g.dscr)))))
@@ -264,17 +266,27 @@ __device__ __forceinline__ bool eval_pair(const SplatRec &r, const SplatRec *rp,
       p.v = g.v;
     }
   }
-  if (amb) {
-    const Resolved rs = resolve_pair(rp, ix, iy, st, BWD);
-    if (!(rs.flags & 1u)) return false;
-    p.at = rs.at;
-    p.clamped = rs.flags & 2u;
-    p.ray = rs.flags & 4u;
-    return true;
-  }
+  if (amb) return kAmbiguous;
   p.clamped = g.arg > kArgClamp;
   p.at = p.clamped ? 0.99f : ex2_approx(g.arg);
+  return kContrib;
+}
+
+__device__ __forceinline__ bool finish_resolved(const Resolved rs, PairEval &p) {
+  if (!(rs.flags & 1u)) return false;
+  p.at = rs.at;
+  p.clamped = rs.flags & 2u;
+  p.ray = rs.flags & 4u;
   return true;
+}
+
+// Convenience form with the call inline (used off the hot loops).
+template <bool BWD>
+__device__ __forceinline__ bool eval_pair(const SplatRec &r, const SplatRec *rp, int ix, int iy, uint32_t flags,
+                                          FrameState *st, PairEval &p) {
+  const int c = eval_fast<BWD>(r, ix, iy, flags, p);
+  if (c != kAmbiguous) return c == kContrib;
+  return finish_resolved(resolve_pair(rp, ix, iy, st, BWD), p);
 }
 
 // Early-stop decision T < 1e-4 (_blend_py.py:111-113).  Near the threshold the
@@ -313,7 +325,7 @@ struct BwdArgs {
   const float *alpha_grad;  // (KG, H, W) or null
   float *acc;               // (n, KG, 16)
   float *acc_ext;           // (n, KG, 4) or null
-  uint8_t *touched_rank;    // (m)
+  uint8_t *touched;         // (n) by Gaussian index, zeroed by the caller
 };
 
 struct ChainArgs {
