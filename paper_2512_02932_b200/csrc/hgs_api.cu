@@ -373,7 +373,7 @@ int hgs_backward(const hgs_scene *scene, const hgs_camera *camera, const hgs_set
   if (rc) return rc;
   rc = check_frame(scene, camera, info);
   if (rc) return rc;
-  if (kg < 1 || !pixel_grads || !grads || !touched) return HGS_ERR_CONFIG;
+  if (kg < 1 || !pixel_grads || (scene->n > 0 && (!grads || !touched))) return HGS_ERR_CONFIG;
   if (scratch_bytes < hgs_backward_scratch_bytes(scene->n, kg)) return HGS_ERR_CONFIG;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int64_t n = scene->n, m = info->m;

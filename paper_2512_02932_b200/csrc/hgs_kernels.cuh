@@ -236,7 +236,7 @@ __device__ __forceinline__ int eval_fast(const SplatRec &r, int ix, int iy, uint
     p.u = g.dx;
     p.v = g.dy;
     // |d error| <= 16 eps S, S = a dx^2 + c dy^2 + 2|b dx dy| (>= every term)
-    const float margin = fmaf(g.S, 16.f * kEps * kHalfLog2e, 1e-5f);
+    const float margin = exact ? fmaf(g.S, 16.f * kEps * kHalfLog2e, 1e-5f) : 0.f;
     if (g.arg < kArgMinAlpha - margin) return kSkip;  // cheap cull: no ex2
     if (exact && (g.arg <= kArgMinAlpha + margin || (BWD && fabsf(g.arg - kArgClamp) <= margin))) amb = true;
   } else {
@@ -250,7 +250,7 @@ __device__ __forceinline__ int eval_fast(const SplatRec &r, int ix, int iy, uint
     }
     if (!amb) {
       geom_2d_solve(r, g);
-      if (g.arg < kArgMinAlpha - kCoarse2D) return kSkip;
+      if (g.arg < kArgMinAlpha - (exact ? kCoarse2D : 0.f)) return kSkip;
       if (exact && (g.arg <= kArgMinAlpha + kCoarse2D ||
                     (BWD && (fabsf(g.arg - kArgClamp) <= kCoarse2D ||
                              fabsf(g.dray - g.dscr) <= 0.02f * (g.dray + g.dscr)))))
