@@ -197,7 +197,7 @@ def main():
     import torch
     import torch.distributed as dist
 
-    from paper_2512_02932_b200 import _lib, grad, raster
+    from paper_2512_02932_b200 import _lib, grad, parallel, raster
     from paper_2512_02932_b200.core import DeviceGaussians
     from paper_2512_02932_b200.settings import RenderSettings
     from paper_2512_02932_b200.synthetic import synthetic_scene
@@ -235,7 +235,7 @@ def main():
         grad.backward_device(frame, pg, grads_out=grads_buf, touched_out=touched_buf, events=be,
                              scratch=scratch)
         if world > 1:
-            dist.all_reduce(grads_buf)
+            parallel.allreduce_grads(grads_buf)  # the multi-view gradient exchange
         return frame
 
     def fwd_only(fe=None):
