@@ -11,7 +11,7 @@ from .errors import (ConfigError, DegenerateScaleError, ExtensionError, Integrit
                      InvalidParameterError, SplatError)
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libhgs.so")
+LIB_PATH = os.environ.get("HGS_LIB", os.path.join(_HERE, "libhgs.so"))
 
 HGS_OK = 0
 HGS_ERR_CONFIG = 1

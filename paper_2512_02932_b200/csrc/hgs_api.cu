@@ -12,10 +12,11 @@ namespace hgs {
 namespace {
 
 constexpr int kMaxGrid = 148 * 8;
+constexpr int kFixupBlocks = 148 * 4;  // persistent fixup grid (one warp per deferred pixel)
 
 struct Layout {
   size_t state, hist_d, off_d, hist_p, off_p, keys_a, keys_b, vals_a, vals_b, lb_sort, lb_scan, recs, pair_off,
-      pk_a, pk_b, pv_a, pv_b, tile_off, pix_T, pix_last, pix_count, total;
+      pk_a, pk_b, pv_a, pv_b, tile_off, pix_T, pix_last, pix_count, fwd_fix, bwd_fix, total;
   size_t small_end;  // [state, small_end) is zeroed at the start of a forward
   size_t lb_sort_bytes, lb_scan_bytes;
 };
@@ -52,6 +53,8 @@ Layout make_layout(int64_t n, int W, int H, int64_t cap) {
   L.pix_T = take((size_t)W * H * 4);
   L.pix_last = take((size_t)W * H * 4);
   L.pix_count = take((size_t)W * H * 4);
+  L.fwd_fix = take((size_t)W * H * sizeof(FwdFix));
+  L.bwd_fix = take((size_t)W * H * sizeof(BwdFix));
   L.pk_a = take(cc * 4);
   L.pk_b = take(cc * 4);
   L.pv_a = take(cc * 4);
@@ -306,11 +309,16 @@ int hgs_forward(const hgs_scene *scene, const hgs_camera *camera, const hgs_sett
   a.pix_last = at<uint32_t>(frame, L.pix_last);
   a.pix_count = at<uint32_t>(frame, L.pix_count);
   a.st = st;
+  a.fwd_fix = at<FwdFix>(frame, L.fwd_fix);
+  a.bwd_fix = at<BwdFix>(frame, L.bwd_fix);
   const bool naive = settings->flags & HGS_FLAG_NAIVE, count = settings->flags & HGS_FLAG_COUNT;
   if (naive && count) k_composite_fwd<true, true><<<(unsigned)n_tiles, kBlock, 0, s>>>(a);
   else if (naive) k_composite_fwd<true, false><<<(unsigned)n_tiles, kBlock, 0, s>>>(a);
   else if (count) k_composite_fwd<false, true><<<(unsigned)n_tiles, kBlock, 0, s>>>(a);
   else k_composite_fwd<false, false><<<(unsigned)n_tiles, kBlock, 0, s>>>(a);
+  HGS_LAUNCHED();
+  // deferred (float32-ambiguous) pixels, float64-exact; exits at once if none
+  k_fixup_fwd<<<kFixupBlocks, 256, 0, s>>>(a);
   HGS_LAUNCHED();
   HGS_CUDA(record_event(settings, 4, s));
   return HGS_OK;
@@ -333,6 +341,8 @@ static CompositeArgs composite_args_for(const hgs_scene *scene, const hgs_camera
   a.pix_last = at<uint32_t>(fr, L.pix_last);
   a.pix_count = at<uint32_t>(fr, L.pix_count);
   a.st = at<FrameState>(fr, L.state);
+  a.fwd_fix = at<FwdFix>(fr, L.fwd_fix);
+  a.bwd_fix = at<BwdFix>(fr, L.bwd_fix);
   (void)scene;
   (void)camera;
   return a;
@@ -357,10 +367,14 @@ size_t hgs_backward_scratch_bytes(int64_t n, int32_t kg) {
 
 template <int KG>
 static void launch_bwd(const BwdArgs &b, int64_t n_tiles, bool ext, cudaStream_t s) {
-  if (ext)
+  // hot replay, then the float64-exact fixup of the deferred pixels
+  if (ext) {
     k_composite_bwd<KG, true><<<(unsigned)n_tiles, kBlock, 0, s>>>(b);
-  else
+    k_fixup_bwd<KG, true><<<kFixupBlocks, 256, 0, s>>>(b);
+  } else {
     k_composite_bwd<KG, false><<<(unsigned)n_tiles, kBlock, 0, s>>>(b);
+    k_fixup_bwd<KG, false><<<kFixupBlocks, 256, 0, s>>>(b);
+  }
 }
 
 extern "C" {
@@ -398,6 +412,7 @@ int hgs_backward(const hgs_scene *scene, const hgs_camera *camera, const hgs_set
   for (int k0 = 0; k0 < kg; k0 += 4) {
     const int kc = std::min(4, kg - k0);
     HGS_CUDA(cudaMemsetAsync(acc, 0, (size_t)nn * kc * 16 * 4, s));
+    HGS_CUDA(cudaMemsetAsync(&b.c.st->n_fix_bwd, 0, sizeof(uint32_t), s));
     if (ext) HGS_CUDA(cudaMemsetAsync(acc_ext, 0, (size_t)nn * kc * 4 * 4, s));
     b.pix_grad = pixel_grads + (int64_t)k0 * HW * 3;
     b.depth_grad = depth_grads ? depth_grads + (int64_t)k0 * HW : nullptr;

@@ -8,306 +8,8 @@
 
 namespace hgs {
 
-// Screen-space accumulator slots per (Gaussian, kg), float32:
-//  0-2 colour, 3 alpha (sum d_at * at = g_alpha_eff * alpha_eff),
-//  4-5 centre (3D Mahalanobis / 2D low-pass), 6-14 geometry:
-//  3D: 6-8 = dL/dcov2d (a, b, c);  2D ray: 6-8 = dL/dM0 (cols 0,1,3),
-//  9-11 = dL/dM1, 12-14 = dL/dM3 w.r.t. anchor-relative pixels; 15 unused.
-// Extension slots (separate array, 4 per (Gaussian, kg)): z, normal xyz.
-constexpr int kAcc = 16;
+constexpr int kAcc = 16;     // accumulator slots per (Gaussian, kg): see hgs_composite_bwd.cu
 constexpr int kAccExt = 4;
-
-// Sum 16 per-lane values over the warp.  On return lane l holds the total of
-// slot ((l >> 4) & 1) * 8 + ((l >> 3) & 1) * 4 + ((l >> 2) & 1) * 2 + ((l >> 1) & 1)
-// (lanes l and l ^ 1 hold the same slot).  16 shuffles instead of 16 x 5.
-__device__ __forceinline__ float warp_transpose_reduce16(float (&v)[16], int lane) {
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const bool hi = lane & 16;
-    float send = hi ? v[i] : v[i + 8];
-    float keep = hi ? v[i + 8] : v[i];
-    v[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
-  }
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const bool hi = lane & 8;
-    float send = hi ? v[i] : v[i + 4];
-    float keep = hi ? v[i + 4] : v[i];
-    v[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
-  }
-#pragma unroll
-  for (int i = 0; i < 2; ++i) {
-    const bool hi = lane & 4;
-    float send = hi ? v[i] : v[i + 2];
-    float keep = hi ? v[i + 2] : v[i];
-    v[i] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
-  }
-  {
-    const bool hi = lane & 2;
-    float send = hi ? v[0] : v[1];
-    float keep = hi ? v[1] : v[0];
-    v[0] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
-  }
-  return v[0] + __shfl_xor_sync(0xffffffffu, v[0], 1);
-}
-
-__device__ __forceinline__ int transpose_slot(int lane) {
-  return ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 + ((lane >> 1) & 1);
-}
-
-// Back-to-front replay (_blend_py.py:149-240).  Same tiling as the forward;
-// each warp culls a batch against its 8 x 4 block and its lanes' last
-// contributor, then walks the relevant splats from the back.  Per splat the
-// 16 gradient slots are summed over the warp with the transpose reduction
-// and flushed with one 16-lane atomic instruction.
-template <int KG, bool EXT>
-__global__ void __launch_bounds__(kBlock, 2) k_composite_bwd(BwdArgs b) {
-  const CompositeArgs &a = b.c;
-  __shared__ SplatRec s_rec[kBlock];
-  __shared__ uint32_t s_max_last;
-  const int tile = blockIdx.x;
-  const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int wx0 = tx * kTile + (warp & 1) * 8, wy0 = ty * kTile + (warp >> 1) * 4;
-  const int ix = wx0 + (lane & 7), iy = wy0 + (lane >> 3);
-  const bool inside = ix < a.width && iy < a.height;
-  const bool naive = a.flags & HGS_FLAG_NAIVE;
-  const int64_t lo = naive ? 0 : (int64_t)a.tile_off[tile];
-  const int64_t HW = (int64_t)a.width * a.height;
-  const int64_t pix = (int64_t)iy * a.width + ix;
-  __shared__ float s_park[8][kBlock];
-  uint32_t last = 0;
-  float T_fin = 1.f;
-  float gp[KG][3], gd[KG], gn[KG][3], ga[KG];
-  // upstream gradients of this pixel (reloaded after out-of-line calls so
-  // they are never live across one)
-  auto load_grads = [&]() {
-#pragma unroll
-    for (int k = 0; k < KG; ++k) {
-      gp[k][0] = gp[k][1] = gp[k][2] = 0.f;
-      gd[k] = ga[k] = 0.f;
-      gn[k][0] = gn[k][1] = gn[k][2] = 0.f;
-      if (!inside) continue;
-      const float *g = b.pix_grad + ((int64_t)k * HW + pix) * 3;
-      gp[k][0] = g[0]; gp[k][1] = g[1]; gp[k][2] = g[2];
-      if (EXT) {
-        if (b.depth_grad) gd[k] = b.depth_grad[(int64_t)k * HW + pix];
-        if (b.alpha_grad) ga[k] = b.alpha_grad[(int64_t)k * HW + pix];
-        if (b.normal_grad) {
-          const float *h = b.normal_grad + ((int64_t)k * HW + pix) * 3;
-          gn[k][0] = h[0]; gn[k][1] = h[1]; gn[k][2] = h[2];
-        }
-      }
-    }
-  };
-  load_grads();
-  if (inside) {
-    last = a.pix_last[pix];
-    T_fin = a.pix_T[pix];
-  }
-  if (threadIdx.x == 0) s_max_last = 0;
-  __syncthreads();
-  uint32_t warp_last = last;
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) warp_last = max(warp_last, __shfl_xor_sync(0xffffffffu, warp_last, o));
-  if (lane == 0 && warp_last) atomicMax(&s_max_last, warp_last);
-  __syncthreads();
-  const int64_t end = lo + s_max_last;  // exclusive
-  const int64_t warp_end = lo + warp_last;
-  // suffix sums (KG independent): colour incl. background, depth, normal
-  float T_run = T_fin;
-  float S0 = a.bg[0] * T_fin, S1 = a.bg[1] * T_fin, S2 = a.bg[2] * T_fin;
-  float SD = 0.f, SN0 = 0.f, SN1 = 0.f, SN2 = 0.f;
-  const int slot = transpose_slot(lane);
-  const bool count = a.flags & HGS_FLAG_COUNT;
-  uint32_t n_ev = 0, n_c3 = 0, n_cr = 0, n_cl = 0;
-
-  for (int64_t top = end; top > lo; top -= kBlock) {
-    const int64_t bstart = top - kBlock > lo ? top - kBlock : lo;
-    const int nb = (int)(top - bstart);
-    __syncthreads();
-    if (threadIdx.x < nb) {
-      const int64_t j = bstart + threadIdx.x;
-      const uint32_t rk = naive ? (uint32_t)j : a.tile_vals[j];
-      s_rec[threadIdx.x] = a.recs[rk];
-    }
-    __syncthreads();
-    if (bstart >= warp_end) continue;  // nothing of this batch precedes the warp's last contributor
-    // 32-splat words from the back
-    for (int w0 = ((nb - 1) >> 5) << 5; w0 >= 0; w0 -= 32) {
-      const int el = w0 + lane;
-      bool rel = el < nb && bstart + el < warp_end;
-      if (!naive && rel) rel = bbox_overlaps(s_rec[el].r5, wx0, wy0, wx0 + 7, wy0 + 3);
-      uint32_t mask = __ballot_sync(0xffffffffu, rel);
-      while (mask) {
-        const int bit = 31 - __clz(mask);
-        mask &= ~(1u << bit);
-        const int e = w0 + bit;
-        const int64_t j = bstart + e;
-        const SplatRec &r = s_rec[e];
-        bool act = inside && (uint32_t)(j - lo) < last;
-        if (act && !naive) act = in_bbox(r.r5, ix, iy);
-        PairEval p;
-        if (count && act) ++n_ev;
-        const int c = act ? eval_fast<true>(r, ix, iy, a.flags, p) : kSkip;
-        if (c == kAmbiguous) {
-          // rare: park the per-pixel state in shared memory, resolve out of
-          // line, reload (nothing accumulated stays live across the call)
-          s_park[0][threadIdx.x] = T_run; s_park[1][threadIdx.x] = S0;
-          s_park[2][threadIdx.x] = S1; s_park[3][threadIdx.x] = S2;
-          s_park[4][threadIdx.x] = SD; s_park[5][threadIdx.x] = SN0;
-          s_park[6][threadIdx.x] = SN1; s_park[7][threadIdx.x] = SN2;
-          const Resolved rs = resolve_pair(&s_rec[e], ix, iy, a.st, true);
-          T_run = s_park[0][threadIdx.x]; S0 = s_park[1][threadIdx.x];
-          S1 = s_park[2][threadIdx.x]; S2 = s_park[3][threadIdx.x];
-          SD = s_park[4][threadIdx.x]; SN0 = s_park[5][threadIdx.x];
-          SN1 = s_park[6][threadIdx.x]; SN2 = s_park[7][threadIdx.x];
-          load_grads();
-          act = finish_resolved(rs, p);
-        } else {
-          act = c == kContrib;
-        }
-        if (!__any_sync(0xffffffffu, act)) continue;
-        const bool is3d = rec_is3d(r);
-        const uint32_t gidx = rec_idx(r);
-        float v[KG][16];
-        float ve[KG][4];
-#pragma unroll
-        for (int k = 0; k < KG; ++k) {
-#pragma unroll
-          for (int s = 0; s < 16; ++s) v[k][s] = 0.f;
-#pragma unroll
-          for (int s = 0; s < 4; ++s) ve[k][s] = 0.f;
-        }
-        if (act) {
-          if (count) {
-            if (is3d) ++n_c3; else if (p.ray) ++n_cr; else ++n_cl;
-          }
-          const float at = p.at;
-          const float inv_om = 1.f / (1.f - at);
-          T_run *= inv_om;  // transmittance before this splat
-          const float w = at * T_run;
-          const float4 c3 = r.r3, c4 = r.r4;
-          const float z = r.r0.z;
-#pragma unroll
-          for (int k = 0; k < KG; ++k) {
-            v[k][0] = gp[k][0] * w;
-            v[k][1] = gp[k][1] * w;
-            v[k][2] = gp[k][2] * w;
-            float d_at = gp[k][0] * (c3.y * T_run - S0 * inv_om) + gp[k][1] * (c3.z * T_run - S1 * inv_om) +
-                         gp[k][2] * (c3.w * T_run - S2 * inv_om);
-            if (EXT) {
-              d_at += gd[k] * (z * T_run - SD * inv_om);
-              d_at += gn[k][0] * (c4.x * T_run - SN0 * inv_om) + gn[k][1] * (c4.y * T_run - SN1 * inv_om) +
-                      gn[k][2] * (c4.z * T_run - SN2 * inv_om);
-              d_at += ga[k] * (T_fin * inv_om);
-              ve[k][0] = gd[k] * w;
-              ve[k][1] = gn[k][0] * w;
-              ve[k][2] = gn[k][1] * w;
-              ve[k][3] = gn[k][2] * w;
-            }
-            if (!p.clamped) {
-              const float da = d_at * at;
-              v[k][3] = da;
-              if (is3d) {
-                const float4 cn = r.r1;
-                const float vx = cn.x * p.u + cn.y * p.v, vy = cn.y * p.u + cn.z * p.v;
-                v[k][4] = vx * da;
-                v[k][5] = vy * da;
-                v[k][6] = 0.5f * da * vx * vx;
-                v[k][7] = 0.5f * da * vx * vy;
-                v[k][8] = 0.5f * da * vy * vy;
-              } else if (p.ray) {
-                const float du = -da * p.u, dv = -da * p.v;
-                const float id = p.inv_den;
-                const float dhu0 = (du * (-p.u * p.hv1) + dv * (-p.hv3 - p.v * p.hv1)) * id;
-                const float dhu1 = (du * (p.hv3 + p.u * p.hv0) + dv * (p.v * p.hv0)) * id;
-                const float dhu3 = (du * (-p.hv1) + dv * p.hv0) * id;
-                const float dhv0 = (du * (p.u * p.hu1) + dv * (p.hu3 + p.v * p.hu1)) * id;
-                const float dhv1 = (du * (-p.hu3 - p.u * p.hu0) + dv * (-p.v * p.hu0)) * id;
-                const float dhv3 = (du * p.hu1 + dv * (-p.hu0)) * id;
-                v[k][6] = -dhu0;
-                v[k][7] = -dhu1;
-                v[k][8] = -dhu3;
-                v[k][9] = -dhv0;
-                v[k][10] = -dhv1;
-                v[k][11] = -dhv3;
-                v[k][12] = p.pxl * dhu0 + p.pyl * dhv0;
-                v[k][13] = p.pxl * dhu1 + p.pyl * dhv1;
-                v[k][14] = p.pxl * dhu3 + p.pyl * dhv3;
-              } else {
-                v[k][4] = 4.f * p.dx * da;
-                v[k][5] = 4.f * p.dy * da;
-              }
-            }
-          }
-          S0 = fmaf(c3.y, w, S0);
-          S1 = fmaf(c3.z, w, S1);
-          S2 = fmaf(c3.w, w, S2);
-          if (EXT) {
-            SD = fmaf(z, w, SD);
-            SN0 = fmaf(c4.x, w, SN0);
-            SN1 = fmaf(c4.y, w, SN1);
-            SN2 = fmaf(c4.z, w, SN2);
-          }
-        }
-        if (lane == 0) b.touched[gidx] = 1;
-#pragma unroll
-        for (int k = 0; k < KG; ++k) {
-          const float tot = warp_transpose_reduce16(v[k], lane);
-          const int nslots = is3d ? 9 : 15;
-          if (!(lane & 1) && slot < nslots && tot != 0.f)
-            atomicAdd(b.acc + ((int64_t)gidx * KG + k) * kAcc + slot, tot);
-          if (EXT) {
-#pragma unroll
-            for (int s = 0; s < 4; ++s) {
-              float x = ve[k][s];
-#pragma unroll
-              for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-              ve[k][s] = x;
-            }
-            if (lane < 4) {
-              const float x = lane == 0 ? ve[k][0] : (lane == 1 ? ve[k][1] : (lane == 2 ? ve[k][2] : ve[k][3]));
-              if (x != 0.f) atomicAdd(b.acc_ext + ((int64_t)gidx * KG + k) * kAccExt + lane, x);
-            }
-          }
-        }
-      }
-    }
-  }
-  if (count) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      n_ev += __shfl_xor_sync(0xffffffffu, n_ev, o);
-      n_c3 += __shfl_xor_sync(0xffffffffu, n_c3, o);
-      n_cr += __shfl_xor_sync(0xffffffffu, n_cr, o);
-      n_cl += __shfl_xor_sync(0xffffffffu, n_cl, o);
-    }
-    if (lane == 0) {
-      atomicAdd(&a.st->diag[6], (unsigned long long)n_c3);
-      atomicAdd(&a.st->diag[7], (unsigned long long)n_cr);
-      atomicAdd(&a.st->diag[8], (unsigned long long)n_cl);
-      atomicAdd(&a.st->diag[9], (unsigned long long)n_ev);
-    }
-  }
-}
-
-// Instantiations: KG 1..4, with / without extension gradients.
-template __global__ void k_composite_bwd<1, false>(BwdArgs);
-template __global__ void k_composite_bwd<2, false>(BwdArgs);
-template __global__ void k_composite_bwd<3, false>(BwdArgs);
-template __global__ void k_composite_bwd<4, false>(BwdArgs);
-template __global__ void k_composite_bwd<1, true>(BwdArgs);
-template __global__ void k_composite_bwd<2, true>(BwdArgs);
-template __global__ void k_composite_bwd<3, true>(BwdArgs);
-template __global__ void k_composite_bwd<4, true>(BwdArgs);
-
-// touched by rank -> touched by Gaussian index
-__global__ void k_touched_scatter(const SplatRec *__restrict__ recs, const uint8_t *__restrict__ touched_rank,
-                                  int64_t m, uint8_t *__restrict__ touched) {
-  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < m; r += (int64_t)gridDim.x * blockDim.x)
-    if (touched_rank[r]) touched[__float_as_uint(recs[r].r4.w) & 0x7fffffffu] = 1;
-}
 
 // --------------------------------------------------------- chain rule
 

@@ -1,0 +1,431 @@
+// hgs_composite_bwd.cu -- the back-to-front replay (raster/_blend_py.py:126-242).
+//
+//  k_composite_bwd : the hot kernel (no function calls).  Same tiling and
+//                    warp-independent streaming as the forward, walking each
+//                    pixel's contributors back to front from its last one.  A
+//                    lane whose next decision (cutoff, clamp, ray branch) is
+//                    ambiguous in float32 saves its replay state to the
+//                    BwdFix worklist and retires.
+//  k_fixup_bwd     : one warp per deferred pixel resumes the replay with the
+//                    float64-exact decisions, 32 entries at a time (product
+//                    scan for the transmittance, prefix sums for the suffix
+//                    colour), per-lane atomics.
+#include "hgs_kernels.cuh"
+
+namespace hgs {
+
+// Screen-space accumulator slots per (Gaussian, kg), float32:
+//  0-2 colour, 3 alpha (sum d_at * at = g_alpha_eff * alpha_eff),
+//  4-5 centre (3D Mahalanobis / 2D low-pass), 6-14 geometry:
+//  3D: 6-8 = dL/dcov2d (a, b, c);  2D ray: 6-8 = dL/dM0 (cols 0,1,3),
+//  9-11 = dL/dM1, 12-14 = dL/dM3 w.r.t. anchor-relative pixels; 15 unused.
+// Extension slots (separate array, 4 per (Gaussian, kg)): z, normal xyz.
+constexpr int kAcc = 16;
+constexpr int kAccExt = 4;
+
+// Sum 16 per-lane values over the warp.  On return lane l holds the total of
+// slot ((l >> 4) & 1) * 8 + ((l >> 3) & 1) * 4 + ((l >> 2) & 1) * 2 + ((l >> 1) & 1)
+// (lanes l and l ^ 1 hold the same slot).  16 shuffles instead of 16 x 5.
+__device__ __forceinline__ float warp_transpose_reduce16(float (&v)[16], int lane) {
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const bool hi = lane & 16;
+    float send = hi ? v[i] : v[i + 8];
+    float keep = hi ? v[i + 8] : v[i];
+    v[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const bool hi = lane & 8;
+    float send = hi ? v[i] : v[i + 4];
+    float keep = hi ? v[i + 4] : v[i];
+    v[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+  }
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const bool hi = lane & 4;
+    float send = hi ? v[i] : v[i + 2];
+    float keep = hi ? v[i + 2] : v[i];
+    v[i] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+  }
+  {
+    const bool hi = lane & 2;
+    float send = hi ? v[0] : v[1];
+    float keep = hi ? v[1] : v[0];
+    v[0] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+  }
+  return v[0] + __shfl_xor_sync(0xffffffffu, v[0], 1);
+}
+
+__device__ __forceinline__ int transpose_slot(int lane) {
+  return ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 + ((lane >> 1) & 1);
+}
+
+// Per-pixel upstream gradients of one pixel (KG stacked).
+template <int KG, bool EXT>
+struct PixGrads {
+  float gp[KG][3], gd[KG], gn[KG][3], ga[KG];
+  __device__ __forceinline__ void load(const BwdArgs &b, bool inside, int64_t pix, int64_t HW) {
+#pragma unroll
+    for (int k = 0; k < KG; ++k) {
+      gp[k][0] = gp[k][1] = gp[k][2] = 0.f;
+      gd[k] = ga[k] = 0.f;
+      gn[k][0] = gn[k][1] = gn[k][2] = 0.f;
+      if (!inside) continue;
+      const float *g = b.pix_grad + ((int64_t)k * HW + pix) * 3;
+      gp[k][0] = g[0]; gp[k][1] = g[1]; gp[k][2] = g[2];
+      if (EXT) {
+        if (b.depth_grad) gd[k] = b.depth_grad[(int64_t)k * HW + pix];
+        if (b.alpha_grad) ga[k] = b.alpha_grad[(int64_t)k * HW + pix];
+        if (b.normal_grad) {
+          const float *h = b.normal_grad + ((int64_t)k * HW + pix) * 3;
+          gn[k][0] = h[0]; gn[k][1] = h[1]; gn[k][2] = h[2];
+        }
+      }
+    }
+  }
+};
+
+// Suffix sums of the replay: colour (incl. background * T_final), depth, normal.
+struct Suffix {
+  float s0, s1, s2, sd, sn0, sn1, sn2;
+};
+
+// Gradient terms of one contributing pair (_blend_py.py:187-236) given the
+// transmittance before it (T_k), 1/(1 - at) and the suffix sums of everything
+// behind it.  v: 16 accumulator slots per kg (see kAcc), ve: extension slots.
+template <int KG, bool EXT>
+__device__ __forceinline__ void pair_grads(const SplatRec &r, const PairEval &p, float T_k, float inv_om, float T_fin,
+                                           const Suffix &S, const PixGrads<KG, EXT> &G, float (&v)[KG][16],
+                                           float (&ve)[KG][4]) {
+  const bool is3d = rec_is3d(r);
+  const float at = p.at;
+  const float w = at * T_k;
+  const float4 c3 = r.r3, c4 = r.r4;
+  const float z = r.r0.z;
+#pragma unroll
+  for (int k = 0; k < KG; ++k) {
+    v[k][0] = G.gp[k][0] * w;
+    v[k][1] = G.gp[k][1] * w;
+    v[k][2] = G.gp[k][2] * w;
+    float d_at = G.gp[k][0] * (c3.y * T_k - S.s0 * inv_om) + G.gp[k][1] * (c3.z * T_k - S.s1 * inv_om) +
+                 G.gp[k][2] * (c3.w * T_k - S.s2 * inv_om);
+    if (EXT) {
+      d_at += G.gd[k] * (z * T_k - S.sd * inv_om);
+      d_at += G.gn[k][0] * (c4.x * T_k - S.sn0 * inv_om) + G.gn[k][1] * (c4.y * T_k - S.sn1 * inv_om) +
+              G.gn[k][2] * (c4.z * T_k - S.sn2 * inv_om);
+      d_at += G.ga[k] * (T_fin * inv_om);
+      ve[k][0] = G.gd[k] * w;
+      ve[k][1] = G.gn[k][0] * w;
+      ve[k][2] = G.gn[k][1] * w;
+      ve[k][3] = G.gn[k][2] * w;
+    }
+    if (!p.clamped) {
+      const float da = d_at * at;  // = dL/dalpha_eff * alpha_eff * exp(-d/2)
+      v[k][3] = da;
+      if (is3d) {
+        const float4 cn = r.r1;
+        const float vx = cn.x * p.u + cn.y * p.v, vy = cn.y * p.u + cn.z * p.v;
+        v[k][4] = vx * da;
+        v[k][5] = vy * da;
+        v[k][6] = 0.5f * da * vx * vx;
+        v[k][7] = 0.5f * da * vx * vy;
+        v[k][8] = 0.5f * da * vy * vy;
+      } else if (p.ray) {
+        const float du = -da * p.u, dv = -da * p.v;
+        const float id = p.inv_den;
+        const float dhu0 = (du * (-p.u * p.hv1) + dv * (-p.hv3 - p.v * p.hv1)) * id;
+        const float dhu1 = (du * (p.hv3 + p.u * p.hv0) + dv * (p.v * p.hv0)) * id;
+        const float dhu3 = (du * (-p.hv1) + dv * p.hv0) * id;
+        const float dhv0 = (du * (p.u * p.hu1) + dv * (p.hu3 + p.v * p.hu1)) * id;
+        const float dhv1 = (du * (-p.hu3 - p.u * p.hu0) + dv * (-p.v * p.hu0)) * id;
+        const float dhv3 = (du * p.hu1 + dv * (-p.hu0)) * id;
+        v[k][6] = -dhu0;
+        v[k][7] = -dhu1;
+        v[k][8] = -dhu3;
+        v[k][9] = -dhv0;
+        v[k][10] = -dhv1;
+        v[k][11] = -dhv3;
+        v[k][12] = p.pxl * dhu0 + p.pyl * dhv0;
+        v[k][13] = p.pxl * dhu1 + p.pyl * dhv1;
+        v[k][14] = p.pxl * dhu3 + p.pyl * dhv3;
+      } else {
+        v[k][4] = 4.f * p.dx * da;
+        v[k][5] = 4.f * p.dy * da;
+      }
+    }
+  }
+}
+
+template <int KG, bool EXT>
+__global__ void __launch_bounds__(kBlock, 3) k_composite_bwd(BwdArgs b) {
+  const CompositeArgs &a = b.c;
+  __shared__ SplatRec s_rec[kBlock / 32][32];
+  const int tile = blockIdx.x;
+  const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int wx0 = tx * kTile + (warp & 1) * 8, wy0 = ty * kTile + (warp >> 1) * 4;
+  const int ix = wx0 + (lane & 7), iy = wy0 + (lane >> 3);
+  const bool inside = ix < a.width && iy < a.height;
+  const bool naive = a.flags & HGS_FLAG_NAIVE;
+  const uint32_t lane_bit = 1u << lane;
+  const uint32_t lo = naive ? 0u : a.tile_off[tile];
+  const int64_t HW = (int64_t)a.width * a.height;
+  const uint32_t pix = (uint32_t)iy * (uint32_t)a.width + (uint32_t)ix;
+  uint32_t last = 0;
+  float T_fin = 1.f;
+  PixGrads<KG, EXT> G;
+  G.load(b, inside, pix, HW);
+  if (inside) {
+    last = a.pix_last[pix];
+    T_fin = a.pix_T[pix];
+  }
+  uint32_t warp_last = last;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) warp_last = max(warp_last, __shfl_xor_sync(0xffffffffu, warp_last, o));
+  const uint32_t warp_end = lo + warp_last;  // exclusive
+  float T_run = T_fin;
+  Suffix S{a.bg[0] * T_fin, a.bg[1] * T_fin, a.bg[2] * T_fin, 0.f, 0.f, 0.f, 0.f};
+  const int slot = transpose_slot(lane);
+  const bool count = a.flags & HGS_FLAG_COUNT;
+  bool dead = false;  // deferred to k_fixup_bwd
+  uint32_t n_ev = 0, n_c3 = 0, n_cr = 0, n_cl = 0;
+  SplatRec *wrec = s_rec[warp];
+
+  for (uint32_t top = warp_end, start; top > lo; top = start) {
+    start = top - lo > 32u ? top - 32u : lo;
+    const uint32_t j = start + lane;
+    uint32_t pm = 0u;
+    if (j < top) {
+      const uint32_t rk = naive ? j : __ldg(a.tile_vals + j);
+      const SplatRec *g = a.recs + rk;
+      const int4 q = __ldg(&g->r5);
+      pm = naive ? 0xffffffffu : pixel_mask(q, wx0, wy0);
+      if (pm) {
+        SplatRec r;
+        r.r0 = __ldg(&g->r0); r.r1 = __ldg(&g->r1); r.r2 = __ldg(&g->r2);
+        r.r3 = __ldg(&g->r3); r.r4 = __ldg(&g->r4); r.r5 = q;
+        wrec[lane] = r;
+      }
+    }
+    uint32_t rel = __ballot_sync(0xffffffffu, pm != 0u);
+    __syncwarp();
+    while (rel) {
+      const int e = 31 - __clz(rel);
+      rel &= ~(1u << e);
+      const uint32_t m = __shfl_sync(0xffffffffu, pm, e);
+      const uint32_t jj = start + e;
+      const SplatRec &r = wrec[e];
+      bool act = !dead && inside && (m & lane_bit) && jj - lo < last;
+      PairEval p;
+      if (count && act) ++n_ev;
+      const int c = act ? eval_fast<true>(r, ix, iy, a.flags, p) : kSkip;
+      if (c == kAmbiguous) {
+        BwdFix f;
+        f.pix = pix; f.entry = jj; f.T_run = T_run;
+        f.S0 = S.s0; f.S1 = S.s1; f.S2 = S.s2; f.SD = S.sd; f.SN0 = S.sn0; f.SN1 = S.sn1; f.SN2 = S.sn2;
+#pragma unroll
+        for (int i = 0; i < 6; ++i) f.pad[i] = 0;
+        b.c.bwd_fix[atomicAdd(&a.st->n_fix_bwd, 1u)] = f;
+        dead = true;
+      }
+      act = c == kContrib;
+      if (!__any_sync(0xffffffffu, act)) continue;
+      const bool is3d = rec_is3d(r);
+      const uint32_t gidx = rec_idx(r);
+      float v[KG][16];
+      float ve[KG][4];
+#pragma unroll
+      for (int k = 0; k < KG; ++k) {
+#pragma unroll
+        for (int s = 0; s < 16; ++s) v[k][s] = 0.f;
+#pragma unroll
+        for (int s = 0; s < 4; ++s) ve[k][s] = 0.f;
+      }
+      if (act) {
+        if (count) {
+          if (is3d) ++n_c3; else if (p.ray) ++n_cr; else ++n_cl;
+        }
+        const float inv_om = 1.f / (1.f - p.at);
+        T_run *= inv_om;  // transmittance before this splat
+        pair_grads<KG, EXT>(r, p, T_run, inv_om, T_fin, S, G, v, ve);
+        const float w = p.at * T_run;
+        S.s0 = fmaf(r.r3.y, w, S.s0);
+        S.s1 = fmaf(r.r3.z, w, S.s1);
+        S.s2 = fmaf(r.r3.w, w, S.s2);
+        if (EXT) {
+          S.sd = fmaf(r.r0.z, w, S.sd);
+          S.sn0 = fmaf(r.r4.x, w, S.sn0);
+          S.sn1 = fmaf(r.r4.y, w, S.sn1);
+          S.sn2 = fmaf(r.r4.z, w, S.sn2);
+        }
+      }
+      if (lane == 0) b.touched[gidx] = 1;
+#pragma unroll
+      for (int k = 0; k < KG; ++k) {
+        const float tot = warp_transpose_reduce16(v[k], lane);
+        const int nslots = is3d ? 9 : 15;
+        if (!(lane & 1) && slot < nslots && tot != 0.f)
+          atomicAdd(b.acc + ((int64_t)gidx * KG + k) * kAcc + slot, tot);
+        if (EXT) {
+#pragma unroll
+          for (int s = 0; s < 4; ++s) {
+            float x = ve[k][s];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+            ve[k][s] = x;
+          }
+          if (lane < 4) {
+            const float x = lane == 0 ? ve[k][0] : (lane == 1 ? ve[k][1] : (lane == 2 ? ve[k][2] : ve[k][3]));
+            if (x != 0.f) atomicAdd(b.acc_ext + ((int64_t)gidx * KG + k) * kAccExt + lane, x);
+          }
+        }
+      }
+    }
+    __syncwarp();  // the next chunk overwrites this warp's staging slots
+    if (__all_sync(0xffffffffu, dead || !inside)) break;
+  }
+  if (count) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      n_ev += __shfl_xor_sync(0xffffffffu, n_ev, o);
+      n_c3 += __shfl_xor_sync(0xffffffffu, n_c3, o);
+      n_cr += __shfl_xor_sync(0xffffffffu, n_cr, o);
+      n_cl += __shfl_xor_sync(0xffffffffu, n_cl, o);
+    }
+    if (lane == 0) {
+      atomicAdd(&a.st->diag[6], (unsigned long long)n_c3);
+      atomicAdd(&a.st->diag[7], (unsigned long long)n_cr);
+      atomicAdd(&a.st->diag[8], (unsigned long long)n_cl);
+      atomicAdd(&a.st->diag[9], (unsigned long long)n_ev);
+    }
+  }
+}
+
+__device__ __forceinline__ float warp_sum_bwd(float x) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+  return x;
+}
+
+__device__ __forceinline__ float scan_add_ex(float x, int lane) {
+  float s = x;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const float y = __shfl_up_sync(0xffffffffu, s, o);
+    if (lane >= o) s += y;
+  }
+  return s - x;
+}
+
+// Deferred pixels of the backward, one warp each.  Lane l evaluates entry
+// (top - 1 - l) -- lane order is the back-to-front replay order -- with the
+// exact decisions; the transmittance before each entry is T_run divided by the
+// inclusive product of (1 - at) over the lanes up to it, the suffix sums are
+// exclusive prefix sums of c * w; every lane then adds its pair's gradients
+// with per-lane atomics.
+template <int KG, bool EXT>
+__global__ void __launch_bounds__(256) k_fixup_bwd(BwdArgs b) {
+  const CompositeArgs &a = b.c;
+  const uint32_t nfix = a.st->n_fix_bwd;
+  const int lane = threadIdx.x & 31;
+  const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+  const bool naive = a.flags & HGS_FLAG_NAIVE;
+  const int64_t HW = (int64_t)a.width * a.height;
+  for (uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < nfix; w += nw) {
+    const BwdFix f = b.c.bwd_fix[w];
+    const int ix = (int)(f.pix % (uint32_t)a.width), iy = (int)(f.pix / (uint32_t)a.width);
+    const int tile = (iy / kTile) * a.tiles_x + ix / kTile;
+    const uint32_t lo = naive ? 0u : a.tile_off[tile];
+    PixGrads<KG, EXT> G;
+    G.load(b, true, f.pix, HW);
+    const float T_fin = a.pix_T[f.pix];
+    float T_run = f.T_run;
+    Suffix S{f.S0, f.S1, f.S2, f.SD, f.SN0, f.SN1, f.SN2};
+    for (int64_t top = (int64_t)f.entry + 1; top > (int64_t)lo; top -= 32) {
+      const int64_t e = top - 1 - lane;
+      bool con = false;
+      PairEval p;
+      SplatRec r;
+      if (e >= (int64_t)lo) {
+        const uint32_t rk = naive ? (uint32_t)e : a.tile_vals[e];
+        r = a.recs[rk];
+        if (naive || in_bbox(r.r5, ix, iy)) con = eval_pair<true>(r, a.recs + rk, ix, iy, a.flags, a.st, p);
+      }
+      const float om = con ? 1.f - p.at : 1.f;
+      float Q = om;  // inclusive product in replay order
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const float y = __shfl_up_sync(0xffffffffu, Q, o);
+        if (lane >= o) Q *= y;
+      }
+      const float T_k = T_run / Q;
+      const float wgt = con ? p.at * T_k : 0.f;
+      const float cw0 = con ? r.r3.y * wgt : 0.f, cw1 = con ? r.r3.z * wgt : 0.f, cw2 = con ? r.r3.w * wgt : 0.f;
+      Suffix Sl = S;
+      Sl.s0 += scan_add_ex(cw0, lane);
+      Sl.s1 += scan_add_ex(cw1, lane);
+      Sl.s2 += scan_add_ex(cw2, lane);
+      float zw = 0.f, nw0 = 0.f, nw1 = 0.f, nw2 = 0.f;
+      if (EXT) {
+        zw = con ? r.r0.z * wgt : 0.f;
+        nw0 = con ? r.r4.x * wgt : 0.f;
+        nw1 = con ? r.r4.y * wgt : 0.f;
+        nw2 = con ? r.r4.z * wgt : 0.f;
+        Sl.sd += scan_add_ex(zw, lane);
+        Sl.sn0 += scan_add_ex(nw0, lane);
+        Sl.sn1 += scan_add_ex(nw1, lane);
+        Sl.sn2 += scan_add_ex(nw2, lane);
+      }
+      if (con) {
+        float v[KG][16];
+        float ve[KG][4];
+#pragma unroll
+        for (int k = 0; k < KG; ++k) {
+#pragma unroll
+          for (int s = 0; s < 16; ++s) v[k][s] = 0.f;
+#pragma unroll
+          for (int s = 0; s < 4; ++s) ve[k][s] = 0.f;
+        }
+        pair_grads<KG, EXT>(r, p, T_k, 1.f / om, T_fin, Sl, G, v, ve);
+        const uint32_t gidx = rec_idx(r);
+        b.touched[gidx] = 1;
+        const int nslots = rec_is3d(r) ? 9 : 15;
+        for (int k = 0; k < KG; ++k) {
+          for (int s = 0; s < nslots; ++s)
+            if (v[k][s] != 0.f) atomicAdd(b.acc + ((int64_t)gidx * KG + k) * kAcc + s, v[k][s]);
+          if (EXT)
+            for (int s = 0; s < 4; ++s)
+              if (ve[k][s] != 0.f) atomicAdd(b.acc_ext + ((int64_t)gidx * KG + k) * kAccExt + s, ve[k][s]);
+        }
+      }
+      // carry T_run and the suffix sums across chunks
+      T_run = T_run / __shfl_sync(0xffffffffu, Q, 31);
+      S.s0 += warp_sum_bwd(cw0);
+      S.s1 += warp_sum_bwd(cw1);
+      S.s2 += warp_sum_bwd(cw2);
+      if (EXT) {
+        S.sd += warp_sum_bwd(zw);
+        S.sn0 += warp_sum_bwd(nw0);
+        S.sn1 += warp_sum_bwd(nw1);
+        S.sn2 += warp_sum_bwd(nw2);
+      }
+    }
+    if (lane == 0) atomicAdd(&a.st->diag[11], 1ull);
+  }
+}
+
+// Instantiations: KG 1..4, with / without extension gradients.
+#define HGS_INST_BWD(KG, EXT)                                  \
+  template __global__ void k_composite_bwd<KG, EXT>(BwdArgs); \
+  template __global__ void k_fixup_bwd<KG, EXT>(BwdArgs);
+HGS_INST_BWD(1, false)
+HGS_INST_BWD(2, false)
+HGS_INST_BWD(3, false)
+HGS_INST_BWD(4, false)
+HGS_INST_BWD(1, true)
+HGS_INST_BWD(2, true)
+HGS_INST_BWD(3, true)
+HGS_INST_BWD(4, true)
+
+}  // namespace hgs

@@ -1,0 +1,267 @@
+// hgs_composite_fwd.cu -- the front-to-back compositor (raster/_blend_py.py:76-117).
+//
+//  k_composite_fwd : the hot kernel.  No function calls: every decision is a
+//                    float32 decision with an error bound; a lane whose next
+//                    decision is ambiguous saves its state to the FwdFix
+//                    worklist and retires (deferred exactness).
+//  k_fixup_fwd     : one warp per deferred pixel resumes the walk with the
+//                    float64-exact decisions, 32 tile-list entries at a time
+//                    (lane-parallel evaluation, product scan for T).
+#include "hgs_kernels.cuh"
+
+#ifndef HGS_FWD_MINB
+#define HGS_FWD_MINB 3  // CTAs per SM the hot compositor is register-budgeted for
+#endif
+
+namespace hgs {
+
+// One CTA per 16 x 16 tile, one thread per pixel, warps own 8 x 4 pixel blocks
+// and run independently (no block barriers): a warp walks its tile list in
+// chunks of 32 entries; lane l loads entry l's rank and bbox and turns the
+// bbox into a 32-bit mask of the warp's pixels it covers (the reference's
+// inclusive bbox test, _blend_py.py:89-91); records of relevant entries are
+// staged in the warp's slice of shared memory and walked in order.  Every
+// lane sees the same splat, so the 2D / 3D branch is warp-uniform; a warp
+// retires as soon as its 32 pixels are saturated or deferred.
+template <bool NAIVE, bool COUNT>
+__global__ void __launch_bounds__(kBlock, HGS_FWD_MINB) k_composite_fwd(CompositeArgs a) {
+  __shared__ SplatRec s_rec[kBlock / 32][32];
+  const int tile = blockIdx.x;
+  const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int wx0 = tx * kTile + (warp & 1) * 8, wy0 = ty * kTile + (warp >> 1) * 4;
+  const int ix = wx0 + (lane & 7), iy = wy0 + (lane >> 3);
+  const bool inside = ix < a.width && iy < a.height;
+  const uint32_t lane_bit = 1u << lane;
+  const bool exact = HGS_EXACT_ENABLED && !(a.flags & HGS_FLAG_FAST);
+  uint32_t lo, hi;
+  if (NAIVE) {
+    lo = 0;
+    hi = (uint32_t)a.m;
+  } else {
+    lo = a.tile_off[tile];
+    hi = a.tile_off[tile + 1];
+  }
+  const uint32_t pix = (uint32_t)iy * (uint32_t)a.width + (uint32_t)ix;
+  float T = 1.f, cr = 0.f, cg = 0.f, cb = 0.f, dep = 0.f, n0 = 0.f, n1 = 0.f, n2 = 0.f;
+  uint32_t cnt = 0, last = 0;
+  bool done = !inside, deferred = false;
+  uint32_t n_ev3 = 0, n_ev2 = 0, n_c3 = 0, n_c2 = 0;  // HGS_FLAG_COUNT
+  SplatRec *wrec = s_rec[warp];
+
+  auto defer = [&](uint32_t entry, uint32_t mode) {
+    FwdFix f;
+    f.pix = pix; f.entry = entry; f.mode = mode; f.cnt = cnt; f.last = last;
+    f.T = T; f.c0 = cr; f.c1 = cg; f.c2 = cb; f.dep = dep; f.n0 = n0; f.n1 = n1; f.n2 = n2;
+    f.pad[0] = f.pad[1] = f.pad[2] = 0;
+    a.fwd_fix[atomicAdd(&a.st->n_fix_fwd, 1u)] = f;
+    deferred = true;
+    done = true;
+  };
+
+  for (uint32_t base = lo; base < hi; base += 32) {
+    if (__all_sync(0xffffffffu, done)) break;
+    // stage: rank + bbox of entry base + lane, pixel mask, record if relevant
+    const uint32_t j = base + lane;
+    uint32_t pm = 0u;
+    if (j < hi) {
+      const uint32_t rk = NAIVE ? j : __ldg(a.tile_vals + j);
+      const SplatRec *g = a.recs + rk;
+      const int4 q = __ldg(&g->r5);
+      pm = NAIVE ? 0xffffffffu : pixel_mask(q, wx0, wy0);
+      if (pm) {
+        SplatRec r;
+        r.r0 = __ldg(&g->r0); r.r1 = __ldg(&g->r1); r.r2 = __ldg(&g->r2);
+        r.r3 = __ldg(&g->r3); r.r4 = __ldg(&g->r4); r.r5 = q;
+        wrec[lane] = r;
+      }
+    }
+    uint32_t rel = __ballot_sync(0xffffffffu, pm != 0u);
+    __syncwarp();
+    while (rel) {
+      const int e = __ffs(rel) - 1;
+      rel &= rel - 1;
+      const uint32_t m = __shfl_sync(0xffffffffu, pm, e);
+      if (done || !(m & lane_bit)) continue;
+      const SplatRec &r = wrec[e];
+      const bool is3d = rec_is3d(r);
+      if (COUNT) (is3d ? n_ev3 : n_ev2) += 1;
+      PairEval p;
+      const int c = eval_fast<false>(r, ix, iy, a.flags, p);
+      if (c == kSkip) continue;
+      if (c == kAmbiguous) {
+        defer(base + e, 0u);
+        continue;
+      }
+      if (COUNT) (is3d ? n_c3 : n_c2) += 1;
+      const float at = p.at;
+      const float w = at * T;
+      const float4 c3 = r.r3, c4 = r.r4;
+      cr = fmaf(w, c3.y, cr);
+      cg = fmaf(w, c3.z, cg);
+      cb = fmaf(w, c3.w, cb);
+      dep = fmaf(w, r.r0.z, dep);
+      n0 = fmaf(w, c4.x, n0);
+      n1 = fmaf(w, c4.y, n1);
+      n2 = fmaf(w, c4.z, n2);
+      ++cnt;
+      last = base + e - lo + 1u;
+      T = T * (1.f - at);
+      // early stop T < 1e-4 (_blend_py.py:111-113); near the threshold the
+      // decision is deferred to the float64 transmittance replay
+      if (exact && fabsf(T - (float)kEarlyStopT) <= 2e-5f * (float)kEarlyStopT)
+        defer(base + e, 1u);
+      else if (T < (float)kEarlyStopT)
+        done = true;
+    }
+    __syncwarp();  // the next chunk overwrites this warp's staging slots
+  }
+  if (COUNT) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      n_ev3 += __shfl_xor_sync(0xffffffffu, n_ev3, o);
+      n_ev2 += __shfl_xor_sync(0xffffffffu, n_ev2, o);
+      n_c3 += __shfl_xor_sync(0xffffffffu, n_c3, o);
+      n_c2 += __shfl_xor_sync(0xffffffffu, n_c2, o);
+    }
+    if (lane == 0) {
+      atomicAdd(&a.st->diag[2], (unsigned long long)n_ev3);
+      atomicAdd(&a.st->diag[3], (unsigned long long)n_ev2);
+      atomicAdd(&a.st->diag[4], (unsigned long long)n_c3);
+      atomicAdd(&a.st->diag[5], (unsigned long long)n_c2);
+    }
+  }
+  if (!inside || deferred) return;  // deferred pixels are written by k_fixup_fwd
+  a.color[3 * pix + 0] = cr + a.bg[0] * T;
+  a.color[3 * pix + 1] = cg + a.bg[1] * T;
+  a.color[3 * pix + 2] = cb + a.bg[2] * T;
+  a.depth[pix] = dep;
+  a.trans[pix] = T;
+  if (a.alpha) a.alpha[pix] = 1.f - T;
+  if (a.normal) {
+    a.normal[3 * pix + 0] = n0;
+    a.normal[3 * pix + 1] = n1;
+    a.normal[3 * pix + 2] = n2;
+  }
+  a.pix_T[pix] = T;
+  a.pix_last[pix] = last;
+  a.pix_count[pix] = cnt;
+}
+
+template __global__ void k_composite_fwd<false, false>(CompositeArgs);
+template __global__ void k_composite_fwd<true, false>(CompositeArgs);
+template __global__ void k_composite_fwd<false, true>(CompositeArgs);
+template __global__ void k_composite_fwd<true, true>(CompositeArgs);
+
+__device__ __forceinline__ float warp_sum(float x) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+  return x;
+}
+
+// Deferred pixels, one warp each (grid-stride over the worklist).  The warp
+// evaluates 32 consecutive tile-list entries in parallel with the exact
+// decisions (float64 re-evaluation where the float32 bound is ambiguous),
+// forms the transmittance with a product scan, resolves the early stop in
+// lane order (float64 replay near the threshold) and accumulates.
+__global__ void __launch_bounds__(256) k_fixup_fwd(CompositeArgs a) {
+  const uint32_t nfix = a.st->n_fix_fwd;
+  const int lane = threadIdx.x & 31;
+  const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+  const bool naive = a.flags & HGS_FLAG_NAIVE;
+  const float thr = (float)kEarlyStopT;
+  for (uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < nfix; w += nw) {
+    const FwdFix f = a.fwd_fix[w];
+    const int ix = (int)(f.pix % (uint32_t)a.width), iy = (int)(f.pix / (uint32_t)a.width);
+    const int tile = (iy / kTile) * a.tiles_x + ix / kTile;
+    const uint32_t lo = naive ? 0u : a.tile_off[tile];
+    const uint32_t hi = naive ? (uint32_t)a.m : a.tile_off[tile + 1];
+    float T = f.T, c0 = f.c0, c1 = f.c1, c2 = f.c2, dep = f.dep, n0 = f.n0, n1 = f.n1, n2 = f.n2;
+    uint32_t cnt = f.cnt, last = f.last;
+    bool stopped = false;
+    uint32_t start = f.entry;
+    if (f.mode == 1u) {  // warp-cooperative float64 replay of the transmittance
+      stopped = replay_T_below(a.recs, a.tile_vals, a.flags, a.st, lo, f.entry, ix, iy);
+      start = f.entry + 1u;
+    }
+    for (uint32_t base = start; base < hi && !stopped; base += 32) {
+      const uint32_t e = base + lane;
+      bool con = false;
+      float at = 0.f;
+      SplatRec r;
+      if (e < hi) {
+        const uint32_t rk = naive ? e : a.tile_vals[e];
+        r = a.recs[rk];
+        if (naive || in_bbox(r.r5, ix, iy)) {
+          PairEval p;
+          con = eval_pair<false>(r, a.recs + rk, ix, iy, a.flags, a.st, p);
+          at = p.at;
+        }
+      }
+      const float om = con ? 1.f - at : 1.f;
+      float P = om;  // inclusive product scan in lane (= entry) order
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const float y = __shfl_up_sync(0xffffffffu, P, o);
+        if (lane >= o) P *= y;
+      }
+      float Pex = __shfl_up_sync(0xffffffffu, P, 1);
+      if (lane == 0) Pex = 1.f;
+      const float Tb = T * Pex, Ta = T * P;
+      // early stop, in lane order: clear float32 decisions first, then the
+      // near-threshold lanes (warp-cooperative float64 replay) before them
+      const bool near = con && fabsf(Ta - thr) <= 2e-5f * thr;
+      const uint32_t clear_stop = __ballot_sync(0xffffffffu, con && !near && Ta < thr);
+      uint32_t near_mask = __ballot_sync(0xffffffffu, near);
+      int first = clear_stop ? __ffs(clear_stop) - 1 : 32;
+      while (near_mask) {
+        const int l = __ffs(near_mask) - 1;
+        if (l > first) break;
+        near_mask &= near_mask - 1;
+        const uint32_t el = __shfl_sync(0xffffffffu, e, l);
+        if (replay_T_below(a.recs, a.tile_vals, a.flags, a.st, lo, el, ix, iy)) {
+          first = l;
+          break;
+        }
+      }
+      const bool valid = con && lane <= first;
+      const float wgt = valid ? at * Tb : 0.f;
+      c0 += warp_sum(valid ? wgt * r.r3.y : 0.f);
+      c1 += warp_sum(valid ? wgt * r.r3.z : 0.f);
+      c2 += warp_sum(valid ? wgt * r.r3.w : 0.f);
+      dep += warp_sum(valid ? wgt * r.r0.z : 0.f);
+      n0 += warp_sum(valid ? wgt * r.r4.x : 0.f);
+      n1 += warp_sum(valid ? wgt * r.r4.y : 0.f);
+      n2 += warp_sum(valid ? wgt * r.r4.z : 0.f);
+      const uint32_t vm = __ballot_sync(0xffffffffu, valid);
+      cnt += __popc(vm);
+      if (vm) last = base + (31 - __clz(vm)) - lo + 1u;
+      if (first < 32) {
+        T = __shfl_sync(0xffffffffu, Ta, first);
+        stopped = true;
+      } else {
+        T = __shfl_sync(0xffffffffu, Ta, 31);
+      }
+    }
+    if (lane == 0) {
+      const uint32_t pix = f.pix;
+      a.color[3 * pix + 0] = c0 + a.bg[0] * T;
+      a.color[3 * pix + 1] = c1 + a.bg[1] * T;
+      a.color[3 * pix + 2] = c2 + a.bg[2] * T;
+      a.depth[pix] = dep;
+      a.trans[pix] = T;
+      if (a.alpha) a.alpha[pix] = 1.f - T;
+      if (a.normal) {
+        a.normal[3 * pix + 0] = n0;
+        a.normal[3 * pix + 1] = n1;
+        a.normal[3 * pix + 2] = n2;
+      }
+      a.pix_T[pix] = T;
+      a.pix_last[pix] = last;
+      a.pix_count[pix] = cnt;
+      atomicAdd(&a.st->diag[10], 1ull);
+    }
+  }
+}
+
+}  // namespace hgs

@@ -4,10 +4,6 @@
 // raster/_blend_py.py:55-123 (paths relative to the reference package).
 #include "hgs_kernels.cuh"
 
-#ifndef HGS_FWD_MINB
-#define HGS_FWD_MINB 2  // CTAs per SM the forward compositor is register-budgeted for
-#endif
-
 namespace hgs {
 
 __global__ void k_init_state(SceneView sc, CamD cam, ModD mod, FrameState *st) {
@@ -188,151 +184,6 @@ __global__ void k_tile_ranges(const uint32_t *__restrict__ skeys, int64_t k, int
 
 // -------------------------------------------------------------- composite
 
-// Per-tile front-to-back compositor (_blend_py.py:76-117).  One CTA per
-// 16 x 16 tile, one thread per pixel; warps own 8 x 4 pixel blocks.  Splat
-// records are staged in shared memory in batches of 256.  Each warp first
-// culls the batch against its 8 x 4 block (one rect test per lane, ballot),
-// then walks only the relevant splats, in order; all lanes of the warp see
-// the same splat, so the 2D / 3D branch is warp-uniform.
-#define PARK_STATE()                                                                   \
-  do {                                                                                 \
-    s_park[0][threadIdx.x] = T; s_park[1][threadIdx.x] = cr;                           \
-    s_park[2][threadIdx.x] = cg; s_park[3][threadIdx.x] = cb;                          \
-    s_park[4][threadIdx.x] = dep; s_park[5][threadIdx.x] = n0;                         \
-    s_park[6][threadIdx.x] = n1; s_park[7][threadIdx.x] = n2;                          \
-    s_park[8][threadIdx.x] = __uint_as_float(cnt);                                     \
-    s_park[9][threadIdx.x] = __uint_as_float(last);                                    \
-  } while (0)
-#define UNPARK_STATE()                                                                 \
-  do {                                                                                 \
-    T = s_park[0][threadIdx.x]; cr = s_park[1][threadIdx.x];                           \
-    cg = s_park[2][threadIdx.x]; cb = s_park[3][threadIdx.x];                          \
-    dep = s_park[4][threadIdx.x]; n0 = s_park[5][threadIdx.x];                         \
-    n1 = s_park[6][threadIdx.x]; n2 = s_park[7][threadIdx.x];                          \
-    cnt = __float_as_uint(s_park[8][threadIdx.x]);                                     \
-    last = __float_as_uint(s_park[9][threadIdx.x]);                                    \
-  } while (0)
 
-template <bool NAIVE, bool COUNT>
-__global__ void __launch_bounds__(kBlock, HGS_FWD_MINB) k_composite_fwd(CompositeArgs a) {
-  __shared__ SplatRec s_rec[kBlock];
-  __shared__ float s_park[10][kBlock];
-  const int tile = blockIdx.x;
-  const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int wx0 = tx * kTile + (warp & 1) * 8, wy0 = ty * kTile + (warp >> 1) * 4;
-  const int ix = wx0 + (lane & 7), iy = wy0 + (lane >> 3);
-  const bool inside = ix < a.width && iy < a.height;
-  int64_t lo, hi;
-  if (NAIVE) {
-    lo = 0;
-    hi = a.m;
-  } else {
-    lo = a.tile_off[tile];
-    hi = a.tile_off[tile + 1];
-  }
-  float T = 1.f, cr = 0.f, cg = 0.f, cb = 0.f, dep = 0.f, n0 = 0.f, n1 = 0.f, n2 = 0.f;
-  uint32_t cnt = 0, last = 0;
-  bool done = !inside;
-  uint32_t n_ev3 = 0, n_ev2 = 0, n_c3 = 0, n_c2 = 0;  // HGS_FLAG_COUNT
-  for (int64_t base = lo; base < hi; base += kBlock) {
-    __syncthreads();
-    const int64_t j = base + threadIdx.x;
-    if (j < hi) {
-      const uint32_t rk = NAIVE ? (uint32_t)j : a.tile_vals[j];
-      s_rec[threadIdx.x] = a.recs[rk];
-    }
-    __syncthreads();
-    const int nb = (int)(hi - base < kBlock ? hi - base : kBlock);
-    for (int w0 = 0; w0 < nb && !__all_sync(0xffffffffu, done); w0 += 32) {
-      const int el = w0 + lane;
-      bool rel = el < nb;
-      if (!NAIVE && rel) rel = bbox_overlaps(s_rec[el].r5, wx0, wy0, wx0 + 7, wy0 + 3);
-      uint32_t mask = __ballot_sync(0xffffffffu, rel);
-      while (mask) {
-        const int e = w0 + __ffs(mask) - 1;
-        mask &= mask - 1;
-        if (done) continue;
-        const SplatRec &r = s_rec[e];
-        if (!NAIVE && !in_bbox(r.r5, ix, iy)) continue;
-        const bool is3d = rec_is3d(r);
-        if (COUNT) (is3d ? n_ev3 : n_ev2) += 1;
-        PairEval p;
-        int c = eval_fast<false>(r, ix, iy, a.flags, p);
-        if (c == kAmbiguous) {
-          // rare: park the loop-carried state in shared memory so nothing
-          // accumulated is live across the out-of-line call
-          PARK_STATE();
-          const Resolved rs = resolve_pair(&s_rec[e], ix, iy, a.st, false);
-          UNPARK_STATE();
-          c = finish_resolved(rs, p) ? kContrib : kSkip;
-        }
-        if (c == kSkip) continue;
-        if (COUNT) (is3d ? n_c3 : n_c2) += 1;
-        const float at = p.at;
-        const float w = at * T;
-        const float4 c3 = r.r3, c4 = r.r4;
-        cr = fmaf(w, c3.y, cr);
-        cg = fmaf(w, c3.z, cg);
-        cb = fmaf(w, c3.w, cb);
-        dep = fmaf(w, r.r0.z, dep);
-        n0 = fmaf(w, c4.x, n0);
-        n1 = fmaf(w, c4.y, n1);
-        n2 = fmaf(w, c4.z, n2);
-        ++cnt;
-        last = (uint32_t)(base + e - lo) + 1u;
-        const float Tn = T * (1.f - at);
-        bool stop;
-        if (!(a.flags & HGS_FLAG_FAST) && fabsf(Tn - (float)kEarlyStopT) <= 2e-5f * (float)kEarlyStopT) {
-          T = Tn;
-          PARK_STATE();
-          stop = replay_T_below(a.recs, a.tile_vals, a.flags, a.st, lo, base + e, ix, iy);
-          UNPARK_STATE();
-        } else {
-          stop = Tn < (float)kEarlyStopT;
-          T = Tn;
-        }
-        if (stop) done = true;
-      }
-    }
-    if (__syncthreads_count(done) == kBlock) break;
-  }
-  if (COUNT) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      n_ev3 += __shfl_xor_sync(0xffffffffu, n_ev3, o);
-      n_ev2 += __shfl_xor_sync(0xffffffffu, n_ev2, o);
-      n_c3 += __shfl_xor_sync(0xffffffffu, n_c3, o);
-      n_c2 += __shfl_xor_sync(0xffffffffu, n_c2, o);
-    }
-    if (lane == 0) {
-      atomicAdd(&a.st->diag[2], (unsigned long long)n_ev3);
-      atomicAdd(&a.st->diag[3], (unsigned long long)n_ev2);
-      atomicAdd(&a.st->diag[4], (unsigned long long)n_c3);
-      atomicAdd(&a.st->diag[5], (unsigned long long)n_c2);
-    }
-  }
-  if (!inside) return;
-  const int64_t pix = (int64_t)iy * a.width + ix;
-  a.color[3 * pix + 0] = cr + a.bg[0] * T;
-  a.color[3 * pix + 1] = cg + a.bg[1] * T;
-  a.color[3 * pix + 2] = cb + a.bg[2] * T;
-  a.depth[pix] = dep;
-  a.trans[pix] = T;
-  if (a.alpha) a.alpha[pix] = 1.f - T;
-  if (a.normal) {
-    a.normal[3 * pix + 0] = n0;
-    a.normal[3 * pix + 1] = n1;
-    a.normal[3 * pix + 2] = n2;
-  }
-  a.pix_T[pix] = T;
-  a.pix_last[pix] = last;
-  a.pix_count[pix] = cnt;
-}
-
-template __global__ void k_composite_fwd<false, false>(CompositeArgs);
-template __global__ void k_composite_fwd<true, false>(CompositeArgs);
-template __global__ void k_composite_fwd<false, true>(CompositeArgs);
-template __global__ void k_composite_fwd<true, true>(CompositeArgs);
 
 }  // namespace hgs

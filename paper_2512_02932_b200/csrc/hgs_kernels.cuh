@@ -16,10 +16,33 @@ struct FrameState {
   unsigned long long k_total;
   uint32_t tile_counters[24];
   unsigned long long diag[16];  // see hgs_frame_stats in include/hgs.h
+  uint32_t n_fix_fwd, n_fix_bwd;  // deferred pixels (worklist lengths)
   SceneView sc;
   CamD cam;
   ModD mod;
 };
+
+// Deferred-exactness worklists.  The hot compositors contain no calls: a lane
+// whose next decision is ambiguous in float32 saves its exact state here and
+// retires; a fixup kernel resumes the pixel with float64-exact decisions.
+struct FwdFix {       // resume the forward walk of one pixel
+  uint32_t pix;       // iy * W + ix
+  uint32_t entry;     // tile-list position (global index) to resume at
+  uint32_t mode;      // 0: pair `entry` is ambiguous (state before it)
+                      // 1: early stop after `entry` is ambiguous (state after it)
+  uint32_t cnt, last;
+  float T, c0, c1, c2, dep, n0, n1, n2;
+  uint32_t pad[3];
+};
+static_assert(sizeof(FwdFix) == 64, "FwdFix is 64 B");
+
+struct BwdFix {       // resume the backward replay of one pixel, going down
+  uint32_t pix;
+  uint32_t entry;     // tile-list position (global index), inclusive
+  float T_run, S0, S1, S2, SD, SN0, SN1, SN2;
+  uint32_t pad[6];
+};
+static_assert(sizeof(BwdFix) == 64, "BwdFix is 64 B");
 
 struct CompositeArgs {
   // binning
@@ -35,6 +58,8 @@ struct CompositeArgs {
   float *pix_T;
   uint32_t *pix_last, *pix_count;
   FrameState *st;  // diagnostics + scene / camera for float64 re-checks
+  FwdFix *fwd_fix;  // (H * W) worklist
+  BwdFix *bwd_fix;  // (H * W) worklist
 };
 
 // log2 domain constants: at = ex2(arg), arg = log2(alpha_eff) - d * 0.5 log2(e)
@@ -42,7 +67,12 @@ constexpr float kHalfLog2e = 0.72134752044448170f;
 constexpr float kArgMinAlpha = -7.99435343685885793f;  // log2(1/255)
 constexpr float kArgClamp = -0.01449956969511509f;     // log2(0.99)
 constexpr float kEps = 5.96046448e-8f;                 // 2^-24
-constexpr float kCoarse2D = 0.05f;                     // log2 units; 2D precise bounds only inside
+constexpr float kCoarse2D = 0.05f;  // log2 units; 2D precise bounds only inside
+#ifndef HGS_EXACT_ENABLED
+#define HGS_EXACT_ENABLED 1  // 0: compile the compositors without the float64 re-check paths (experiments)
+#endif
+
+enum : int { kSkip = 0, kContrib = 1, kAmbiguous = 2 };  // pair decision outcomes
 
 __device__ __forceinline__ bool rec_is3d(const SplatRec &r) { return __float_as_uint(r.r4.w) >> 31; }
 __device__ __forceinline__ uint32_t rec_idx(const SplatRec &r) { return __float_as_uint(r.r4.w) & 0x7fffffffu; }
@@ -52,6 +82,20 @@ __device__ __forceinline__ bool in_bbox(const int4 q, int ix, int iy) {
   const int x0 = q.x & 0xffff, y0 = (int)((uint32_t)q.x >> 16);
   const int x1 = q.y & 0xffff, y1 = (int)((uint32_t)q.y >> 16);
   return !(ix < x0 || ix > x1 || iy < y0 || iy > y1);
+}
+
+// 32-bit mask of the pixels of an 8 x 4 warp block (lane = row * 8 + col,
+// origin (wx0, wy0)) that lie inside the inclusive bbox: bit `lane` is set iff
+// in_bbox(q, wx0 + lane % 8, wy0 + lane / 8).
+__device__ __forceinline__ uint32_t pixel_mask(const int4 q, int wx0, int wy0) {
+  const int x0 = (q.x & 0xffff) - wx0, y0 = (int)((uint32_t)q.x >> 16) - wy0;
+  const int x1 = (q.y & 0xffff) - wx0, y1 = (int)((uint32_t)q.y >> 16) - wy0;
+  const int c0 = max(x0, 0), c1 = min(x1, 7), r0 = max(y0, 0), r1 = min(y1, 3);
+  if (c0 > c1 || r0 > r1) return 0u;
+  const uint32_t cols = (0xffu << c0) & (0xffu >> (7 - c1));
+  const uint32_t rows = (0xfu << r0) & (0xfu >> (3 - r1));
+  const uint32_t spread = (rows & 1u) | ((rows & 2u) << 7) | ((rows & 4u) << 14) | ((rows & 8u) << 21);
+  return cols * spread;  // no carries: cols < 256, spread bits 8 apart
 }
 
 // bbox overlaps the pixel rectangle [rx0, rx1] x [ry0, ry1]
@@ -168,40 +212,47 @@ struct Resolved {
 // Out-of-line: exact decisions for a pair the fast path found ambiguous.
 // 2D pairs first get a first-order float32 error bound of the 2x2 solve;
 // anything still ambiguous is re-evaluated in float64 (pair_f64).
+// Precise first-order float32 error bound of a 2D pair that the coarse band
+// flagged (pure FP32 arithmetic, no calls: safe on the hot path).  Returns
+// kSkip / kContrib when the bound separates every decision, kAmbiguous if not.
+__device__ __forceinline__ int refine_2d(const SplatRec &r, const Geom &g, bool bwd) {
+  const float4 m1 = r.r1, m2 = r.r2;
+  const float m23 = r.r3.x;
+  const float A0 = fabsf(g.pxl * m2.z) + fabsf(m1.x), A1 = fabsf(g.pxl * m2.w) + fabsf(m1.y);
+  const float A3 = fabsf(g.pxl * m23) + fabsf(m1.z);
+  const float B0 = fabsf(g.pyl * m2.z) + fabsf(m1.w), B1 = fabsf(g.pyl * m2.w) + fabsf(m2.x);
+  const float B3 = fabsf(g.pyl * m23) + fabsf(m2.y);
+  const float ad = fabsf(g.den);
+  const float iad = rcp_approx(ad) * (1.f + 4.f * kEps);
+  const float dden = 6.f * kEps * (A0 * B1 + A1 * B0);
+  const float du = (6.f * kEps * (A1 * B3 + A3 * B1) + fabsf(g.u) * dden) * iad + 4.f * kEps * fabsf(g.u);
+  const float dv = (6.f * kEps * (A3 * B0 + A0 * B3) + fabsf(g.v) * dden) * iad + 4.f * kEps * fabsf(g.v);
+  const float e_ray = 2.f * (fabsf(g.u) * du + fabsf(g.v) * dv) + 4.f * kEps * g.dray;
+  const float e_scr = 8.f * kEps * g.dscr + 1e-6f * (fabsf(g.dx) + fabsf(g.dy));
+  const float margin = fmaf(g.ray ? e_ray : e_scr, kHalfLog2e, 1e-5f);
+  if (!(ad > (float)kDegenerateDen + dden) || !(margin < kCoarse2D)) return kAmbiguous;
+  if (g.arg < kArgMinAlpha - margin) return kSkip;
+  if (g.arg <= kArgMinAlpha + margin) return kAmbiguous;
+  if (bwd && (fabsf(g.arg - kArgClamp) <= margin || fabsf(g.dray - g.dscr) <= e_ray + e_scr)) return kAmbiguous;
+  return kContrib;
+}
+
 static __device__ __noinline__ Resolved resolve_pair(const SplatRec *rp, int ix, int iy, FrameState *st, bool bwd) {
   const SplatRec r = *rp;
   Geom g;
   geom_common(r, ix, iy, g);
-  bool amb = true;
   Resolved out{0.f, 0u};
   if (!rec_is3d(r)) {
     geom_2d_rows(r, g);
     if (!near_degenerate(g)) {
       geom_2d_solve(r, g);
-      const float4 m1 = r.r1, m2 = r.r2;
-      const float m23 = r.r3.x;
-      const float A0 = fabsf(g.pxl * m2.z) + fabsf(m1.x), A1 = fabsf(g.pxl * m2.w) + fabsf(m1.y);
-      const float A3 = fabsf(g.pxl * m23) + fabsf(m1.z);
-      const float B0 = fabsf(g.pyl * m2.z) + fabsf(m1.w), B1 = fabsf(g.pyl * m2.w) + fabsf(m2.x);
-      const float B3 = fabsf(g.pyl * m23) + fabsf(m2.y);
-      const float ad = fabsf(g.den);
-      const float dden = 6.f * kEps * (A0 * B1 + A1 * B0);
-      const float du = (6.f * kEps * (A1 * B3 + A3 * B1) + fabsf(g.u) * dden) / ad + 4.f * kEps * fabsf(g.u);
-      const float dv = (6.f * kEps * (A3 * B0 + A0 * B3) + fabsf(g.v) * dden) / ad + 4.f * kEps * fabsf(g.v);
-      const float e_ray = 2.f * (fabsf(g.u) * du + fabsf(g.v) * dv) + 4.f * kEps * g.dray;
-      const float e_scr = 8.f * kEps * g.dscr + 1e-6f * (fabsf(g.dx) + fabsf(g.dy));
-      const float margin = fmaf(g.ray ? e_ray : e_scr, kHalfLog2e, 1e-5f);
-      const bool deg_ok = ad > (float)kDegenerateDen + dden;
-      if (deg_ok && margin < kCoarse2D) {
-        if (g.arg < kArgMinAlpha - margin) return out;  // skip
-        amb = g.arg <= kArgMinAlpha + margin;
-        if (bwd && (fabsf(g.arg - kArgClamp) <= margin || fabsf(g.dray - g.dscr) <= e_ray + e_scr)) amb = true;
-        if (!amb) {
-          const bool cl = g.arg > kArgClamp;
-          out.at = cl ? 0.99f : ex2_approx(g.arg);
-          out.flags = 1u | (cl ? 2u : 0u) | (g.ray ? 4u : 0u);
-          return out;
-        }
+      const int c = refine_2d(r, g, bwd);
+      if (c == kSkip) return out;
+      if (c == kContrib) {
+        const bool cl = g.arg > kArgClamp;
+        out.at = cl ? 0.99f : ex2_approx(g.arg);
+        out.flags = 1u | (cl ? 2u : 0u) | (g.ray ? 4u : 0u);
+        return out;
       }
     }
   }
@@ -214,7 +265,6 @@ static __device__ __noinline__ Resolved resolve_pair(const SplatRec *rp, int ix,
   return out;
 }
 
-enum : int { kSkip = 0, kContrib = 1, kAmbiguous = 2 };
 
 // Evaluate a pair in float32 (fast path, no calls).  BWD additionally needs
 // the backward-only decisions (ray branch, clamp) and the 2D solve
@@ -228,7 +278,7 @@ __device__ __forceinline__ int eval_fast(const SplatRec &r, int ix, int iy, uint
   p.dy = g.dy;
   p.pxl = g.pxl;
   p.pyl = g.pyl;
-  const bool exact = !(flags & HGS_FLAG_FAST);
+  const bool exact = HGS_EXACT_ENABLED && !(flags & HGS_FLAG_FAST);
   bool amb = false;
   p.ray = false;
   if (rec_is3d(r)) {
@@ -253,8 +303,12 @@ __device__ __forceinline__ int eval_fast(const SplatRec &r, int ix, int iy, uint
       if (g.arg < kArgMinAlpha - (exact ? kCoarse2D : 0.f)) return kSkip;
       if (exact && (g.arg <= kArgMinAlpha + kCoarse2D ||
                     (BWD && (fabsf(g.arg - kArgClamp) <= kCoarse2D ||
-                             fabsf(g.dray - g.dscr) <= 0.02f * (g.dray + g.dscr)))))
-        amb = true;
+                             fabsf(g.dray - g.dscr) <= 0.02f * (g.dray + g.dscr))))) {
+        // coarse band hit: the precise bound usually separates the decision
+        const int c = refine_2d(r, g, BWD);
+        if (c == kSkip) return kSkip;
+        amb = c == kAmbiguous;
+      }
       p.ray = g.ray;
     }
     if (BWD) {
@@ -291,30 +345,33 @@ __device__ __forceinline__ bool eval_pair(const SplatRec &r, const SplatRec *rp,
 
 // Early-stop decision T < 1e-4 (_blend_py.py:111-113).  Near the threshold the
 // pixel's transmittance is replayed in float64 over its tile list.
+// Warp-cooperative: all 32 lanes call it with the same arguments.  32 entries
+// per step, each lane evaluates its entry with the exact decisions and the
+// float64 alpha; the float64 factors are multiplied across the warp.
 static __device__ __noinline__ bool replay_T_below(const SplatRec *recs, const uint32_t *tile_vals, uint32_t flags,
-                                                   FrameState *st, int64_t lo, int64_t upto, int ix, int iy) {
-  atomicAdd(&st->diag[1], 1ull);
+                                                   FrameState *st, uint32_t lo, uint32_t upto, int ix, int iy) {
+  const int lane = threadIdx.x & 31;
+  if (lane == 0) atomicAdd(&st->diag[1], 1ull);
   const bool naive = flags & HGS_FLAG_NAIVE;
   double T = 1.0;
-  for (int64_t j = lo; j <= upto; ++j) {
-    const uint32_t rk = naive ? (uint32_t)j : tile_vals[j];
-    const SplatRec r = recs[rk];
-    if (!naive && !in_bbox(r.r5, ix, iy)) continue;
-    PairEval p;
-    if (!eval_pair<false>(r, recs + rk, ix, iy, flags, st, p)) continue;
-    double at64;
-    bool ray64, cl64;
-    if (!pair_f64(st->sc, st->cam, st->mod, rec_idx(r), ix, iy, &at64, &ray64, &cl64)) continue;
-    T *= 1.0 - at64;
+  for (uint32_t base = lo; base <= upto; base += 32) {
+    const uint32_t j = base + lane;
+    double om = 1.0;
+    if (j <= upto) {
+      const uint32_t rk = naive ? j : tile_vals[j];
+      const SplatRec r = recs[rk];
+      PairEval p;
+      if ((naive || in_bbox(r.r5, ix, iy)) && eval_pair<false>(r, recs + rk, ix, iy, flags, st, p)) {
+        double at64;
+        bool ray64, cl64;
+        if (pair_f64(st->sc, st->cam, st->mod, rec_idx(r), ix, iy, &at64, &ray64, &cl64)) om = 1.0 - at64;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) om *= __shfl_xor_sync(0xffffffffu, om, o);
+    T *= om;
   }
   return T < kEarlyStopT;
-}
-
-__device__ __forceinline__ bool early_stop(float Tn, const CompositeArgs &a, int64_t lo, int64_t e, int ix, int iy) {
-  const float thr = (float)kEarlyStopT;
-  if (!(a.flags & HGS_FLAG_FAST) && fabsf(Tn - thr) <= 2e-5f * thr)
-    return replay_T_below(a.recs, a.tile_vals, a.flags, a.st, lo, e, ix, iy);
-  return Tn < thr;
 }
 
 struct BwdArgs {
@@ -354,9 +411,11 @@ __global__ void k_duplicate(const SplatRec *recs, const unsigned long long *pair
 __global__ void k_tile_ranges(const uint32_t *skeys, int64_t k, int64_t n_tiles, uint32_t *tile_off);
 template <bool NAIVE, bool COUNT>
 __global__ void k_composite_fwd(CompositeArgs a);
+__global__ void k_fixup_fwd(CompositeArgs a);
 template <int KG, bool EXT>
 __global__ void k_composite_bwd(BwdArgs b);
-__global__ void k_touched_scatter(const SplatRec *recs, const uint8_t *touched_rank, int64_t m, uint8_t *touched);
+template <int KG, bool EXT>
+__global__ void k_fixup_bwd(BwdArgs b);
 __global__ void k_chain_rule(ChainArgs c);
 __global__ void k_exchange_scan(int64_t n, const float *log_scale, const uint8_t *type_spec, double theta_e,
                                 float *eranks, ExchangeState *st);
