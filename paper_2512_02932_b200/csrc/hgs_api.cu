@@ -435,7 +435,13 @@ int hgs_backward(const hgs_scene *scene, const hgs_camera *camera, const hgs_set
     c.kg = kc;
     c.grads = grads + (int64_t)k0 * n * P;
     if (n > 0) {
-      k_chain_rule<<<grid_for(n, 128), 128, 0, s>>>(c);
+      const int grid = grid_for(n, 128);
+      switch (scene->sh_bases) {
+        case 1: k_chain_rule_t<0><<<grid, 128, 0, s>>>(c); break;
+        case 4: k_chain_rule_t<1><<<grid, 128, 0, s>>>(c); break;
+        case 9: k_chain_rule_t<2><<<grid, 128, 0, s>>>(c); break;
+        default: k_chain_rule_t<3><<<grid, 128, 0, s>>>(c); break;
+      }
       HGS_LAUNCHED();
     }
   }

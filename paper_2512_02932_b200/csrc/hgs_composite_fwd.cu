@@ -10,7 +10,7 @@
 #include "hgs_kernels.cuh"
 
 #ifndef HGS_FWD_MINB
-#define HGS_FWD_MINB 3  // CTAs per SM the hot compositor is register-budgeted for
+#define HGS_FWD_MINB 4  // CTAs per SM the hot compositor is register-budgeted for
 #endif
 
 namespace hgs {
@@ -73,7 +73,10 @@ __global__ void __launch_bounds__(kBlock, HGS_FWD_MINB) k_composite_fwd(Composit
         SplatRec r;
         r.r0 = __ldg(&g->r0); r.r1 = __ldg(&g->r1); r.r2 = __ldg(&g->r2);
         r.r3 = __ldg(&g->r3); r.r4 = __ldg(&g->r4); r.r5 = q;
-        wrec[lane] = r;
+        if (!NAIVE && rec_is3d(r) && cull_3d(r, pm, wx0, wy0))
+          pm = 0u;  // bbox hit, but the 1/255 ellipse misses every covered pixel
+        else
+          wrec[lane] = r;
       }
     }
     uint32_t rel = __ballot_sync(0xffffffffu, pm != 0u);

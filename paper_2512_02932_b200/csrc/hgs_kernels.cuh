@@ -98,6 +98,35 @@ __device__ __forceinline__ uint32_t pixel_mask(const int4 q, int wx0, int wy0) {
   return cols * spread;  // no carries: cols < 256, spread bits 8 apart
 }
 
+// Warp-level cull of a 3D splat whose bbox covers part of the warp's 8 x 4
+// block (pixel mask pm != 0): true if no pixel centre of the covered
+// rectangle can reach the 1/255 cutoff, i.e. the minimum of the conic
+// quadratic form over that rectangle exceeds the cutoff distance
+// d* = 2 ln(255 alpha_eff) (with a 1e-3 margin, far above float32 error, so
+// a pair the evaluation would keep is never culled).  Exact minimum of a
+// convex quadratic over a rectangle: 0 if the centre is inside, otherwise
+// on the boundary, at the clamped 1D minimiser of each edge.
+__device__ __forceinline__ bool cull_3d(const SplatRec &r, uint32_t pm, int wx0, int wy0) {
+  const float dstar = (r.r0.w - kArgMinAlpha) * (1.f / kHalfLog2e);
+  if (dstar < 0.f) return true;  // alpha_eff < 1/255: never contributes
+  // covered rectangle of pixel centres, relative to the splat centre
+  const int c0 = __ffs(pm) - 1;  // first covered lane gives the top-left
+  const int c1 = 31 - __clz(pm);  // last covered lane gives the bottom-right
+  const int4 q = r.r5;
+  const float X0 = (float)(wx0 + (c0 & 7) - q.z) + 0.5f - r.r0.x;
+  const float X1 = (float)(wx0 + (c1 & 7) - q.z) + 0.5f - r.r0.x;
+  const float Y0 = (float)(wy0 + (c0 >> 3) - q.w) + 0.5f - r.r0.y;
+  const float Y1 = (float)(wy0 + (c1 >> 3) - q.w) + 0.5f - r.r0.y;
+  if (X0 <= 0.f && 0.f <= X1 && Y0 <= 0.f && 0.f <= Y1) return false;
+  const float a = r.r1.x, b = r.r1.y, c = r.r1.z;
+  const float ia = rcp_approx(a), ic = rcp_approx(c);
+  auto qf = [&](float x, float y) { return fmaf(a * x, x, fmaf(2.f * b * x, y, c * y * y)); };
+  const float ya = fminf(fmaxf(-b * X0 * ic, Y0), Y1), yb = fminf(fmaxf(-b * X1 * ic, Y0), Y1);
+  const float xa = fminf(fmaxf(-b * Y0 * ia, X0), X1), xb = fminf(fmaxf(-b * Y1 * ia, X0), X1);
+  const float qmin = fminf(fminf(qf(X0, ya), qf(X1, yb)), fminf(qf(xa, Y0), qf(xb, Y1)));
+  return qmin > fmaf(dstar, 1.001f, 1e-3f);
+}
+
 // bbox overlaps the pixel rectangle [rx0, rx1] x [ry0, ry1]
 __device__ __forceinline__ bool bbox_overlaps(const int4 q, int rx0, int ry0, int rx1, int ry1) {
   const int x0 = q.x & 0xffff, y0 = (int)((uint32_t)q.x >> 16);
@@ -416,7 +445,8 @@ template <int KG, bool EXT>
 __global__ void k_composite_bwd(BwdArgs b);
 template <int KG, bool EXT>
 __global__ void k_fixup_bwd(BwdArgs b);
-__global__ void k_chain_rule(ChainArgs c);
+template <int DEG>
+__global__ void k_chain_rule_t(ChainArgs c);
 __global__ void k_exchange_scan(int64_t n, const float *log_scale, const uint8_t *type_spec, double theta_e,
                                 float *eranks, ExchangeState *st);
 __global__ void k_exchange_apply(int64_t n, float *log_scale, float *rotation, uint8_t *type_spec, double theta_e);
