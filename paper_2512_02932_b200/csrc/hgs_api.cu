@@ -256,9 +256,13 @@ int hgs_forward(const hgs_scene *scene, const hgs_camera *camera, const hgs_sett
   int64_t K = 0;
   if (m > 0) {
     HGS_CUDA(cudaMemsetAsync(at<char>(frame, L.lb_scan), 0, L.lb_scan_bytes, s));
-    k_preprocess<<<(unsigned)ceil_div(m, kScanThreads), kScanThreads, 0, s>>>(
-        sc, cam, mod, vals_sorted, m, at<SplatRec>(frame, L.recs), at<unsigned long long>(frame, L.pair_off),
-        at<unsigned long long>(frame, L.lb_scan), st);
+    // tile counts per rank go to the (now free) depth-key buffer
+    uint32_t *counts = at<uint32_t>(frame, L.keys_a);
+    k_preprocess<<<grid_for(m, 128), 128, 0, s>>>(sc, cam, mod, vals_sorted, m, at<SplatRec>(frame, L.recs),
+                                                  counts);
+    HGS_LAUNCHED();
+    k_scan_counts<<<(unsigned)ceil_div(m, kScanTile), kScanThreads, 0, s>>>(
+        counts, m, at<unsigned long long>(frame, L.pair_off), at<unsigned long long>(frame, L.lb_scan), st);
     HGS_LAUNCHED();
     unsigned long long kt;
     HGS_CUDA(cudaMemcpyAsync(&kt, &st->k_total, 8, cudaMemcpyDeviceToHost, s));

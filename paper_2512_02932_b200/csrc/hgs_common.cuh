@@ -74,30 +74,38 @@ static_assert(sizeof(SplatRec) == 96, "record must be 96 B");
 __device__ __forceinline__ double expit_d(double x) { return 1.0 / (1.0 + exp(-x)); }
 
 // core/sh.py:32-60
+template <typename F>
+__device__ __forceinline__ void sh_basis_t(int deg, F x, F y, F z, F *o);
+
 __device__ __forceinline__ void sh_basis_d(int deg, double x, double y, double z, double *o) {
-  o[0] = 0.28209479177387814;
+  sh_basis_t<double>(deg, x, y, z, o);
+}
+
+template <typename F>
+__device__ __forceinline__ void sh_basis_t(int deg, F x, F y, F z, F *o) {
+  o[0] = (F)0.28209479177387814;
   if (deg >= 1) {
-    o[1] = -0.4886025119029199 * y;
-    o[2] = 0.4886025119029199 * z;
-    o[3] = -0.4886025119029199 * x;
+    o[1] = (F)-0.4886025119029199 * y;
+    o[2] = (F)0.4886025119029199 * z;
+    o[3] = (F)-0.4886025119029199 * x;
   }
   if (deg >= 2) {
-    double xx = x * x, yy = y * y, zz = z * z;
-    o[4] = 1.0925484305920792 * x * y;
-    o[5] = -1.0925484305920792 * y * z;
-    o[6] = 0.31539156525252005 * (2.0 * zz - xx - yy);
-    o[7] = -1.0925484305920792 * x * z;
-    o[8] = 0.5462742152960396 * (xx - yy);
+    const F xx = x * x, yy = y * y, zz = z * z;
+    o[4] = (F)1.0925484305920792 * x * y;
+    o[5] = (F)-1.0925484305920792 * y * z;
+    o[6] = (F)0.31539156525252005 * ((F)2.0 * zz - xx - yy);
+    o[7] = (F)-1.0925484305920792 * x * z;
+    o[8] = (F)0.5462742152960396 * (xx - yy);
   }
   if (deg >= 3) {
-    double xx = x * x, yy = y * y, zz = z * z;
-    o[9] = -0.5900435899266435 * y * (3.0 * xx - yy);
-    o[10] = 2.890611442640554 * x * y * z;
-    o[11] = -0.4570457994644658 * y * (4.0 * zz - xx - yy);
-    o[12] = 0.3731763325901154 * z * (2.0 * zz - 3.0 * xx - 3.0 * yy);
-    o[13] = -0.4570457994644658 * x * (4.0 * zz - xx - yy);
-    o[14] = 1.445305721320277 * z * (xx - yy);
-    o[15] = -0.5900435899266435 * x * (xx - 3.0 * yy);
+    const F xx = x * x, yy = y * y, zz = z * z;
+    o[9] = (F)-0.5900435899266435 * y * ((F)3.0 * xx - yy);
+    o[10] = (F)2.890611442640554 * x * y * z;
+    o[11] = (F)-0.4570457994644658 * y * ((F)4.0 * zz - xx - yy);
+    o[12] = (F)0.3731763325901154 * z * ((F)2.0 * zz - (F)3.0 * xx - (F)3.0 * yy);
+    o[13] = (F)-0.4570457994644658 * x * ((F)4.0 * zz - xx - yy);
+    o[14] = (F)1.445305721320277 * z * (xx - yy);
+    o[15] = (F)-0.5900435899266435 * x * (xx - (F)3.0 * yy);
   }
 }
 
@@ -180,6 +188,9 @@ struct ProjD {
   bool quat_ok;
 };
 
+// COLOR64 = false evaluates the SH colour in float32 (the record stores a
+// float32 colour; the float64 path serves the exports and re-checks).
+template <bool COLOR64 = true>
 __device__ __forceinline__ void project_d(const SceneView &sc, int64_t i, const CamD &cam, const ModD &mod,
                                           ProjD &o) {
   double p[3];
@@ -242,15 +253,28 @@ __device__ __forceinline__ void project_d(const SceneView &sc, int64_t i, const 
   double vx = dl[0] / den, vy = dl[1] / den, vz = dl[2] / den;
   const int B = sc.sh_bases;
   const int deg = B == 1 ? 0 : (B == 4 ? 1 : (B == 9 ? 2 : 3));
-  double basis[16];
-  sh_basis_d(deg, vx, vy, vz, basis);
   const float *shc = sc.sh + (int64_t)3 * B * i;
+  if (COLOR64) {
+    double basis[16];
+    sh_basis_d(deg, vx, vy, vz, basis);
 #pragma unroll
-  for (int ch = 0; ch < 3; ++ch) {
-    double acc = 0.0;
-    for (int bb = 0; bb < B; ++bb) acc += (double)shc[ch * B + bb] * basis[bb];
-    double v = acc + 0.5;
-    o.color[ch] = v > 0.0 ? v : 0.0;
+    for (int ch = 0; ch < 3; ++ch) {
+      double acc = 0.0;
+      for (int bb = 0; bb < B; ++bb) acc += (double)shc[ch * B + bb] * basis[bb];
+      double v = acc + 0.5;
+      o.color[ch] = v > 0.0 ? v : 0.0;
+    }
+  } else {
+    float basis[16];
+    sh_basis_t<float>(deg, (float)vx, (float)vy, (float)vz, basis);
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch) {
+      float acc = 0.f;
+#pragma unroll
+      for (int bb = 0; bb < 16; ++bb)  // static indices keep basis[] in registers
+        if (bb < B) acc = fmaf(shc[ch * B + bb], basis[bb], acc);
+      o.color[ch] = fmaxf(acc + 0.5f, 0.f);
+    }
   }
   // extension: camera-space normal facing the camera
   int ax = 2;

@@ -103,35 +103,50 @@ __device__ __forceinline__ void write_record(const ProjD &o, uint32_t idx, Splat
 
 // One thread per depth rank r < M: float64 projection of Gaussian
 // sorted_idx[r], record write, tile count, exclusive scan -> pair offsets.
-__global__ void __launch_bounds__(kScanThreads) k_preprocess(SceneView sc, CamD cam, ModD mod,
-                                                             const uint32_t *__restrict__ sorted_idx, int64_t m,
-                                                             SplatRec *__restrict__ recs,
-                                                             unsigned long long *__restrict__ pair_off,
-                                                             unsigned long long *__restrict__ scan_lb,
-                                                             FrameState *__restrict__ st) {
+__global__ void __launch_bounds__(128) k_preprocess(SceneView sc, CamD cam, ModD mod,
+                                                    const uint32_t *__restrict__ sorted_idx, int64_t m,
+                                                    SplatRec *__restrict__ recs, uint32_t *__restrict__ counts) {
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < m; r += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t i = sorted_idx[r];
+    ProjD o;
+    project_d<false>(sc, i, cam, mod, o);
+    bbox_d(o, cam.width, cam.height);
+    write_record(o, i, recs + r);
+    counts[r] = tile_count_of(o.bbox);
+  }
+}
+
+// Exclusive scan of the per-rank tile counts into pair offsets (decoupled
+// look-back, kScanItems counts per thread); the last tile writes K.
+__global__ void __launch_bounds__(kScanThreads) k_scan_counts(const uint32_t *__restrict__ counts, int64_t m,
+                                                              unsigned long long *__restrict__ pair_off,
+                                                              unsigned long long *__restrict__ scan_lb,
+                                                              FrameState *__restrict__ st) {
   __shared__ uint32_t s_tile;
   __shared__ unsigned long long s_warp[32];
   __shared__ unsigned long long s_excl;
   if (threadIdx.x == 0) s_tile = atomicAdd(&st->tile_counters[0], 1u);
   __syncthreads();
   const uint32_t tile = s_tile;
-  const int64_t base = (int64_t)tile * kScanThreads;
-  const int64_t r = base + threadIdx.x;
-  uint32_t cnt = 0;
-  if (r < m) {
-    uint32_t i = sorted_idx[r];
-    ProjD o;
-    project_d(sc, i, cam, mod, o);
-    bbox_d(o, cam.width, cam.height);
-    write_record(o, i, recs + r);
-    cnt = tile_count_of(o.bbox);
+  const int64_t base = (int64_t)tile * kScanTile + (int64_t)threadIdx.x * kScanItems;
+  uint32_t c[kScanItems];
+  unsigned long long sum = 0;
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) {
+    c[k] = base + k < m ? counts[base + k] : 0u;
+    sum += c[k];
   }
   unsigned long long total;
-  unsigned long long ex = block_exclusive_scan_u64(cnt, s_warp, total);
+  const unsigned long long ex = block_exclusive_scan_u64(sum, s_warp, total);
   if (threadIdx.x == 0) s_excl = scan_lookback(scan_lb, tile, total);
   __syncthreads();
-  if (r < m) pair_off[r] = s_excl + ex;
-  if (base + kScanThreads >= m && threadIdx.x == 0) st->k_total = s_excl + total;
+  unsigned long long run = s_excl + ex;
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) {
+    if (base + k < m) pair_off[base + k] = run;
+    run += c[k];
+  }
+  if ((int64_t)(tile + 1) * kScanTile >= m && threadIdx.x == 0) st->k_total = s_excl + total;
 }
 
 // ------------------------------------------------------------ duplicate

@@ -434,7 +434,9 @@ __global__ void k_init_state(SceneView sc, CamD cam, ModD mod, FrameState *st);
 __global__ void k_depth_keys(SceneView sc, CamD cam, unsigned long long *keys, uint32_t *vals, uint32_t *hist,
                              FrameState *st);
 __global__ void k_preprocess(SceneView sc, CamD cam, ModD mod, const uint32_t *sorted_idx, int64_t m, SplatRec *recs,
-                             unsigned long long *pair_off, unsigned long long *scan_lb, FrameState *st);
+                             uint32_t *counts);
+__global__ void k_scan_counts(const uint32_t *counts, int64_t m, unsigned long long *pair_off,
+                              unsigned long long *scan_lb, FrameState *st);
 __global__ void k_duplicate(const SplatRec *recs, const unsigned long long *pair_off, int64_t m, int tiles_x,
                             uint32_t *pkeys, uint32_t *pvals, int n_digits, uint32_t *hist);
 __global__ void k_tile_ranges(const uint32_t *skeys, int64_t k, int64_t n_tiles, uint32_t *tile_off);
