@@ -49,6 +49,9 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=2, choices=[2, 3, 5],
+                    help="BASELINE.json config: 2 (headline, default), 3 (DTU-like + exchange), "
+                         "5 (64-view batch sharded over the GPUs)")
     ap.add_argument("--n", type=int, default=1_000_000)
     ap.add_argument("--width", type=int, default=1920)
     ap.add_argument("--height", type=int, default=1080)
@@ -189,10 +192,115 @@ def run_reference(a):
 
 
 # --------------------------------------------------------------- our arm
+def run_extra(a):
+    """--config 3 / 5 (BASELINE.json configs[2], configs[4]); evidence lines,
+    the driver's headline run is config 2."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2512_02932_b200 import _lib, exchange, grad, parallel, raster
+    from paper_2512_02932_b200.core import DeviceGaussians
+    from paper_2512_02932_b200.settings import ExchangeConfig, RenderSettings
+    from paper_2512_02932_b200.synthetic import f32_exact, orbit_cameras, synthetic_scene
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    st = RenderSettings()
+    flags = _lib.HGS_FLAG_FAST if a.fast else 0
+    if a.config == 3:
+        n, W, H = 300_000, 800, 600
+        scene, cam = synthetic_scene(n, W, H, 3, seed=0)
+        cams, views = [cam], [0]
+        workload = ("config 3: synthetic 300k-Gaussian mixed scene, 800x600, SH 3, RGB + depth + "
+                    "normal outputs and upstream gradients, Adaptive Type Exchange pass every step")
+        unit = "iters/s"
+    else:
+        n, W, H = a.n, a.width, a.height
+        scene, _ = synthetic_scene(n, W, H, 3, seed=0)
+        scene.center[:] = f32_exact(scene.center - scene.center.mean(axis=0))
+        cams = orbit_cameras(scene, 64, W, H, radius=5.0)
+        views = parallel.shard_views(len(cams), rank, world)
+        workload = ("config 5: synthetic 1M-Gaussian scene centred at the origin, 64 cameras on a "
+                    "circle of radius 5, 1920x1080, fwd + bwd per view, views sharded over %d GPU(s), "
+                    "one gradient all-reduce per step" % world)
+        unit = "views/s"
+    ds = DeviceGaussians.from_host(scene, dev)
+    P = 11 + 3 * ds.sh_bases
+    gen = torch.Generator(device=dev).manual_seed(99 + rank)
+    pg = torch.randn((1, H, W, 3), device=dev, generator=gen)
+    dg = torch.randn((1, H, W), device=dev, generator=gen) * 0.1 if a.config == 3 else None
+    ng = torch.randn((1, H, W, 3), device=dev, generator=gen) * 0.1 if a.config == 3 else None
+    acc = torch.zeros(n * P, dtype=torch.float32, device=dev)
+    gbuf = torch.empty((1, n * P), dtype=torch.float32, device=dev)
+    tbuf = torch.empty(n, dtype=torch.uint8, device=dev)
+    scratch = torch.empty(_lib.lib().hgs_backward_scratch_bytes(n, 1), dtype=torch.uint8, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    xcfg = ExchangeConfig()
+    info = {}
+
+    def step():
+        acc.zero_()
+        for v in views:
+            _, frame = raster.rasterize(ds, cams[v], st, flags)
+            grad.backward_device(frame, pg, depth_grads=dg, normal_grads=ng, grads_out=gbuf,
+                                 touched_out=tbuf, scratch=scratch)
+            acc.add_(gbuf[0])
+            info["K"] = frame.pair_count
+        if world > 1:
+            parallel.allreduce_grads(acc)
+        if a.config == 3:
+            info["exchange"] = exchange.exchange_pass_device(ds, xcfg)
+
+    for _ in range(a.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    s_ev = [torch.cuda.Event(enable_timing=True) for _ in range(a.steps)]
+    e_ev = [torch.cuda.Event(enable_timing=True) for _ in range(a.steps)]
+    with ClockSampler(local) as clocks:
+        for i in range(a.steps):
+            flush.fill_(i & 0xff)
+            s_ev[i].record()
+            step()
+            e_ev[i].record()
+        torch.cuda.synchronize()
+    ms = float(np.mean([s_ev[i].elapsed_time(e_ev[i]) for i in range(a.steps)]))
+    if world > 1:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t[0])
+    per_step = len(cams) if a.config == 5 else 1
+    value = per_step * 1000.0 / ms if a.config == 5 else world * 1000.0 / ms
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": unit, "n_gpus": world, "steps": a.steps,
+                "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True,
+                "scaling": "strong" if a.config == 5 else "weak", "vs_baseline": None,
+                "dtype": "fp32", "data": "synthetic (seeded generator, SURVEY.md 8d)",
+                "config": {"workload": workload, "n_gaussians": n, "width": W, "height": H,
+                           "views_per_step": per_step, "l2": "flushed between timed steps"},
+                "clocks": clocks.summary(), "last_K_pairs": info.get("K")}
+        if a.config == 3 and "exchange" in info:
+            rep = info["exchange"]
+            line["exchange_last_step"] = {"n_3d_to_2d": rep.n_3d_to_2d, "n_2d_to_3d": rep.n_2d_to_3d,
+                                          "n_2d": rep.n_2d, "n_3d": rep.n_3d}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def main():
     a = parse()
     if a.impl == "reference":
         run_reference(a)
+        return
+    if a.config in (3, 5):
+        run_extra(a)
         return
     import torch
     import torch.distributed as dist
