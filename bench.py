@@ -79,56 +79,92 @@ def workload_config(a, n_gpus):
 
 # ------------------------------------------------------------------ clocks
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clocks + throttle reasons sampled DURING the timed region: NVML
+    polled every 10 ms from a thread (nvidia-smi -lms 200 as a fallback), so
+    even a sub-second timed region yields tens of samples."""
 
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
 
-    def __init__(self, gpu_index):
+    def __init__(self, gpu_index, period_s=0.01):
         self.gpu = gpu_index
-        self.rows = []
+        self.period = period_s
+        self.sm, self.mx, self.reasons = [], [], set()
         self.proc = None
+        self.nvml = None
+        self.stop = threading.Event()
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.gpu), "--query-gpu=" + self.Q,
-                 "--format=csv,noheader,nounits", "-lms", "200"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
-            self.t.start()
-        except OSError:
-            self.proc = None
+            import pynvml
+            pynvml.nvmlInit()
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+            idx = int(vis.split(",")[self.gpu]) if vis and vis.split(",")[0].isdigit() else self.gpu
+            self.nvml = (pynvml, pynvml.nvmlDeviceGetHandleByIndex(idx))
+            self.t = threading.Thread(target=self._poll_nvml, daemon=True)
+        except Exception:
+            self.nvml = None
+            try:
+                self.proc = subprocess.Popen(
+                    ["nvidia-smi", "-i", str(self.gpu), "--query-gpu=" + self.Q,
+                     "--format=csv,noheader,nounits", "-lms", "200"],
+                    stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                self.t = threading.Thread(target=self._read_smi, daemon=True)
+            except OSError:
+                self.proc = None
+                return self
+        self.t.start()
         return self
 
-    def _read(self):
+    def _poll_nvml(self):
+        nv, h = self.nvml
+        bits = {"hw_slowdown": nv.nvmlClocksEventReasonHwSlowdown,
+                "hw_thermal_slowdown": nv.nvmlClocksEventReasonHwThermalSlowdown,
+                "sw_thermal_slowdown": nv.nvmlClocksEventReasonSwThermalSlowdown,
+                "sw_power_cap": nv.nvmlClocksEventReasonSwPowerCap}
+        while True:
+            try:
+                self.sm.append(float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)))
+                self.mx.append(float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                for nm, b in bits.items():
+                    if r & b:
+                        self.reasons.add(nm)
+            except Exception:
+                pass
+            if self.stop.wait(self.period):
+                return
+
+    def _read_smi(self):
         for line in self.proc.stdout:
-            self.rows.append([x.strip() for x in line.split(",")])
+            r = [x.strip() for x in line.split(",")]
+            if r[1].replace(".", "").isdigit():
+                self.sm.append(float(r[1]))
+            if r[2].replace(".", "").isdigit():
+                self.mx.append(float(r[2]))
+            for nm, v in zip(self.NAMES, r[5:9]):
+                if v.lower() == "active":
+                    self.reasons.add(nm)
 
     def __exit__(self, *exc):
+        self.stop.set()
         if self.proc is not None:
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=5)
             except Exception:
                 self.proc.kill()
+        if self.nvml is not None or self.proc is not None:
             self.t.join(timeout=2)
 
     def summary(self):
-        if not self.rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = set()
-        for r in self.rows:
-            for nm, v in zip(names, r[5:9]):
-                if v.lower() == "active":
-                    reasons.add(nm)
-        return {"sm_mhz": float(np.median(sm)) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
-                "samples": len(self.rows)}
+        if not self.sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["clock sampling unavailable"]}
+        return {"sm_mhz": float(np.median(self.sm)), "sm_max_mhz": max(self.mx) if self.mx else None,
+                "reasons": sorted(self.reasons), "samples": len(self.sm),
+                "source": "nvml 10 ms" if self.nvml is not None else "nvidia-smi 200 ms"}
 
 
 # ------------------------------------------------------------ CPU baseline
@@ -472,7 +508,11 @@ def main():
         host_scene = GaussianSet(scene.center, scene.log_scale, scene.rotation, scene.opacity_logit,
                                  scene.sh_coeffs, scene.type_spec)
         pg_host = pg[0].double().cpu().numpy()
-        h2d = sum(getattr(host_scene, f).nbytes for f in GaussianSet.FIELDS) + pg_host.nbytes
+        # float32 crosses PCIe (the float64 <-> float32 conversion runs on the
+        # host cores into pinned staging, _hostio.py); uint8 type mask
+        h2d = 4 * (host_scene.center.size + host_scene.log_scale.size + host_scene.rotation.size
+                   + host_scene.opacity_logit.size + host_scene.sh_coeffs.size
+                   + pg_host.size) + host_scene.type_spec.size
         ts = []
         for i in range(a.e2e_steps + 1):
             torch.cuda.synchronize()
@@ -482,8 +522,8 @@ def main():
             torch.cuda.synchronize()
             if i:
                 ts.append(time.perf_counter() - t0)
-        d2h = (out.color.nbytes + out.depth.nbytes + out.transmittance.nbytes + out.alpha.nbytes
-               + out.normal.nbytes + gr.flat().nbytes + touched.nbytes)
+        d2h = (4 * (out.color.size + out.depth.size + out.transmittance.size + out.alpha.size
+                    + out.normal.size + gr.flat().size) + touched.size)
         tt = float(np.mean(ts))
         if world > 1:
             t = torch.tensor([tt], device=dev, dtype=torch.float64)
@@ -492,7 +532,7 @@ def main():
         e2e = {"value": world / tt, "unit": "iters/s", "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h),
                "path": "raster.render(GaussianSet float64 numpy) + grad.backward(numpy pixel_grad)"
-                       " -> numpy float64 images and ParamGrads; wall clock with device syncs"}
+                       " -> numpy float64 images and ParamGrads (float32 over PCIe via pinned staging, f64<->f32 on the host cores); wall clock with device syncs"}
 
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:

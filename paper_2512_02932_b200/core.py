@@ -142,15 +142,20 @@ class DeviceGaussians:
 
     @classmethod
     def from_host(cls, scene, device="cuda", validate=False):
+        """Upload a host scene: float64 -> float32 on the host cores into
+        pinned staging, pipelined with the DMA (_hostio.upload)."""
         import torch
 
-        def up(a, dt):
-            return torch.from_numpy(np.ascontiguousarray(a)).to(device=device, dtype=dt,
-                                                                 non_blocking=False)
-        return cls(up(scene.center, torch.float32), up(scene.log_scale, torch.float32),
-                   up(scene.rotation, torch.float32), up(scene.opacity_logit, torch.float32),
-                   up(scene.sh_coeffs, torch.float32), up(scene.type_spec, torch.uint8),
-                   extent=scene.extent, validate=validate)
+        from ._hostio import upload
+        if isinstance(device, str):
+            device = torch.device(device)
+        if device.type == "cuda" and device.index is None:
+            device = torch.device("cuda", torch.cuda.current_device())
+        t = upload([(scene.center, torch.float32), (scene.log_scale, torch.float32),
+                    (scene.rotation, torch.float32), (scene.opacity_logit, torch.float32),
+                    (scene.sh_coeffs, torch.float32), (scene.type_spec, torch.uint8)],
+                   device, tag="scene")
+        return cls(*t, extent=scene.extent, validate=validate)
 
     def to_host(self):
         return GaussianSet(*(getattr(self, f).detach().cpu().numpy() for f in self.FIELDS),

@@ -95,7 +95,7 @@ def _views(flat_block, n, B):
     out = []
     for shape in ((n, 3), (n, 3), (n, 4), (n,), (n, 3, B)):
         size = int(np.prod(shape))
-        out.append(flat_block[o:o + size].view(*shape))
+        out.append(flat_block[o:o + size].reshape(shape))
         o += size
     return ParamGrads(*out)
 
@@ -104,8 +104,11 @@ def _as_device(a, dev, name, shape):
     import torch
     if a is None:
         return None
-    t = a if isinstance(a, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(a))
-    t = t.to(device=dev, dtype=torch.float32)
+    if isinstance(a, torch.Tensor):
+        t = a.to(device=dev, dtype=torch.float32)
+    else:
+        from ._hostio import upload
+        t = upload([(np.asarray(a), torch.float32)], dev, tag="grad_in." + name)[0]
     if t.dim() == len(shape) - 1:
         t = t.unsqueeze(0)
     if tuple(t.shape[1:]) != shape[1:]:
@@ -173,10 +176,13 @@ def backward(scene, camera, output, pixel_grad, depth_grad=None, normal_grad=Non
     grads, touched = backward_device(frame, pg, dg, ng, ag)
     n, B = frame.scene.count, frame.scene.sh_bases
     if host:
-        g = grads.double().cpu()
-        out = [ParamGrads(*(x.numpy() for x in (lambda v: (v.center, v.log_scale, v.rotation,
-                                                            v.opacity_logit, v.sh_coeffs))(
-            _views(g[k], n, B)))) for k in range(kg)]
+        from ._hostio import download
+        g = download([grads], tag="grads")[0]
+        out = []
+        for k in range(kg):
+            v = _views(g[k], n, B)
+            out.append(ParamGrads(v.center, v.log_scale, v.rotation, v.opacity_logit,
+                                  v.sh_coeffs))
         touched = touched.cpu().numpy().astype(bool)
     else:
         out = [_views(grads[k], n, B) for k in range(kg)]

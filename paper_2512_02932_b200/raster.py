@@ -301,7 +301,9 @@ def _render(scene, camera, settings, naive, fast):
                             scene.sh_coeffs, scene.type_spec)
     ds = DeviceGaussians.from_host(scene)
     imgs, frame = rasterize(ds, camera, settings, flags)
-    host = {k: v.double().cpu().numpy() for k, v in imgs.items()}
+    from ._hostio import download
+    keys = ("color", "depth", "transmittance", "alpha", "normal")
+    host = dict(zip(keys, download([imgs[k] for k in keys], tag="images")))
     return RenderOutput(host["color"], host["depth"], host["transmittance"], host["alpha"],
                         host["normal"], frame, scene_fingerprint(scene), host_scene=scene)
 
