@@ -25,10 +25,17 @@ HGS_FLAG_NAIVE = 0x1
 HGS_FLAG_FAST = 0x2
 HGS_FLAG_COUNT = 0x4
 
-# Every symbol include/hgs.h declares.
+# hgs_train.h constants
+HGS_LOSS_L1, HGS_LOSS_SSIM, HGS_LOSS_LOW, HGS_LOSS_HIGH, HGS_LOSS_COLOR = range(5)
+HGS_LOSS_COUNT = 5
+COMBINE_MODES = {"projection": 0, "naive": 1, "mask": 2}
+
+# Every symbol include/hgs.h and include/hgs_train.h declare.
 EXPORTS = ("hgs_abi_version", "hgs_status_string", "hgs_frame_bytes", "hgs_forward",
            "hgs_backward_scratch_bytes", "hgs_backward", "hgs_exchange",
-           "hgs_frame_export_arrays", "hgs_blend_log", "hgs_frame_stats")
+           "hgs_frame_export_arrays", "hgs_blend_log", "hgs_frame_stats",
+           "hgs_loss_scratch_bytes", "hgs_image_losses", "hgs_dwt_level1", "hgs_dwt_inverse",
+           "hgs_combine_gradients", "hgs_adam_step", "hgs_combine_adam_step")
 
 _vp = ctypes.c_void_p
 _i64 = ctypes.c_int64
@@ -70,6 +77,22 @@ class FrameInfo(ctypes.Structure):
 class ExchangeReport(ctypes.Structure):
     _fields_ = [("n_3d_to_2d", _i64), ("n_2d_to_3d", _i64), ("n_2d", _i64), ("n_3d", _i64),
                 ("erank_hist", _i64 * 20)]
+
+
+class LossWeights(ctypes.Structure):
+    _fields_ = [("lam", ctypes.c_double), ("lambda_low", ctypes.c_double),
+                ("lambda_high", ctypes.c_double)]
+
+
+class Params(ctypes.Structure):
+    _fields_ = [("n", _i64), ("sh_bases", _i32), ("reserved", _i32),
+                ("center", _vp), ("log_scale", _vp), ("rotation", _vp),
+                ("opacity_logit", _vp), ("sh", _vp)]
+
+
+class AdamCfg(ctypes.Structure):
+    _fields_ = [("lr", ctypes.c_float * 5), ("beta1", ctypes.c_float), ("beta2", ctypes.c_float),
+                ("eps", ctypes.c_float), ("step", _i64)]
 
 
 class FrameExport(ctypes.Structure):
@@ -118,6 +141,16 @@ def lib():
     L.hgs_blend_log.argtypes = [P(Scene), P(Camera), P(Settings), _vp, P(FrameInfo), _vp, _vp,
                                 _vp, _vp, _vp, _vp]
     L.hgs_frame_stats.argtypes = [_vp, P(FrameInfo), _vp, _vp]
+    L.hgs_loss_scratch_bytes.restype = ctypes.c_size_t
+    L.hgs_loss_scratch_bytes.argtypes = [_i32, _i32, _i32]
+    L.hgs_image_losses.argtypes = [_i32, _i32, _i32, _vp, _vp, P(LossWeights), _vp, _vp, _vp,
+                                   ctypes.c_size_t, _vp]
+    L.hgs_dwt_level1.argtypes = [_i32, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp]
+    L.hgs_dwt_inverse.argtypes = [_i32, _i32, _i32, _vp, _vp, _vp, _vp, _i32, _vp, _vp]
+    L.hgs_combine_gradients.argtypes = [_i64, _i32, _vp, _vp, _vp, _vp, _i32, _vp, _vp, _vp]
+    L.hgs_adam_step.argtypes = [P(Params), _vp, _vp, _vp, P(AdamCfg), _vp]
+    L.hgs_combine_adam_step.argtypes = [P(Params), _vp, _vp, _vp, _vp, _i32, _vp, _vp, P(AdamCfg),
+                                        _vp, _vp]
     if L.hgs_abi_version() != 1:
         _load_error = "libhgs.so ABI version mismatch"
         raise ExtensionError(_load_error)
@@ -200,3 +233,9 @@ def frame_stats(frame):
     check(lib().hgs_frame_stats(ptr(frame.buf), frame.info, out.ctypes.data_as(ctypes.c_void_p),
                                 current_stream_handle(frame.buf.device)), "hgs_frame_stats")
     return out
+
+
+def params_struct(ds):
+    """hgs_params (mutable scene) of a DeviceGaussians."""
+    return Params(ds.count, ds.sh_bases, 0, ds.center.data_ptr(), ds.log_scale.data_ptr(),
+                  ds.rotation.data_ptr(), ds.opacity_logit.data_ptr(), ds.sh_coeffs.data_ptr())

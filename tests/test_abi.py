@@ -12,7 +12,9 @@ REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 def _header_symbols():
-    src = open(os.path.join(REPO, "include", "hgs.h")).read()
+    inc = os.path.join(REPO, "include")
+    src = "".join(open(os.path.join(inc, f)).read() for f in sorted(os.listdir(inc))
+                  if f.endswith(".h"))
     return sorted(set(re.findall(r"^\s*(?:int|size_t|const char \*)\s*(hgs_\w+)\s*\(", src, re.M)))
 
 
@@ -56,6 +58,22 @@ def test_struct_sizes_match_header():
     assert ctypes.sizeof(_lib.Scene) == 8 + 4 + 4 + 6 * 8
     assert ctypes.sizeof(_lib.Camera) == 4 * 8 + 8 + 16 * 8 + 2 * 8
     assert ctypes.sizeof(_lib.FrameInfo) == 4 * 8 + 4 * 4 + 8 + 4 + 4 + 16
+    assert ctypes.sizeof(_lib.LossWeights) == 3 * 8
+    assert ctypes.sizeof(_lib.Params) == 8 + 4 + 4 + 5 * 8
+    assert ctypes.sizeof(_lib.AdamCfg) == 5 * 4 + 3 * 4 + 8
+
+
+def test_train_host_entry_points(L):
+    # scratch sizes grow with the image; invalid shapes report 0 / CONFIG
+    assert L.hgs_loss_scratch_bytes(64, 64, 3) < L.hgs_loss_scratch_bytes(128, 64, 3)
+    assert L.hgs_loss_scratch_bytes(0, 64, 3) == 0
+    from paper_2512_02932_b200 import _lib
+    w = _lib.LossWeights(0.2, 0.2, 0.4)
+    assert L.hgs_image_losses(0, 8, 3, None, None, w, None, None, None, 0, None) == 1
+    assert L.hgs_combine_gradients(10, 5, None, None, None, None, 0, None, None, None) == 1
+    cfg = _lib.AdamCfg((ctypes.c_float * 5)(1, 1, 1, 1, 1), 0.9, 0.999, 1e-15, 0)
+    prm = _lib.Params(0, 1, 0, None, None, None, None, None)
+    assert L.hgs_adam_step(prm, None, None, None, cfg, None) == 1  # step must be >= 1
 
 
 def test_errors_are_reference_classes():
