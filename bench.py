@@ -49,8 +49,9 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", type=int, default=2, choices=[2, 3, 5],
+    ap.add_argument("--config", type=int, default=2, choices=[2, 3, 4, 5],
                     help="BASELINE.json config: 2 (headline, default), 3 (DTU-like + exchange), "
+                         "4 (3M Gaussians, full frequency-decoupled training step), "
                          "5 (64-view batch sharded over the GPUs)")
     ap.add_argument("--n", type=int, default=1_000_000)
     ap.add_argument("--width", type=int, default=1920)
@@ -330,10 +331,138 @@ def run_extra(a):
         dist.destroy_process_group()
 
 
+def run_train(a):
+    """--config 4 (BASELINE.json configs[3]): 3M-Gaussian synthetic scene at
+    1080p, SH 3; one step = the full frequency-decoupled training step of one
+    view (SPEC.md:402-405): render -> L_color / L_low / L_high and their
+    (3, H, W, 3) upstream gradients -> backward with KG = 3 -> per-Gaussian
+    gradient surgery (Alg. 1, projection mode) -> Adam -> quaternion
+    renormalisation.  Under torchrun every rank trains on its own view and the
+    combined gradient is all-reduced before the (replicated) Adam step."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2512_02932_b200 import freq, grad, optim, parallel, raster
+    from paper_2512_02932_b200.core import DeviceGaussians
+    from paper_2512_02932_b200.settings import RenderSettings
+    from paper_2512_02932_b200.synthetic import synthetic_scene
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    n = 3_000_000 if a.n == 1_000_000 else a.n
+    W, H = a.width, a.height
+    scene, cam = synthetic_scene(n, W, H, 3, seed=0)
+    st = RenderSettings()
+    ds = DeviceGaussians.from_host(scene, dev)
+    # target image: render of an independent scene of the same statistics
+    tscene, _ = synthetic_scene(n, W, H, 3, seed=100 + rank)
+    gt_imgs, _ = raster.rasterize(DeviceGaussians.from_host(tscene, dev), cam, st)
+    gt = gt_imgs["color"].clone()
+    del tscene, gt_imgs
+    w = freq.LossWeights()
+    opt = optim.Adam(ds)
+    P = 11 + 3 * ds.sh_bases
+    comb = torch.empty(n * P, dtype=torch.float32, device=dev) if world > 1 else None
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    def ev():
+        return torch.cuda.Event(enable_timing=True)
+
+    def step(evs=None):
+        if world == 1:
+            return optim.train_step(ds, cam, gt, opt, w, st, events=evs)
+        if evs:
+            evs[0].record()
+        imgs, frame = raster.rasterize(ds, cam, st)
+        if evs:
+            evs[1].record()
+        losses, stack = freq.image_losses(imgs["color"], gt, w)
+        if evs:
+            evs[2].record()
+        g, _ = grad.backward_device(frame, stack)
+        if evs:
+            evs[3].record()
+        nc = freq.combine_gradients_device(g[0], g[1], g[2], ds.type_spec, w.mode, out=comb)[1]
+        parallel.allreduce_grads(comb)
+        opt.step(comb)
+        return optim.TrainStepResult(losses, nc, frame.pair_count, imgs["color"])
+
+    for _ in range(a.warmup):
+        res = step()
+    torch.cuda.synchronize()
+    l0 = res.losses.cpu().tolist()
+    if world > 1:
+        dist.barrier()
+    K = a.steps
+    s_ev = [ev() for _ in range(K)]
+    e_ev = [ev() for _ in range(K)]
+    st_ev = [[ev() for _ in range(4)] for _ in range(K)]
+    with ClockSampler(local) as clocks:
+        for i in range(K):
+            flush.fill_(i & 0xff)
+            s_ev[i].record()
+            res = step(st_ev[i])
+            e_ev[i].record()
+        torch.cuda.synchronize()
+    ms = float(np.mean([s_ev[i].elapsed_time(e_ev[i]) for i in range(K)]))
+    names = ["render", "losses(L1+SSIM+DWT, KG=3 stack)", "backward(KG=3)"]
+    stages = {nm: float(np.mean([st_ev[i][j].elapsed_time(st_ev[i][j + 1]) for i in range(K)]))
+              for j, nm in enumerate(names)}
+    stages["surgery+adam(+allreduce)"] = float(np.mean([st_ev[i][3].elapsed_time(e_ev[i])
+                                                       for i in range(K)]))
+    if world > 1:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t[0])
+    peaks = json.load(open(MEASURED_PEAKS)) if os.path.exists(MEASURED_PEAKS) else {}
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    # HBM roofline of the two new HBM-bound stages (algorithmic bytes, DESIGN.md)
+    loss_bytes = H * W * 3 * 52 + 0
+    opt_bytes = n * 4 * P * (6 + 3) if world == 1 else n * 4 * P * (1 + 3 + 3)
+    stage_roofs = {
+        "losses(L1+SSIM+DWT, KG=3 stack)": {"GB/s": loss_bytes / stages[names[1]] / 1e6,
+                                            "hbm_frac": loss_bytes / stages[names[1]] / 1e6
+                                            / hbm_peak},
+        "surgery+adam(+allreduce)": {"GB/s": opt_bytes / stages["surgery+adam(+allreduce)"] / 1e6,
+                                     "hbm_frac": opt_bytes / stages["surgery+adam(+allreduce)"]
+                                     / 1e6 / hbm_peak}}
+    if rank == 0:
+        l1 = res.losses.cpu().tolist()
+        line = {"metric": METRIC, "value": world * 1000.0 / ms, "unit": "iters/s", "n_gpus": world,
+                "steps": K, "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "fp32",
+                "data": "synthetic (seeded generator, SURVEY.md 8d); target = render of an "
+                        "independent synthetic scene",
+                "config": {"workload": "config 4: synthetic %d-Gaussian scene, %dx%d, SH 3, full "
+                                       "frequency-decoupled training step per view (render, "
+                                       "L_color/L_low/L_high, backward KG=3, gradient surgery "
+                                       "(projection), Adam, quaternion renormalisation)"
+                                       % (n, W, H),
+                           "n_gaussians": n, "width": W, "height": H, "views_per_gpu_per_step": 1,
+                           "parallelism": "dp%d (combined gradient all-reduced)" % world
+                           if world > 1 else "single GPU",
+                           "l2": "flushed between timed steps (256 MiB write)"},
+                "stages_ms": stages, "stage_rooflines": stage_roofs, "clocks": clocks.summary(),
+                "K_pairs": res.pair_count,
+                "loss_first_warmup_step": l0, "loss_last_step": l1,
+                "n_conflicts_last_step": int(res.n_conflicts.item())}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def main():
     a = parse()
     if a.impl == "reference":
         run_reference(a)
+        return
+    if a.config == 4:
+        run_train(a)
         return
     if a.config in (3, 5):
         run_extra(a)
