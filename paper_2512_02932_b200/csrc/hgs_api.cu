@@ -373,10 +373,10 @@ template <int KG>
 static void launch_bwd(const BwdArgs &b, int64_t n_tiles, bool ext, cudaStream_t s) {
   // hot replay, then the float64-exact fixup of the deferred pixels
   if (ext) {
-    k_composite_bwd<KG, true><<<(unsigned)n_tiles, kBlock, 0, s>>>(b);
+    k_composite_bwd<KG, true><<<(unsigned)n_tiles, kBwdThreads, 0, s>>>(b);
     k_fixup_bwd<KG, true><<<kFixupBlocks, 256, 0, s>>>(b);
   } else {
-    k_composite_bwd<KG, false><<<(unsigned)n_tiles, kBlock, 0, s>>>(b);
+    k_composite_bwd<KG, false><<<(unsigned)n_tiles, kBwdThreads, 0, s>>>(b);
     k_fixup_bwd<KG, false><<<kFixupBlocks, 256, 0, s>>>(b);
   }
 }

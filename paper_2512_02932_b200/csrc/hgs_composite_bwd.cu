@@ -20,6 +20,9 @@ namespace hgs {
 //  3D: 6-8 = dL/dcov2d (a, b, c);  2D ray: 6-8 = dL/dM0 (cols 0,1,3),
 //  9-11 = dL/dM1, 12-14 = dL/dM3 w.r.t. anchor-relative pixels; 15 unused.
 // Extension slots (separate array, 4 per (Gaussian, kg)): z, normal xyz.
+#ifndef HGS_BWD_MINB1
+#define HGS_BWD_MINB1 5  // CTAs per SM the KG = 1 backward is register-budgeted for
+#endif
 constexpr int kAcc = 16;
 constexpr int kAccExt = 4;
 
@@ -105,9 +108,9 @@ __device__ __forceinline__ void pair_grads(const SplatRec &r, const PairEval &p,
   const float z = r.r0.z;
 #pragma unroll
   for (int k = 0; k < KG; ++k) {
-    v[k][0] = G.gp[k][0] * w;
-    v[k][1] = G.gp[k][1] * w;
-    v[k][2] = G.gp[k][2] * w;
+    v[k][0] += G.gp[k][0] * w;
+    v[k][1] += G.gp[k][1] * w;
+    v[k][2] += G.gp[k][2] * w;
     float d_at = G.gp[k][0] * (c3.y * T_k - S.s0 * inv_om) + G.gp[k][1] * (c3.z * T_k - S.s1 * inv_om) +
                  G.gp[k][2] * (c3.w * T_k - S.s2 * inv_om);
     if (EXT) {
@@ -115,22 +118,22 @@ __device__ __forceinline__ void pair_grads(const SplatRec &r, const PairEval &p,
       d_at += G.gn[k][0] * (c4.x * T_k - S.sn0 * inv_om) + G.gn[k][1] * (c4.y * T_k - S.sn1 * inv_om) +
               G.gn[k][2] * (c4.z * T_k - S.sn2 * inv_om);
       d_at += G.ga[k] * (T_fin * inv_om);
-      ve[k][0] = G.gd[k] * w;
-      ve[k][1] = G.gn[k][0] * w;
-      ve[k][2] = G.gn[k][1] * w;
-      ve[k][3] = G.gn[k][2] * w;
+      ve[k][0] += G.gd[k] * w;
+      ve[k][1] += G.gn[k][0] * w;
+      ve[k][2] += G.gn[k][1] * w;
+      ve[k][3] += G.gn[k][2] * w;
     }
     if (!p.clamped) {
       const float da = d_at * at;  // = dL/dalpha_eff * alpha_eff * exp(-d/2)
-      v[k][3] = da;
+      v[k][3] += da;
       if (is3d) {
         const float4 cn = r.r1;
         const float vx = cn.x * p.u + cn.y * p.v, vy = cn.y * p.u + cn.z * p.v;
-        v[k][4] = vx * da;
-        v[k][5] = vy * da;
-        v[k][6] = 0.5f * da * vx * vx;
-        v[k][7] = 0.5f * da * vx * vy;
-        v[k][8] = 0.5f * da * vy * vy;
+        v[k][4] += vx * da;
+        v[k][5] += vy * da;
+        v[k][6] += 0.5f * da * vx * vx;
+        v[k][7] += 0.5f * da * vx * vy;
+        v[k][8] += 0.5f * da * vy * vy;
       } else if (p.ray) {
         const float du = -da * p.u, dv = -da * p.v;
         const float id = p.inv_den;
@@ -140,129 +143,149 @@ __device__ __forceinline__ void pair_grads(const SplatRec &r, const PairEval &p,
         const float dhv0 = (du * (p.u * p.hu1) + dv * (p.hu3 + p.v * p.hu1)) * id;
         const float dhv1 = (du * (-p.hu3 - p.u * p.hu0) + dv * (-p.v * p.hu0)) * id;
         const float dhv3 = (du * p.hu1 + dv * (-p.hu0)) * id;
-        v[k][6] = -dhu0;
-        v[k][7] = -dhu1;
-        v[k][8] = -dhu3;
-        v[k][9] = -dhv0;
-        v[k][10] = -dhv1;
-        v[k][11] = -dhv3;
-        v[k][12] = p.pxl * dhu0 + p.pyl * dhv0;
-        v[k][13] = p.pxl * dhu1 + p.pyl * dhv1;
-        v[k][14] = p.pxl * dhu3 + p.pyl * dhv3;
+        v[k][6] += -dhu0;
+        v[k][7] += -dhu1;
+        v[k][8] += -dhu3;
+        v[k][9] += -dhv0;
+        v[k][10] += -dhv1;
+        v[k][11] += -dhv3;
+        v[k][12] += p.pxl * dhu0 + p.pyl * dhv0;
+        v[k][13] += p.pxl * dhu1 + p.pyl * dhv1;
+        v[k][14] += p.pxl * dhu3 + p.pyl * dhv3;
       } else {
-        v[k][4] = 4.f * p.dx * da;
-        v[k][5] = 4.f * p.dy * da;
+        v[k][4] += 4.f * p.dx * da;
+        v[k][5] += 4.f * p.dy * da;
       }
     }
   }
 }
 
+// One CTA (4 warps) per 16 x 16 tile; a warp owns an 8 x 8 block and each
+// lane two pixels of it, (x, y) and (x, y + 4).  Every staged splat is walked
+// once for both pixels of a lane: the chunk staging, the splat header and --
+// the dominant per-splat cost -- the 16-slot warp reduction + atomic flush
+// are shared by 64 pixels instead of 32, while the per-pixel math is
+// unchanged (a pixel's evaluation runs only where its 8 x 4 half is covered).
 template <int KG, bool EXT>
-__global__ void __launch_bounds__(kBlock, 3) k_composite_bwd(BwdArgs b) {
+__global__ void __launch_bounds__(kBwdThreads, KG == 1 ? HGS_BWD_MINB1 : 4) k_composite_bwd(BwdArgs b) {
   const CompositeArgs &a = b.c;
-  __shared__ SplatRec s_rec[kBlock / 32][32];
+  __shared__ SplatRec s_rec[kBwdThreads / 32][32];
   const int tile = blockIdx.x;
   const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int wx0 = tx * kTile + (warp & 1) * 8, wy0 = ty * kTile + (warp >> 1) * 4;
-  const int ix = wx0 + (lane & 7), iy = wy0 + (lane >> 3);
-  const bool inside = ix < a.width && iy < a.height;
+  const int wx0 = tx * kTile + (warp & 1) * 8, wy0 = ty * kTile + (warp >> 1) * 8;
+  const int ix = wx0 + (lane & 7);
   const bool naive = a.flags & HGS_FLAG_NAIVE;
   const uint32_t lane_bit = 1u << lane;
   const uint32_t lo = naive ? 0u : a.tile_off[tile];
   const int64_t HW = (int64_t)a.width * a.height;
-  const uint32_t pix = (uint32_t)iy * (uint32_t)a.width + (uint32_t)ix;
-  uint32_t last = 0;
-  float T_fin = 1.f;
-  PixGrads<KG, EXT> G;
-  G.load(b, inside, pix, HW);
-  if (inside) {
-    last = a.pix_last[pix];
-    T_fin = a.pix_T[pix];
+  int iy[2];
+  bool inside[2], dead[2];
+  uint32_t pix[2], last[2];
+  float T_fin[2], T_run[2];
+  Suffix S[2];
+  PixGrads<KG, EXT> G[2];
+  uint32_t warp_last = 0;
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    iy[q] = wy0 + (lane >> 3) + 4 * q;
+    inside[q] = ix < a.width && iy[q] < a.height;
+    pix[q] = (uint32_t)iy[q] * (uint32_t)a.width + (uint32_t)ix;
+    G[q].load(b, inside[q], pix[q], HW);
+    last[q] = inside[q] ? a.pix_last[pix[q]] : 0u;
+    T_fin[q] = inside[q] ? a.pix_T[pix[q]] : 1.f;
+    T_run[q] = T_fin[q];
+    S[q] = Suffix{a.bg[0] * T_fin[q], a.bg[1] * T_fin[q], a.bg[2] * T_fin[q], 0.f, 0.f, 0.f, 0.f};
+    dead[q] = false;
+    warp_last = max(warp_last, last[q]);
   }
-  uint32_t warp_last = last;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) warp_last = max(warp_last, __shfl_xor_sync(0xffffffffu, warp_last, o));
   const uint32_t warp_end = lo + warp_last;  // exclusive
-  float T_run = T_fin;
-  Suffix S{a.bg[0] * T_fin, a.bg[1] * T_fin, a.bg[2] * T_fin, 0.f, 0.f, 0.f, 0.f};
   const int slot = transpose_slot(lane);
   const bool count = a.flags & HGS_FLAG_COUNT;
-  bool dead = false;  // deferred to k_fixup_bwd
   uint32_t n_ev = 0, n_c3 = 0, n_cr = 0, n_cl = 0;
   SplatRec *wrec = s_rec[warp];
 
   for (uint32_t top = warp_end, start; top > lo; top = start) {
     start = top - lo > 32u ? top - 32u : lo;
     const uint32_t j = start + lane;
-    uint32_t pm = 0u;
+    uint32_t pm0 = 0u, pm1 = 0u;
     if (j < top) {
       const uint32_t rk = naive ? j : __ldg(a.tile_vals + j);
       const SplatRec *g = a.recs + rk;
       const int4 q = __ldg(&g->r5);
-      pm = naive ? 0xffffffffu : pixel_mask(q, wx0, wy0);
-      if (pm) {
+      pm0 = naive ? 0xffffffffu : pixel_mask(q, wx0, wy0);
+      pm1 = naive ? 0xffffffffu : pixel_mask(q, wx0, wy0 + 4);
+      if (pm0 | pm1) {
         SplatRec r;
         r.r0 = __ldg(&g->r0); r.r1 = __ldg(&g->r1); r.r2 = __ldg(&g->r2);
         r.r3 = __ldg(&g->r3); r.r4 = __ldg(&g->r4); r.r5 = q;
-        if (!naive && rec_is3d(r) && cull_3d(r, pm, wx0, wy0))
-          pm = 0u;  // bbox hit, but the 1/255 ellipse misses every covered pixel
-        else
-          wrec[lane] = r;
+        if (!naive && rec_is3d(r)) {  // the 1/255 ellipse may miss a covered half
+          if (pm0 && cull_3d(r, pm0, wx0, wy0)) pm0 = 0u;
+          if (pm1 && cull_3d(r, pm1, wx0, wy0 + 4)) pm1 = 0u;
+        }
+        if (pm0 | pm1) wrec[lane] = r;
       }
     }
-    uint32_t rel = __ballot_sync(0xffffffffu, pm != 0u);
+    uint32_t rel = __ballot_sync(0xffffffffu, (pm0 | pm1) != 0u);
     __syncwarp();
     while (rel) {
       const int e = 31 - __clz(rel);
       rel &= ~(1u << e);
-      const uint32_t m = __shfl_sync(0xffffffffu, pm, e);
+      const uint32_t m0 = __shfl_sync(0xffffffffu, pm0, e), m1 = __shfl_sync(0xffffffffu, pm1, e);
       const uint32_t jj = start + e;
       const SplatRec &r = wrec[e];
-      bool act = !dead && inside && (m & lane_bit) && jj - lo < last;
-      PairEval p;
-      if (count && act) ++n_ev;
-      const int c = act ? eval_fast<true>(r, ix, iy, a.flags, p) : kSkip;
-      if (c == kAmbiguous) {
-        BwdFix f;
-        f.pix = pix; f.entry = jj; f.T_run = T_run;
-        f.S0 = S.s0; f.S1 = S.s1; f.S2 = S.s2; f.SD = S.sd; f.SN0 = S.sn0; f.SN1 = S.sn1; f.SN2 = S.sn2;
-#pragma unroll
-        for (int i = 0; i < 6; ++i) f.pad[i] = 0;
-        b.c.bwd_fix[atomicAdd(&a.st->n_fix_bwd, 1u)] = f;
-        dead = true;
-      }
-      act = c == kContrib;
-      if (!__any_sync(0xffffffffu, act)) continue;
-      const bool is3d = rec_is3d(r);
-      const uint32_t gidx = rec_idx(r);
       float v[KG][16];
       float ve[KG][4];
 #pragma unroll
       for (int k = 0; k < KG; ++k) {
 #pragma unroll
-        for (int s = 0; s < 16; ++s) v[k][s] = 0.f;
+        for (int s2 = 0; s2 < 16; ++s2) v[k][s2] = 0.f;
 #pragma unroll
-        for (int s = 0; s < 4; ++s) ve[k][s] = 0.f;
+        for (int s2 = 0; s2 < 4; ++s2) ve[k][s2] = 0.f;
       }
-      if (act) {
-        if (count) {
-          if (is3d) ++n_c3; else if (p.ray) ++n_cr; else ++n_cl;
+      bool any = false;
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const uint32_t m = q ? m1 : m0;
+        const bool act = !dead[q] && inside[q] && (m & lane_bit) && jj - lo < last[q];
+        PairEval p;
+        if (count && act) ++n_ev;
+        const int c = act ? eval_fast<true>(r, ix, iy[q], a.flags, p) : kSkip;
+        if (c == kAmbiguous) {
+          BwdFix f;
+          f.pix = pix[q]; f.entry = jj; f.T_run = T_run[q];
+          f.S0 = S[q].s0; f.S1 = S[q].s1; f.S2 = S[q].s2; f.SD = S[q].sd;
+          f.SN0 = S[q].sn0; f.SN1 = S[q].sn1; f.SN2 = S[q].sn2;
+#pragma unroll
+          for (int i = 0; i < 6; ++i) f.pad[i] = 0;
+          b.c.bwd_fix[atomicAdd(&a.st->n_fix_bwd, 1u)] = f;
+          dead[q] = true;
         }
-        const float inv_om = 1.f / (1.f - p.at);
-        T_run *= inv_om;  // transmittance before this splat
-        pair_grads<KG, EXT>(r, p, T_run, inv_om, T_fin, S, G, v, ve);
-        const float w = p.at * T_run;
-        S.s0 = fmaf(r.r3.y, w, S.s0);
-        S.s1 = fmaf(r.r3.z, w, S.s1);
-        S.s2 = fmaf(r.r3.w, w, S.s2);
-        if (EXT) {
-          S.sd = fmaf(r.r0.z, w, S.sd);
-          S.sn0 = fmaf(r.r4.x, w, S.sn0);
-          S.sn1 = fmaf(r.r4.y, w, S.sn1);
-          S.sn2 = fmaf(r.r4.z, w, S.sn2);
+        if (c == kContrib) {
+          any = true;
+          if (count) {
+            if (rec_is3d(r)) ++n_c3; else if (p.ray) ++n_cr; else ++n_cl;
+          }
+          const float inv_om = 1.f / (1.f - p.at);
+          T_run[q] *= inv_om;  // transmittance before this splat
+          pair_grads<KG, EXT>(r, p, T_run[q], inv_om, T_fin[q], S[q], G[q], v, ve);
+          const float w = p.at * T_run[q];
+          S[q].s0 = fmaf(r.r3.y, w, S[q].s0);
+          S[q].s1 = fmaf(r.r3.z, w, S[q].s1);
+          S[q].s2 = fmaf(r.r3.w, w, S[q].s2);
+          if (EXT) {
+            S[q].sd = fmaf(r.r0.z, w, S[q].sd);
+            S[q].sn0 = fmaf(r.r4.x, w, S[q].sn0);
+            S[q].sn1 = fmaf(r.r4.y, w, S[q].sn1);
+            S[q].sn2 = fmaf(r.r4.z, w, S[q].sn2);
+          }
         }
       }
+      if (!__any_sync(0xffffffffu, any)) continue;
+      const bool is3d = rec_is3d(r);
+      const uint32_t gidx = rec_idx(r);
       if (lane == 0) b.touched[gidx] = 1;
 #pragma unroll
       for (int k = 0; k < KG; ++k) {
@@ -272,11 +295,11 @@ __global__ void __launch_bounds__(kBlock, 3) k_composite_bwd(BwdArgs b) {
           atomicAdd(b.acc + ((int64_t)gidx * KG + k) * kAcc + slot, tot);
         if (EXT) {
 #pragma unroll
-          for (int s = 0; s < 4; ++s) {
-            float x = ve[k][s];
+          for (int s2 = 0; s2 < 4; ++s2) {
+            float x = ve[k][s2];
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-            ve[k][s] = x;
+            ve[k][s2] = x;
           }
           if (lane < 4) {
             const float x = lane == 0 ? ve[k][0] : (lane == 1 ? ve[k][1] : (lane == 2 ? ve[k][2] : ve[k][3]));
@@ -286,7 +309,7 @@ __global__ void __launch_bounds__(kBlock, 3) k_composite_bwd(BwdArgs b) {
       }
     }
     __syncwarp();  // the next chunk overwrites this warp's staging slots
-    if (__all_sync(0xffffffffu, dead || !inside)) break;
+    if (__all_sync(0xffffffffu, (dead[0] || !inside[0]) && (dead[1] || !inside[1]))) break;
   }
   if (count) {
 #pragma unroll

@@ -73,6 +73,7 @@ constexpr float kCoarse2D = 0.05f;  // log2 units; 2D precise bounds only inside
 #endif
 
 enum : int { kSkip = 0, kContrib = 1, kAmbiguous = 2 };  // pair decision outcomes
+constexpr int kBwdThreads = 128;  // backward compositor: 4 warps per tile, 2 pixels per lane
 
 __device__ __forceinline__ bool rec_is3d(const SplatRec &r) { return __float_as_uint(r.r4.w) >> 31; }
 __device__ __forceinline__ uint32_t rec_idx(const SplatRec &r) { return __float_as_uint(r.r4.w) & 0x7fffffffu; }
