@@ -221,9 +221,9 @@ __global__ void __launch_bounds__(kBwdThreads, KG == 1 ? HGS_BWD_MINB1 : 4) k_co
         SplatRec r;
         r.r0 = __ldg(&g->r0); r.r1 = __ldg(&g->r1); r.r2 = __ldg(&g->r2);
         r.r3 = __ldg(&g->r3); r.r4 = __ldg(&g->r4); r.r5 = q;
-        if (!naive && rec_is3d(r)) {  // the 1/255 ellipse may miss a covered half
-          if (pm0 && cull_3d(r, pm0, wx0, wy0)) pm0 = 0u;
-          if (pm1 && cull_3d(r, pm1, wx0, wy0 + 4)) pm1 = 0u;
+        if (!naive) {  // the 1/255 support may miss a covered half
+          if (pm0 && cull_splat(r, pm0, wx0, wy0)) pm0 = 0u;
+          if (pm1 && cull_splat(r, pm1, wx0, wy0 + 4)) pm1 = 0u;
         }
         if (pm0 | pm1) wrec[lane] = r;
       }

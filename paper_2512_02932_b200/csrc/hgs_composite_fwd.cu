@@ -73,8 +73,8 @@ __global__ void __launch_bounds__(kBlock, HGS_FWD_MINB) k_composite_fwd(Composit
         SplatRec r;
         r.r0 = __ldg(&g->r0); r.r1 = __ldg(&g->r1); r.r2 = __ldg(&g->r2);
         r.r3 = __ldg(&g->r3); r.r4 = __ldg(&g->r4); r.r5 = q;
-        if (!NAIVE && rec_is3d(r) && cull_3d(r, pm, wx0, wy0))
-          pm = 0u;  // bbox hit, but the 1/255 ellipse misses every covered pixel
+        if (!NAIVE && cull_splat(r, pm, wx0, wy0))
+          pm = 0u;  // bbox hit, but the 1/255 support misses every covered pixel
         else
           wrec[lane] = r;
       }

@@ -128,6 +128,72 @@ __device__ __forceinline__ bool cull_3d(const SplatRec &r, uint32_t pm, int wx0,
   return qmin > fmaf(dstar, 1.001f, 1e-3f);
 }
 
+// Minimum of the convex quadratic form a X^2 + 2b XY + c Y^2 (a, c > 0,
+// ac > b^2) over the rectangle [X0, X1] x [Y0, Y1]: 0 if the origin is inside,
+// otherwise on the boundary at the clamped 1D minimiser of each edge.
+__device__ __forceinline__ float rect_min_quad(float a, float b, float c, float X0, float X1, float Y0, float Y1) {
+  if (X0 <= 0.f && 0.f <= X1 && Y0 <= 0.f && 0.f <= Y1) return 0.f;
+  const float ia = rcp_approx(a), ic = rcp_approx(c);
+  auto qf = [&](float x, float y) { return fmaf(a * x, x, fmaf(2.f * b * x, y, c * y * y)); };
+  const float ya = fminf(fmaxf(-b * X0 * ic, Y0), Y1), yb = fminf(fmaxf(-b * X1 * ic, Y0), Y1);
+  const float xa = fminf(fmaxf(-b * Y0 * ia, X0), X1), xb = fminf(fmaxf(-b * Y1 * ia, X0), X1);
+  return fminf(fminf(qf(X0, ya), qf(X1, yb)), fminf(qf(xa, Y0), qf(xb, Y1)));
+}
+
+// Warp-level cull of a 2D surfel whose bbox covers part of the warp's 8 x 4
+// block: true if no covered pixel centre can reach the 1/255 cutoff through
+// either branch of d = min(d_ray, d_screen) (_blend_py.py:17-44).
+//  * screen branch: 4 |p - c|^2 <= d*  -- a circle of radius sqrt(d*)/2;
+//  * ray branch: u^2 + v^2 <= d* with (u, v, 1) ~ adj(H) p, H = [m0'; m1'; m2]
+//    the anchor-relative homography of the record -- the image of the disk
+//    is the conic p^T adj(H)^T diag(1, 1, -d*) adj(H) p <= 0 (squares: no
+//    sign ambiguity of the homogeneous scale).  Used only when that conic is a
+//    well-conditioned ellipse; the cull needs both branches out by a 5%
+//    margin in d, far above the float32 error of the conic, so a pair the
+//    exact evaluation would keep is never culled (degenerate cases keep).
+__device__ __forceinline__ bool cull_2d(const SplatRec &r, uint32_t pm, int wx0, int wy0) {
+  const float dstar = (r.r0.w - kArgMinAlpha) * (1.f / kHalfLog2e);
+  if (dstar < 0.f) return true;  // alpha_eff < 1/255: never contributes
+  const int c0 = __ffs(pm) - 1, c1 = 31 - __clz(pm);
+  const int4 q = r.r5;
+  // covered rectangle of anchor-relative pixel centres
+  const float PX0 = (float)(wx0 + (c0 & 7) - q.z) + 0.5f, PX1 = (float)(wx0 + (c1 & 7) - q.z) + 0.5f;
+  const float PY0 = (float)(wy0 + (c0 >> 3) - q.w) + 0.5f, PY1 = (float)(wy0 + (c1 >> 3) - q.w) + 0.5f;
+  // screen (low-pass) branch: squared distance from the centre to the rectangle
+  const float ex = fmaxf(fmaxf(PX0 - r.r0.x, r.r0.x - PX1), 0.f);
+  const float ey = fmaxf(fmaxf(PY0 - r.r0.y, r.r0.y - PY1), 0.f);
+  if (4.f * (ex * ex + ey * ey) <= fmaf(dstar, 1.05f, 1e-3f)) return false;
+  // ray branch: conic of the disk image
+  const float h00 = r.r1.x, h01 = r.r1.y, h02 = r.r1.z;   // m0' (cols 0, 1, 3)
+  const float h10 = r.r1.w, h11 = r.r2.x, h12 = r.r2.y;   // m1'
+  const float h20 = r.r2.z, h21 = r.r2.w, h22 = r.r3.x;   // m2
+  // A = adj(H): A p = (U1, U2, U3) up to scale
+  const float A00 = h11 * h22 - h12 * h21, A01 = h02 * h21 - h01 * h22, A02 = h01 * h12 - h02 * h11;
+  const float A10 = h12 * h20 - h10 * h22, A11 = h00 * h22 - h02 * h20, A12 = h02 * h10 - h00 * h12;
+  const float A20 = h10 * h21 - h11 * h20, A21 = h01 * h20 - h00 * h21, A22 = h00 * h11 - h01 * h10;
+  // C = A^T diag(1, 1, -d*) A  (symmetric 3x3)
+  auto cij = [&](float a0i, float a1i, float a2i, float a0j, float a1j, float a2j) {
+    return fmaf(a0i, a0j, fmaf(a1i, a1j, -dstar * a2i * a2j));
+  };
+  const float ca = cij(A00, A10, A20, A00, A10, A20), cb = cij(A00, A10, A20, A01, A11, A21);
+  const float cc = cij(A01, A11, A21, A01, A11, A21), cd = cij(A00, A10, A20, A02, A12, A22);
+  const float ce = cij(A01, A11, A21, A02, A12, A22), cf = cij(A02, A12, A22, A02, A12, A22);
+  const float det = ca * cc - cb * cb;
+  // well-conditioned ellipse only: PD quadratic part, axis ratio <= ~30
+  if (!(ca > 0.f) || !(det > 1e-3f * (ca + cc) * (ca + cc) * 0.25f)) return false;
+  const float idet = 1.f / det;
+  const float x0 = (cb * ce - cc * cd) * idet, y0 = (cb * cd - ca * ce) * idet;  // centre
+  const float fp = cf + cd * x0 + ce * y0;  // Q at the centre (< 0: non-empty interior)
+  if (!(fp < -1e-2f * fabsf(cf))) return false;
+  const float s = -1.f / fp;  // normalise: interior is Qn <= 1
+  const float qmin = rect_min_quad(ca * s, cb * s, cc * s, PX0 - x0, PX1 - x0, PY0 - y0, PY1 - y0);
+  return qmin > 1.05f;
+}
+
+__device__ __forceinline__ bool cull_splat(const SplatRec &r, uint32_t pm, int wx0, int wy0) {
+  return rec_is3d(r) ? cull_3d(r, pm, wx0, wy0) : cull_2d(r, pm, wx0, wy0);
+}
+
 // bbox overlaps the pixel rectangle [rx0, rx1] x [ry0, ry1]
 __device__ __forceinline__ bool bbox_overlaps(const int4 q, int rx0, int ry0, int rx1, int ry1) {
   const int x0 = q.x & 0xffff, y0 = (int)((uint32_t)q.x >> 16);
