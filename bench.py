@@ -59,7 +59,8 @@ def parse():
     ap.add_argument("--sh-degree", type=int, default=3)
     ap.add_argument("--kg", type=int, default=1)
     ap.add_argument("--fast", action="store_true", help="HGS_FLAG_FAST (skip f64 re-checks)")
-    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--e2e-warmup", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-crop", type=int, default=4, help="cpu sample = 1/crop^2 of the frame")
@@ -643,13 +644,13 @@ def main():
                    + host_scene.opacity_logit.size + host_scene.sh_coeffs.size
                    + pg_host.size) + host_scene.type_spec.size
         ts = []
-        for i in range(a.e2e_steps + 1):
+        for i in range(a.e2e_warmup + a.e2e_steps):
             torch.cuda.synchronize()
             t0 = time.perf_counter()
             out = raster.render(host_scene, cam, st, fast=a.fast)
             gr, touched = grad.backward(host_scene, cam, out, pg_host)
             torch.cuda.synchronize()
-            if i:
+            if i >= a.e2e_warmup:
                 ts.append(time.perf_counter() - t0)
         d2h = (4 * (out.color.size + out.depth.size + out.transmittance.size + out.alpha.size
                     + out.normal.size + gr.flat().size) + touched.size)

@@ -15,9 +15,71 @@ memory, single-threaded.  Here instead:
   widened to float64 on all host cores as each chunk lands.
 
 Only float32 crosses PCIe in either direction.
+
+Large host outputs come from a recycling pool of anonymous mappings
+(``host_empty``): at 1M Gaussians the float64 ParamGrads is 472 MB, and
+first-touch page faults of fresh memory -- not the copies -- dominated its
+download (25-50 ms per call).  A mapping goes back to the pool only when the
+last numpy view of it has been garbage collected (a finalizer on the buffer
+owner, which every view's base chain keeps alive), the way a caching
+allocator recycles device memory.
 """
 
+import mmap
+import threading
+import weakref
+
 import numpy as np
+
+_POOL_MIN = 4 << 20        # bytes; smaller outputs use the normal allocator
+_POOL_CAP = 8 << 30        # bytes of idle mappings kept for reuse
+_pool = {}                 # nbytes -> [mmap]
+_pool_bytes = [0]
+_pool_lock = threading.Lock()
+
+
+class _HostBlock:
+    """Buffer owner of one pooled mapping (PEP 688 buffer export)."""
+
+    def __init__(self, mm):
+        self.mm = mm
+
+    def __buffer__(self, flags):
+        return memoryview(self.mm)
+
+    def __release_buffer__(self, view):
+        view.release()
+
+
+def _recycle(mm, nbytes):
+    with _pool_lock:
+        if _pool_bytes[0] + nbytes <= _POOL_CAP:
+            _pool.setdefault(nbytes, []).append(mm)
+            _pool_bytes[0] += nbytes
+            return
+    mm.close()
+
+
+def host_empty(shape, dtype=np.float64):
+    """A new (uninitialised) numpy array; large ones reuse pooled, already
+    faulted-in mappings."""
+    dtype = np.dtype(dtype)
+    n = int(np.prod(shape)) if len(shape) else 1
+    nbytes = n * dtype.itemsize
+    if nbytes < _POOL_MIN:
+        return np.empty(shape, dtype)
+    size = (nbytes + (2 << 20) - 1) & ~((2 << 20) - 1)
+    with _pool_lock:
+        lst = _pool.get(size)
+        mm = lst.pop() if lst else None
+        if mm is not None:
+            _pool_bytes[0] -= size
+    if mm is None:
+        mm = mmap.mmap(-1, size)
+    owner = _HostBlock(mm)
+    weakref.finalize(owner, _recycle, mm, size)
+    return np.frombuffer(owner, dtype=dtype, count=n).reshape(shape)
+
 
 _CHUNK = 16 << 20  # bytes of float32 per pipelined chunk
 _stages = {}       # tag -> [pinned uint8 tensor, cuda event guarding reuse]
@@ -95,7 +157,7 @@ def download(tensors, dtype=np.float64, tag="down"):
         flat = t.reshape(-1)
         hv = stage[off:off + nb].view(t.dtype)
         step = max(_CHUNK // t.element_size(), 1)
-        out = torch.empty(t.shape, dtype=tdt)
+        out = torch.from_numpy(host_empty(tuple(t.shape), dtype))
         oflat = out.reshape(-1)
         for s in range(0, flat.numel(), step):
             e = min(s + step, flat.numel())

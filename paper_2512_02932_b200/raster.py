@@ -47,8 +47,9 @@ def scene_fingerprint(scene):
     scenes use tensor version counters (no device sync)."""
     if isinstance(scene, DeviceGaussians):
         return ("device", scene.count) + scene.versions()
-    return (scene.count, float(scene.center.sum()), float(scene.opacity_logit.sum()),
-            float(scene.log_scale.sum()))
+    import torch  # multi-threaded sums (numpy's are single-threaded: 5 ms at 1M)
+    return (scene.count,) + tuple(float(torch.from_numpy(np.ascontiguousarray(a)).sum())
+                                  for a in (scene.center, scene.opacity_logit, scene.log_scale))
 
 
 @dataclass
