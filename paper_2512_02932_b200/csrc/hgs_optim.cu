@@ -23,7 +23,6 @@ namespace {
 
 constexpr int kG = 64;           // Gaussians per CTA
 constexpr int kOThreads = 256;
-constexpr int kPMax = 11 + 3 * 16;
 constexpr int kStride = kG + 1;  // padded row: (j * 65 + g) % 32 spreads banks
 
 enum : int { kOpCombine = 0, kOpAdam = 1, kOpCombineAdam = 2 };
@@ -43,15 +42,18 @@ struct OptArgs {
   float beta1, beta2, eps, bc2_sqrt;
 };
 
-__device__ __forceinline__ int field_width(int f, int B) { return f < 2 ? 3 : (f == 2 ? 4 : (f == 3 ? 1 : 3 * B)); }
-__device__ __forceinline__ int field_j0(int f) { return f == 0 ? 0 : (f == 1 ? 3 : (f == 2 ? 6 : (f == 3 ? 10 : 11))); }
+__host__ __device__ constexpr int field_width(int f, int B) { return f < 2 ? 3 : (f == 2 ? 4 : (f == 3 ? 1 : 3 * B)); }
+__host__ __device__ constexpr int field_j0(int f) { return f == 0 ? 0 : (f == 1 ? 3 : (f == 2 ? 6 : (f == 3 ? 10 : 11))); }
 __device__ __forceinline__ int64_t field_off(int f, int64_t n) { return (int64_t)field_j0(f) * n; }
 
-template <int OP>
+// Templated on the SH basis count so every field width is a compile-time
+// constant (index division becomes multiply-shift; loops unroll).
+template <int OP, int B>
 __global__ void __launch_bounds__(kOThreads) k_optim(OptArgs a) {
   constexpr bool kCombine = OP != kOpAdam;
   constexpr bool kAdam = OP != kOpCombine;
-  __shared__ float sl[kCombine ? kPMax : 1][kStride], sh[kCombine ? kPMax : 1][kStride];
+  constexpr int P = 11 + 3 * B;
+  __shared__ float sl[kCombine ? P : 1][kStride], sh[kCombine ? P : 1][kStride];
   __shared__ double part[4][kG][3];
   __shared__ float coef[kG];
   __shared__ int kind[kG];
@@ -59,14 +61,15 @@ __global__ void __launch_bounds__(kOThreads) k_optim(OptArgs a) {
   __shared__ unsigned int nconf;
   const int64_t g0 = (int64_t)blockIdx.x * kG;
   const int gn = (int)(a.n - g0 < kG ? a.n - g0 : kG);
-  const int B = a.B, P = 11 + 3 * B;
   const int tid = threadIdx.x;
 
   if (kCombine) {
     // 1. stage g_low / g_high transposed into shared memory
+#pragma unroll
     for (int f = 0; f < 5; ++f) {
       const int fw = field_width(f, B), j0 = field_j0(f);
       const int64_t base = field_off(f, a.n) + g0 * fw;
+#pragma unroll 4
       for (int e = tid; e < gn * fw; e += kOThreads) {
         const int g = e / fw, j = j0 + e - g * fw;
         sl[j][g] = __ldg(a.gl + base + e);
@@ -112,41 +115,64 @@ __global__ void __launch_bounds__(kOThreads) k_optim(OptArgs a) {
     if (tid == 0 && nconf && a.n_conflicts) atomicAdd(a.n_conflicts, (unsigned long long)nconf);
   }
 
-  // 3. element-wise: combined gradient, then (optionally) the Adam update
+  // 3. element-wise: combined gradient, then (optionally) the Adam update.
+  //    kU elements per thread per step, all global loads issued before any
+  //    store (the pointers may alias as far as the compiler knows, so it
+  //    would otherwise serialise them): kU x 4 loads in flight per thread.
+  constexpr int kU = 4;
+#pragma unroll
   for (int f = 0; f < 5; ++f) {
     const int fw = field_width(f, B), j0 = field_j0(f);
     const int64_t base = field_off(f, a.n) + g0 * fw;
-    for (int e = tid; e < gn * fw; e += kOThreads) {
-      const int g = e / fw, j = j0 + e - g * fw;
-      float grad;
-      if (kCombine) {
-        float gl = sl[j][g], gh = sh[j][g];
-        switch (kind[g]) {
-          case kProjHigh: gh = fmaf(-coef[g], gl, gh); break;
-          case kProjLow: gl = fmaf(-coef[g], gh, gl); break;
-          case kZeroHigh: gh = 0.f; break;
-          case kZeroLow: gl = 0.f; break;
-          default: break;
+    const int cnt = gn * fw;
+    float *const prm = kAdam ? a.field[f] + g0 * fw : nullptr;
+    for (int e0 = tid; e0 < cnt; e0 += kOThreads * kU) {
+      float gcv[kU], mv[kU], vv[kU], pv[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int e = e0 + u * kOThreads;
+        if (e < cnt) {
+          gcv[u] = __ldcs(a.gc + base + e);
+          if (kAdam) {
+            mv[u] = __ldcs(a.m + base + e);
+            vv[u] = __ldcs(a.v + base + e);
+            pv[u] = __ldcs(prm + e);
+          }
         }
-        grad = (__ldg(a.gc + base + e) + gl) + gh;  // surgery.py:92
-      } else {
-        grad = __ldg(a.gc + base + e);
       }
-      if (!kAdam) {
-        a.out[base + e] = grad;
-        continue;
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int e = e0 + u * kOThreads;
+        if (e >= cnt) continue;
+        const int g = e / fw, j = j0 + e - g * fw;
+        float grad = gcv[u];
+        if (kCombine) {
+          float gl = sl[j][g], gh = sh[j][g];
+          switch (kind[g]) {
+            case kProjHigh: gh = fmaf(-coef[g], gl, gh); break;
+            case kProjLow: gl = fmaf(-coef[g], gh, gl); break;
+            case kZeroHigh: gh = 0.f; break;
+            case kZeroLow: gl = 0.f; break;
+            default: break;
+          }
+          grad = (grad + gl) + gh;  // surgery.py:92
+        }
+        if (!kAdam) {
+          __stcs(a.out + base + e, grad);
+          continue;
+        }
+        float m = mv[u], v = vv[u];
+        m = fmaf(1.f - a.beta1, grad - m, m);                // exp_avg.lerp_(grad, 1 - beta1)
+        v = fmaf(1.f - a.beta2, grad * grad, v * a.beta2);   // exp_avg_sq.mul_(beta2).addcmul_(g, g, 1 - beta2)
+        const float denom = sqrtf(v) / a.bc2_sqrt + a.eps;
+        const float pn = pv[u] - a.step_size[f] * (m / denom);
+        __stcs(a.m + base + e, m);
+        __stcs(a.v + base + e, v);
+        if (f == 2)
+          rot[g][e - g * fw] = pn;  // renormalised below
+        else
+          __stcs(prm + e, pn);
       }
-      float m = a.m[base + e], v = a.v[base + e];
-      m = fmaf(1.f - a.beta1, grad - m, m);                    // exp_avg.lerp_(grad, 1 - beta1)
-      v = fmaf(1.f - a.beta2, grad * grad, v * a.beta2);        // exp_avg_sq.mul_(beta2).addcmul_(g, g, 1 - beta2)
-      const float denom = sqrtf(v) / a.bc2_sqrt + a.eps;
-      const float p = a.field[f][g0 * fw + e] - a.step_size[f] * (m / denom);
-      a.m[base + e] = m;
-      a.v[base + e] = v;
-      if (f == 2)
-        rot[g][e - g * fw] = p;  // renormalised below
-      else
-        a.field[f][g0 * fw + e] = p;
     }
     if (kAdam && f == 2) {  // renormalize_rotations (core/types.py:136-142)
       __syncthreads();
@@ -165,13 +191,23 @@ __global__ void __launch_bounds__(kOThreads) k_optim(OptArgs a) {
   }
 }
 
+template <int B>
+void launch_b(int op, OptArgs &a, int blocks, cudaStream_t s) {
+  switch (op) {
+    case kOpCombine: k_optim<kOpCombine, B><<<blocks, kOThreads, 0, s>>>(a); break;
+    case kOpAdam: k_optim<kOpAdam, B><<<blocks, kOThreads, 0, s>>>(a); break;
+    default: k_optim<kOpCombineAdam, B><<<blocks, kOThreads, 0, s>>>(a); break;
+  }
+}
+
 int launch(int op, OptArgs &a, cudaStream_t s) {
   if (a.n <= 0) return HGS_OK;
   const int blocks = (int)((a.n + kG - 1) / kG);
-  switch (op) {
-    case kOpCombine: k_optim<kOpCombine><<<blocks, kOThreads, 0, s>>>(a); break;
-    case kOpAdam: k_optim<kOpAdam><<<blocks, kOThreads, 0, s>>>(a); break;
-    default: k_optim<kOpCombineAdam><<<blocks, kOThreads, 0, s>>>(a); break;
+  switch (a.B) {
+    case 1: launch_b<1>(op, a, blocks, s); break;
+    case 4: launch_b<4>(op, a, blocks, s); break;
+    case 9: launch_b<9>(op, a, blocks, s); break;
+    default: launch_b<16>(op, a, blocks, s); break;
   }
   return cudaGetLastError() == cudaSuccess ? HGS_OK : HGS_ERR_CUDA;
 }
