@@ -191,3 +191,13 @@ def test_train_step_fixed_point_and_descent():
     w = freq.LossWeights()
     hist = [optim.train_step(ds2, cam, gt, opt2, w, st).total_loss(w) for _ in range(40)]
     assert hist[-1] < 0.5 * hist[0], hist[::8]
+
+
+def test_device_checkpoint_round_trip(tmp_path):
+    import torch
+    from paper_2512_02932_b200 import io as hio
+    _, _, ds = _scene(1234, seed=2)
+    hio.save_checkpoint(ds, tmp_path / "d.ckpt")
+    back = hio.load_checkpoint(tmp_path / "d.ckpt", device="cuda:0")
+    for f in ("center", "log_scale", "rotation", "opacity_logit", "sh_coeffs", "type_spec"):
+        assert torch.equal(getattr(ds, f), getattr(back, f)), f
