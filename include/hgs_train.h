@@ -127,6 +127,41 @@ int hgs_combine_adam_step(const hgs_params *params, const float *g_color, const 
                           const uint8_t *type_spec, int32_t mode, float *exp_avg, float *exp_avg_sq,
                           const hgs_adam *cfg, unsigned long long *n_conflicts, void *stream);
 
+/* ------------------------------------------------- adaptive density control */
+/* SPEC.md:411-419, 425-427 (the reference ships the stats / keep / append
+ * helpers, core/types.py:48-49, 110-130, but no densify code). */
+typedef struct hgs_densify_config {
+  double grad_threshold; /* mean NDC positional-gradient norm above which a Gaussian grows (2e-4) */
+  double prune_opacity;  /* sigmoid(opacity_logit) below this is removed (0.005) */
+  double split_scale;    /* max scale above this splits, else clones (0.01 * scene extent) */
+  double clone_step;     /* clone offset, in units of the max scale, against the centre's Adam moment (0 = copy) */
+} hgs_densify_config;
+
+/* After hgs_backward (kg <= 4, same scratch): per Gaussian touched by the view,
+ * grad_accum += |NDC-space gradient of the projected centre| summed over the
+ * kg stacked losses, obs_count += 1 (3DGS's densification statistics). */
+int hgs_densify_stats(const hgs_scene *scene, const hgs_camera *camera, const void *bwd_scratch, int32_t kg,
+                      const uint8_t *touched, float *grad_accum, int32_t *obs_count, void *stream);
+
+size_t hgs_densify_scratch_bytes(int64_t n);
+
+/* Decide prune / keep / clone / split per Gaussian and scan the output row
+ * counts; synchronises the stream once to return the new count in *n_out and
+ * (nullable, host) census[4] = {kept, pruned, cloned, split}.
+ * Invariant: n_out = n + clones + 2 splits - splits - pruned. */
+int hgs_densify_plan(const hgs_scene *scene, const float *grad_accum, const int32_t *obs_count,
+                     const hgs_densify_config *cfg, void *scratch, size_t scratch_bytes, int64_t *n_out,
+                     int64_t *census, void *stream);
+
+/* Write the densified scene (out->n = n_out rows, order-preserving: each
+ * survivor's rows at its scanned offset).  Split: two children at +-0.5 sigma
+ * along the major axis (in-plane for 2D surfels), scales / 1.6.  Clone: the
+ * parent and a copy.  Adam moments (nullable) are carried for survivors and
+ * zero for new rows.  The caller resets grad_accum / obs_count. */
+int hgs_densify_apply(const hgs_scene *scene, const float *exp_avg, const float *exp_avg_sq, const void *scratch,
+                      const hgs_densify_config *cfg, const hgs_params *out, uint8_t *out_type_spec,
+                      float *out_exp_avg, float *out_exp_avg_sq, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -35,7 +35,8 @@ EXPORTS = ("hgs_abi_version", "hgs_status_string", "hgs_frame_bytes", "hgs_forwa
            "hgs_backward_scratch_bytes", "hgs_backward", "hgs_exchange",
            "hgs_frame_export_arrays", "hgs_blend_log", "hgs_frame_stats",
            "hgs_loss_scratch_bytes", "hgs_image_losses", "hgs_dwt_level1", "hgs_dwt_inverse",
-           "hgs_combine_gradients", "hgs_adam_step", "hgs_combine_adam_step")
+           "hgs_combine_gradients", "hgs_adam_step", "hgs_combine_adam_step",
+           "hgs_densify_stats", "hgs_densify_scratch_bytes", "hgs_densify_plan", "hgs_densify_apply")
 
 _vp = ctypes.c_void_p
 _i64 = ctypes.c_int64
@@ -95,6 +96,11 @@ class AdamCfg(ctypes.Structure):
                 ("eps", ctypes.c_float), ("step", _i64)]
 
 
+class DensifyCfg(ctypes.Structure):
+    _fields_ = [("grad_threshold", ctypes.c_double), ("prune_opacity", ctypes.c_double),
+                ("split_scale", ctypes.c_double), ("clone_step", ctypes.c_double)]
+
+
 class FrameExport(ctypes.Structure):
     _fields_ = [("idx", _vp), ("typ", _vp), ("depth", _vp), ("center2d", _vp), ("cov2d", _vp),
                 ("conic", _vp), ("mrow", _vp), ("alpha_eff", _vp), ("color", _vp),
@@ -151,6 +157,13 @@ def lib():
     L.hgs_adam_step.argtypes = [P(Params), _vp, _vp, _vp, P(AdamCfg), _vp]
     L.hgs_combine_adam_step.argtypes = [P(Params), _vp, _vp, _vp, _vp, _i32, _vp, _vp, P(AdamCfg),
                                         _vp, _vp]
+    L.hgs_densify_stats.argtypes = [P(Scene), P(Camera), _vp, _i32, _vp, _vp, _vp, _vp]
+    L.hgs_densify_scratch_bytes.restype = ctypes.c_size_t
+    L.hgs_densify_scratch_bytes.argtypes = [_i64]
+    L.hgs_densify_plan.argtypes = [P(Scene), _vp, _vp, P(DensifyCfg), _vp, ctypes.c_size_t,
+                                   P(_i64), P(_i64), _vp]
+    L.hgs_densify_apply.argtypes = [P(Scene), _vp, _vp, _vp, P(DensifyCfg), P(Params), _vp, _vp, _vp,
+                                    _vp]
     if L.hgs_abi_version() != 1:
         _load_error = "libhgs.so ABI version mismatch"
         raise ExtensionError(_load_error)

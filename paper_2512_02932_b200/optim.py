@@ -144,10 +144,13 @@ class _Workspace:
 _ws = {}
 
 
-def train_step(scene, camera, gt, optimizer, weights=None, settings=None, flags=0, events=None):
+def train_step(scene, camera, gt, optimizer, weights=None, settings=None, flags=0, events=None,
+               stats=None):
     """One frequency-decoupled training step of one view, all on the GPU
     (Alg. 1).  ``gt``: (H, W, 3) float32 CUDA image.
-    Returns a TrainStepResult (device tensors; no host sync)."""
+    ``stats`` (densify.DensifyStats) accumulates the densification
+    statistics of this view.  Returns a TrainStepResult (device tensors; no
+    host sync)."""
     from . import freq, grad, raster
     from .settings import RenderSettings
     w = weights or freq.LossWeights()
@@ -156,9 +159,10 @@ def train_step(scene, camera, gt, optimizer, weights=None, settings=None, flags=
     if tuple(gt.shape) != (H, W, 3):
         raise ConfigError("gt image shape %s does not match the camera" % (tuple(gt.shape),))
     key = (scene.count, scene.sh_bases, H, W)
-    ws = _ws.get(id(scene))
+    ws = _ws.get(scene.device)  # one workspace per device, rebuilt when the sizes change
     if ws is None or ws.key != key:
-        ws = _ws[id(scene)] = _Workspace(scene, H, W)
+        _ws.pop(scene.device, None)
+        ws = _ws[scene.device] = _Workspace(scene, H, W)
     ev = events or [None] * 4
     if ev[0] is not None:
         ev[0].record()
@@ -170,6 +174,9 @@ def train_step(scene, camera, gt, optimizer, weights=None, settings=None, flags=
         ev[2].record()
     g, _ = grad.backward_device(frame, stack, grads_out=ws.grads, touched_out=ws.touched,
                                 scratch=ws.bwd_scratch)
+    if stats is not None:
+        from . import densify
+        densify.accumulate(scene, camera, stats, ws.bwd_scratch, 3, ws.touched)
     if ev[3] is not None:
         ev[3].record()
     nc = optimizer.step_combined(g[0], g[1], g[2], w.mode)
