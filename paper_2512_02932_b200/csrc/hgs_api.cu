@@ -219,6 +219,7 @@ int hgs_forward(const hgs_scene *scene, const hgs_camera *camera, const hgs_sett
   HGS_LAUNCHED();
   // 1. depth keys + digit histograms
   uint32_t *vals_sorted = at<uint32_t>(frame, L.vals_a);
+  uint32_t *rank_of = at<uint32_t>(frame, L.vals_b);
   int64_t m = 0;
   if (n > 0) {
     k_depth_keys<<<grid_for(n, 256), 256, 0, s>>>(sc, cam, at<unsigned long long>(frame, L.keys_a),
@@ -248,6 +249,7 @@ int hgs_forward(const hgs_scene *scene, const hgs_camera *camera, const hgs_sett
                                         st->tile_counters + 1, s, &in_b);
     if (rc) return rc;
     vals_sorted = at<uint32_t>(frame, in_b ? L.vals_b : L.vals_a);
+    rank_of = at<uint32_t>(frame, in_b ? L.vals_a : L.vals_b);  // the free ping-pong buffer
     info->internal[2] = (uint32_t)np;  // depth-sort passes (diagnostics / launch count)
   }
   info->m = m;
@@ -258,8 +260,10 @@ int hgs_forward(const hgs_scene *scene, const hgs_camera *camera, const hgs_sett
     HGS_CUDA(cudaMemsetAsync(at<char>(frame, L.lb_scan), 0, L.lb_scan_bytes, s));
     // tile counts per rank go to the (now free) depth-key buffer
     uint32_t *counts = at<uint32_t>(frame, L.keys_a);
-    k_preprocess<<<grid_for(m, 128), 128, 0, s>>>(sc, cam, mod, vals_sorted, m, at<SplatRec>(frame, L.recs),
-                                                  counts);
+    HGS_CUDA(cudaMemsetAsync(rank_of, 0xff, (size_t)n * 4, s));
+    k_rank_scatter<<<grid_for(m, 256), 256, 0, s>>>(vals_sorted, m, rank_of);
+    HGS_LAUNCHED();
+    k_preprocess<<<grid_for(n, 128), 128, 0, s>>>(sc, cam, mod, rank_of, at<SplatRec>(frame, L.recs), counts);
     HGS_LAUNCHED();
     k_scan_counts<<<(unsigned)ceil_div(m, kScanTile), kScanThreads, 0, s>>>(
         counts, m, at<unsigned long long>(frame, L.pair_off), at<unsigned long long>(frame, L.lb_scan), st);

@@ -101,17 +101,25 @@ __device__ __forceinline__ void write_record(const ProjD &o, uint32_t idx, Splat
   *rec = r;
 }
 
-// One thread per depth rank r < M: float64 projection of Gaussian
-// sorted_idx[r], record write, tile count, exclusive scan -> pair offsets.
+// Inverse of the depth permutation: rank_of[sorted_idx[r]] = r for the M
+// kept splats (culled Gaussians keep the caller's 0xffffffff fill).
+__global__ void k_rank_scatter(const uint32_t *__restrict__ sorted_idx, int64_t m, uint32_t *__restrict__ rank_of) {
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < m; r += (int64_t)gridDim.x * blockDim.x)
+    rank_of[sorted_idx[r]] = (uint32_t)r;
+}
+
+// One thread per Gaussian in index order (coalesced scene reads): float64
+// projection, record + tile count written at the Gaussian's depth rank.
 __global__ void __launch_bounds__(128) k_preprocess(SceneView sc, CamD cam, ModD mod,
-                                                    const uint32_t *__restrict__ sorted_idx, int64_t m,
+                                                    const uint32_t *__restrict__ rank_of,
                                                     SplatRec *__restrict__ recs, uint32_t *__restrict__ counts) {
-  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < m; r += (int64_t)gridDim.x * blockDim.x) {
-    const uint32_t i = sorted_idx[r];
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < sc.n; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t r = rank_of[i];
+    if (r == 0xffffffffu) continue;
     ProjD o;
-    project_d<false>(sc, i, cam, mod, o);
+    project_d<false>(sc, (uint32_t)i, cam, mod, o);
     bbox_d(o, cam.width, cam.height);
-    write_record(o, i, recs + r);
+    write_record(o, (uint32_t)i, recs + r);
     counts[r] = tile_count_of(o.bbox);
   }
 }
