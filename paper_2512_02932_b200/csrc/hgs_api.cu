@@ -443,12 +443,14 @@ int hgs_backward(const hgs_scene *scene, const hgs_camera *camera, const hgs_set
     c.kg = kc;
     c.grads = grads + (int64_t)k0 * n * P;
     if (n > 0) {
-      const int grid = grid_for(n, 128);
+      // one warp per CTA; shared memory: SH rows in + kc SH-gradient rows out
+      const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 32), 148 * 48));
+      const size_t smem = (size_t)(1 + kc) * 32 * (3 * scene->sh_bases + 1) * sizeof(float);
       switch (scene->sh_bases) {
-        case 1: k_chain_rule_t<0><<<grid, 128, 0, s>>>(c); break;
-        case 4: k_chain_rule_t<1><<<grid, 128, 0, s>>>(c); break;
-        case 9: k_chain_rule_t<2><<<grid, 128, 0, s>>>(c); break;
-        default: k_chain_rule_t<3><<<grid, 128, 0, s>>>(c); break;
+        case 1: k_chain_rule_t<0><<<grid, 32, smem, s>>>(c); break;
+        case 4: k_chain_rule_t<1><<<grid, 32, smem, s>>>(c); break;
+        case 9: k_chain_rule_t<2><<<grid, 32, smem, s>>>(c); break;
+        default: k_chain_rule_t<3><<<grid, 32, smem, s>>>(c); break;
       }
       HGS_LAUNCHED();
     }

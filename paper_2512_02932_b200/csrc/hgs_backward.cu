@@ -90,15 +90,34 @@ __device__ __forceinline__ float clamp_mask(const float *shc_ch, const float *ba
   return (r + 0.5) > 0.0 ? 1.f : 0.f;
 }
 
-// One thread per Gaussian.  Gaussians with an all-zero accumulator (culled or
-// never composited) get exactly zero gradients (the chain rule is linear).
+// One thread per Gaussian, one warp per CTA, 32 consecutive Gaussians per
+// warp step.  The SH coefficients (3B floats per Gaussian) are read and the SH
+// gradients written through shared memory, as one contiguous, coalesced
+// segment per warp step: per-thread rows of 3B floats at a 12B-byte stride
+// would issue 3B scalar memory instructions per thread (LSU-throttled).
+// Gaussians with an all-zero accumulator (culled or never composited) get
+// exactly zero gradients (the chain rule is linear).
+constexpr int kChainThreads = 32;
+
 template <int DEG>
-__global__ void __launch_bounds__(128) k_chain_rule_t(ChainArgs c) {
+__global__ void __launch_bounds__(kChainThreads) k_chain_rule_t(ChainArgs c) {
   constexpr int B = (DEG + 1) * (DEG + 1);
+  constexpr int SB = 3 * B, SS = 3 * B + 1;  // row length, padded smem stride
+  extern __shared__ float s_chain[];
+  float *s_in = s_chain;                     // [32][SS] SH coefficients
   const int64_t n = c.sc.n;
   const int64_t P = 11 + 3 * B;
   const CamD &cam = c.cam;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+  const int lane = threadIdx.x;
+  for (int64_t base = (int64_t)blockIdx.x * kChainThreads; base < n; base += (int64_t)gridDim.x * kChainThreads) {
+    const int cnt = (int)(n - base < kChainThreads ? n - base : kChainThreads);
+    for (int e = lane; e < cnt * SB; e += kChainThreads) {
+      const int r = e / SB;
+      s_in[r * SS + (e - r * SB)] = __ldg(c.sc.sh + base * SB + e);
+    }
+    __syncwarp();
+    const int64_t i = base + lane;
+    if (lane < cnt) {
     bool any = false;
     for (int k = 0; k < c.kg; ++k) {
       const float4 *a4 = reinterpret_cast<const float4 *>(c.acc + ((int64_t)i * c.kg + k) * kAcc);
@@ -120,11 +139,11 @@ __global__ void __launch_bounds__(128) k_chain_rule_t(ChainArgs c) {
 #pragma unroll
         for (int s = 0; s < 4; ++s) g[6 * n + 4 * i + s] = 0.f;
         g[10 * n + i] = 0.f;
+        float *so = s_chain + (1 + k) * kChainThreads * SS + lane * SS;
 #pragma unroll
-        for (int s = 0; s < 3 * B; ++s) g[11 * n + 3 * B * i + s] = 0.f;
+        for (int s = 0; s < SB; ++s) so[s] = 0.f;
       }
-      continue;
-    }
+    } else {
     double pd[3], td[3];
     load_center_d(c.sc, i, pd);
     t_cam_d(cam, pd, td);
@@ -160,7 +179,7 @@ __global__ void __launch_bounds__(128) k_chain_rule_t(ChainArgs c) {
     const float vx = (float)vxd, vy = (float)vyd, vz = (float)vzd, dist = (float)distd;
     float basis[16];
     sh_basis_t<float>(DEG, vx, vy, vz, basis);
-    const float *shc = c.sc.sh + (int64_t)3 * B * i;
+    const float *shc = s_in + lane * SS;
     const float mask0 = clamp_mask<B>(shc, basis, vxd, vyd, vzd);
     const float mask1 = clamp_mask<B>(shc + B, basis, vxd, vyd, vzd);
     const float mask2 = clamp_mask<B>(shc + 2 * B, basis, vxd, vyd, vzd);
@@ -182,11 +201,12 @@ __global__ void __launch_bounds__(128) k_chain_rule_t(ChainArgs c) {
       // SH (core/sh.py:125-141)
       const float up0 = A[0] * mask0, up1 = A[1] * mask1, up2 = A[2] * mask2;
       float db[16];
+      float *so = s_chain + (1 + k) * kChainThreads * SS + lane * SS;
 #pragma unroll
       for (int bb = 0; bb < B; ++bb) {
-        g[11 * n + 3 * B * i + bb] = up0 * basis[bb];
-        g[11 * n + 3 * B * i + B + bb] = up1 * basis[bb];
-        g[11 * n + 3 * B * i + 2 * B + bb] = up2 * basis[bb];
+        so[bb] = up0 * basis[bb];
+        so[B + bb] = up1 * basis[bb];
+        so[2 * B + bb] = up2 * basis[bb];
         db[bb] = (shc[bb] * up0 + shc[B + bb] * up1) + shc[2 * B + bb] * up2;
       }
       float gdx, gdy, gdz;
@@ -324,6 +344,19 @@ __global__ void __launch_bounds__(128) k_chain_rule_t(ChainArgs c) {
       g[6 * n + 4 * i + 3] = (dzq - dotq * zq) * iqn;
       g[10 * n + i] = d_logit;
     }
+    }  // any
+    }  // lane < cnt
+    __syncwarp();
+    // coalesced SH-gradient segments of this warp step, one per kg
+    for (int k = 0; k < c.kg; ++k) {
+      float *gs = c.grads + (int64_t)k * n * P + 11 * n + base * SB;
+      const float *so = s_chain + (1 + k) * kChainThreads * SS;
+      for (int e = lane; e < cnt * SB; e += kChainThreads) {
+        const int r = e / SB;
+        gs[e] = so[r * SS + (e - r * SB)];
+      }
+    }
+    __syncwarp();
   }
 }
 
