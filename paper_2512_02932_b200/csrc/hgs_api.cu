@@ -263,7 +263,7 @@ int hgs_forward(const hgs_scene *scene, const hgs_camera *camera, const hgs_sett
     HGS_CUDA(cudaMemsetAsync(rank_of, 0xff, (size_t)n * 4, s));
     k_rank_scatter<<<grid_for(m, 256), 256, 0, s>>>(vals_sorted, m, rank_of);
     HGS_LAUNCHED();
-    k_preprocess<<<grid_for(n, 128), 128, 0, s>>>(sc, cam, mod, rank_of, at<SplatRec>(frame, L.recs), counts);
+    HGS_CUDA(launch_preprocess(sc, cam, mod, rank_of, at<SplatRec>(frame, L.recs), counts, s));
     HGS_LAUNCHED();
     k_scan_counts<<<(unsigned)ceil_div(m, kScanTile), kScanThreads, 0, s>>>(
         counts, m, at<unsigned long long>(frame, L.pair_off), at<unsigned long long>(frame, L.lb_scan), st);

@@ -192,7 +192,7 @@ struct ProjD {
 // float32 colour; the float64 path serves the exports and re-checks).
 template <bool COLOR64 = true>
 __device__ __forceinline__ void project_d(const SceneView &sc, int64_t i, const CamD &cam, const ModD &mod,
-                                          ProjD &o) {
+                                          ProjD &o, const float *sh_row = nullptr) {
   double p[3];
   load_center_d(sc, i, p);
   t_cam_d(cam, p, o.t);
@@ -253,7 +253,7 @@ __device__ __forceinline__ void project_d(const SceneView &sc, int64_t i, const 
   double vx = dl[0] / den, vy = dl[1] / den, vz = dl[2] / den;
   const int B = sc.sh_bases;
   const int deg = B == 1 ? 0 : (B == 4 ? 1 : (B == 9 ? 2 : 3));
-  const float *shc = sc.sh + (int64_t)3 * B * i;
+  const float *shc = sh_row ? sh_row : sc.sh + (int64_t)3 * B * i;  // sh_row: staged copy (shared memory)
   if (COLOR64) {
     double basis[16];
     sh_basis_d(deg, vx, vy, vz, basis);

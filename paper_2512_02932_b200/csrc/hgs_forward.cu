@@ -108,20 +108,49 @@ __global__ void k_rank_scatter(const uint32_t *__restrict__ sorted_idx, int64_t 
     rank_of[sorted_idx[r]] = (uint32_t)r;
 }
 
-// One thread per Gaussian in index order (coalesced scene reads): float64
-// projection, record + tile count written at the Gaussian's depth rank.
-__global__ void __launch_bounds__(128) k_preprocess(SceneView sc, CamD cam, ModD mod,
-                                                    const uint32_t *__restrict__ rank_of,
-                                                    SplatRec *__restrict__ recs, uint32_t *__restrict__ counts) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < sc.n; i += (int64_t)gridDim.x * blockDim.x) {
+// One thread per Gaussian in index order, one warp per CTA and 32 consecutive
+// Gaussians per warp step: the SH rows (3B floats each) are staged through
+// shared memory as one coalesced segment (per-thread strided rows were
+// LSU-throttled); float64 projection; record + tile count written at the
+// Gaussian's depth rank.
+template <int B>
+__global__ void __launch_bounds__(32) k_preprocess(SceneView sc, CamD cam, ModD mod,
+                                                   const uint32_t *__restrict__ rank_of,
+                                                   SplatRec *__restrict__ recs, uint32_t *__restrict__ counts) {
+  constexpr int SB = 3 * B, SS = 3 * B + 1;
+  __shared__ float s_sh[32 * SS];
+  const int lane = threadIdx.x;
+  for (int64_t base = (int64_t)blockIdx.x * 32; base < sc.n; base += (int64_t)gridDim.x * 32) {
+    const int cnt = (int)(sc.n - base < 32 ? sc.n - base : 32);
+    __syncwarp();
+    for (int e = lane; e < cnt * SB; e += 32) {
+      const int r = e / SB;
+      s_sh[r * SS + (e - r * SB)] = __ldg(sc.sh + base * SB + e);
+    }
+    __syncwarp();
+    const int64_t i = base + lane;
+    if (lane >= cnt) continue;
     const uint32_t r = rank_of[i];
     if (r == 0xffffffffu) continue;
     ProjD o;
-    project_d<false>(sc, (uint32_t)i, cam, mod, o);
+    project_d<false>(sc, i, cam, mod, o, s_sh + lane * SS);
     bbox_d(o, cam.width, cam.height);
     write_record(o, (uint32_t)i, recs + r);
     counts[r] = tile_count_of(o.bbox);
   }
+}
+// Host launcher (the template is launched from this translation unit).
+cudaError_t launch_preprocess(const SceneView &sc, const CamD &cam, const ModD &mod, const uint32_t *rank_of,
+                              SplatRec *recs, uint32_t *counts, cudaStream_t s) {
+  const int64_t nb = (sc.n + 31) / 32;
+  const int g = (int)(nb < 1 ? 1 : (nb > 148 * 48 ? 148 * 48 : nb));  // one warp per CTA
+  switch (sc.sh_bases) {
+    case 1: k_preprocess<1><<<g, 32, 0, s>>>(sc, cam, mod, rank_of, recs, counts); break;
+    case 4: k_preprocess<4><<<g, 32, 0, s>>>(sc, cam, mod, rank_of, recs, counts); break;
+    case 9: k_preprocess<9><<<g, 32, 0, s>>>(sc, cam, mod, rank_of, recs, counts); break;
+    default: k_preprocess<16><<<g, 32, 0, s>>>(sc, cam, mod, rank_of, recs, counts); break;
+  }
+  return cudaGetLastError();
 }
 
 // Exclusive scan of the per-rank tile counts into pair offsets (decoupled

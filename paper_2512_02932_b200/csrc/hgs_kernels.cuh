@@ -501,8 +501,8 @@ __global__ void k_init_state(SceneView sc, CamD cam, ModD mod, FrameState *st);
 __global__ void k_depth_keys(SceneView sc, CamD cam, unsigned long long *keys, uint32_t *vals, uint32_t *hist,
                              FrameState *st);
 __global__ void k_rank_scatter(const uint32_t *sorted_idx, int64_t m, uint32_t *rank_of);
-__global__ void k_preprocess(SceneView sc, CamD cam, ModD mod, const uint32_t *rank_of, SplatRec *recs,
-                             uint32_t *counts);
+cudaError_t launch_preprocess(const SceneView &sc, const CamD &cam, const ModD &mod, const uint32_t *rank_of,
+                              SplatRec *recs, uint32_t *counts, cudaStream_t s);
 __global__ void k_scan_counts(const uint32_t *counts, int64_t m, unsigned long long *pair_off,
                               unsigned long long *scan_lb, FrameState *st);
 __global__ void k_duplicate(const SplatRec *recs, const unsigned long long *pair_off, int64_t m, int tiles_x,
