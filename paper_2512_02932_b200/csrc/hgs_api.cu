@@ -376,11 +376,14 @@ size_t hgs_backward_scratch_bytes(int64_t n, int32_t kg) {
 template <int KG>
 static void launch_bwd(const BwdArgs &b, int64_t n_tiles, bool ext, cudaStream_t s) {
   // hot replay, then the float64-exact fixup of the deferred pixels
+  // pixels per lane: 2 (4 warps per tile) shares the splat walk and the warp
+  // reduction between two pixels; 1 (8 warps) for register-heavy KG
+  constexpr int ppl = KG == 1 ? 2 : HGS_BWD_PPL_KG;
   if (ext) {
-    k_composite_bwd<KG, true><<<(unsigned)n_tiles, kBwdThreads, 0, s>>>(b);
+    k_composite_bwd<KG, true, ppl><<<(unsigned)n_tiles, 256 / ppl, 0, s>>>(b);
     k_fixup_bwd<KG, true><<<kFixupBlocks, 256, 0, s>>>(b);
   } else {
-    k_composite_bwd<KG, false><<<(unsigned)n_tiles, kBwdThreads, 0, s>>>(b);
+    k_composite_bwd<KG, false, ppl><<<(unsigned)n_tiles, 256 / ppl, 0, s>>>(b);
     k_fixup_bwd<KG, false><<<kFixupBlocks, 256, 0, s>>>(b);
   }
 }

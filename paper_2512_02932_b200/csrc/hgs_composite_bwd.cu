@@ -160,34 +160,34 @@ __device__ __forceinline__ void pair_grads(const SplatRec &r, const PairEval &p,
   }
 }
 
-// One CTA (4 warps) per 16 x 16 tile; a warp owns an 8 x 8 block and each
-// lane two pixels of it, (x, y) and (x, y + 4).  Every staged splat is walked
+// One CTA per 16 x 16 tile; a warp owns an 8 x (4 PPL) block and each lane
+// PPL pixels of it, (x, y + 4q).  With PPL = 2 (4 warps per tile)  Every staged splat is walked
 // once for both pixels of a lane: the chunk staging, the splat header and --
 // the dominant per-splat cost -- the 16-slot warp reduction + atomic flush
 // are shared by 64 pixels instead of 32, while the per-pixel math is
 // unchanged (a pixel's evaluation runs only where its 8 x 4 half is covered).
-template <int KG, bool EXT>
-__global__ void __launch_bounds__(kBwdThreads, KG == 1 ? HGS_BWD_MINB1 : 4) k_composite_bwd(BwdArgs b) {
+template <int KG, bool EXT, int PPL>
+__global__ void __launch_bounds__(256 / PPL, PPL == 2 ? (KG == 1 ? HGS_BWD_MINB1 : 4) : 3) k_composite_bwd(BwdArgs b) {
   const CompositeArgs &a = b.c;
-  __shared__ SplatRec s_rec[kBwdThreads / 32][32];
+  __shared__ SplatRec s_rec[8 / PPL][32];
   const int tile = blockIdx.x;
   const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int wx0 = tx * kTile + (warp & 1) * 8, wy0 = ty * kTile + (warp >> 1) * 8;
+  const int wx0 = tx * kTile + (warp & 1) * 8, wy0 = ty * kTile + (warp >> 1) * 4 * PPL;
   const int ix = wx0 + (lane & 7);
   const bool naive = a.flags & HGS_FLAG_NAIVE;
   const uint32_t lane_bit = 1u << lane;
   const uint32_t lo = naive ? 0u : a.tile_off[tile];
   const int64_t HW = (int64_t)a.width * a.height;
-  int iy[2];
-  bool inside[2], dead[2];
-  uint32_t pix[2], last[2];
-  float T_fin[2], T_run[2];
-  Suffix S[2];
-  PixGrads<KG, EXT> G[2];
+  int iy[PPL];
+  bool inside[PPL], dead[PPL];
+  uint32_t pix[PPL], last[PPL];
+  float T_fin[PPL], T_run[PPL];
+  Suffix S[PPL];
+  PixGrads<KG, EXT> G[PPL];
   uint32_t warp_last = 0;
 #pragma unroll
-  for (int q = 0; q < 2; ++q) {
+  for (int q = 0; q < PPL; ++q) {
     iy[q] = wy0 + (lane >> 3) + 4 * q;
     inside[q] = ix < a.width && iy[q] < a.height;
     pix[q] = (uint32_t)iy[q] * (uint32_t)a.width + (uint32_t)ix;
@@ -210,30 +210,41 @@ __global__ void __launch_bounds__(kBwdThreads, KG == 1 ? HGS_BWD_MINB1 : 4) k_co
   for (uint32_t top = warp_end, start; top > lo; top = start) {
     start = top - lo > 32u ? top - 32u : lo;
     const uint32_t j = start + lane;
-    uint32_t pm0 = 0u, pm1 = 0u;
+    uint32_t pm[PPL], any_pm = 0u;
+#pragma unroll
+    for (int q = 0; q < PPL; ++q) pm[q] = 0u;
     if (j < top) {
       const uint32_t rk = naive ? j : __ldg(a.tile_vals + j);
       const SplatRec *g = a.recs + rk;
-      const int4 q = __ldg(&g->r5);
-      pm0 = naive ? 0xffffffffu : pixel_mask(q, wx0, wy0);
-      pm1 = naive ? 0xffffffffu : pixel_mask(q, wx0, wy0 + 4);
-      if (pm0 | pm1) {
+      const int4 qb = __ldg(&g->r5);
+#pragma unroll
+      for (int q = 0; q < PPL; ++q) {
+        pm[q] = naive ? 0xffffffffu : pixel_mask(qb, wx0, wy0 + 4 * q);
+        any_pm |= pm[q];
+      }
+      if (any_pm) {
         SplatRec r;
         r.r0 = __ldg(&g->r0); r.r1 = __ldg(&g->r1); r.r2 = __ldg(&g->r2);
-        r.r3 = __ldg(&g->r3); r.r4 = __ldg(&g->r4); r.r5 = q;
-        if (!naive) {  // the 1/255 support may miss a covered half
-          if (pm0 && cull_splat(r, pm0, wx0, wy0)) pm0 = 0u;
-          if (pm1 && cull_splat(r, pm1, wx0, wy0 + 4)) pm1 = 0u;
+        r.r3 = __ldg(&g->r3); r.r4 = __ldg(&g->r4); r.r5 = qb;
+        if (!naive) {  // the 1/255 support may miss a covered 8 x 4 block
+          any_pm = 0u;
+#pragma unroll
+          for (int q = 0; q < PPL; ++q) {
+            if (pm[q] && cull_splat(r, pm[q], wx0, wy0 + 4 * q)) pm[q] = 0u;
+            any_pm |= pm[q];
+          }
         }
-        if (pm0 | pm1) wrec[lane] = r;
+        if (any_pm) wrec[lane] = r;
       }
     }
-    uint32_t rel = __ballot_sync(0xffffffffu, (pm0 | pm1) != 0u);
+    uint32_t rel = __ballot_sync(0xffffffffu, any_pm != 0u);
     __syncwarp();
     while (rel) {
       const int e = 31 - __clz(rel);
       rel &= ~(1u << e);
-      const uint32_t m0 = __shfl_sync(0xffffffffu, pm0, e), m1 = __shfl_sync(0xffffffffu, pm1, e);
+      uint32_t mq[PPL];
+#pragma unroll
+      for (int q = 0; q < PPL; ++q) mq[q] = __shfl_sync(0xffffffffu, pm[q], e);
       const uint32_t jj = start + e;
       const SplatRec &r = wrec[e];
       float v[KG][16];
@@ -247,8 +258,8 @@ __global__ void __launch_bounds__(kBwdThreads, KG == 1 ? HGS_BWD_MINB1 : 4) k_co
       }
       bool any = false;
 #pragma unroll
-      for (int q = 0; q < 2; ++q) {
-        const uint32_t m = q ? m1 : m0;
+      for (int q = 0; q < PPL; ++q) {
+        const uint32_t m = mq[q];
         const bool act = !dead[q] && inside[q] && (m & lane_bit) && jj - lo < last[q];
         PairEval p;
         if (count && act) ++n_ev;
@@ -309,7 +320,10 @@ __global__ void __launch_bounds__(kBwdThreads, KG == 1 ? HGS_BWD_MINB1 : 4) k_co
       }
     }
     __syncwarp();  // the next chunk overwrites this warp's staging slots
-    if (__all_sync(0xffffffffu, (dead[0] || !inside[0]) && (dead[1] || !inside[1]))) break;
+    bool finished = true;
+#pragma unroll
+    for (int q = 0; q < PPL; ++q) finished = finished && (dead[q] || !inside[q]);
+    if (__all_sync(0xffffffffu, finished)) break;
   }
   if (count) {
 #pragma unroll
@@ -442,8 +456,9 @@ __global__ void __launch_bounds__(256) k_fixup_bwd(BwdArgs b) {
 }
 
 // Instantiations: KG 1..4, with / without extension gradients.
-#define HGS_INST_BWD(KG, EXT)                                  \
-  template __global__ void k_composite_bwd<KG, EXT>(BwdArgs); \
+#define HGS_INST_BWD(KG, EXT)                                     \
+  template __global__ void k_composite_bwd<KG, EXT, 1>(BwdArgs); \
+  template __global__ void k_composite_bwd<KG, EXT, 2>(BwdArgs); \
   template __global__ void k_fixup_bwd<KG, EXT>(BwdArgs);
 HGS_INST_BWD(1, false)
 HGS_INST_BWD(2, false)

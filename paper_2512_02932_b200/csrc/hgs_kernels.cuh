@@ -73,7 +73,9 @@ constexpr float kCoarse2D = 0.05f;  // log2 units; 2D precise bounds only inside
 #endif
 
 enum : int { kSkip = 0, kContrib = 1, kAmbiguous = 2 };  // pair decision outcomes
-constexpr int kBwdThreads = 128;  // backward compositor: 4 warps per tile, 2 pixels per lane
+#ifndef HGS_BWD_PPL_KG
+#define HGS_BWD_PPL_KG 2  // pixels per lane of the backward compositor for KG >= 2 (KG = 1 always 2)
+#endif
 
 __device__ __forceinline__ bool rec_is3d(const SplatRec &r) { return __float_as_uint(r.r4.w) >> 31; }
 __device__ __forceinline__ uint32_t rec_idx(const SplatRec &r) { return __float_as_uint(r.r4.w) & 0x7fffffffu; }
@@ -511,7 +513,7 @@ __global__ void k_tile_ranges(const uint32_t *skeys, int64_t k, int64_t n_tiles,
 template <bool NAIVE, bool COUNT>
 __global__ void k_composite_fwd(CompositeArgs a);
 __global__ void k_fixup_fwd(CompositeArgs a);
-template <int KG, bool EXT>
+template <int KG, bool EXT, int PPL>
 __global__ void k_composite_bwd(BwdArgs b);
 template <int KG, bool EXT>
 __global__ void k_fixup_bwd(BwdArgs b);
