@@ -9,6 +9,9 @@
 //                    (lane-parallel evaluation, product scan for T).
 #include "hgs_kernels.cuh"
 
+#ifndef HGS_FWD_STOP_FAST
+#define HGS_FWD_STOP_FAST 1
+#endif
 #ifndef HGS_FWD_MINB
 #define HGS_FWD_MINB 4  // CTAs per SM the hot compositor is register-budgeted for
 #endif
@@ -111,11 +114,21 @@ __global__ void __launch_bounds__(kBlock, HGS_FWD_MINB) k_composite_fwd(Composit
       last = base + e - lo + 1u;
       T = T * (1.f - at);
       // early stop T < 1e-4 (_blend_py.py:111-113); near the threshold the
-      // decision is deferred to the float64 transmittance replay
+      // decision is deferred to the float64 transmittance replay.  One
+      // compare on the common path (T well above the threshold).
+#if HGS_FWD_STOP_FAST
+      if (T <= (float)kEarlyStopT * (1.f + 2e-5f)) {
+        if (exact && T >= (float)kEarlyStopT * (1.f - 2e-5f))
+          defer(base + e, 1u);
+        else if (T < (float)kEarlyStopT)
+          done = true;
+      }
+#else
       if (exact && fabsf(T - (float)kEarlyStopT) <= 2e-5f * (float)kEarlyStopT)
         defer(base + e, 1u);
       else if (T < (float)kEarlyStopT)
         done = true;
+#endif
     }
     __syncwarp();  // the next chunk overwrites this warp's staging slots
   }
