@@ -190,7 +190,9 @@ struct ProjD {
 
 // COLOR64 = false evaluates the SH colour in float32 (the record stores a
 // float32 colour; the float64 path serves the exports and re-checks).
-template <bool COLOR64 = true>
+// GEOM_ONLY skips the colour and the normal (the float64 pair re-checks need
+// only the geometry and alpha_eff).
+template <bool COLOR64 = true, bool GEOM_ONLY = false>
 __device__ __forceinline__ void project_d(const SceneView &sc, int64_t i, const CamD &cam, const ModD &mod,
                                           ProjD &o, const float *sh_row = nullptr) {
   double p[3];
@@ -246,6 +248,7 @@ __device__ __forceinline__ void project_d(const SceneView &sc, int64_t i, const 
     double mz = expit_d((sz - mod.theta_z) / mod.t_z) * sz;
     o.alpha_eff = o.alpha * exp(-mod.lambda_z * mz);
   }
+  if (GEOM_ONLY) return;
   // view-dependent colour (project.py:248-252, sh.py:110-122)
   double dl[3] = {p[0] - cam.campos[0], p[1] - cam.campos[1], p[2] - cam.campos[2]};
   double dist = sqrt((dl[0] * dl[0] + dl[1] * dl[1]) + dl[2] * dl[2]);

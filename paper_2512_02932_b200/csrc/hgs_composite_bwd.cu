@@ -365,7 +365,7 @@ __device__ __forceinline__ float scan_add_ex(float x, int lane) {
 // exclusive prefix sums of c * w; every lane then adds its pair's gradients
 // with per-lane atomics.
 template <int KG, bool EXT>
-__global__ void __launch_bounds__(256) k_fixup_bwd(BwdArgs b) {
+__global__ void __launch_bounds__(256, HGS_FIXUP_MINB) k_fixup_bwd(BwdArgs b) {
   const CompositeArgs &a = b.c;
   const uint32_t nfix = a.st->n_fix_bwd;
   const int lane = threadIdx.x & 31;

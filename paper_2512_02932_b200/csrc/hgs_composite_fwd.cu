@@ -180,7 +180,7 @@ __device__ __forceinline__ float warp_sum(float x) {
 // decisions (float64 re-evaluation where the float32 bound is ambiguous),
 // forms the transmittance with a product scan, resolves the early stop in
 // lane order (float64 replay near the threshold) and accumulates.
-__global__ void __launch_bounds__(256) k_fixup_fwd(CompositeArgs a) {
+__global__ void __launch_bounds__(256, HGS_FIXUP_MINB) k_fixup_fwd(CompositeArgs a) {
   const uint32_t nfix = a.st->n_fix_fwd;
   const int lane = threadIdx.x & 31;
   const uint32_t nw = (gridDim.x * blockDim.x) >> 5;

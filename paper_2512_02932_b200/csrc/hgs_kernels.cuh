@@ -73,6 +73,9 @@ constexpr float kCoarse2D = 0.05f;  // log2 units; 2D precise bounds only inside
 #endif
 
 enum : int { kSkip = 0, kContrib = 1, kAmbiguous = 2 };  // pair decision outcomes
+#ifndef HGS_FIXUP_MINB
+#define HGS_FIXUP_MINB 3  // CTAs (of 256) per SM the float64 fixup kernels are register-budgeted for
+#endif
 #ifndef HGS_BWD_PPL_KG
 #define HGS_BWD_PPL_KG 2  // pixels per lane of the backward compositor for KG >= 2 (KG = 1 always 2)
 #endif
@@ -219,7 +222,7 @@ struct PairEval {
 static __device__ __noinline__ bool pair_f64(const SceneView &sc, const CamD &cam, const ModD &mod, uint32_t idx,
                                              int ix, int iy, double *at_out, bool *ray_out, bool *clamped_out) {
   ProjD o;
-  project_d(sc, idx, cam, mod, o);
+  project_d<false, true>(sc, idx, cam, mod, o);  // geometry + alpha only
   const double px = ix + 0.5, py = iy + 0.5;
   const double dx = px - o.ctr[0], dy = py - o.ctr[1];
   double d;
