@@ -89,6 +89,9 @@ typedef struct hgs_settings {
 #define HGS_FLAG_NAIVE 0x1u /* render_naive: every splat for every pixel, no tiles, no bbox test (render.py:101-118) */
 #define HGS_FLAG_FAST 0x2u  /* skip the float64 re-evaluation of near-threshold decisions */
 #define HGS_FLAG_COUNT 0x4u /* count evaluated / contributing pairs per type (hgs_frame_stats) */
+#define HGS_FLAG_DETERMINISTIC 0x8u /* backward: fixed-order (sorted-record) gradient reduction instead of
+                                     * float atomics -- bitwise reproducible; needs the
+                                     * scratch of hgs_backward_det_scratch_bytes */
 
 /* Output images (device, row-major).  Any of normal / alpha may be NULL. */
 typedef struct hgs_images {
@@ -124,6 +127,12 @@ int hgs_forward(const hgs_scene *scene, const hgs_camera *camera, const hgs_sett
 
 /* Scratch bytes for hgs_backward with kg stacked upstream gradients. */
 size_t hgs_backward_scratch_bytes(int64_t n, int32_t kg);
+
+/* Scratch bytes for a HGS_FLAG_DETERMINISTIC backward with room for `records`
+ * per-(splat, warp) / per-(splat, deferred pixel) partial records (about
+ * 1.3 x K at KG = 1).  hgs_backward returns HGS_ERR_PAIR_CAPACITY if they do
+ * not fit: grow the scratch and call again. */
+size_t hgs_backward_det_scratch_bytes(int64_t n, int32_t kg, int64_t records);
 
 /* backward (grad/backward.py:37-181).
  *   pixel_grads  (kg, H, W, 3) dL/dcolor, required

@@ -24,6 +24,7 @@ HGS_ERR_CUDA = 6
 HGS_FLAG_NAIVE = 0x1
 HGS_FLAG_FAST = 0x2
 HGS_FLAG_COUNT = 0x4
+HGS_FLAG_DETERMINISTIC = 0x8
 
 # hgs_train.h constants
 HGS_LOSS_L1, HGS_LOSS_SSIM, HGS_LOSS_LOW, HGS_LOSS_HIGH, HGS_LOSS_COLOR = range(5)
@@ -32,7 +33,7 @@ COMBINE_MODES = {"projection": 0, "naive": 1, "mask": 2}
 
 # Every symbol include/hgs.h and include/hgs_train.h declare.
 EXPORTS = ("hgs_abi_version", "hgs_status_string", "hgs_frame_bytes", "hgs_forward",
-           "hgs_backward_scratch_bytes", "hgs_backward", "hgs_exchange",
+           "hgs_backward_scratch_bytes", "hgs_backward_det_scratch_bytes", "hgs_backward", "hgs_exchange",
            "hgs_frame_export_arrays", "hgs_blend_log", "hgs_frame_stats",
            "hgs_loss_scratch_bytes", "hgs_image_losses", "hgs_dwt_level1", "hgs_dwt_inverse",
            "hgs_combine_gradients", "hgs_adam_step", "hgs_combine_adam_step",
@@ -138,6 +139,8 @@ def lib():
                               P(FrameInfo), _vp]
     L.hgs_backward_scratch_bytes.restype = ctypes.c_size_t
     L.hgs_backward_scratch_bytes.argtypes = [_i64, _i32]
+    L.hgs_backward_det_scratch_bytes.restype = ctypes.c_size_t
+    L.hgs_backward_det_scratch_bytes.argtypes = [_i64, _i32, _i64]
     L.hgs_backward.argtypes = [P(Scene), P(Camera), P(Settings), _vp, P(FrameInfo), _i32, _vp, _vp,
                                _vp, _vp, _vp, ctypes.c_size_t, _vp, _vp, _vp]
     L.hgs_exchange.argtypes = [_i64, _vp, _vp, _vp, ctypes.c_double, _vp, _vp, P(ExchangeReport),

@@ -373,19 +373,81 @@ size_t hgs_backward_scratch_bytes(int64_t n, int32_t kg) {
 
 }  // extern "C"
 
-template <int KG>
+namespace {
+
+// Deterministic-mode record buffers, after the base backward scratch.
+struct DetLayout {
+  size_t count, keys_a, keys_b, vals_a, vals_b, pay, hist, off, lookback, counters, total;
+};
+
+DetLayout det_layout(size_t base, int64_t kc, int64_t cap) {
+  DetLayout d;
+  size_t off = base;
+  auto take = [&](size_t bytes) {
+    size_t o = off;
+    off += (bytes + 255) & ~(size_t)255;
+    return o;
+  };
+  const int64_t cc = std::max<int64_t>(cap, 1);
+  d.count = take(16);
+  d.keys_a = take(cc * 8);
+  d.keys_b = take(cc * 8);
+  d.vals_a = take(cc * 4);
+  d.vals_b = take(cc * 4);
+  d.pay = take((size_t)cc * kc * 20 * 4);
+  d.hist = take(8 * kRadix * 4);
+  d.off = take(8 * kRadix * 4);
+  d.lookback = take((size_t)ceil_div(cc, kSortTile) * kRadix * 4 * 8);
+  d.counters = take(64);
+  d.total = off;
+  return d;
+}
+
+// largest record capacity that fits in scratch_bytes (0 if none)
+int64_t det_capacity(size_t base, int64_t kc, size_t scratch_bytes) {
+  if (det_layout(base, kc, 1).total > scratch_bytes) return 0;
+  int64_t lo = 1, hi = 2;
+  while (det_layout(base, kc, hi).total <= scratch_bytes && hi < (1ll << 32)) hi *= 2;
+  while (hi - lo > 1) {
+    const int64_t mid = (lo + hi) / 2;
+    if (det_layout(base, kc, mid).total <= scratch_bytes) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
+}  // namespace
+
+extern "C" {
+
+size_t hgs_backward_det_scratch_bytes(int64_t n, int32_t kg, int64_t records) {
+  if (n < 0 || kg < 1 || records < 0) return 0;
+  const int64_t kc = std::min<int32_t>(kg, 4);
+  return det_layout(hgs_backward_scratch_bytes(n, kg), kc, records).total;
+}
+
+}  // extern "C"
+
+template <int KG, bool DET>
 static void launch_bwd(const BwdArgs &b, int64_t n_tiles, bool ext, cudaStream_t s) {
-  // hot replay, then the float64-exact fixup of the deferred pixels
-  // pixels per lane: 2 (4 warps per tile) shares the splat walk and the warp
+  // hot replay, then the float64-exact fixup of the deferred pixels.  Pixels
+  // per lane: 2 (4 warps per tile) shares the splat walk and the warp
   // reduction between two pixels; 1 (8 warps) for register-heavy KG
   constexpr int ppl = KG == 1 ? 2 : HGS_BWD_PPL_KG;
   if (ext) {
-    k_composite_bwd<KG, true, ppl><<<(unsigned)n_tiles, 256 / ppl, 0, s>>>(b);
-    k_fixup_bwd<KG, true><<<kFixupBlocks, 256, 0, s>>>(b);
+    k_composite_bwd<KG, true, ppl, DET><<<(unsigned)n_tiles, 256 / ppl, 0, s>>>(b);
+    k_fixup_bwd<KG, true, DET><<<kFixupBlocks, 256, 0, s>>>(b);
   } else {
-    k_composite_bwd<KG, false, ppl><<<(unsigned)n_tiles, 256 / ppl, 0, s>>>(b);
-    k_fixup_bwd<KG, false><<<kFixupBlocks, 256, 0, s>>>(b);
+    k_composite_bwd<KG, false, ppl, DET><<<(unsigned)n_tiles, 256 / ppl, 0, s>>>(b);
+    k_fixup_bwd<KG, false, DET><<<kFixupBlocks, 256, 0, s>>>(b);
   }
+}
+
+template <int KG>
+static void launch_bwd(const BwdArgs &b, int64_t n_tiles, bool ext, bool det, cudaStream_t s) {
+  if (det)
+    launch_bwd<KG, true>(b, n_tiles, ext, s);
+  else
+    launch_bwd<KG, false>(b, n_tiles, ext, s);
 }
 
 extern "C" {
@@ -400,6 +462,13 @@ int hgs_backward(const hgs_scene *scene, const hgs_camera *camera, const hgs_set
   if (rc) return rc;
   if (kg < 1 || !pixel_grads || (scene->n > 0 && (!grads || !touched))) return HGS_ERR_CONFIG;
   if (scratch_bytes < hgs_backward_scratch_bytes(scene->n, kg)) return HGS_ERR_CONFIG;
+  const bool det = settings->flags & HGS_FLAG_DETERMINISTIC;
+  const int64_t kc4 = std::min<int32_t>(kg, 4);
+  const size_t base_bytes = hgs_backward_scratch_bytes(scene->n, kg);
+  const int64_t rec_cap = det ? std::min<int64_t>(det_capacity(base_bytes, kc4, scratch_bytes), 0xffffffffll) : 0;
+  if (det && rec_cap < 1) return HGS_ERR_CONFIG;
+  const DetLayout DL = det_layout(base_bytes, kc4, std::max<int64_t>(rec_cap, 1));
+  char *scr = static_cast<char *>(scratch);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int64_t n = scene->n, m = info->m;
   const int64_t P = 11 + 3 * (int64_t)scene->sh_bases;
@@ -432,14 +501,57 @@ int hgs_backward(const hgs_scene *scene, const hgs_camera *camera, const hgs_set
     b.acc = acc;
     b.acc_ext = ext ? acc_ext : nullptr;
     b.touched = touched;
+    b.rec_keys = det ? reinterpret_cast<unsigned long long *>(scr + DL.keys_a) : nullptr;
+    b.rec_vals = det ? reinterpret_cast<uint32_t *>(scr + DL.vals_a) : nullptr;
+    b.rec_pay = det ? reinterpret_cast<float *>(scr + DL.pay) : nullptr;
+    b.rec_count = det ? reinterpret_cast<uint32_t *>(scr + DL.count) : nullptr;
+    b.rec_cap = (uint32_t)rec_cap;
+    if (det) HGS_CUDA(cudaMemsetAsync(b.rec_count, 0, 4, s));
     if (m > 0) {
       switch (kc) {
-        case 1: launch_bwd<1>(b, info->n_tiles, ext, s); break;
-        case 2: launch_bwd<2>(b, info->n_tiles, ext, s); break;
-        case 3: launch_bwd<3>(b, info->n_tiles, ext, s); break;
-        default: launch_bwd<4>(b, info->n_tiles, ext, s); break;
+        case 1: launch_bwd<1>(b, info->n_tiles, ext, det, s); break;
+        case 2: launch_bwd<2>(b, info->n_tiles, ext, det, s); break;
+        case 3: launch_bwd<3>(b, info->n_tiles, ext, det, s); break;
+        default: launch_bwd<4>(b, info->n_tiles, ext, det, s); break;
       }
       HGS_LAUNCHED();
+      if (det) {  // sort the records by (Gaussian, tile, sub) and reduce in that order
+        uint32_t nrec = 0;
+        HGS_CUDA(cudaMemcpyAsync(&nrec, b.rec_count, 4, cudaMemcpyDeviceToHost, s));
+        HGS_CUDA(cudaStreamSynchronize(s));
+        if ((int64_t)nrec > rec_cap) return HGS_ERR_PAIR_CAPACITY;  // grow the scratch, call again
+        uint32_t *hist = reinterpret_cast<uint32_t *>(scr + DL.hist);
+        uint32_t *offs = reinterpret_cast<uint32_t *>(scr + DL.off);
+        HGS_CUDA(cudaMemsetAsync(hist, 0, 8 * kRadix * 4, s));
+        if (nrec > 0) {
+          k_radix_histogram<unsigned long long><<<grid_for(nrec, 256), 256, 0, s>>>(b.rec_keys, nrec, 8, hist);
+          HGS_LAUNCHED();
+        }
+        k_radix_offsets<<<8, kRadix, 0, s>>>(hist, offs);
+        HGS_LAUNCHED();
+        uint32_t h[8 * kRadix];
+        HGS_CUDA(cudaMemcpyAsync(h, hist, sizeof(h), cudaMemcpyDeviceToHost, s));
+        HGS_CUDA(cudaStreamSynchronize(s));
+        int passes[8], np = 0;
+        for (int pss = 0; pss < 8; ++pss) {
+          bool trivial = false;
+          for (int d = 0; d < kRadix; ++d)
+            if (h[pss * kRadix + d] == nrec) trivial = true;
+          if (!trivial) passes[np++] = pss;
+        }
+        bool in_b = false;
+        rc = radix_sort<unsigned long long>(b.rec_keys, reinterpret_cast<unsigned long long *>(scr + DL.keys_b),
+                                            b.rec_vals, reinterpret_cast<uint32_t *>(scr + DL.vals_b), nrec, passes,
+                                            np, offs, reinterpret_cast<uint32_t *>(scr + DL.lookback),
+                                            reinterpret_cast<uint32_t *>(scr + DL.counters), s, &in_b);
+        if (rc) return rc;
+        const unsigned long long *sk = in_b ? reinterpret_cast<unsigned long long *>(scr + DL.keys_b) : b.rec_keys;
+        const uint32_t *sv = in_b ? reinterpret_cast<uint32_t *>(scr + DL.vals_b) : b.rec_vals;
+        if (nrec > 0) {
+          k_det_reduce<<<grid_for(nrec, 256), 256, 0, s>>>(sk, sv, b.rec_pay, nrec, kc, acc, ext ? acc_ext : nullptr);
+          HGS_LAUNCHED();
+        }
+      }
       if (k0 == 0) HGS_CUDA(record_event(settings, 1, s));
     }
     ChainArgs c = c0;

@@ -161,12 +161,14 @@ __device__ __forceinline__ void pair_grads(const SplatRec &r, const PairEval &p,
 }
 
 // One CTA per 16 x 16 tile; a warp owns an 8 x (4 PPL) block and each lane
-// PPL pixels of it, (x, y + 4q).  With PPL = 2 (4 warps per tile)  Every staged splat is walked
-// once for both pixels of a lane: the chunk staging, the splat header and --
-// the dominant per-splat cost -- the 16-slot warp reduction + atomic flush
-// are shared by 64 pixels instead of 32, while the per-pixel math is
-// unchanged (a pixel's evaluation runs only where its 8 x 4 half is covered).
-template <int KG, bool EXT, int PPL>
+// PPL pixels of it, (x, y + 4q).  With PPL = 2 (4 warps per tile) every
+// staged splat is walked once for both pixels of a lane: the chunk staging,
+// the splat header and -- the dominant per-splat cost -- the 16-slot warp
+// reduction + atomic flush are shared by 64 pixels instead of 32, while the
+// per-pixel math is unchanged (a pixel's evaluation runs only where its 8 x 4
+// half is covered).  DET: the flush writes one record per (splat, warp)
+// instead of atomics (HGS_FLAG_DETERMINISTIC, reduced by k_det_reduce).
+template <int KG, bool EXT, int PPL, bool DET>
 __global__ void __launch_bounds__(256 / PPL, PPL == 2 ? (KG == 1 ? HGS_BWD_MINB1 : 4) : 3) k_composite_bwd(BwdArgs b) {
   const CompositeArgs &a = b.c;
   __shared__ SplatRec s_rec[8 / PPL][32];
@@ -298,12 +300,26 @@ __global__ void __launch_bounds__(256 / PPL, PPL == 2 ? (KG == 1 ? HGS_BWD_MINB1
       const bool is3d = rec_is3d(r);
       const uint32_t gidx = rec_idx(r);
       if (lane == 0) b.touched[gidx] = 1;
+      uint32_t rec = 0;
+      if (DET) {  // one record per (splat, warp); written in full (zeros included)
+        if (lane == 0) {
+          rec = atomicAdd(b.rec_count, 1u);
+          if (rec < b.rec_cap) {
+            b.rec_keys[rec] = det_key(gidx, (uint32_t)tile, (uint32_t)warp);
+            b.rec_vals[rec] = rec;
+          }
+        }
+        rec = __shfl_sync(0xffffffffu, rec, 0);
+      }
 #pragma unroll
       for (int k = 0; k < KG; ++k) {
         const float tot = warp_transpose_reduce16(v[k], lane);
         const int nslots = is3d ? 9 : 15;
-        if (!(lane & 1) && slot < nslots && tot != 0.f)
+        if (DET) {
+          if (!(lane & 1) && rec < b.rec_cap) b.rec_pay[(size_t)rec * (KG * 20) + k * 20 + slot] = tot;
+        } else if (!(lane & 1) && slot < nslots && tot != 0.f) {
           atomicAdd(b.acc + ((int64_t)gidx * KG + k) * kAcc + slot, tot);
+        }
         if (EXT) {
 #pragma unroll
           for (int s2 = 0; s2 < 4; ++s2) {
@@ -314,8 +330,14 @@ __global__ void __launch_bounds__(256 / PPL, PPL == 2 ? (KG == 1 ? HGS_BWD_MINB1
           }
           if (lane < 4) {
             const float x = lane == 0 ? ve[k][0] : (lane == 1 ? ve[k][1] : (lane == 2 ? ve[k][2] : ve[k][3]));
-            if (x != 0.f) atomicAdd(b.acc_ext + ((int64_t)gidx * KG + k) * kAccExt + lane, x);
+            if (DET) {
+              if (rec < b.rec_cap) b.rec_pay[(size_t)rec * (KG * 20) + k * 20 + 16 + lane] = x;
+            } else if (x != 0.f) {
+              atomicAdd(b.acc_ext + ((int64_t)gidx * KG + k) * kAccExt + lane, x);
+            }
           }
+        } else if (DET && lane < 4 && rec < b.rec_cap) {
+          b.rec_pay[(size_t)rec * (KG * 20) + k * 20 + 16 + lane] = 0.f;
         }
       }
     }
@@ -364,7 +386,7 @@ __device__ __forceinline__ float scan_add_ex(float x, int lane) {
 // inclusive product of (1 - at) over the lanes up to it, the suffix sums are
 // exclusive prefix sums of c * w; every lane then adds its pair's gradients
 // with per-lane atomics.
-template <int KG, bool EXT>
+template <int KG, bool EXT, bool DET>
 __global__ void __launch_bounds__(256, HGS_FIXUP_MINB) k_fixup_bwd(BwdArgs b) {
   const CompositeArgs &a = b.c;
   const uint32_t nfix = a.st->n_fix_bwd;
@@ -431,12 +453,25 @@ __global__ void __launch_bounds__(256, HGS_FIXUP_MINB) k_fixup_bwd(BwdArgs b) {
         const uint32_t gidx = rec_idx(r);
         b.touched[gidx] = 1;
         const int nslots = rec_is3d(r) ? 9 : 15;
-        for (int k = 0; k < KG; ++k) {
-          for (int s = 0; s < nslots; ++s)
-            if (v[k][s] != 0.f) atomicAdd(b.acc + ((int64_t)gidx * KG + k) * kAcc + s, v[k][s]);
-          if (EXT)
-            for (int s = 0; s < 4; ++s)
-              if (ve[k][s] != 0.f) atomicAdd(b.acc_ext + ((int64_t)gidx * KG + k) * kAccExt + s, ve[k][s]);
+        if (DET) {  // one record per (splat, pixel)
+          const uint32_t rec = atomicAdd(b.rec_count, 1u);
+          if (rec < b.rec_cap) {
+            b.rec_keys[rec] = det_key(gidx, (uint32_t)tile, 4u + (uint32_t)((iy % kTile) * kTile + ix % kTile));
+            b.rec_vals[rec] = rec;
+            float *pp = b.rec_pay + (size_t)rec * (KG * 20);
+            for (int k = 0; k < KG; ++k) {
+              for (int s = 0; s < 16; ++s) pp[k * 20 + s] = v[k][s];
+              for (int s = 0; s < 4; ++s) pp[k * 20 + 16 + s] = EXT ? ve[k][s] : 0.f;
+            }
+          }
+        } else {
+          for (int k = 0; k < KG; ++k) {
+            for (int s = 0; s < nslots; ++s)
+              if (v[k][s] != 0.f) atomicAdd(b.acc + ((int64_t)gidx * KG + k) * kAcc + s, v[k][s]);
+            if (EXT)
+              for (int s = 0; s < 4; ++s)
+                if (ve[k][s] != 0.f) atomicAdd(b.acc_ext + ((int64_t)gidx * KG + k) * kAccExt + s, ve[k][s]);
+          }
         }
       }
       // carry T_run and the suffix sums across chunks
@@ -455,11 +490,40 @@ __global__ void __launch_bounds__(256, HGS_FIXUP_MINB) k_fixup_bwd(BwdArgs b) {
   }
 }
 
-// Instantiations: KG 1..4, with / without extension gradients.
-#define HGS_INST_BWD(KG, EXT)                                     \
-  template __global__ void k_composite_bwd<KG, EXT, 1>(BwdArgs); \
-  template __global__ void k_composite_bwd<KG, EXT, 2>(BwdArgs); \
-  template __global__ void k_fixup_bwd<KG, EXT>(BwdArgs);
+// Deterministic mode: records sorted by key (Gaussian, tile, sub) -> sum each
+// Gaussian's records in key order into its accumulator slots.
+__global__ void k_det_reduce(const unsigned long long *__restrict__ keys, const uint32_t *__restrict__ vals,
+                             const float *__restrict__ pay, int64_t nrec, int kg, float *__restrict__ acc,
+                             float *__restrict__ acc_ext) {
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < nrec; p += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t g = (uint32_t)(keys[p] >> 32);
+    if (p > 0 && (uint32_t)(keys[p - 1] >> 32) == g) continue;  // not the head of its segment
+    for (int k = 0; k < kg; ++k) {
+      float sum[20];
+#pragma unroll
+      for (int s = 0; s < 20; ++s) sum[s] = 0.f;
+      for (int64_t q = p; q < nrec && (uint32_t)(keys[q] >> 32) == g; ++q) {
+        const float *pp = pay + (size_t)vals[q] * (kg * 20) + k * 20;
+#pragma unroll
+        for (int s = 0; s < 20; ++s) sum[s] += pp[s];
+      }
+#pragma unroll
+      for (int s = 0; s < 16; ++s) acc[((int64_t)g * kg + k) * kAcc + s] = sum[s];
+      if (acc_ext)
+#pragma unroll
+        for (int s = 0; s < 4; ++s) acc_ext[((int64_t)g * kg + k) * kAccExt + s] = sum[16 + s];
+    }
+  }
+}
+
+// Instantiations: KG 1..4, with / without extension gradients, atomic and
+// deterministic accumulation; the pixels-per-lane the launcher uses.
+#define HGS_PPL(KG) ((KG) == 1 ? 2 : HGS_BWD_PPL_KG)
+#define HGS_INST_BWD(KG, EXT)                                                   \
+  template __global__ void k_composite_bwd<KG, EXT, HGS_PPL(KG), false>(BwdArgs); \
+  template __global__ void k_composite_bwd<KG, EXT, HGS_PPL(KG), true>(BwdArgs);  \
+  template __global__ void k_fixup_bwd<KG, EXT, false>(BwdArgs);                  \
+  template __global__ void k_fixup_bwd<KG, EXT, true>(BwdArgs);
 HGS_INST_BWD(1, false)
 HGS_INST_BWD(2, false)
 HGS_INST_BWD(3, false)

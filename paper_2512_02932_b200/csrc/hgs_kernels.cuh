@@ -484,7 +484,20 @@ struct BwdArgs {
   float *acc;               // (n, KG, 16)
   float *acc_ext;           // (n, KG, 4) or null
   uint8_t *touched;         // (n) by Gaussian index, zeroed by the caller
+  // HGS_FLAG_DETERMINISTIC: per-(splat, warp) / per-(splat, pixel) records
+  // instead of atomics; sorted by key and reduced in key order afterwards
+  unsigned long long *rec_keys;  // (rec_cap) gidx << 32 | tile << 9 | sub
+  uint32_t *rec_vals;            // (rec_cap) record index (the sort's values)
+  float *rec_pay;                // (rec_cap, KG * 20): 16 slots + 4 extension slots per kg
+  uint32_t *rec_count;
+  uint32_t rec_cap;
 };
+
+// sub-key of a deterministic-mode record: the warp (main kernel) or 4 + the
+// pixel within its tile (fixup kernel) -- unique per (Gaussian, tile)
+__device__ __forceinline__ unsigned long long det_key(uint32_t gidx, uint32_t tile, uint32_t sub) {
+  return ((unsigned long long)gidx << 32) | ((unsigned long long)tile << 9) | sub;
+}
 
 struct ChainArgs {
   SceneView sc;
@@ -516,10 +529,12 @@ __global__ void k_tile_ranges(const uint32_t *skeys, int64_t k, int64_t n_tiles,
 template <bool NAIVE, bool COUNT>
 __global__ void k_composite_fwd(CompositeArgs a);
 __global__ void k_fixup_fwd(CompositeArgs a);
-template <int KG, bool EXT, int PPL>
+template <int KG, bool EXT, int PPL, bool DET>
 __global__ void k_composite_bwd(BwdArgs b);
-template <int KG, bool EXT>
+template <int KG, bool EXT, bool DET>
 __global__ void k_fixup_bwd(BwdArgs b);
+__global__ void k_det_reduce(const unsigned long long *keys, const uint32_t *vals, const float *pay, int64_t nrec,
+                             int kg, float *acc, float *acc_ext);
 template <int DEG>
 __global__ void k_chain_rule_t(ChainArgs c);
 __global__ void k_exchange_scan(int64_t n, const float *log_scale, const uint8_t *type_spec, double theta_e,

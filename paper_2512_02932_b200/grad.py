@@ -116,11 +116,17 @@ def _as_device(a, dev, name, shape):
     return t.contiguous()
 
 
+_det_hint = {}  # (n, kg, W, H) -> record capacity that sufficed last time
+
+
 def backward_device(frame, pixel_grads, depth_grads=None, normal_grads=None, alpha_grads=None,
-                    grads_out=None, touched_out=None, events=None, flags=None, scratch=None):
+                    grads_out=None, touched_out=None, events=None, flags=None, scratch=None,
+                    deterministic=False):
     """Device-level backward.  pixel_grads (KG,H,W,3) float32 CUDA; returns
     (grads (KG, n*P) float32, touched (n,) uint8).  ``events`` (3
-    torch.cuda.Event) are recorded at the library's stage boundaries."""
+    torch.cuda.Event) are recorded at the library's stage boundaries.
+    ``deterministic``: fixed-order gradient reduction (HGS_FLAG_DETERMINISTIC),
+    bitwise reproducible run to run, at extra memory and time."""
     import torch
     L = _lib.lib()
     ds = frame.scene
@@ -132,21 +138,34 @@ def backward_device(frame, pixel_grads, depth_grads=None, normal_grads=None, alp
         grads_out = torch.empty((kg, n * P), dtype=torch.float32, device=dev)
     if touched_out is None:
         touched_out = torch.empty(max(n, 1), dtype=torch.uint8, device=dev)
-    nscr = L.hgs_backward_scratch_bytes(n, kg)
-    if scratch is None or scratch.numel() < nscr:
-        scratch = torch.empty(nscr, dtype=torch.uint8, device=dev)
     fl = frame.flags if flags is None else flags
-    _lib.check(L.hgs_backward(
-        _lib.scene_struct(ds), _lib.camera_struct(frame.camera),
-        _lib.settings_struct(frame.settings, fl, events), _lib.ptr(frame.buf), frame.info, kg,
-        _lib.ptr(pixel_grads), _lib.ptr(depth_grads), _lib.ptr(normal_grads),
-        _lib.ptr(alpha_grads), _lib.ptr(scratch), nscr, _lib.ptr(grads_out), _lib.ptr(touched_out),
-        _lib.current_stream_handle(dev)), "hgs_backward")
-    return grads_out, touched_out[:n]
+    if deterministic:
+        fl |= _lib.HGS_FLAG_DETERMINISTIC
+    key = (n, kg, frame.width, frame.height)
+    records = _det_hint.get(key, 2 * frame.pair_count + (1 << 16))
+    for _ in range(8):
+        nscr = (L.hgs_backward_det_scratch_bytes(n, kg, records) if deterministic
+                else L.hgs_backward_scratch_bytes(n, kg))
+        if scratch is None or scratch.numel() < nscr:
+            scratch = torch.empty(nscr, dtype=torch.uint8, device=dev)
+        rc = L.hgs_backward(
+            _lib.scene_struct(ds), _lib.camera_struct(frame.camera),
+            _lib.settings_struct(frame.settings, fl, events), _lib.ptr(frame.buf), frame.info, kg,
+            _lib.ptr(pixel_grads), _lib.ptr(depth_grads), _lib.ptr(normal_grads),
+            _lib.ptr(alpha_grads), _lib.ptr(scratch), scratch.numel(), _lib.ptr(grads_out),
+            _lib.ptr(touched_out), _lib.current_stream_handle(dev))
+        if deterministic and rc == _lib.HGS_ERR_PAIR_CAPACITY:
+            records *= 8
+            continue
+        _lib.check(rc, "hgs_backward")
+        if deterministic:
+            _det_hint[key] = records
+        return grads_out, touched_out[:n]
+    raise _lib.ExtensionError("could not size the deterministic backward scratch")
 
 
 def backward(scene, camera, output, pixel_grad, depth_grad=None, normal_grad=None,
-             alpha_grad=None, validate=True):
+             alpha_grad=None, validate=True, deterministic=False):
     """Gradients of a scalar image loss with upstream dL/d(color image)
     (grad/backward.py:37-181).  pixel_grad (H,W,3) or (KG,H,W,3).  Returns a
     ParamGrads (or a list of KG) and the per-Gaussian touched mask."""
@@ -173,7 +192,7 @@ def backward(scene, camera, output, pixel_grad, depth_grad=None, normal_grad=Non
             raise IntegrityError("pixel_grad contains non-finite values")
     output.check_scene(scene)
     host = isinstance(scene, GaussianSet)
-    grads, touched = backward_device(frame, pg, dg, ng, ag)
+    grads, touched = backward_device(frame, pg, dg, ng, ag, deterministic=deterministic)
     n, B = frame.scene.count, frame.scene.sh_bases
     if host:
         from ._hostio import download
