@@ -609,6 +609,17 @@ def main():
         ach = hbm_bytes[dom] / t_dom / 1e9
         roof = {"kernel": dom, "bound": "hbm", "achieved": ach, "peak": hbm_peak, "unit": "GB/s",
                 "frac": ach / hbm_peak, "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
+    # the limiter of the compositors is the SM issue rate, not a pipe peak:
+    # quote the committed ncu capture of the same kernel (profiles/)
+    ncu_file = os.path.join(REPO, "profiles", "ncu_r01b_kernels.json")
+    if dom in ("composite_fwd", "composite_bwd") and os.path.exists(ncu_file):
+        pref = "k_composite_fwd<0, 0>" if dom == "composite_fwd" else "k_composite_bwd<1, 0, 2>"
+        for kd in json.load(open(ncu_file)):
+            if kd.get("config") == "c2" and kd.get("kernel") == pref:
+                roof["limiter"] = ("SM instruction issue (ncu, profiles/ncu_r01b_kernels.json: issue "
+                                   "active %.0f%%, FP32 pipe %.0f%%, DRAM %.0f%%, %.1f of 32 lanes active)"
+                                   % (kd.get("issue_active_pct", 0), kd.get("fma_pipe_pct", 0),
+                                      kd.get("dram_pct", 0), kd.get("thread_inst_per_inst", 0)))
     traffic_file = os.path.join(REPO, "profiles", "traffic.json")
     roof["traffic"] = None
     if os.path.exists(traffic_file):
