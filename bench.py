@@ -43,6 +43,18 @@ FLOP_BWD_2D_RAY = 115
 FLOP_BWD_2D_LP = 40
 
 
+def init_dist(dev):
+    """NCCL process group (one process per GPU).  HGS_DIST_BACKEND=gloo runs
+    the same multi-rank code path with several ranks on one GPU (a logic
+    check on single-GPU boxes; NCCL refuses duplicate devices)."""
+    import torch.distributed as dist
+    backend = os.environ.get("HGS_DIST_BACKEND", "nccl")
+    if backend == "nccl":
+        dist.init_process_group("nccl", device_id=dev)
+    else:
+        dist.init_process_group(backend)
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -175,6 +187,9 @@ def cpu_baseline(scene, cam, st, crop, kg=1):
     centred 1/crop^2 crop, extrapolated linearly in pixel count."""
     import oracle
     from paper_2512_02932_b200.synthetic import synthetic_camera
+    # all host cores (torchrun sets OMP_NUM_THREADS=1 per rank)
+    oracle.set_num_threads(len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity")
+                           else os.cpu_count())
     W, H = cam.width, cam.height
     cw, ch = W // crop, H // crop
     ccam = synthetic_camera(cw, ch)
@@ -243,11 +258,11 @@ def run_extra(a):
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0")) % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        init_dist(dev)
     st = RenderSettings()
     flags = _lib.HGS_FLAG_FAST if a.fast else 0
     if a.config == 3:
@@ -350,11 +365,11 @@ def run_train(a):
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0")) % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        init_dist(dev)
     n = 3_000_000 if a.n == 1_000_000 else a.n
     W, H = a.width, a.height
     scene, cam = synthetic_scene(n, W, H, 3, seed=0)
@@ -478,11 +493,11 @@ def main():
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0")) % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        init_dist(dev)
 
     scene, cam = synthetic_scene(a.n, a.width, a.height, a.sh_degree, seed=0)
     st = RenderSettings()
