@@ -16,7 +16,7 @@ constexpr int kFixupBlocks = 148 * 4;  // persistent fixup grid (one warp per de
 
 struct Layout {
   size_t state, hist_d, off_d, hist_p, off_p, keys_a, keys_b, vals_a, vals_b, lb_sort, lb_scan, recs, pair_off,
-      pk_a, pk_b, pv_a, pv_b, tile_off, pix_T, pix_last, pix_count, fwd_fix, bwd_fix, total;
+      pk_a, pk_b, pv_a, pv_b, tile_off, pix_T, pix_last, pix_count, fwd_fix, bwd_fix, pix_mask, total;
   size_t small_end;  // [state, small_end) is zeroed at the start of a forward
   size_t lb_sort_bytes, lb_scan_bytes;
 };
@@ -55,6 +55,9 @@ Layout make_layout(int64_t n, int W, int H, int64_t cap) {
   L.pix_count = take((size_t)W * H * 4);
   L.fwd_fix = take((size_t)W * H * sizeof(FwdFix));
   L.bwd_fix = take((size_t)W * H * sizeof(BwdFix));
+  // contribution masks: one 32-bit word per (pixel, 32-entry chunk of its
+  // tile list), chunk words of tile t at floor(lo_t / 32) + t + c
+  L.pix_mask = take((size_t)((cc >> 5) + n_tiles + 2) * kBlock * 4);
   L.pk_a = take(cc * 4);
   L.pk_b = take(cc * 4);
   L.pv_a = take(cc * 4);
@@ -319,6 +322,7 @@ int hgs_forward(const hgs_scene *scene, const hgs_camera *camera, const hgs_sett
   a.st = st;
   a.fwd_fix = at<FwdFix>(frame, L.fwd_fix);
   a.bwd_fix = at<BwdFix>(frame, L.bwd_fix);
+  a.pix_mask = at<uint32_t>(frame, L.pix_mask);
   const bool naive = settings->flags & HGS_FLAG_NAIVE, count = settings->flags & HGS_FLAG_COUNT;
   if (naive && count) k_composite_fwd<true, true><<<(unsigned)n_tiles, kBlock, 0, s>>>(a);
   else if (naive) k_composite_fwd<true, false><<<(unsigned)n_tiles, kBlock, 0, s>>>(a);
@@ -351,6 +355,7 @@ static CompositeArgs composite_args_for(const hgs_scene *scene, const hgs_camera
   a.st = at<FrameState>(fr, L.state);
   a.fwd_fix = at<FwdFix>(fr, L.fwd_fix);
   a.bwd_fix = at<BwdFix>(fr, L.bwd_fix);
+  a.pix_mask = at<uint32_t>(fr, L.pix_mask);
   (void)scene;
   (void)camera;
   return a;

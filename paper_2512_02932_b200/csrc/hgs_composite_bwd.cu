@@ -210,11 +210,36 @@ __global__ void __launch_bounds__(256 / PPL, PPL == 2 ? (KG == 1 ? HGS_BWD_MINB1
   SplatRec *wrec = s_rec[warp];
 
   for (uint32_t top = warp_end, start; top > lo; top = start) {
-    start = top - lo > 32u ? top - 32u : lo;
+    // chunks aligned to the forward's 32-entry chunks (contribution masks)
+    start = naive ? (top - lo > 32u ? top - 32u : lo) : lo + (((top - 1u - lo) >> 5) << 5);
     const uint32_t j = start + lane;
     uint32_t pm[PPL], any_pm = 0u;
 #pragma unroll
     for (int q = 0; q < PPL; ++q) pm[q] = 0u;
+    uint32_t rel;
+    if (!naive) {
+      // the forward's exact decisions: pm[q] = this lane's pixel q contributing
+      // entries of the chunk (bits at or past the pixel's last contributor cleared)
+      const uint32_t ch = (start - lo) >> 5;
+#pragma unroll
+      for (int q = 0; q < PPL; ++q) {
+        if (!dead[q] && inside[q] && (ch << 5) < last[q]) {
+          uint32_t w = a.pix_mask[mask_word(lo, tile, ch, (uint32_t)((iy[q] & (kTile - 1)) * kTile + (ix & (kTile - 1))))];
+          const uint32_t rem = last[q] - (ch << 5);
+          if (rem < 32u) w &= (1u << rem) - 1u;
+          pm[q] = w;
+        }
+        any_pm |= pm[q];
+      }
+      rel = __reduce_or_sync(0xffffffffu, any_pm);
+      if ((rel >> lane) & 1u) {
+        const SplatRec *g = a.recs + __ldg(a.tile_vals + j);
+        SplatRec r;
+        r.r0 = __ldg(&g->r0); r.r1 = __ldg(&g->r1); r.r2 = __ldg(&g->r2);
+        r.r3 = __ldg(&g->r3); r.r4 = __ldg(&g->r4); r.r5 = __ldg(&g->r5);
+        wrec[lane] = r;
+      }
+    } else {
     if (j < top) {
       const uint32_t rk = naive ? j : __ldg(a.tile_vals + j);
       const SplatRec *g = a.recs + rk;
@@ -239,14 +264,15 @@ __global__ void __launch_bounds__(256 / PPL, PPL == 2 ? (KG == 1 ? HGS_BWD_MINB1
         if (any_pm) wrec[lane] = r;
       }
     }
-    uint32_t rel = __ballot_sync(0xffffffffu, any_pm != 0u);
+    rel = __ballot_sync(0xffffffffu, any_pm != 0u);
+    }  // naive staging
     __syncwarp();
     while (rel) {
       const int e = 31 - __clz(rel);
       rel &= ~(1u << e);
       uint32_t mq[PPL];
 #pragma unroll
-      for (int q = 0; q < PPL; ++q) mq[q] = __shfl_sync(0xffffffffu, pm[q], e);
+      for (int q = 0; q < PPL; ++q) mq[q] = naive ? __shfl_sync(0xffffffffu, pm[q], e) : pm[q];
       const uint32_t jj = start + e;
       const SplatRec &r = wrec[e];
       float v[KG][16];
@@ -262,7 +288,8 @@ __global__ void __launch_bounds__(256 / PPL, PPL == 2 ? (KG == 1 ? HGS_BWD_MINB1
 #pragma unroll
       for (int q = 0; q < PPL; ++q) {
         const uint32_t m = mq[q];
-        const bool act = !dead[q] && inside[q] && (m & lane_bit) && jj - lo < last[q];
+        const bool act = naive ? (!dead[q] && inside[q] && (m & lane_bit) && jj - lo < last[q])
+                               : (!dead[q] && ((m >> e) & 1u));
         PairEval p;
         if (count && act) ++n_ev;
         const int c = act ? eval_fast<true>(r, ix, iy[q], a.flags, p) : kSkip;

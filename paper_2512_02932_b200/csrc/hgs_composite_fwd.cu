@@ -84,6 +84,8 @@ __global__ void __launch_bounds__(kBlock, HGS_FWD_MINB) k_composite_fwd(Composit
     }
     uint32_t rel = __ballot_sync(0xffffffffu, pm != 0u);
     __syncwarp();
+    const bool walking = !done;  // this chunk's mask word is written iff the pixel walks it
+    uint32_t cm = 0u;
     while (rel) {
       const int e = __ffs(rel) - 1;
       rel &= rel - 1;
@@ -111,6 +113,7 @@ __global__ void __launch_bounds__(kBlock, HGS_FWD_MINB) k_composite_fwd(Composit
       n1 = fmaf(w, c4.y, n1);
       n2 = fmaf(w, c4.z, n2);
       ++cnt;
+      cm |= 1u << e;
       last = base + e - lo + 1u;
       T = T * (1.f - at);
       // early stop T < 1e-4 (_blend_py.py:111-113); near the threshold the
@@ -130,6 +133,8 @@ __global__ void __launch_bounds__(kBlock, HGS_FWD_MINB) k_composite_fwd(Composit
         done = true;
 #endif
     }
+    if (!NAIVE && walking)
+      a.pix_mask[mask_word(lo, tile, (base - lo) >> 5, (uint32_t)((iy & (kTile - 1)) * kTile + (ix & (kTile - 1))))] = cm;
     __syncwarp();  // the next chunk overwrites this warp's staging slots
   }
   if (COUNT) {
@@ -200,6 +205,11 @@ __global__ void __launch_bounds__(256, HGS_FIXUP_MINB) k_fixup_fwd(CompositeArgs
       stopped = replay_T_below(a.recs, a.tile_vals, a.flags, a.st, lo, f.entry, ix, iy);
       start = f.entry + 1u;
     }
+    // contribution-mask words from the resume point on (the main kernel wrote
+    // the deferral chunk's bits before the resume point)
+    const uint32_t pit = (uint32_t)((iy & (kTile - 1)) * kTile + (ix & (kTile - 1)));
+    uint32_t w_cur = (start - lo) >> 5;
+    uint32_t cur = (!naive && w_cur == ((f.entry - lo) >> 5)) ? a.pix_mask[mask_word(lo, tile, w_cur, pit)] : 0u;
     for (uint32_t base = start; base < hi && !stopped; base += 32) {
       const uint32_t e = base + lane;
       bool con = false;
@@ -250,6 +260,13 @@ __global__ void __launch_bounds__(256, HGS_FIXUP_MINB) k_fixup_fwd(CompositeArgs
       n1 += warp_sum(valid ? wgt * r.r4.y : 0.f);
       n2 += warp_sum(valid ? wgt * r.r4.z : 0.f);
       const uint32_t vm = __ballot_sync(0xffffffffu, valid);
+      if (!naive && lane == 0) {  // window [base, base + 32) completes word w_cur, opens w_cur + 1
+        const uint32_t sh = (base - lo) & 31u;
+        cur |= vm << sh;
+        a.pix_mask[mask_word(lo, tile, w_cur, pit)] = cur;
+        cur = sh ? vm >> (32 - sh) : 0u;
+        ++w_cur;
+      }
       cnt += __popc(vm);
       if (vm) last = base + (31 - __clz(vm)) - lo + 1u;
       if (first < 32) {
@@ -260,6 +277,9 @@ __global__ void __launch_bounds__(256, HGS_FIXUP_MINB) k_fixup_fwd(CompositeArgs
       }
     }
     if (lane == 0) {
+      // the open word, if it is still a chunk of this tile list (words past
+      // the list belong to the next tile)
+      if (!naive && hi > lo && w_cur <= ((hi - 1 - lo) >> 5)) a.pix_mask[mask_word(lo, tile, w_cur, pit)] = cur;
       const uint32_t pix = f.pix;
       a.color[3 * pix + 0] = c0 + a.bg[0] * T;
       a.color[3 * pix + 1] = c1 + a.bg[1] * T;

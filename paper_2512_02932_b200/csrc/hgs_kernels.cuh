@@ -60,7 +60,15 @@ struct CompositeArgs {
   FrameState *st;  // diagnostics + scene / camera for float64 re-checks
   FwdFix *fwd_fix;  // (H * W) worklist
   BwdFix *bwd_fix;  // (H * W) worklist
+  // the forward's exact contribution decisions, replayed by the backward:
+  // bit e of word mask_word(lo, tile, c) * 256 + pixel-in-tile is set iff
+  // tile-list entry lo + 32 c + e contributed to the pixel (not NAIVE)
+  uint32_t *pix_mask;
 };
+
+__device__ __forceinline__ size_t mask_word(uint32_t lo, int tile, uint32_t chunk, uint32_t pix_in_tile) {
+  return ((size_t)(lo >> 5) + (size_t)tile + chunk) * kBlock + pix_in_tile;
+}
 
 // log2 domain constants: at = ex2(arg), arg = log2(alpha_eff) - d * 0.5 log2(e)
 constexpr float kHalfLog2e = 0.72134752044448170f;
