@@ -464,13 +464,21 @@ __global__ void __launch_bounds__(256, HGS_FIXUP_MINB) k_fixup_bwd(BwdArgs b) {
     const float T_fin = a.pix_T[f.pix];
     float T_run = f.T_run;
     Suffix S{f.S0, f.S1, f.S2, f.SD, f.SN0, f.SN1, f.SN2};
+    // software pipeline: next window's ranks loaded, records prefetched into L2
+    const int64_t e0 = (int64_t)f.entry - lane;
+    uint32_t rk_next = e0 >= (int64_t)lo ? (naive ? (uint32_t)e0 : a.tile_vals[e0]) : 0u;
     for (int64_t top = (int64_t)f.entry + 1; top > (int64_t)lo; top -= 32) {
       const int64_t e = top - 1 - lane;
+      const uint32_t rk_cur = rk_next;
+      if (e - 32 >= (int64_t)lo) {
+        rk_next = naive ? (uint32_t)(e - 32) : a.tile_vals[e - 32];
+        prefetch_rec(a.recs + rk_next);
+      }
       bool con = false;
       PairEval p;
       SplatRec r;
       if (e >= (int64_t)lo) {
-        const uint32_t rk = naive ? (uint32_t)e : a.tile_vals[e];
+        const uint32_t rk = rk_cur;
         r = a.recs[rk];
         if (naive || in_bbox(r.r5, ix, iy)) con = eval_pair<true>(r, a.recs + rk, ix, iy, a.flags, a.st, p);
       }

@@ -98,6 +98,7 @@ __global__ void __launch_bounds__(kBlock, HGS_FWD_MINB) k_composite_fwd(Composit
       const int c = eval_fast<false>(r, ix, iy, a.flags, p);
       if (c == kSkip) continue;
       if (c == kAmbiguous) {
+        if (COUNT) atomicAdd(&a.st->diag[is3d ? 12 : 13], 1ull);  // deferral reasons
         defer(base + e, 0u);
         continue;
       }
@@ -121,8 +122,10 @@ __global__ void __launch_bounds__(kBlock, HGS_FWD_MINB) k_composite_fwd(Composit
       // compare on the common path (T well above the threshold).
 #if HGS_FWD_STOP_FAST
       if (T <= (float)kEarlyStopT * (1.f + 2e-5f)) {
-        if (exact && T >= (float)kEarlyStopT * (1.f - 2e-5f))
+        if (exact && T >= (float)kEarlyStopT * (1.f - 2e-5f)) {
+          if (COUNT) atomicAdd(&a.st->diag[14], 1ull);
           defer(base + e, 1u);
+        }
         else if (T < (float)kEarlyStopT)
           done = true;
       }
@@ -210,13 +213,21 @@ __global__ void __launch_bounds__(256, HGS_FIXUP_MINB) k_fixup_fwd(CompositeArgs
     const uint32_t pit = (uint32_t)((iy & (kTile - 1)) * kTile + (ix & (kTile - 1)));
     uint32_t w_cur = (start - lo) >> 5;
     uint32_t cur = (!naive && w_cur == ((f.entry - lo) >> 5)) ? a.pix_mask[mask_word(lo, tile, w_cur, pit)] : 0u;
+    // software pipeline: the next window's ranks are loaded and its records
+    // prefetched into L2 while this window is evaluated
+    uint32_t rk_next = start + lane < hi ? (naive ? start + lane : a.tile_vals[start + lane]) : 0u;
     for (uint32_t base = start; base < hi && !stopped; base += 32) {
       const uint32_t e = base + lane;
+      const uint32_t rk_cur = rk_next;
+      if (base + 32 + lane < hi) {
+        rk_next = naive ? base + 32 + lane : a.tile_vals[base + 32 + lane];
+        prefetch_rec(a.recs + rk_next);
+      }
       bool con = false;
       float at = 0.f;
       SplatRec r;
       if (e < hi) {
-        const uint32_t rk = naive ? e : a.tile_vals[e];
+        const uint32_t rk = rk_cur;
         r = a.recs[rk];
         if (naive || in_bbox(r.r5, ix, iy)) {
           PairEval p;

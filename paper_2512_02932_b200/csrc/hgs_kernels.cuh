@@ -66,6 +66,12 @@ struct CompositeArgs {
   uint32_t *pix_mask;
 };
 
+// L2 prefetch of one splat record (96 B: at most two 128-B lines).
+__device__ __forceinline__ void prefetch_rec(const SplatRec *r) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(r));
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const char *>(r) + 95));
+}
+
 __device__ __forceinline__ size_t mask_word(uint32_t lo, int tile, uint32_t chunk, uint32_t pix_in_tile) {
   return ((size_t)(lo >> 5) + (size_t)tile + chunk) * kBlock + pix_in_tile;
 }
