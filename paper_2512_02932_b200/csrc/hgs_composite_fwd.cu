@@ -63,7 +63,9 @@ __global__ void __launch_bounds__(kBlock, HGS_FWD_MINB) k_composite_fwd(Composit
   };
 
   for (uint32_t base = lo; base < hi; base += 32) {
-    if (__all_sync(0xffffffffu, done)) break;
+    // pixels still compositing (saturated / deferred ones drop out of the masks)
+    const uint32_t alive = __ballot_sync(0xffffffffu, !done);
+    if (!alive) break;
     // stage: rank + bbox of entry base + lane, pixel mask, record if relevant
     const uint32_t j = base + lane;
     uint32_t pm = 0u;
@@ -71,7 +73,7 @@ __global__ void __launch_bounds__(kBlock, HGS_FWD_MINB) k_composite_fwd(Composit
       const uint32_t rk = NAIVE ? j : __ldg(a.tile_vals + j);
       const SplatRec *g = a.recs + rk;
       const int4 q = __ldg(&g->r5);
-      pm = NAIVE ? 0xffffffffu : pixel_mask(q, wx0, wy0);
+      pm = (NAIVE ? 0xffffffffu : pixel_mask(q, wx0, wy0)) & alive;
       if (pm) {
         SplatRec r;
         r.r0 = __ldg(&g->r0); r.r1 = __ldg(&g->r1); r.r2 = __ldg(&g->r2);
