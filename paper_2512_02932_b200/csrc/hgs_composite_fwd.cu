@@ -73,15 +73,15 @@ __global__ void __launch_bounds__(kBlock, HGS_FWD_MINB) k_composite_fwd(Composit
       const uint32_t rk = NAIVE ? j : __ldg(a.tile_vals + j);
       const SplatRec *g = a.recs + rk;
       const int4 q = __ldg(&g->r5);
-      pm = (NAIVE ? 0xffffffffu : pixel_mask(q, wx0, wy0)) & alive;
+      pm = NAIVE ? 0xffffffffu : pixel_mask(q, wx0, wy0);  // a rectangle: the culls rely on it
       if (pm) {
         SplatRec r;
         r.r0 = __ldg(&g->r0); r.r1 = __ldg(&g->r1); r.r2 = __ldg(&g->r2);
         r.r3 = __ldg(&g->r3); r.r4 = __ldg(&g->r4); r.r5 = q;
         if (!NAIVE && cull_splat(r, pm, wx0, wy0))
           pm = 0u;  // bbox hit, but the 1/255 support misses every covered pixel
-        else
-          wrec[lane] = r;
+        pm &= alive;  // only pixels still compositing
+        if (pm) wrec[lane] = r;
       }
     }
     uint32_t rel = __ballot_sync(0xffffffffu, pm != 0u);

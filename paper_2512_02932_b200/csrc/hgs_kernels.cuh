@@ -209,8 +209,11 @@ __device__ __forceinline__ bool cull_2d(const SplatRec &r, uint32_t pm, int wx0,
   return qmin > 1.05f;
 }
 
+#ifndef HGS_CULL_2D
+#define HGS_CULL_2D 1
+#endif
 __device__ __forceinline__ bool cull_splat(const SplatRec &r, uint32_t pm, int wx0, int wy0) {
-  return rec_is3d(r) ? cull_3d(r, pm, wx0, wy0) : cull_2d(r, pm, wx0, wy0);
+  return rec_is3d(r) ? cull_3d(r, pm, wx0, wy0) : (HGS_CULL_2D && cull_2d(r, pm, wx0, wy0));
 }
 
 // bbox overlaps the pixel rectangle [rx0, rx1] x [ry0, ry1]
