@@ -53,3 +53,21 @@ def test_long_tile_lists():
     out = _check(scene, cam, RenderSettings())
     lists = np.diff(out.frame.export()["tile_offsets"])
     assert lists.max() > 2000  # > 60 chunks in the longest list
+
+
+@pytest.mark.parametrize("case", range(8))
+def test_randomised_scenes(case):
+    """Seeded sweep over density, opacity, splat size, SH degree, type mix
+    and image shape: images, tile lists and gradients against the oracle."""
+    from paper_2512_02932_b200.settings import RenderSettings
+    from paper_2512_02932_b200.synthetic import synthetic_scene
+    rng = np.random.default_rng(1000 + case)
+    w, h = int(rng.integers(8, 70)), int(rng.integers(8, 70))
+    n = int(rng.integers(50, 4000))
+    deg = int(rng.integers(0, 4))
+    lo_s = float(rng.uniform(0.3, 2.0))
+    scene, cam = synthetic_scene(n, w, h, deg, seed=case, frac_3d=float(rng.uniform(0, 1)),
+                                 sigma_px=(lo_s, lo_s * float(rng.uniform(1.5, 10.0))))
+    scene.opacity_logit[:] = (scene.opacity_logit + np.float32(rng.uniform(-2, 3))).astype(np.float32)
+    bg = tuple(float(x) for x in rng.uniform(0, 1, 3))
+    _check(scene, cam, RenderSettings(background=bg))
