@@ -28,6 +28,10 @@ constexpr int kRadix = 1 << kRadixBits;
 constexpr uint32_t kFlagAgg = 1u << 30;
 constexpr uint32_t kFlagPrefix = 2u << 30;
 constexpr uint32_t kValueMask = (1u << 30) - 1;
+#ifndef HGS_LOOKBACK
+#define HGS_LOOKBACK 8
+#endif
+constexpr int kLB = HGS_LOOKBACK;  // predecessors read per look-back round trip
 
 template <typename K>
 __device__ __forceinline__ uint32_t digit_of(K key, int shift) {
@@ -141,14 +145,23 @@ __global__ void __launch_bounds__(kSortThreads) k_onesweep(const K *__restrict__
       s_gbase[d] = digit_offsets[d];
     } else {
       __stcg(lb, kFlagAgg | count);
+      // look back kLB predecessors per round trip (independent loads), so a
+      // tile that must sum many aggregates waits ~kLB x fewer L2 latencies
       uint32_t excl = 0;
       int64_t p = (int64_t)tile - 1;
-      while (true) {
-        uint32_t v = ld_volatile_u32(lookback + p * kRadix + d);
-        if ((v & ~kValueMask) == 0) continue;  // not yet published: spin
-        excl += v & kValueMask;
-        if (v & kFlagPrefix) break;
-        --p;
+      bool found = false;
+      while (!found) {
+        uint32_t v[kLB];
+#pragma unroll
+        for (int i = 0; i < kLB; ++i) v[i] = p - i >= 0 ? ld_volatile_u32(lookback + (p - i) * kRadix + d) : kFlagPrefix;
+#pragma unroll
+        for (int i = 0; i < kLB; ++i) {
+          if (found) break;
+          if ((v[i] & ~kValueMask) == 0) break;  // not yet published: re-poll from here
+          excl += v[i] & kValueMask;
+          --p;
+          if (v[i] & kFlagPrefix) found = true;
+        }
       }
       __stcg(lb, kFlagPrefix | (excl + count));
       s_gbase[d] = digit_offsets[d] + excl;
@@ -237,12 +250,19 @@ __device__ __forceinline__ unsigned long long scan_lookback(unsigned long long *
   __stcg(lb + tile, kScanAgg | agg);
   unsigned long long excl = 0;
   int64_t p = (int64_t)tile - 1;
-  while (true) {
-    unsigned long long v = ld_volatile_u64(lb + p);
-    if ((v & ~kScanMask) == 0) continue;
-    excl += v & kScanMask;
-    if (v & kScanPrefix) break;
-    --p;
+  bool found = false;
+  while (!found) {  // kLB predecessors per round trip
+    unsigned long long v[kLB];
+#pragma unroll
+    for (int i = 0; i < kLB; ++i) v[i] = p - i >= 0 ? ld_volatile_u64(lb + (p - i)) : kScanPrefix;
+#pragma unroll
+    for (int i = 0; i < kLB; ++i) {
+      if (found) break;
+      if ((v[i] & ~kScanMask) == 0) break;
+      excl += v[i] & kScanMask;
+      --p;
+      if (v[i] & kScanPrefix) found = true;
+    }
   }
   __stcg(lb + tile, kScanPrefix | (excl + agg));
   return excl;
