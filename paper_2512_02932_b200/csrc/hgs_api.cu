@@ -230,11 +230,18 @@ int hgs_forward(const hgs_scene *scene, const hgs_camera *camera, const hgs_sett
     HGS_LAUNCHED();
     k_radix_offsets<<<8, kRadix, 0, s>>>(at<uint32_t>(frame, L.hist_d), at<uint32_t>(frame, L.off_d));
     HGS_LAUNCHED();
-    uint32_t hist[8 * kRadix];
-    FrameState hst;
-    HGS_CUDA(cudaMemcpyAsync(hist, at<uint32_t>(frame, L.hist_d), sizeof(hist), cudaMemcpyDeviceToHost, s));
-    HGS_CUDA(cudaMemcpyAsync(&hst, st, sizeof(hst), cudaMemcpyDeviceToHost, s));
+    // one device-to-host copy: the state block and the digit histograms are
+    // adjacent in the frame (make_layout)
+    static_assert(sizeof(FrameState) <= 4096, "FrameState fits the staging block");
+    alignas(16) unsigned char head[4096 + 8 * kRadix * 4];
+    const size_t head_bytes = L.hist_d + 8 * kRadix * 4;
+    if (head_bytes > sizeof(head)) return HGS_ERR_CONFIG;
+    HGS_CUDA(cudaMemcpyAsync(head, frame, head_bytes, cudaMemcpyDeviceToHost, s));
     HGS_CUDA(cudaStreamSynchronize(s));
+    FrameState hst;
+    memcpy(&hst, head + L.state, sizeof(hst));
+    uint32_t hist[8 * kRadix];
+    memcpy(hist, head + L.hist_d, sizeof(hist));
     if (hst.status) return (int)hst.status;
     m = hst.m_count;
     // 2. depth sort over the digit passes that are not constant
