@@ -15,7 +15,7 @@ constexpr int kMaxGrid = 148 * 8;
 constexpr int kFixupBlocks = 148 * 4;  // persistent fixup grid (one warp per deferred pixel)
 
 struct Layout {
-  size_t state, hist_d, off_d, hist_p, off_p, keys_a, keys_b, vals_a, vals_b, lb_sort, lb_scan, recs, pair_off,
+  size_t state, hist_d, off_d, hist_p, off_p, keys_a, keys_b, vals_a, vals_b, lb_sort, lb_scan, recs, recs64, pair_off,
       pk_a, pk_b, pv_a, pv_b, tile_off, pix_T, pix_last, pix_count, fwd_fix, bwd_fix, pix_mask, total;
   size_t small_end;  // [state, small_end) is zeroed at the start of a forward
   size_t lb_sort_bytes, lb_scan_bytes;
@@ -48,6 +48,7 @@ Layout make_layout(int64_t n, int W, int H, int64_t cap) {
   L.vals_a = take(nn * 4);
   L.vals_b = take(nn * 4);
   L.recs = take(nn * sizeof(SplatRec));
+  L.recs64 = take(nn * sizeof(Rec64));
   L.pair_off = take(nn * 8);
   L.tile_off = take((n_tiles + 1) * 4);
   L.pix_T = take((size_t)W * H * 4);
@@ -218,7 +219,7 @@ int hgs_forward(const hgs_scene *scene, const hgs_camera *camera, const hgs_sett
 
   HGS_CUDA(record_event(settings, 0, s));
   HGS_CUDA(cudaMemsetAsync(frame, 0, L.small_end, s));
-  k_init_state<<<1, 1, 0, s>>>(sc, cam, mod, st);
+  k_init_state<<<1, 1, 0, s>>>(sc, cam, mod, at<SplatRec>(frame, L.recs), at<Rec64>(frame, L.recs64), st);
   HGS_LAUNCHED();
   // 1. depth keys + digit histograms
   uint32_t *vals_sorted = at<uint32_t>(frame, L.vals_a);
@@ -273,7 +274,8 @@ int hgs_forward(const hgs_scene *scene, const hgs_camera *camera, const hgs_sett
     HGS_CUDA(cudaMemsetAsync(rank_of, 0xff, (size_t)n * 4, s));
     k_rank_scatter<<<grid_for(m, 256), 256, 0, s>>>(vals_sorted, m, rank_of);
     HGS_LAUNCHED();
-    HGS_CUDA(launch_preprocess(sc, cam, mod, rank_of, at<SplatRec>(frame, L.recs), counts, s));
+    HGS_CUDA(launch_preprocess(sc, cam, mod, rank_of, at<SplatRec>(frame, L.recs), at<Rec64>(frame, L.recs64),
+                               counts, s));
     HGS_LAUNCHED();
     k_scan_counts<<<(unsigned)ceil_div(m, kScanTile), kScanThreads, 0, s>>>(
         counts, m, at<unsigned long long>(frame, L.pair_off), at<unsigned long long>(frame, L.lb_scan), st);
@@ -498,7 +500,11 @@ int hgs_backward(const hgs_scene *scene, const hgs_camera *camera, const hgs_set
   const SceneView sc = make_scene(*scene);
   const CamD cam = make_cam(*camera);
   const ModD mod{settings->theta_z, settings->t_z, settings->lambda_z};
-  k_init_state<<<1, 1, 0, s>>>(sc, cam, mod, b.c.st);
+  {
+    const Layout FL = make_layout(info->n, info->width, info->height, info->pair_capacity);
+    k_init_state<<<1, 1, 0, s>>>(sc, cam, mod, at<SplatRec>(const_cast<void *>(frame), FL.recs),
+                                 at<Rec64>(const_cast<void *>(frame), FL.recs64), b.c.st);
+  }
   HGS_LAUNCHED();
   const ChainArgs c0{sc, cam, mod, acc, ext ? acc_ext : nullptr, 0, nullptr};
   for (int k0 = 0; k0 < kg; k0 += 4) {

@@ -6,10 +6,35 @@
 
 namespace hgs {
 
-__global__ void k_init_state(SceneView sc, CamD cam, ModD mod, FrameState *st) {
+__global__ void k_init_state(SceneView sc, CamD cam, ModD mod, const SplatRec *recs, const Rec64 *recs64,
+                             FrameState *st) {
   st->sc = sc;
   st->cam = cam;
   st->mod = mod;
+  st->recs = recs;
+  st->recs64 = recs64;
+}
+
+// The float64 projection a pair re-check needs (Rec64).
+__device__ __forceinline__ void write_rec64(const ProjD &o, Rec64 *q) {
+  Rec64 r;
+  r.ctr[0] = o.ctr[0];
+  r.ctr[1] = o.ctr[1];
+  r.alpha_eff = o.alpha_eff;
+  if (o.typ == 1) {
+    r.g[0] = o.conic[0]; r.g[1] = o.conic[1]; r.g[2] = o.conic[2];
+    for (int k = 3; k < 9; ++k) r.g[k] = 0.0;
+  } else {
+    const double *m = o.mrow;
+    r.g[0] = m[0]; r.g[1] = m[1]; r.g[2] = m[3];
+    r.g[3] = m[4]; r.g[4] = m[5]; r.g[5] = m[7];
+    r.g[6] = m[8]; r.g[7] = m[9]; r.g[8] = m[11];
+  }
+  // six 16-byte streaming stores (the records are read only by rare re-checks)
+  const double2 *src = reinterpret_cast<const double2 *>(&r);
+  double2 *dst = reinterpret_cast<double2 *>(q);
+#pragma unroll
+  for (int k = 0; k < 6; ++k) __stcs(dst + k, src[k]);
 }
 
 // ------------------------------------------------------------ depth keys
@@ -116,7 +141,8 @@ __global__ void k_rank_scatter(const uint32_t *__restrict__ sorted_idx, int64_t 
 template <int B>
 __global__ void __launch_bounds__(32) k_preprocess(SceneView sc, CamD cam, ModD mod,
                                                    const uint32_t *__restrict__ rank_of,
-                                                   SplatRec *__restrict__ recs, uint32_t *__restrict__ counts) {
+                                                   SplatRec *__restrict__ recs, Rec64 *__restrict__ recs64,
+                                                   uint32_t *__restrict__ counts) {
   constexpr int SB = 3 * B, SS = 3 * B + 1;
   __shared__ float s_sh[32 * SS];
   const int lane = threadIdx.x;
@@ -136,19 +162,20 @@ __global__ void __launch_bounds__(32) k_preprocess(SceneView sc, CamD cam, ModD 
     project_d<false>(sc, i, cam, mod, o, s_sh + lane * SS);
     bbox_d(o, cam.width, cam.height);
     write_record(o, (uint32_t)i, recs + r);
+    write_rec64(o, recs64 + r);
     counts[r] = tile_count_of(o.bbox);
   }
 }
 // Host launcher (the template is launched from this translation unit).
 cudaError_t launch_preprocess(const SceneView &sc, const CamD &cam, const ModD &mod, const uint32_t *rank_of,
-                              SplatRec *recs, uint32_t *counts, cudaStream_t s) {
+                              SplatRec *recs, Rec64 *recs64, uint32_t *counts, cudaStream_t s) {
   const int64_t nb = (sc.n + 31) / 32;
   const int g = (int)(nb < 1 ? 1 : (nb > 148 * 48 ? 148 * 48 : nb));  // one warp per CTA
   switch (sc.sh_bases) {
-    case 1: k_preprocess<1><<<g, 32, 0, s>>>(sc, cam, mod, rank_of, recs, counts); break;
-    case 4: k_preprocess<4><<<g, 32, 0, s>>>(sc, cam, mod, rank_of, recs, counts); break;
-    case 9: k_preprocess<9><<<g, 32, 0, s>>>(sc, cam, mod, rank_of, recs, counts); break;
-    default: k_preprocess<16><<<g, 32, 0, s>>>(sc, cam, mod, rank_of, recs, counts); break;
+    case 1: k_preprocess<1><<<g, 32, 0, s>>>(sc, cam, mod, rank_of, recs, recs64, counts); break;
+    case 4: k_preprocess<4><<<g, 32, 0, s>>>(sc, cam, mod, rank_of, recs, recs64, counts); break;
+    case 9: k_preprocess<9><<<g, 32, 0, s>>>(sc, cam, mod, rank_of, recs, recs64, counts); break;
+    default: k_preprocess<16><<<g, 32, 0, s>>>(sc, cam, mod, rank_of, recs, recs64, counts); break;
   }
   return cudaGetLastError();
 }

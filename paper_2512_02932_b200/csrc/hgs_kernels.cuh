@@ -10,6 +10,16 @@ namespace hgs {
 // Device-side state at the head of the frame buffer.  The scene / camera
 // copies serve the rare float64 re-evaluation paths, which read them through
 // a global pointer instead of (large) kernel parameters.
+// The float64 projection of one splat at its depth rank, as the reference
+// computes it (project.py:169-258): all a float64 pair re-check needs, so the
+// re-checks never re-project the Gaussian from the scene.
+struct Rec64 {
+  double ctr[2];
+  double alpha_eff;
+  double g[9];  // 3D: conic (3); 2D: rows (0, 1, 3) x columns (0, 1, 3) of M
+};
+static_assert(sizeof(Rec64) == 96, "Rec64 is 96 B");
+
 struct FrameState {
   uint32_t status;
   uint32_t m_count;
@@ -20,6 +30,8 @@ struct FrameState {
   SceneView sc;
   CamD cam;
   ModD mod;
+  const SplatRec *recs;  // float32 records (rank order) ...
+  const Rec64 *recs64;   // ... and their float64 counterparts
 };
 
 // Deferred-exactness worklists.  The hot compositors contain no calls: a lane
@@ -235,21 +247,21 @@ struct PairEval {
 };
 
 // float64 re-evaluation of one pair exactly as the reference does it
-// (_blend_py.py:17-44, 96-100).  Returns false if the pair is skipped.
-static __device__ __noinline__ bool pair_f64(const SceneView &sc, const CamD &cam, const ModD &mod, uint32_t idx,
-                                             int ix, int iy, double *at_out, bool *ray_out, bool *clamped_out) {
-  ProjD o;
-  project_d<false, true>(sc, idx, cam, mod, o);  // geometry + alpha only
+// (_blend_py.py:17-44, 96-100), from the splat's stored float64 projection.
+// Returns false if the pair is skipped.
+static __device__ __noinline__ bool pair_f64(const Rec64 *q, bool is3d, int ix, int iy, double *at_out,
+                                             bool *ray_out, bool *clamped_out) {
+  const Rec64 o = *q;
   const double px = ix + 0.5, py = iy + 0.5;
   const double dx = px - o.ctr[0], dy = py - o.ctr[1];
   double d;
   bool ray = false;
-  if (o.typ == 1) {
-    d = (o.conic[0] * dx * dx + 2.0 * o.conic[1] * dx * dy) + o.conic[2] * dy * dy;
+  if (is3d) {
+    d = (o.g[0] * dx * dx + 2.0 * o.g[1] * dx * dy) + o.g[2] * dy * dy;
   } else {
-    const double *m = o.mrow;
-    double hu0 = px * m[8] - m[0], hu1 = px * m[9] - m[1], hu3 = px * m[11] - m[3];
-    double hv0 = py * m[8] - m[4], hv1 = py * m[9] - m[5], hv3 = py * m[11] - m[7];
+    const double *m = o.g;  // (m00 m01 m03 | m10 m11 m13 | m30 m31 m33)
+    double hu0 = px * m[6] - m[0], hu1 = px * m[7] - m[1], hu3 = px * m[8] - m[2];
+    double hv0 = py * m[6] - m[3], hv1 = py * m[7] - m[4], hv3 = py * m[8] - m[5];
     double den = hu0 * hv1 - hu1 * hv0;
     if (fabs(den) < kDegenerateDen) return false;
     double u = (hu1 * hv3 - hu3 * hv1) / den, v = (hu3 * hv0 - hu0 * hv3) / den;
@@ -377,7 +389,7 @@ static __device__ __noinline__ Resolved resolve_pair(const SplatRec *rp, int ix,
   atomicAdd(&st->diag[0], 1ull);
   double at64;
   bool ray64, cl64;
-  if (!pair_f64(st->sc, st->cam, st->mod, rec_idx(r), ix, iy, &at64, &ray64, &cl64)) return out;
+  if (!pair_f64(st->recs64 + (rp - st->recs), rec_is3d(r), ix, iy, &at64, &ray64, &cl64)) return out;
   out.at = (float)at64;
   out.flags = 1u | (cl64 ? 2u : 0u) | (ray64 ? 4u : 0u);
   return out;
@@ -482,7 +494,7 @@ static __device__ __noinline__ bool replay_T_below(const SplatRec *recs, const u
       if ((naive || in_bbox(r.r5, ix, iy)) && eval_pair<false>(r, recs + rk, ix, iy, flags, st, p)) {
         double at64;
         bool ray64, cl64;
-        if (pair_f64(st->sc, st->cam, st->mod, rec_idx(r), ix, iy, &at64, &ray64, &cl64)) om = 1.0 - at64;
+        if (pair_f64(st->recs64 + rk, rec_is3d(r), ix, iy, &at64, &ray64, &cl64)) om = 1.0 - at64;
       }
     }
 #pragma unroll
@@ -532,12 +544,13 @@ struct ExchangeState {
 };
 
 // kernels (defined in hgs_forward.cu / hgs_backward.cu / hgs_exchange.cu)
-__global__ void k_init_state(SceneView sc, CamD cam, ModD mod, FrameState *st);
+__global__ void k_init_state(SceneView sc, CamD cam, ModD mod, const SplatRec *recs, const Rec64 *recs64,
+                             FrameState *st);
 __global__ void k_depth_keys(SceneView sc, CamD cam, unsigned long long *keys, uint32_t *vals, uint32_t *hist,
                              FrameState *st);
 __global__ void k_rank_scatter(const uint32_t *sorted_idx, int64_t m, uint32_t *rank_of);
 cudaError_t launch_preprocess(const SceneView &sc, const CamD &cam, const ModD &mod, const uint32_t *rank_of,
-                              SplatRec *recs, uint32_t *counts, cudaStream_t s);
+                              SplatRec *recs, Rec64 *recs64, uint32_t *counts, cudaStream_t s);
 __global__ void k_scan_counts(const uint32_t *counts, int64_t m, unsigned long long *pair_off,
                               unsigned long long *scan_lb, FrameState *st);
 __global__ void k_duplicate(const SplatRec *recs, const unsigned long long *pair_off, int64_t m, int tiles_x,
