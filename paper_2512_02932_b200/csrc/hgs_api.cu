@@ -446,7 +446,7 @@ static void launch_bwd(const BwdArgs &b, int64_t n_tiles, bool ext, cudaStream_t
   // hot replay, then the float64-exact fixup of the deferred pixels.  Pixels
   // per lane: 2 (4 warps per tile) shares the splat walk and the warp
   // reduction between two pixels; 1 (8 warps) for register-heavy KG
-  constexpr int ppl = KG == 1 ? 2 : HGS_BWD_PPL_KG;
+  constexpr int ppl = KG == 1 ? HGS_BWD_PPL1 : HGS_BWD_PPL_KG;
   if (ext) {
     k_composite_bwd<KG, true, ppl, DET><<<(unsigned)n_tiles, 256 / ppl, 0, s>>>(b);
     k_fixup_bwd<KG, true, DET><<<kFixupBlocks, 256, 0, s>>>(b);

@@ -196,7 +196,7 @@ __device__ __forceinline__ void pair_grads(const SplatRec &r, const PairEval &p,
 // half is covered).  DET: the flush writes one record per (splat, warp)
 // instead of atomics (HGS_FLAG_DETERMINISTIC, reduced by k_det_reduce).
 template <int KG, bool EXT, int PPL, bool DET>
-__global__ void __launch_bounds__(256 / PPL, PPL == 2 ? (KG == 1 ? HGS_BWD_MINB1 : 4) : 3) k_composite_bwd(BwdArgs b) {
+__global__ void __launch_bounds__(256 / PPL, PPL == 4 ? 10 : (PPL == 2 ? (KG == 1 ? HGS_BWD_MINB1 : 4) : 3)) k_composite_bwd(BwdArgs b) {
   const CompositeArgs &a = b.c;
   __shared__ SplatRec s_rec[8 / PPL][32];
   __shared__ __align__(16) float s_red[HGS_BWD_SMEM_REDUCE ? 8 / PPL : 1][HGS_BWD_SMEM_REDUCE ? kRedWarp : 4];
@@ -586,7 +586,7 @@ __global__ void k_det_reduce(const unsigned long long *__restrict__ keys, const 
 
 // Instantiations: KG 1..4, with / without extension gradients, atomic and
 // deterministic accumulation; the pixels-per-lane the launcher uses.
-#define HGS_PPL(KG) ((KG) == 1 ? 2 : HGS_BWD_PPL_KG)
+#define HGS_PPL(KG) ((KG) == 1 ? HGS_BWD_PPL1 : HGS_BWD_PPL_KG)
 #define HGS_INST_BWD(KG, EXT)                                                   \
   template __global__ void k_composite_bwd<KG, EXT, HGS_PPL(KG), false>(BwdArgs); \
   template __global__ void k_composite_bwd<KG, EXT, HGS_PPL(KG), true>(BwdArgs);  \

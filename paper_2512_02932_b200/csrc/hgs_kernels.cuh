@@ -103,7 +103,10 @@ enum : int { kSkip = 0, kContrib = 1, kAmbiguous = 2 };  // pair decision outcom
 #define HGS_FIXUP_MINB 3  // CTAs (of 256) per SM the float64 fixup kernels are register-budgeted for
 #endif
 #ifndef HGS_BWD_PPL_KG
-#define HGS_BWD_PPL_KG 2  // pixels per lane of the backward compositor for KG >= 2 (KG = 1 always 2)
+#define HGS_BWD_PPL_KG 2  // pixels per lane of the backward compositor for KG >= 2
+#endif
+#ifndef HGS_BWD_PPL1
+#define HGS_BWD_PPL1 2    // pixels per lane of the backward compositor for KG = 1
 #endif
 
 __device__ __forceinline__ bool rec_is3d(const SplatRec &r) { return __float_as_uint(r.r4.w) >> 31; }
