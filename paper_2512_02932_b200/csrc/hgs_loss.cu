@@ -27,11 +27,12 @@ namespace hgs {
 
 namespace {
 
-constexpr int kLTX = 32, kLTY = 8;       // output tile
+constexpr int kLTX = 32, kLTY = 32;      // output tile (tall: the 10-row halo is amortised over 32 rows)
 constexpr int kHalo = 5;                  // 11-tap window
 constexpr int kPW = kLTX + 2 * kHalo;     // 42
-constexpr int kPH = kLTY + 2 * kHalo;     // 18
-constexpr int kLThreads = kLTX * kLTY;    // 256
+constexpr int kPH = kLTY + 2 * kHalo;     // 42
+constexpr int kLThreads = 256;            // 32 x 8 threads, 4 output rows each
+constexpr int kRowsPer = kLTY / (kLThreads / kLTX);
 constexpr int kNSums = 4;                 // ssim, l1, ll^2, detail^2
 
 struct LossArgs {
@@ -76,9 +77,8 @@ __global__ void __launch_bounds__(kLThreads) k_loss_moments(LossArgs a) {
   __shared__ float h[5][kPH][kLTX];
   __shared__ double red[kLThreads / 32];
   const int x0 = blockIdx.x * kLTX, y0 = blockIdx.y * kLTY;
-  const int tx = threadIdx.x % kLTX, ty = threadIdx.x / kLTX;
-  const int ix = x0 + tx, iy = y0 + ty;
-  const bool inside = ix < a.W && iy < a.H;
+  const int tx = threadIdx.x % kLTX, ty0 = threadIdx.x / kLTX;
+  const int ix = x0 + tx;
   const int H = a.H, W = a.W, C = a.C;
   double s_ssim = 0.0, s_l1 = 0.0, s_ll = 0.0, s_det = 0.0;
   for (int c = 0; c < C; ++c) {
@@ -102,7 +102,9 @@ __global__ void __launch_bounds__(kLThreads) k_loss_moments(LossArgs a) {
       h[0][py][px] = mx; h[1][py][px] = my; h[2][py][px] = mxx; h[3][py][px] = myy; h[4][py][px] = mxy;
     }
     __syncthreads();
-    if (inside) {
+    for (int rr = 0; rr < kRowsPer; ++rr) {
+    const int ty = ty0 + rr * (kLThreads / kLTX), iy = y0 + ty;
+    if (ix < W && iy < H) {
       float m[5] = {0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
       for (int t = 0; t < 11; ++t) {
@@ -142,6 +144,7 @@ __global__ void __launch_bounds__(kLThreads) k_loss_moments(LossArgs a) {
         s_det += (double)(lh * lh) + (double)(hl * hl) + (double)(hh * hh);
       }
     }
+    }  // rows
   }
   const int blk = blockIdx.y * gridDim.x + blockIdx.x;
   const double t0 = block_sum(s_ssim, red), t1 = block_sum(s_l1, red);
@@ -156,21 +159,14 @@ __global__ void __launch_bounds__(kLThreads) k_loss_grads(LossArgs a) {
   __shared__ float pa[kPH][kPW], pb[kPH][kPW], pc[kPH][kPW];
   __shared__ float h[3][kPH][kLTX];
   const int x0 = blockIdx.x * kLTX, y0 = blockIdx.y * kLTY;
-  const int tx = threadIdx.x % kLTX, ty = threadIdx.x / kLTX;
-  const int ix = x0 + tx, iy = y0 + ty;
-  const bool inside = ix < a.W && iy < a.H;
+  const int tx = threadIdx.x % kLTX, ty0 = threadIdx.x / kLTX;
+  const int ix = x0 + tx;
   const int H = a.H, W = a.W, C = a.C;
   const size_t plane = (size_t)H * W * C;
   const float inv_size = (float)(1.0 / ((double)H * W * C));
   const int h2 = (H + 1) / 2, w2 = (W + 1) / 2;
   const float inv_bsize = (float)(1.0 / ((double)h2 * w2 * C));
   const float lam = (float)a.lam, lam_low = (float)a.lam_low, lam_high = (float)a.lam_high;
-  // 2x2 Haar block of this pixel; which padded positions fold onto it
-  const int bx0 = ix & ~1, by0 = iy & ~1;
-  const int ox = ix & 1, oy = iy & 1;
-  const int px1 = (bx0 + 1 < W) ? 1 : 0, py1 = (by0 + 1 < H) ? 1 : 0;
-  // row offsets a' (and column offsets b') whose padded pixel maps here
-  const int na = (oy == 0 && !py1) ? 2 : 1, nb = (ox == 0 && !px1) ? 2 : 1;
   for (int c = 0; c < C; ++c) {
     __syncthreads();
     load_patch(a.mA, H, W, C, c, x0, y0, pa);
@@ -190,7 +186,15 @@ __global__ void __launch_bounds__(kLThreads) k_loss_grads(LossArgs a) {
       h[0][py][px] = sa; h[1][py][px] = sb; h[2][py][px] = sc;
     }
     __syncthreads();
-    if (!inside) continue;
+    for (int rr = 0; rr < kRowsPer; ++rr) {
+    const int ty = ty0 + rr * (kLThreads / kLTX), iy = y0 + ty;
+    if (ix >= W || iy >= H) continue;
+    // 2x2 Haar block of this pixel; which padded positions fold onto it
+    const int bx0 = ix & ~1, by0 = iy & ~1;
+    const int ox = ix & 1, oy = iy & 1;
+    const int px1 = (bx0 + 1 < W) ? 1 : 0, py1 = (by0 + 1 < H) ? 1 : 0;
+    // row offsets a' (and column offsets b') whose padded pixel maps here
+    const int na = (oy == 0 && !py1) ? 2 : 1, nb = (ox == 0 && !px1) ? 2 : 1;
     float ba = 0.f, bb = 0.f, bc = 0.f;
 #pragma unroll
     for (int t = 0; t < 11; ++t) {
@@ -234,6 +238,7 @@ __global__ void __launch_bounds__(kLThreads) k_loss_grads(LossArgs a) {
       a.out[plane + o] = lam_low * g_low;
       a.out[2 * plane + o] = lam_high * g_high;
     }
+    }  // rows
   }
 }
 
