@@ -628,7 +628,7 @@ def main():
     # quote the committed ncu capture of the same kernel (profiles/)
     ncu_file = os.path.join(REPO, "profiles", "ncu_r01b_kernels.json")
     if dom in ("composite_fwd", "composite_bwd") and os.path.exists(ncu_file):
-        pref = "k_composite_fwd<0, 0>" if dom == "composite_fwd" else "k_composite_bwd<1, 0, 2>"
+        pref = "k_composite_fwd<0, 0>" if dom == "composite_fwd" else "k_composite_bwd<1, 0, 2, 0>"
         for kd in json.load(open(ncu_file)):
             if kd.get("config") == "c2" and kd.get("kernel") == pref:
                 roof["limiter"] = ("SM instruction issue (ncu, profiles/ncu_r01b_kernels.json: issue "
