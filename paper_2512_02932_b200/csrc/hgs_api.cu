@@ -709,9 +709,15 @@ int hgs_frame_export_arrays(const hgs_scene *scene, const hgs_camera *camera, co
   }
   if (out->tile_ids && info->k > 0)
     HGS_CUDA(cudaMemcpyAsync(out->tile_ids, a.tile_vals, (size_t)info->k * 4, cudaMemcpyDeviceToDevice, s));
-  if (out->pixel_count)
-    HGS_CUDA(cudaMemcpyAsync(out->pixel_count, a.pix_count, (size_t)info->width * info->height * 4,
-                             cudaMemcpyDeviceToDevice, s));
+  if (out->pixel_count) {
+    if (info->flags & HGS_FLAG_NAIVE) {
+      HGS_CUDA(cudaMemcpyAsync(out->pixel_count, a.pix_count, (size_t)info->width * info->height * 4,
+                               cudaMemcpyDeviceToDevice, s));
+    } else {
+      k_pixel_counts<<<grid_for((int64_t)info->width * info->height, 256), 256, 0, s>>>(a, reinterpret_cast<uint32_t *>(out->pixel_count));
+      HGS_LAUNCHED();
+    }
+  }
   return HGS_OK;
 }
 

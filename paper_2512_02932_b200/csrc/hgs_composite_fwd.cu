@@ -115,7 +115,7 @@ __global__ void __launch_bounds__(kBlock, HGS_FWD_MINB) k_composite_fwd(Composit
       n0 = fmaf(w, c4.x, n0);
       n1 = fmaf(w, c4.y, n1);
       n2 = fmaf(w, c4.z, n2);
-      ++cnt;
+      if (NAIVE) ++cnt;  // tiled frames derive the blend-log counts from the masks
       cm |= 1u << e;
       last = base + e - lo + 1u;
       T = T * (1.f - at);
@@ -171,13 +171,33 @@ __global__ void __launch_bounds__(kBlock, HGS_FWD_MINB) k_composite_fwd(Composit
   }
   a.pix_T[pix] = T;
   a.pix_last[pix] = last;
-  a.pix_count[pix] = cnt;
+  if (NAIVE) a.pix_count[pix] = cnt;
 }
 
 template __global__ void k_composite_fwd<false, false>(CompositeArgs);
 template __global__ void k_composite_fwd<true, false>(CompositeArgs);
 template __global__ void k_composite_fwd<false, true>(CompositeArgs);
 template __global__ void k_composite_fwd<true, true>(CompositeArgs);
+
+// Blend-log entry count per pixel of a tiled frame: the popcount of its
+// contribution-mask words up to its last contributor.
+__global__ void k_pixel_counts(CompositeArgs a, uint32_t *counts) {
+  const int64_t HW = (int64_t)a.width * a.height;
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < HW; p += (int64_t)gridDim.x * blockDim.x) {
+    const int ix = (int)(p % a.width), iy = (int)(p / a.width);
+    const int tile = (iy / kTile) * a.tiles_x + ix / kTile;
+    const uint32_t lo = a.tile_off[tile], last = a.pix_last[p];
+    const uint32_t pit = (uint32_t)((iy & (kTile - 1)) * kTile + (ix & (kTile - 1)));
+    uint32_t c = 0;
+    for (uint32_t ch = 0; (ch << 5) < last; ++ch) {
+      uint32_t w = a.pix_mask[mask_word(lo, tile, ch, pit)];
+      const uint32_t rem = last - (ch << 5);
+      if (rem < 32u) w &= (1u << rem) - 1u;
+      c += __popc(w);
+    }
+    counts[p] = c;
+  }
+}
 
 __device__ __forceinline__ float warp_sum(float x) {
 #pragma unroll
@@ -307,7 +327,7 @@ __global__ void __launch_bounds__(256, HGS_FIXUP_MINB) k_fixup_fwd(CompositeArgs
       }
       a.pix_T[pix] = T;
       a.pix_last[pix] = last;
-      a.pix_count[pix] = cnt;
+      if (naive) a.pix_count[pix] = cnt;
       atomicAdd(&a.st->diag[10], 1ull);
     }
   }

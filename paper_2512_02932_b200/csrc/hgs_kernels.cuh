@@ -562,6 +562,7 @@ __global__ void k_tile_ranges(const uint32_t *skeys, int64_t k, int64_t n_tiles,
 template <bool NAIVE, bool COUNT>
 __global__ void k_composite_fwd(CompositeArgs a);
 __global__ void k_fixup_fwd(CompositeArgs a);
+__global__ void k_pixel_counts(CompositeArgs a, uint32_t *counts);
 template <int KG, bool EXT, int PPL, bool DET>
 __global__ void k_composite_bwd(BwdArgs b);
 template <int KG, bool EXT, bool DET>
