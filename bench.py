@@ -650,9 +650,9 @@ def main():
             gbs = hbm_bytes[nm] / (t_ms * 1e-3) / 1e9
             stage_roofs[nm] = {"ms": t_ms, "GB/s": gbs, "hbm_frac": gbs / hbm_peak}
 
-    # init_state, depth_keys, radix_offsets, depth passes, rank_scatter, preprocess, scan, duplicate,
-    # radix_offsets, tile passes, tile_ranges, composite_fwd, fixup_fwd
-    launches_fwd = 1 + 1 + 1 + n_depth_passes + 1 + 1 + 1 + 1 + n_tile_passes + 1 + 1 + 1
+    # init_state, depth_keys, radix_offsets, <depth passes>, rank_scatter, preprocess, scan_counts,
+    # duplicate, radix_offsets, <tile passes>, tile_ranges, composite_fwd, fixup_fwd
+    launches_fwd = 11 + n_depth_passes + n_tile_passes
     # init_state + (composite_bwd + fixup_bwd + chain_rule) per chunk of <= 4 gradients
     launches_bwd = 1 + 3 * ((a.kg + 3) // 4)
     value = world * 1000.0 / step_ms
