@@ -4,6 +4,10 @@
 // raster/_blend_py.py:55-123 (paths relative to the reference package).
 #include "hgs_kernels.cuh"
 
+#ifndef HGS_PRE_MINB
+#define HGS_PRE_MINB 1  // one-warp CTAs per SM the float64 preprocess is register-budgeted for
+#endif
+
 namespace hgs {
 
 __global__ void k_init_state(SceneView sc, CamD cam, ModD mod, const SplatRec *recs, const Rec64 *recs64,
@@ -139,7 +143,7 @@ __global__ void k_rank_scatter(const uint32_t *__restrict__ sorted_idx, int64_t 
 // LSU-throttled); float64 projection; record + tile count written at the
 // Gaussian's depth rank.
 template <int B>
-__global__ void __launch_bounds__(32) k_preprocess(SceneView sc, CamD cam, ModD mod,
+__global__ void __launch_bounds__(32, HGS_PRE_MINB) k_preprocess(SceneView sc, CamD cam, ModD mod,
                                                    const uint32_t *__restrict__ rank_of,
                                                    SplatRec *__restrict__ recs, Rec64 *__restrict__ recs64,
                                                    uint32_t *__restrict__ counts) {
