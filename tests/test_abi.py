@@ -86,3 +86,36 @@ def test_errors_are_reference_classes():
         _lib.check(3, "x")
     with pytest.raises(errors.DegenerateScaleError):
         _lib.check(4, "x")
+
+
+def _build_c_example(tmp):
+    import shutil
+    import subprocess
+    cc = shutil.which("gcc")
+    cuda_inc = "/usr/local/cuda/include"
+    if cc is None or not os.path.isdir(cuda_inc):
+        pytest.skip("gcc / CUDA headers not available")
+    exe = os.path.join(str(tmp), "c_render")
+    subprocess.run([cc, "-O2", "-Wall", "-Werror", "-I", os.path.join(REPO, "include"), "-I", cuda_inc,
+                    os.path.join(REPO, "examples", "c_render.c"), "-L",
+                    os.path.join(REPO, "paper_2512_02932_b200"), "-lhgs", "-L", "/usr/local/cuda/lib64",
+                    "-lcudart", "-o", exe], check=True)
+    return exe
+
+
+def test_c_example_compiles_against_the_abi(tmp_path, L):
+    """The boundary is a plain C ABI: a C program includes hgs.h and links
+    libhgs.so without Python or torch (examples/c_render.c)."""
+    assert os.path.exists(_build_c_example(tmp_path))
+
+
+@pytest.mark.gpu
+def test_c_example_runs(tmp_path):
+    import subprocess
+    exe = _build_c_example(tmp_path)
+    env = dict(os.environ)
+    env["LD_LIBRARY_PATH"] = os.pathsep.join([os.path.join(REPO, "paper_2512_02932_b200"),
+                                              "/usr/local/cuda/lib64", env.get("LD_LIBRARY_PATH", "")])
+    out = subprocess.run([exe], env=env, capture_output=True, text=True, timeout=120)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert out.stdout.strip().endswith("ok")
