@@ -61,7 +61,7 @@ __device__ __forceinline__ float warp_transpose_reduce16(float (&v)[16], int lan
 }
 
 #ifndef HGS_BWD_SMEM_REDUCE
-#define HGS_BWD_SMEM_REDUCE 1
+#define HGS_BWD_SMEM_REDUCE 2
 #endif
 constexpr int kRedStride = 20;                   // floats per lane row (16-byte aligned rows)
 constexpr int kRedWarp = 32 * kRedStride + 16;   // upper half shifted 16 banks: conflict-free column reads
@@ -85,6 +85,26 @@ __device__ __forceinline__ float warp_smem_reduce16(const float (&v)[16], int la
   acc += __shfl_xor_sync(0xffffffffu, acc, 16);
   __syncwarp();  // the next reduction overwrites the rows
   return acc;
+}
+
+// The same reduction on 32-bit shared-window addresses computed once per
+// thread (row_sa: this lane's row, col_sa: the column it sums), with four
+// partial sums.  Explicit st/ld.shared keeps the compiler from re-forming a
+// generic shared pointer around every call.
+__device__ __forceinline__ float warp_smem_reduce16_sa(const float (&v)[16], uint32_t row_sa, uint32_t col_sa) {
+  asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(row_sa), "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]));
+  asm volatile("st.shared.v4.f32 [%0+16], {%1, %2, %3, %4};" ::"r"(row_sa), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7]));
+  asm volatile("st.shared.v4.f32 [%0+32], {%1, %2, %3, %4};" ::"r"(row_sa), "f"(v[8]), "f"(v[9]), "f"(v[10]), "f"(v[11]));
+  asm volatile("st.shared.v4.f32 [%0+48], {%1, %2, %3, %4};" ::"r"(row_sa), "f"(v[12]), "f"(v[13]), "f"(v[14]), "f"(v[15]));
+  __syncwarp();
+  float x[16];
+#pragma unroll
+  for (int t = 0; t < 16; ++t)
+    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(x[t]) : "r"(col_sa + (uint32_t)(t * kRedStride * 4)));
+  const float acc = ((x[0] + x[1]) + (x[2] + x[3])) + ((x[4] + x[5]) + (x[6] + x[7])) +
+                    (((x[8] + x[9]) + (x[10] + x[11])) + ((x[12] + x[13]) + (x[14] + x[15])));
+  __syncwarp();  // the next reduction overwrites the rows
+  return acc + __shfl_xor_sync(0xffffffffu, acc, 16);
 }
 
 __device__ __forceinline__ int transpose_slot(int lane) {
@@ -233,6 +253,9 @@ __global__ void __launch_bounds__(256 / PPL, PPL == 4 ? 10 : (PPL == 2 ? (KG == 
   for (int o = 16; o > 0; o >>= 1) warp_last = max(warp_last, __shfl_xor_sync(0xffffffffu, warp_last, o));
   const uint32_t warp_end = lo + warp_last;  // exclusive
   const int slot = HGS_BWD_SMEM_REDUCE ? (lane & 15) : transpose_slot(lane);
+  const uint32_t red_sa = (uint32_t)__cvta_generic_to_shared(&s_red[warp][0]);
+  const uint32_t row_sa = red_sa + (uint32_t)((lane * kRedStride + (lane >= 16 ? 16 : 0)) * 4);
+  const uint32_t col_sa = red_sa + (uint32_t)(((lane & 16) * kRedStride + (lane >= 16 ? 16 : 0) + (lane & 15)) * 4);
   const bool writer = HGS_BWD_SMEM_REDUCE ? lane < 16 : !(lane & 1);  // one lane per slot
   const bool count = a.flags & HGS_FLAG_COUNT;
   uint32_t n_ev = 0, n_c3 = 0, n_cr = 0, n_cl = 0;
@@ -369,7 +392,9 @@ __global__ void __launch_bounds__(256 / PPL, PPL == 4 ? 10 : (PPL == 2 ? (KG == 
       }
 #pragma unroll
       for (int k = 0; k < KG; ++k) {
-#if HGS_BWD_SMEM_REDUCE
+#if HGS_BWD_SMEM_REDUCE == 2
+        const float tot = warp_smem_reduce16_sa(v[k], row_sa, col_sa);
+#elif HGS_BWD_SMEM_REDUCE
         const float tot = warp_smem_reduce16(v[k], lane, s_red[warp]);
 #else
         const float tot = warp_transpose_reduce16(v[k], lane);
