@@ -60,6 +60,9 @@ __device__ __forceinline__ float warp_transpose_reduce16(float (&v)[16], int lan
   return v[0] + __shfl_xor_sync(0xffffffffu, v[0], 1);
 }
 
+#ifndef HGS_BWD_KNOWN
+#define HGS_BWD_KNOWN 1  // backward evaluation skips the cutoff decisions the masks already fixed
+#endif
 #ifndef HGS_BWD_SMEM_REDUCE
 #define HGS_BWD_SMEM_REDUCE 2
 #endif
@@ -344,7 +347,13 @@ __global__ void __launch_bounds__(256 / PPL, PPL == 4 ? 10 : (PPL == 2 ? (KG == 
                                : (!dead[q] && ((m >> e) & 1u));
         PairEval p;
         if (count && act) ++n_ev;
+#if HGS_BWD_KNOWN
+        const int c = !act ? kSkip
+                           : (naive ? eval_fast<true>(r, ix, iy[q], a.flags, p)
+                                    : eval_fast<true, true>(r, ix, iy[q], a.flags, p));
+#else
         const int c = act ? eval_fast<true>(r, ix, iy[q], a.flags, p) : kSkip;
+#endif
         if (c == kAmbiguous) {
           BwdFix f;
           f.pix = pix[q]; f.entry = jj; f.T_run = T_run[q];

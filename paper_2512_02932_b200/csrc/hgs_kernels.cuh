@@ -348,7 +348,7 @@ struct Resolved {
 // Precise first-order float32 error bound of a 2D pair that the coarse band
 // flagged (pure FP32 arithmetic, no calls: safe on the hot path).  Returns
 // kSkip / kContrib when the bound separates every decision, kAmbiguous if not.
-__device__ __forceinline__ int refine_2d(const SplatRec &r, const Geom &g, bool bwd) {
+__device__ __forceinline__ int refine_2d(const SplatRec &r, const Geom &g, bool bwd, bool known = false) {
   const float4 m1 = r.r1, m2 = r.r2;
   const float m23 = r.r3.x;
   const float A0 = fabsf(g.pxl * m2.z) + fabsf(m1.x), A1 = fabsf(g.pxl * m2.w) + fabsf(m1.y);
@@ -364,8 +364,10 @@ __device__ __forceinline__ int refine_2d(const SplatRec &r, const Geom &g, bool 
   const float e_scr = 8.f * kEps * g.dscr + 1e-6f * (fabsf(g.dx) + fabsf(g.dy));
   const float margin = fmaf(g.ray ? e_ray : e_scr, kHalfLog2e, 1e-5f);
   if (!(ad > (float)kDegenerateDen + dden) || !(margin < kCoarse2D)) return kAmbiguous;
-  if (g.arg < kArgMinAlpha - margin) return kSkip;
-  if (g.arg <= kArgMinAlpha + margin) return kAmbiguous;
+  if (!known) {  // known: the forward's exact decision says the pair contributes
+    if (g.arg < kArgMinAlpha - margin) return kSkip;
+    if (g.arg <= kArgMinAlpha + margin) return kAmbiguous;
+  }
   if (bwd && (fabsf(g.arg - kArgClamp) <= margin || fabsf(g.dray - g.dscr) <= e_ray + e_scr)) return kAmbiguous;
   return kContrib;
 }
@@ -403,7 +405,10 @@ static __device__ __noinline__ Resolved resolve_pair(const SplatRec *rp, int ix,
 // the backward-only decisions (ray branch, clamp) and the 2D solve
 // quantities.  Returns kSkip, kContrib, or kAmbiguous -- the caller then runs
 // resolve_pair (out of line) and applies finish_resolved.
-template <bool BWD>
+// KNOWN (backward with contribution masks): the forward already decided,
+// exactly, that the pair contributes -- only the backward-only decisions
+// (clamp, ray branch, degenerate solve) are checked.
+template <bool BWD, bool KNOWN = false>
 __device__ __forceinline__ int eval_fast(const SplatRec &r, int ix, int iy, uint32_t flags, PairEval &p) {
   Geom g;
   geom_common(r, ix, iy, g);
@@ -420,8 +425,9 @@ __device__ __forceinline__ int eval_fast(const SplatRec &r, int ix, int iy, uint
     p.v = g.dy;
     // |d error| <= 16 eps S, S = a dx^2 + c dy^2 + 2|b dx dy| (>= every term)
     const float margin = exact ? fmaf(g.S, 16.f * kEps * kHalfLog2e, 1e-5f) : 0.f;
-    if (g.arg < kArgMinAlpha - margin) return kSkip;  // cheap cull: no ex2
-    if (exact && (g.arg <= kArgMinAlpha + margin || (BWD && fabsf(g.arg - kArgClamp) <= margin))) amb = true;
+    if (!KNOWN && g.arg < kArgMinAlpha - margin) return kSkip;  // cheap cull: no ex2
+    if (exact && ((!KNOWN && g.arg <= kArgMinAlpha + margin) || (BWD && fabsf(g.arg - kArgClamp) <= margin)))
+      amb = true;
   } else {
     geom_2d_rows(r, g);
     if (near_degenerate(g)) {  // (near-)degenerate ray/plane intersection (_blend_py.py:36-37)
@@ -433,12 +439,12 @@ __device__ __forceinline__ int eval_fast(const SplatRec &r, int ix, int iy, uint
     }
     if (!amb) {
       geom_2d_solve(r, g);
-      if (g.arg < kArgMinAlpha - (exact ? kCoarse2D : 0.f)) return kSkip;
-      if (exact && (g.arg <= kArgMinAlpha + kCoarse2D ||
+      if (!KNOWN && g.arg < kArgMinAlpha - (exact ? kCoarse2D : 0.f)) return kSkip;
+      if (exact && ((!KNOWN && g.arg <= kArgMinAlpha + kCoarse2D) ||
                     (BWD && (fabsf(g.arg - kArgClamp) <= kCoarse2D ||
                              fabsf(g.dray - g.dscr) <= 0.02f * (g.dray + g.dscr))))) {
         // coarse band hit: the precise bound usually separates the decision
-        const int c = refine_2d(r, g, BWD);
+        const int c = refine_2d(r, g, BWD, KNOWN);
         if (c == kSkip) return kSkip;
         amb = c == kAmbiguous;
       }
