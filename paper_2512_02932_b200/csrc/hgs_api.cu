@@ -447,6 +447,16 @@ static void launch_bwd(const BwdArgs &b, int64_t n_tiles, bool ext, cudaStream_t
   // per lane: 2 (4 warps per tile) shares the splat walk and the warp
   // reduction between two pixels; 1 (8 warps) for register-heavy KG
   constexpr int ppl = KG == 1 ? HGS_BWD_PPL1 : HGS_BWD_PPL_KG;
+  if (HGS_BWD_COMPACT && !(b.c.flags & HGS_FLAG_NAIVE)) {
+    if (ext) {
+      launch_composite_bwd_c<KG, true, DET>(b, n_tiles, s);
+      k_fixup_bwd<KG, true, DET><<<kFixupBlocks, 256, 0, s>>>(b);
+    } else {
+      launch_composite_bwd_c<KG, false, DET>(b, n_tiles, s);
+      k_fixup_bwd<KG, false, DET><<<kFixupBlocks, 256, 0, s>>>(b);
+    }
+    return;
+  }
   if (ext) {
     k_composite_bwd<KG, true, ppl, DET><<<(unsigned)n_tiles, 256 / ppl, 0, s>>>(b);
     k_fixup_bwd<KG, true, DET><<<kFixupBlocks, 256, 0, s>>>(b);

@@ -26,6 +26,12 @@ namespace hgs {
 constexpr int kAcc = 16;
 constexpr int kAccExt = 4;
 
+__device__ __forceinline__ float warp_sum_f(float x) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+  return x;
+}
+
 // Sum 16 per-lane values over the warp.  On return lane l holds the total of
 // slot ((l >> 4) & 1) * 8 + ((l >> 3) & 1) * 4 + ((l >> 2) & 1) * 2 + ((l >> 1) & 1)
 // (lanes l and l ^ 1 hold the same slot).  16 shuffles instead of 16 x 5.
@@ -458,6 +464,277 @@ __global__ void __launch_bounds__(256 / PPL, PPL == 4 ? 10 : (PPL == 2 ? (KG == 
   }
 }
 
+// ---------------------------------------------------------------------------
+// Compacted backward (contribution-mask mode).  Same 8 x 8 warp blocks and
+// back-to-front chunk walk as k_composite_bwd, but the per-pixel replay state
+// lives in the warp's shared memory instead of its owner lane's registers, so
+// for each splat the pixels it contributes to (a handful of the 64, known
+// exactly from the forward's masks) are packed onto consecutive lanes: one
+// evaluation pass at ~full lane occupancy instead of one pass per pixel row
+// half at ~40%.  The owner lanes only keep the mask words.
+//   a[p]  = T_run, S0, S1, S2        (read / written by the pixel's worker)
+//   e[p]  = SD, SN0, SN1, SN2        (EXT)
+//   g[k][p]  = dL/dC (3), dL/dalpha * T_fin   (read only)
+//   ge[k][p] = dL/dD, dL/dN (3)                (EXT, read only)
+constexpr int kCPix = 64;  // pixels per warp (8 x 8)
+
+template <int KG, bool EXT>
+struct CState {
+  float4 a[kCPix];
+  float4 e[EXT ? kCPix : 1];
+  float4 g[KG][kCPix];
+  float4 ge[EXT ? KG : 1][EXT ? kCPix : 1];
+  uint8_t list[kCPix];
+};
+
+template <int KG, bool EXT>
+constexpr size_t cstate_bytes() {
+  return ((sizeof(CState<KG, EXT>) + 15) / 16) * 16;
+}
+
+#ifndef HGS_BWDC_MINB1
+#define HGS_BWDC_MINB1 6  // CTAs per SM the compacted KG = 1 backward is budgeted for
+#endif
+
+template <int KG, bool EXT, bool DET>
+__global__ void __launch_bounds__(128, KG == 1 ? (EXT ? 5 : HGS_BWDC_MINB1) : 3) k_composite_bwd_c(BwdArgs b) {
+  const CompositeArgs &a = b.c;
+  __shared__ SplatRec s_rec[4][32];
+  __shared__ __align__(16) float s_red[4][kRedWarp];
+  extern __shared__ __align__(16) unsigned char s_dyn[];
+  const int tile = blockIdx.x;
+  const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  CState<KG, EXT> &cs = *reinterpret_cast<CState<KG, EXT> *>(s_dyn + warp * cstate_bytes<KG, EXT>());
+  const int wx0 = tx * kTile + (warp & 1) * 8, wy0 = ty * kTile + (warp >> 1) * 8;
+  const uint32_t lo = a.tile_off[tile];
+  const int64_t HW = (int64_t)a.width * a.height;
+  uint32_t last[2], mw[2];
+  bool live[2];
+  uint32_t warp_last = 0;
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const int p = lane + 32 * q;
+    const int ix = wx0 + (lane & 7), iy = wy0 + (lane >> 3) + 4 * q;
+    const bool inside = ix < a.width && iy < a.height;
+    const int64_t pix = (int64_t)iy * a.width + ix;
+    last[q] = inside ? a.pix_last[pix] : 0u;
+    live[q] = last[q] > 0u;
+    mw[q] = (uint32_t)((iy & (kTile - 1)) * kTile + (ix & (kTile - 1)));
+    const float T_fin = inside ? a.pix_T[pix] : 1.f;
+    cs.a[p] = make_float4(T_fin, a.bg[0] * T_fin, a.bg[1] * T_fin, a.bg[2] * T_fin);
+    if (EXT) cs.e[p] = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int k = 0; k < KG; ++k) {
+      float4 gv = make_float4(0.f, 0.f, 0.f, 0.f), gx = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (inside) {
+        const float *g = b.pix_grad + ((int64_t)k * HW + pix) * 3;
+        gv.x = g[0]; gv.y = g[1]; gv.z = g[2];
+        if (EXT) {
+          if (b.alpha_grad) gv.w = b.alpha_grad[(int64_t)k * HW + pix] * T_fin;
+          if (b.depth_grad) gx.x = b.depth_grad[(int64_t)k * HW + pix];
+          if (b.normal_grad) {
+            const float *h = b.normal_grad + ((int64_t)k * HW + pix) * 3;
+            gx.y = h[0]; gx.z = h[1]; gx.w = h[2];
+          }
+        }
+      }
+      cs.g[k][p] = gv;
+      if (EXT) cs.ge[k][p] = gx;
+    }
+    warp_last = max(warp_last, last[q]);
+  }
+  warp_last = __reduce_max_sync(0xffffffffu, warp_last);
+  __syncwarp();
+  const int slot = lane & 15;
+  const uint32_t red_sa = (uint32_t)__cvta_generic_to_shared(&s_red[warp][0]);
+  const uint32_t row_sa = red_sa + (uint32_t)((lane * kRedStride + (lane >= 16 ? 16 : 0)) * 4);
+  const uint32_t col_sa = red_sa + (uint32_t)(((lane & 16) * kRedStride + (lane >= 16 ? 16 : 0) + (lane & 15)) * 4);
+  const bool writer = lane < 16;
+  const bool count = a.flags & HGS_FLAG_COUNT;
+  uint32_t n_ev = 0, n_c3 = 0, n_cr = 0, n_cl = 0;
+  uint32_t lt;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(lt));
+  SplatRec *wrec = s_rec[warp];
+
+  for (uint32_t top = lo + warp_last, start; top > lo; top = start) {
+    start = lo + (((top - 1u - lo) >> 5) << 5);  // the forward's 32-entry chunks
+    const uint32_t ch = (start - lo) >> 5;
+    uint32_t pm[2];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      pm[q] = 0u;
+      if (live[q] && (ch << 5) < last[q]) {
+        uint32_t w = a.pix_mask[mask_word(lo, tile, ch, mw[q])];
+        const uint32_t rem = last[q] - (ch << 5);
+        if (rem < 32u) w &= (1u << rem) - 1u;
+        pm[q] = w;
+      }
+    }
+    uint32_t rel = __reduce_or_sync(0xffffffffu, pm[0] | pm[1]);
+    if ((rel >> lane) & 1u) {
+      const SplatRec *g = a.recs + __ldg(a.tile_vals + start + lane);
+      SplatRec r;
+      r.r0 = __ldg(&g->r0); r.r1 = __ldg(&g->r1); r.r2 = __ldg(&g->r2);
+      r.r3 = __ldg(&g->r3); r.r4 = __ldg(&g->r4); r.r5 = __ldg(&g->r5);
+      wrec[lane] = r;
+    }
+    __syncwarp();
+    while (rel) {
+      const int e = 31 - __clz(rel);
+      rel &= ~(1u << e);
+      const bool b0 = live[0] && ((pm[0] >> e) & 1u), b1 = live[1] && ((pm[1] >> e) & 1u);
+      const uint32_t B0 = __ballot_sync(0xffffffffu, b0), B1 = __ballot_sync(0xffffffffu, b1);
+      const int n0 = __popc(B0), n = n0 + __popc(B1);
+      if (n == 0) continue;  // every pixel of this splat was deferred
+      const int r0 = __popc(B0 & lt), r1 = n0 + __popc(B1 & lt);
+      if (b0) cs.list[r0] = (uint8_t)lane;
+      if (b1) cs.list[r1] = (uint8_t)(lane + 32);
+      __syncwarp();
+      const uint32_t jj = start + e;
+      const SplatRec &r = wrec[e];
+      float v[KG][16];
+      float ve[KG][4];
+#pragma unroll
+      for (int k = 0; k < KG; ++k) {
+#pragma unroll
+        for (int s2 = 0; s2 < 16; ++s2) v[k][s2] = 0.f;
+#pragma unroll
+        for (int s2 = 0; s2 < 4; ++s2) ve[k][s2] = 0.f;
+      }
+      uint32_t amb_lo = 0u, amb_hi = 0u;
+#pragma unroll 1
+      for (int i0 = 0; i0 < n; i0 += 32) {
+        const bool act = i0 + lane < n;
+        bool amb = false;
+        if (act) {
+          const int p = cs.list[i0 + lane];
+          const int ix = wx0 + (p & 7), iy = wy0 + (p >> 3);
+          const float4 A = cs.a[p];
+          PairEval pe;
+          if (count) ++n_ev;
+          const int c = eval_fast<true, true>(r, ix, iy, a.flags, pe);
+          if (c == kAmbiguous) {
+            const float4 E = EXT ? cs.e[p] : make_float4(0.f, 0.f, 0.f, 0.f);
+            BwdFix f;
+            f.pix = (uint32_t)iy * (uint32_t)a.width + (uint32_t)ix; f.entry = jj; f.T_run = A.x;
+            f.S0 = A.y; f.S1 = A.z; f.S2 = A.w; f.SD = E.x; f.SN0 = E.y; f.SN1 = E.z; f.SN2 = E.w;
+#pragma unroll
+            for (int i = 0; i < 6; ++i) f.pad[i] = 0;
+            b.c.bwd_fix[atomicAdd(&a.st->n_fix_bwd, 1u)] = f;
+            amb = true;
+          } else if (c == kContrib) {
+            if (count) {
+              if (rec_is3d(r)) ++n_c3; else if (pe.ray) ++n_cr; else ++n_cl;
+            }
+            const float inv_om = 1.f / (1.f - pe.at);
+            const float T_k = A.x * inv_om;  // transmittance before this splat
+            Suffix S{A.y, A.z, A.w, 0.f, 0.f, 0.f, 0.f};
+            if (EXT) {
+              const float4 E = cs.e[p];
+              S.sd = E.x; S.sn0 = E.y; S.sn1 = E.z; S.sn2 = E.w;
+            }
+            PixGrads<KG, EXT> G;
+#pragma unroll
+            for (int k = 0; k < KG; ++k) {
+              const float4 gv = cs.g[k][p];
+              G.gp[k][0] = gv.x; G.gp[k][1] = gv.y; G.gp[k][2] = gv.z;
+              G.ga[k] = gv.w;
+              if (EXT) {
+                const float4 gx = cs.ge[k][p];
+                G.gd[k] = gx.x; G.gn[k][0] = gx.y; G.gn[k][1] = gx.z; G.gn[k][2] = gx.w;
+              } else {
+                G.gd[k] = 0.f; G.gn[k][0] = G.gn[k][1] = G.gn[k][2] = 0.f;
+              }
+            }
+            pair_grads<KG, EXT>(r, pe, T_k, inv_om, 1.f, S, G, v, ve);
+            const float w = pe.at * T_k;
+            cs.a[p] = make_float4(T_k, fmaf(r.r3.y, w, S.s0), fmaf(r.r3.z, w, S.s1), fmaf(r.r3.w, w, S.s2));
+            if (EXT)
+              cs.e[p] = make_float4(fmaf(r.r0.z, w, S.sd), fmaf(r.r4.x, w, S.sn0), fmaf(r.r4.y, w, S.sn1),
+                                    fmaf(r.r4.z, w, S.sn2));
+          }
+        }
+        const uint32_t bal = __ballot_sync(0xffffffffu, amb);
+        if (i0 == 0) amb_lo = bal; else amb_hi = bal;
+      }
+      if (amb_lo | amb_hi) {  // deferred pixels drop out of the walk
+        if (b0 && (((r0 < 32 ? amb_lo >> r0 : amb_hi >> (r0 - 32))) & 1u)) live[0] = false;
+        if (b1 && (((r1 < 32 ? amb_lo >> r1 : amb_hi >> (r1 - 32))) & 1u)) live[1] = false;
+      }
+      __syncwarp();  // pixel state and the list are rewritten for the next splat
+      if (__popc(amb_lo) + __popc(amb_hi) == n) continue;  // nothing contributed
+      const bool is3d = rec_is3d(r);
+      const uint32_t gidx = rec_idx(r);
+      if (lane == 0) b.touched[gidx] = 1;
+      uint32_t rec = 0;
+      if (DET) {
+        if (lane == 0) {
+          rec = atomicAdd(b.rec_count, 1u);
+          if (rec < b.rec_cap) {
+            b.rec_keys[rec] = det_key(gidx, (uint32_t)tile, (uint32_t)warp);
+            b.rec_vals[rec] = rec;
+          }
+        }
+        rec = __shfl_sync(0xffffffffu, rec, 0);
+      }
+#pragma unroll
+      for (int k = 0; k < KG; ++k) {
+        const float tot = warp_smem_reduce16_sa(v[k], row_sa, col_sa);
+        const int nslots = is3d ? 9 : 15;
+        if (DET) {
+          if (writer && rec < b.rec_cap) b.rec_pay[(size_t)rec * (KG * 20) + k * 20 + slot] = tot;
+        } else if (writer && slot < nslots && tot != 0.f) {
+          atomicAdd(b.acc + ((int64_t)gidx * KG + k) * kAcc + slot, tot);
+        }
+        if (EXT) {
+#pragma unroll
+          for (int s2 = 0; s2 < 4; ++s2) ve[k][s2] = warp_sum_f(ve[k][s2]);
+          if (lane < 4) {
+            const float x = lane == 0 ? ve[k][0] : (lane == 1 ? ve[k][1] : (lane == 2 ? ve[k][2] : ve[k][3]));
+            if (DET) {
+              if (rec < b.rec_cap) b.rec_pay[(size_t)rec * (KG * 20) + k * 20 + 16 + lane] = x;
+            } else if (x != 0.f) {
+              atomicAdd(b.acc_ext + ((int64_t)gidx * KG + k) * kAccExt + lane, x);
+            }
+          }
+        } else if (DET && lane < 4 && rec < b.rec_cap) {
+          b.rec_pay[(size_t)rec * (KG * 20) + k * 20 + 16 + lane] = 0.f;
+        }
+      }
+    }
+    __syncwarp();  // the next chunk overwrites this warp's staging slots
+    if (!__any_sync(0xffffffffu, live[0] || live[1])) break;
+  }
+  if (count) {
+    n_ev = __reduce_add_sync(0xffffffffu, n_ev);
+    n_c3 = __reduce_add_sync(0xffffffffu, n_c3);
+    n_cr = __reduce_add_sync(0xffffffffu, n_cr);
+    n_cl = __reduce_add_sync(0xffffffffu, n_cl);
+    if (lane == 0) {
+      atomicAdd(&a.st->diag[6], (unsigned long long)n_c3);
+      atomicAdd(&a.st->diag[7], (unsigned long long)n_cr);
+      atomicAdd(&a.st->diag[8], (unsigned long long)n_cl);
+      atomicAdd(&a.st->diag[9], (unsigned long long)n_ev);
+    }
+  }
+}
+
+// Host launcher (the kernel template is instantiated in this translation unit).
+template <int KG, bool EXT, bool DET>
+cudaError_t launch_composite_bwd_c(const BwdArgs &b, int64_t n_tiles, cudaStream_t s) {
+  const size_t dyn = 4 * cstate_bytes<KG, EXT>();
+  static bool attr_set = false;
+  if (!attr_set) {
+    const cudaError_t err =
+        cudaFuncSetAttribute(k_composite_bwd_c<KG, EXT, DET>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+    if (err != cudaSuccess) return err;
+    attr_set = true;
+  }
+  k_composite_bwd_c<KG, EXT, DET><<<(unsigned)n_tiles, 128, dyn, s>>>(b);
+  return cudaGetLastError();
+}
+
 __device__ __forceinline__ float warp_sum_bwd(float x) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
@@ -625,7 +902,9 @@ __global__ void k_det_reduce(const unsigned long long *__restrict__ keys, const 
   template __global__ void k_composite_bwd<KG, EXT, HGS_PPL(KG), false>(BwdArgs); \
   template __global__ void k_composite_bwd<KG, EXT, HGS_PPL(KG), true>(BwdArgs);  \
   template __global__ void k_fixup_bwd<KG, EXT, false>(BwdArgs);                  \
-  template __global__ void k_fixup_bwd<KG, EXT, true>(BwdArgs);
+  template __global__ void k_fixup_bwd<KG, EXT, true>(BwdArgs);                  \
+  template cudaError_t launch_composite_bwd_c<KG, EXT, false>(const BwdArgs &, int64_t, cudaStream_t); \
+  template cudaError_t launch_composite_bwd_c<KG, EXT, true>(const BwdArgs &, int64_t, cudaStream_t);
 HGS_INST_BWD(1, false)
 HGS_INST_BWD(2, false)
 HGS_INST_BWD(3, false)

@@ -105,6 +105,9 @@ enum : int { kSkip = 0, kContrib = 1, kAmbiguous = 2 };  // pair decision outcom
 #ifndef HGS_BWD_PPL_KG
 #define HGS_BWD_PPL_KG 2  // pixels per lane of the backward compositor for KG >= 2
 #endif
+#ifndef HGS_BWD_COMPACT
+#define HGS_BWD_COMPACT 1  // contribution-mask backward with lane-compacted pixel work
+#endif
 #ifndef HGS_BWD_PPL1
 #define HGS_BWD_PPL1 2    // pixels per lane of the backward compositor for KG = 1
 #endif
@@ -571,6 +574,8 @@ __global__ void k_fixup_fwd(CompositeArgs a);
 __global__ void k_pixel_counts(CompositeArgs a, uint32_t *counts);
 template <int KG, bool EXT, int PPL, bool DET>
 __global__ void k_composite_bwd(BwdArgs b);
+template <int KG, bool EXT, bool DET>
+cudaError_t launch_composite_bwd_c(const BwdArgs &b, int64_t n_tiles, cudaStream_t s);
 template <int KG, bool EXT, bool DET>
 __global__ void k_fixup_bwd(BwdArgs b);
 __global__ void k_det_reduce(const unsigned long long *keys, const uint32_t *vals, const float *pay, int64_t nrec,
