@@ -476,44 +476,54 @@ __global__ void __launch_bounds__(256 / PPL, PPL == 4 ? 10 : (PPL == 2 ? (KG == 
 //   e[p]  = SD, SN0, SN1, SN2        (EXT)
 //   g[k][p]  = dL/dC (3), dL/dalpha * T_fin   (read only)
 //   ge[k][p] = dL/dD, dL/dN (3)                (EXT, read only)
-constexpr int kCPix = 64;  // pixels per warp (8 x 8)
-
-template <int KG, bool EXT>
+template <int KG, bool EXT, int QP>
 struct CState {
-  float4 a[kCPix];
-  float4 e[EXT ? kCPix : 1];
-  float4 g[KG][kCPix];
-  float4 ge[EXT ? KG : 1][EXT ? kCPix : 1];
-  uint8_t list[kCPix];
+  float4 a[32 * QP];
+  float4 e[EXT ? 32 * QP : 1];
+  float4 g[KG][32 * QP];
+  float4 ge[EXT ? KG : 1][EXT ? 32 * QP : 1];
+  uint8_t list[32 * QP];
+  uint8_t dead[32 * QP];  // set by the worker that defers the pixel
 };
 
-template <int KG, bool EXT>
+template <int KG, bool EXT, int QP>
 constexpr size_t cstate_bytes() {
-  return ((sizeof(CState<KG, EXT>) + 15) / 16) * 16;
+  return ((sizeof(CState<KG, EXT, QP>) + 15) / 16) * 16;
 }
 
 #ifndef HGS_BWDC_MINB1
-#define HGS_BWDC_MINB1 6  // CTAs per SM the compacted KG = 1 backward is budgeted for
+#define HGS_BWDC_MINB1 5  // CTA budget of the compacted KG = 1 backward, in units of 4 warps
+#endif
+#ifndef HGS_BWDC_MINBK
+#define HGS_BWDC_MINBK 4  // the same for KG >= 2
+#endif
+#ifndef HGS_BWDC_QP
+#define HGS_BWDC_QP 4  // pixels per lane: warp blocks of 8 x (4 QP) pixels, 8 / QP warps per tile
 #endif
 
-template <int KG, bool EXT, bool DET>
-__global__ void __launch_bounds__(128, KG == 1 ? (EXT ? 5 : HGS_BWDC_MINB1) : 3) k_composite_bwd_c(BwdArgs b) {
+// warps per SM budget: (256 / QP) threads per CTA
+#define HGS_BWDC_MINB(KG, EXT, QP) \
+  (((KG) == 1 ? ((EXT) ? 4 : HGS_BWDC_MINB1) : ((EXT) ? 3 : HGS_BWDC_MINBK)) * (QP) / 2)
+
+template <int KG, bool EXT, bool DET, int QP>
+__global__ void __launch_bounds__(256 / QP, HGS_BWDC_MINB(KG, EXT, QP)) k_composite_bwd_c(BwdArgs b) {
+  constexpr int NW = 8 / QP;  // warps per tile
   const CompositeArgs &a = b.c;
-  __shared__ SplatRec s_rec[4][32];
-  __shared__ __align__(16) float s_red[4][kRedWarp];
+  __shared__ SplatRec s_rec[NW][32];
+  __shared__ __align__(16) float s_red[NW][kRedWarp];
   extern __shared__ __align__(16) unsigned char s_dyn[];
   const int tile = blockIdx.x;
   const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  CState<KG, EXT> &cs = *reinterpret_cast<CState<KG, EXT> *>(s_dyn + warp * cstate_bytes<KG, EXT>());
-  const int wx0 = tx * kTile + (warp & 1) * 8, wy0 = ty * kTile + (warp >> 1) * 8;
+  CState<KG, EXT, QP> &cs = *reinterpret_cast<CState<KG, EXT, QP> *>(s_dyn + warp * cstate_bytes<KG, EXT, QP>());
+  const int wx0 = tx * kTile + (warp & 1) * 8, wy0 = ty * kTile + (warp >> 1) * 4 * QP;
   const uint32_t lo = a.tile_off[tile];
   const int64_t HW = (int64_t)a.width * a.height;
-  uint32_t last[2], mw[2];
-  bool live[2];
+  uint32_t last[QP], mw[QP];
+  bool live[QP];
   uint32_t warp_last = 0;
 #pragma unroll
-  for (int q = 0; q < 2; ++q) {
+  for (int q = 0; q < QP; ++q) {
     const int p = lane + 32 * q;
     const int ix = wx0 + (lane & 7), iy = wy0 + (lane >> 3) + 4 * q;
     const bool inside = ix < a.width && iy < a.height;
@@ -523,6 +533,7 @@ __global__ void __launch_bounds__(128, KG == 1 ? (EXT ? 5 : HGS_BWDC_MINB1) : 3)
     mw[q] = (uint32_t)((iy & (kTile - 1)) * kTile + (ix & (kTile - 1)));
     const float T_fin = inside ? a.pix_T[pix] : 1.f;
     cs.a[p] = make_float4(T_fin, a.bg[0] * T_fin, a.bg[1] * T_fin, a.bg[2] * T_fin);
+    cs.dead[p] = 0;
     if (EXT) cs.e[p] = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
     for (int k = 0; k < KG; ++k) {
@@ -560,9 +571,9 @@ __global__ void __launch_bounds__(128, KG == 1 ? (EXT ? 5 : HGS_BWDC_MINB1) : 3)
   for (uint32_t top = lo + warp_last, start; top > lo; top = start) {
     start = lo + (((top - 1u - lo) >> 5) << 5);  // the forward's 32-entry chunks
     const uint32_t ch = (start - lo) >> 5;
-    uint32_t pm[2];
+    uint32_t pm[QP], any_pm = 0u;
 #pragma unroll
-    for (int q = 0; q < 2; ++q) {
+    for (int q = 0; q < QP; ++q) {
       pm[q] = 0u;
       if (live[q] && (ch << 5) < last[q]) {
         uint32_t w = a.pix_mask[mask_word(lo, tile, ch, mw[q])];
@@ -570,8 +581,9 @@ __global__ void __launch_bounds__(128, KG == 1 ? (EXT ? 5 : HGS_BWDC_MINB1) : 3)
         if (rem < 32u) w &= (1u << rem) - 1u;
         pm[q] = w;
       }
+      any_pm |= pm[q];
     }
-    uint32_t rel = __reduce_or_sync(0xffffffffu, pm[0] | pm[1]);
+    uint32_t rel = __reduce_or_sync(0xffffffffu, any_pm);
     if ((rel >> lane) & 1u) {
       const SplatRec *g = a.recs + __ldg(a.tile_vals + start + lane);
       SplatRec r;
@@ -583,13 +595,17 @@ __global__ void __launch_bounds__(128, KG == 1 ? (EXT ? 5 : HGS_BWDC_MINB1) : 3)
     while (rel) {
       const int e = 31 - __clz(rel);
       rel &= ~(1u << e);
-      const bool b0 = live[0] && ((pm[0] >> e) & 1u), b1 = live[1] && ((pm[1] >> e) & 1u);
-      const uint32_t B0 = __ballot_sync(0xffffffffu, b0), B1 = __ballot_sync(0xffffffffu, b1);
-      const int n0 = __popc(B0), n = n0 + __popc(B1);
+      // pack this splat's pixels onto lanes 0..n-1 in pixel order
+      bool bq[QP];
+      int n = 0;
+#pragma unroll
+      for (int q = 0; q < QP; ++q) {
+        bq[q] = live[q] && ((pm[q] >> e) & 1u);
+        const uint32_t B = __ballot_sync(0xffffffffu, bq[q]);
+        if (bq[q]) cs.list[n + __popc(B & lt)] = (uint8_t)(lane + 32 * q);
+        n += __popc(B);
+      }
       if (n == 0) continue;  // every pixel of this splat was deferred
-      const int r0 = __popc(B0 & lt), r1 = n0 + __popc(B1 & lt);
-      if (b0) cs.list[r0] = (uint8_t)lane;
-      if (b1) cs.list[r1] = (uint8_t)(lane + 32);
       __syncwarp();
       const uint32_t jj = start + e;
       const SplatRec &r = wrec[e];
@@ -602,7 +618,7 @@ __global__ void __launch_bounds__(128, KG == 1 ? (EXT ? 5 : HGS_BWDC_MINB1) : 3)
 #pragma unroll
         for (int s2 = 0; s2 < 4; ++s2) ve[k][s2] = 0.f;
       }
-      uint32_t amb_lo = 0u, amb_hi = 0u;
+      int n_amb = 0;
 #pragma unroll 1
       for (int i0 = 0; i0 < n; i0 += 32) {
         const bool act = i0 + lane < n;
@@ -622,6 +638,7 @@ __global__ void __launch_bounds__(128, KG == 1 ? (EXT ? 5 : HGS_BWDC_MINB1) : 3)
 #pragma unroll
             for (int i = 0; i < 6; ++i) f.pad[i] = 0;
             b.c.bwd_fix[atomicAdd(&a.st->n_fix_bwd, 1u)] = f;
+            cs.dead[p] = 1;
             amb = true;
           } else if (c == kContrib) {
             if (count) {
@@ -655,15 +672,15 @@ __global__ void __launch_bounds__(128, KG == 1 ? (EXT ? 5 : HGS_BWDC_MINB1) : 3)
                                     fmaf(r.r4.z, w, S.sn2));
           }
         }
-        const uint32_t bal = __ballot_sync(0xffffffffu, amb);
-        if (i0 == 0) amb_lo = bal; else amb_hi = bal;
+        n_amb += __popc(__ballot_sync(0xffffffffu, amb));
       }
-      if (amb_lo | amb_hi) {  // deferred pixels drop out of the walk
-        if (b0 && (((r0 < 32 ? amb_lo >> r0 : amb_hi >> (r0 - 32))) & 1u)) live[0] = false;
-        if (b1 && (((r1 < 32 ? amb_lo >> r1 : amb_hi >> (r1 - 32))) & 1u)) live[1] = false;
+      __syncwarp();  // pixel state, dead flags and the list are rewritten for the next splat
+      if (n_amb) {   // deferred pixels drop out of the walk
+#pragma unroll
+        for (int q = 0; q < QP; ++q)
+          if (bq[q] && cs.dead[lane + 32 * q]) live[q] = false;
+        if (n_amb == n) continue;  // nothing contributed
       }
-      __syncwarp();  // pixel state and the list are rewritten for the next splat
-      if (__popc(amb_lo) + __popc(amb_hi) == n) continue;  // nothing contributed
       const bool is3d = rec_is3d(r);
       const uint32_t gidx = rec_idx(r);
       if (lane == 0) b.touched[gidx] = 1;
@@ -704,7 +721,10 @@ __global__ void __launch_bounds__(128, KG == 1 ? (EXT ? 5 : HGS_BWDC_MINB1) : 3)
       }
     }
     __syncwarp();  // the next chunk overwrites this warp's staging slots
-    if (!__any_sync(0xffffffffu, live[0] || live[1])) break;
+    bool any_live = false;
+#pragma unroll
+    for (int q = 0; q < QP; ++q) any_live = any_live || live[q];
+    if (!__any_sync(0xffffffffu, any_live)) break;
   }
   if (count) {
     n_ev = __reduce_add_sync(0xffffffffu, n_ev);
@@ -723,15 +743,16 @@ __global__ void __launch_bounds__(128, KG == 1 ? (EXT ? 5 : HGS_BWDC_MINB1) : 3)
 // Host launcher (the kernel template is instantiated in this translation unit).
 template <int KG, bool EXT, bool DET>
 cudaError_t launch_composite_bwd_c(const BwdArgs &b, int64_t n_tiles, cudaStream_t s) {
-  const size_t dyn = 4 * cstate_bytes<KG, EXT>();
+  constexpr int QP = HGS_BWDC_QP;
+  const size_t dyn = (8 / QP) * cstate_bytes<KG, EXT, QP>();
   static bool attr_set = false;
   if (!attr_set) {
-    const cudaError_t err =
-        cudaFuncSetAttribute(k_composite_bwd_c<KG, EXT, DET>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+    const cudaError_t err = cudaFuncSetAttribute(k_composite_bwd_c<KG, EXT, DET, QP>,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
     if (err != cudaSuccess) return err;
     attr_set = true;
   }
-  k_composite_bwd_c<KG, EXT, DET><<<(unsigned)n_tiles, 128, dyn, s>>>(b);
+  k_composite_bwd_c<KG, EXT, DET, QP><<<(unsigned)n_tiles, 256 / QP, dyn, s>>>(b);
   return cudaGetLastError();
 }
 
