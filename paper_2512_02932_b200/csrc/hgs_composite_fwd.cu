@@ -9,8 +9,8 @@
 //                    (lane-parallel evaluation, product scan for T).
 #include "hgs_kernels.cuh"
 
-#ifndef HGS_FWD_STOP_FAST
-#define HGS_FWD_STOP_FAST 1
+#ifndef HGS_FWD_ONE_DEFER
+#define HGS_FWD_ONE_DEFER 1
 #endif
 #ifndef HGS_FWD_MINB
 #define HGS_FWD_MINB 4  // CTAs per SM the hot compositor is register-budgeted for
@@ -99,43 +99,55 @@ __global__ void __launch_bounds__(kBlock, HGS_FWD_MINB) k_composite_fwd(Composit
       PairEval p;
       const int c = eval_fast<false>(r, ix, iy, a.flags, p);
       if (c == kSkip) continue;
+#if HGS_FWD_ONE_DEFER
+      // one deferral site (the pair's decision or the early-stop decision), so
+      // the worklist address is formed only on that rare path
+      uint32_t dmode = 2u;
+      if (c == kAmbiguous) {
+        if (COUNT) atomicAdd(&a.st->diag[is3d ? 12 : 13], 1ull);  // deferral reasons
+        dmode = 0u;
+      } else {
+#else
       if (c == kAmbiguous) {
         if (COUNT) atomicAdd(&a.st->diag[is3d ? 12 : 13], 1ull);  // deferral reasons
         defer(base + e, 0u);
         continue;
       }
-      if (COUNT) (is3d ? n_c3 : n_c2) += 1;
-      const float at = p.at;
-      const float w = at * T;
-      const float4 c3 = r.r3, c4 = r.r4;
-      cr = fmaf(w, c3.y, cr);
-      cg = fmaf(w, c3.z, cg);
-      cb = fmaf(w, c3.w, cb);
-      dep = fmaf(w, r.r0.z, dep);
-      n0 = fmaf(w, c4.x, n0);
-      n1 = fmaf(w, c4.y, n1);
-      n2 = fmaf(w, c4.z, n2);
-      if (NAIVE) ++cnt;  // tiled frames derive the blend-log counts from the masks
-      cm |= 1u << e;
-      last = base + e - lo + 1u;
-      T = T * (1.f - at);
-      // early stop T < 1e-4 (_blend_py.py:111-113); near the threshold the
-      // decision is deferred to the float64 transmittance replay.  One
-      // compare on the common path (T well above the threshold).
-#if HGS_FWD_STOP_FAST
-      if (T <= (float)kEarlyStopT * (1.f + 2e-5f)) {
-        if (exact && T >= (float)kEarlyStopT * (1.f - 2e-5f)) {
-          if (COUNT) atomicAdd(&a.st->diag[14], 1ull);
-          defer(base + e, 1u);
-        }
-        else if (T < (float)kEarlyStopT)
-          done = true;
-      }
+      {
+#endif
+        if (COUNT) (is3d ? n_c3 : n_c2) += 1;
+        const float at = p.at;
+        const float w = at * T;
+        const float4 c3 = r.r3, c4 = r.r4;
+        cr = fmaf(w, c3.y, cr);
+        cg = fmaf(w, c3.z, cg);
+        cb = fmaf(w, c3.w, cb);
+        dep = fmaf(w, r.r0.z, dep);
+        n0 = fmaf(w, c4.x, n0);
+        n1 = fmaf(w, c4.y, n1);
+        n2 = fmaf(w, c4.z, n2);
+        if (NAIVE) ++cnt;  // tiled frames derive the blend-log counts from the masks
+        cm |= 1u << e;
+        last = base + e - lo + 1u;
+        T = T * (1.f - at);
+        // early stop T < 1e-4 (_blend_py.py:111-113); near the threshold the
+        // decision is deferred to the float64 transmittance replay.  One
+        // compare on the common path (T well above the threshold).
+        if (T <= (float)kEarlyStopT * (1.f + 2e-5f)) {
+          if (exact && T >= (float)kEarlyStopT * (1.f - 2e-5f)) {
+            if (COUNT) atomicAdd(&a.st->diag[14], 1ull);
+#if HGS_FWD_ONE_DEFER
+            dmode = 1u;
 #else
-      if (exact && fabsf(T - (float)kEarlyStopT) <= 2e-5f * (float)kEarlyStopT)
-        defer(base + e, 1u);
-      else if (T < (float)kEarlyStopT)
-        done = true;
+            defer(base + e, 1u);
+#endif
+          }
+          else if (T < (float)kEarlyStopT)
+            done = true;
+        }
+      }
+#if HGS_FWD_ONE_DEFER
+      if (dmode != 2u) defer(base + e, dmode);
 #endif
     }
     if (!NAIVE && walking)

@@ -46,17 +46,20 @@ __host__ __device__ constexpr int field_width(int f, int B) { return f < 2 ? 3 :
 __host__ __device__ constexpr int field_j0(int f) { return f == 0 ? 0 : (f == 1 ? 3 : (f == 2 ? 6 : (f == 3 ? 10 : 11))); }
 __device__ __forceinline__ int64_t field_off(int f, int64_t n) { return (int64_t)field_j0(f) * n; }
 
+#ifndef HGS_OPT_MINB
+#define HGS_OPT_MINB 4  // 4 CTAs x 256 threads per SM: 64 registers
+#endif
+
 // Templated on the SH basis count so every field width is a compile-time
 // constant (index division becomes multiply-shift; loops unroll).
 template <int OP, int B>
-__global__ void __launch_bounds__(kOThreads) k_optim(OptArgs a) {
+__global__ void __launch_bounds__(kOThreads, HGS_OPT_MINB) k_optim(OptArgs a) {
   constexpr bool kCombine = OP != kOpAdam;
   constexpr bool kAdam = OP != kOpCombine;
   constexpr int P = 11 + 3 * B;
   __shared__ float sl[kCombine ? P : 1][kStride], sh[kCombine ? P : 1][kStride];
   __shared__ double part[4][kG][3];
-  __shared__ float coef[kG];
-  __shared__ int kind[kG];
+  __shared__ float4 surg[kG];
   __shared__ float rot[kG][4];
   __shared__ unsigned int nconf;
   const int64_t g0 = (int64_t)blockIdx.x * kG;
@@ -69,11 +72,15 @@ __global__ void __launch_bounds__(kOThreads) k_optim(OptArgs a) {
     for (int f = 0; f < 5; ++f) {
       const int fw = field_width(f, B), j0 = field_j0(f);
       const int64_t base = field_off(f, a.n) + g0 * fw;
+      const int cnt = gn * fw;
+      const float *const glf = a.gl + base, *const ghf = a.gh + base;
+      {
 #pragma unroll 4
-      for (int e = tid; e < gn * fw; e += kOThreads) {
-        const int g = e / fw, j = j0 + e - g * fw;
-        sl[j][g] = __ldg(a.gl + base + e);
-        sh[j][g] = __ldg(a.gh + base + e);
+        for (int e = tid; e < cnt; e += kOThreads) {
+          const int g = e / fw, j = j0 + e - g * fw;
+          sl[j][g] = __ldg(glf + e);
+          sh[j][g] = __ldg(ghf + e);
+        }
       }
     }
     if (tid == 0) nconf = 0u;
@@ -107,8 +114,9 @@ __global__ void __launch_bounds__(kOThreads) k_optim(OptArgs a) {
         if (flat && nl > 0.0) { k = kProjHigh; c = (float)(d / nl); }   // Eq. 9, surgery.py:88-89
         if (!flat && nh > 0.0) { k = kProjLow; c = (float)(d / nh); }   // Eq. 10, surgery.py:90-91
       }
-      kind[tid] = k;
-      coef[tid] = c;
+      // branch-free form of the five cases (exact: fmaf(-0, x, y) == y, 1 * y == y)
+      surg[tid] = make_float4(k == kProjHigh ? c : 0.f, k == kProjLow ? c : 0.f, k == kZeroHigh ? 0.f : 1.f,
+                              k == kZeroLow ? 0.f : 1.f);
       if (conflicted) atomicAdd(&nconf, 1u);
     }
     __syncthreads();
@@ -119,23 +127,31 @@ __global__ void __launch_bounds__(kOThreads) k_optim(OptArgs a) {
   //    kU elements per thread per step, all global loads issued before any
   //    store (the pointers may alias as far as the compiler knows, so it
   //    would otherwise serialise them): kU x 4 loads in flight per thread.
+  //    Per-field base pointers + 32-bit indices keep the address arithmetic
+  //    to one IMAD.WIDE per access; the surgery is branch-free:
+  //    gh' = mh * (gh - ch gl), gl' = ml * (gl - cl gh)  (surgery.py:83-91)
   constexpr int kU = 4;
 #pragma unroll
   for (int f = 0; f < 5; ++f) {
     const int fw = field_width(f, B), j0 = field_j0(f);
     const int64_t base = field_off(f, a.n) + g0 * fw;
     const int cnt = gn * fw;
+    const float *const gcf = a.gc + base;
+    float *const mf = kAdam ? a.m + base : nullptr;
+    float *const vf = kAdam ? a.v + base : nullptr;
+    float *const of = kAdam ? nullptr : a.out + base;
     float *const prm = kAdam ? a.field[f] + g0 * fw : nullptr;
+    const float step = kAdam ? a.step_size[f] : 0.f;
     for (int e0 = tid; e0 < cnt; e0 += kOThreads * kU) {
       float gcv[kU], mv[kU], vv[kU], pv[kU];
 #pragma unroll
       for (int u = 0; u < kU; ++u) {
         const int e = e0 + u * kOThreads;
         if (e < cnt) {
-          gcv[u] = __ldcs(a.gc + base + e);
+          gcv[u] = __ldcs(gcf + e);
           if (kAdam) {
-            mv[u] = __ldcs(a.m + base + e);
-            vv[u] = __ldcs(a.v + base + e);
+            mv[u] = __ldcs(mf + e);
+            vv[u] = __ldcs(vf + e);
             pv[u] = __ldcs(prm + e);
           }
         }
@@ -147,27 +163,21 @@ __global__ void __launch_bounds__(kOThreads) k_optim(OptArgs a) {
         const int g = e / fw, j = j0 + e - g * fw;
         float grad = gcv[u];
         if (kCombine) {
-          float gl = sl[j][g], gh = sh[j][g];
-          switch (kind[g]) {
-            case kProjHigh: gh = fmaf(-coef[g], gl, gh); break;
-            case kProjLow: gl = fmaf(-coef[g], gh, gl); break;
-            case kZeroHigh: gh = 0.f; break;
-            case kZeroLow: gl = 0.f; break;
-            default: break;
-          }
-          grad = (grad + gl) + gh;  // surgery.py:92
+          const float gl = sl[j][g], gh = sh[j][g];
+          const float4 w = surg[g];  // ch, cl, mh, ml
+          grad = (grad + w.w * fmaf(-w.y, gh, gl)) + w.z * fmaf(-w.x, gl, gh);  // surgery.py:92
         }
         if (!kAdam) {
-          __stcs(a.out + base + e, grad);
+          __stcs(of + e, grad);
           continue;
         }
         float m = mv[u], v = vv[u];
         m = fmaf(1.f - a.beta1, grad - m, m);                // exp_avg.lerp_(grad, 1 - beta1)
         v = fmaf(1.f - a.beta2, grad * grad, v * a.beta2);   // exp_avg_sq.mul_(beta2).addcmul_(g, g, 1 - beta2)
         const float denom = sqrtf(v) / a.bc2_sqrt + a.eps;
-        const float pn = pv[u] - a.step_size[f] * (m / denom);
-        __stcs(a.m + base + e, m);
-        __stcs(a.v + base + e, v);
+        const float pn = pv[u] - step * (m / denom);
+        __stcs(mf + e, m);
+        __stcs(vf + e, v);
         if (f == 2)
           rot[g][e - g * fw] = pn;  // renormalised below
         else
