@@ -588,7 +588,7 @@ int hgs_backward(const hgs_scene *scene, const hgs_camera *camera, const hgs_set
     if (n > 0) {
       // one warp per CTA; shared memory: SH rows in + kc SH-gradient rows out
       const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 32), 148 * 48));
-      const size_t smem = (size_t)(1 + kc) * 32 * (3 * scene->sh_bases + 1) * sizeof(float);
+      const size_t smem = (size_t)2 * 32 * (3 * scene->sh_bases + 1) * sizeof(float);  // SH in + one SH out
       switch (scene->sh_bases) {
         case 1: k_chain_rule_t<0><<<grid, 32, smem, s>>>(c); break;
         case 4: k_chain_rule_t<1><<<grid, 32, smem, s>>>(c); break;

@@ -98,9 +98,12 @@ __device__ __forceinline__ float clamp_mask(const float *shc_ch, const float *ba
 // Gaussians with an all-zero accumulator (culled or never composited) get
 // exactly zero gradients (the chain rule is linear).
 constexpr int kChainThreads = 32;
+#ifndef HGS_CHAIN_MINB
+#define HGS_CHAIN_MINB 16  // 16 warps per SM: 128 registers
+#endif
 
 template <int DEG>
-__global__ void __launch_bounds__(kChainThreads) k_chain_rule_t(ChainArgs c) {
+__global__ void __launch_bounds__(kChainThreads, HGS_CHAIN_MINB) k_chain_rule_t(ChainArgs c) {
   constexpr int B = (DEG + 1) * (DEG + 1);
   constexpr int SB = 3 * B, SS = 3 * B + 1;  // row length, padded smem stride
   extern __shared__ float s_chain[];
@@ -117,43 +120,43 @@ __global__ void __launch_bounds__(kChainThreads) k_chain_rule_t(ChainArgs c) {
     }
     __syncwarp();
     const int64_t i = base + lane;
-    if (lane < cnt) {
+    const bool valid = lane < cnt;
     bool any = false;
-    for (int k = 0; k < c.kg; ++k) {
-      const float4 *a4 = reinterpret_cast<const float4 *>(c.acc + ((int64_t)i * c.kg + k) * kAcc);
+    if (valid) {
+      for (int k = 0; k < c.kg; ++k) {
+        const float4 *a4 = reinterpret_cast<const float4 *>(c.acc + ((int64_t)i * c.kg + k) * kAcc);
 #pragma unroll
-      for (int s = 0; s < 4; ++s) {
-        const float4 x = a4[s];
-        any |= (x.x != 0.f) | (x.y != 0.f) | (x.z != 0.f) | (x.w != 0.f);
-      }
-      if (c.acc_ext) {
-        const float4 x = *reinterpret_cast<const float4 *>(c.acc_ext + ((int64_t)i * c.kg + k) * kAccExt);
-        any |= (x.x != 0.f) | (x.y != 0.f) | (x.z != 0.f) | (x.w != 0.f);
+        for (int s = 0; s < 4; ++s) {
+          const float4 x = a4[s];
+          any |= (x.x != 0.f) | (x.y != 0.f) | (x.z != 0.f) | (x.w != 0.f);
+        }
+        if (c.acc_ext) {
+          const float4 x = *reinterpret_cast<const float4 *>(c.acc_ext + ((int64_t)i * c.kg + k) * kAccExt);
+          any |= (x.x != 0.f) | (x.y != 0.f) | (x.z != 0.f) | (x.w != 0.f);
+        }
       }
     }
-    if (!any) {
-      for (int k = 0; k < c.kg; ++k) {
-        float *g = c.grads + (int64_t)k * n * P;
+    // per-Gaussian quantities shared by the kg gradient sets
+    double pd[3] = {0.0, 0.0, 0.0}, td[3] = {0.0, 0.0, 1.0};
+    float X = 0.f, Y = 0.f, Z = 1.f, w = 1.f, x = 0.f, y = 0.f, zq = 0.f, iqn = 1.f;
+    float R[9], V[9], basis[16];
+    float sv0 = 1.f, sv1 = 1.f, sv2 = 1.f, ls2 = 0.f, alpha = 0.f, vx = 0.f, vy = 0.f, vz = 0.f, dist = 1.f;
+    float mask0 = 0.f, mask1 = 0.f, mask2 = 0.f, sg = 1.f;
+    bool is3d = false;
+    int ax = 2;
+    const float fx = (float)cam.fx, fy = (float)cam.fy;
 #pragma unroll
-        for (int s = 0; s < 3; ++s) { g[3 * i + s] = 0.f; g[3 * n + 3 * i + s] = 0.f; }
-#pragma unroll
-        for (int s = 0; s < 4; ++s) g[6 * n + 4 * i + s] = 0.f;
-        g[10 * n + i] = 0.f;
-        float *so = s_chain + (1 + k) * kChainThreads * SS + lane * SS;
-#pragma unroll
-        for (int s = 0; s < SB; ++s) so[s] = 0.f;
-      }
-    } else {
-    double pd[3], td[3];
+    for (int k = 0; k < 9; ++k) V[k] = (float)cam.V[k];
+    const float *shc = s_in + lane * SS;
+    if (any) {
     load_center_d(c.sc, i, pd);
     t_cam_d(cam, pd, td);
-    const float X = (float)td[0], Y = (float)td[1], Z = (float)td[2];
+    X = (float)td[0]; Y = (float)td[1]; Z = (float)td[2];
     const float q0 = c.sc.rotation[4 * i], q1 = c.sc.rotation[4 * i + 1], q2 = c.sc.rotation[4 * i + 2],
                 q3 = c.sc.rotation[4 * i + 3];
     const float qn = sqrtf(((q0 * q0 + q1 * q1) + q2 * q2) + q3 * q3);
-    const float iqn = 1.f / qn;
-    const float w = q0 * iqn, x = q1 * iqn, y = q2 * iqn, zq = q3 * iqn;
-    float R[9];
+    iqn = 1.f / qn;
+    w = q0 * iqn; x = q1 * iqn; y = q2 * iqn; zq = q3 * iqn;
     R[0] = 1.f - 2.f * (y * y + zq * zq);
     R[1] = 2.f * (x * y - w * zq);
     R[2] = 2.f * (x * zq + w * y);
@@ -163,45 +166,51 @@ __global__ void __launch_bounds__(kChainThreads) k_chain_rule_t(ChainArgs c) {
     R[6] = 2.f * (x * zq - w * y);
     R[7] = 2.f * (y * zq + w * x);
     R[8] = 1.f - 2.f * (x * x + y * y);
-    const float ls0 = c.sc.log_scale[3 * i], ls1 = c.sc.log_scale[3 * i + 1], ls2 = c.sc.log_scale[3 * i + 2];
-    const float sv0 = expf(ls0), sv1 = expf(ls1), sv2 = expf(ls2);
-    const float alpha = 1.f / (1.f + expf(-c.sc.opacity_logit[i]));
-    const bool is3d = c.sc.type_spec[i] == 1;
-    const float fx = (float)cam.fx, fy = (float)cam.fy;
-    float V[9];
-#pragma unroll
-    for (int k = 0; k < 9; ++k) V[k] = (float)cam.V[k];
+    const float ls0 = c.sc.log_scale[3 * i], ls1 = c.sc.log_scale[3 * i + 1];
+    ls2 = c.sc.log_scale[3 * i + 2];
+    sv0 = expf(ls0); sv1 = expf(ls1); sv2 = expf(ls2);
+    alpha = 1.f / (1.f + expf(-c.sc.opacity_logit[i]));
+    is3d = c.sc.type_spec[i] == 1;
     // view direction, SH basis, colour-clamp mask (core/sh.py:110-141)
     const double dl0 = pd[0] - cam.campos[0], dl1 = pd[1] - cam.campos[1], dl2 = pd[2] - cam.campos[2];
     const double distd = sqrt((dl0 * dl0 + dl1 * dl1) + dl2 * dl2);
     const double dden = distd > 1e-12 ? distd : 1e-12;
     const double vxd = dl0 / dden, vyd = dl1 / dden, vzd = dl2 / dden;
-    const float vx = (float)vxd, vy = (float)vyd, vz = (float)vzd, dist = (float)distd;
-    float basis[16];
+    vx = (float)vxd; vy = (float)vyd; vz = (float)vzd; dist = (float)distd;
     sh_basis_t<float>(DEG, vx, vy, vz, basis);
-    const float *shc = s_in + lane * SS;
-    const float mask0 = clamp_mask<B>(shc, basis, vxd, vyd, vzd);
-    const float mask1 = clamp_mask<B>(shc + B, basis, vxd, vyd, vzd);
-    const float mask2 = clamp_mask<B>(shc + 2 * B, basis, vxd, vyd, vzd);
+    mask0 = clamp_mask<B>(shc, basis, vxd, vyd, vzd);
+    mask1 = clamp_mask<B>(shc + B, basis, vxd, vyd, vzd);
+    mask2 = clamp_mask<B>(shc + 2 * B, basis, vxd, vyd, vzd);
     // normal extension: axis and facing sign
     // (log-scale order == the forward's float64 scale order; facing sign in float64)
-    int ax = 2;
     if (is3d) ax = (ls0 <= ls1 && ls0 <= ls2) ? 0 : (ls1 <= ls2 ? 1 : 2);
     double ncd[3];
 #pragma unroll
     for (int r = 0; r < 3; ++r)
       ncd[r] = (cam.V[r * 3] * (double)R[ax] + cam.V[r * 3 + 1] * (double)R[3 + ax]) + cam.V[r * 3 + 2] * (double)R[6 + ax];
-    const float sg = ((ncd[0] * td[0] + ncd[1] * td[1]) + ncd[2] * td[2]) > 0.0 ? -1.f : 1.f;
+    sg = ((ncd[0] * td[0] + ncd[1] * td[1]) + ncd[2] * td[2]) > 0.0 ? -1.f : 1.f;
 
+    }  // any
+    // one gradient set at a time: the SH rows go through one shared buffer
+    float *const so = s_chain + kChainThreads * SS + lane * SS;
     for (int k = 0; k < c.kg; ++k) {
-      const float *A = c.acc + ((int64_t)i * c.kg + k) * kAcc;
       float *g = c.grads + (int64_t)k * n * P;
+      if (valid && !any) {
+#pragma unroll
+        for (int s = 0; s < 3; ++s) { g[3 * i + s] = 0.f; g[3 * n + 3 * i + s] = 0.f; }
+#pragma unroll
+        for (int s = 0; s < 4; ++s) g[6 * n + 4 * i + s] = 0.f;
+        g[10 * n + i] = 0.f;
+#pragma unroll
+        for (int s = 0; s < SB; ++s) so[s] = 0.f;
+      }
+      if (any) {
+      const float *A = c.acc + ((int64_t)i * c.kg + k) * kAcc;
       float d_center[3] = {0.f, 0.f, 0.f}, d_ls[3] = {0.f, 0.f, 0.f};
       float d_R[9] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
       // SH (core/sh.py:125-141)
       const float up0 = A[0] * mask0, up1 = A[1] * mask1, up2 = A[2] * mask2;
       float db[16];
-      float *so = s_chain + (1 + k) * kChainThreads * SS + lane * SS;
 #pragma unroll
       for (int bb = 0; bb < B; ++bb) {
         so[bb] = up0 * basis[bb];
@@ -343,20 +352,17 @@ __global__ void __launch_bounds__(kChainThreads) k_chain_rule_t(ChainArgs c) {
       g[6 * n + 4 * i + 2] = (dyq - dotq * y) * iqn;
       g[6 * n + 4 * i + 3] = (dzq - dotq * zq) * iqn;
       g[10 * n + i] = d_logit;
-    }
-    }  // any
-    }  // lane < cnt
-    __syncwarp();
-    // coalesced SH-gradient segments of this warp step, one per kg
-    for (int k = 0; k < c.kg; ++k) {
-      float *gs = c.grads + (int64_t)k * n * P + 11 * n + base * SB;
-      const float *so = s_chain + (1 + k) * kChainThreads * SS;
+      }  // any
+      __syncwarp();
+      // coalesced SH-gradient segment of this warp step
+      float *gs = g + 11 * n + base * SB;
+      const float *sk = s_chain + kChainThreads * SS;
       for (int e = lane; e < cnt * SB; e += kChainThreads) {
         const int r = e / SB;
-        gs[e] = so[r * SS + (e - r * SB)];
+        gs[e] = sk[r * SS + (e - r * SB)];
       }
+      __syncwarp();
     }
-    __syncwarp();
   }
 }
 
