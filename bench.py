@@ -29,6 +29,7 @@ REPO = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, REPO)
 
 MEASURED_PEAKS = os.path.join(REPO, "MEASURED_PEAKS.json")
+NCU_TAG = "r01e"  # profiles/ncu_<tag>_kernels.json: the committed capture the roofline limiter quotes
 METRIC = "hybrid-GS frames/s fwd & iters/s fwd+bwd at 1M Gaussians 1080p; 1/2/4/8 B200"
 N_SM = 148
 FMA_PER_SM_CLK = 128
@@ -626,12 +627,12 @@ def main():
                 "frac": ach / hbm_peak, "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
     # the limiter of the compositors is the SM issue rate, not a pipe peak:
     # quote the committed ncu capture of the same kernel (profiles/)
-    ncu_file = os.path.join(REPO, "profiles", "ncu_r01b_kernels.json")
+    ncu_file = os.path.join(REPO, "profiles", "ncu_%s_kernels.json" % NCU_TAG)
     if dom in ("composite_fwd", "composite_bwd") and os.path.exists(ncu_file):
-        pref = "k_composite_fwd<0, 0>" if dom == "composite_fwd" else "k_composite_bwd<1, 0, 2, 0>"
+        pref = "k_composite_fwd<0, 0>" if dom == "composite_fwd" else "k_composite_bwd_c<1, 0, 0, 4>"
         for kd in json.load(open(ncu_file)):
             if kd.get("config") == "c2" and kd.get("kernel") == pref:
-                roof["limiter"] = ("SM instruction issue (ncu, profiles/ncu_r01b_kernels.json: issue "
+                roof["limiter"] = ("SM instruction issue (ncu, profiles/ncu_%s_kernels.json: issue " % NCU_TAG +
                                    "active %.0f%%, FP32 pipe %.0f%%, DRAM %.0f%%, %.1f of 32 lanes active)"
                                    % (kd.get("issue_active_pct", 0), kd.get("fma_pipe_pct", 0),
                                       kd.get("dram_pct", 0), kd.get("thread_inst_per_inst", 0)))

@@ -2,7 +2,7 @@
 profiles/: per-kernel metrics JSON, DRAM traffic per stage (read by bench.py
 for roofline.traffic) and a markdown table.
 
-    python tools/ncu_summary.py gpurun_out/prof_c2_raw.csv gpurun_out/prof_c4_raw.csv
+    python tools/ncu_summary.py [--tag r01e] gpurun_out/prof_c2_raw.csv gpurun_out/prof_c4_raw.csv
 """
 import csv
 import json
@@ -58,11 +58,15 @@ def load(path):
 
 
 def main():
+    args = sys.argv[1:]
+    tag = "r01b"
+    if args and args[0] == "--tag":
+        tag, args = args[1], args[2:]
     allk = []
-    for p in sys.argv[1:]:
-        tag = "c4" if "c4" in os.path.basename(p) else "c2"
+    for p in args:
+        cfg = "c4" if "c4" in os.path.basename(p) else "c2"
         for d in load(p):
-            d["config"] = tag
+            d["config"] = cfg
             allk.append(d)
     # first launch of each (config, kernel)
     seen, uniq = set(), []
@@ -73,12 +77,12 @@ def main():
         seen.add(key)
         uniq.append(d)
     os.makedirs("profiles", exist_ok=True)
-    json.dump(uniq, open("profiles/ncu_r01b_kernels.json", "w"), indent=1)
+    json.dump(uniq, open("profiles/ncu_%s_kernels.json" % tag, "w"), indent=1)
     # per-stage DRAM traffic (bytes) of the config-2 kernels, as bench.py names the stages
     stage = {"composite_fwd": ["k_composite_fwd"], "composite_bwd": ["k_composite_bwd"],
              "chain_rule(+touched)": ["k_chain_rule"], "preprocess_f64+scan": ["k_preprocess", "k_scan_counts",
                                                                                 "k_rank_scatter"]}
-    tr = {"_source": "profiles/ncu_r01b_kernels.json (ncu --set full, one launch each, config 2): "
+    tr = {"_source": "profiles/ncu_%s_kernels.json (ncu --set full, one launch each, config 2): " % tag +
                      "dram__bytes_read.sum + dram__bytes_write.sum per launch"}
     for st, pref in stage.items():
         b = sum((d.get("dram_read_MB", 0) + d.get("dram_write_MB", 0)) * 1e6 for d in uniq
@@ -91,7 +95,7 @@ def main():
     for d in uniq:
         lines.append("| %s | %s | " % (d["config"], d["kernel"]) +
                      " | ".join(("%.3f" % d[c]) if isinstance(d.get(c), float) else str(d.get(c, "")) for c in cols) + " |")
-    open("profiles/ncu_r01b_table.md", "w").write("\n".join(lines) + "\n")
+    open("profiles/ncu_%s_table.md" % tag, "w").write("\n".join(lines) + "\n")
     print("\n".join(lines))
 
 
