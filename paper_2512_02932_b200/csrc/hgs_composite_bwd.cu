@@ -567,6 +567,7 @@ __global__ void __launch_bounds__(256 / QP, HGS_BWDC_MINB(KG, EXT, QP)) k_compos
   uint32_t lt;
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(lt));
   SplatRec *wrec = s_rec[warp];
+  const uint32_t list_sa = (uint32_t)__cvta_generic_to_shared(cs.list);
 
   for (uint32_t top = lo + warp_last, start; top > lo; top = start) {
     start = lo + (((top - 1u - lo) >> 5) << 5);  // the forward's 32-entry chunks
@@ -595,14 +596,18 @@ __global__ void __launch_bounds__(256 / QP, HGS_BWDC_MINB(KG, EXT, QP)) k_compos
     while (rel) {
       const int e = 31 - __clz(rel);
       rel &= ~(1u << e);
-      // pack this splat's pixels onto lanes 0..n-1 in pixel order
+      // pack this splat's pixels onto lanes 0..n-1 in pixel order (pm[q] is
+      // cleared when the pixel is deferred, so the mask bit alone decides)
       bool bq[QP];
       int n = 0;
 #pragma unroll
       for (int q = 0; q < QP; ++q) {
-        bq[q] = live[q] && ((pm[q] >> e) & 1u);
+        bq[q] = (pm[q] >> e) & 1u;
         const uint32_t B = __ballot_sync(0xffffffffu, bq[q]);
-        if (bq[q]) cs.list[n + __popc(B & lt)] = (uint8_t)(lane + 32 * q);
+        asm volatile("{ .reg .pred p; setp.ne.u32 p, %2, 0; @p st.shared.u8 [%0], %1; }" ::"r"(
+                         list_sa + (uint32_t)(n + __popc(B & lt))),
+                     "r"(lane + 32 * q), "r"((uint32_t)bq[q])
+                     : "memory");
         n += __popc(B);
       }
       if (n == 0) continue;  // every pixel of this splat was deferred
@@ -678,7 +683,10 @@ __global__ void __launch_bounds__(256 / QP, HGS_BWDC_MINB(KG, EXT, QP)) k_compos
       if (n_amb) {   // deferred pixels drop out of the walk
 #pragma unroll
         for (int q = 0; q < QP; ++q)
-          if (bq[q] && cs.dead[lane + 32 * q]) live[q] = false;
+          if (bq[q] && cs.dead[lane + 32 * q]) {
+            live[q] = false;
+            pm[q] = 0u;
+          }
         if (n_amb == n) continue;  // nothing contributed
       }
       const bool is3d = rec_is3d(r);
