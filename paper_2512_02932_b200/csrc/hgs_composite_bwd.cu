@@ -497,6 +497,9 @@ constexpr size_t cstate_bytes() {
 #ifndef HGS_BWDC_MINBK
 #define HGS_BWDC_MINBK 4  // the same for KG >= 2
 #endif
+#ifndef HGS_BWDC_PIN_SA
+#define HGS_BWDC_PIN_SA 1
+#endif
 #ifndef HGS_BWDC_QP
 #define HGS_BWDC_QP 4  // pixels per lane: warp blocks of 8 x (4 QP) pixels, 8 / QP warps per tile
 #endif
@@ -559,8 +562,14 @@ __global__ void __launch_bounds__(256 / QP, HGS_BWDC_MINB(KG, EXT, QP)) k_compos
   __syncwarp();
   const int slot = lane & 15;
   const uint32_t red_sa = (uint32_t)__cvta_generic_to_shared(&s_red[warp][0]);
-  const uint32_t row_sa = red_sa + (uint32_t)((lane * kRedStride + (lane >= 16 ? 16 : 0)) * 4);
-  const uint32_t col_sa = red_sa + (uint32_t)(((lane & 16) * kRedStride + (lane >= 16 ? 16 : 0) + (lane & 15)) * 4);
+  uint32_t row_sa = red_sa + (uint32_t)((lane * kRedStride + (lane >= 16 ? 16 : 0)) * 4);
+  uint32_t col_sa = red_sa + (uint32_t)(((lane & 16) * kRedStride + (lane >= 16 ? 16 : 0) + (lane & 15)) * 4);
+#if HGS_BWDC_PIN_SA
+  // opaque copies: kept in registers instead of being re-derived from
+  // %tid / the shared window base at every splat
+  asm volatile("mov.u32 %0, %0;" : "+r"(row_sa));
+  asm volatile("mov.u32 %0, %0;" : "+r"(col_sa));
+#endif
   const bool writer = lane < 16;
   const bool count = a.flags & HGS_FLAG_COUNT;
   uint32_t n_ev = 0, n_c3 = 0, n_cr = 0, n_cl = 0;

@@ -9,6 +9,9 @@
 //                    (lane-parallel evaluation, product scan for T).
 #include "hgs_kernels.cuh"
 
+#ifndef HGS_FWD_PIN_SA
+#define HGS_FWD_PIN_SA 1
+#endif
 #ifndef HGS_FWD_ONE_DEFER
 #define HGS_FWD_ONE_DEFER 1
 #endif
@@ -51,6 +54,10 @@ __global__ void __launch_bounds__(kBlock, HGS_FWD_MINB) k_composite_fwd(Composit
   bool done = !inside, deferred = false;
   uint32_t n_ev3 = 0, n_ev2 = 0, n_c3 = 0, n_c2 = 0;  // HGS_FLAG_COUNT
   SplatRec *wrec = s_rec[warp];
+#if HGS_FWD_PIN_SA
+  uint32_t wrec_sa = (uint32_t)__cvta_generic_to_shared(wrec);
+  asm volatile("mov.u32 %0, %0;" : "+r"(wrec_sa));  // opaque: kept, not re-derived per splat
+#endif
 
   auto defer = [&](uint32_t entry, uint32_t mode) {
     FwdFix f;
@@ -93,7 +100,20 @@ __global__ void __launch_bounds__(kBlock, HGS_FWD_MINB) k_composite_fwd(Composit
       rel &= rel - 1;
       const uint32_t m = __shfl_sync(0xffffffffu, pm, e);
       if (done || !(m & lane_bit)) continue;
+#if HGS_FWD_PIN_SA
+      SplatRec r;
+      {
+        const uint32_t ra = wrec_sa + (uint32_t)e * (uint32_t)sizeof(SplatRec);
+        asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(r.r0.x), "=f"(r.r0.y), "=f"(r.r0.z), "=f"(r.r0.w) : "r"(ra));
+        asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4+16];" : "=f"(r.r1.x), "=f"(r.r1.y), "=f"(r.r1.z), "=f"(r.r1.w) : "r"(ra));
+        asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4+32];" : "=f"(r.r2.x), "=f"(r.r2.y), "=f"(r.r2.z), "=f"(r.r2.w) : "r"(ra));
+        asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4+48];" : "=f"(r.r3.x), "=f"(r.r3.y), "=f"(r.r3.z), "=f"(r.r3.w) : "r"(ra));
+        asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4+64];" : "=f"(r.r4.x), "=f"(r.r4.y), "=f"(r.r4.z), "=f"(r.r4.w) : "r"(ra));
+        asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4+80];" : "=r"(r.r5.x), "=r"(r.r5.y), "=r"(r.r5.z), "=r"(r.r5.w) : "r"(ra));
+      }
+#else
       const SplatRec &r = wrec[e];
+#endif
       const bool is3d = rec_is3d(r);
       if (COUNT) (is3d ? n_ev3 : n_ev2) += 1;
       PairEval p;
