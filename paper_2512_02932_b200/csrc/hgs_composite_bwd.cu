@@ -497,6 +497,9 @@ constexpr size_t cstate_bytes() {
 #ifndef HGS_BWDC_MINBK
 #define HGS_BWDC_MINBK 4  // the same for KG >= 2
 #endif
+#ifndef HGS_BWD_RCP_APPROX
+#define HGS_BWD_RCP_APPROX 1
+#endif
 #ifndef HGS_BWDC_PIN_SA
 #define HGS_BWDC_PIN_SA 1
 #endif
@@ -576,6 +579,10 @@ __global__ void __launch_bounds__(256 / QP, HGS_BWDC_MINB(KG, EXT, QP)) k_compos
   uint32_t lt;
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(lt));
   SplatRec *wrec = s_rec[warp];
+#if HGS_BWDC_PIN_SA
+  uint32_t wrec_sa = (uint32_t)__cvta_generic_to_shared(wrec);
+  asm volatile("mov.u32 %0, %0;" : "+r"(wrec_sa));
+#endif
   const uint32_t list_sa = (uint32_t)__cvta_generic_to_shared(cs.list);
 
   for (uint32_t top = lo + warp_last, start; top > lo; top = start) {
@@ -622,7 +629,12 @@ __global__ void __launch_bounds__(256 / QP, HGS_BWDC_MINB(KG, EXT, QP)) k_compos
       if (n == 0) continue;  // every pixel of this splat was deferred
       __syncwarp();
       const uint32_t jj = start + e;
+#if HGS_BWDC_PIN_SA
+      const SplatRec &r =
+          *reinterpret_cast<const SplatRec *>(__cvta_shared_to_generic(wrec_sa + (uint32_t)e * (uint32_t)sizeof(SplatRec)));
+#else
       const SplatRec &r = wrec[e];
+#endif
       float v[KG][16];
       float ve[KG][4];
 #pragma unroll
@@ -658,7 +670,14 @@ __global__ void __launch_bounds__(256 / QP, HGS_BWDC_MINB(KG, EXT, QP)) k_compos
             if (count) {
               if (rec_is3d(r)) ++n_c3; else if (pe.ray) ++n_cr; else ++n_cl;
             }
+#if HGS_BWD_RCP_APPROX
+            // 1 - at >= 0.01: the approximate reciprocal (1 ulp) is far inside
+            // the gradient tolerance and skips the IEEE division's refinement
+            float inv_om;
+            asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(inv_om) : "f"(1.f - pe.at));
+#else
             const float inv_om = 1.f / (1.f - pe.at);
+#endif
             const float T_k = A.x * inv_om;  // transmittance before this splat
             Suffix S{A.y, A.z, A.w, 0.f, 0.f, 0.f, 0.f};
             if (EXT) {
