@@ -12,7 +12,6 @@ namespace hgs {
 namespace {
 
 constexpr int kMaxGrid = 148 * 8;
-constexpr int kFixupBlocks = 148 * 4;  // persistent fixup grid (one warp per deferred pixel)
 
 struct Layout {
   size_t state, hist_d, off_d, hist_p, off_p, keys_a, keys_b, vals_a, vals_b, lb_sort, lb_scan, recs, recs64, pair_off,
@@ -333,11 +332,7 @@ int hgs_forward(const hgs_scene *scene, const hgs_camera *camera, const hgs_sett
   a.bwd_fix = at<BwdFix>(frame, L.bwd_fix);
   a.pix_mask = at<uint32_t>(frame, L.pix_mask);
   const bool naive = settings->flags & HGS_FLAG_NAIVE, count = settings->flags & HGS_FLAG_COUNT;
-  if (naive && count) k_composite_fwd<true, true><<<(unsigned)n_tiles, kBlock, 0, s>>>(a);
-  else if (naive) k_composite_fwd<true, false><<<(unsigned)n_tiles, kBlock, 0, s>>>(a);
-  else if (count) k_composite_fwd<false, true><<<(unsigned)n_tiles, kBlock, 0, s>>>(a);
-  else k_composite_fwd<false, false><<<(unsigned)n_tiles, kBlock, 0, s>>>(a);
-  HGS_LAUNCHED();
+  HGS_CUDA(launch_composite_fwd(a, n_tiles, naive, count, s));
   // deferred (float32-ambiguous) pixels, float64-exact; exits at once if none
   k_fixup_fwd<<<kFixupBlocks, 256, 0, s>>>(a);
   HGS_LAUNCHED();
@@ -441,39 +436,6 @@ size_t hgs_backward_det_scratch_bytes(int64_t n, int32_t kg, int64_t records) {
 
 }  // extern "C"
 
-template <int KG, bool DET>
-static void launch_bwd(const BwdArgs &b, int64_t n_tiles, bool ext, cudaStream_t s) {
-  // hot replay, then the float64-exact fixup of the deferred pixels.  Pixels
-  // per lane: 2 (4 warps per tile) shares the splat walk and the warp
-  // reduction between two pixels; 1 (8 warps) for register-heavy KG
-  constexpr int ppl = KG == 1 ? HGS_BWD_PPL1 : HGS_BWD_PPL_KG;
-  if (HGS_BWD_COMPACT && !(b.c.flags & HGS_FLAG_NAIVE)) {
-    if (ext) {
-      launch_composite_bwd_c<KG, true, DET>(b, n_tiles, s);
-      k_fixup_bwd<KG, true, DET><<<kFixupBlocks, 256, 0, s>>>(b);
-    } else {
-      launch_composite_bwd_c<KG, false, DET>(b, n_tiles, s);
-      k_fixup_bwd<KG, false, DET><<<kFixupBlocks, 256, 0, s>>>(b);
-    }
-    return;
-  }
-  if (ext) {
-    k_composite_bwd<KG, true, ppl, DET><<<(unsigned)n_tiles, 256 / ppl, 0, s>>>(b);
-    k_fixup_bwd<KG, true, DET><<<kFixupBlocks, 256, 0, s>>>(b);
-  } else {
-    k_composite_bwd<KG, false, ppl, DET><<<(unsigned)n_tiles, 256 / ppl, 0, s>>>(b);
-    k_fixup_bwd<KG, false, DET><<<kFixupBlocks, 256, 0, s>>>(b);
-  }
-}
-
-template <int KG>
-static void launch_bwd(const BwdArgs &b, int64_t n_tiles, bool ext, bool det, cudaStream_t s) {
-  if (det)
-    launch_bwd<KG, true>(b, n_tiles, ext, s);
-  else
-    launch_bwd<KG, false>(b, n_tiles, ext, s);
-}
-
 extern "C" {
 
 int hgs_backward(const hgs_scene *scene, const hgs_camera *camera, const hgs_settings *settings, const void *frame,
@@ -536,13 +498,7 @@ int hgs_backward(const hgs_scene *scene, const hgs_camera *camera, const hgs_set
     b.rec_cap = (uint32_t)rec_cap;
     if (det) HGS_CUDA(cudaMemsetAsync(b.rec_count, 0, 4, s));
     if (m > 0) {
-      switch (kc) {
-        case 1: launch_bwd<1>(b, info->n_tiles, ext, det, s); break;
-        case 2: launch_bwd<2>(b, info->n_tiles, ext, det, s); break;
-        case 3: launch_bwd<3>(b, info->n_tiles, ext, det, s); break;
-        default: launch_bwd<4>(b, info->n_tiles, ext, det, s); break;
-      }
-      HGS_LAUNCHED();
+      HGS_CUDA(launch_composite_bwd(b, (int)kc, info->n_tiles, ext, det, s));
       if (det) {  // sort the records by (Gaussian, tile, sub) and reduce in that order
         uint32_t nrec = 0;
         HGS_CUDA(cudaMemcpyAsync(&nrec, b.rec_count, 4, cudaMemcpyDeviceToHost, s));
@@ -589,13 +545,7 @@ int hgs_backward(const hgs_scene *scene, const hgs_camera *camera, const hgs_set
       // one warp per CTA; shared memory: SH rows in + kc SH-gradient rows out
       const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 32), 148 * 48));
       const size_t smem = (size_t)2 * 32 * (3 * scene->sh_bases + 1) * sizeof(float);  // SH in + one SH out
-      switch (scene->sh_bases) {
-        case 1: k_chain_rule_t<0><<<grid, 32, smem, s>>>(c); break;
-        case 4: k_chain_rule_t<1><<<grid, 32, smem, s>>>(c); break;
-        case 9: k_chain_rule_t<2><<<grid, 32, smem, s>>>(c); break;
-        default: k_chain_rule_t<3><<<grid, 32, smem, s>>>(c); break;
-      }
-      HGS_LAUNCHED();
+      HGS_CUDA(launch_chain_rule(c, scene->sh_bases, grid, smem, s));
     }
   }
   HGS_CUDA(record_event(settings, 2, s));

@@ -366,9 +366,14 @@ __global__ void __launch_bounds__(kChainThreads, HGS_CHAIN_MINB) k_chain_rule_t(
   }
 }
 
-template __global__ void k_chain_rule_t<0>(ChainArgs);
-template __global__ void k_chain_rule_t<1>(ChainArgs);
-template __global__ void k_chain_rule_t<2>(ChainArgs);
-template __global__ void k_chain_rule_t<3>(ChainArgs);
+cudaError_t launch_chain_rule(const ChainArgs &c, int sh_bases, int grid, size_t smem, cudaStream_t s) {
+  switch (sh_bases) {
+    case 1: k_chain_rule_t<0><<<grid, kChainThreads, smem, s>>>(c); break;
+    case 4: k_chain_rule_t<1><<<grid, kChainThreads, smem, s>>>(c); break;
+    case 9: k_chain_rule_t<2><<<grid, kChainThreads, smem, s>>>(c); break;
+    default: k_chain_rule_t<3><<<grid, kChainThreads, smem, s>>>(c); break;
+  }
+  return cudaGetLastError();
+}
 
 }  // namespace hgs

@@ -20,9 +20,6 @@ namespace hgs {
 //  3D: 6-8 = dL/dcov2d (a, b, c);  2D ray: 6-8 = dL/dM0 (cols 0,1,3),
 //  9-11 = dL/dM1, 12-14 = dL/dM3 w.r.t. anchor-relative pixels; 15 unused.
 // Extension slots (separate array, 4 per (Gaussian, kg)): z, normal xyz.
-#ifndef HGS_BWD_MINB1
-#define HGS_BWD_MINB1 5  // CTAs per SM the KG = 1 backward is register-budgeted for
-#endif
 constexpr int kAcc = 16;
 constexpr int kAccExt = 4;
 
@@ -32,69 +29,8 @@ __device__ __forceinline__ float warp_sum_f(float x) {
   return x;
 }
 
-// Sum 16 per-lane values over the warp.  On return lane l holds the total of
-// slot ((l >> 4) & 1) * 8 + ((l >> 3) & 1) * 4 + ((l >> 2) & 1) * 2 + ((l >> 1) & 1)
-// (lanes l and l ^ 1 hold the same slot).  16 shuffles instead of 16 x 5.
-__device__ __forceinline__ float warp_transpose_reduce16(float (&v)[16], int lane) {
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const bool hi = lane & 16;
-    float send = hi ? v[i] : v[i + 8];
-    float keep = hi ? v[i + 8] : v[i];
-    v[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
-  }
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const bool hi = lane & 8;
-    float send = hi ? v[i] : v[i + 4];
-    float keep = hi ? v[i + 4] : v[i];
-    v[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
-  }
-#pragma unroll
-  for (int i = 0; i < 2; ++i) {
-    const bool hi = lane & 4;
-    float send = hi ? v[i] : v[i + 2];
-    float keep = hi ? v[i + 2] : v[i];
-    v[i] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
-  }
-  {
-    const bool hi = lane & 2;
-    float send = hi ? v[0] : v[1];
-    float keep = hi ? v[1] : v[0];
-    v[0] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
-  }
-  return v[0] + __shfl_xor_sync(0xffffffffu, v[0], 1);
-}
-
-#ifndef HGS_BWD_KNOWN
-#define HGS_BWD_KNOWN 1  // backward evaluation skips the cutoff decisions the masks already fixed
-#endif
-#ifndef HGS_BWD_SMEM_REDUCE
-#define HGS_BWD_SMEM_REDUCE 2
-#endif
 constexpr int kRedStride = 20;                   // floats per lane row (16-byte aligned rows)
 constexpr int kRedWarp = 32 * kRedStride + 16;   // upper half shifted 16 banks: conflict-free column reads
-
-// Sum 16 per-lane values over the warp through shared memory: each lane stores
-// its row (4 x STS.128), lane l sums column (l & 15) over its half-warp's 16
-// rows, one shuffle joins the halves.  On return lane l holds slot (l & 15)
-// (lanes l and l ^ 16 hold the same slot).  ~37 instructions instead of the
-// transpose reduction's 16 shuffles + 30 selects + 16 adds.
-__device__ __forceinline__ float warp_smem_reduce16(const float (&v)[16], int lane, float *red) {
-  float *row = red + lane * kRedStride + (lane >= 16 ? 16 : 0);
-  reinterpret_cast<float4 *>(row)[0] = make_float4(v[0], v[1], v[2], v[3]);
-  reinterpret_cast<float4 *>(row)[1] = make_float4(v[4], v[5], v[6], v[7]);
-  reinterpret_cast<float4 *>(row)[2] = make_float4(v[8], v[9], v[10], v[11]);
-  reinterpret_cast<float4 *>(row)[3] = make_float4(v[12], v[13], v[14], v[15]);
-  __syncwarp();
-  const float *col = red + (lane & 16) * kRedStride + (lane >= 16 ? 16 : 0) + (lane & 15);
-  float acc = 0.f;
-#pragma unroll
-  for (int t = 0; t < 16; ++t) acc += col[t * kRedStride];
-  acc += __shfl_xor_sync(0xffffffffu, acc, 16);
-  __syncwarp();  // the next reduction overwrites the rows
-  return acc;
-}
 
 // The same reduction on 32-bit shared-window addresses computed once per
 // thread (row_sa: this lane's row, col_sa: the column it sums), with four
@@ -114,10 +50,6 @@ __device__ __forceinline__ float warp_smem_reduce16_sa(const float (&v)[16], uin
                     (((x[8] + x[9]) + (x[10] + x[11])) + ((x[12] + x[13]) + (x[14] + x[15])));
   __syncwarp();  // the next reduction overwrites the rows
   return acc + __shfl_xor_sync(0xffffffffu, acc, 16);
-}
-
-__device__ __forceinline__ int transpose_slot(int lane) {
-  return ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 + ((lane >> 1) & 1);
 }
 
 // Per-pixel upstream gradients of one pixel (KG stacked).
@@ -216,27 +148,26 @@ __device__ __forceinline__ void pair_grads(const SplatRec &r, const PairEval &p,
   }
 }
 
-// One CTA per 16 x 16 tile; a warp owns an 8 x (4 PPL) block and each lane
-// PPL pixels of it, (x, y + 4q).  With PPL = 2 (4 warps per tile) every
-// staged splat is walked once for both pixels of a lane: the chunk staging,
-// the splat header and -- the dominant per-splat cost -- the 16-slot warp
-// reduction + atomic flush are shared by 64 pixels instead of 32, while the
-// per-pixel math is unchanged (a pixel's evaluation runs only where its 8 x 4
-// half is covered).  DET: the flush writes one record per (splat, warp)
-// instead of atomics (HGS_FLAG_DETERMINISTIC, reduced by k_det_reduce).
-template <int KG, bool EXT, int PPL, bool DET>
-__global__ void __launch_bounds__(256 / PPL, PPL == 4 ? 10 : (PPL == 2 ? (KG == 1 ? HGS_BWD_MINB1 : 4) : 3)) k_composite_bwd(BwdArgs b) {
+// The untiled replay (HGS_FLAG_NAIVE: the reference's pure-Python loop over
+// every splat for every pixel, _blend_py.py:149-240, kept for parity tests of
+// the tiling itself).  One CTA per 16 x 16 block of pixels, a warp owns an
+// 8 x 8 block and each lane two pixels of it, (x, y + 4q); the warp walks all
+// M splats back to front from its pixels' last contributor, 32 at a time,
+// with the per-pixel state in registers.  DET: the flush writes one record
+// per (splat, warp) instead of atomics (HGS_FLAG_DETERMINISTIC).
+template <int KG, bool EXT, bool DET>
+__global__ void __launch_bounds__(128, KG == 1 ? 5 : 4) k_composite_bwd_naive(BwdArgs b) {
+  constexpr int PPL = 2;
   const CompositeArgs &a = b.c;
-  __shared__ SplatRec s_rec[8 / PPL][32];
-  __shared__ __align__(16) float s_red[HGS_BWD_SMEM_REDUCE ? 8 / PPL : 1][HGS_BWD_SMEM_REDUCE ? kRedWarp : 4];
+  __shared__ SplatRec s_rec[4][32];
+  __shared__ __align__(16) float s_red[4][kRedWarp];
   const int tile = blockIdx.x;
   const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int wx0 = tx * kTile + (warp & 1) * 8, wy0 = ty * kTile + (warp >> 1) * 4 * PPL;
   const int ix = wx0 + (lane & 7);
-  const bool naive = a.flags & HGS_FLAG_NAIVE;
   const uint32_t lane_bit = 1u << lane;
-  const uint32_t lo = naive ? 0u : a.tile_off[tile];
+  const uint32_t lo = 0u;
   const int64_t HW = (int64_t)a.width * a.height;
   int iy[PPL];
   bool inside[PPL], dead[PPL];
@@ -261,79 +192,39 @@ __global__ void __launch_bounds__(256 / PPL, PPL == 4 ? 10 : (PPL == 2 ? (KG == 
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) warp_last = max(warp_last, __shfl_xor_sync(0xffffffffu, warp_last, o));
   const uint32_t warp_end = lo + warp_last;  // exclusive
-  const int slot = HGS_BWD_SMEM_REDUCE ? (lane & 15) : transpose_slot(lane);
+  const int slot = lane & 15;
   const uint32_t red_sa = (uint32_t)__cvta_generic_to_shared(&s_red[warp][0]);
   const uint32_t row_sa = red_sa + (uint32_t)((lane * kRedStride + (lane >= 16 ? 16 : 0)) * 4);
   const uint32_t col_sa = red_sa + (uint32_t)(((lane & 16) * kRedStride + (lane >= 16 ? 16 : 0) + (lane & 15)) * 4);
-  const bool writer = HGS_BWD_SMEM_REDUCE ? lane < 16 : !(lane & 1);  // one lane per slot
+  const bool writer = lane < 16;  // one lane per slot
   const bool count = a.flags & HGS_FLAG_COUNT;
   uint32_t n_ev = 0, n_c3 = 0, n_cr = 0, n_cl = 0;
   SplatRec *wrec = s_rec[warp];
 
   for (uint32_t top = warp_end, start; top > lo; top = start) {
-    // chunks aligned to the forward's 32-entry chunks (contribution masks)
-    start = naive ? (top - lo > 32u ? top - 32u : lo) : lo + (((top - 1u - lo) >> 5) << 5);
+    start = top - lo > 32u ? top - 32u : lo;
     const uint32_t j = start + lane;
     uint32_t pm[PPL], any_pm = 0u;
 #pragma unroll
     for (int q = 0; q < PPL; ++q) pm[q] = 0u;
-    uint32_t rel;
-    if (!naive) {
-      // the forward's exact decisions: pm[q] = this lane's pixel q contributing
-      // entries of the chunk (bits at or past the pixel's last contributor cleared)
-      const uint32_t ch = (start - lo) >> 5;
-#pragma unroll
-      for (int q = 0; q < PPL; ++q) {
-        if (!dead[q] && inside[q] && (ch << 5) < last[q]) {
-          uint32_t w = a.pix_mask[mask_word(lo, tile, ch, (uint32_t)((iy[q] & (kTile - 1)) * kTile + (ix & (kTile - 1))))];
-          const uint32_t rem = last[q] - (ch << 5);
-          if (rem < 32u) w &= (1u << rem) - 1u;
-          pm[q] = w;
-        }
-        any_pm |= pm[q];
-      }
-      rel = __reduce_or_sync(0xffffffffu, any_pm);
-      if ((rel >> lane) & 1u) {
-        const SplatRec *g = a.recs + __ldg(a.tile_vals + j);
-        SplatRec r;
-        r.r0 = __ldg(&g->r0); r.r1 = __ldg(&g->r1); r.r2 = __ldg(&g->r2);
-        r.r3 = __ldg(&g->r3); r.r4 = __ldg(&g->r4); r.r5 = __ldg(&g->r5);
-        wrec[lane] = r;
-      }
-    } else {
     if (j < top) {
-      const uint32_t rk = naive ? j : __ldg(a.tile_vals + j);
-      const SplatRec *g = a.recs + rk;
-      const int4 qb = __ldg(&g->r5);
+      const SplatRec *g = a.recs + j;
 #pragma unroll
-      for (int q = 0; q < PPL; ++q) {
-        pm[q] = naive ? 0xffffffffu : pixel_mask(qb, wx0, wy0 + 4 * q);
-        any_pm |= pm[q];
-      }
-      if (any_pm) {
-        SplatRec r;
-        r.r0 = __ldg(&g->r0); r.r1 = __ldg(&g->r1); r.r2 = __ldg(&g->r2);
-        r.r3 = __ldg(&g->r3); r.r4 = __ldg(&g->r4); r.r5 = qb;
-        if (!naive) {  // the 1/255 support may miss a covered 8 x 4 block
-          any_pm = 0u;
-#pragma unroll
-          for (int q = 0; q < PPL; ++q) {
-            if (pm[q] && cull_splat(r, pm[q], wx0, wy0 + 4 * q)) pm[q] = 0u;
-            any_pm |= pm[q];
-          }
-        }
-        if (any_pm) wrec[lane] = r;
-      }
+      for (int q = 0; q < PPL; ++q) pm[q] = 0xffffffffu;
+      any_pm = 0xffffffffu;
+      SplatRec r;
+      r.r0 = __ldg(&g->r0); r.r1 = __ldg(&g->r1); r.r2 = __ldg(&g->r2);
+      r.r3 = __ldg(&g->r3); r.r4 = __ldg(&g->r4); r.r5 = __ldg(&g->r5);
+      wrec[lane] = r;
     }
-    rel = __ballot_sync(0xffffffffu, any_pm != 0u);
-    }  // naive staging
+    uint32_t rel = __ballot_sync(0xffffffffu, any_pm != 0u);
     __syncwarp();
     while (rel) {
       const int e = 31 - __clz(rel);
       rel &= ~(1u << e);
       uint32_t mq[PPL];
 #pragma unroll
-      for (int q = 0; q < PPL; ++q) mq[q] = naive ? __shfl_sync(0xffffffffu, pm[q], e) : pm[q];
+      for (int q = 0; q < PPL; ++q) mq[q] = __shfl_sync(0xffffffffu, pm[q], e);
       const uint32_t jj = start + e;
       const SplatRec &r = wrec[e];
       float v[KG][16];
@@ -349,17 +240,10 @@ __global__ void __launch_bounds__(256 / PPL, PPL == 4 ? 10 : (PPL == 2 ? (KG == 
 #pragma unroll
       for (int q = 0; q < PPL; ++q) {
         const uint32_t m = mq[q];
-        const bool act = naive ? (!dead[q] && inside[q] && (m & lane_bit) && jj - lo < last[q])
-                               : (!dead[q] && ((m >> e) & 1u));
+        const bool act = !dead[q] && inside[q] && (m & lane_bit) && jj - lo < last[q];
         PairEval p;
         if (count && act) ++n_ev;
-#if HGS_BWD_KNOWN
-        const int c = !act ? kSkip
-                           : (naive ? eval_fast<true>(r, ix, iy[q], a.flags, p)
-                                    : eval_fast<true, true>(r, ix, iy[q], a.flags, p));
-#else
         const int c = act ? eval_fast<true>(r, ix, iy[q], a.flags, p) : kSkip;
-#endif
         if (c == kAmbiguous) {
           BwdFix f;
           f.pix = pix[q]; f.entry = jj; f.T_run = T_run[q];
@@ -407,13 +291,7 @@ __global__ void __launch_bounds__(256 / PPL, PPL == 4 ? 10 : (PPL == 2 ? (KG == 
       }
 #pragma unroll
       for (int k = 0; k < KG; ++k) {
-#if HGS_BWD_SMEM_REDUCE == 2
         const float tot = warp_smem_reduce16_sa(v[k], row_sa, col_sa);
-#elif HGS_BWD_SMEM_REDUCE
-        const float tot = warp_smem_reduce16(v[k], lane, s_red[warp]);
-#else
-        const float tot = warp_transpose_reduce16(v[k], lane);
-#endif
         const int nslots = is3d ? 9 : 15;
         if (DET) {
           if (writer && rec < b.rec_cap) b.rec_pay[(size_t)rec * (KG * 20) + k * 20 + slot] = tot;
@@ -776,22 +654,6 @@ __global__ void __launch_bounds__(256 / QP, HGS_BWDC_MINB(KG, EXT, QP)) k_compos
   }
 }
 
-// Host launcher (the kernel template is instantiated in this translation unit).
-template <int KG, bool EXT, bool DET>
-cudaError_t launch_composite_bwd_c(const BwdArgs &b, int64_t n_tiles, cudaStream_t s) {
-  constexpr int QP = HGS_BWDC_QP;
-  const size_t dyn = (8 / QP) * cstate_bytes<KG, EXT, QP>();
-  static bool attr_set = false;
-  if (!attr_set) {
-    const cudaError_t err = cudaFuncSetAttribute(k_composite_bwd_c<KG, EXT, DET, QP>,
-                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
-    if (err != cudaSuccess) return err;
-    attr_set = true;
-  }
-  k_composite_bwd_c<KG, EXT, DET, QP><<<(unsigned)n_tiles, 256 / QP, dyn, s>>>(b);
-  return cudaGetLastError();
-}
-
 __device__ __forceinline__ float warp_sum_bwd(float x) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
@@ -952,23 +814,42 @@ __global__ void k_det_reduce(const unsigned long long *__restrict__ keys, const 
   }
 }
 
-// Instantiations: KG 1..4, with / without extension gradients, atomic and
-// deterministic accumulation; the pixels-per-lane the launcher uses.
-#define HGS_PPL(KG) ((KG) == 1 ? HGS_BWD_PPL1 : HGS_BWD_PPL_KG)
-#define HGS_INST_BWD(KG, EXT)                                                   \
-  template __global__ void k_composite_bwd<KG, EXT, HGS_PPL(KG), false>(BwdArgs); \
-  template __global__ void k_composite_bwd<KG, EXT, HGS_PPL(KG), true>(BwdArgs);  \
-  template __global__ void k_fixup_bwd<KG, EXT, false>(BwdArgs);                  \
-  template __global__ void k_fixup_bwd<KG, EXT, true>(BwdArgs);                  \
-  template cudaError_t launch_composite_bwd_c<KG, EXT, false>(const BwdArgs &, int64_t, cudaStream_t); \
-  template cudaError_t launch_composite_bwd_c<KG, EXT, true>(const BwdArgs &, int64_t, cudaStream_t);
-HGS_INST_BWD(1, false)
-HGS_INST_BWD(2, false)
-HGS_INST_BWD(3, false)
-HGS_INST_BWD(4, false)
-HGS_INST_BWD(1, true)
-HGS_INST_BWD(2, true)
-HGS_INST_BWD(3, true)
-HGS_INST_BWD(4, true)
+// Host launcher: the hot replay (the lane-compacted walk of the contribution
+// masks, or the untiled naive replay), then the float64-exact fixup of the
+// deferred pixels.  All template kernels are instantiated here.
+template <int KG, bool EXT, bool DET>
+static cudaError_t launch_bwd_t(const BwdArgs &b, int64_t n_tiles, cudaStream_t s) {
+  if (b.c.flags & HGS_FLAG_NAIVE) {
+    k_composite_bwd_naive<KG, EXT, DET><<<(unsigned)n_tiles, 128, 0, s>>>(b);
+  } else {
+    constexpr int QP = HGS_BWDC_QP;
+    const size_t dyn = (8 / QP) * cstate_bytes<KG, EXT, QP>();
+    static bool attr_set = false;
+    if (!attr_set) {
+      const cudaError_t err = cudaFuncSetAttribute(k_composite_bwd_c<KG, EXT, DET, QP>,
+                                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+      if (err != cudaSuccess) return err;
+      attr_set = true;
+    }
+    k_composite_bwd_c<KG, EXT, DET, QP><<<(unsigned)n_tiles, 256 / QP, dyn, s>>>(b);
+  }
+  k_fixup_bwd<KG, EXT, DET><<<kFixupBlocks, 256, 0, s>>>(b);
+  return cudaGetLastError();
+}
+
+template <int KG>
+static cudaError_t launch_bwd_kg(const BwdArgs &b, int64_t n_tiles, bool ext, bool det, cudaStream_t s) {
+  if (ext) return det ? launch_bwd_t<KG, true, true>(b, n_tiles, s) : launch_bwd_t<KG, true, false>(b, n_tiles, s);
+  return det ? launch_bwd_t<KG, false, true>(b, n_tiles, s) : launch_bwd_t<KG, false, false>(b, n_tiles, s);
+}
+
+cudaError_t launch_composite_bwd(const BwdArgs &b, int kg, int64_t n_tiles, bool ext, bool det, cudaStream_t s) {
+  switch (kg) {
+    case 1: return launch_bwd_kg<1>(b, n_tiles, ext, det, s);
+    case 2: return launch_bwd_kg<2>(b, n_tiles, ext, det, s);
+    case 3: return launch_bwd_kg<3>(b, n_tiles, ext, det, s);
+    default: return launch_bwd_kg<4>(b, n_tiles, ext, det, s);
+  }
+}
 
 }  // namespace hgs

@@ -206,10 +206,13 @@ __global__ void __launch_bounds__(kBlock, HGS_FWD_MINB) k_composite_fwd(Composit
   if (NAIVE) a.pix_count[pix] = cnt;
 }
 
-template __global__ void k_composite_fwd<false, false>(CompositeArgs);
-template __global__ void k_composite_fwd<true, false>(CompositeArgs);
-template __global__ void k_composite_fwd<false, true>(CompositeArgs);
-template __global__ void k_composite_fwd<true, true>(CompositeArgs);
+cudaError_t launch_composite_fwd(const CompositeArgs &a, int64_t n_tiles, bool naive, bool count, cudaStream_t s) {
+  if (naive && count) k_composite_fwd<true, true><<<(unsigned)n_tiles, kBlock, 0, s>>>(a);
+  else if (naive) k_composite_fwd<true, false><<<(unsigned)n_tiles, kBlock, 0, s>>>(a);
+  else if (count) k_composite_fwd<false, true><<<(unsigned)n_tiles, kBlock, 0, s>>>(a);
+  else k_composite_fwd<false, false><<<(unsigned)n_tiles, kBlock, 0, s>>>(a);
+  return cudaGetLastError();
+}
 
 // Blend-log entry count per pixel of a tiled frame: the popcount of its
 // contribution-mask words up to its last contributor.

@@ -102,15 +102,6 @@ enum : int { kSkip = 0, kContrib = 1, kAmbiguous = 2 };  // pair decision outcom
 #ifndef HGS_FIXUP_MINB
 #define HGS_FIXUP_MINB 3  // CTAs (of 256) per SM the float64 fixup kernels are register-budgeted for
 #endif
-#ifndef HGS_BWD_PPL_KG
-#define HGS_BWD_PPL_KG 2  // pixels per lane of the backward compositor for KG >= 2
-#endif
-#ifndef HGS_BWD_COMPACT
-#define HGS_BWD_COMPACT 1  // contribution-mask backward with lane-compacted pixel work
-#endif
-#ifndef HGS_BWD_PPL1
-#define HGS_BWD_PPL1 2    // pixels per lane of the backward compositor for KG = 1
-#endif
 
 __device__ __forceinline__ bool rec_is3d(const SplatRec &r) { return __float_as_uint(r.r4.w) >> 31; }
 __device__ __forceinline__ uint32_t rec_idx(const SplatRec &r) { return __float_as_uint(r.r4.w) & 0x7fffffffu; }
@@ -568,20 +559,16 @@ __global__ void k_scan_counts(const uint32_t *counts, int64_t m, unsigned long l
 __global__ void k_duplicate(const SplatRec *recs, const unsigned long long *pair_off, int64_t m, int tiles_x,
                             uint32_t *pkeys, uint32_t *pvals, int n_digits, uint32_t *hist);
 __global__ void k_tile_ranges(const uint32_t *skeys, int64_t k, int64_t n_tiles, uint32_t *tile_off);
-template <bool NAIVE, bool COUNT>
-__global__ void k_composite_fwd(CompositeArgs a);
+// Host launchers of the template kernels (each instantiated and launched in
+// its own translation unit).
+cudaError_t launch_composite_fwd(const CompositeArgs &a, int64_t n_tiles, bool naive, bool count, cudaStream_t s);
 __global__ void k_fixup_fwd(CompositeArgs a);
 __global__ void k_pixel_counts(CompositeArgs a, uint32_t *counts);
-template <int KG, bool EXT, int PPL, bool DET>
-__global__ void k_composite_bwd(BwdArgs b);
-template <int KG, bool EXT, bool DET>
-cudaError_t launch_composite_bwd_c(const BwdArgs &b, int64_t n_tiles, cudaStream_t s);
-template <int KG, bool EXT, bool DET>
-__global__ void k_fixup_bwd(BwdArgs b);
+// backward compositor (compacted, or naive) + the float64 fixup of deferred pixels
+cudaError_t launch_composite_bwd(const BwdArgs &b, int kg, int64_t n_tiles, bool ext, bool det, cudaStream_t s);
 __global__ void k_det_reduce(const unsigned long long *keys, const uint32_t *vals, const float *pay, int64_t nrec,
                              int kg, float *acc, float *acc_ext);
-template <int DEG>
-__global__ void k_chain_rule_t(ChainArgs c);
+cudaError_t launch_chain_rule(const ChainArgs &c, int sh_bases, int grid, size_t smem, cudaStream_t s);
 __global__ void k_exchange_scan(int64_t n, const float *log_scale, const uint8_t *type_spec, double theta_e,
                                 float *eranks, ExchangeState *st);
 __global__ void k_exchange_apply(int64_t n, float *log_scale, float *rotation, uint8_t *type_spec, double theta_e);
