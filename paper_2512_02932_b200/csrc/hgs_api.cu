@@ -14,7 +14,7 @@ namespace {
 constexpr int kMaxGrid = 148 * 8;
 
 struct Layout {
-  size_t state, hist_d, off_d, hist_p, off_p, keys_a, keys_b, vals_a, vals_b, lb_sort, lb_scan, recs, recs64, pair_off,
+  size_t state, hist_d, off_d, hist_p, off_p, keys_a, keys_b, vals_a, vals_b, lb_sort, lb_scan, recs, recs64, cull2d, pair_off,
       pk_a, pk_b, pv_a, pv_b, tile_off, pix_T, pix_last, pix_count, fwd_fix, bwd_fix, pix_mask, total;
   size_t small_end;  // [state, small_end) is zeroed at the start of a forward
   size_t lb_sort_bytes, lb_scan_bytes;
@@ -48,6 +48,7 @@ Layout make_layout(int64_t n, int W, int H, int64_t cap) {
   L.vals_b = take(nn * 4);
   L.recs = take(nn * sizeof(SplatRec));
   L.recs64 = take(nn * sizeof(Rec64));
+  L.cull2d = take(nn * 2 * sizeof(float4));
   L.pair_off = take(nn * 8);
   L.tile_off = take((n_tiles + 1) * 4);
   L.pix_T = take((size_t)W * H * 4);
@@ -274,6 +275,7 @@ int hgs_forward(const hgs_scene *scene, const hgs_camera *camera, const hgs_sett
     k_rank_scatter<<<grid_for(m, 256), 256, 0, s>>>(vals_sorted, m, rank_of);
     HGS_LAUNCHED();
     HGS_CUDA(launch_preprocess(sc, cam, mod, rank_of, at<SplatRec>(frame, L.recs), at<Rec64>(frame, L.recs64),
+                               at<float4>(frame, L.cull2d),
                                counts, s));
     HGS_LAUNCHED();
     k_scan_counts<<<(unsigned)ceil_div(m, kScanTile), kScanThreads, 0, s>>>(
@@ -331,6 +333,7 @@ int hgs_forward(const hgs_scene *scene, const hgs_camera *camera, const hgs_sett
   a.fwd_fix = at<FwdFix>(frame, L.fwd_fix);
   a.bwd_fix = at<BwdFix>(frame, L.bwd_fix);
   a.pix_mask = at<uint32_t>(frame, L.pix_mask);
+  a.cull2d = at<float4>(frame, L.cull2d);
   const bool naive = settings->flags & HGS_FLAG_NAIVE, count = settings->flags & HGS_FLAG_COUNT;
   HGS_CUDA(launch_composite_fwd(a, n_tiles, naive, count, s));
   // deferred (float32-ambiguous) pixels, float64-exact; exits at once if none
@@ -360,6 +363,7 @@ static CompositeArgs composite_args_for(const hgs_scene *scene, const hgs_camera
   a.fwd_fix = at<FwdFix>(fr, L.fwd_fix);
   a.bwd_fix = at<BwdFix>(fr, L.bwd_fix);
   a.pix_mask = at<uint32_t>(fr, L.pix_mask);
+  a.cull2d = at<float4>(fr, L.cull2d);
   (void)scene;
   (void)camera;
   return a;

@@ -85,7 +85,8 @@ __global__ void __launch_bounds__(kBlock, HGS_FWD_MINB) k_composite_fwd(Composit
         SplatRec r;
         r.r0 = __ldg(&g->r0); r.r1 = __ldg(&g->r1); r.r2 = __ldg(&g->r2);
         r.r3 = __ldg(&g->r3); r.r4 = __ldg(&g->r4); r.r5 = q;
-        if (!NAIVE && cull_splat(r, pm, wx0, wy0))
+        if (!NAIVE && (HGS_CULL_PRE ? cull_splat_pre(r, a.cull2d + 2 * (size_t)rk, pm, wx0, wy0)
+                                    : cull_splat(r, pm, wx0, wy0)))
           pm = 0u;  // bbox hit, but the 1/255 support misses every covered pixel
         pm &= alive;  // only pixels still compositing
         if (pm) wrec[lane] = r;

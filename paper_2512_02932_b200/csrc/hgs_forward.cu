@@ -97,7 +97,8 @@ __device__ __forceinline__ uint32_t tile_count_of(const int *bb) {
   return tx * ty;
 }
 
-__device__ __forceinline__ void write_record(const ProjD &o, uint32_t idx, SplatRec *__restrict__ rec) {
+__device__ __forceinline__ void write_record(const ProjD &o, uint32_t idx, SplatRec *__restrict__ rec,
+                                             float4 *__restrict__ cull) {
   // anchor pixel = floor(centre), kept within +-2^30 so (ix - ax) stays exact
   double axd = floor(o.ctr[0]), ayd = floor(o.ctr[1]);
   axd = fmin(fmax(axd, -1073741824.0), 1073741824.0);
@@ -128,6 +129,12 @@ __device__ __forceinline__ void write_record(const ProjD &o, uint32_t idx, Splat
   r.r5 = make_int4((int)((uint32_t)x0 | ((uint32_t)y0 << 16)), (int)((uint32_t)x1 | ((uint32_t)y1 << 16)), (int)axd,
                    (int)ayd);
   *rec = r;
+  if (o.typ != 1) {  // the 2D support conic of the compositor's warp cull
+    float4 k0, k1;
+    cull2d_prep(r, k0, k1);
+    cull[0] = k0;
+    cull[1] = k1;
+  }
 }
 
 // Inverse of the depth permutation: rank_of[sorted_idx[r]] = r for the M
@@ -146,7 +153,7 @@ template <int B>
 __global__ void __launch_bounds__(32, HGS_PRE_MINB) k_preprocess(SceneView sc, CamD cam, ModD mod,
                                                    const uint32_t *__restrict__ rank_of,
                                                    SplatRec *__restrict__ recs, Rec64 *__restrict__ recs64,
-                                                   uint32_t *__restrict__ counts) {
+                                                   float4 *__restrict__ cull2d, uint32_t *__restrict__ counts) {
   constexpr int SB = 3 * B, SS = 3 * B + 1;
   __shared__ float s_sh[32 * SS];
   const int lane = threadIdx.x;
@@ -165,21 +172,21 @@ __global__ void __launch_bounds__(32, HGS_PRE_MINB) k_preprocess(SceneView sc, C
     ProjD o;
     project_d<false>(sc, i, cam, mod, o, s_sh + lane * SS);
     bbox_d(o, cam.width, cam.height);
-    write_record(o, (uint32_t)i, recs + r);
+    write_record(o, (uint32_t)i, recs + r, cull2d + 2 * (size_t)r);
     write_rec64(o, recs64 + r);
     counts[r] = tile_count_of(o.bbox);
   }
 }
 // Host launcher (the template is launched from this translation unit).
 cudaError_t launch_preprocess(const SceneView &sc, const CamD &cam, const ModD &mod, const uint32_t *rank_of,
-                              SplatRec *recs, Rec64 *recs64, uint32_t *counts, cudaStream_t s) {
+                              SplatRec *recs, Rec64 *recs64, float4 *cull2d, uint32_t *counts, cudaStream_t s) {
   const int64_t nb = (sc.n + 31) / 32;
   const int g = (int)(nb < 1 ? 1 : (nb > 148 * 48 ? 148 * 48 : nb));  // one warp per CTA
   switch (sc.sh_bases) {
-    case 1: k_preprocess<1><<<g, 32, 0, s>>>(sc, cam, mod, rank_of, recs, recs64, counts); break;
-    case 4: k_preprocess<4><<<g, 32, 0, s>>>(sc, cam, mod, rank_of, recs, recs64, counts); break;
-    case 9: k_preprocess<9><<<g, 32, 0, s>>>(sc, cam, mod, rank_of, recs, recs64, counts); break;
-    default: k_preprocess<16><<<g, 32, 0, s>>>(sc, cam, mod, rank_of, recs, recs64, counts); break;
+    case 1: k_preprocess<1><<<g, 32, 0, s>>>(sc, cam, mod, rank_of, recs, recs64, cull2d, counts); break;
+    case 4: k_preprocess<4><<<g, 32, 0, s>>>(sc, cam, mod, rank_of, recs, recs64, cull2d, counts); break;
+    case 9: k_preprocess<9><<<g, 32, 0, s>>>(sc, cam, mod, rank_of, recs, recs64, cull2d, counts); break;
+    default: k_preprocess<16><<<g, 32, 0, s>>>(sc, cam, mod, rank_of, recs, recs64, cull2d, counts); break;
   }
   return cudaGetLastError();
 }

@@ -76,6 +76,7 @@ struct CompositeArgs {
   // bit e of word mask_word(lo, tile, c) * 256 + pixel-in-tile is set iff
   // tile-list entry lo + 32 c + e contributed to the pixel (not NAIVE)
   uint32_t *pix_mask;
+  const float4 *cull2d;  // per rank, 2 x float4: cull2d_prep of 2D splats
 };
 
 // L2 prefetch of one splat record (96 B: at most two 128-B lines).
@@ -179,27 +180,20 @@ __device__ __forceinline__ float rect_min_quad(float a, float b, float c, float 
 //    well-conditioned ellipse; the cull needs both branches out by a 5%
 //    margin in d, far above the float32 error of the conic, so a pair the
 //    exact evaluation would keep is never culled (degenerate cases keep).
-__device__ __forceinline__ bool cull_2d(const SplatRec &r, uint32_t pm, int wx0, int wy0) {
+// The ray-branch conic depends only on the splat: cull2d_prep normalises it
+// to Qn <= 1, (ca s, cb s, cc s, x0 | y0, valid), once per splat in the
+// preprocess; cull_splat_pre runs the per-warp rectangle test for both types.
+__device__ __forceinline__ void cull2d_prep(const SplatRec &r, float4 &k0, float4 &k1) {
+  k0 = make_float4(0.f, 0.f, 0.f, 0.f);
+  k1 = make_float4(0.f, 0.f, 0.f, 0.f);
   const float dstar = (r.r0.w - kArgMinAlpha) * (1.f / kHalfLog2e);
-  if (dstar < 0.f) return true;  // alpha_eff < 1/255: never contributes
-  const int c0 = __ffs(pm) - 1, c1 = 31 - __clz(pm);
-  const int4 q = r.r5;
-  // covered rectangle of anchor-relative pixel centres
-  const float PX0 = (float)(wx0 + (c0 & 7) - q.z) + 0.5f, PX1 = (float)(wx0 + (c1 & 7) - q.z) + 0.5f;
-  const float PY0 = (float)(wy0 + (c0 >> 3) - q.w) + 0.5f, PY1 = (float)(wy0 + (c1 >> 3) - q.w) + 0.5f;
-  // screen (low-pass) branch: squared distance from the centre to the rectangle
-  const float ex = fmaxf(fmaxf(PX0 - r.r0.x, r.r0.x - PX1), 0.f);
-  const float ey = fmaxf(fmaxf(PY0 - r.r0.y, r.r0.y - PY1), 0.f);
-  if (4.f * (ex * ex + ey * ey) <= fmaf(dstar, 1.05f, 1e-3f)) return false;
-  // ray branch: conic of the disk image
-  const float h00 = r.r1.x, h01 = r.r1.y, h02 = r.r1.z;   // m0' (cols 0, 1, 3)
-  const float h10 = r.r1.w, h11 = r.r2.x, h12 = r.r2.y;   // m1'
-  const float h20 = r.r2.z, h21 = r.r2.w, h22 = r.r3.x;   // m2
-  // A = adj(H): A p = (U1, U2, U3) up to scale
+  if (dstar < 0.f) return;
+  const float h00 = r.r1.x, h01 = r.r1.y, h02 = r.r1.z;
+  const float h10 = r.r1.w, h11 = r.r2.x, h12 = r.r2.y;
+  const float h20 = r.r2.z, h21 = r.r2.w, h22 = r.r3.x;
   const float A00 = h11 * h22 - h12 * h21, A01 = h02 * h21 - h01 * h22, A02 = h01 * h12 - h02 * h11;
   const float A10 = h12 * h20 - h10 * h22, A11 = h00 * h22 - h02 * h20, A12 = h02 * h10 - h00 * h12;
   const float A20 = h10 * h21 - h11 * h20, A21 = h01 * h20 - h00 * h21, A22 = h00 * h11 - h01 * h10;
-  // C = A^T diag(1, 1, -d*) A  (symmetric 3x3)
   auto cij = [&](float a0i, float a1i, float a2i, float a0j, float a1j, float a2j) {
     return fmaf(a0i, a0j, fmaf(a1i, a1j, -dstar * a2i * a2j));
   };
@@ -207,22 +201,53 @@ __device__ __forceinline__ bool cull_2d(const SplatRec &r, uint32_t pm, int wx0,
   const float cc = cij(A01, A11, A21, A01, A11, A21), cd = cij(A00, A10, A20, A02, A12, A22);
   const float ce = cij(A01, A11, A21, A02, A12, A22), cf = cij(A02, A12, A22, A02, A12, A22);
   const float det = ca * cc - cb * cb;
-  // well-conditioned ellipse only: PD quadratic part, axis ratio <= ~30
-  if (!(ca > 0.f) || !(det > 1e-3f * (ca + cc) * (ca + cc) * 0.25f)) return false;
+  if (!(ca > 0.f) || !(det > 1e-3f * (ca + cc) * (ca + cc) * 0.25f)) return;
   const float idet = 1.f / det;
-  const float x0 = (cb * ce - cc * cd) * idet, y0 = (cb * cd - ca * ce) * idet;  // centre
-  const float fp = cf + cd * x0 + ce * y0;  // Q at the centre (< 0: non-empty interior)
-  if (!(fp < -1e-2f * fabsf(cf))) return false;
-  const float s = -1.f / fp;  // normalise: interior is Qn <= 1
-  const float qmin = rect_min_quad(ca * s, cb * s, cc * s, PX0 - x0, PX1 - x0, PY0 - y0, PY1 - y0);
-  return qmin > 1.05f;
+  const float x0 = (cb * ce - cc * cd) * idet, y0 = (cb * cd - ca * ce) * idet;
+  const float fp = cf + cd * x0 + ce * y0;
+  if (!(fp < -1e-2f * fabsf(cf))) return;
+  const float sc = -1.f / fp;
+  k0 = make_float4(ca * sc, cb * sc, cc * sc, x0);
+  k1 = make_float4(y0, 1.f, 0.f, 0.f);
+}
+
+__device__ __forceinline__ bool cull_splat_pre(const SplatRec &r, const float4 *c2, uint32_t pm, int wx0, int wy0) {
+  const float dstar = (r.r0.w - kArgMinAlpha) * (1.f / kHalfLog2e);
+  if (dstar < 0.f) return true;  // alpha_eff < 1/255: never contributes
+  const int c0 = __ffs(pm) - 1, c1 = 31 - __clz(pm);
+  const int4 q = r.r5;
+  const float PX0 = (float)(wx0 + (c0 & 7) - q.z) + 0.5f, PX1 = (float)(wx0 + (c1 & 7) - q.z) + 0.5f;
+  const float PY0 = (float)(wy0 + (c0 >> 3) - q.w) + 0.5f, PY1 = (float)(wy0 + (c1 >> 3) - q.w) + 0.5f;
+  float A, B, C, cx, cy, thr;
+  if (rec_is3d(r)) {
+    A = r.r1.x; B = r.r1.y; C = r.r1.z;
+    cx = r.r0.x; cy = r.r0.y;
+    thr = fmaf(dstar, 1.001f, 1e-3f);
+  } else {
+    const float ex = fmaxf(fmaxf(PX0 - r.r0.x, r.r0.x - PX1), 0.f);
+    const float ey = fmaxf(fmaxf(PY0 - r.r0.y, r.r0.y - PY1), 0.f);
+    if (4.f * (ex * ex + ey * ey) <= fmaf(dstar, 1.05f, 1e-3f)) return false;  // low-pass circle reaches
+    const float4 k0 = c2[0], k1 = c2[1];
+    if (!(k1.y > 0.f)) return false;  // no well-conditioned ray conic: keep
+    A = k0.x; B = k0.y; C = k0.z;
+    cx = k0.w; cy = k1.x;
+    thr = 1.05f;
+  }
+  return rect_min_quad(A, B, C, PX0 - cx, PX1 - cx, PY0 - cy, PY1 - cy) > thr;
 }
 
 #ifndef HGS_CULL_2D
 #define HGS_CULL_2D 1
 #endif
+#ifndef HGS_CULL_PRE
+#define HGS_CULL_PRE 1
+#endif
 __device__ __forceinline__ bool cull_splat(const SplatRec &r, uint32_t pm, int wx0, int wy0) {
-  return rec_is3d(r) ? cull_3d(r, pm, wx0, wy0) : (HGS_CULL_2D && cull_2d(r, pm, wx0, wy0));
+  if (rec_is3d(r)) return cull_3d(r, pm, wx0, wy0);
+  if (!HGS_CULL_2D) return false;
+  float4 k[2];
+  cull2d_prep(r, k[0], k[1]);  // per warp instead of once per splat (HGS_CULL_PRE = 0)
+  return cull_splat_pre(r, k, pm, wx0, wy0);
 }
 
 // bbox overlaps the pixel rectangle [rx0, rx1] x [ry0, ry1]
@@ -553,7 +578,7 @@ __global__ void k_depth_keys(SceneView sc, CamD cam, unsigned long long *keys, u
                              FrameState *st);
 __global__ void k_rank_scatter(const uint32_t *sorted_idx, int64_t m, uint32_t *rank_of);
 cudaError_t launch_preprocess(const SceneView &sc, const CamD &cam, const ModD &mod, const uint32_t *rank_of,
-                              SplatRec *recs, Rec64 *recs64, uint32_t *counts, cudaStream_t s);
+                              SplatRec *recs, Rec64 *recs64, float4 *cull2d, uint32_t *counts, cudaStream_t s);
 __global__ void k_scan_counts(const uint32_t *counts, int64_t m, unsigned long long *pair_off,
                               unsigned long long *scan_lb, FrameState *st);
 __global__ void k_duplicate(const SplatRec *recs, const unsigned long long *pair_off, int64_t m, int tiles_x,
