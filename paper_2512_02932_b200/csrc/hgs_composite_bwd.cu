@@ -484,6 +484,7 @@ __global__ void __launch_bounds__(256 / QP, HGS_BWDC_MINB(KG, EXT, QP)) k_compos
       SplatRec r;
       r.r0 = __ldg(&g->r0); r.r1 = __ldg(&g->r1); r.r2 = __ldg(&g->r2);
       r.r3 = __ldg(&g->r3); r.r4 = __ldg(&g->r4); r.r5 = __ldg(&g->r5);
+      if (HGS_STAGED_ORIGIN) stage_block_origin(r, wx0, wy0);
       wrec[lane] = r;
     }
     __syncwarp();
@@ -533,7 +534,9 @@ __global__ void __launch_bounds__(256 / QP, HGS_BWDC_MINB(KG, EXT, QP)) k_compos
           const float4 A = cs.a[p];
           PairEval pe;
           if (count) ++n_ev;
-          const int c = eval_fast<true, true>(r, ix, iy, a.flags, pe);
+          const int c = HGS_STAGED_ORIGIN
+                            ? eval_fast<true, true, true>(r, ix, iy, a.flags, pe, (float)(p & 7), (float)(p >> 3))
+                            : eval_fast<true, true>(r, ix, iy, a.flags, pe);
           if (c == kAmbiguous) {
             const float4 E = EXT ? cs.e[p] : make_float4(0.f, 0.f, 0.f, 0.f);
             BwdFix f;

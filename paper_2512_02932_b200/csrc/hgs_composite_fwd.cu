@@ -39,6 +39,7 @@ __global__ void __launch_bounds__(kBlock, HGS_FWD_MINB) k_composite_fwd(Composit
   const int ix = wx0 + (lane & 7), iy = wy0 + (lane >> 3);
   const bool inside = ix < a.width && iy < a.height;
   const uint32_t lane_bit = 1u << lane;
+  const float lox = (float)(lane & 7), loy = (float)(lane >> 3);  // offset in the warp block
   const bool exact = HGS_EXACT_ENABLED && !(a.flags & HGS_FLAG_FAST);
   uint32_t lo, hi;
   if (NAIVE) {
@@ -89,6 +90,7 @@ __global__ void __launch_bounds__(kBlock, HGS_FWD_MINB) k_composite_fwd(Composit
                                     : cull_splat(r, pm, wx0, wy0)))
           pm = 0u;  // bbox hit, but the 1/255 support misses every covered pixel
         pm &= alive;  // only pixels still compositing
+        if (HGS_STAGED_ORIGIN && !NAIVE) stage_block_origin(r, wx0, wy0);
         if (pm) wrec[lane] = r;
       }
     }
@@ -118,7 +120,8 @@ __global__ void __launch_bounds__(kBlock, HGS_FWD_MINB) k_composite_fwd(Composit
       const bool is3d = rec_is3d(r);
       if (COUNT) (is3d ? n_ev3 : n_ev2) += 1;
       PairEval p;
-      const int c = eval_fast<false>(r, ix, iy, a.flags, p);
+      const int c = (HGS_STAGED_ORIGIN && !NAIVE) ? eval_fast<false, false, true>(r, ix, iy, a.flags, p, lox, loy)
+                                                  : eval_fast<false>(r, ix, iy, a.flags, p);
       if (c == kSkip) continue;
 #if HGS_FWD_ONE_DEFER
       // one deferral site (the pair's decision or the early-stop decision), so

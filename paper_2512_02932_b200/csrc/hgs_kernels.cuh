@@ -242,12 +242,22 @@ __device__ __forceinline__ bool cull_splat_pre(const SplatRec &r, const float4 *
 #ifndef HGS_CULL_PRE
 #define HGS_CULL_PRE 1
 #endif
+#ifndef HGS_STAGED_ORIGIN
+#define HGS_STAGED_ORIGIN 1  // compositors stage records with the float block origin
+#endif
 __device__ __forceinline__ bool cull_splat(const SplatRec &r, uint32_t pm, int wx0, int wy0) {
   if (rec_is3d(r)) return cull_3d(r, pm, wx0, wy0);
   if (!HGS_CULL_2D) return false;
   float4 k[2];
   cull2d_prep(r, k[0], k[1]);  // per warp instead of once per splat (HGS_CULL_PRE = 0)
   return cull_splat_pre(r, k, pm, wx0, wy0);
+}
+
+// Staged-record form of the anchor (see eval_fast<..., STAGED>): exact while
+// |wx0 - ax| < 2^22, i.e. for every pixel within 4M pixels of the anchor.
+__device__ __forceinline__ void stage_block_origin(SplatRec &r, int wx0, int wy0) {
+  r.r5.z = __float_as_int(__fadd_rn((float)(wx0 - r.r5.z), 0.5f));
+  r.r5.w = __float_as_int(__fadd_rn((float)(wy0 - r.r5.w), 0.5f));
 }
 
 // bbox overlaps the pixel rectangle [rx0, rx1] x [ry0, ry1]
@@ -427,10 +437,22 @@ static __device__ __noinline__ Resolved resolve_pair(const SplatRec *rp, int ix,
 // KNOWN (backward with contribution masks): the forward already decided,
 // exactly, that the pair contributes -- only the backward-only decisions
 // (clamp, ray branch, degenerate solve) are checked.
-template <bool BWD, bool KNOWN = false>
-__device__ __forceinline__ int eval_fast(const SplatRec &r, int ix, int iy, uint32_t flags, PairEval &p) {
+// STAGED: r is a compositor's shared-memory copy whose r5.z / r5.w hold the
+// float anchor-relative centre of the warp block's first pixel,
+// (wx0 - ax) + 0.5 (stage_block_origin), and (ox, oy) is the pixel's offset
+// in the block: pxl = that + ox is the same exact value as (ix - ax) + 0.5.
+template <bool BWD, bool KNOWN = false, bool STAGED = false>
+__device__ __forceinline__ int eval_fast(const SplatRec &r, int ix, int iy, uint32_t flags, PairEval &p,
+                                         float ox = 0.f, float oy = 0.f) {
   Geom g;
-  geom_common(r, ix, iy, g);
+  if (STAGED) {
+    g.pxl = __fadd_rn(__int_as_float(r.r5.z), ox);
+    g.pyl = __fadd_rn(__int_as_float(r.r5.w), oy);
+    g.dx = __fsub_rn(g.pxl, r.r0.x);
+    g.dy = __fsub_rn(g.pyl, r.r0.y);
+  } else {
+    geom_common(r, ix, iy, g);
+  }
   p.dx = g.dx;
   p.dy = g.dy;
   p.pxl = g.pxl;
