@@ -4,6 +4,9 @@
 // raster/_blend_py.py:55-123 (paths relative to the reference package).
 #include "hgs_kernels.cuh"
 
+#ifndef HGS_PRE_ASYNC
+#define HGS_PRE_ASYNC 1
+#endif
 #ifndef HGS_PRE_MINB
 #define HGS_PRE_MINB 1  // one-warp CTAs per SM the float64 preprocess is register-budgeted for
 #endif
@@ -155,8 +158,38 @@ __global__ void __launch_bounds__(32, HGS_PRE_MINB) k_preprocess(SceneView sc, C
                                                    SplatRec *__restrict__ recs, Rec64 *__restrict__ recs64,
                                                    float4 *__restrict__ cull2d, uint32_t *__restrict__ counts) {
   constexpr int SB = 3 * B, SS = 3 * B + 1;
-  __shared__ float s_sh[32 * SS];
   const int lane = threadIdx.x;
+#if HGS_PRE_ASYNC
+  // double-buffered SH staging: the next warp step's rows are in flight
+  // (cp.async, no registers) while this step's float64 projection runs
+  __shared__ float s_buf[2][32 * SS];
+  const int64_t stride = (int64_t)gridDim.x * 32;
+  auto stage = [&](int64_t b0, float *dst) {
+    const int c = (int)(sc.n - b0 < 32 ? sc.n - b0 : 32);
+    const float *src = sc.sh + b0 * SB;
+    for (int e = lane; e < c * SB; e += 32) {
+      const int r = e / SB;
+      const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst + r * SS + (e - r * SB));
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(src + e) : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  int buf = 0;
+  if ((int64_t)blockIdx.x * 32 < sc.n) stage((int64_t)blockIdx.x * 32, s_buf[0]);
+  for (int64_t base = (int64_t)blockIdx.x * 32; base < sc.n; base += stride) {
+    const int cnt = (int)(sc.n - base < 32 ? sc.n - base : 32);
+    __syncwarp();  // every lane is done with the buffer the next copy overwrites
+    if (base + stride < sc.n) {
+      stage(base + stride, s_buf[buf ^ 1]);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
+    __syncwarp();
+    const float *s_sh = s_buf[buf];
+    buf ^= 1;
+#else
+  __shared__ float s_sh[32 * SS];
   for (int64_t base = (int64_t)blockIdx.x * 32; base < sc.n; base += (int64_t)gridDim.x * 32) {
     const int cnt = (int)(sc.n - base < 32 ? sc.n - base : 32);
     __syncwarp();
@@ -165,6 +198,7 @@ __global__ void __launch_bounds__(32, HGS_PRE_MINB) k_preprocess(SceneView sc, C
       s_sh[r * SS + (e - r * SB)] = __ldg(sc.sh + base * SB + e);
     }
     __syncwarp();
+#endif
     const int64_t i = base + lane;
     if (lane >= cnt) continue;
     const uint32_t r = rank_of[i];
