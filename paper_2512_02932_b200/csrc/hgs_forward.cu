@@ -4,6 +4,9 @@
 // raster/_blend_py.py:55-123 (paths relative to the reference package).
 #include "hgs_kernels.cuh"
 
+#ifndef HGS_PRE_PREFETCH
+#define HGS_PRE_PREFETCH 1
+#endif
 #ifndef HGS_PRE_ASYNC
 #define HGS_PRE_ASYNC 1
 #endif
@@ -181,6 +184,19 @@ __global__ void __launch_bounds__(32, HGS_PRE_MINB) k_preprocess(SceneView sc, C
     __syncwarp();  // every lane is done with the buffer the next copy overwrites
     if (base + stride < sc.n) {
       stage(base + stride, s_buf[buf ^ 1]);
+#if HGS_PRE_PREFETCH
+      {  // the next step's scalar fields into L1: 13 lines, one per lane
+        const int64_t nb = base + stride;
+        const char *ptr = nullptr;
+        if (lane < 3) ptr = reinterpret_cast<const char *>(sc.center + 3 * nb) + 128 * lane;
+        else if (lane < 6) ptr = reinterpret_cast<const char *>(sc.log_scale + 3 * nb) + 128 * (lane - 3);
+        else if (lane < 10) ptr = reinterpret_cast<const char *>(sc.rotation + 4 * nb) + 128 * (lane - 6);
+        else if (lane == 10) ptr = reinterpret_cast<const char *>(sc.opacity_logit + nb);
+        else if (lane == 11) ptr = reinterpret_cast<const char *>(sc.type_spec + nb);
+        else if (lane == 12) ptr = reinterpret_cast<const char *>(rank_of + nb);
+        if (ptr) asm volatile("prefetch.global.L1 [%0];" ::"l"(ptr));
+      }
+#endif
       asm volatile("cp.async.wait_group 1;" ::: "memory");
     } else {
       asm volatile("cp.async.wait_group 0;" ::: "memory");
