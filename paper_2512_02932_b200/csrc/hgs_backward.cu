@@ -98,6 +98,9 @@ __device__ __forceinline__ float clamp_mask(const float *shc_ch, const float *ba
 // Gaussians with an all-zero accumulator (culled or never composited) get
 // exactly zero gradients (the chain rule is linear).
 constexpr int kChainThreads = 32;
+#ifndef HGS_CHAIN_PREFETCH
+#define HGS_CHAIN_PREFETCH 1
+#endif
 #ifndef HGS_CHAIN_MINB
 #define HGS_CHAIN_MINB 16  // 16 warps per SM: 128 registers
 #endif
@@ -118,6 +121,27 @@ __global__ void __launch_bounds__(kChainThreads, HGS_CHAIN_MINB) k_chain_rule_t(
       const int r = e / SB;
       s_in[r * SS + (e - r * SB)] = __ldg(c.sc.sh + base * SB + e);
     }
+#if HGS_CHAIN_PREFETCH
+    {  // next warp step's SH rows, accumulators and scalar fields into L2
+      const int64_t nb = base + (int64_t)gridDim.x * kChainThreads;
+      if (nb < n && c.kg == 1) {  // (measured: a net loss for the 3-gradient training step)
+        const int nc = (int)(n - nb < kChainThreads ? n - nb : kChainThreads);
+        const char *sh0 = reinterpret_cast<const char *>(c.sc.sh + nb * SB);
+        for (int l = lane; l * 128 < nc * SB * 4; l += kChainThreads)
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(sh0 + 128 * l));
+        const char *ac0 = reinterpret_cast<const char *>(c.acc + nb * c.kg * kAcc);
+        for (int l = lane; l * 128 < nc * c.kg * kAcc * 4; l += kChainThreads)
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(ac0 + 128 * l));
+        const char *ptr = nullptr;
+        if (lane < 3) ptr = reinterpret_cast<const char *>(c.sc.center + 3 * nb) + 128 * lane;
+        else if (lane < 6) ptr = reinterpret_cast<const char *>(c.sc.log_scale + 3 * nb) + 128 * (lane - 3);
+        else if (lane < 10) ptr = reinterpret_cast<const char *>(c.sc.rotation + 4 * nb) + 128 * (lane - 6);
+        else if (lane == 10) ptr = reinterpret_cast<const char *>(c.sc.opacity_logit + nb);
+        else if (lane == 11) ptr = reinterpret_cast<const char *>(c.sc.type_spec + nb);
+        if (ptr) asm volatile("prefetch.global.L2 [%0];" ::"l"(ptr));
+      }
+    }
+#endif
     __syncwarp();
     const int64_t i = base + lane;
     const bool valid = lane < cnt;
