@@ -46,6 +46,9 @@ __host__ __device__ constexpr int field_width(int f, int B) { return f < 2 ? 3 :
 __host__ __device__ constexpr int field_j0(int f) { return f == 0 ? 0 : (f == 1 ? 3 : (f == 2 ? 6 : (f == 3 ? 10 : 11))); }
 __device__ __forceinline__ int64_t field_off(int f, int64_t n) { return (int64_t)field_j0(f) * n; }
 
+#ifndef HGS_OPT_ZERO_FAST
+#define HGS_OPT_ZERO_FAST 1
+#endif
 #ifndef HGS_OPT_MINB
 #define HGS_OPT_MINB 4  // 4 CTAs x 256 threads per SM: 64 registers
 #endif
@@ -174,8 +177,16 @@ __global__ void __launch_bounds__(kOThreads, HGS_OPT_MINB) k_optim(OptArgs a) {
         float m = mv[u], v = vv[u];
         m = fmaf(1.f - a.beta1, grad - m, m);                // exp_avg.lerp_(grad, 1 - beta1)
         v = fmaf(1.f - a.beta2, grad * grad, v * a.beta2);   // exp_avg_sq.mul_(beta2).addcmul_(g, g, 1 - beta2)
+#if HGS_OPT_ZERO_FAST
+        // zero moments (untouched Gaussians) bypass the IEEE division and
+        // square root, whose slow paths they would take: same results
+        // (0 / x = 0, sqrt(0) / b = 0), far fewer instructions
+        const float denom = (v == 0.f ? 0.f : sqrtf(v) / a.bc2_sqrt) + a.eps;
+        const float pn = m == 0.f ? pv[u] : pv[u] - step * (m / denom);
+#else
         const float denom = sqrtf(v) / a.bc2_sqrt + a.eps;
         const float pn = pv[u] - step * (m / denom);
+#endif
         __stcs(mf + e, m);
         __stcs(vf + e, v);
         if (f == 2)
