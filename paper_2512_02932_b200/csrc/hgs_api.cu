@@ -311,7 +311,7 @@ int hgs_forward(const hgs_scene *scene, const hgs_camera *camera, const hgs_sett
     info->internal[0] = in_b ? 1u : 0u;
     info->internal[3] = (uint32_t)nd;  // tile-sort passes
   }
-  k_tile_ranges<<<(unsigned)std::max<int64_t>(1, ceil_div(std::max<int64_t>(K, n_tiles + 1), 256)), 256, 0, s>>>(
+  k_tile_ranges<<<grid_for(ceil_div(std::max<int64_t>(K, n_tiles + 1), 4), 256), 256, 0, s>>>(
       tile_keys, K, n_tiles, at<uint32_t>(frame, L.tile_off));
   HGS_LAUNCHED();
   HGS_CUDA(record_event(settings, 3, s));

@@ -276,7 +276,13 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_counts(const uint32_t *__
 
 // ------------------------------------------------------------ duplicate
 // Emit (tile id, rank) pairs in rank order at the scanned offsets and build
-// the tile-id digit histograms for the pair sort.
+// the tile-id digit histograms for the pair sort.  A lane emits the pairs of
+// its own splat when it has at most kDupOwn of them; the warp emits the
+// pairs of larger splats together, one splat at a time (a full-screen 2D
+// surfel has 8160 pairs at 1080p: one thread looping over them was the
+// kernel's whole duration).
+constexpr int kDupOwn = 32;
+
 __global__ void __launch_bounds__(256) k_duplicate(const SplatRec *__restrict__ recs,
                                                    const unsigned long long *__restrict__ pair_off, int64_t m,
                                                    int tiles_x, uint32_t *__restrict__ pkeys,
@@ -285,21 +291,49 @@ __global__ void __launch_bounds__(256) k_duplicate(const SplatRec *__restrict__ 
   __shared__ uint32_t sh[2 * kRadix];
   for (int i = threadIdx.x; i < 2 * kRadix; i += blockDim.x) sh[i] = 0;
   __syncthreads();
-  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < m; r += (int64_t)gridDim.x * blockDim.x) {
-    int4 q = recs[r].r5;
-    int x0 = q.x & 0xffff, y0 = (int)((uint32_t)q.x >> 16), x1 = q.y & 0xffff, y1 = (int)((uint32_t)q.y >> 16);
-    if (x1 < x0) continue;
-    unsigned long long o = pair_off[r];
-    int tx0 = x0 / kTile, tx1 = x1 / kTile, ty0 = y0 / kTile, ty1 = y1 / kTile;
-    for (int ty = ty0; ty <= ty1; ++ty)
-      for (int tx = tx0; tx <= tx1; ++tx) {
-        uint32_t t = (uint32_t)(ty * tiles_x + tx);
-        pkeys[o] = t;
-        pvals[o] = (uint32_t)r;
-        ++o;
-        atomicAdd(&sh[t & 0xff], 1u);
-        if (n_digits > 1) atomicAdd(&sh[kRadix + ((t >> 8) & 0xff)], 1u);
+  const int lane = threadIdx.x & 31;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  auto emit = [&](uint32_t t, unsigned long long o, uint32_t r) {
+    pkeys[o] = t;
+    pvals[o] = r;
+    atomicAdd(&sh[t & 0xff], 1u);
+    if (n_digits > 1) atomicAdd(&sh[kRadix + ((t >> 8) & 0xff)], 1u);
+  };
+  // warp-aligned grid stride: the loop condition is warp-uniform
+  for (int64_t r0 = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); r0 < m; r0 += stride) {
+    const int64_t r = r0 + lane;
+    int tx0 = 0, ty0 = 0, bw = 1;
+    uint32_t cnt = 0;
+    unsigned long long o = 0;
+    if (r < m) {
+      const int4 q = recs[r].r5;
+      const int x0 = q.x & 0xffff, y0 = (int)((uint32_t)q.x >> 16), x1 = q.y & 0xffff, y1 = (int)((uint32_t)q.y >> 16);
+      if (x1 >= x0) {
+        tx0 = x0 / kTile; ty0 = y0 / kTile;
+        bw = x1 / kTile - tx0 + 1;
+        cnt = (uint32_t)(bw * (y1 / kTile - ty0 + 1));
+        o = pair_off[r];
       }
+    }
+    if (cnt <= (uint32_t)kDupOwn) {
+      for (uint32_t j = 0, dy = 0, dx = 0; j < cnt; ++j) {  // row-major over the tile rectangle
+        emit((uint32_t)((ty0 + (int)dy) * tiles_x + tx0 + (int)dx), o + j, (uint32_t)r);
+        if (++dx == (uint32_t)bw) { dx = 0; ++dy; }
+      }
+    }
+    uint32_t big = __ballot_sync(0xffffffffu, cnt > (uint32_t)kDupOwn);
+    while (big) {
+      const int l = __ffs(big) - 1;
+      big &= big - 1;
+      const uint32_t c = __shfl_sync(0xffffffffu, cnt, l);
+      const unsigned long long ob = __shfl_sync(0xffffffffu, o, l);
+      const int bx = __shfl_sync(0xffffffffu, tx0, l), by = __shfl_sync(0xffffffffu, ty0, l);
+      const int w = __shfl_sync(0xffffffffu, bw, l);
+      for (uint32_t j = lane; j < c; j += 32) {
+        const uint32_t dy = j / (uint32_t)w, dx = j - dy * (uint32_t)w;
+        emit((uint32_t)((by + (int)dy) * tiles_x + bx + (int)dx), ob + j, (uint32_t)(r0 + l));
+      }
+    }
   }
   __syncthreads();
   for (int i = threadIdx.x; i < n_digits * kRadix; i += blockDim.x)
@@ -307,19 +341,37 @@ __global__ void __launch_bounds__(256) k_duplicate(const SplatRec *__restrict__ 
 }
 
 // tile_offsets (n_tiles + 1) from the tile-sorted keys (project.py:344-345).
-__global__ void k_tile_ranges(const uint32_t *__restrict__ skeys, int64_t k, int64_t n_tiles,
-                              uint32_t *__restrict__ tile_off) {
-  int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+// Four keys per thread (one 16-byte load), grid-stride.
+__global__ void __launch_bounds__(256) k_tile_ranges(const uint32_t *__restrict__ skeys, int64_t k, int64_t n_tiles,
+                                                     uint32_t *__restrict__ tile_off) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (k == 0) {
-    for (int64_t t = p; t <= n_tiles; t += (int64_t)gridDim.x * blockDim.x) tile_off[t] = 0;
+    for (int64_t t = tid; t <= n_tiles; t += stride) tile_off[t] = 0;
     return;
   }
-  if (p >= k) return;
-  int64_t t = skeys[p];
-  int64_t prev = p ? (int64_t)skeys[p - 1] : -1;
-  for (int64_t tt = prev + 1; tt <= t; ++tt) tile_off[tt] = (uint32_t)p;
-  if (p == k - 1)
-    for (int64_t tt = t + 1; tt <= n_tiles; ++tt) tile_off[tt] = (uint32_t)k;
+  const bool vec = ((uintptr_t)skeys & 15u) == 0;
+  for (int64_t p0 = tid * 4; p0 < k; p0 += stride * 4) {
+    uint32_t v[4];
+    if (vec && p0 + 4 <= k) {
+      const uint4 q = *reinterpret_cast<const uint4 *>(skeys + p0);
+      v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
+    } else {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) v[i] = p0 + i < k ? skeys[p0 + i] : 0u;
+    }
+    int64_t prev = p0 ? (int64_t)skeys[p0 - 1] : -1;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int64_t p = p0 + i;
+      if (p >= k) break;
+      const int64_t t = v[i];
+      for (int64_t tt = prev + 1; tt <= t; ++tt) tile_off[tt] = (uint32_t)p;
+      if (p == k - 1)
+        for (int64_t tt = t + 1; tt <= n_tiles; ++tt) tile_off[tt] = (uint32_t)k;
+      prev = t;
+    }
+  }
 }
 
 // -------------------------------------------------------------- composite
