@@ -92,6 +92,8 @@ typedef struct hgs_settings {
 #define HGS_FLAG_DETERMINISTIC 0x8u /* backward: fixed-order (sorted-record) gradient reduction instead of
                                      * float atomics -- bitwise reproducible; needs the
                                      * scratch of hgs_backward_det_scratch_bytes */
+#define HGS_FLAG_DEFER_ALL 0x10u /* tests: with HGS_FLAG_COUNT, defer every pixel of the forward to the float64
+                                    resume kernel (exercises the deferred-pixel path on a whole image) */
 
 /* Output images (device, row-major).  Any of normal / alpha may be NULL. */
 typedef struct hgs_images {

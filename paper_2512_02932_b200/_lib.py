@@ -25,6 +25,7 @@ HGS_FLAG_NAIVE = 0x1
 HGS_FLAG_FAST = 0x2
 HGS_FLAG_COUNT = 0x4
 HGS_FLAG_DETERMINISTIC = 0x8
+HGS_FLAG_DEFER_ALL = 0x10  # tests: with HGS_FLAG_COUNT, every pixel goes through the float64 resume kernel
 
 # hgs_train.h constants
 HGS_LOSS_L1, HGS_LOSS_SSIM, HGS_LOSS_LOW, HGS_LOSS_HIGH, HGS_LOSS_COLOR = range(5)

@@ -20,7 +20,10 @@ namespace hgs {
 
 constexpr int kTile = 16;
 constexpr int kBlock = kTile * kTile;  // one thread per pixel of a tile
-constexpr int kFixupBlocks = 148 * 4;       // persistent fixup grids (one warp per deferred pixel)
+#ifndef HGS_FIXUP_BLOCKS
+#define HGS_FIXUP_BLOCKS (148 * 4)
+#endif
+constexpr int kFixupBlocks = HGS_FIXUP_BLOCKS;     // persistent fixup grids (one warp per deferred pixel)
 constexpr double kAlphaClamp = 0.99;   // raster/project.py:20
 constexpr double kMinAlpha = 1.0 / 255.0;
 constexpr double kEarlyStopT = 1e-4;

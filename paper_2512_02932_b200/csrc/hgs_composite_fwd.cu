@@ -41,6 +41,7 @@ __global__ void __launch_bounds__(kBlock, HGS_FWD_MINB) k_composite_fwd(Composit
   const uint32_t lane_bit = 1u << lane;
   const float lox = (float)(lane & 7), loy = (float)(lane >> 3);  // offset in the warp block
   const bool exact = HGS_EXACT_ENABLED && !(a.flags & HGS_FLAG_FAST);
+  const bool stress = COUNT && !NAIVE && (a.flags & HGS_FLAG_DEFER_ALL);
   uint32_t lo, hi;
   if (NAIVE) {
     lo = 0;
@@ -127,10 +128,14 @@ __global__ void __launch_bounds__(kBlock, HGS_FWD_MINB) k_composite_fwd(Composit
       // one deferral site (the pair's decision or the early-stop decision), so
       // the worklist address is formed only on that rare path
       uint32_t dmode = 2u;
-      if (c == kAmbiguous) {
-        if (COUNT) atomicAdd(&a.st->diag[is3d ? 12 : 13], 1ull);  // deferral reasons
+      // HGS_FLAG_DEFER_ALL (tests, counting instantiation only): every pixel is
+      // deferred at its first contribution, even pixels before it (mode 0),
+      // odd pixels after it (mode 1), so the whole image goes through k_fixup_fwd
+      if (c == kAmbiguous || (stress && last == 0u && !(pix & 1u))) {
+        if (COUNT && c == kAmbiguous) atomicAdd(&a.st->diag[is3d ? 12 : 13], 1ull);  // deferral reasons
         dmode = 0u;
       } else {
+        if (stress && last == 0u) dmode = 1u;
 #else
       if (c == kAmbiguous) {
         if (COUNT) atomicAdd(&a.st->diag[is3d ? 12 : 13], 1ull);  // deferral reasons
@@ -244,12 +249,26 @@ __device__ __forceinline__ float warp_sum(float x) {
   return x;
 }
 
+#ifndef HGS_FIXUP_E
+#define HGS_FIXUP_E 4  // tile-list entries per lane per window of k_fixup_fwd
+#endif
+
 // Deferred pixels, one warp each (grid-stride over the worklist).  The warp
-// evaluates 32 consecutive tile-list entries in parallel with the exact
-// decisions (float64 re-evaluation where the float32 bound is ambiguous),
-// forms the transmittance with a product scan, resolves the early stop in
-// lane order (float64 replay near the threshold) and accumulates.
+// evaluates a window of 32 x E consecutive tile-list entries in parallel with
+// the exact decisions (float64 re-evaluation where the float32 bound is
+// ambiguous): lane l owns entries E l .. E l + E - 1 of the window, forms
+// their transmittance with a lane-local product and a warp product scan,
+// resolves the early stop in entry order (float64 replay near the
+// threshold) and accumulates lane-local partial sums, reduced once at the
+// end.  Windows are aligned to the forward's 32-entry chunks, so each window
+// writes E whole contribution-mask words.  The walk of a pixel is a serial
+// chain of windows (the kernel's duration is the longest one): E entries per
+// lane make it E times shorter.
 __global__ void __launch_bounds__(256, HGS_FIXUP_MINB) k_fixup_fwd(CompositeArgs a) {
+  constexpr int E = HGS_FIXUP_E;
+  constexpr uint32_t WIN = 32u * E;
+  constexpr int LPC = 32 / E;  // lanes per 32-entry chunk
+  static_assert(E == 1 || E == 2 || E == 4, "E divides 32");
   const uint32_t nfix = a.st->n_fix_fwd;
   const int lane = threadIdx.x & 31;
   const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
@@ -261,7 +280,8 @@ __global__ void __launch_bounds__(256, HGS_FIXUP_MINB) k_fixup_fwd(CompositeArgs
     const int tile = (iy / kTile) * a.tiles_x + ix / kTile;
     const uint32_t lo = naive ? 0u : a.tile_off[tile];
     const uint32_t hi = naive ? (uint32_t)a.m : a.tile_off[tile + 1];
-    float T = f.T, c0 = f.c0, c1 = f.c1, c2 = f.c2, dep = f.dep, n0 = f.n0, n1 = f.n1, n2 = f.n2;
+    float T = f.T;
+    float q0 = 0.f, q1 = 0.f, q2 = 0.f, qd = 0.f, qn0 = 0.f, qn1 = 0.f, qn2 = 0.f;  // lane partial sums
     uint32_t cnt = f.cnt, last = f.last;
     bool stopped = false;
     uint32_t start = f.entry;
@@ -269,89 +289,135 @@ __global__ void __launch_bounds__(256, HGS_FIXUP_MINB) k_fixup_fwd(CompositeArgs
       stopped = replay_T_below(a.recs, a.tile_vals, a.flags, a.st, lo, f.entry, ix, iy);
       start = f.entry + 1u;
     }
-    // contribution-mask words from the resume point on (the main kernel wrote
-    // the deferral chunk's bits before the resume point)
     const uint32_t pit = (uint32_t)((iy & (kTile - 1)) * kTile + (ix & (kTile - 1)));
-    uint32_t w_cur = (start - lo) >> 5;
-    uint32_t cur = (!naive && w_cur == ((f.entry - lo) >> 5)) ? a.pix_mask[mask_word(lo, tile, w_cur, pit)] : 0u;
-    // software pipeline: the next window's ranks are loaded and its records
-    // prefetched into L2 while this window is evaluated
-    uint32_t rk_next = start + lane < hi ? (naive ? start + lane : a.tile_vals[start + lane]) : 0u;
-    for (uint32_t base = start; base < hi && !stopped; base += 32) {
-      const uint32_t e = base + lane;
-      const uint32_t rk_cur = rk_next;
-      if (base + 32 + lane < hi) {
-        rk_next = naive ? base + 32 + lane : a.tile_vals[base + 32 + lane];
-        prefetch_rec(a.recs + rk_next);
-      }
-      bool con = false;
-      float at = 0.f;
-      SplatRec r;
-      if (e < hi) {
-        const uint32_t rk = rk_cur;
-        r = a.recs[rk];
-        if (naive || in_bbox(r.r5, ix, iy)) {
-          PairEval p;
-          con = eval_pair<false>(r, a.recs + rk, ix, iy, a.flags, a.st, p);
-          at = p.at;
+    const uint32_t n_chunks = (hi - lo + 31u) >> 5;  // words past the list belong to the next tile
+    // the main kernel wrote the bits before the resume point of the deferral chunk
+    const uint32_t c_start = (start - lo) >> 5;
+    const uint32_t stored =
+        (!naive && !stopped && c_start == ((f.entry - lo) >> 5)) ? a.pix_mask[mask_word(lo, tile, c_start, pit)] : 0u;
+    uint32_t n_win = 0;  // HGS_FLAG_COUNT: windows walked (diag 15 = the longest walk)
+    for (uint32_t base = lo + (c_start << 5); base < hi && !stopped; base += WIN) {
+      ++n_win;
+      float at[E], Pi[E];
+      uint32_t rks[E];
+      uint32_t conm = 0u;
+      float P = 1.f;
+#pragma unroll
+      for (int i = 0; i < E; ++i) {
+        const uint32_t e = base + (uint32_t)(E * lane + i);
+        at[i] = 0.f;
+        rks[i] = 0u;
+        if (e >= start && e < hi) {
+          const uint32_t rk = naive ? e : a.tile_vals[e];
+          rks[i] = rk;
+          const SplatRec r = a.recs[rk];
+          if (naive || in_bbox(r.r5, ix, iy)) {
+            PairEval p;
+            if (eval_pair<false>(r, a.recs + rk, ix, iy, a.flags, a.st, p)) {
+              conm |= 1u << i;
+              at[i] = p.at;
+            }
+          }
         }
+        P *= 1.f - at[i];  // at = 0 for non-contributing entries
+        Pi[i] = P;
       }
-      const float om = con ? 1.f - at : 1.f;
-      float P = om;  // inclusive product scan in lane (= entry) order
+      float S = P;  // inclusive product scan of the lane products, in entry order
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
-        const float y = __shfl_up_sync(0xffffffffu, P, o);
-        if (lane >= o) P *= y;
+        const float y = __shfl_up_sync(0xffffffffu, S, o);
+        if (lane >= o) S *= y;
       }
-      float Pex = __shfl_up_sync(0xffffffffu, P, 1);
-      if (lane == 0) Pex = 1.f;
-      const float Tb = T * Pex, Ta = T * P;
-      // early stop, in lane order: clear float32 decisions first, then the
-      // near-threshold lanes (warp-cooperative float64 replay) before them
-      const bool near = con && fabsf(Ta - thr) <= 2e-5f * thr;
-      const uint32_t clear_stop = __ballot_sync(0xffffffffu, con && !near && Ta < thr);
-      uint32_t near_mask = __ballot_sync(0xffffffffu, near);
-      int first = clear_stop ? __ffs(clear_stop) - 1 : 32;
-      while (near_mask) {
-        const int l = __ffs(near_mask) - 1;
-        if (l > first) break;
-        near_mask &= near_mask - 1;
-        const uint32_t el = __shfl_sync(0xffffffffu, e, l);
-        if (replay_T_below(a.recs, a.tile_vals, a.flags, a.st, lo, el, ix, iy)) {
-          first = l;
-          break;
+      float Sex = __shfl_up_sync(0xffffffffu, S, 1);
+      if (lane == 0) Sex = 1.f;
+      const float Tl = T * Sex;  // transmittance before this lane's first entry
+      // early stop, in entry order: clear float32 decisions first, then the
+      // near-threshold entries (warp-cooperative float64 replay) before them
+      uint32_t nearm = 0u, clearm = 0u;
+#pragma unroll
+      for (int i = 0; i < E; ++i) {
+        const float Ta = Tl * Pi[i];
+        const bool con = (conm >> i) & 1u;
+        const bool near = con && fabsf(Ta - thr) <= 2e-5f * thr;
+        if (near) nearm |= 1u << i;
+        if (con && !near && Ta < thr) clearm |= 1u << i;
+      }
+      int first = (int)WIN;  // window-relative index of the stop entry
+      const uint32_t clear_lanes = __ballot_sync(0xffffffffu, clearm != 0u);
+      if (clear_lanes) {
+        const int l = __ffs(clear_lanes) - 1;
+        first = E * l + __ffs(__shfl_sync(0xffffffffu, clearm, l)) - 1;
+      }
+      uint32_t near_lanes = __ballot_sync(0xffffffffu, nearm != 0u);
+      bool hit = false;
+      while (near_lanes && !hit) {
+        const int l = __ffs(near_lanes) - 1;
+        near_lanes &= near_lanes - 1;
+        if (E * l > first) break;
+        uint32_t nm = __shfl_sync(0xffffffffu, nearm, l);
+        while (nm) {
+          const int i = __ffs(nm) - 1;
+          nm &= nm - 1;
+          const int idx = E * l + i;
+          if (idx > first) break;
+          if (replay_T_below(a.recs, a.tile_vals, a.flags, a.st, lo, base + (uint32_t)idx, ix, iy)) {
+            first = idx;
+            hit = true;
+            break;
+          }
         }
       }
-      const bool valid = con && lane <= first;
-      const float wgt = valid ? at * Tb : 0.f;
-      c0 += warp_sum(valid ? wgt * r.r3.y : 0.f);
-      c1 += warp_sum(valid ? wgt * r.r3.z : 0.f);
-      c2 += warp_sum(valid ? wgt * r.r3.w : 0.f);
-      dep += warp_sum(valid ? wgt * r.r0.z : 0.f);
-      n0 += warp_sum(valid ? wgt * r.r4.x : 0.f);
-      n1 += warp_sum(valid ? wgt * r.r4.y : 0.f);
-      n2 += warp_sum(valid ? wgt * r.r4.z : 0.f);
-      const uint32_t vm = __ballot_sync(0xffffffffu, valid);
-      if (!naive && lane == 0) {  // window [base, base + 32) completes word w_cur, opens w_cur + 1
-        const uint32_t sh = (base - lo) & 31u;
-        cur |= vm << sh;
-        a.pix_mask[mask_word(lo, tile, w_cur, pit)] = cur;
-        cur = sh ? vm >> (32 - sh) : 0u;
-        ++w_cur;
+      // contributions up to and including the stop entry
+      uint32_t vm = 0u;
+      float Tb = Tl;
+#pragma unroll
+      for (int i = 0; i < E; ++i) {
+        if (((conm >> i) & 1u) && E * lane + i <= first) {
+          vm |= 1u << i;
+          const float wgt = at[i] * Tb;
+          const SplatRec *g = a.recs + rks[i];  // just loaded: L1 hit
+          const float4 c3 = g->r3, c4 = g->r4;
+          q0 = fmaf(wgt, c3.y, q0);
+          q1 = fmaf(wgt, c3.z, q1);
+          q2 = fmaf(wgt, c3.w, q2);
+          qd = fmaf(wgt, g->r0.z, qd);
+          qn0 = fmaf(wgt, c4.x, qn0);
+          qn1 = fmaf(wgt, c4.y, qn1);
+          qn2 = fmaf(wgt, c4.z, qn2);
+        }
+        Tb = Tl * Pi[i];
       }
-      cnt += __popc(vm);
-      if (vm) last = base + (31 - __clz(vm)) - lo + 1u;
-      if (first < 32) {
-        T = __shfl_sync(0xffffffffu, Ta, first);
+      cnt += __reduce_add_sync(0xffffffffu, (uint32_t)__popc(vm));
+      const uint32_t hi_idx = __reduce_max_sync(0xffffffffu, vm ? (uint32_t)(E * lane + 32 - __clz(vm)) : 0u);
+      if (hi_idx) last = base + hi_idx - lo;  // one past the last contributor, relative to lo
+      if (!naive) {
+        // contribution-mask word of each chunk of the window: OR of the
+        // lanes' E-bit groups over the LPC lanes of the chunk
+        uint32_t word = vm << (E * (lane % LPC));
+#pragma unroll
+        for (int o = 1; o < LPC; o <<= 1) word |= __shfl_xor_sync(0xffffffffu, word, o);
+        const uint32_t c = ((base - lo) >> 5) + (uint32_t)(lane / LPC);
+        if (lane % LPC == 0 && c < n_chunks && 32 * (lane / LPC) <= first) {
+          if (c == c_start) word |= stored;
+          a.pix_mask[mask_word(lo, tile, c, pit)] = word;
+        }
+      }
+      if (first < (int)WIN) {
+        const int l = first / E, i = first % E;
+        float Tf = Pi[0];
+#pragma unroll
+        for (int k = 1; k < E; ++k)
+          if (k == i) Tf = Pi[k];
+        T = __shfl_sync(0xffffffffu, Tl * Tf, l);
         stopped = true;
       } else {
-        T = __shfl_sync(0xffffffffu, Ta, 31);
+        T = T * __shfl_sync(0xffffffffu, S, 31);
       }
     }
+    const float c0 = f.c0 + warp_sum(q0), c1 = f.c1 + warp_sum(q1), c2 = f.c2 + warp_sum(q2);
+    const float dep = f.dep + warp_sum(qd);
+    const float n0 = f.n0 + warp_sum(qn0), n1 = f.n1 + warp_sum(qn1), n2 = f.n2 + warp_sum(qn2);
     if (lane == 0) {
-      // the open word, if it is still a chunk of this tile list (words past
-      // the list belong to the next tile)
-      if (!naive && hi > lo && w_cur <= ((hi - 1 - lo) >> 5)) a.pix_mask[mask_word(lo, tile, w_cur, pit)] = cur;
       const uint32_t pix = f.pix;
       a.color[3 * pix + 0] = c0 + a.bg[0] * T;
       a.color[3 * pix + 1] = c1 + a.bg[1] * T;
@@ -368,6 +434,7 @@ __global__ void __launch_bounds__(256, HGS_FIXUP_MINB) k_fixup_fwd(CompositeArgs
       a.pix_last[pix] = last;
       if (naive) a.pix_count[pix] = cnt;
       atomicAdd(&a.st->diag[10], 1ull);
+      if (a.flags & HGS_FLAG_COUNT) atomicMax(&a.st->diag[15], (unsigned long long)n_win);
     }
   }
 }

@@ -528,23 +528,35 @@ __device__ __forceinline__ bool eval_pair(const SplatRec &r, const SplatRec *rp,
 // Warp-cooperative: all 32 lanes call it with the same arguments.  32 entries
 // per step, each lane evaluates its entry with the exact decisions and the
 // float64 alpha; the float64 factors are multiplied across the warp.
+#ifndef HGS_REPLAY_E
+#define HGS_REPLAY_E 4  // tile-list entries per lane per step of the float64 transmittance replay
+#endif
+// Float64 transmittance of pixel (ix, iy) after tile-list entries lo..upto,
+// exactly as the reference accumulates it (_blend_py.py:104-113).  Each pair's
+// contribution decision and alpha come straight from its float64 evaluation
+// (pair_f64 -- the decision the float32 path reproduces), 32 x HGS_REPLAY_E
+// entries per step so the serial chain of a deep replay is short.
 static __device__ __noinline__ bool replay_T_below(const SplatRec *recs, const uint32_t *tile_vals, uint32_t flags,
                                                    FrameState *st, uint32_t lo, uint32_t upto, int ix, int iy) {
+  constexpr int E = HGS_REPLAY_E;
   const int lane = threadIdx.x & 31;
   if (lane == 0) atomicAdd(&st->diag[1], 1ull);
   const bool naive = flags & HGS_FLAG_NAIVE;
   double T = 1.0;
-  for (uint32_t base = lo; base <= upto; base += 32) {
-    const uint32_t j = base + lane;
+  for (uint32_t base = lo; base <= upto; base += 32 * E) {
     double om = 1.0;
-    if (j <= upto) {
-      const uint32_t rk = naive ? j : tile_vals[j];
-      const SplatRec r = recs[rk];
-      PairEval p;
-      if ((naive || in_bbox(r.r5, ix, iy)) && eval_pair<false>(r, recs + rk, ix, iy, flags, st, p)) {
-        double at64;
-        bool ray64, cl64;
-        if (pair_f64(st->recs64 + rk, rec_is3d(r), ix, iy, &at64, &ray64, &cl64)) om = 1.0 - at64;
+#pragma unroll
+    for (int i = 0; i < E; ++i) {
+      const uint32_t j = base + (uint32_t)(32 * i + lane);
+      if (j <= upto) {
+        const uint32_t rk = naive ? j : tile_vals[j];
+        const SplatRec *g = recs + rk;
+        if (naive || in_bbox(__ldg(&g->r5), ix, iy)) {
+          double at64;
+          bool ray64, cl64;
+          if (pair_f64(st->recs64 + rk, __float_as_uint(__ldg(&g->r4.w)) >> 31, ix, iy, &at64, &ray64, &cl64))
+            om *= 1.0 - at64;
+        }
       }
     }
 #pragma unroll

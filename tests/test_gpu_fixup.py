@@ -1,0 +1,76 @@
+"""The deferred-pixel path of the forward (k_fixup_fwd) on whole images.
+
+Near-threshold decisions are rare (a few thousand pixels per 1080p frame), so
+the golden scenes exercise the float64 resume kernel only lightly.  With
+HGS_FLAG_DEFER_ALL every pixel of the forward is handed to it at its first
+contribution (even pixels before it, odd pixels after it, i.e. through the
+transmittance replay), and the result must still match the reference's own
+outputs: images, blend log (contribution masks) and gradients (the backward
+replays the masks the resume kernel wrote).  Same tolerances as
+test_gpu_parity.py.
+"""
+
+import numpy as np
+import pytest
+
+from _fixtures import SCENES, grad_rel_err, load
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", params=SCENES)
+def deferred(request):
+    from paper_2512_02932_b200 import _lib, raster
+    from paper_2512_02932_b200.core import DeviceGaussians
+    scene, cam, st, d = load(request.param)
+    ds = DeviceGaussians.from_host(scene, "cuda", validate=True)
+    imgs, frame = raster.rasterize(ds, cam, st, _lib.HGS_FLAG_COUNT | _lib.HGS_FLAG_DEFER_ALL)
+    return request.param, scene, cam, d, imgs, frame
+
+
+def test_every_pixel_deferred(deferred):
+    from paper_2512_02932_b200 import _lib
+    name, scene, cam, d, imgs, frame = deferred
+    stats = _lib.frame_stats(frame)
+    covered = int(np.count_nonzero(d["transmittance"] < 1.0))
+    assert int(stats[10]) >= covered, (name, int(stats[10]), covered)
+
+
+def test_images(deferred):
+    name, scene, cam, d, imgs, frame = deferred
+    color = imgs["color"].double().cpu().numpy()
+    T = imgs["transmittance"].double().cpu().numpy()
+    depth = imgs["depth"].double().cpu().numpy()
+    assert np.abs(color - d["color"]).max() <= 1e-4, name
+    assert np.abs(T - d["transmittance"]).max() <= 1e-4, name
+    rel = np.abs(depth - d["depth"]) / np.maximum(np.abs(d["depth"]), 1.0)
+    assert rel.max() <= 5e-4, name
+
+
+def test_blend_log(deferred):
+    from paper_2512_02932_b200 import raster
+    name, scene, cam, d, imgs, frame = deferred
+    lg = raster._materialise_log(frame)
+    if "log_offsets" in d:
+        assert np.array_equal(lg.offsets, d["log_offsets"]), name
+        assert np.array_equal(lg.position, d["log_pos"]), name
+        np.testing.assert_allclose(lg.alpha, d["log_alpha"], atol=2e-6, rtol=1e-4)
+    else:
+        assert np.array_equal(np.diff(lg.offsets), d["log_counts"].astype(np.int64)), name
+
+
+def test_gradients(deferred):
+    import torch
+    from paper_2512_02932_b200 import grad
+    name, scene, cam, d, imgs, frame = deferred
+    pg = torch.from_numpy(d["pixel_grad"]).cuda().float()
+    if pg.dim() == 3:
+        pg = pg.unsqueeze(0)
+    g, touched = grad.backward_device(frame, pg.contiguous())
+    assert np.array_equal(touched.cpu().numpy().astype(bool), d["touched"].astype(bool)), name
+    B = scene.sh_coeffs.shape[2]
+    n = scene.count
+    for k in range(g.shape[0]):
+        got = grad._views(g[k], n, B).flat().double().cpu().numpy()
+        err = grad_rel_err(got, d["grads"][k], B)
+        assert max(err.values()) <= 1e-3, (name, k, err)
