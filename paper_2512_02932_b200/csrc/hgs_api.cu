@@ -271,8 +271,7 @@ int hgs_forward(const hgs_scene *scene, const hgs_camera *camera, const hgs_sett
     HGS_CUDA(cudaMemsetAsync(at<char>(frame, L.lb_scan), 0, L.lb_scan_bytes, s));
     // tile counts per rank go to the (now free) depth-key buffer
     uint32_t *counts = at<uint32_t>(frame, L.keys_a);
-    HGS_CUDA(cudaMemsetAsync(rank_of, 0xff, (size_t)n * 4, s));
-    k_rank_scatter<<<grid_for(m, 256), 256, 0, s>>>(vals_sorted, m, rank_of);
+    k_rank_scatter<<<grid_for(n, 256), 256, 0, s>>>(vals_sorted, m, n, rank_of);
     HGS_LAUNCHED();
     HGS_CUDA(launch_preprocess(sc, cam, mod, rank_of, at<SplatRec>(frame, L.recs), at<Rec64>(frame, L.recs64),
                                at<float4>(frame, L.cull2d),

@@ -145,9 +145,12 @@ __device__ __forceinline__ void write_record(const ProjD &o, uint32_t idx, Splat
 
 // Inverse of the depth permutation: rank_of[sorted_idx[r]] = r for the M
 // kept splats (culled Gaussians keep the caller's 0xffffffff fill).
-__global__ void k_rank_scatter(const uint32_t *__restrict__ sorted_idx, int64_t m, uint32_t *__restrict__ rank_of) {
-  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < m; r += (int64_t)gridDim.x * blockDim.x)
-    rank_of[sorted_idx[r]] = (uint32_t)r;
+// Inverse depth permutation over all n sorted slots: culled Gaussians (keys
+// ~0, sorted after the m kept ones) get rank 0xffffffff.
+__global__ void k_rank_scatter(const uint32_t *__restrict__ sorted_idx, int64_t m, int64_t n,
+                               uint32_t *__restrict__ rank_of) {
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x)
+    rank_of[sorted_idx[r]] = r < m ? (uint32_t)r : 0xffffffffu;
 }
 
 // One thread per Gaussian in index order, one warp per CTA and 32 consecutive

@@ -610,7 +610,7 @@ __global__ void k_init_state(SceneView sc, CamD cam, ModD mod, const SplatRec *r
                              FrameState *st);
 __global__ void k_depth_keys(SceneView sc, CamD cam, unsigned long long *keys, uint32_t *vals, uint32_t *hist,
                              FrameState *st);
-__global__ void k_rank_scatter(const uint32_t *sorted_idx, int64_t m, uint32_t *rank_of);
+__global__ void k_rank_scatter(const uint32_t *sorted_idx, int64_t m, int64_t n, uint32_t *rank_of);
 cudaError_t launch_preprocess(const SceneView &sc, const CamD &cam, const ModD &mod, const uint32_t *rank_of,
                               SplatRec *recs, Rec64 *recs64, float4 *cull2d, uint32_t *counts, cudaStream_t s);
 __global__ void k_scan_counts(const uint32_t *counts, int64_t m, unsigned long long *pair_off,
