@@ -143,8 +143,6 @@ __device__ __forceinline__ void write_record(const ProjD &o, uint32_t idx, Splat
   }
 }
 
-// Inverse of the depth permutation: rank_of[sorted_idx[r]] = r for the M
-// kept splats (culled Gaussians keep the caller's 0xffffffff fill).
 // Inverse depth permutation over all n sorted slots: culled Gaussians (keys
 // ~0, sorted after the m kept ones) get rank 0xffffffff.
 __global__ void k_rank_scatter(const uint32_t *__restrict__ sorted_idx, int64_t m, int64_t n,
