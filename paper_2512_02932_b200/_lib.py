@@ -161,7 +161,7 @@ def lib():
     L.hgs_adam_step.argtypes = [P(Params), _vp, _vp, _vp, P(AdamCfg), _vp]
     L.hgs_combine_adam_step.argtypes = [P(Params), _vp, _vp, _vp, _vp, _i32, _vp, _vp, P(AdamCfg),
                                         _vp, _vp]
-    L.hgs_densify_stats.argtypes = [P(Scene), P(Camera), _vp, P(FrameInfo), _vp, _i32, _vp, _vp, _vp, _vp]
+    L.hgs_densify_stats.argtypes = [P(Scene), P(Camera), _vp, _i32, _vp, _vp, _vp, _vp]
     L.hgs_densify_scratch_bytes.restype = ctypes.c_size_t
     L.hgs_densify_scratch_bytes.argtypes = [_i64]
     L.hgs_densify_plan.argtypes = [P(Scene), _vp, _vp, P(DensifyCfg), _vp, ctypes.c_size_t,

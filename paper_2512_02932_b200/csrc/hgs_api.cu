@@ -158,13 +158,6 @@ int radix_sort(K *ka, K *kb, uint32_t *va, uint32_t *vb, int64_t n, const int *p
 }
 
 }  // namespace
-
-// Device views of a forward's frame buffer for the training-side kernels.
-void frame_views(const void *frame, const hgs_frame_info *info, const SplatRec **recs, const uint32_t **rank_of) {
-  const Layout L = make_layout(info->n, info->width, info->height, info->pair_capacity);
-  *recs = at<SplatRec>(const_cast<void *>(frame), L.recs);
-  *rank_of = at<uint32_t>(const_cast<void *>(frame), info->internal[1] ? L.vals_a : L.vals_b);
-}
 }  // namespace hgs
 
 using namespace hgs;
@@ -268,7 +261,6 @@ int hgs_forward(const hgs_scene *scene, const hgs_camera *camera, const hgs_sett
     if (rc) return rc;
     vals_sorted = at<uint32_t>(frame, in_b ? L.vals_b : L.vals_a);
     rank_of = at<uint32_t>(frame, in_b ? L.vals_a : L.vals_b);  // the free ping-pong buffer
-    info->internal[1] = in_b ? 1u : 0u;  // where rank_of lives (the backward's chain rule reads it)
     info->internal[2] = (uint32_t)np;  // depth-sort passes (diagnostics / launch count)
   }
   info->m = m;
@@ -483,14 +475,13 @@ int hgs_backward(const hgs_scene *scene, const hgs_camera *camera, const hgs_set
   const SceneView sc = make_scene(*scene);
   const CamD cam = make_cam(*camera);
   const ModD mod{settings->theta_z, settings->t_z, settings->lambda_z};
-  const Layout FL = make_layout(info->n, info->width, info->height, info->pair_capacity);
-  const SplatRec *f_recs = at<SplatRec>(const_cast<void *>(frame), FL.recs);
-  const Rec64 *f_recs64 = at<Rec64>(const_cast<void *>(frame), FL.recs64);
-  k_init_state<<<1, 1, 0, s>>>(sc, cam, mod, f_recs, f_recs64, b.c.st);
+  {
+    const Layout FL = make_layout(info->n, info->width, info->height, info->pair_capacity);
+    k_init_state<<<1, 1, 0, s>>>(sc, cam, mod, at<SplatRec>(const_cast<void *>(frame), FL.recs),
+                                 at<Rec64>(const_cast<void *>(frame), FL.recs64), b.c.st);
+  }
   HGS_LAUNCHED();
-  // the forward's inverse depth permutation (the free ping-pong buffer of the depth sort)
-  const uint32_t *rank_of = at<uint32_t>(const_cast<void *>(frame), info->internal[1] ? FL.vals_a : FL.vals_b);
-  const ChainArgs c0{sc, cam, mod, acc, ext ? acc_ext : nullptr, 0, nullptr, rank_of, f_recs64};
+  const ChainArgs c0{sc, cam, mod, acc, ext ? acc_ext : nullptr, 0, nullptr};
   for (int k0 = 0; k0 < kg; k0 += 4) {
     const int kc = std::min(4, kg - k0);
     HGS_CUDA(cudaMemsetAsync(acc, 0, (size_t)nn * kc * 16 * 4, s));

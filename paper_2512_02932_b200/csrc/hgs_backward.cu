@@ -320,13 +320,9 @@ __global__ void __launch_bounds__(kChainThreads, HGS_CHAIN_MINB) k_chain_rule_t(
         double ayd = fmin(fmax(floor(ctr_y), -1073741824.0), 1073741824.0);
         if (isnan(axd)) axd = 0.0;
         if (isnan(ayd)) ayd = 0.0;
-        // slots 6-14 hold dL/d(linear-form coefficients) (geom_2d_rows): row
-        // gradients from the splat's float64 rows, gathered by depth rank
-        float ga[3], gb[3], gc[3];
-        coef_to_row_grads(c.recs64[c.rank_of[i]].g, axd, ayd, A, ga, gb, gc);
-        const double gm0[3] = {ga[0], ga[1], ga[2]};  // columns 0, 1, 3
-        const double gm1[3] = {gb[0], gb[1], gb[2]};
-        double gm3[3] = {gc[0], gc[1], gc[2]};
+        const double gm0[3] = {A[6], A[7], A[8]};  // columns 0, 1, 3
+        const double gm1[3] = {A[9], A[10], A[11]};
+        double gm3[3] = {A[12], A[13], A[14]};
 #pragma unroll
         for (int d = 0; d < 3; ++d) gm3[d] -= axd * gm0[d] + ayd * gm1[d];
         // dH = T^T dM over rows (0, 1, 3) of T (backward.py:152-164); columns 0, 1, 3 of H

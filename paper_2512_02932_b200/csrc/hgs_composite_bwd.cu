@@ -123,21 +123,23 @@ __device__ __forceinline__ void pair_grads(const SplatRec &r, const PairEval &p,
         v[k][7] += 0.5f * da * vx * vy;
         v[k][8] += 0.5f * da * vy * vy;
       } else if (p.ray) {
-        // u = Nu / den, v = Nv / den (geom_2d_rows): slots 6-14 collect dL/d of
-        // the linear-form coefficients (U, V, D) x (1, px, py); the chain rule
-        // turns them into row gradients (coef_to_row_grads)
         const float du = -da * p.u, dv = -da * p.v;
         const float id = p.inv_den;
-        const float gu = du * id, gv = dv * id, gd = -(du * p.u + dv * p.v) * id;
-        v[k][6] += gu;
-        v[k][7] += gu * p.pxl;
-        v[k][8] += gu * p.pyl;
-        v[k][9] += gv;
-        v[k][10] += gv * p.pxl;
-        v[k][11] += gv * p.pyl;
-        v[k][12] += gd;
-        v[k][13] += gd * p.pxl;
-        v[k][14] += gd * p.pyl;
+        const float dhu0 = (du * (-p.u * p.hv1) + dv * (-p.hv3 - p.v * p.hv1)) * id;
+        const float dhu1 = (du * (p.hv3 + p.u * p.hv0) + dv * (p.v * p.hv0)) * id;
+        const float dhu3 = (du * (-p.hv1) + dv * p.hv0) * id;
+        const float dhv0 = (du * (p.u * p.hu1) + dv * (p.hu3 + p.v * p.hu1)) * id;
+        const float dhv1 = (du * (-p.hu3 - p.u * p.hu0) + dv * (-p.v * p.hu0)) * id;
+        const float dhv3 = (du * p.hu1 + dv * (-p.hu0)) * id;
+        v[k][6] += -dhu0;
+        v[k][7] += -dhu1;
+        v[k][8] += -dhu3;
+        v[k][9] += -dhv0;
+        v[k][10] += -dhv1;
+        v[k][11] += -dhv3;
+        v[k][12] += p.pxl * dhu0 + p.pyl * dhv0;
+        v[k][13] += p.pxl * dhu1 + p.pyl * dhv1;
+        v[k][14] += p.pxl * dhu3 + p.pyl * dhv3;
       } else {
         v[k][4] += 4.f * p.dx * da;
         v[k][5] += 4.f * p.dy * da;

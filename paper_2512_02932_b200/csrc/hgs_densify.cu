@@ -33,22 +33,25 @@ constexpr int kDScan = 1024;
 
 enum : uint8_t { kKeep = 0, kPrune = 1, kClone = 2, kSplit = 3 };
 
-__global__ void k_densify_stats(SceneView sc, const float *acc, int kg, const uint8_t *touched,
-                                const SplatRec *recs, const uint32_t *rank_of, float half_w, float half_h,
-                                float *grad_accum, int32_t *obs_count) {
+__global__ void k_densify_stats(SceneView sc, CamD cam, const float *acc, int kg, const uint8_t *touched,
+                                float half_w, float half_h, float *grad_accum, int32_t *obs_count) {
   const int64_t n = sc.n;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     if (!touched[i]) continue;
-    // 2D: slots 6-14 are dL/d(U, V, D), the linear-form coefficients of the
-    // ray/plane solve (geom_2d_rows); a screen translation by (dx, dy) moves
-    // the rows a += dx c, b += dy c, i.e. dD0 = -D1 dx - D2 dy, dU0 = -U1 dx
-    // - U2 dy, dV0 = -V1 dx - V2 dy (the other coefficients are invariant)
+    float m2[3] = {0.f, 0.f, 0.f};
     const bool is3d = sc.type_spec[i] == 1;
-    float U1 = 0.f, U2 = 0.f, V1 = 0.f, V2 = 0.f, D1 = 0.f, D2 = 0.f;
-    if (!is3d) {
-      const SplatRec *r = recs + rank_of[i];
-      const float4 q1 = r->r1, q2 = r->r2;
-      U1 = q1.y; U2 = q1.z; V1 = q2.x; V2 = q2.y; D1 = q2.w; D2 = r->r3.x;
+    if (!is3d) {  // depth row of M (columns 0, 1, 3): screen translation moves m0', m1' by delta m2
+      const float q0 = sc.rotation[4 * i], q1 = sc.rotation[4 * i + 1], q2 = sc.rotation[4 * i + 2],
+                  q3 = sc.rotation[4 * i + 3];
+      const float iq = rsqrtf(q0 * q0 + q1 * q1 + q2 * q2 + q3 * q3);
+      const float w = q0 * iq, x = q1 * iq, y = q2 * iq, z = q3 * iq;
+      const float R0[3] = {1.f - 2.f * (y * y + z * z), 2.f * (x * y + w * z), 2.f * (x * z - w * y)};
+      const float R1[3] = {2.f * (x * y - w * z), 1.f - 2.f * (x * x + z * z), 2.f * (y * z + w * x)};
+      const float V6 = (float)cam.V[6], V7 = (float)cam.V[7], V8 = (float)cam.V[8];
+      m2[0] = expf(sc.log_scale[3 * i]) * (V6 * R0[0] + V7 * R0[1] + V8 * R0[2]);
+      m2[1] = expf(sc.log_scale[3 * i + 1]) * (V6 * R1[0] + V7 * R1[1] + V8 * R1[2]);
+      m2[2] = (float)(cam.V[6] * sc.center[3 * i] + cam.V[7] * sc.center[3 * i + 1] +
+                      cam.V[8] * sc.center[3 * i + 2] + cam.tv[2]);
     }
     float gx = 0.f, gy = 0.f;
     for (int k = 0; k < kg; ++k) {
@@ -56,8 +59,8 @@ __global__ void k_densify_stats(SceneView sc, const float *acc, int kg, const ui
       gx += A[4];
       gy += A[5];
       if (!is3d) {
-        gx -= (A[6] * U1 + A[9] * V1) + A[12] * D1;
-        gy -= (A[6] * U2 + A[9] * V2) + A[12] * D2;
+        gx += (A[6] * m2[0] + A[7] * m2[1]) + A[8] * m2[2];
+        gy += (A[9] * m2[0] + A[10] * m2[1]) + A[11] * m2[2];
       }
     }
     gx *= half_w;  // pixel -> NDC units (3DGS viewspace gradient convention)
@@ -286,19 +289,19 @@ using namespace hgs;
 
 extern "C" {
 
-int hgs_densify_stats(const hgs_scene *scene, const hgs_camera *camera, const void *frame,
-                      const hgs_frame_info *info, const void *bwd_scratch, int32_t kg, const uint8_t *touched,
-                      float *grad_accum, int32_t *obs_count, void *stream) {
+int hgs_densify_stats(const hgs_scene *scene, const hgs_camera *camera, const void *bwd_scratch, int32_t kg,
+                      const uint8_t *touched, float *grad_accum, int32_t *obs_count, void *stream) {
   if (!scene || !camera || scene->n < 0 || kg < 1 || kg > 4) return HGS_ERR_CONFIG;
   if (scene->n == 0) return HGS_OK;
-  if (!frame || !info || !bwd_scratch || !touched || !grad_accum || !obs_count) return HGS_ERR_INTEGRITY;
-  if (info->n != scene->n) return HGS_ERR_INTEGRITY;
-  const SplatRec *recs;
-  const uint32_t *rank_of;
-  frame_views(frame, info, &recs, &rank_of);
+  if (!bwd_scratch || !touched || !grad_accum || !obs_count) return HGS_ERR_INTEGRITY;
+  CamD cam;
+  for (int r = 0; r < 3; ++r) {
+    for (int k = 0; k < 3; ++k) cam.V[r * 3 + k] = camera->world_to_camera[r * 4 + k];
+    cam.tv[r] = camera->world_to_camera[r * 4 + 3];
+  }
   k_densify_stats<<<grid_of(scene->n), 256, 0, static_cast<cudaStream_t>(stream)>>>(
-      view_of(*scene), static_cast<const float *>(bwd_scratch), kg, touched, recs, rank_of,
-      0.5f * (float)camera->width, 0.5f * (float)camera->height, grad_accum, obs_count);
+      view_of(*scene), cam, static_cast<const float *>(bwd_scratch), kg, touched, 0.5f * (float)camera->width,
+      0.5f * (float)camera->height, grad_accum, obs_count);
   return cudaGetLastError() == cudaSuccess ? HGS_OK : HGS_ERR_CUDA;
 }
 

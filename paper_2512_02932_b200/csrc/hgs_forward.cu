@@ -111,7 +111,7 @@ __device__ __forceinline__ void write_record(const ProjD &o, uint32_t idx, Splat
   ayd = fmin(fmax(ayd, -1073741824.0), 1073741824.0);
   if (isnan(axd)) axd = 0.0;
   if (isnan(ayd)) ayd = 0.0;
-  SplatRec r, rows;
+  SplatRec r;
   r.r0 = make_float4((float)(o.ctr[0] - axd), (float)(o.ctr[1] - ayd), (float)o.t[2], (float)log2(o.alpha_eff));
   if (o.typ == 1) {
     // relative float32 error amplification of the conic quadratic form
@@ -120,24 +120,11 @@ __device__ __forceinline__ void write_record(const ProjD &o, uint32_t idx, Splat
     r.r3 = make_float4(0.f, (float)o.color[0], (float)o.color[1], (float)o.color[2]);
   } else {
     const double *m = o.mrow;  // rows x(0..3), y(4..7), w(8..11)
-    // anchor-rebased rows (columns 0, 1, 3): a = M0 - ax M3, b = M1 - ay M3, c = M3
-    const double a0 = m[0] - axd * m[8], a1 = m[1] - axd * m[9], a3 = m[3] - axd * m[11];
-    const double b0 = m[4] - ayd * m[8], b1 = m[5] - ayd * m[9], b3 = m[7] - ayd * m[11];
-    const double c0 = m[8], c1 = m[9], c3 = m[11];
-    // the 2x2 ray/plane solve as three linear forms of the anchor-relative
-    // pixel (px, py): with hu_i = px c_i - a_i, hv_i = py c_i - b_i the px py
-    // terms cancel, so den = hu0 hv1 - hu1 hv0 = D0 + D1 px + D2 py and the
-    // numerators of u, v are U0 + U1 px + U2 py, V0 + V1 px + V2 py
-    // (_blend_py.py:32-42); coefficients in float64, rounded once
-    r.r1 = make_float4((float)(a1 * b3 - a3 * b1), (float)(c3 * b1 - c1 * b3), (float)(a3 * c1 - a1 * c3),
-                       (float)(a3 * b0 - a0 * b3));
-    r.r2 = make_float4((float)(c0 * b3 - c3 * b0), (float)(a0 * c3 - a3 * c0), (float)(a0 * b1 - a1 * b0),
-                       (float)(c1 * b0 - c0 * b1));
-    r.r3 = make_float4((float)(a1 * c0 - a0 * c1), (float)o.color[0], (float)o.color[1], (float)o.color[2]);
-    // rows for the warp-cull conic (cull2d_prep reads the row layout)
-    rows.r1 = make_float4((float)a0, (float)a1, (float)a3, (float)b0);
-    rows.r2 = make_float4((float)b1, (float)b3, (float)c0, (float)c1);
-    rows.r3 = make_float4((float)c3, 0.f, 0.f, 0.f);
+    double m00 = m[0] - axd * m[8], m01 = m[1] - axd * m[9], m03 = m[3] - axd * m[11];
+    double m10 = m[4] - ayd * m[8], m11 = m[5] - ayd * m[9], m13 = m[7] - ayd * m[11];
+    r.r1 = make_float4((float)m00, (float)m01, (float)m03, (float)m10);
+    r.r2 = make_float4((float)m11, (float)m13, (float)m[8], (float)m[9]);
+    r.r3 = make_float4((float)m[11], (float)o.color[0], (float)o.color[1], (float)o.color[2]);
   }
   uint32_t tag = idx | ((uint32_t)(o.typ == 1) << 31);
   r.r4 = make_float4((float)o.normal[0], (float)o.normal[1], (float)o.normal[2], __uint_as_float(tag));
@@ -150,10 +137,7 @@ __device__ __forceinline__ void write_record(const ProjD &o, uint32_t idx, Splat
   *rec = r;
   if (o.typ != 1) {  // the 2D support conic of the compositor's warp cull
     float4 k0, k1;
-    rows.r0 = r.r0;
-    rows.r4 = r.r4;
-    rows.r5 = r.r5;
-    cull2d_prep(rows, k0, k1);
+    cull2d_prep(r, k0, k1);
     cull[0] = k0;
     cull[1] = k1;
   }

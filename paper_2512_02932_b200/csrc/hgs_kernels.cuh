@@ -245,13 +245,12 @@ __device__ __forceinline__ bool cull_splat_pre(const SplatRec &r, const float4 *
 #ifndef HGS_STAGED_ORIGIN
 #define HGS_STAGED_ORIGIN 1  // compositors stage records with the float block origin
 #endif
-// 2D records hold linear-form coefficients, not the rows cull2d_prep reads:
-// the support conic is prepared once per splat by the preprocess
-#if !HGS_CULL_PRE
-#error "HGS_CULL_PRE = 0 (per-warp 2D conic preparation) needs the row layout of 2D records"
-#endif
 __device__ __forceinline__ bool cull_splat(const SplatRec &r, uint32_t pm, int wx0, int wy0) {
-  return rec_is3d(r) && cull_3d(r, pm, wx0, wy0);
+  if (rec_is3d(r)) return cull_3d(r, pm, wx0, wy0);
+  if (!HGS_CULL_2D) return false;
+  float4 k[2];
+  cull2d_prep(r, k[0], k[1]);  // per warp instead of once per splat (HGS_CULL_PRE = 0)
+  return cull_splat_pre(r, k, pm, wx0, wy0);
 }
 
 // Staged-record form of the anchor (see eval_fast<..., STAGED>): exact while
@@ -273,7 +272,7 @@ struct PairEval {
   float at;       // clamped alpha
   float dx, dy;   // pixel - centre (pixels)
   float u, v;     // 3D: (dx, dy); 2D: tangent-plane intersection
-  float inv_den;  // 2D: 1 / den of the ray/plane solve
+  float hu0, hu1, hu3, hv0, hv1, hv3, inv_den;  // 2D ray quantities
   float pxl, pyl; // pixel relative to the anchor
   bool ray;       // 2D: ray branch chosen (d_ray <= d_screen)
   bool clamped;   // raw alpha > 0.99 (colour-only gradient)
@@ -315,7 +314,7 @@ static __device__ __noinline__ bool pair_f64(const Rec64 *q, bool is3d, int ix, 
 struct Geom {
   float dx, dy, pxl, pyl;
   float d, arg, S;                               // 3D: S bounds |terms| of d
-  float den, dmag;  // 2D: den and |D0| + |D1 px| + |D2 py| (bounds its float32 error)
+  float hu0, hu1, hu3, hv0, hv1, hv3, den, dmag;  // 2D
   float inv_den, u, v, dray, dscr;               // 2D
   bool ray;
 };
@@ -336,23 +335,25 @@ __device__ __forceinline__ void geom_3d(const SplatRec &r, Geom &g) {
   g.S = __fadd_rn(g.d, __fmul_rn(2.f, __fsub_rn(fabsf(t), t)));
 }
 
-// 2D record (write_record): the ray/plane solve of _blend_py.py:32-42 as
-// three linear forms of the anchor-relative pixel centre (px, py):
-//   Nu = U0 + U1 px + U2 py,  Nv = V0 + V1 px + V2 py,  den = D0 + D1 px + D2 py
-// r1 = (U0, U1, U2, V0), r2 = (V1, V2, D0, D1), r3.x = D2;  u = Nu / den,
-// v = Nv / den -- the same values as the reference's hu / hv products (the
-// px py terms cancel), at 6 FFMA instead of 6 FFMA + 6 products.
 __device__ __forceinline__ void geom_2d_rows(const SplatRec &r, Geom &g) {
-  const float D0 = r.r2.z, D1 = r.r2.w, D2 = r.r3.x;
-  g.den = fmaf(D1, g.pxl, fmaf(D2, g.pyl, D0));
-  g.dmag = __fadd_rn(__fadd_rn(fabsf(D0), fabsf(__fmul_rn(D1, g.pxl))), fabsf(__fmul_rn(D2, g.pyl)));
+  const float4 m1 = r.r1, m2 = r.r2;
+  const float m23 = r.r3.x;
+  // rows re-based at the anchor: hu = pxl m2 - m0', hv = pyl m2 - m1'
+  g.hu0 = fmaf(g.pxl, m2.z, -m1.x);
+  g.hu1 = fmaf(g.pxl, m2.w, -m1.y);
+  g.hu3 = fmaf(g.pxl, m23, -m1.z);
+  g.hv0 = fmaf(g.pyl, m2.z, -m1.w);
+  g.hv1 = fmaf(g.pyl, m2.w, -m2.x);
+  g.hv3 = fmaf(g.pyl, m23, -m2.y);
+  const float a = __fmul_rn(g.hu0, g.hv1), b = __fmul_rn(g.hu1, g.hv0);
+  g.den = __fsub_rn(a, b);
+  g.dmag = __fadd_rn(fabsf(a), fabsf(b));
 }
 
 __device__ __forceinline__ void geom_2d_solve(const SplatRec &r, Geom &g) {
   g.inv_den = rcp_approx(g.den);  // MUFU.RCP: no out-of-line slow path in the hot loop
-  const float4 q1 = r.r1, q2 = r.r2;
-  g.u = __fmul_rn(fmaf(q1.y, g.pxl, fmaf(q1.z, g.pyl, q1.x)), g.inv_den);
-  g.v = __fmul_rn(fmaf(q2.x, g.pxl, fmaf(q2.y, g.pyl, q1.w)), g.inv_den);
+  g.u = __fmul_rn(__fsub_rn(__fmul_rn(g.hu1, g.hv3), __fmul_rn(g.hu3, g.hv1)), g.inv_den);
+  g.v = __fmul_rn(__fsub_rn(__fmul_rn(g.hu3, g.hv0), __fmul_rn(g.hu0, g.hv3)), g.inv_den);
   g.dray = fmaf(g.u, g.u, __fmul_rn(g.v, g.v));
   g.dscr = __fmul_rn(fmaf(g.dx, g.dx, __fmul_rn(g.dy, g.dy)), 4.f);
   g.ray = g.dray <= g.dscr;
@@ -377,16 +378,17 @@ struct Resolved {
 // flagged (pure FP32 arithmetic, no calls: safe on the hot path).  Returns
 // kSkip / kContrib when the bound separates every decision, kAmbiguous if not.
 __device__ __forceinline__ int refine_2d(const SplatRec &r, const Geom &g, bool bwd, bool known = false) {
-  // each linear form: coefficient rounding + two FFMA roundings <= 3 eps of
-  // the sum of its term magnitudes (4 eps used)
-  const float4 q1 = r.r1, q2 = r.r2;
-  const float Um = fabsf(q1.x) + fabsf(q1.y * g.pxl) + fabsf(q1.z * g.pyl);
-  const float Vm = fabsf(q1.w) + fabsf(q2.x * g.pxl) + fabsf(q2.y * g.pyl);
+  const float4 m1 = r.r1, m2 = r.r2;
+  const float m23 = r.r3.x;
+  const float A0 = fabsf(g.pxl * m2.z) + fabsf(m1.x), A1 = fabsf(g.pxl * m2.w) + fabsf(m1.y);
+  const float A3 = fabsf(g.pxl * m23) + fabsf(m1.z);
+  const float B0 = fabsf(g.pyl * m2.z) + fabsf(m1.w), B1 = fabsf(g.pyl * m2.w) + fabsf(m2.x);
+  const float B3 = fabsf(g.pyl * m23) + fabsf(m2.y);
   const float ad = fabsf(g.den);
   const float iad = rcp_approx(ad) * (1.f + 4.f * kEps);
-  const float dden = 4.f * kEps * g.dmag;
-  const float du = (4.f * kEps * Um + fabsf(g.u) * dden) * iad + 4.f * kEps * fabsf(g.u);
-  const float dv = (4.f * kEps * Vm + fabsf(g.v) * dden) * iad + 4.f * kEps * fabsf(g.v);
+  const float dden = 6.f * kEps * (A0 * B1 + A1 * B0);
+  const float du = (6.f * kEps * (A1 * B3 + A3 * B1) + fabsf(g.u) * dden) * iad + 4.f * kEps * fabsf(g.u);
+  const float dv = (6.f * kEps * (A3 * B0 + A0 * B3) + fabsf(g.v) * dden) * iad + 4.f * kEps * fabsf(g.v);
   const float e_ray = 2.f * (fabsf(g.u) * du + fabsf(g.v) * dv) + 4.f * kEps * g.dray;
   const float e_scr = 8.f * kEps * g.dscr + 1e-6f * (fabsf(g.dx) + fabsf(g.dy));
   const float margin = fmaf(g.ray ? e_ray : e_scr, kHalfLog2e, 1e-5f);
@@ -490,6 +492,8 @@ __device__ __forceinline__ int eval_fast(const SplatRec &r, int ix, int iy, uint
       p.ray = g.ray;
     }
     if (BWD) {
+      p.hu0 = g.hu0; p.hu1 = g.hu1; p.hu3 = g.hu3;
+      p.hv0 = g.hv0; p.hv1 = g.hv1; p.hv3 = g.hv3;
       if (amb && near_degenerate(g)) geom_2d_solve(r, g);
       p.inv_den = g.inv_den;
       p.u = g.u;
@@ -594,38 +598,7 @@ struct ChainArgs {
   const float *acc_ext;  // (n, KG, 4) or null
   int kg;
   float *grads;          // (KG, n*P) field-major blocks
-  const uint32_t *rank_of;  // Gaussian index -> depth rank (the forward's frame)
-  const Rec64 *recs64;      // float64 projection per rank
 };
-
-// The compositors accumulate a 2D splat's geometry gradient with respect to
-// its nine linear-form coefficients (U, V, D: slots 6-8, 9-11, 12-14, see
-// geom_2d_rows).  The coefficients are 2x2 minors of the anchor-rebased rows
-// a = M0', b = M1', c = M3 (columns 0, 1, 3; write_record):
-//   D = (a0 b1 - a1 b0, c1 b0 - c0 b1, a1 c0 - a0 c1)
-//   U = (a1 b3 - a3 b1, c3 b1 - c1 b3, a3 c1 - a1 c3)
-//   V = (a3 b0 - a0 b3, c0 b3 - c3 b0, a0 c3 - a3 c0)
-// so dL/d(a, b, c) follows by the product rule from the splat's float64 rows
-// g = (m00 m01 m03 | m10 m11 m13 | m30 m31 m33) and its anchor: the anchoring
-// (M0 - ax M3 cancels ~1e3 pixels) in float64, the products in float32.
-__device__ __forceinline__ void coef_to_row_grads(const double *g, double ax, double ay, const float *A,
-                                                  float (&ga)[3], float (&gb)[3], float (&gc)[3]) {
-  const float c0 = (float)g[6], c1 = (float)g[7], c3 = (float)g[8];
-  const float a0 = (float)(g[0] - ax * g[6]), a1 = (float)(g[1] - ax * g[7]), a3 = (float)(g[2] - ax * g[8]);
-  const float b0 = (float)(g[3] - ay * g[6]), b1 = (float)(g[4] - ay * g[7]), b3 = (float)(g[5] - ay * g[8]);
-  const float gU0 = A[6], gU1 = A[7], gU2 = A[8];
-  const float gV0 = A[9], gV1 = A[10], gV2 = A[11];
-  const float gD0 = A[12], gD1 = A[13], gD2 = A[14];
-  ga[0] = gD0 * b1 - gD2 * c1 - gV0 * b3 + gV2 * c3;
-  ga[1] = -gD0 * b0 + gD2 * c0 + gU0 * b3 - gU2 * c3;
-  ga[2] = -gU0 * b1 + gU2 * c1 + gV0 * b0 - gV2 * c0;
-  gb[0] = -gD0 * a1 + gD1 * c1 + gV0 * a3 - gV1 * c3;
-  gb[1] = gD0 * a0 - gD1 * c0 - gU0 * a3 + gU1 * c3;
-  gb[2] = gU0 * a1 - gU1 * c1 - gV0 * a0 + gV1 * c0;
-  gc[0] = -gD1 * b1 + gD2 * a1 + gV1 * b3 - gV2 * a3;
-  gc[1] = gD1 * b0 - gD2 * a0 - gU1 * b3 + gU2 * a3;
-  gc[2] = gU1 * b1 - gU2 * a1 - gV1 * b0 + gV2 * a0;
-}
 
 struct ExchangeState {
   unsigned long long counts[4];  // demote, promote, n3 before, degenerate rows
@@ -638,7 +611,6 @@ __global__ void k_init_state(SceneView sc, CamD cam, ModD mod, const SplatRec *r
 __global__ void k_depth_keys(SceneView sc, CamD cam, unsigned long long *keys, uint32_t *vals, uint32_t *hist,
                              FrameState *st);
 __global__ void k_rank_scatter(const uint32_t *sorted_idx, int64_t m, int64_t n, uint32_t *rank_of);
-void frame_views(const void *frame, const hgs_frame_info *info, const SplatRec **recs, const uint32_t **rank_of);
 cudaError_t launch_preprocess(const SceneView &sc, const CamD &cam, const ModD &mod, const uint32_t *rank_of,
                               SplatRec *recs, Rec64 *recs64, float4 *cull2d, uint32_t *counts, cudaStream_t s);
 __global__ void k_scan_counts(const uint32_t *counts, int64_t m, unsigned long long *pair_off,

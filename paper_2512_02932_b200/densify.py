@@ -67,14 +67,13 @@ class DensifyStats:
         return int(self.grad_accum.shape[0])
 
 
-def accumulate(scene, camera, stats, frame, bwd_scratch, kg, touched):
+def accumulate(scene, camera, stats, bwd_scratch, kg, touched):
     """Add one view's statistics (call right after grad.backward_device with
-    the same scratch and that view's SplatFrame; kg <= 4)."""
+    the same scratch; kg <= 4)."""
     if stats.count != scene.count:
         raise ConfigError("densify statistics do not match the scene")
     _lib.check(_lib.lib().hgs_densify_stats(
-        _lib.scene_struct(scene), _lib.camera_struct(camera), _lib.ptr(frame.buf), frame.info,
-        _lib.ptr(bwd_scratch), int(kg),
+        _lib.scene_struct(scene), _lib.camera_struct(camera), _lib.ptr(bwd_scratch), int(kg),
         _lib.ptr(touched), _lib.ptr(stats.grad_accum), _lib.ptr(stats.obs_count),
         _lib.current_stream_handle(scene.device)), "hgs_densify_stats")
 
