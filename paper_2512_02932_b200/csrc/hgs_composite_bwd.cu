@@ -115,8 +115,8 @@ __device__ __forceinline__ void pair_grads(const SplatRec &r, const PairEval &p,
       const float da = d_at * at;  // = dL/dalpha_eff * alpha_eff * exp(-d/2)
       v[k][3] += da;
       if (is3d) {
-        const float4 cn = r.r1;
-        const float vx = cn.x * p.u + cn.y * p.v, vy = cn.y * p.u + cn.z * p.v;
+        const float4 e = r.r1;  // conic x offset = R^T (wp, wq) (eigenbasis, geom_3d)
+        const float vx = e.x * p.wp - e.y * p.wq, vy = e.y * p.wp + e.x * p.wq;
         v[k][4] += vx * da;
         v[k][5] += vy * da;
         v[k][6] += 0.5f * da * vx * vx;

@@ -114,8 +114,19 @@ __device__ __forceinline__ void write_record(const ProjD &o, uint32_t idx, Splat
   SplatRec r;
   r.r0 = make_float4((float)(o.ctr[0] - axd), (float)(o.ctr[1] - ayd), (float)o.t[2], (float)log2(o.alpha_eff));
   if (o.typ == 1) {
-    // relative float32 error amplification of the conic quadratic form
-    r.r1 = make_float4((float)o.conic[0], (float)o.conic[1], (float)o.conic[2], 0.f);
+    // the conic in its eigenbasis, (cos t, sin t, lambda_p, lambda_q): the
+    // compositors evaluate d = lambda_p p^2 + lambda_q q^2 on the rotated
+    // offset (p, q), a sum of non-negative terms (the (a, b, c) form cancels
+    // catastrophically for elongated splats at the cutoff)
+    // eigenvector of the larger eigenvalue from the row of (Q - l1 I) without
+    // cancellation; the smaller eigenvalue as det / l1
+    const double A = o.conic[0], B = o.conic[1], C = o.conic[2];
+    const double hd = 0.5 * (A - C), h = sqrt(hd * hd + B * B);
+    const double l1 = 0.5 * (A + C) + h, l2 = l1 > 0.0 ? (A * C - B * B) / l1 : 0.0;
+    double vx = hd >= 0.0 ? hd + h : B, vy = hd >= 0.0 ? B : h - hd;
+    const double vn = sqrt(vx * vx + vy * vy);
+    if (vn > 0.0) { vx /= vn; vy /= vn; } else { vx = 1.0; vy = 0.0; }
+    r.r1 = make_float4((float)vx, (float)vy, (float)l1, (float)l2);
     r.r2 = make_float4(0.f, 0.f, 0.f, 0.f);
     r.r3 = make_float4(0.f, (float)o.color[0], (float)o.color[1], (float)o.color[2]);
   } else {

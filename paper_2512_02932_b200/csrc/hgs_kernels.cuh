@@ -148,7 +148,9 @@ __device__ __forceinline__ bool cull_3d(const SplatRec &r, uint32_t pm, int wx0,
   const float Y0 = (float)(wy0 + (c0 >> 3) - q.w) + 0.5f - r.r0.y;
   const float Y1 = (float)(wy0 + (c1 >> 3) - q.w) + 0.5f - r.r0.y;
   if (X0 <= 0.f && 0.f <= X1 && Y0 <= 0.f && 0.f <= Y1) return false;
-  const float a = r.r1.x, b = r.r1.y, c = r.r1.z;
+  const float4 e = r.r1;  // (c, s, lambda_p, lambda_q) -> conic (a, b, c)
+  const float a = fmaf(e.z * e.x, e.x, e.w * e.y * e.y), b = (e.z - e.w) * e.x * e.y;
+  const float c = fmaf(e.z * e.y, e.y, e.w * e.x * e.x);
   const float ia = rcp_approx(a), ic = rcp_approx(c);
   auto qf = [&](float x, float y) { return fmaf(a * x, x, fmaf(2.f * b * x, y, c * y * y)); };
   const float ya = fminf(fmaxf(-b * X0 * ic, Y0), Y1), yb = fminf(fmaxf(-b * X1 * ic, Y0), Y1);
@@ -220,7 +222,10 @@ __device__ __forceinline__ bool cull_splat_pre(const SplatRec &r, const float4 *
   const float PY0 = (float)(wy0 + (c0 >> 3) - q.w) + 0.5f, PY1 = (float)(wy0 + (c1 >> 3) - q.w) + 0.5f;
   float A, B, C, cx, cy, thr;
   if (rec_is3d(r)) {
-    A = r.r1.x; B = r.r1.y; C = r.r1.z;
+    const float4 e = r.r1;  // (c, s, lambda_p, lambda_q) -> conic (A, B, C)
+    A = fmaf(e.z * e.x, e.x, e.w * e.y * e.y);
+    B = (e.z - e.w) * e.x * e.y;
+    C = fmaf(e.z * e.y, e.y, e.w * e.x * e.x);
     cx = r.r0.x; cy = r.r0.y;
     thr = fmaf(dstar, 1.001f, 1e-3f);
   } else {
@@ -273,6 +278,7 @@ struct PairEval {
   float dx, dy;   // pixel - centre (pixels)
   float u, v;     // 3D: (dx, dy); 2D: tangent-plane intersection
   float hu0, hu1, hu3, hv0, hv1, hv3, inv_den;  // 2D ray quantities
+  float wp, wq;   // 3D: lambda_p p, lambda_q q (the conic times the offset, in the eigenbasis)
   float pxl, pyl; // pixel relative to the anchor
   bool ray;       // 2D: ray branch chosen (d_ray <= d_screen)
   bool clamped;   // raw alpha > 0.99 (colour-only gradient)
@@ -313,7 +319,7 @@ static __device__ __noinline__ bool pair_f64(const Rec64 *q, bool is3d, int ix, 
 // inline fast path and the out-of-line resolver compute identical bits.
 struct Geom {
   float dx, dy, pxl, pyl;
-  float d, arg, S;                               // 3D: S bounds |terms| of d
+  float d, arg, wp, wq, m;                       // 3D: eigenbasis terms, m = |dx| + |dy|
   float hu0, hu1, hu3, hv0, hv1, hv3, den, dmag;  // 2D
   float inv_den, u, v, dray, dscr;               // 2D
   bool ray;
@@ -327,13 +333,26 @@ __device__ __forceinline__ void geom_common(const SplatRec &r, int ix, int iy, G
   g.dy = __fsub_rn(g.pyl, r.r0.y);
 }
 
+// 3D record: r1 = (c, s, lambda_p, lambda_q), the conic's eigenbasis
+// (write_record).  (p, q) = rotated offset, d = lambda_p p^2 + lambda_q q^2.
+// Float32 error: |p error| <= eps (2m + |p|) (m = |dx| + |dy|), so
+// |d error| <= eps (6 d + 4 m (lambda_p |p| + lambda_q |q|)).
 __device__ __forceinline__ void geom_3d(const SplatRec &r, Geom &g) {
-  const float4 cn = r.r1;
-  const float t = __fmul_rn(__fmul_rn(cn.y, g.dx), g.dy);
-  g.d = fmaf(__fmul_rn(cn.x, g.dx), g.dx, fmaf(__fmul_rn(cn.z, g.dy), g.dy, __fmul_rn(2.f, t)));
+  const float4 e = r.r1;
+  const float p = fmaf(e.x, g.dx, __fmul_rn(e.y, g.dy));
+  const float q = fmaf(e.x, g.dy, -__fmul_rn(e.y, g.dx));
+  g.wp = __fmul_rn(e.z, p);
+  g.wq = __fmul_rn(e.w, q);
+  g.d = fmaf(g.wp, p, __fmul_rn(g.wq, q));
   g.arg = fmaf(g.d, -kHalfLog2e, r.r0.w);
-  g.S = __fadd_rn(g.d, __fmul_rn(2.f, __fsub_rn(fabsf(t), t)));
+  g.m = __fadd_rn(fabsf(g.dx), fabsf(g.dy));
 }
+
+// Coarse 3D band (log2 units): inside it the precise bound is formed.  Valid
+// while m < kCoarseM3D: with conic eigenvalues <= 1 / 0.3 (the dilation) the
+// bound above stays below the band for every d.
+constexpr float kCoarse3D = 0.05f;
+constexpr float kCoarseM3D = 8192.f;
 
 __device__ __forceinline__ void geom_2d_rows(const SplatRec &r, Geom &g) {
   const float4 m1 = r.r1, m2 = r.r2;
@@ -464,11 +483,19 @@ __device__ __forceinline__ int eval_fast(const SplatRec &r, int ix, int iy, uint
     geom_3d(r, g);
     p.u = g.dx;
     p.v = g.dy;
-    // |d error| <= 16 eps S, S = a dx^2 + c dy^2 + 2|b dx dy| (>= every term)
-    const float margin = exact ? fmaf(g.S, 16.f * kEps * kHalfLog2e, 1e-5f) : 0.f;
-    if (!KNOWN && g.arg < kArgMinAlpha - margin) return kSkip;  // cheap cull: no ex2
-    if (exact && ((!KNOWN && g.arg <= kArgMinAlpha + margin) || (BWD && fabsf(g.arg - kArgClamp) <= margin)))
-      amb = true;
+    p.wp = g.wp;
+    p.wq = g.wq;
+    // cheap cull (no ex2): outside the coarse band no bound is needed
+    if (!KNOWN && g.arg < (exact ? kArgMinAlpha - kCoarse3D : kArgMinAlpha) && (!exact || g.m < kCoarseM3D))
+      return kSkip;
+    if (exact && ((!KNOWN && g.arg <= kArgMinAlpha + kCoarse3D) || (BWD && fabsf(g.arg - kArgClamp) <= kCoarse3D) ||
+                  !(g.m < kCoarseM3D))) {
+      // |d error| <= eps (6 d + 4 m (|wp| + |wq|)), 25% slack
+      const float margin =
+          fmaf(fmaf(4.f * g.m, fabsf(g.wp) + fabsf(g.wq), 6.f * g.d), 1.25f * kEps * kHalfLog2e, 1e-5f);
+      if (!KNOWN && g.arg < kArgMinAlpha - margin) return kSkip;
+      if ((!KNOWN && g.arg <= kArgMinAlpha + margin) || (BWD && fabsf(g.arg - kArgClamp) <= margin)) amb = true;
+    }
   } else {
     geom_2d_rows(r, g);
     if (near_degenerate(g)) {  // (near-)degenerate ray/plane intersection (_blend_py.py:36-37)
