@@ -498,30 +498,25 @@ __device__ __forceinline__ int eval_fast(const SplatRec &r, int ix, int iy, uint
     }
   } else {
     geom_2d_rows(r, g);
-    if (near_degenerate(g)) {  // (near-)degenerate ray/plane intersection (_blend_py.py:36-37)
-      if (!exact) {
-        if (fabsf(g.den) < (float)kDegenerateDen) return kSkip;
-      } else {
-        amb = true;
-      }
+    // (near-)degenerate ray/plane intersection (_blend_py.py:36-37): outside
+    // the coarse-band regime, so its decisions always take the precise bound
+    // (refine_2d leaves them ambiguous unless |den| clears its error bound)
+    const bool nd = near_degenerate(g);
+    if (nd && !exact && fabsf(g.den) < (float)kDegenerateDen) return kSkip;
+    geom_2d_solve(r, g);
+    if (!nd && !KNOWN && g.arg < kArgMinAlpha - (exact ? kCoarse2D : 0.f)) return kSkip;
+    if (exact && (nd || (!KNOWN && g.arg <= kArgMinAlpha + kCoarse2D) ||
+                  (BWD && (fabsf(g.arg - kArgClamp) <= kCoarse2D ||
+                           fabsf(g.dray - g.dscr) <= 0.02f * (g.dray + g.dscr))))) {
+      // coarse band hit: the precise bound usually separates the decision
+      const int c = refine_2d(r, g, BWD, KNOWN);
+      if (c == kSkip) return kSkip;
+      amb = c == kAmbiguous;
     }
-    if (!amb) {
-      geom_2d_solve(r, g);
-      if (!KNOWN && g.arg < kArgMinAlpha - (exact ? kCoarse2D : 0.f)) return kSkip;
-      if (exact && ((!KNOWN && g.arg <= kArgMinAlpha + kCoarse2D) ||
-                    (BWD && (fabsf(g.arg - kArgClamp) <= kCoarse2D ||
-                             fabsf(g.dray - g.dscr) <= 0.02f * (g.dray + g.dscr))))) {
-        // coarse band hit: the precise bound usually separates the decision
-        const int c = refine_2d(r, g, BWD, KNOWN);
-        if (c == kSkip) return kSkip;
-        amb = c == kAmbiguous;
-      }
-      p.ray = g.ray;
-    }
+    p.ray = g.ray;
     if (BWD) {
       p.hu0 = g.hu0; p.hu1 = g.hu1; p.hu3 = g.hu3;
       p.hv0 = g.hv0; p.hv1 = g.hv1; p.hv3 = g.hv3;
-      if (amb && near_degenerate(g)) geom_2d_solve(r, g);
       p.inv_den = g.inv_den;
       p.u = g.u;
       p.v = g.v;
