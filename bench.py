@@ -29,7 +29,7 @@ REPO = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, REPO)
 
 MEASURED_PEAKS = os.path.join(REPO, "MEASURED_PEAKS.json")
-NCU_TAG = "r01h"  # profiles/ncu_<tag>_kernels.json: the committed capture the roofline limiter quotes
+NCU_TAG = "r01i"  # profiles/ncu_<tag>_kernels.json: the committed capture the roofline limiter quotes
 METRIC = "hybrid-GS frames/s fwd & iters/s fwd+bwd at 1M Gaussians 1080p; 1/2/4/8 B200"
 N_SM = 148
 FMA_PER_SM_CLK = 128
