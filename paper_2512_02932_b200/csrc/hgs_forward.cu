@@ -119,14 +119,22 @@ __device__ __forceinline__ void write_record(const ProjD &o, uint32_t idx, Splat
     // offset (p, q), a sum of non-negative terms (the (a, b, c) form cancels
     // catastrophically for elongated splats at the cutoff)
     // eigenvector of the larger eigenvalue from the row of (Q - l1 I) without
-    // cancellation; the smaller eigenvalue as det / l1
+    // cancellation; l2 = mean - h directly (its float64 cancellation, ~1e-16
+    // l1, is far below the float32 the record keeps); no divisions
     const double A = o.conic[0], B = o.conic[1], C = o.conic[2];
     const double hd = 0.5 * (A - C), h = sqrt(hd * hd + B * B);
-    const double l1 = 0.5 * (A + C) + h, l2 = l1 > 0.0 ? (A * C - B * B) / l1 : 0.0;
+    const double l1 = 0.5 * (A + C) + h, l2 = 0.5 * (A + C) - h;
     double vx = hd >= 0.0 ? hd + h : B, vy = hd >= 0.0 ? B : h - hd;
-    const double vn = sqrt(vx * vx + vy * vy);
-    if (vn > 0.0) { vx /= vn; vy /= vn; } else { vx = 1.0; vy = 0.0; }
-    r.r1 = make_float4((float)vx, (float)vy, (float)l1, (float)l2);
+    const double vq = vx * vx + vy * vy;
+    if (vq > 0.0) {
+      const double rn = rsqrt(vq);
+      vx *= rn;
+      vy *= rn;
+    } else {
+      vx = 1.0;
+      vy = 0.0;
+    }
+    r.r1 = make_float4((float)vx, (float)vy, (float)l1, (float)fmax(l2, 0.0));
     r.r2 = make_float4(0.f, 0.f, 0.f, 0.f);
     r.r3 = make_float4(0.f, (float)o.color[0], (float)o.color[1], (float)o.color[2]);
   } else {
