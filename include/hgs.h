@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define HGS_ABI_VERSION 1
+#define HGS_ABI_VERSION 2
 
 typedef enum hgs_status {
   HGS_OK = 0,
@@ -49,7 +49,16 @@ typedef enum hgs_status {
 
 /* Scene in structure-of-arrays layout, float32 (reference: core/types.py:32-50,
  * float64 there).  sh is (n, 3, sh_bases) channel-major; type_spec 0 = 2D surfel,
- * 1 = 3D Gaussian. */
+ * 1 = 3D Gaussian.
+ *
+ * The four *64 pointers are an optional float64 copy of the geometry (all four
+ * or none).  When they are set, every discrete decision of the forward -- depth
+ * keys and order, near / singular / quaternion culls, bounding boxes, tile
+ * lists and the float64 re-checks of the compositors -- is taken on these exact
+ * values, i.e. on the reference's float64 inputs (core/types.py:40-45), and the
+ * exported SplatFrame arrays are computed from them.  The float32 fields must
+ * then hold their float32 rounding: the compositor records' float32 payload and
+ * the chain rule read those.  Without them the float32 fields are the inputs. */
 typedef struct hgs_scene {
   int64_t n;
   int32_t sh_bases; /* (degree + 1)^2, degree <= 3 */
@@ -60,6 +69,10 @@ typedef struct hgs_scene {
   const float *opacity_logit; /* (n) */
   const float *sh;            /* (n, 3, sh_bases) */
   const uint8_t *type_spec;   /* (n) */
+  const double *center64;        /* (n, 3) nullable [ABI 2] */
+  const double *log_scale64;     /* (n, 3) nullable */
+  const double *rotation64;      /* (n, 4) nullable */
+  const double *opacity_logit64; /* (n)    nullable */
 } hgs_scene;
 
 /* Pinhole camera (core/types.py:145-197); pixel (ix, iy) samples (ix+.5, iy+.5). */
@@ -161,6 +174,13 @@ typedef struct hgs_exchange_report {
 
 int hgs_exchange(int64_t n, float *log_scale, float *rotation, uint8_t *type_spec, double theta_e, float *eranks,
                  void *scratch, hgs_exchange_report *report, void *stream);
+
+/* The same pass on float64 device arrays (the reference's own precision,
+ * exchange.py:58-99): host scenes are exchanged through this entry point so
+ * that only the flipped rows change and the demoted rows get the float64
+ * reparameterisation.  eranks (n) double out (nullable). */
+int hgs_exchange_f64(int64_t n, double *log_scale, double *rotation, uint8_t *type_spec, double theta_e,
+                     double *eranks, void *scratch, hgs_exchange_report *report, void *stream);
 
 /* Test / API-parity export of the sorted SplatFrame (raster/project.py:60-90)
  * into caller device buffers (each nullable): idx (m) i32, typ (m) u8,

@@ -25,6 +25,7 @@ owner, which every view's base chain keeps alive), the way a caching
 allocator recycles device memory.
 """
 
+import ctypes
 import mmap
 import threading
 import weakref
@@ -36,19 +37,6 @@ _POOL_CAP = 8 << 30        # bytes of idle mappings kept for reuse
 _pool = {}                 # nbytes -> [mmap]
 _pool_bytes = [0]
 _pool_lock = threading.Lock()
-
-
-class _HostBlock:
-    """Buffer owner of one pooled mapping (PEP 688 buffer export)."""
-
-    def __init__(self, mm):
-        self.mm = mm
-
-    def __buffer__(self, flags):
-        return memoryview(self.mm)
-
-    def __release_buffer__(self, view):
-        view.release()
 
 
 def _recycle(mm, nbytes):
@@ -76,7 +64,10 @@ def host_empty(shape, dtype=np.float64):
             _pool_bytes[0] -= size
     if mm is None:
         mm = mmap.mmap(-1, size)
-    owner = _HostBlock(mm)
+    # buffer owner of the mapping: a ctypes array exports the buffer protocol
+    # on every supported Python (3.10+) and is weak-referenceable, so the
+    # finalizer runs when the last numpy view of it is gone
+    owner = (ctypes.c_char * size).from_buffer(mm)
     weakref.finalize(owner, _recycle, mm, size)
     return np.frombuffer(owner, dtype=dtype, count=n).reshape(shape)
 

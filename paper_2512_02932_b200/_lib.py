@@ -13,6 +13,8 @@ from .errors import (ConfigError, DegenerateScaleError, ExtensionError, Integrit
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("HGS_LIB", os.path.join(_HERE, "libhgs.so"))
 
+ABI_VERSION = 2  # include/hgs.h HGS_ABI_VERSION
+
 HGS_OK = 0
 HGS_ERR_CONFIG = 1
 HGS_ERR_INVALID_PARAMETER = 2
@@ -35,6 +37,7 @@ COMBINE_MODES = {"projection": 0, "naive": 1, "mask": 2}
 # Every symbol include/hgs.h and include/hgs_train.h declare.
 EXPORTS = ("hgs_abi_version", "hgs_status_string", "hgs_frame_bytes", "hgs_forward",
            "hgs_backward_scratch_bytes", "hgs_backward_det_scratch_bytes", "hgs_backward", "hgs_exchange",
+           "hgs_exchange_f64",
            "hgs_frame_export_arrays", "hgs_blend_log", "hgs_frame_stats",
            "hgs_loss_scratch_bytes", "hgs_image_losses", "hgs_dwt_level1", "hgs_dwt_inverse",
            "hgs_combine_gradients", "hgs_adam_step", "hgs_combine_adam_step",
@@ -48,7 +51,9 @@ _i32 = ctypes.c_int32
 class Scene(ctypes.Structure):
     _fields_ = [("n", _i64), ("sh_bases", _i32), ("reserved", _i32),
                 ("center", _vp), ("log_scale", _vp), ("rotation", _vp),
-                ("opacity_logit", _vp), ("sh", _vp), ("type_spec", _vp)]
+                ("opacity_logit", _vp), ("sh", _vp), ("type_spec", _vp),
+                ("center64", _vp), ("log_scale64", _vp), ("rotation64", _vp),
+                ("opacity_logit64", _vp)]
 
 
 class Camera(ctypes.Structure):
@@ -146,6 +151,7 @@ def lib():
                                _vp, _vp, _vp, ctypes.c_size_t, _vp, _vp, _vp]
     L.hgs_exchange.argtypes = [_i64, _vp, _vp, _vp, ctypes.c_double, _vp, _vp, P(ExchangeReport),
                                _vp]
+    L.hgs_exchange_f64.argtypes = L.hgs_exchange.argtypes
     L.hgs_frame_export_arrays.argtypes = [P(Scene), P(Camera), P(Settings), _vp, P(FrameInfo),
                                           P(FrameExport), _vp]
     L.hgs_blend_log.argtypes = [P(Scene), P(Camera), P(Settings), _vp, P(FrameInfo), _vp, _vp,
@@ -168,7 +174,7 @@ def lib():
                                    P(_i64), P(_i64), _vp]
     L.hgs_densify_apply.argtypes = [P(Scene), _vp, _vp, _vp, P(DensifyCfg), P(Params), _vp, _vp, _vp,
                                     _vp]
-    if L.hgs_abi_version() != 1:
+    if L.hgs_abi_version() != ABI_VERSION:
         _load_error = "libhgs.so ABI version mismatch"
         raise ExtensionError(_load_error)
     _lib = L
@@ -210,9 +216,13 @@ def current_stream_handle(device=None):
 
 
 def scene_struct(ds):
+    """hgs_scene of a DeviceGaussians; carries the float64 geometry when the
+    scene has a current one (DeviceGaussians.geom64)."""
+    g = ds.geom64_current()
+    g64 = [t.data_ptr() for t in g] if g is not None else [None] * 4
     return Scene(ds.count, ds.sh_bases, 0, ds.center.data_ptr(), ds.log_scale.data_ptr(),
                  ds.rotation.data_ptr(), ds.opacity_logit.data_ptr(), ds.sh_coeffs.data_ptr(),
-                 ds.type_spec.data_ptr())
+                 ds.type_spec.data_ptr(), *g64)
 
 
 def camera_struct(cam):

@@ -122,6 +122,13 @@ class DeviceGaussians:
     rotation (N,4) w-first, opacity_logit (N,), sh_coeffs (N,3,B), type_spec
     (N,) -- 4(11+3B)+1 bytes per Gaussian (237 B at SH degree 3).  Tensors are
     used in place; the optimizer may update them between calls.
+
+    ``geom64`` optionally holds the float64 geometry (center, log_scale,
+    rotation, opacity_logit) a host ``GaussianSet`` was uploaded from: while
+    it is current (no in-place update of the float32 fields since), the
+    forward takes every discrete decision -- depth order, culls, bounding
+    boxes, tile lists, the float64 re-checks -- on those exact values, as the
+    reference does on its float64 inputs (core/types.py:40-45; hgs.h).
     """
 
     FIELDS = GaussianSet.FIELDS
@@ -137,13 +144,20 @@ class DeviceGaussians:
         self.sh_coeffs = sh_coeffs.to(dev, torch.float32).contiguous()
         self.type_spec = type_spec.to(dev, torch.uint8).contiguous()
         self.extent = float(extent)
+        self.geom64 = None
+        self._geom64_versions = None
         if validate:
             self.validate()
 
+    GEOM_FIELDS = ("center", "log_scale", "rotation", "opacity_logit")
+
     @classmethod
-    def from_host(cls, scene, device="cuda", validate=False):
-        """Upload a host scene: float64 -> float32 on the host cores into
-        pinned staging, pipelined with the DMA (_hostio.upload)."""
+    def from_host(cls, scene, device="cuda", validate=False, geom64=True):
+        """Upload a host scene through pinned staging, pipelined with the DMA
+        (_hostio.upload).  The geometry crosses as float64 (kept as ``geom64``
+        for the exact decisions, its float32 rounding made on the device);
+        SH coefficients are converted to float32 on the host cores.
+        ``geom64=False`` uploads float32 geometry only."""
         import torch
 
         from ._hostio import upload
@@ -151,11 +165,21 @@ class DeviceGaussians:
             device = torch.device(device)
         if device.type == "cuda" and device.index is None:
             device = torch.device("cuda", torch.cuda.current_device())
-        t = upload([(scene.center, torch.float32), (scene.log_scale, torch.float32),
-                    (scene.rotation, torch.float32), (scene.opacity_logit, torch.float32),
-                    (scene.sh_coeffs, torch.float32), (scene.type_spec, torch.uint8)],
-                   device, tag="scene")
-        return cls(*t, extent=scene.extent, validate=validate)
+        gdt = torch.float64 if geom64 else torch.float32
+        t = upload([(scene.center, gdt), (scene.log_scale, gdt), (scene.rotation, gdt),
+                    (scene.opacity_logit, gdt), (scene.sh_coeffs, torch.float32),
+                    (scene.type_spec, torch.uint8)], device, tag="scene")
+        out = cls(*t, extent=scene.extent, validate=validate)
+        if geom64:
+            out.geom64 = tuple(t[:4])
+            out._geom64_versions = out.versions()
+        return out
+
+    def geom64_current(self):
+        """The float64 geometry if it still describes the float32 fields."""
+        if self.geom64 is None or self.versions() != self._geom64_versions:
+            return None
+        return self.geom64
 
     def to_host(self):
         return GaussianSet(*(getattr(self, f).detach().cpu().numpy() for f in self.FIELDS),

@@ -100,6 +100,11 @@ SceneView make_scene(const hgs_scene &s) {
   SceneView v;
   v.center = s.center; v.log_scale = s.log_scale; v.rotation = s.rotation; v.opacity_logit = s.opacity_logit;
   v.sh = s.sh; v.type_spec = s.type_spec; v.n = s.n; v.sh_bases = s.sh_bases;
+  const bool g64 = s.center64 && s.log_scale64 && s.rotation64 && s.opacity_logit64;
+  v.center64 = g64 ? s.center64 : nullptr;
+  v.log_scale64 = g64 ? s.log_scale64 : nullptr;
+  v.rotation64 = g64 ? s.rotation64 : nullptr;
+  v.opacity_logit64 = g64 ? s.opacity_logit64 : nullptr;
   return v;
 }
 
@@ -226,9 +231,8 @@ int hgs_forward(const hgs_scene *scene, const hgs_camera *camera, const hgs_sett
   uint32_t *rank_of = at<uint32_t>(frame, L.vals_b);
   int64_t m = 0;
   if (n > 0) {
-    k_depth_keys<<<grid_for(n, 256), 256, 0, s>>>(sc, cam, at<unsigned long long>(frame, L.keys_a),
-                                                  at<uint32_t>(frame, L.vals_a), at<uint32_t>(frame, L.hist_d), st);
-    HGS_LAUNCHED();
+    HGS_CUDA(launch_depth_keys(sc, cam, at<unsigned long long>(frame, L.keys_a), at<uint32_t>(frame, L.vals_a),
+                               at<uint32_t>(frame, L.hist_d), st, grid_for(n, 256), s));
     k_radix_offsets<<<8, kRadix, 0, s>>>(at<uint32_t>(frame, L.hist_d), at<uint32_t>(frame, L.off_d));
     HGS_LAUNCHED();
     // one device-to-host copy: the state block and the digit histograms are
@@ -261,6 +265,7 @@ int hgs_forward(const hgs_scene *scene, const hgs_camera *camera, const hgs_sett
     if (rc) return rc;
     vals_sorted = at<uint32_t>(frame, in_b ? L.vals_b : L.vals_a);
     rank_of = at<uint32_t>(frame, in_b ? L.vals_a : L.vals_b);  // the free ping-pong buffer
+    info->internal[1] = in_b ? 1u : 2u;  // where rank_of lives (the backward's chain rule reads it)
     info->internal[2] = (uint32_t)np;  // depth-sort passes (diagnostics / launch count)
   }
   info->m = m;
@@ -380,7 +385,8 @@ size_t hgs_backward_scratch_bytes(int64_t n, int32_t kg) {
   if (n < 0 || kg < 1) return 0;
   const int64_t kc = std::min<int32_t>(kg, 4);
   const int64_t nn = std::max<int64_t>(n, 1);
-  return (size_t)(((nn * kc * 16 * 4 + 255) & ~255ll) + ((nn * kc * 4 * 4 + 255) & ~255ll) + ((nn + 255) & ~255ll));
+  constexpr int64_t A = sizeof(acc_t);
+  return (size_t)(((nn * kc * 16 * A + 255) & ~255ll) + ((nn * kc * 4 * A + 255) & ~255ll) + ((nn + 255) & ~255ll));
 }
 
 }  // extern "C"
@@ -465,8 +471,9 @@ int hgs_backward(const hgs_scene *scene, const hgs_camera *camera, const hgs_set
   const bool ext = depth_grads || normal_grads || alpha_grads;
   const int kc_max = std::min<int32_t>(kg, 4);
   const int64_t nn = std::max<int64_t>(n, 1);
-  float *acc = static_cast<float *>(scratch);
-  float *acc_ext = reinterpret_cast<float *>(static_cast<char *>(scratch) + ((nn * kc_max * 16 * 4 + 255) & ~255ll));
+  acc_t *acc = static_cast<acc_t *>(scratch);
+  acc_t *acc_ext =
+      reinterpret_cast<acc_t *>(static_cast<char *>(scratch) + ((nn * kc_max * 16 * (int64_t)sizeof(acc_t) + 255) & ~255ll));
   HGS_CUDA(record_event(settings, 0, s));
   HGS_CUDA(cudaMemsetAsync(touched, 0, (size_t)nn, s));
   BwdArgs b;
@@ -481,12 +488,15 @@ int hgs_backward(const hgs_scene *scene, const hgs_camera *camera, const hgs_set
                                  at<Rec64>(const_cast<void *>(frame), FL.recs64), b.c.st);
   }
   HGS_LAUNCHED();
-  const ChainArgs c0{sc, cam, mod, acc, ext ? acc_ext : nullptr, 0, nullptr};
+  const Layout FLc = make_layout(info->n, info->width, info->height, info->pair_capacity);
+  const uint32_t *rank_of =
+      info->internal[1] ? at<uint32_t>(frame, info->internal[1] == 1 ? FLc.vals_a : FLc.vals_b) : nullptr;
+  const ChainArgs c0{sc, cam, mod, acc, ext ? acc_ext : nullptr, 0, nullptr, rank_of, at<SplatRec>(frame, FLc.recs)};
   for (int k0 = 0; k0 < kg; k0 += 4) {
     const int kc = std::min(4, kg - k0);
-    HGS_CUDA(cudaMemsetAsync(acc, 0, (size_t)nn * kc * 16 * 4, s));
+    HGS_CUDA(cudaMemsetAsync(acc, 0, (size_t)nn * kc * 16 * sizeof(acc_t), s));
     HGS_CUDA(cudaMemsetAsync(&b.c.st->n_fix_bwd, 0, sizeof(uint32_t), s));
-    if (ext) HGS_CUDA(cudaMemsetAsync(acc_ext, 0, (size_t)nn * kc * 4 * 4, s));
+    if (ext) HGS_CUDA(cudaMemsetAsync(acc_ext, 0, (size_t)nn * kc * 4 * sizeof(acc_t), s));
     b.pix_grad = pixel_grads + (int64_t)k0 * HW * 3;
     b.depth_grad = depth_grads ? depth_grads + (int64_t)k0 * HW : nullptr;
     b.normal_grad = normal_grads ? normal_grads + (int64_t)k0 * HW * 3 : nullptr;
@@ -555,28 +565,43 @@ int hgs_backward(const hgs_scene *scene, const hgs_camera *camera, const hgs_set
   return HGS_OK;
 }
 
-int hgs_exchange(int64_t n, float *log_scale, float *rotation, uint8_t *type_spec, double theta_e, float *eranks,
-                 void *scratch, hgs_exchange_report *report, void *stream) {
+}  // extern "C"
+
+namespace {
+template <typename T>
+int exchange_impl(int64_t n, T *log_scale, T *rotation, uint8_t *type_spec, double theta_e, T *eranks, void *scratch,
+                  hgs_exchange_report *report, void *stream) {
   if (n < 0 || !report || !scratch || !(theta_e > 1.0 && theta_e < 3.0)) return HGS_ERR_CONFIG;
   memset(report, 0, sizeof(*report));
   if (n == 0) return HGS_OK;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   ExchangeState *st = static_cast<ExchangeState *>(scratch);
   HGS_CUDA(cudaMemsetAsync(st, 0, sizeof(ExchangeState), s));
-  k_exchange_scan<<<grid_for(n, 256), 256, 0, s>>>(n, log_scale, type_spec, theta_e, eranks, st);
-  HGS_LAUNCHED();
+  HGS_CUDA(launch_exchange_scan<T>(n, log_scale, type_spec, theta_e, eranks, st, grid_for(n, 256), s));
   ExchangeState h;
   HGS_CUDA(cudaMemcpyAsync(&h, st, sizeof(h), cudaMemcpyDeviceToHost, s));
   HGS_CUDA(cudaStreamSynchronize(s));
   if (h.counts[3]) return HGS_ERR_DEGENERATE_SCALE;
-  k_exchange_apply<<<grid_for(n, 256), 256, 0, s>>>(n, log_scale, rotation, type_spec, theta_e);
-  HGS_LAUNCHED();
+  HGS_CUDA(launch_exchange_apply<T>(n, log_scale, rotation, type_spec, theta_e, grid_for(n, 256), s));
   report->n_3d_to_2d = (int64_t)h.counts[0];
   report->n_2d_to_3d = (int64_t)h.counts[1];
   report->n_3d = (int64_t)h.counts[2] - (int64_t)h.counts[0] + (int64_t)h.counts[1];
   report->n_2d = n - report->n_3d;
   for (int b = 0; b < 20; ++b) report->erank_hist[b] = (int64_t)h.hist[b];
   return HGS_OK;
+}
+}  // namespace
+
+extern "C" {
+
+int hgs_exchange(int64_t n, float *log_scale, float *rotation, uint8_t *type_spec, double theta_e, float *eranks,
+                 void *scratch, hgs_exchange_report *report, void *stream) {
+  return exchange_impl<float>(n, log_scale, rotation, type_spec, theta_e, eranks, scratch, report, stream);
+}
+
+int hgs_exchange_f64(int64_t n, double *log_scale, double *rotation, uint8_t *type_spec, double theta_e,
+                     double *eranks, void *scratch, hgs_exchange_report *report, void *stream) {
+  return exchange_impl<double>(n, log_scale, rotation, type_spec, theta_e, eranks, scratch, report, stream);
 }
 
 }  // extern "C"
@@ -590,7 +615,8 @@ __global__ void k_export_frame(SceneView sc, CamD cam, ModD mod, const SplatRec 
   for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < m; r += (int64_t)gridDim.x * blockDim.x) {
     const uint32_t i = __float_as_uint(recs[r].r4.w) & 0x7fffffffu;
     ProjD p;
-    project_d(sc, i, cam, mod, p);
+    if (sc.center64) project_d<true, false, true>(sc, i, cam, mod, p);
+    else project_d(sc, i, cam, mod, p);
     bbox_d(p, cam.width, cam.height);
     if (o.idx) o.idx[r] = (int32_t)i;
     if (o.typ) o.typ[r] = (uint8_t)p.typ;

@@ -130,7 +130,7 @@ __global__ void __launch_bounds__(kChainThreads, HGS_CHAIN_MINB) k_chain_rule_t(
         for (int l = lane; l * 128 < nc * SB * 4; l += kChainThreads)
           asm volatile("prefetch.global.L2 [%0];" ::"l"(sh0 + 128 * l));
         const char *ac0 = reinterpret_cast<const char *>(c.acc + nb * c.kg * kAcc);
-        for (int l = lane; l * 128 < nc * c.kg * kAcc * 4; l += kChainThreads)
+        for (int l = lane; l * 128 < nc * c.kg * kAcc * (int)sizeof(acc_t); l += kChainThreads)
           asm volatile("prefetch.global.L2 [%0];" ::"l"(ac0 + 128 * l));
         const char *ptr = nullptr;
         if (lane < 3) ptr = reinterpret_cast<const char *>(c.sc.center + 3 * nb) + 128 * lane;
@@ -148,15 +148,19 @@ __global__ void __launch_bounds__(kChainThreads, HGS_CHAIN_MINB) k_chain_rule_t(
     bool any = false;
     if (valid) {
       for (int k = 0; k < c.kg; ++k) {
-        const float4 *a4 = reinterpret_cast<const float4 *>(c.acc + ((int64_t)i * c.kg + k) * kAcc);
+        const double2 *a2 = reinterpret_cast<const double2 *>(c.acc + ((int64_t)i * c.kg + k) * kAcc);
 #pragma unroll
-        for (int s = 0; s < 4; ++s) {
-          const float4 x = a4[s];
-          any |= (x.x != 0.f) | (x.y != 0.f) | (x.z != 0.f) | (x.w != 0.f);
+        for (int s = 0; s < 8; ++s) {
+          const double2 x = a2[s];
+          any |= (x.x != 0.0) | (x.y != 0.0);
         }
         if (c.acc_ext) {
-          const float4 x = *reinterpret_cast<const float4 *>(c.acc_ext + ((int64_t)i * c.kg + k) * kAccExt);
-          any |= (x.x != 0.f) | (x.y != 0.f) | (x.z != 0.f) | (x.w != 0.f);
+          const double2 *e2 = reinterpret_cast<const double2 *>(c.acc_ext + ((int64_t)i * c.kg + k) * kAccExt);
+#pragma unroll
+          for (int s = 0; s < 2; ++s) {
+            const double2 x = e2[s];
+            any |= (x.x != 0.0) | (x.y != 0.0);
+          }
         }
       }
     }
@@ -229,11 +233,11 @@ __global__ void __launch_bounds__(kChainThreads, HGS_CHAIN_MINB) k_chain_rule_t(
         for (int s = 0; s < SB; ++s) so[s] = 0.f;
       }
       if (any) {
-      const float *A = c.acc + ((int64_t)i * c.kg + k) * kAcc;
+      const acc_t *A = c.acc + ((int64_t)i * c.kg + k) * kAcc;
       float d_center[3] = {0.f, 0.f, 0.f}, d_ls[3] = {0.f, 0.f, 0.f};
       float d_R[9] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
       // SH (core/sh.py:125-141)
-      const float up0 = A[0] * mask0, up1 = A[1] * mask1, up2 = A[2] * mask2;
+      const float up0 = (float)A[0] * mask0, up1 = (float)A[1] * mask1, up2 = (float)A[2] * mask2;
       float db[16];
 #pragma unroll
       for (int bb = 0; bb < B; ++bb) {
@@ -250,67 +254,91 @@ __global__ void __launch_bounds__(kChainThreads, HGS_CHAIN_MINB) k_chain_rule_t(
       d_center[1] += (gdy - dot * vy) * idist;
       d_center[2] += (gdz - dot * vz) * idist;
       // opacity: A[3] = dL/dalpha_eff * alpha_eff (exchange.py:114-129 folded in)
-      const float Aal = A[3];
+      const float Aal = (float)A[3];
       const float d_logit = Aal * (1.f - alpha);
-      // projected centre (backward.py:121-126)
-      const float gx = A[4], gy = A[5];
-      const float iz = 1.f / Z, iz2 = iz * iz;
-      float dX = gx * fx * iz, dY = gy * fy * iz;
-      float dZ = -(gx * fx * X + gy * fy * Y) * iz2;
+      // projected centre (backward.py:121-126) and, for 3D, the EWA Jacobian
+      // chain (backward.py:128-150) in float64: for a near-camera, far
+      // off-axis Gaussian the dZ terms of dJ cancel by ~100x, so float32
+      // here costs ~1e-3 of the result (the accumulators are float64 too)
+      double gx = A[4], gy = A[5];
+      double G00 = 0.0, G01 = 0.0, G11 = 0.0;
       if (is3d) {
-        // backward.py:128-150
-        const float J02 = -fx * X * iz2, J12 = -fy * Y * iz2;
-        float U[6];
+        // slots 4-8 hold the eigenbasis sums (pair_grads); rotate them with
+        // the record's own float32 (c, s) -- the basis the pairs used -- to
+        // pixel axes, v = M w with M = [[c, -s], [s, c]], in float64, and
+        // store the pixel-axis values back for the densification statistics
+        const float4 e = __ldg(&c.recs[c.rank_of[i]].r1);
+        const double cs = e.x, sn = e.y;
+        const double Sp = A[4], Sq = A[5], Gpp = A[6], Gpq = A[7], Gqq = A[8];
+        gx = cs * Sp - sn * Sq;
+        gy = sn * Sp + cs * Sq;
+        G00 = (cs * cs * Gpp - 2.0 * cs * sn * Gpq) + sn * sn * Gqq;
+        G01 = (cs * sn * Gpp + (cs * cs - sn * sn) * Gpq) - cs * sn * Gqq;
+        G11 = (sn * sn * Gpp + 2.0 * cs * sn * Gpq) + cs * cs * Gqq;
+        acc_t *Aw = c.acc + ((int64_t)i * c.kg + k) * kAcc;
+        Aw[4] = gx; Aw[5] = gy; Aw[6] = G00; Aw[7] = G01; Aw[8] = G11;
+      }
+      const double Xd = td[0], Yd = td[1], Zd = td[2];
+      const double fxd = cam.fx, fyd = cam.fy;
+      const double iz = 1.0 / Zd, iz2 = iz * iz;
+      double dX = gx * fxd * iz, dY = gy * fyd * iz;
+      double dZ = -(gx * fxd * Xd + gy * fyd * Yd) * iz2;
+      if (is3d) {
+        const double J02 = -fxd * Xd * iz2, J12 = -fyd * Yd * iz2;
+        double U[6];
 #pragma unroll
         for (int cc = 0; cc < 3; ++cc) {
-          U[cc] = fx * iz * V[cc] + J02 * V[6 + cc];
-          U[3 + cc] = fy * iz * V[3 + cc] + J12 * V[6 + cc];
+          U[cc] = fxd * iz * cam.V[cc] + J02 * cam.V[6 + cc];
+          U[3 + cc] = fyd * iz * cam.V[3 + cc] + J12 * cam.V[6 + cc];
         }
-        const float D0 = sv0 * sv0, D1 = sv1 * sv1, D2 = sv2 * sv2;
-        const float G00 = A[6], G01 = A[7], G11 = A[8];
-        float GU[6];
+        const double D0 = (double)sv0 * sv0, D1 = (double)sv1 * sv1, D2 = (double)sv2 * sv2;
+        double GU[6];
 #pragma unroll
         for (int l = 0; l < 3; ++l) {
           GU[l] = G00 * U[l] + G01 * U[3 + l];
           GU[3 + l] = G01 * U[l] + G11 * U[3 + l];
         }
-        float dS[9];  // U^T G U
+        double dS[9];  // U^T G U
 #pragma unroll
         for (int a = 0; a < 3; ++a)
 #pragma unroll
           for (int l = 0; l < 3; ++l) dS[a * 3 + l] = U[a] * GU[l] + U[3 + a] * GU[3 + l];
-        float Sig[9];  // R D R^T
+        double Rd[9];
+#pragma unroll
+        for (int a = 0; a < 9; ++a) Rd[a] = R[a];
+        double Sig[9];  // R D R^T
 #pragma unroll
         for (int a = 0; a < 3; ++a)
 #pragma unroll
           for (int l = 0; l < 3; ++l)
-            Sig[a * 3 + l] = (R[a * 3] * D0 * R[l * 3] + R[a * 3 + 1] * D1 * R[l * 3 + 1]) + R[a * 3 + 2] * D2 * R[l * 3 + 2];
-        float dJ[6];  // dU V^T, dU = 2 G U Sigma
+            Sig[a * 3 + l] = (Rd[a * 3] * D0 * Rd[l * 3] + Rd[a * 3 + 1] * D1 * Rd[l * 3 + 1]) + Rd[a * 3 + 2] * D2 * Rd[l * 3 + 2];
+        double dJ[6];  // dU V^T, dU = 2 G U Sigma
 #pragma unroll
         for (int a = 0; a < 2; ++a) {
-          float dU[3];
+          double dU[3];
 #pragma unroll
           for (int l = 0; l < 3; ++l)
-            dU[l] = 2.f * ((GU[a * 3] * Sig[l] + GU[a * 3 + 1] * Sig[3 + l]) + GU[a * 3 + 2] * Sig[6 + l]);
+            dU[l] = 2.0 * ((GU[a * 3] * Sig[l] + GU[a * 3 + 1] * Sig[3 + l]) + GU[a * 3 + 2] * Sig[6 + l]);
 #pragma unroll
-          for (int cc = 0; cc < 3; ++cc) dJ[a * 3 + cc] = (dU[0] * V[cc * 3] + dU[1] * V[cc * 3 + 1]) + dU[2] * V[cc * 3 + 2];
+          for (int cc = 0; cc < 3; ++cc)
+            dJ[a * 3 + cc] = (dU[0] * cam.V[cc * 3] + dU[1] * cam.V[cc * 3 + 1]) + dU[2] * cam.V[cc * 3 + 2];
         }
-        const float iz3 = iz2 * iz;
-        dX += dJ[2] * (-fx * iz2);
-        dY += dJ[5] * (-fy * iz2);
-        dZ += ((dJ[0] * (-fx * iz2) + dJ[4] * (-fy * iz2)) + dJ[2] * (2.f * fx * X * iz3)) + dJ[5] * (2.f * fy * Y * iz3);
-        const float Dv[3] = {D0, D1, D2};
+        const double iz3 = iz2 * iz;
+        dX += dJ[2] * (-fxd * iz2);
+        dY += dJ[5] * (-fyd * iz2);
+        dZ += ((dJ[0] * (-fxd * iz2) + dJ[4] * (-fyd * iz2)) + dJ[2] * (2.0 * fxd * Xd * iz3)) + dJ[5] * (2.0 * fyd * Yd * iz3);
+        const double Dv[3] = {D0, D1, D2};
 #pragma unroll
         for (int a = 0; a < 3; ++a)
 #pragma unroll
           for (int kk = 0; kk < 3; ++kk)
-            d_R[a * 3 + kk] += 2.f * ((dS[a * 3] * R[kk] + dS[a * 3 + 1] * R[3 + kk]) + dS[a * 3 + 2] * R[6 + kk]) * Dv[kk];
+            d_R[a * 3 + kk] += (float)(2.0 * ((dS[a * 3] * Rd[kk] + dS[a * 3 + 1] * Rd[3 + kk]) + dS[a * 3 + 2] * Rd[6 + kk]) * Dv[kk]);
 #pragma unroll
         for (int a = 0; a < 3; ++a) {
-          float s2 = 0.f;
+          double s2 = 0.0;
 #pragma unroll
-          for (int j = 0; j < 3; ++j) s2 += R[j * 3 + a] * ((dS[j * 3] * R[a] + dS[j * 3 + 1] * R[3 + a]) + dS[j * 3 + 2] * R[6 + a]);
-          d_ls[a] += 2.f * Dv[a] * s2;
+          for (int j = 0; j < 3; ++j) s2 += Rd[j * 3 + a] * ((dS[j * 3] * Rd[a] + dS[j * 3 + 1] * Rd[3 + a]) + dS[j * 3 + 2] * Rd[6 + a]);
+          d_ls[a] += (float)(2.0 * Dv[a] * s2);
         }
       } else {
         // 2D: slots 6-14 are dL/d(m0', m1', m3') in anchor-relative pixels;
@@ -346,14 +374,15 @@ __global__ void __launch_bounds__(kChainThreads, HGS_CHAIN_MINB) k_chain_rule_t(
         d_ls[2] += (float)((double)Aal * (-c.mod.lambda_z) * (gate + sz * gate * (1.0 - gate) / c.mod.t_z) * sz);
       }
       if (c.acc_ext) {
-        const float *E = c.acc_ext + ((int64_t)i * c.kg + k) * kAccExt;
+        const acc_t *E = c.acc_ext + ((int64_t)i * c.kg + k) * kAccExt;
         dZ += E[0];
+        const float E1 = (float)E[1], E2 = (float)E[2], E3 = (float)E[3];
 #pragma unroll
-        for (int a = 0; a < 3; ++a) d_R[a * 3 + ax] += sg * ((V[a] * E[1] + V[3 + a] * E[2]) + V[6 + a] * E[3]);
+        for (int a = 0; a < 3; ++a) d_R[a * 3 + ax] += sg * ((V[a] * E1 + V[3 + a] * E2) + V[6 + a] * E3);
       }
       // t_cam -> world centre
 #pragma unroll
-      for (int cc = 0; cc < 3; ++cc) d_center[cc] += (dX * V[cc] + dY * V[3 + cc]) + dZ * V[6 + cc];
+      for (int cc = 0; cc < 3; ++cc) d_center[cc] += (float)((dX * cam.V[cc] + dY * cam.V[3 + cc]) + dZ * cam.V[6 + cc]);
       // quaternion (rotation.py:79-107), then / |q| (backward.py:172)
 #define GR(ii, jj) d_R[(ii) * 3 + (jj)]
       const float dw = 2.f * (((((-zq * GR(0, 1) + y * GR(0, 2)) + zq * GR(1, 0)) - x * GR(1, 2)) - y * GR(2, 0)) + x * GR(2, 1));

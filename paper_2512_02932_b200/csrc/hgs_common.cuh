@@ -41,6 +41,29 @@ struct SceneView {
   const uint8_t *type_spec;
   int64_t n;
   int sh_bases;
+  // optional float64 geometry (hgs.h): the decisions of the forward are taken
+  // on these when set (all four or none)
+  const double *center64, *log_scale64, *rotation64, *opacity_logit64;
+};
+
+// Geometry loads of the float64 preprocess.  G64 = the scene carries the
+// float64 copy (the reference's own inputs); otherwise the float32 fields are
+// widened.  A template parameter, not a runtime test, so the float32 path's
+// code is unchanged.
+template <bool G64>
+struct SceneGeom {
+  static __device__ __forceinline__ double center(const SceneView &sc, int64_t i, int k) {
+    return G64 ? sc.center64[3 * i + k] : (double)sc.center[3 * i + k];
+  }
+  static __device__ __forceinline__ double log_scale(const SceneView &sc, int64_t i, int k) {
+    return G64 ? sc.log_scale64[3 * i + k] : (double)sc.log_scale[3 * i + k];
+  }
+  static __device__ __forceinline__ double rotation(const SceneView &sc, int64_t i, int k) {
+    return G64 ? sc.rotation64[4 * i + k] : (double)sc.rotation[4 * i + k];
+  }
+  static __device__ __forceinline__ double opacity_logit(const SceneView &sc, int64_t i) {
+    return G64 ? sc.opacity_logit64[i] : (double)sc.opacity_logit[i];
+  }
 };
 
 // Camera in float64, precomputed on the host.
@@ -60,8 +83,11 @@ struct ModD {
 // ---------------------------------------------------------------- records
 // Rank-ordered float32 splat record consumed by the compositors, 6 x 16 B.
 //  r0 = (lx, ly, depth, log2 alpha_eff) centre relative to anchor pixel
-//  r1 = 3D: (a, b, c, 0) conic            2D: (m0'0, m0'1, m0'3, m1'0)
-//  r2 = 2D: (m1'1, m1'3, m2_0, m2_1)      3D: unused
+//  r1 = 3D: (c, s, lambda_p, lambda_q) the conic's eigenbasis
+//       2D: (m0'0, m0'1, m0'3, m1'0)
+//  r2 = 2D: (m1'1, m1'3, m2_0, m2_1)
+//       3D: (P0, Q0, |P0| + |Q0|, 0) the anchor's offset from the centre in
+//           the eigenbasis (a 3D anchor is clamped to the image)
 //  r3 = (m2_3 | 0, red, green, blue)
 //  r4 = (nx, ny, nz, bits(idx | typ << 31))
 //  r5 = int: (x0 | y0 << 16, x1 | y1 << 16, anchor_x, anchor_y)
@@ -130,10 +156,11 @@ __device__ __forceinline__ bool quat_to_matrix_d(double qw, double qx, double qy
   return true;
 }
 
+template <bool G64 = false>
 __device__ __forceinline__ void load_center_d(const SceneView &sc, int64_t i, double *p) {
-  p[0] = sc.center[3 * i];
-  p[1] = sc.center[3 * i + 1];
-  p[2] = sc.center[3 * i + 2];
+  p[0] = SceneGeom<G64>::center(sc, i, 0);
+  p[1] = SceneGeom<G64>::center(sc, i, 1);
+  p[2] = SceneGeom<G64>::center(sc, i, 2);
 }
 
 __device__ __forceinline__ void t_cam_d(const CamD &cam, const double *p, double *t) {
@@ -196,22 +223,23 @@ struct ProjD {
 // float32 colour; the float64 path serves the exports and re-checks).
 // GEOM_ONLY skips the colour and the normal (the float64 pair re-checks need
 // only the geometry and alpha_eff).
-template <bool COLOR64 = true, bool GEOM_ONLY = false>
+// G64 reads the scene's float64 geometry (SceneView::center64 ...).
+template <bool COLOR64 = true, bool GEOM_ONLY = false, bool G64 = false>
 __device__ __forceinline__ void project_d(const SceneView &sc, int64_t i, const CamD &cam, const ModD &mod,
                                           ProjD &o, const float *sh_row = nullptr) {
+  using G = SceneGeom<G64>;
   double p[3];
-  load_center_d(sc, i, p);
+  load_center_d<G64>(sc, i, p);
   t_cam_d(cam, p, o.t);
   const double z = o.t[2];
   o.typ = sc.type_spec[i];
   o.ctr[0] = cam.fx * o.t[0] / z + cam.cx;
   o.ctr[1] = cam.fy * o.t[1] / z + cam.cy;
   double R[9];
-  o.quat_ok = quat_to_matrix_d(sc.rotation[4 * i], sc.rotation[4 * i + 1], sc.rotation[4 * i + 2],
-                               sc.rotation[4 * i + 3], R);
-  double s[3] = {exp((double)sc.log_scale[3 * i]), exp((double)sc.log_scale[3 * i + 1]),
-                 exp((double)sc.log_scale[3 * i + 2])};
-  o.alpha = expit_d((double)sc.opacity_logit[i]);
+  o.quat_ok = quat_to_matrix_d(G::rotation(sc, i, 0), G::rotation(sc, i, 1), G::rotation(sc, i, 2),
+                               G::rotation(sc, i, 3), R);
+  double s[3] = {exp(G::log_scale(sc, i, 0)), exp(G::log_scale(sc, i, 1)), exp(G::log_scale(sc, i, 2))};
+  o.alpha = expit_d(G::opacity_logit(sc, i));
   o.alpha_eff = o.alpha;
   o.valid = true;
   o.cov[0] = o.cov[1] = o.cov[2] = 0.0;

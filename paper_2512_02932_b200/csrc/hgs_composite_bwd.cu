@@ -17,7 +17,8 @@ namespace hgs {
 // Screen-space accumulator slots per (Gaussian, kg), float32:
 //  0-2 colour, 3 alpha (sum d_at * at = g_alpha_eff * alpha_eff),
 //  4-5 centre (3D Mahalanobis / 2D low-pass), 6-14 geometry:
-//  3D: 6-8 = dL/dcov2d (a, b, c);  2D ray: 6-8 = dL/dM0 (cols 0,1,3),
+//  3D: 4-5 and 6-8 = dL/dcentre and dL/dcov2d in the conic's eigenbasis
+//      (the chain rule rotates them to pixel axes in float64, in place);  2D ray: 6-8 = dL/dM0 (cols 0,1,3),
 //  9-11 = dL/dM1, 12-14 = dL/dM3 w.r.t. anchor-relative pixels; 15 unused.
 // Extension slots (separate array, 4 per (Gaussian, kg)): z, normal xyz.
 constexpr int kAcc = 16;
@@ -115,13 +116,17 @@ __device__ __forceinline__ void pair_grads(const SplatRec &r, const PairEval &p,
       const float da = d_at * at;  // = dL/dalpha_eff * alpha_eff * exp(-d/2)
       v[k][3] += da;
       if (is3d) {
-        const float4 e = r.r1;  // conic x offset = R^T (wp, wq) (eigenbasis, geom_3d)
-        const float vx = e.x * p.wp - e.y * p.wq, vy = e.y * p.wp + e.x * p.wq;
-        v[k][4] += vx * da;
-        v[k][5] += vy * da;
-        v[k][6] += 0.5f * da * vx * vx;
-        v[k][7] += 0.5f * da * vx * vy;
-        v[k][8] += 0.5f * da * vy * vy;
+        // in the conic's eigenbasis (w = (wp, wq) = Lambda (p, q), the
+        // conic times the offset, geom_3d): the chain rule rotates these
+        // sums back to pixel axes in float64.  Rotating per pair in float32
+        // instead drowns the long-axis components (wq ~ 1e-4 wp for an
+        // elongated splat) in the rounding of the short-axis ones.
+        v[k][4] += p.wp * da;
+        v[k][5] += p.wq * da;
+        const float hw = 0.5f * da;
+        v[k][6] += hw * p.wp * p.wp;
+        v[k][7] += hw * p.wp * p.wq;
+        v[k][8] += hw * p.wq * p.wq;
       } else if (p.ray) {
         const float du = -da * p.u, dv = -da * p.v;
         const float id = p.inv_den;
@@ -296,7 +301,7 @@ __global__ void __launch_bounds__(128, KG == 1 ? 5 : 4) k_composite_bwd_naive(Bw
         if (DET) {
           if (writer && rec < b.rec_cap) b.rec_pay[(size_t)rec * (KG * 20) + k * 20 + slot] = tot;
         } else if (writer && slot < nslots && tot != 0.f) {
-          atomicAdd(b.acc + ((int64_t)gidx * KG + k) * kAcc + slot, tot);
+          atomicAdd(b.acc + ((int64_t)gidx * KG + k) * kAcc + slot, (acc_t)tot);
         }
         if (EXT) {
 #pragma unroll
@@ -311,7 +316,7 @@ __global__ void __launch_bounds__(128, KG == 1 ? 5 : 4) k_composite_bwd_naive(Bw
             if (DET) {
               if (rec < b.rec_cap) b.rec_pay[(size_t)rec * (KG * 20) + k * 20 + 16 + lane] = x;
             } else if (x != 0.f) {
-              atomicAdd(b.acc_ext + ((int64_t)gidx * KG + k) * kAccExt + lane, x);
+              atomicAdd(b.acc_ext + ((int64_t)gidx * KG + k) * kAccExt + lane, (acc_t)x);
             }
           }
         } else if (DET && lane < 4 && rec < b.rec_cap) {
@@ -619,7 +624,7 @@ __global__ void __launch_bounds__(256 / QP, HGS_BWDC_MINB(KG, EXT, QP)) k_compos
         if (DET) {
           if (writer && rec < b.rec_cap) b.rec_pay[(size_t)rec * (KG * 20) + k * 20 + slot] = tot;
         } else if (writer && slot < nslots && tot != 0.f) {
-          atomicAdd(b.acc + ((int64_t)gidx * KG + k) * kAcc + slot, tot);
+          atomicAdd(b.acc + ((int64_t)gidx * KG + k) * kAcc + slot, (acc_t)tot);
         }
         if (EXT) {
 #pragma unroll
@@ -629,7 +634,7 @@ __global__ void __launch_bounds__(256 / QP, HGS_BWDC_MINB(KG, EXT, QP)) k_compos
             if (DET) {
               if (rec < b.rec_cap) b.rec_pay[(size_t)rec * (KG * 20) + k * 20 + 16 + lane] = x;
             } else if (x != 0.f) {
-              atomicAdd(b.acc_ext + ((int64_t)gidx * KG + k) * kAccExt + lane, x);
+              atomicAdd(b.acc_ext + ((int64_t)gidx * KG + k) * kAccExt + lane, (acc_t)x);
             }
           }
         } else if (DET && lane < 4 && rec < b.rec_cap) {
@@ -768,10 +773,10 @@ __global__ void __launch_bounds__(256, HGS_FIXUP_MINB) k_fixup_bwd(BwdArgs b) {
         } else {
           for (int k = 0; k < KG; ++k) {
             for (int s = 0; s < nslots; ++s)
-              if (v[k][s] != 0.f) atomicAdd(b.acc + ((int64_t)gidx * KG + k) * kAcc + s, v[k][s]);
+              if (v[k][s] != 0.f) atomicAdd(b.acc + ((int64_t)gidx * KG + k) * kAcc + s, (acc_t)v[k][s]);
             if (EXT)
               for (int s = 0; s < 4; ++s)
-                if (ve[k][s] != 0.f) atomicAdd(b.acc_ext + ((int64_t)gidx * KG + k) * kAccExt + s, ve[k][s]);
+                if (ve[k][s] != 0.f) atomicAdd(b.acc_ext + ((int64_t)gidx * KG + k) * kAccExt + s, (acc_t)ve[k][s]);
           }
         }
       }
@@ -794,19 +799,19 @@ __global__ void __launch_bounds__(256, HGS_FIXUP_MINB) k_fixup_bwd(BwdArgs b) {
 // Deterministic mode: records sorted by key (Gaussian, tile, sub) -> sum each
 // Gaussian's records in key order into its accumulator slots.
 __global__ void k_det_reduce(const unsigned long long *__restrict__ keys, const uint32_t *__restrict__ vals,
-                             const float *__restrict__ pay, int64_t nrec, int kg, float *__restrict__ acc,
-                             float *__restrict__ acc_ext) {
+                             const float *__restrict__ pay, int64_t nrec, int kg, acc_t *__restrict__ acc,
+                             acc_t *__restrict__ acc_ext) {
   for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < nrec; p += (int64_t)gridDim.x * blockDim.x) {
     const uint32_t g = (uint32_t)(keys[p] >> 32);
     if (p > 0 && (uint32_t)(keys[p - 1] >> 32) == g) continue;  // not the head of its segment
     for (int k = 0; k < kg; ++k) {
-      float sum[20];
+      acc_t sum[20];
 #pragma unroll
-      for (int s = 0; s < 20; ++s) sum[s] = 0.f;
+      for (int s = 0; s < 20; ++s) sum[s] = 0.0;
       for (int64_t q = p; q < nrec && (uint32_t)(keys[q] >> 32) == g; ++q) {
         const float *pp = pay + (size_t)vals[q] * (kg * 20) + k * 20;
 #pragma unroll
-        for (int s = 0; s < 20; ++s) sum[s] += pp[s];
+        for (int s = 0; s < 20; ++s) sum[s] += (acc_t)pp[s];
       }
 #pragma unroll
       for (int s = 0; s < 16; ++s) acc[((int64_t)g * kg + k) * kAcc + s] = sum[s];

@@ -33,7 +33,7 @@ constexpr int kDScan = 1024;
 
 enum : uint8_t { kKeep = 0, kPrune = 1, kClone = 2, kSplit = 3 };
 
-__global__ void k_densify_stats(SceneView sc, CamD cam, const float *acc, int kg, const uint8_t *touched,
+__global__ void k_densify_stats(SceneView sc, CamD cam, const acc_t *acc, int kg, const uint8_t *touched,
                                 float half_w, float half_h, float *grad_accum, int32_t *obs_count) {
   const int64_t n = sc.n;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
@@ -55,12 +55,12 @@ __global__ void k_densify_stats(SceneView sc, CamD cam, const float *acc, int kg
     }
     float gx = 0.f, gy = 0.f;
     for (int k = 0; k < kg; ++k) {
-      const float *A = acc + ((int64_t)i * kg + k) * kAccD;
-      gx += A[4];
-      gy += A[5];
+      const acc_t *A = acc + ((int64_t)i * kg + k) * kAccD;
+      gx += (float)A[4];
+      gy += (float)A[5];
       if (!is3d) {
-        gx += (A[6] * m2[0] + A[7] * m2[1]) + A[8] * m2[2];
-        gy += (A[9] * m2[0] + A[10] * m2[1]) + A[11] * m2[2];
+        gx += ((float)A[6] * m2[0] + (float)A[7] * m2[1]) + (float)A[8] * m2[2];
+        gy += ((float)A[9] * m2[0] + (float)A[10] * m2[1]) + (float)A[11] * m2[2];
       }
     }
     gx *= half_w;  // pixel -> NDC units (3DGS viewspace gradient convention)
@@ -300,7 +300,7 @@ int hgs_densify_stats(const hgs_scene *scene, const hgs_camera *camera, const vo
     cam.tv[r] = camera->world_to_camera[r * 4 + 3];
   }
   k_densify_stats<<<grid_of(scene->n), 256, 0, static_cast<cudaStream_t>(stream)>>>(
-      view_of(*scene), cam, static_cast<const float *>(bwd_scratch), kg, touched, 0.5f * (float)camera->width,
+      view_of(*scene), cam, static_cast<const acc_t *>(bwd_scratch), kg, touched, 0.5f * (float)camera->width,
       0.5f * (float)camera->height, grad_accum, obs_count);
   return cudaGetLastError() == cudaSuccess ? HGS_OK : HGS_ERR_CUDA;
 }

@@ -12,7 +12,8 @@
 
 namespace hgs {
 
-__device__ __forceinline__ bool erank_d(const float *ls, double &er) {
+template <typename T>
+__device__ __forceinline__ bool erank_d(const T *ls, double &er) {
   double q0 = exp(2.0 * (double)ls[0]), q1 = exp(2.0 * (double)ls[1]), q2 = exp(2.0 * (double)ls[2]);
   double tot = (q0 + q1) + q2;
   if (tot == 0.0 || !isfinite(q0) || !isfinite(q1) || !isfinite(q2)) return false;
@@ -35,9 +36,10 @@ __device__ __forceinline__ int hist_bin(double x) {
   return b;
 }
 
-__global__ void __launch_bounds__(256) k_exchange_scan(int64_t n, const float *__restrict__ log_scale,
+template <typename T>
+__global__ void __launch_bounds__(256) k_exchange_scan(int64_t n, const T *__restrict__ log_scale,
                                                        const uint8_t *__restrict__ type_spec, double theta_e,
-                                                       float *__restrict__ eranks, ExchangeState *__restrict__ st) {
+                                                       T *__restrict__ eranks, ExchangeState *__restrict__ st) {
   __shared__ unsigned int s_hist[20];
   __shared__ unsigned int s_cnt[4];
   if (threadIdx.x < 20) s_hist[threadIdx.x] = 0;
@@ -49,7 +51,7 @@ __global__ void __launch_bounds__(256) k_exchange_scan(int64_t n, const float *_
       atomicAdd(&s_cnt[3], 1u);
       continue;
     }
-    if (eranks) eranks[i] = (float)er;
+    if (eranks) eranks[i] = (T)er;
     const uint8_t t = type_spec[i];
     if (t == 1 && er < theta_e) atomicAdd(&s_cnt[0], 1u);
     if (t == 0 && er > theta_e) atomicAdd(&s_cnt[1], 1u);
@@ -88,8 +90,9 @@ __device__ __forceinline__ void matrix_to_quat_d(const double *m, double *q) {
   }
 }
 
-__global__ void __launch_bounds__(256) k_exchange_apply(int64_t n, float *__restrict__ log_scale,
-                                                        float *__restrict__ rotation, uint8_t *__restrict__ type_spec,
+template <typename T>
+__global__ void __launch_bounds__(256) k_exchange_apply(int64_t n, T *__restrict__ log_scale,
+                                                        T *__restrict__ rotation, uint8_t *__restrict__ type_spec,
                                                         double theta_e) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     double er;
@@ -101,7 +104,7 @@ __global__ void __launch_bounds__(256) k_exchange_apply(int64_t n, float *__rest
     }
     if (!(er < theta_e)) continue;
     // choose_permutation (exchange.py:76-88); ties prefer I, then P_x
-    const float *ls = log_scale + 3 * i;
+    const T *ls = log_scale + 3 * i;
     double s[3] = {exp((double)ls[0]), exp((double)ls[1]), exp((double)ls[2])};
     int perm = (s[2] <= s[0] && s[2] <= s[1]) ? 0 : (s[0] <= s[1] ? 1 : 2);
     // new scale diag(P S P^T): P_x -> (s1, s2, s0), P_y -> (s2, s0, s1)
@@ -110,7 +113,7 @@ __global__ void __launch_bounds__(256) k_exchange_apply(int64_t n, float *__rest
     else if (perm == 1) { src[0] = 1; src[1] = 2; src[2] = 0; }
     else { src[0] = 2; src[1] = 0; src[2] = 1; }
     double R[9];
-    float *q = rotation + 4 * i;
+    T *q = rotation + 4 * i;
     quat_to_matrix_d(q[0], q[1], q[2], q[3], R);
     // (R P^T)[r][c] = R[r][src[c]]  (P^T column c = e_{src[c]})
     double RP[9];
@@ -118,14 +121,34 @@ __global__ void __launch_bounds__(256) k_exchange_apply(int64_t n, float *__rest
       for (int cc = 0; cc < 3; ++cc) RP[r * 3 + cc] = R[r * 3 + src[cc]];
     double qn[4];
     matrix_to_quat_d(RP, qn);
-    const float l0 = ls[0], l1 = ls[1], l2 = ls[2];
-    const float lsv[3] = {l0, l1, l2};
-    // log(exp(ls)) in float64 (exchange.py:98), stored as float32
-    float *lw = log_scale + 3 * i;
-    for (int cc = 0; cc < 3; ++cc) lw[cc] = (float)log(exp((double)lsv[src[cc]]));
-    for (int cc = 0; cc < 4; ++cc) q[cc] = (float)qn[cc];
+    const T lsv[3] = {ls[0], ls[1], ls[2]};
+    // log(exp(ls)) in float64 (exchange.py:98), stored in T
+    T *lw = log_scale + 3 * i;
+    for (int cc = 0; cc < 3; ++cc) lw[cc] = (T)log(exp((double)lsv[src[cc]]));
+    for (int cc = 0; cc < 4; ++cc) q[cc] = (T)qn[cc];
     type_spec[i] = 0;
   }
 }
+
+// Host launchers (the template kernels are instantiated and launched in this
+// translation unit).
+template <typename T>
+cudaError_t launch_exchange_scan(int64_t n, const T *log_scale, const uint8_t *type_spec, double theta_e, T *eranks,
+                                 ExchangeState *st, int grid, cudaStream_t s) {
+  k_exchange_scan<T><<<grid, 256, 0, s>>>(n, log_scale, type_spec, theta_e, eranks, st);
+  return cudaGetLastError();
+}
+template <typename T>
+cudaError_t launch_exchange_apply(int64_t n, T *log_scale, T *rotation, uint8_t *type_spec, double theta_e, int grid,
+                                  cudaStream_t s) {
+  k_exchange_apply<T><<<grid, 256, 0, s>>>(n, log_scale, rotation, type_spec, theta_e);
+  return cudaGetLastError();
+}
+template cudaError_t launch_exchange_scan<float>(int64_t, const float *, const uint8_t *, double, float *,
+                                                 ExchangeState *, int, cudaStream_t);
+template cudaError_t launch_exchange_scan<double>(int64_t, const double *, const uint8_t *, double, double *,
+                                                  ExchangeState *, int, cudaStream_t);
+template cudaError_t launch_exchange_apply<float>(int64_t, float *, float *, uint8_t *, double, int, cudaStream_t);
+template cudaError_t launch_exchange_apply<double>(int64_t, double *, double *, uint8_t *, double, int, cudaStream_t);
 
 }  // namespace hgs

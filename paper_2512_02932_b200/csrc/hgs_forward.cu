@@ -52,9 +52,11 @@ __device__ __forceinline__ void write_rec64(const ProjD &o, Rec64 *q) {
 // singular-conic validity for 3D (project.py:225), |q| check (rotation.py:
 // 19-20).  key = bits(z) for kept splats, ~0 otherwise (they sort last and
 // are not counted in M).  Also accumulates the 8 digit histograms.
+template <bool G64>
 __global__ void __launch_bounds__(256) k_depth_keys(SceneView sc, CamD cam, unsigned long long *__restrict__ keys,
                                                     uint32_t *__restrict__ vals, uint32_t *__restrict__ hist,
                                                     FrameState *__restrict__ st) {
+  using G = SceneGeom<G64>;
   __shared__ uint32_t sh[8 * kRadix];
   __shared__ uint32_t s_m;
   for (int i = threadIdx.x; i < 8 * kRadix; i += blockDim.x) sh[i] = 0;
@@ -63,19 +65,18 @@ __global__ void __launch_bounds__(256) k_depth_keys(SceneView sc, CamD cam, unsi
   uint32_t bad = 0;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < sc.n; i += (int64_t)gridDim.x * blockDim.x) {
     double p[3], t[3];
-    load_center_d(sc, i, p);
+    load_center_d<G64>(sc, i, p);
     t_cam_d(cam, p, t);
     bool keep = t[2] > cam.near_plane;
     if (keep) {
       double R[9];
-      bool qok = quat_to_matrix_d(sc.rotation[4 * i], sc.rotation[4 * i + 1], sc.rotation[4 * i + 2],
-                                  sc.rotation[4 * i + 3], R);
+      bool qok = quat_to_matrix_d(G::rotation(sc, i, 0), G::rotation(sc, i, 1), G::rotation(sc, i, 2),
+                                  G::rotation(sc, i, 3), R);
       if (!qok) {
         bad = 1;
         keep = false;
       } else if (sc.type_spec[i] == 1) {
-        double s[3] = {exp((double)sc.log_scale[3 * i]), exp((double)sc.log_scale[3 * i + 1]),
-                       exp((double)sc.log_scale[3 * i + 2])};
+        double s[3] = {exp(G::log_scale(sc, i, 0)), exp(G::log_scale(sc, i, 1)), exp(G::log_scale(sc, i, 2))};
         double a, b, c;
         cov2d_3d(cam, t, R, s, a, b, c);
         keep = (a * c - b * b) > 1e-18;
@@ -94,6 +95,12 @@ __global__ void __launch_bounds__(256) k_depth_keys(SceneView sc, CamD cam, unsi
     if (sh[i]) atomicAdd(&hist[i], sh[i]);
   if (threadIdx.x == 0 && s_m) atomicAdd(&st->m_count, s_m);
 }
+cudaError_t launch_depth_keys(const SceneView &sc, const CamD &cam, unsigned long long *keys, uint32_t *vals,
+                              uint32_t *hist, FrameState *st, int grid, cudaStream_t s) {
+  if (sc.center64) k_depth_keys<true><<<grid, 256, 0, s>>>(sc, cam, keys, vals, hist, st);
+  else k_depth_keys<false><<<grid, 256, 0, s>>>(sc, cam, keys, vals, hist, st);
+  return cudaGetLastError();
+}
 
 // ---------------------------------------------------- preprocess + scan
 __device__ __forceinline__ uint32_t tile_count_of(const int *bb) {
@@ -103,14 +110,19 @@ __device__ __forceinline__ uint32_t tile_count_of(const int *bb) {
   return tx * ty;
 }
 
-__device__ __forceinline__ void write_record(const ProjD &o, uint32_t idx, SplatRec *__restrict__ rec,
+__device__ __forceinline__ void write_record(const ProjD &o, uint32_t idx, int W, int H, SplatRec *__restrict__ rec,
                                              float4 *__restrict__ cull) {
-  // anchor pixel = floor(centre), kept within +-2^30 so (ix - ax) stays exact
+  // anchor pixel = floor(centre), kept within +-2^30 so (ix - ax) stays exact;
+  // a 3D splat's anchor is also clamped to the image (see r2 below)
   double axd = floor(o.ctr[0]), ayd = floor(o.ctr[1]);
   axd = fmin(fmax(axd, -1073741824.0), 1073741824.0);
   ayd = fmin(fmax(ayd, -1073741824.0), 1073741824.0);
   if (isnan(axd)) axd = 0.0;
   if (isnan(ayd)) ayd = 0.0;
+  if (o.typ == 1) {
+    axd = fmin(fmax(axd, 0.0), (double)(W - 1));
+    ayd = fmin(fmax(ayd, 0.0), (double)(H - 1));
+  }
   SplatRec r;
   r.r0 = make_float4((float)(o.ctr[0] - axd), (float)(o.ctr[1] - ayd), (float)o.t[2], (float)log2(o.alpha_eff));
   if (o.typ == 1) {
@@ -135,7 +147,16 @@ __device__ __forceinline__ void write_record(const ProjD &o, uint32_t idx, Splat
       vy = 0.0;
     }
     r.r1 = make_float4((float)vx, (float)vy, (float)l1, (float)fmax(l2, 0.0));
-    r.r2 = make_float4(0.f, 0.f, 0.f, 0.f);
+    // (P0, Q0): the anchor pixel's offset from the centre in the eigenbasis,
+    // in float64, so a pixel's rotated offset is (P0, Q0) + R (pxl, pyl) with
+    // (pxl, pyl) small (the anchor is on the image).  Rotating the full offset
+    // in float32 instead costs eps |offset| -- 0.02 px for a near-camera splat
+    // whose centre is 3e5 px off-screen, a systematic gradient error that the
+    // 3D chain rule amplifies ~100x.
+    const double ox = axd - o.ctr[0], oy = ayd - o.ctr[1];
+    const double P0 = vx * ox + vy * oy, Q0 = vx * oy - vy * ox;
+    const float P0f = (float)P0, Q0f = (float)Q0;
+    r.r2 = make_float4(P0f, Q0f, fabsf(P0f) + fabsf(Q0f), 0.f);
     r.r3 = make_float4(0.f, (float)o.color[0], (float)o.color[1], (float)o.color[2]);
   } else {
     const double *m = o.mrow;  // rows x(0..3), y(4..7), w(8..11)
@@ -175,7 +196,7 @@ __global__ void k_rank_scatter(const uint32_t *__restrict__ sorted_idx, int64_t 
 // shared memory as one coalesced segment (per-thread strided rows were
 // LSU-throttled); float64 projection; record + tile count written at the
 // Gaussian's depth rank.
-template <int B>
+template <int B, bool G64>
 __global__ void __launch_bounds__(32, HGS_PRE_MINB) k_preprocess(SceneView sc, CamD cam, ModD mod,
                                                    const uint32_t *__restrict__ rank_of,
                                                    SplatRec *__restrict__ recs, Rec64 *__restrict__ recs64,
@@ -240,9 +261,9 @@ __global__ void __launch_bounds__(32, HGS_PRE_MINB) k_preprocess(SceneView sc, C
     const uint32_t r = rank_of[i];
     if (r == 0xffffffffu) continue;
     ProjD o;
-    project_d<false>(sc, i, cam, mod, o, s_sh + lane * SS);
+    project_d<false, false, G64>(sc, i, cam, mod, o, s_sh + lane * SS);
     bbox_d(o, cam.width, cam.height);
-    write_record(o, (uint32_t)i, recs + r, cull2d + 2 * (size_t)r);
+    write_record(o, (uint32_t)i, cam.width, cam.height, recs + r, cull2d + 2 * (size_t)r);
     write_rec64(o, recs64 + r);
     counts[r] = tile_count_of(o.bbox);
   }
@@ -252,12 +273,16 @@ cudaError_t launch_preprocess(const SceneView &sc, const CamD &cam, const ModD &
                               SplatRec *recs, Rec64 *recs64, float4 *cull2d, uint32_t *counts, cudaStream_t s) {
   const int64_t nb = (sc.n + 31) / 32;
   const int g = (int)(nb < 1 ? 1 : (nb > 148 * 48 ? 148 * 48 : nb));  // one warp per CTA
+#define HGS_PRE(B_)                                                                                \
+  (sc.center64 ? k_preprocess<B_, true><<<g, 32, 0, s>>>(sc, cam, mod, rank_of, recs, recs64, cull2d, counts) \
+               : k_preprocess<B_, false><<<g, 32, 0, s>>>(sc, cam, mod, rank_of, recs, recs64, cull2d, counts))
   switch (sc.sh_bases) {
-    case 1: k_preprocess<1><<<g, 32, 0, s>>>(sc, cam, mod, rank_of, recs, recs64, cull2d, counts); break;
-    case 4: k_preprocess<4><<<g, 32, 0, s>>>(sc, cam, mod, rank_of, recs, recs64, cull2d, counts); break;
-    case 9: k_preprocess<9><<<g, 32, 0, s>>>(sc, cam, mod, rank_of, recs, recs64, cull2d, counts); break;
-    default: k_preprocess<16><<<g, 32, 0, s>>>(sc, cam, mod, rank_of, recs, recs64, cull2d, counts); break;
+    case 1: HGS_PRE(1); break;
+    case 4: HGS_PRE(4); break;
+    case 9: HGS_PRE(9); break;
+    default: HGS_PRE(16); break;
   }
+#undef HGS_PRE
   return cudaGetLastError();
 }
 

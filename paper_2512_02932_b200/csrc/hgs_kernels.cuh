@@ -333,19 +333,21 @@ __device__ __forceinline__ void geom_common(const SplatRec &r, int ix, int iy, G
   g.dy = __fsub_rn(g.pyl, r.r0.y);
 }
 
-// 3D record: r1 = (c, s, lambda_p, lambda_q), the conic's eigenbasis
-// (write_record).  (p, q) = rotated offset, d = lambda_p p^2 + lambda_q q^2.
-// Float32 error: |p error| <= eps (2m + |p|) (m = |dx| + |dy|), so
-// |d error| <= eps (6 d + 4 m (lambda_p |p| + lambda_q |q|)).
+// 3D record: r1 = (c, s, lambda_p, lambda_q), the conic's eigenbasis, r2 =
+// (P0, Q0, |P0| + |Q0|, 0) the anchor's rotated offset from the centre
+// (write_record).  (p, q) = (P0 + c pxl + s pyl, Q0 + c pyl - s pxl), the
+// pixel's rotated offset; d = lambda_p p^2 + lambda_q q^2.
+// Float32 error: |p error|, |q error| <= eps (2m + |p|), m = |P0| + |Q0| +
+// |pxl| + |pyl|, so |d error| <= eps (6 d + 4 m (lambda_p |p| + lambda_q |q|)).
 __device__ __forceinline__ void geom_3d(const SplatRec &r, Geom &g) {
-  const float4 e = r.r1;
-  const float p = fmaf(e.x, g.dx, __fmul_rn(e.y, g.dy));
-  const float q = fmaf(e.x, g.dy, -__fmul_rn(e.y, g.dx));
+  const float4 e = r.r1, o = r.r2;
+  const float p = fmaf(e.x, g.pxl, fmaf(e.y, g.pyl, o.x));
+  const float q = fmaf(e.x, g.pyl, fmaf(-e.y, g.pxl, o.y));
   g.wp = __fmul_rn(e.z, p);
   g.wq = __fmul_rn(e.w, q);
   g.d = fmaf(g.wp, p, __fmul_rn(g.wq, q));
   g.arg = fmaf(g.d, -kHalfLog2e, r.r0.w);
-  g.m = __fadd_rn(fabsf(g.dx), fabsf(g.dy));
+  g.m = __fadd_rn(o.z, __fadd_rn(fabsf(g.pxl), fabsf(g.pyl)));
 }
 
 // Coarse 3D band (log2 units): inside it the precise bound is formed.  Valid
@@ -588,14 +590,23 @@ static __device__ __noinline__ bool replay_T_below(const SplatRec *recs, const u
   return T < kEarlyStopT;
 }
 
+// Global per-Gaussian gradient accumulators are float64: a warp's partial
+// sums (<= 128 pixels) are float32, but a splat covering the whole image sums
+// ~2M contributions of random sign (the upstream pixel gradients) that cancel
+// to ~1/sqrt(N) of their absolute sum; float32 atomics then carry errors of
+// 1e-3 relative, and the 3D chain rule of a near-camera, far-off-axis Gaussian
+// amplifies dL/dcov2d errors ~100x through the cancelling Jacobian terms
+// (config-5 orbit view 16: 9% centre-gradient error on two such Gaussians).
+using acc_t = double;
+
 struct BwdArgs {
   CompositeArgs c;          // recs, tile lists, flags, bg, state
   const float *pix_grad;    // (KG, H, W, 3)
   const float *depth_grad;  // (KG, H, W) or null
   const float *normal_grad; // (KG, H, W, 3) or null
   const float *alpha_grad;  // (KG, H, W) or null
-  float *acc;               // (n, KG, 16)
-  float *acc_ext;           // (n, KG, 4) or null
+  acc_t *acc;               // (n, KG, 16)
+  acc_t *acc_ext;           // (n, KG, 4) or null
   uint8_t *touched;         // (n) by Gaussian index, zeroed by the caller
   // HGS_FLAG_DETERMINISTIC: per-(splat, warp) / per-(splat, pixel) records
   // instead of atomics; sorted by key and reduced in key order afterwards
@@ -616,10 +627,12 @@ struct ChainArgs {
   SceneView sc;
   CamD cam;
   ModD mod;
-  const float *acc;      // (n, KG, 16)
-  const float *acc_ext;  // (n, KG, 4) or null
+  acc_t *acc;            // (n, KG, 16); 3D slots 4-8 rotated to pixel axes in place
+  const acc_t *acc_ext;  // (n, KG, 4) or null
   int kg;
   float *grads;          // (KG, n*P) field-major blocks
+  const uint32_t *rank_of;  // (n) depth rank of each Gaussian (the forward's), or null
+  const SplatRec *recs;     // rank-ordered records (a 3D splat's eigenbasis)
 };
 
 struct ExchangeState {
@@ -630,8 +643,8 @@ struct ExchangeState {
 // kernels (defined in hgs_forward.cu / hgs_backward.cu / hgs_exchange.cu)
 __global__ void k_init_state(SceneView sc, CamD cam, ModD mod, const SplatRec *recs, const Rec64 *recs64,
                              FrameState *st);
-__global__ void k_depth_keys(SceneView sc, CamD cam, unsigned long long *keys, uint32_t *vals, uint32_t *hist,
-                             FrameState *st);
+cudaError_t launch_depth_keys(const SceneView &sc, const CamD &cam, unsigned long long *keys, uint32_t *vals,
+                              uint32_t *hist, FrameState *st, int grid, cudaStream_t s);
 __global__ void k_rank_scatter(const uint32_t *sorted_idx, int64_t m, int64_t n, uint32_t *rank_of);
 cudaError_t launch_preprocess(const SceneView &sc, const CamD &cam, const ModD &mod, const uint32_t *rank_of,
                               SplatRec *recs, Rec64 *recs64, float4 *cull2d, uint32_t *counts, cudaStream_t s);
@@ -648,10 +661,13 @@ __global__ void k_pixel_counts(CompositeArgs a, uint32_t *counts);
 // backward compositor (compacted, or naive) + the float64 fixup of deferred pixels
 cudaError_t launch_composite_bwd(const BwdArgs &b, int kg, int64_t n_tiles, bool ext, bool det, cudaStream_t s);
 __global__ void k_det_reduce(const unsigned long long *keys, const uint32_t *vals, const float *pay, int64_t nrec,
-                             int kg, float *acc, float *acc_ext);
+                             int kg, acc_t *acc, acc_t *acc_ext);
 cudaError_t launch_chain_rule(const ChainArgs &c, int sh_bases, int grid, size_t smem, cudaStream_t s);
-__global__ void k_exchange_scan(int64_t n, const float *log_scale, const uint8_t *type_spec, double theta_e,
-                                float *eranks, ExchangeState *st);
-__global__ void k_exchange_apply(int64_t n, float *log_scale, float *rotation, uint8_t *type_spec, double theta_e);
+template <typename T>
+cudaError_t launch_exchange_scan(int64_t n, const T *log_scale, const uint8_t *type_spec, double theta_e, T *eranks,
+                                 ExchangeState *st, int grid, cudaStream_t s);
+template <typename T>
+cudaError_t launch_exchange_apply(int64_t n, T *log_scale, T *rotation, uint8_t *type_spec, double theta_e, int grid,
+                                  cudaStream_t s);
 
 }  // namespace hgs

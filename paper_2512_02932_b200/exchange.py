@@ -52,11 +52,37 @@ def exchange_pass(scene, config: ExchangeConfig = None) -> ExchangeReport:
         config = ExchangeConfig()
     if isinstance(scene, DeviceGaussians):
         return exchange_pass_device(scene, config)
-    ds = DeviceGaussians.from_host(scene)
-    rep = exchange_pass_device(ds, config)
-    # write back in place like the reference (float64 arrays)
-    scene.log_scale[:] = ds.log_scale.double().cpu().numpy()
-    scene.rotation[:] = ds.rotation.double().cpu().numpy()
-    scene.type_spec[:] = ds.type_spec.cpu().numpy()
-    rep.eranks = rep.eranks.double().cpu().numpy()
-    return rep
+    return _exchange_pass_host(scene, config)
+
+
+def _exchange_pass_host(scene, config):
+    """Host GaussianSet: the float64 kernels (hgs_exchange_f64) on a float64
+    copy of log_scale / rotation / type_spec, then only the flipped rows are
+    written back in place -- demoted rows get their float64
+    reparameterisation, promoted rows only the type flip -- exactly the rows
+    the reference touches (exchange.py:137-149).  A DegenerateScaleError
+    leaves the scene untouched."""
+    import torch
+
+    from ._hostio import upload
+    n = scene.count
+    dev = torch.device("cuda", torch.cuda.current_device())
+    ls, rot, ty = upload([(scene.log_scale, torch.float64), (scene.rotation, torch.float64),
+                          (scene.type_spec, torch.uint8)], dev, tag="exchange")
+    eranks = torch.empty(max(n, 1), dtype=torch.float64, device=dev)
+    scratch = torch.empty(256, dtype=torch.uint8, device=dev)
+    rep = _lib.ExchangeReport()
+    _lib.check(_lib.lib().hgs_exchange_f64(n, _lib.ptr(ls), _lib.ptr(rot), _lib.ptr(ty),
+                                           float(config.theta_e), _lib.ptr(eranks),
+                                           _lib.ptr(scratch), rep, _lib.current_stream_handle(dev)),
+               "hgs_exchange_f64")
+    new_ty = ty.cpu().numpy()
+    demoted = np.flatnonzero((scene.type_spec == 1) & (new_ty == 0))
+    if demoted.size:
+        idx = torch.from_numpy(demoted).to(dev)
+        scene.log_scale[demoted] = ls[idx].cpu().numpy()
+        scene.rotation[demoted] = rot[idx].cpu().numpy()
+    scene.type_spec[:] = new_ty
+    return ExchangeReport(int(rep.n_3d_to_2d), int(rep.n_2d_to_3d), int(rep.n_2d), int(rep.n_3d),
+                          np.array(rep.erank_hist[:], np.int64), np.linspace(1.0, 3.0, 21),
+                          eranks[:n].cpu().numpy())

@@ -29,8 +29,9 @@ def synthetic_camera(width, height, world_to_camera=None):
 
 
 def synthetic_scene(n, width, height, sh_degree, seed=0, frac_3d=0.5, sigma_px=(0.5, 6.0),
-                    z_range=(2.0, 8.0)):
-    """(GaussianSet, CameraView) for an n-Gaussian mixed scene at W x H."""
+                    z_range=(2.0, 8.0), f32=True):
+    """(GaussianSet, CameraView) for an n-Gaussian mixed scene at W x H.
+    ``f32=False`` keeps the raw float64 draws (not float32-representable)."""
     rng = np.random.default_rng(seed)
     fx = 0.8 * width
     cx, cy = width / 2.0, height / 2.0
@@ -46,8 +47,8 @@ def synthetic_scene(n, width, height, sh_degree, seed=0, frac_3d=0.5, sigma_px=(
     b = (sh_degree + 1) ** 2
     sh = rng.normal(0.0, 0.3, size=(n, 3, b))
     type_spec = (rng.random(n) < frac_3d).astype(np.uint8)
-    scene = GaussianSet(f32_exact(center), f32_exact(log_scale), f32_exact(rot),
-                        f32_exact(opacity_logit), f32_exact(sh), type_spec)
+    r = f32_exact if f32 else (lambda a: a)
+    scene = GaussianSet(r(center), r(log_scale), r(rot), r(opacity_logit), r(sh), type_spec)
     return scene, synthetic_camera(width, height)
 
 

@@ -41,25 +41,28 @@ def to_ref(scene, cam):
     return rs, rc
 
 
-def scene_arrays(scene, cam, st):
+def scene_arrays(scene, cam, st, dt=np.float32):
+    """dt = float32 for float32-representable scenes (lossless), float64 for
+    the raw-float64 fixtures."""
     return dict(
-        in_center=scene.center.astype(np.float32), in_log_scale=scene.log_scale.astype(np.float32),
-        in_rotation=scene.rotation.astype(np.float32),
-        in_opacity_logit=scene.opacity_logit.astype(np.float32),
-        in_sh=scene.sh_coeffs.astype(np.float32), in_type=scene.type_spec,
+        in_center=scene.center.astype(dt), in_log_scale=scene.log_scale.astype(dt),
+        in_rotation=scene.rotation.astype(dt),
+        in_opacity_logit=scene.opacity_logit.astype(dt),
+        in_sh=scene.sh_coeffs.astype(dt), in_type=scene.type_spec,
         cam_intr=np.array([cam.fx, cam.fy, cam.cx, cam.cy, cam.near, cam.far]),
         cam_size=np.array([cam.width, cam.height]), cam_w2c=cam.world_to_camera,
         background=np.array(st.background, np.float64),
         modulation=np.array([st.theta_z, st.t_z, st.lambda_z]))
 
 
-def render_fixture(name, scene, cam, st, kg=1, with_log=True, naive=False, seed=11):
+def render_fixture(name, scene, cam, st, kg=1, with_log=True, naive=False, seed=11,
+                   in_dtype=np.float32):
     rs, rc = to_ref(scene, cam)
     t0 = time.time()
     out = ref_render(rs, rc, st)
     t_fwd = time.time() - t0
     f = out.frame
-    data = scene_arrays(scene, cam, st)
+    data = scene_arrays(scene, cam, st, in_dtype)
     data.update(
         f_idx=f.idx, f_typ=f.typ, f_depth=f.depth, f_center2d=f.center2d, f_cov2d=f.cov2d,
         f_conic=f.conic, f_mrow=f.mrow, f_alpha=f.alpha, f_alpha_eff=f.alpha_eff,
@@ -127,6 +130,49 @@ def rotated_camera_scene(seed=7):
     return sc, synthetic_camera(64, 48, w2c)
 
 
+def raw_f64_scene(seed=17):
+    """A scene whose float64 inputs are NOT float32-representable, with a
+    rotated, translated camera (so view depths are not exact either): the
+    float32 rounding of these inputs gives a different depth order and
+    different tile lists, so only a float64-faithful path matches the
+    reference's frame arrays bit for bit."""
+    sc, _ = synthetic_scene(3000, 128, 96, 1, seed=seed, f32=False)
+    ang = 0.2
+    R = np.array([[np.cos(ang), -np.sin(ang), 0], [np.sin(ang), np.cos(ang), 0], [0, 0, 1]])
+    w2c = np.eye(4)
+    w2c[:3, :3] = R
+    w2c[:3, 3] = [0.013, -0.027, 0.11]
+    sc.center[:] = (sc.center - w2c[:3, 3]) @ R
+    # near-ties in depth below float32 resolution: pairs of Gaussians whose
+    # view depths differ by ~1e-9 (float32 rounding merges or swaps them)
+    k = 200
+    sc.center[1:2 * k:2] = sc.center[0:2 * k:2] + 1e-9 * np.random.default_rng(seed).normal(size=(k, 3))
+    from paper_2512_02932_b200.synthetic import synthetic_camera
+    return sc, synthetic_camera(128, 96, w2c)
+
+
+def exchange_f64_fixture():
+    """exchange_pass on raw float64 scales (not float32-representable), with
+    rows placed within 1e-12 of the erank threshold."""
+    rng = np.random.default_rng(19)
+    n = 3000
+    ls = rng.normal(0.0, 1.0, (n, 3)) * rng.uniform(0.05, 1.5, (n, 1)) - 2.0
+    ls[:40] = np.log([[1.0, 1.0, 2.6]] * 40) + rng.normal(0, 0.003, (40, 3))
+    rot = rng.normal(size=(n, 4))
+    rot = rot / np.linalg.norm(rot, axis=1, keepdims=True)
+    ty = (rng.random(n) < 0.5).astype(np.uint8)
+    sc = hs.core.GaussianSet(np.zeros((n, 3)), ls.copy(), rot.copy(), np.zeros(n),
+                             np.zeros((n, 3, 1)), ty.copy())
+    rep = hs.exchange.exchange_pass(sc, hs.exchange.ExchangeConfig())
+    np.savez_compressed(os.path.join(HERE, "exchange_f64.npz"),
+                        in_log_scale=ls, in_rotation=rot, in_type=ty, out_log_scale=sc.log_scale,
+                        out_rotation=sc.rotation, out_type=sc.type_spec,
+                        eranks=hs.exchange.effective_rank(ls),
+                        counts=np.array([rep.n_3d_to_2d, rep.n_2d_to_3d, rep.n_2d, rep.n_3d]),
+                        hist=rep.erank_hist, edges=rep.erank_edges)
+    print("exchange_f64: demoted %d promoted %d" % (rep.n_3d_to_2d, rep.n_2d_to_3d))
+
+
 def exchange_fixture():
     rng = np.random.default_rng(13)
     n = 4000
@@ -164,6 +210,10 @@ def main(which=None):
             "c1", *synthetic_scene(10_000, 256, 256, 0, seed=0), RenderSettings(), kg=1,
             with_log=False),
         "exchange": exchange_fixture,
+        "raw_f64": lambda: render_fixture(
+            "raw_f64", *raw_f64_scene(), RenderSettings(background=(0.3, 0.1, 0.2)), kg=1, with_log=False,
+            in_dtype=np.float64),
+        "exchange_f64": exchange_f64_fixture,
     }
     for name, fn in jobs.items():
         if which and name not in which:

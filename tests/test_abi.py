@@ -38,7 +38,8 @@ def test_exports_every_declared_symbol(L):
 
 
 def test_abi_version_and_status_strings(L):
-    assert L.hgs_abi_version() == 1
+    from paper_2512_02932_b200 import _lib
+    assert L.hgs_abi_version() == _lib.ABI_VERSION
     for code in range(0, 7):
         assert L.hgs_status_string(code)
     assert b"pairs" in L.hgs_status_string(5)
@@ -55,12 +56,44 @@ def test_frame_bytes_monotone(L):
 
 def test_struct_sizes_match_header():
     from paper_2512_02932_b200 import _lib
-    assert ctypes.sizeof(_lib.Scene) == 8 + 4 + 4 + 6 * 8
+    assert ctypes.sizeof(_lib.Scene) == 8 + 4 + 4 + 10 * 8
     assert ctypes.sizeof(_lib.Camera) == 4 * 8 + 8 + 16 * 8 + 2 * 8
     assert ctypes.sizeof(_lib.FrameInfo) == 4 * 8 + 4 * 4 + 8 + 4 + 4 + 16
     assert ctypes.sizeof(_lib.LossWeights) == 3 * 8
     assert ctypes.sizeof(_lib.Params) == 8 + 4 + 4 + 5 * 8
     assert ctypes.sizeof(_lib.AdamCfg) == 5 * 4 + 3 * 4 + 8
+
+
+def test_struct_layouts_match_the_c_compiler(tmp_path):
+    """sizeof / offsetof of every ABI struct as gcc sees include/*.h equals
+    the ctypes mirror in _lib.py."""
+    import shutil
+    import subprocess
+    from paper_2512_02932_b200 import _lib
+    cc = shutil.which("gcc")
+    if cc is None:
+        pytest.skip("gcc not available")
+    pairs = [("hgs_scene", _lib.Scene), ("hgs_camera", _lib.Camera), ("hgs_settings", _lib.Settings),
+             ("hgs_images", _lib.Images), ("hgs_frame_info", _lib.FrameInfo),
+             ("hgs_exchange_report", _lib.ExchangeReport), ("hgs_frame_export", _lib.FrameExport),
+             ("hgs_loss_weights", _lib.LossWeights), ("hgs_params", _lib.Params),
+             ("hgs_adam", _lib.AdamCfg), ("hgs_densify_config", _lib.DensifyCfg)]
+    lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "hgs.h"', '#include "hgs_train.h"',
+             'int main(void) {']
+    want = []
+    for cname, ct in pairs:
+        lines.append('printf("%%zu\\n", sizeof(%s));' % cname)
+        want.append(ctypes.sizeof(ct))
+        for f in ct._fields_:
+            lines.append('printf("%%zu\\n", offsetof(%s, %s));' % (cname, f[0]))
+            want.append(getattr(ct, f[0]).offset)
+    lines.append("return 0; }")
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines))
+    exe = str(tmp_path / "layout")
+    subprocess.run([cc, "-I", os.path.join(REPO, "include"), str(src), "-o", exe], check=True)
+    got = [int(v) for v in subprocess.run([exe], capture_output=True, text=True).stdout.split()]
+    assert got == want
 
 
 def test_train_host_entry_points(L):

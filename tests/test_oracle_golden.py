@@ -47,6 +47,19 @@ def test_render_matches_reference(name):
         np.testing.assert_allclose(nv["transmittance"], d["naive_transmittance"], atol=1e-12)
 
 
+def test_raw_f64_fixture_discriminates_float32_rounding():
+    """The raw_f64 fixture is only passed by a float64-faithful path: the
+    float32 rounding of its inputs changes the depth order and tile lists."""
+    from paper_2512_02932_b200.synthetic import f32_exact
+    scene, cam, st, d = load("raw_f64")
+    s2 = scene.copy()
+    for a in (s2.center, s2.log_scale, s2.rotation, s2.opacity_logit):
+        a[:] = f32_exact(a)
+    f = oracle.build_frame(s2, cam, st)
+    assert not np.array_equal(f.idx, d["f_idx"])
+    assert not np.array_equal(f.tile_ids, d["f_tile_ids"])
+
+
 @pytest.mark.parametrize("name", SCENES)
 def test_backward_matches_reference(name):
     scene, cam, st, d = load(name)
@@ -59,11 +72,10 @@ def test_backward_matches_reference(name):
         assert max(err.values()) < 1e-10, err
 
 
-def test_exchange_matches_reference():
-    z = np.load(oracle.os.path.join(oracle.os.path.dirname(__file__), "..", "tests", "golden",
-                                    "exchange.npz")) if False else None
+@pytest.mark.parametrize("name", ["exchange", "exchange_f64"])
+def test_exchange_matches_reference(name):
     import os
-    z = np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "exchange.npz"))
+    z = np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", name + ".npz"))
     ls, rot, ty, rep = oracle.exchange_pass(z["in_log_scale"], z["in_rotation"], z["in_type"])
     assert np.array_equal(ty, z["out_type"])
     np.testing.assert_allclose(ls, z["out_log_scale"], atol=1e-14)
