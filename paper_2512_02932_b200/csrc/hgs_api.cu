@@ -14,7 +14,7 @@ namespace {
 constexpr int kMaxGrid = 148 * 8;
 
 struct Layout {
-  size_t state, hist_d, off_d, hist_p, off_p, keys_a, keys_b, vals_a, vals_b, lb_sort, lb_scan, recs, recs64, cull2d, pair_off,
+  size_t state, hist_d, off_d, hist_p, off_p, keys_a, keys_b, vals_a, vals_b, lb_sort, lb_scan, recs, recs64, cull2d, eig, pair_off,
       pk_a, pk_b, pv_a, pv_b, tile_off, pix_T, pix_last, pix_count, fwd_fix, bwd_fix, pix_mask, total;
   size_t small_end;  // [state, small_end) is zeroed at the start of a forward
   size_t lb_sort_bytes, lb_scan_bytes;
@@ -49,6 +49,7 @@ Layout make_layout(int64_t n, int W, int H, int64_t cap) {
   L.recs = take(nn * sizeof(SplatRec));
   L.recs64 = take(nn * sizeof(Rec64));
   L.cull2d = take(nn * 2 * sizeof(float4));
+  L.eig = take(nn * sizeof(float2));  // by Gaussian index: a 3D splat's eigenbasis (c, s)
   L.pair_off = take(nn * 8);
   L.tile_off = take((n_tiles + 1) * 4);
   L.pix_T = take((size_t)W * H * 4);
@@ -265,7 +266,6 @@ int hgs_forward(const hgs_scene *scene, const hgs_camera *camera, const hgs_sett
     if (rc) return rc;
     vals_sorted = at<uint32_t>(frame, in_b ? L.vals_b : L.vals_a);
     rank_of = at<uint32_t>(frame, in_b ? L.vals_a : L.vals_b);  // the free ping-pong buffer
-    info->internal[1] = in_b ? 1u : 2u;  // where rank_of lives (the backward's chain rule reads it)
     info->internal[2] = (uint32_t)np;  // depth-sort passes (diagnostics / launch count)
   }
   info->m = m;
@@ -279,8 +279,7 @@ int hgs_forward(const hgs_scene *scene, const hgs_camera *camera, const hgs_sett
     k_rank_scatter<<<grid_for(n, 256), 256, 0, s>>>(vals_sorted, m, n, rank_of);
     HGS_LAUNCHED();
     HGS_CUDA(launch_preprocess(sc, cam, mod, rank_of, at<SplatRec>(frame, L.recs), at<Rec64>(frame, L.recs64),
-                               at<float4>(frame, L.cull2d),
-                               counts, s));
+                               at<float4>(frame, L.cull2d), at<float2>(frame, L.eig), counts, s));
     HGS_LAUNCHED();
     k_scan_counts<<<(unsigned)ceil_div(m, kScanTile), kScanThreads, 0, s>>>(
         counts, m, at<unsigned long long>(frame, L.pair_off), at<unsigned long long>(frame, L.lb_scan), st);
@@ -489,9 +488,7 @@ int hgs_backward(const hgs_scene *scene, const hgs_camera *camera, const hgs_set
   }
   HGS_LAUNCHED();
   const Layout FLc = make_layout(info->n, info->width, info->height, info->pair_capacity);
-  const uint32_t *rank_of =
-      info->internal[1] ? at<uint32_t>(frame, info->internal[1] == 1 ? FLc.vals_a : FLc.vals_b) : nullptr;
-  const ChainArgs c0{sc, cam, mod, acc, ext ? acc_ext : nullptr, 0, nullptr, rank_of, at<SplatRec>(frame, FLc.recs)};
+  const ChainArgs c0{sc, cam, mod, acc, ext ? acc_ext : nullptr, 0, nullptr, at<float2>(frame, FLc.eig)};
   for (int k0 = 0; k0 < kg; k0 += 4) {
     const int kc = std::min(4, kg - k0);
     HGS_CUDA(cudaMemsetAsync(acc, 0, (size_t)nn * kc * 16 * sizeof(acc_t), s));

@@ -101,6 +101,9 @@ constexpr int kChainThreads = 32;
 #ifndef HGS_CHAIN_PREFETCH
 #define HGS_CHAIN_PREFETCH 1
 #endif
+#ifndef HGS_CHAIN_WB
+#define HGS_CHAIN_WB 1  // store the pixel-axis 3D sums back (hgs_densify_stats reads them)
+#endif
 #ifndef HGS_CHAIN_MINB
 #define HGS_CHAIN_MINB 16  // 16 warps per SM: 128 registers
 #endif
@@ -267,7 +270,7 @@ __global__ void __launch_bounds__(kChainThreads, HGS_CHAIN_MINB) k_chain_rule_t(
         // the record's own float32 (c, s) -- the basis the pairs used -- to
         // pixel axes, v = M w with M = [[c, -s], [s, c]], in float64, and
         // store the pixel-axis values back for the densification statistics
-        const float4 e = __ldg(&c.recs[c.rank_of[i]].r1);
+        const float2 e = __ldg(&c.eig[i]);
         const double cs = e.x, sn = e.y;
         const double Sp = A[4], Sq = A[5], Gpp = A[6], Gpq = A[7], Gqq = A[8];
         gx = cs * Sp - sn * Sq;
@@ -275,8 +278,10 @@ __global__ void __launch_bounds__(kChainThreads, HGS_CHAIN_MINB) k_chain_rule_t(
         G00 = (cs * cs * Gpp - 2.0 * cs * sn * Gpq) + sn * sn * Gqq;
         G01 = (cs * sn * Gpp + (cs * cs - sn * sn) * Gpq) - cs * sn * Gqq;
         G11 = (sn * sn * Gpp + 2.0 * cs * sn * Gpq) + cs * cs * Gqq;
+#if HGS_CHAIN_WB
         acc_t *Aw = c.acc + ((int64_t)i * c.kg + k) * kAcc;
         Aw[4] = gx; Aw[5] = gy; Aw[6] = G00; Aw[7] = G01; Aw[8] = G11;
+#endif
       }
       const double Xd = td[0], Yd = td[1], Zd = td[2];
       const double fxd = cam.fx, fyd = cam.fy;

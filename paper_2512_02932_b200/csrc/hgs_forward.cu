@@ -111,7 +111,7 @@ __device__ __forceinline__ uint32_t tile_count_of(const int *bb) {
 }
 
 __device__ __forceinline__ void write_record(const ProjD &o, uint32_t idx, int W, int H, SplatRec *__restrict__ rec,
-                                             float4 *__restrict__ cull) {
+                                             float4 *__restrict__ cull, float2 *__restrict__ eig) {
   // anchor pixel = floor(centre), kept within +-2^30 so (ix - ax) stays exact;
   // a 3D splat's anchor is also clamped to the image (see r2 below)
   double axd = floor(o.ctr[0]), ayd = floor(o.ctr[1]);
@@ -157,6 +157,7 @@ __device__ __forceinline__ void write_record(const ProjD &o, uint32_t idx, int W
     const double P0 = vx * ox + vy * oy, Q0 = vx * oy - vy * ox;
     const float P0f = (float)P0, Q0f = (float)Q0;
     r.r2 = make_float4(P0f, Q0f, fabsf(P0f) + fabsf(Q0f), 0.f);
+    *eig = make_float2(r.r1.x, r.r1.y);  // the chain rule rotates the eigenbasis sums back with these
     r.r3 = make_float4(0.f, (float)o.color[0], (float)o.color[1], (float)o.color[2]);
   } else {
     const double *m = o.mrow;  // rows x(0..3), y(4..7), w(8..11)
@@ -200,7 +201,8 @@ template <int B, bool G64>
 __global__ void __launch_bounds__(32, HGS_PRE_MINB) k_preprocess(SceneView sc, CamD cam, ModD mod,
                                                    const uint32_t *__restrict__ rank_of,
                                                    SplatRec *__restrict__ recs, Rec64 *__restrict__ recs64,
-                                                   float4 *__restrict__ cull2d, uint32_t *__restrict__ counts) {
+                                                   float4 *__restrict__ cull2d, float2 *__restrict__ eig,
+                                                   uint32_t *__restrict__ counts) {
   constexpr int SB = 3 * B, SS = 3 * B + 1;
   const int lane = threadIdx.x;
 #if HGS_PRE_ASYNC
@@ -263,19 +265,20 @@ __global__ void __launch_bounds__(32, HGS_PRE_MINB) k_preprocess(SceneView sc, C
     ProjD o;
     project_d<false, false, G64>(sc, i, cam, mod, o, s_sh + lane * SS);
     bbox_d(o, cam.width, cam.height);
-    write_record(o, (uint32_t)i, cam.width, cam.height, recs + r, cull2d + 2 * (size_t)r);
+    write_record(o, (uint32_t)i, cam.width, cam.height, recs + r, cull2d + 2 * (size_t)r, eig + i);
     write_rec64(o, recs64 + r);
     counts[r] = tile_count_of(o.bbox);
   }
 }
 // Host launcher (the template is launched from this translation unit).
 cudaError_t launch_preprocess(const SceneView &sc, const CamD &cam, const ModD &mod, const uint32_t *rank_of,
-                              SplatRec *recs, Rec64 *recs64, float4 *cull2d, uint32_t *counts, cudaStream_t s) {
+                              SplatRec *recs, Rec64 *recs64, float4 *cull2d, float2 *eig, uint32_t *counts,
+                              cudaStream_t s) {
   const int64_t nb = (sc.n + 31) / 32;
   const int g = (int)(nb < 1 ? 1 : (nb > 148 * 48 ? 148 * 48 : nb));  // one warp per CTA
 #define HGS_PRE(B_)                                                                                \
-  (sc.center64 ? k_preprocess<B_, true><<<g, 32, 0, s>>>(sc, cam, mod, rank_of, recs, recs64, cull2d, counts) \
-               : k_preprocess<B_, false><<<g, 32, 0, s>>>(sc, cam, mod, rank_of, recs, recs64, cull2d, counts))
+  (sc.center64 ? k_preprocess<B_, true><<<g, 32, 0, s>>>(sc, cam, mod, rank_of, recs, recs64, cull2d, eig, counts) \
+               : k_preprocess<B_, false><<<g, 32, 0, s>>>(sc, cam, mod, rank_of, recs, recs64, cull2d, eig, counts))
   switch (sc.sh_bases) {
     case 1: HGS_PRE(1); break;
     case 4: HGS_PRE(4); break;

@@ -631,8 +631,7 @@ struct ChainArgs {
   const acc_t *acc_ext;  // (n, KG, 4) or null
   int kg;
   float *grads;          // (KG, n*P) field-major blocks
-  const uint32_t *rank_of;  // (n) depth rank of each Gaussian (the forward's), or null
-  const SplatRec *recs;     // rank-ordered records (a 3D splat's eigenbasis)
+  const float2 *eig;     // (n) a 3D splat's float32 eigenbasis (c, s), by Gaussian index
 };
 
 struct ExchangeState {
@@ -647,7 +646,8 @@ cudaError_t launch_depth_keys(const SceneView &sc, const CamD &cam, unsigned lon
                               uint32_t *hist, FrameState *st, int grid, cudaStream_t s);
 __global__ void k_rank_scatter(const uint32_t *sorted_idx, int64_t m, int64_t n, uint32_t *rank_of);
 cudaError_t launch_preprocess(const SceneView &sc, const CamD &cam, const ModD &mod, const uint32_t *rank_of,
-                              SplatRec *recs, Rec64 *recs64, float4 *cull2d, uint32_t *counts, cudaStream_t s);
+                              SplatRec *recs, Rec64 *recs64, float4 *cull2d, float2 *eig, uint32_t *counts,
+                              cudaStream_t s);
 __global__ void k_scan_counts(const uint32_t *counts, int64_t m, unsigned long long *pair_off,
                               unsigned long long *scan_lb, FrameState *st);
 __global__ void k_duplicate(const SplatRec *recs, const unsigned long long *pair_off, int64_t m, int tiles_x,
