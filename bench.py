@@ -34,6 +34,7 @@ METRIC = "hybrid-GS frames/s fwd & iters/s fwd+bwd at 1M Gaussians 1080p; 1/2/4/
 N_SM = 148
 FMA_PER_SM_CLK = 128
 MUFU_PER_SM_CLK = 16
+N_BUCKETS = 4  # gradient all-reduce buckets (parallel.view_batch_grads)
 
 # Algorithmic work per pair (_blend_py.py:17-44, 96-113, 149-240)
 FLOP_EVAL_3D = 13       # distance + alpha of a bbox-passing 3D pair
@@ -48,12 +49,46 @@ def init_dist(dev):
     """NCCL process group (one process per GPU).  HGS_DIST_BACKEND=gloo runs
     the same multi-rank code path with several ranks on one GPU (a logic
     check on single-GPU boxes; NCCL refuses duplicate devices)."""
+    import torch
     import torch.distributed as dist
     backend = os.environ.get("HGS_DIST_BACKEND", "nccl")
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     if backend == "nccl":
+        if torch.cuda.device_count() < world:
+            raise SystemExit("bench.py: %d ranks need %d GPUs for NCCL (this box has %d); set "
+                             "HGS_DIST_BACKEND=gloo to run the ranks on shared GPUs"
+                             % (world, world, torch.cuda.device_count()))
         dist.init_process_group("nccl", device_id=dev)
     else:
         dist.init_process_group(backend)
+
+
+def self_launch(a):
+    """``bench.py --gpus N`` without a launcher: re-exec under
+    torch.distributed.run with N ranks on this node (127.0.0.1).  Returns the
+    launcher's exit code, or None when already inside a launched rank."""
+    if a.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return None
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node",
+           str(a.gpus), "--master-addr", "127.0.0.1", "--master-port", str(port),
+           os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def rank_camera(cam, rank):
+    """Config 2 under N ranks: rank r renders its own view of the replicated
+    scene -- the config-2 camera translated by 0.05 r along x (about 15 px of
+    parallax at the scene's median depth; rank 0 = the single-GPU view)."""
+    if rank == 0:
+        return cam
+    from paper_2512_02932_b200.synthetic import synthetic_camera
+    w2c = np.array(cam.world_to_camera, dtype=np.float64)
+    w2c[0, 3] -= 0.05 * rank
+    return synthetic_camera(cam.width, cam.height, w2c)
 
 
 def parse():
@@ -76,7 +111,7 @@ def parse():
     ap.add_argument("--e2e-warmup", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-crop", type=int, default=4, help="cpu sample = 1/crop^2 of the frame")
+    ap.add_argument("--cpu-steps", type=int, default=1, help="full-frame CPU baseline steps")
     return ap.parse_args()
 
 
@@ -86,7 +121,9 @@ def workload_config(a, n_gpus):
                         % (a.n, a.sh_degree, a.width, a.height, a.kg),
             "n_gaussians": a.n, "width": a.width, "height": a.height, "sh_degree": a.sh_degree,
             "kg": a.kg, "views_per_gpu_per_step": 1,
-            "parallelism": "camera-sharded dp%d + NCCL all-reduce of the gradient buffer" % n_gpus
+            "parallelism": "camera-sharded dp%d (a distinct view per rank) + %s all-reduce of the "
+                           "gradient buffer in %d buckets overlapped with the chain rule"
+                           % (n_gpus, os.environ.get("HGS_DIST_BACKEND", "nccl").upper(), N_BUCKETS)
             if n_gpus > 1 else "single GPU",
             "l2": "flushed between timed steps (256 MiB write); scene (237 MB) > L2 (126 MB)",
             "decisions": "fast (f32 only)" if a.fast else "exact (f64 re-check near thresholds)"}
@@ -183,61 +220,81 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------ CPU baseline
-def cpu_baseline(scene, cam, st, crop, kg=1):
-    """The oracle port on all host cores: full build_frame + fwd/bwd blend of a
-    centred 1/crop^2 crop, extrapolated linearly in pixel count."""
-    import oracle
-    from paper_2512_02932_b200.synthetic import synthetic_camera
+def _host_threads():
     # all host cores (torchrun sets OMP_NUM_THREADS=1 per rank)
-    oracle.set_num_threads(len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity")
-                           else os.cpu_count())
-    W, H = cam.width, cam.height
-    cw, ch = W // crop, H // crop
-    ccam = synthetic_camera(cw, ch)
-    ccam.fx, ccam.fy = cam.fx, cam.fy
-    ccam.cx, ccam.cy = cam.cx - (W - cw) / 2.0, cam.cy - (H - ch) / 2.0
+    return len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+
+
+def cpu_frame_step(scene, cam, st, kg=1, seed=0):
+    """One full step of the reference's CPU path on the whole frame (no crop,
+    no extrapolation): build_frame + forward blend + backward (blend replay +
+    chain rule) on all host cores.  Returns (seconds, fwd seconds, parts)."""
+    import oracle
+    oracle.set_num_threads(_host_threads())
+    rng = np.random.default_rng(seed)
+    pg = rng.normal(size=(kg, cam.height, cam.width, 3))
     t0 = time.perf_counter()
-    oracle.build_frame(scene, cam, st)
-    t_build = time.perf_counter() - t0
-    fc = oracle.build_frame(scene, ccam, st)
-    rng = np.random.default_rng(0)
-    pg = rng.normal(size=(kg, ch, cw, 3))
-    t0 = time.perf_counter()
-    oracle.render(scene, ccam, st, frame=fc)
-    t_fwd = time.perf_counter() - t0
-    t0 = time.perf_counter()
-    oracle.backward(scene, ccam, st, pg, frame=fc)
-    t_bwd = time.perf_counter() - t0
-    scale = (W * H) / float(cw * ch)
-    t_iter = t_build + (t_fwd + t_bwd) * scale
-    t_frame = t_build + t_fwd * scale
+    f = oracle.build_frame(scene, cam, st)
+    t1 = time.perf_counter()
+    oracle.render(scene, cam, st, frame=f)
+    t2 = time.perf_counter()
+    oracle.backward(scene, cam, st, pg, frame=f)
+    t3 = time.perf_counter()
+    return t3 - t0, t2 - t0, (t1 - t0, t2 - t1, t3 - t2)
+
+
+def cpu_baseline(scene, cam, st, kg=1, steps=1):
+    """The oracle port (float64 C restatement of the reference CPU path) on all
+    host cores, timed on full 1080p frames of the same workload."""
+    import oracle
+    ts, tf, parts = [], [], None
+    for i in range(steps):
+        t, f, parts = cpu_frame_step(scene, cam, st, kg, seed=i)
+        ts.append(t)
+        tf.append(f)
+    t_iter, t_fwd = float(np.mean(ts)), float(np.mean(tf))
     return {"value": 1.0 / t_iter, "unit": "iters/s", "cores": oracle.num_threads(),
-            "kind": "port", "fwd_frames_per_s": 1.0 / t_frame,
-            "sample": "oracle/hgs_oracle.c (float64, OpenMP): build_frame on all %d Gaussians "
-                      "(%.2fs) + fwd (%.2fs) + bwd (%.2fs) blend of a centred %dx%d crop, "
-                      "extrapolated x%.1f in pixel count" % (scene.count, t_build, t_fwd, t_bwd,
-                                                             cw, ch, scale)}
+            "kind": "port", "fwd_frames_per_s": 1.0 / t_fwd,
+            "sample": "oracle/hgs_oracle.c (float64, OpenMP, %d threads): %d full %dx%d step(s) on "
+                      "all %d Gaussians, measured (no crop, no extrapolation): build_frame %.2fs + "
+                      "forward blend %.2fs + backward %.2fs (last step)"
+                      % ((oracle.num_threads(), steps, cam.width, cam.height, scene.count) + parts)}
 
 
 def run_reference(a):
-    """--impl reference: the reference's CPU path (oracle port, all host
-    threads) on the same workload; rank 0 only."""
+    """--impl reference: the reference's CPU path (the oracle port, all host
+    threads) on the same workload, full frames; rank 0 only.  Warm-up is one
+    step and the timed steps are capped so the run stays within ~2 minutes."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
+    import oracle
     from paper_2512_02932_b200.settings import RenderSettings
     from paper_2512_02932_b200.synthetic import synthetic_scene
     scene, cam = synthetic_scene(a.n, a.width, a.height, a.sh_degree, seed=0)
     st = RenderSettings()
-    vals = []
-    for i in range(a.warmup + a.steps):
-        cb = cpu_baseline(scene, cam, st, a.cpu_crop, a.kg)
-        if i >= a.warmup:
-            vals.append(cb["value"])
-    v = float(np.mean(vals))
-    cb["value"] = v
-    line = {"metric": METRIC, "value": v, "unit": "iters/s", "n_gpus": a.gpus, "steps": a.steps,
-            "warmup": a.warmup, "ms_per_step": 1000.0 / v, "higher_is_better": True,
+    budget_s = float(os.environ.get("HGS_REF_BUDGET_S", "120"))
+    t_w = 0.0
+    for i in range(min(a.warmup, 1)):
+        t_w = cpu_frame_step(scene, cam, st, a.kg, seed=1000 + i)[0]
+    steps = a.steps
+    if t_w > 0:
+        steps = max(1, min(a.steps, int(budget_s / t_w)))
+    ts, tf, parts = [], [], None
+    for i in range(steps):
+        t, f, parts = cpu_frame_step(scene, cam, st, a.kg, seed=i)
+        ts.append(t)
+        tf.append(f)
+    v = 1.0 / float(np.mean(ts))
+    cb = {"value": v, "unit": "iters/s", "cores": oracle.num_threads(), "kind": "port",
+          "fwd_frames_per_s": 1.0 / float(np.mean(tf)),
+          "sample": "oracle/hgs_oracle.c (float64, OpenMP, %d threads): %d timed full %dx%d "
+                    "fwd+bwd steps (+%d warm-up; --steps %d capped to a %.0f s budget), all %d "
+                    "Gaussians, measured: build_frame %.2fs + forward blend %.2fs + backward %.2fs "
+                    "(last step)" % ((oracle.num_threads(), steps, a.width, a.height, min(a.warmup, 1),
+                                     a.steps, budget_s, a.n) + parts)}
+    line = {"metric": METRIC, "value": v, "unit": "iters/s", "n_gpus": a.gpus, "steps": steps,
+            "warmup": min(a.warmup, 1), "ms_per_step": 1000.0 / v, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": workload_config(a, 1), "impl": "reference", "cpu_baseline": cb,
             "e2e": {"value": v, "unit": "iters/s", "h2d_bytes_per_step": 0,
@@ -285,12 +342,13 @@ def run_extra(a):
         unit = "views/s"
     ds = DeviceGaussians.from_host(scene, dev)
     P = 11 + 3 * ds.sh_bases
+    if a.config == 3 and world > 1:  # one view per rank: a distinct camera each (camera sharding)
+        cams = [rank_camera(cam, rank)]
     gen = torch.Generator(device=dev).manual_seed(99 + rank)
     pg = torch.randn((1, H, W, 3), device=dev, generator=gen)
     dg = torch.randn((1, H, W), device=dev, generator=gen) * 0.1 if a.config == 3 else None
     ng = torch.randn((1, H, W, 3), device=dev, generator=gen) * 0.1 if a.config == 3 else None
     acc = torch.zeros(n * P, dtype=torch.float32, device=dev)
-    gbuf = torch.empty((1, n * P), dtype=torch.float32, device=dev)
     tbuf = torch.empty(n, dtype=torch.uint8, device=dev)
     scratch = torch.empty(_lib.lib().hgs_backward_scratch_bytes(n, 1), dtype=torch.uint8, device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
@@ -298,15 +356,13 @@ def run_extra(a):
     info = {}
 
     def step():
-        acc.zero_()
-        for v in views:
-            _, frame = raster.rasterize(ds, cams[v], st, flags)
-            grad.backward_device(frame, pg, depth_grads=dg, normal_grads=ng, grads_out=gbuf,
-                                 touched_out=tbuf, scratch=scratch)
-            acc.add_(gbuf[0])
+        # every view's gradient summed by the chain rule itself (HGS_FLAG_ACCUMULATE),
+        # the all-reduce bucketed and overlapped with the last view's chain rule
+        frame = parallel.view_batch_grads(ds, [cams[v] for v in views], st, lambda j, im: pg, acc,
+                                          scratch=scratch, touched=tbuf, flags=flags,
+                                          buckets=N_BUCKETS, ext_grads=(dg, ng, None))
+        if frame is not None:
             info["K"] = frame.pair_count
-        if world > 1:
-            parallel.allreduce_grads(acc)
         if a.config == 3:
             info["exchange"] = exchange.exchange_pass_device(ds, xcfg)
 
@@ -374,6 +430,7 @@ def run_train(a):
     n = 3_000_000 if a.n == 1_000_000 else a.n
     W, H = a.width, a.height
     scene, cam = synthetic_scene(n, W, H, 3, seed=0)
+    cam = rank_camera(cam, rank)  # each rank trains on its own view
     st = RenderSettings()
     ds = DeviceGaussians.from_host(scene, dev)
     # target image: render of an independent scene of the same statistics
@@ -478,6 +535,9 @@ def main():
     if a.impl == "reference":
         run_reference(a)
         return
+    rc = self_launch(a)
+    if rc is not None:
+        sys.exit(rc)
     if a.config == 4:
         run_train(a)
         return
@@ -499,8 +559,11 @@ def main():
     dev = torch.device("cuda", local)
     if world > 1:
         init_dist(dev)
+        if a.kg != 1:
+            raise SystemExit("bench.py: the multi-rank step sums KG = 1 view gradients")
 
-    scene, cam = synthetic_scene(a.n, a.width, a.height, a.sh_degree, seed=0)
+    scene, cam0 = synthetic_scene(a.n, a.width, a.height, a.sh_degree, seed=0)
+    cam = rank_camera(cam0, rank)  # distinct view per rank (camera sharding)
     st = RenderSettings()
     ds = DeviceGaussians.from_host(scene, dev)
     flags = _lib.HGS_FLAG_FAST if a.fast else 0
@@ -521,11 +584,14 @@ def main():
         return torch.cuda.Event(enable_timing=True)
 
     def step(fe=None, be=None):
+        if world > 1:  # the multi-view gradient exchange, bucketed and overlapped
+            return parallel.view_batch_grads(ds, [cam], st, lambda j, im: pg, grads_buf[0],
+                                             scratch=scratch, touched=touched_buf, flags=flags,
+                                             buckets=N_BUCKETS, events=be, fwd_events=fe,
+                                             outputs=imgs)
         _, frame = raster.rasterize(ds, cam, st, flags, outputs=imgs, events=fe)
         grad.backward_device(frame, pg, grads_out=grads_buf, touched_out=touched_buf, events=be,
                              scratch=scratch)
-        if world > 1:
-            parallel.allreduce_grads(grads_buf)  # the multi-view gradient exchange
         return frame
 
     def fwd_only(fe=None):
@@ -654,8 +720,9 @@ def main():
     # init_state, depth_keys, radix_offsets, <depth passes>, rank_scatter, preprocess, scan_counts,
     # duplicate, radix_offsets, <tile passes>, tile_ranges, composite_fwd, fixup_fwd
     launches_fwd = 11 + n_depth_passes + n_tile_passes
-    # init_state + (composite_bwd + fixup_bwd + chain_rule) per chunk of <= 4 gradients
-    launches_bwd = 1 + 3 * ((a.kg + 3) // 4)
+    # init_state + (composite_bwd + fixup_bwd + chain_rule) per chunk of <= 4 gradients; under
+    # N ranks the chain rule runs in N_BUCKETS Gaussian ranges (overlapped all-reduce)
+    launches_bwd = 1 + 3 * ((a.kg + 3) // 4) + ((N_BUCKETS - 1) if world > 1 else 0)
     value = world * 1000.0 / step_ms
 
     # ---- e2e through the public API with host buffers (rank-local)
@@ -665,11 +732,12 @@ def main():
         host_scene = GaussianSet(scene.center, scene.log_scale, scene.rotation, scene.opacity_logit,
                                  scene.sh_coeffs, scene.type_spec)
         pg_host = pg[0].double().cpu().numpy()
-        # float32 crosses PCIe (the float64 <-> float32 conversion runs on the
-        # host cores into pinned staging, _hostio.py); uint8 type mask
-        h2d = 4 * (host_scene.center.size + host_scene.log_scale.size + host_scene.rotation.size
-                   + host_scene.opacity_logit.size + host_scene.sh_coeffs.size
-                   + pg_host.size) + host_scene.type_spec.size
+        # the geometry crosses PCIe as float64 (the exact-decision inputs), SH
+        # coefficients and the pixel gradient as float32 (converted on the host
+        # cores into pinned staging, _hostio.py); uint8 type mask
+        h2d = (8 * (host_scene.center.size + host_scene.log_scale.size + host_scene.rotation.size
+                    + host_scene.opacity_logit.size)
+               + 4 * (host_scene.sh_coeffs.size + pg_host.size) + host_scene.type_spec.size)
         ts = []
         for i in range(a.e2e_warmup + a.e2e_steps):
             torch.cuda.synchronize()
@@ -689,11 +757,11 @@ def main():
         e2e = {"value": world / tt, "unit": "iters/s", "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h),
                "path": "raster.render(GaussianSet float64 numpy) + grad.backward(numpy pixel_grad)"
-                       " -> numpy float64 images and ParamGrads (float32 over PCIe via pinned staging, f64<->f32 on the host cores); wall clock with device syncs"}
+                       " -> numpy float64 images and ParamGrads (geometry float64, SH / images / gradients float32 over PCIe via pinned staging; conversions on the host cores); wall clock with device syncs"}
 
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
-        cpu = cpu_baseline(scene, cam, st, a.cpu_crop, a.kg)
+        cpu = cpu_baseline(scene, cam, st, a.kg, a.cpu_steps)
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "iters/s", "n_gpus": world,

@@ -107,6 +107,10 @@ typedef struct hgs_settings {
                                      * scratch of hgs_backward_det_scratch_bytes */
 #define HGS_FLAG_DEFER_ALL 0x10u /* tests: with HGS_FLAG_COUNT, defer every pixel of the forward to the float64
                                     resume kernel (exercises the deferred-pixel path on a whole image) */
+#define HGS_FLAG_REPLAY_ONLY 0x20u /* hgs_backward (kg <= 4): the back-to-front replay only; the screen-space
+                                      accumulators stay in the scratch for hgs_backward_chain */
+#define HGS_FLAG_ACCUMULATE 0x40u  /* hgs_backward / hgs_backward_chain: grads += this view's gradient
+                                      (multi-view batches) instead of grads = */
 
 /* Output images (device, row-major).  Any of normal / alpha may be NULL. */
 typedef struct hgs_images {
@@ -163,6 +167,16 @@ int hgs_backward(const hgs_scene *scene, const hgs_camera *camera, const hgs_set
                  const hgs_frame_info *info, int32_t kg, const float *pixel_grads, const float *depth_grads,
                  const float *normal_grads, const float *alpha_grads, void *scratch, size_t scratch_bytes,
                  float *grads, uint8_t *touched, void *stream);
+
+/* The per-Gaussian chain rule (grad/backward.py:68-178) of the last
+ * hgs_backward with HGS_FLAG_REPLAY_ONLY on this scratch (kg <= 4), for the
+ * Gaussians [g0, g1) only: grads rows g0..g1-1 of every field are written (or,
+ * with HGS_FLAG_ACCUMULATE, added to).  A multi-view step runs it in buckets
+ * so each bucket's gradient all-reduce overlaps the next bucket's chain rule. */
+int hgs_backward_chain(const hgs_scene *scene, const hgs_camera *camera, const hgs_settings *settings,
+                       const void *frame, const hgs_frame_info *info, int32_t kg, const float *depth_grads,
+                       const float *normal_grads, const float *alpha_grads, const void *scratch,
+                       size_t scratch_bytes, int64_t g0, int64_t g1, float *grads, void *stream);
 
 /* Adaptive type exchange (exchange.py:137-155), in place on log_scale, rotation
  * and type_spec (device).  eranks (n) float out (nullable).  report (host) =

@@ -137,11 +137,13 @@ typedef struct hgs_densify_config {
   double clone_step;     /* clone offset, in units of the max scale, against the centre's Adam moment (0 = copy) */
 } hgs_densify_config;
 
-/* After hgs_backward (kg <= 4, same scratch): per Gaussian touched by the view,
- * grad_accum += |NDC-space gradient of the projected centre| summed over the
- * kg stacked losses, obs_count += 1 (3DGS's densification statistics). */
-int hgs_densify_stats(const hgs_scene *scene, const hgs_camera *camera, const void *bwd_scratch, int32_t kg,
-                      const uint8_t *touched, float *grad_accum, int32_t *obs_count, void *stream);
+/* After hgs_backward (kg <= 4, same scratch, and the frame it replayed): per
+ * Gaussian touched by the view, grad_accum += |NDC-space gradient of the
+ * projected centre| summed over the kg stacked losses, obs_count += 1 (3DGS's
+ * densification statistics). */
+int hgs_densify_stats(const hgs_scene *scene, const hgs_camera *camera, const void *frame,
+                      const hgs_frame_info *info, const void *bwd_scratch, int32_t kg, const uint8_t *touched,
+                      float *grad_accum, int32_t *obs_count, void *stream);
 
 size_t hgs_densify_scratch_bytes(int64_t n);
 

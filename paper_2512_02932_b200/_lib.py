@@ -28,6 +28,8 @@ HGS_FLAG_FAST = 0x2
 HGS_FLAG_COUNT = 0x4
 HGS_FLAG_DETERMINISTIC = 0x8
 HGS_FLAG_DEFER_ALL = 0x10  # tests: with HGS_FLAG_COUNT, every pixel goes through the float64 resume kernel
+HGS_FLAG_REPLAY_ONLY = 0x20  # hgs_backward: replay only, the chain rule follows via hgs_backward_chain
+HGS_FLAG_ACCUMULATE = 0x40   # grads += (multi-view batches)
 
 # hgs_train.h constants
 HGS_LOSS_L1, HGS_LOSS_SSIM, HGS_LOSS_LOW, HGS_LOSS_HIGH, HGS_LOSS_COLOR = range(5)
@@ -36,7 +38,8 @@ COMBINE_MODES = {"projection": 0, "naive": 1, "mask": 2}
 
 # Every symbol include/hgs.h and include/hgs_train.h declare.
 EXPORTS = ("hgs_abi_version", "hgs_status_string", "hgs_frame_bytes", "hgs_forward",
-           "hgs_backward_scratch_bytes", "hgs_backward_det_scratch_bytes", "hgs_backward", "hgs_exchange",
+           "hgs_backward_scratch_bytes", "hgs_backward_det_scratch_bytes", "hgs_backward",
+           "hgs_backward_chain", "hgs_exchange",
            "hgs_exchange_f64",
            "hgs_frame_export_arrays", "hgs_blend_log", "hgs_frame_stats",
            "hgs_loss_scratch_bytes", "hgs_image_losses", "hgs_dwt_level1", "hgs_dwt_inverse",
@@ -149,6 +152,8 @@ def lib():
     L.hgs_backward_det_scratch_bytes.argtypes = [_i64, _i32, _i64]
     L.hgs_backward.argtypes = [P(Scene), P(Camera), P(Settings), _vp, P(FrameInfo), _i32, _vp, _vp,
                                _vp, _vp, _vp, ctypes.c_size_t, _vp, _vp, _vp]
+    L.hgs_backward_chain.argtypes = [P(Scene), P(Camera), P(Settings), _vp, P(FrameInfo), _i32, _vp,
+                                     _vp, _vp, _vp, ctypes.c_size_t, _i64, _i64, _vp, _vp]
     L.hgs_exchange.argtypes = [_i64, _vp, _vp, _vp, ctypes.c_double, _vp, _vp, P(ExchangeReport),
                                _vp]
     L.hgs_exchange_f64.argtypes = L.hgs_exchange.argtypes
@@ -167,7 +172,8 @@ def lib():
     L.hgs_adam_step.argtypes = [P(Params), _vp, _vp, _vp, P(AdamCfg), _vp]
     L.hgs_combine_adam_step.argtypes = [P(Params), _vp, _vp, _vp, _vp, _i32, _vp, _vp, P(AdamCfg),
                                         _vp, _vp]
-    L.hgs_densify_stats.argtypes = [P(Scene), P(Camera), _vp, _i32, _vp, _vp, _vp, _vp]
+    L.hgs_densify_stats.argtypes = [P(Scene), P(Camera), _vp, P(FrameInfo), _vp, _i32, _vp, _vp, _vp,
+                                    _vp]
     L.hgs_densify_scratch_bytes.restype = ctypes.c_size_t
     L.hgs_densify_scratch_bytes.argtypes = [_i64]
     L.hgs_densify_plan.argtypes = [P(Scene), _vp, _vp, P(DensifyCfg), _vp, ctypes.c_size_t,

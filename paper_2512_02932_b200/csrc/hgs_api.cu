@@ -130,6 +130,17 @@ int check_common(const hgs_scene *sc, const hgs_camera *cam, const hgs_settings 
 
 #define HGS_LAUNCHED() HGS_CUDA(cudaGetLastError())
 
+// The chain rule over Gaussians [g0, g1): one warp per CTA; shared memory:
+// SH rows in + one SH-gradient set out.
+cudaError_t chain_rule_range(ChainArgs c, int sh_bases, int64_t g0, int64_t g1, cudaStream_t s) {
+  if (g1 <= g0) return cudaSuccess;
+  c.g0 = g0;
+  c.g1 = g1;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(g1 - g0, 32), 148 * 48));
+  const size_t smem = (size_t)2 * 32 * (3 * sh_bases + 1) * sizeof(float);
+  return launch_chain_rule(c, sh_bases, grid, smem, s);
+}
+
 cudaError_t record_event(const hgs_settings *st, int i, cudaStream_t s) {
   if (!st->timing_events || i >= st->n_timing_events || !st->timing_events[i]) return cudaSuccess;
   return cudaEventRecord(static_cast<cudaEvent_t>(st->timing_events[i]), s);
@@ -164,6 +175,12 @@ int radix_sort(K *ka, K *kb, uint32_t *va, uint32_t *vb, int64_t n, const int *p
 }
 
 }  // namespace
+
+const float2 *frame_eig(const void *frame, const hgs_frame_info *info) {
+  const Layout L = make_layout(info->n, info->width, info->height, info->pair_capacity);
+  return at<float2>(frame, L.eig);
+}
+
 }  // namespace hgs
 
 using namespace hgs;
@@ -488,7 +505,10 @@ int hgs_backward(const hgs_scene *scene, const hgs_camera *camera, const hgs_set
   }
   HGS_LAUNCHED();
   const Layout FLc = make_layout(info->n, info->width, info->height, info->pair_capacity);
-  const ChainArgs c0{sc, cam, mod, acc, ext ? acc_ext : nullptr, 0, nullptr, at<float2>(frame, FLc.eig)};
+  const bool replay_only = settings->flags & HGS_FLAG_REPLAY_ONLY;
+  if (replay_only && kg > 4) return HGS_ERR_CONFIG;
+  const ChainArgs c0{sc, cam, mod, acc, ext ? acc_ext : nullptr, 0, nullptr, at<float2>(frame, FLc.eig),
+                     0, 0, (settings->flags & HGS_FLAG_ACCUMULATE) ? 1 : 0};
   for (int k0 = 0; k0 < kg; k0 += 4) {
     const int kc = std::min(4, kg - k0);
     HGS_CUDA(cudaMemsetAsync(acc, 0, (size_t)nn * kc * 16 * sizeof(acc_t), s));
@@ -548,17 +568,37 @@ int hgs_backward(const hgs_scene *scene, const hgs_camera *camera, const hgs_set
       }
       if (k0 == 0) HGS_CUDA(record_event(settings, 1, s));
     }
+    if (replay_only) break;  // kg <= 4: the accumulators stay for hgs_backward_chain
     ChainArgs c = c0;
     c.kg = kc;
     c.grads = grads + (int64_t)k0 * n * P;
-    if (n > 0) {
-      // one warp per CTA; shared memory: SH rows in + kc SH-gradient rows out
-      const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 32), 148 * 48));
-      const size_t smem = (size_t)2 * 32 * (3 * scene->sh_bases + 1) * sizeof(float);  // SH in + one SH out
-      HGS_CUDA(launch_chain_rule(c, scene->sh_bases, grid, smem, s));
-    }
+    HGS_CUDA(chain_rule_range(c, scene->sh_bases, 0, n, s));
   }
   HGS_CUDA(record_event(settings, 2, s));
+  return HGS_OK;
+}
+
+int hgs_backward_chain(const hgs_scene *scene, const hgs_camera *camera, const hgs_settings *settings,
+                       const void *frame, const hgs_frame_info *info, int32_t kg, const float *depth_grads,
+                       const float *normal_grads, const float *alpha_grads, const void *scratch,
+                       size_t scratch_bytes, int64_t g0, int64_t g1, float *grads, void *stream) {
+  int rc = check_common(scene, camera, settings);
+  if (rc) return rc;
+  rc = check_frame(scene, camera, info);
+  if (rc) return rc;
+  if (kg < 1 || kg > 4 || !scratch || scratch_bytes < hgs_backward_scratch_bytes(scene->n, kg)) return HGS_ERR_CONFIG;
+  if (g0 < 0 || g1 < g0 || g1 > scene->n || (g1 > g0 && !grads)) return HGS_ERR_CONFIG;
+  if (g1 == g0) return HGS_OK;
+  const int64_t nn = std::max<int64_t>(scene->n, 1);
+  const acc_t *acc = static_cast<const acc_t *>(scratch);
+  const acc_t *acc_ext = reinterpret_cast<const acc_t *>(static_cast<const char *>(scratch) +
+                                                         ((nn * kg * 16 * (int64_t)sizeof(acc_t) + 255) & ~255ll));
+  const bool ext = depth_grads || normal_grads || alpha_grads;
+  const Layout FL = make_layout(info->n, info->width, info->height, info->pair_capacity);
+  ChainArgs c{make_scene(*scene), make_cam(*camera), ModD{settings->theta_z, settings->t_z, settings->lambda_z},
+              acc, ext ? acc_ext : nullptr, kg, grads, at<float2>(frame, FL.eig), 0, 0,
+              (settings->flags & HGS_FLAG_ACCUMULATE) ? 1 : 0};
+  HGS_CUDA(chain_rule_range(c, scene->sh_bases, g0, g1, static_cast<cudaStream_t>(stream)));
   return HGS_OK;
 }
 

@@ -101,9 +101,6 @@ constexpr int kChainThreads = 32;
 #ifndef HGS_CHAIN_PREFETCH
 #define HGS_CHAIN_PREFETCH 1
 #endif
-#ifndef HGS_CHAIN_WB
-#define HGS_CHAIN_WB 1  // store the pixel-axis 3D sums back (hgs_densify_stats reads them)
-#endif
 #ifndef HGS_CHAIN_MINB
 #define HGS_CHAIN_MINB 16  // 16 warps per SM: 128 registers
 #endif
@@ -118,8 +115,10 @@ __global__ void __launch_bounds__(kChainThreads, HGS_CHAIN_MINB) k_chain_rule_t(
   const int64_t P = 11 + 3 * B;
   const CamD &cam = c.cam;
   const int lane = threadIdx.x;
-  for (int64_t base = (int64_t)blockIdx.x * kChainThreads; base < n; base += (int64_t)gridDim.x * kChainThreads) {
-    const int cnt = (int)(n - base < kChainThreads ? n - base : kChainThreads);
+  const int64_t g_end = c.g1;  // Gaussians [g0, g1) (HGS ranged chain rule); n is the field stride
+  for (int64_t base = c.g0 + (int64_t)blockIdx.x * kChainThreads; base < g_end;
+       base += (int64_t)gridDim.x * kChainThreads) {
+    const int cnt = (int)(g_end - base < kChainThreads ? g_end - base : kChainThreads);
     for (int e = lane; e < cnt * SB; e += kChainThreads) {
       const int r = e / SB;
       s_in[r * SS + (e - r * SB)] = __ldg(c.sc.sh + base * SB + e);
@@ -127,8 +126,8 @@ __global__ void __launch_bounds__(kChainThreads, HGS_CHAIN_MINB) k_chain_rule_t(
 #if HGS_CHAIN_PREFETCH
     {  // next warp step's SH rows, accumulators and scalar fields into L2
       const int64_t nb = base + (int64_t)gridDim.x * kChainThreads;
-      if (nb < n && c.kg == 1) {  // (measured: a net loss for the 3-gradient training step)
-        const int nc = (int)(n - nb < kChainThreads ? n - nb : kChainThreads);
+      if (nb < g_end && c.kg == 1) {  // (measured: a net loss for the 3-gradient training step)
+        const int nc = (int)(g_end - nb < kChainThreads ? g_end - nb : kChainThreads);
         const char *sh0 = reinterpret_cast<const char *>(c.sc.sh + nb * SB);
         for (int l = lane; l * 128 < nc * SB * 4; l += kChainThreads)
           asm volatile("prefetch.global.L2 [%0];" ::"l"(sh0 + 128 * l));
@@ -227,11 +226,13 @@ __global__ void __launch_bounds__(kChainThreads, HGS_CHAIN_MINB) k_chain_rule_t(
     for (int k = 0; k < c.kg; ++k) {
       float *g = c.grads + (int64_t)k * n * P;
       if (valid && !any) {
+        if (!c.accumulate) {
 #pragma unroll
-        for (int s = 0; s < 3; ++s) { g[3 * i + s] = 0.f; g[3 * n + 3 * i + s] = 0.f; }
+          for (int s = 0; s < 3; ++s) { g[3 * i + s] = 0.f; g[3 * n + 3 * i + s] = 0.f; }
 #pragma unroll
-        for (int s = 0; s < 4; ++s) g[6 * n + 4 * i + s] = 0.f;
-        g[10 * n + i] = 0.f;
+          for (int s = 0; s < 4; ++s) g[6 * n + 4 * i + s] = 0.f;
+          g[10 * n + i] = 0.f;
+        }
 #pragma unroll
         for (int s = 0; s < SB; ++s) so[s] = 0.f;
       }
@@ -268,8 +269,7 @@ __global__ void __launch_bounds__(kChainThreads, HGS_CHAIN_MINB) k_chain_rule_t(
       if (is3d) {
         // slots 4-8 hold the eigenbasis sums (pair_grads); rotate them with
         // the record's own float32 (c, s) -- the basis the pairs used -- to
-        // pixel axes, v = M w with M = [[c, -s], [s, c]], in float64, and
-        // store the pixel-axis values back for the densification statistics
+        // pixel axes, v = M w with M = [[c, -s], [s, c]], in float64
         const float2 e = __ldg(&c.eig[i]);
         const double cs = e.x, sn = e.y;
         const double Sp = A[4], Sq = A[5], Gpp = A[6], Gpq = A[7], Gqq = A[8];
@@ -278,10 +278,6 @@ __global__ void __launch_bounds__(kChainThreads, HGS_CHAIN_MINB) k_chain_rule_t(
         G00 = (cs * cs * Gpp - 2.0 * cs * sn * Gpq) + sn * sn * Gqq;
         G01 = (cs * sn * Gpp + (cs * cs - sn * sn) * Gpq) - cs * sn * Gqq;
         G11 = (sn * sn * Gpp + 2.0 * cs * sn * Gpq) + cs * cs * Gqq;
-#if HGS_CHAIN_WB
-        acc_t *Aw = c.acc + ((int64_t)i * c.kg + k) * kAcc;
-        Aw[4] = gx; Aw[5] = gy; Aw[6] = G00; Aw[7] = G01; Aw[8] = G11;
-#endif
       }
       const double Xd = td[0], Yd = td[1], Zd = td[2];
       const double fxd = cam.fx, fyd = cam.fy;
@@ -399,25 +395,34 @@ __global__ void __launch_bounds__(kChainThreads, HGS_CHAIN_MINB) k_chain_rule_t(
                                  2.f * zq * GR(1, 1)) + y * GR(1, 2)) + x * GR(2, 0)) + y * GR(2, 1));
 #undef GR
       const float dotq = ((dw * w + dxq * x) + dyq * y) + dzq * zq;
-      g[3 * i + 0] = d_center[0];
-      g[3 * i + 1] = d_center[1];
-      g[3 * i + 2] = d_center[2];
-      g[3 * n + 3 * i + 0] = d_ls[0];
-      g[3 * n + 3 * i + 1] = d_ls[1];
-      g[3 * n + 3 * i + 2] = d_ls[2];
-      g[6 * n + 4 * i + 0] = (dw - dotq * w) * iqn;
-      g[6 * n + 4 * i + 1] = (dxq - dotq * x) * iqn;
-      g[6 * n + 4 * i + 2] = (dyq - dotq * y) * iqn;
-      g[6 * n + 4 * i + 3] = (dzq - dotq * zq) * iqn;
-      g[10 * n + i] = d_logit;
+      const float gv[11] = {d_center[0], d_center[1], d_center[2], d_ls[0], d_ls[1], d_ls[2],
+                            (dw - dotq * w) * iqn, (dxq - dotq * x) * iqn, (dyq - dotq * y) * iqn,
+                            (dzq - dotq * zq) * iqn, d_logit};
+      float *const gp[11] = {g + 3 * i, g + 3 * i + 1, g + 3 * i + 2, g + 3 * n + 3 * i, g + 3 * n + 3 * i + 1,
+                             g + 3 * n + 3 * i + 2, g + 6 * n + 4 * i, g + 6 * n + 4 * i + 1, g + 6 * n + 4 * i + 2,
+                             g + 6 * n + 4 * i + 3, g + 10 * n + i};
+      if (c.accumulate) {  // multi-view: this view's gradient is added to the running sum
+#pragma unroll
+        for (int f = 0; f < 11; ++f) *gp[f] += gv[f];
+      } else {
+#pragma unroll
+        for (int f = 0; f < 11; ++f) *gp[f] = gv[f];
+      }
       }  // any
       __syncwarp();
       // coalesced SH-gradient segment of this warp step
       float *gs = g + 11 * n + base * SB;
       const float *sk = s_chain + kChainThreads * SS;
-      for (int e = lane; e < cnt * SB; e += kChainThreads) {
-        const int r = e / SB;
-        gs[e] = sk[r * SS + (e - r * SB)];
+      if (c.accumulate) {
+        for (int e = lane; e < cnt * SB; e += kChainThreads) {
+          const int r = e / SB;
+          gs[e] += sk[r * SS + (e - r * SB)];
+        }
+      } else {
+        for (int e = lane; e < cnt * SB; e += kChainThreads) {
+          const int r = e / SB;
+          gs[e] = sk[r * SS + (e - r * SB)];
+        }
       }
       __syncwarp();
     }

@@ -33,7 +33,8 @@ constexpr int kDScan = 1024;
 
 enum : uint8_t { kKeep = 0, kPrune = 1, kClone = 2, kSplit = 3 };
 
-__global__ void k_densify_stats(SceneView sc, CamD cam, const acc_t *acc, int kg, const uint8_t *touched,
+__global__ void k_densify_stats(SceneView sc, CamD cam, const acc_t *acc, const float2 *eig, int kg,
+                                const uint8_t *touched,
                                 float half_w, float half_h, float *grad_accum, int32_t *obs_count) {
   const int64_t n = sc.n;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
@@ -56,9 +57,13 @@ __global__ void k_densify_stats(SceneView sc, CamD cam, const acc_t *acc, int kg
     float gx = 0.f, gy = 0.f;
     for (int k = 0; k < kg; ++k) {
       const acc_t *A = acc + ((int64_t)i * kg + k) * kAccD;
-      gx += (float)A[4];
-      gy += (float)A[5];
-      if (!is3d) {
+      if (is3d) {  // eigenbasis sums (hgs_composite_bwd.cu): rotate to pixel axes
+        const float2 e = eig[i];
+        gx += (float)(e.x * A[4] - e.y * A[5]);
+        gy += (float)(e.y * A[4] + e.x * A[5]);
+      } else {
+        gx += (float)A[4];
+        gy += (float)A[5];
         gx += ((float)A[6] * m2[0] + (float)A[7] * m2[1]) + (float)A[8] * m2[2];
         gy += ((float)A[9] * m2[0] + (float)A[10] * m2[1]) + (float)A[11] * m2[2];
       }
@@ -289,18 +294,21 @@ using namespace hgs;
 
 extern "C" {
 
-int hgs_densify_stats(const hgs_scene *scene, const hgs_camera *camera, const void *bwd_scratch, int32_t kg,
-                      const uint8_t *touched, float *grad_accum, int32_t *obs_count, void *stream) {
+int hgs_densify_stats(const hgs_scene *scene, const hgs_camera *camera, const void *frame,
+                      const hgs_frame_info *info, const void *bwd_scratch, int32_t kg, const uint8_t *touched,
+                      float *grad_accum, int32_t *obs_count, void *stream) {
   if (!scene || !camera || scene->n < 0 || kg < 1 || kg > 4) return HGS_ERR_CONFIG;
   if (scene->n == 0) return HGS_OK;
-  if (!bwd_scratch || !touched || !grad_accum || !obs_count) return HGS_ERR_INTEGRITY;
+  if (!bwd_scratch || !touched || !grad_accum || !obs_count || !frame || !info) return HGS_ERR_INTEGRITY;
+  if (info->n != scene->n) return HGS_ERR_INTEGRITY;
   CamD cam;
   for (int r = 0; r < 3; ++r) {
     for (int k = 0; k < 3; ++k) cam.V[r * 3 + k] = camera->world_to_camera[r * 4 + k];
     cam.tv[r] = camera->world_to_camera[r * 4 + 3];
   }
   k_densify_stats<<<grid_of(scene->n), 256, 0, static_cast<cudaStream_t>(stream)>>>(
-      view_of(*scene), cam, static_cast<const acc_t *>(bwd_scratch), kg, touched, 0.5f * (float)camera->width,
+      view_of(*scene), cam, static_cast<const acc_t *>(bwd_scratch), frame_eig(frame, info), kg, touched,
+      0.5f * (float)camera->width,
       0.5f * (float)camera->height, grad_accum, obs_count);
   return cudaGetLastError() == cudaSuccess ? HGS_OK : HGS_ERR_CUDA;
 }

@@ -627,11 +627,13 @@ struct ChainArgs {
   SceneView sc;
   CamD cam;
   ModD mod;
-  acc_t *acc;            // (n, KG, 16); 3D slots 4-8 rotated to pixel axes in place
+  const acc_t *acc;      // (n, KG, 16)
   const acc_t *acc_ext;  // (n, KG, 4) or null
   int kg;
   float *grads;          // (KG, n*P) field-major blocks
   const float2 *eig;     // (n) a 3D splat's float32 eigenbasis (c, s), by Gaussian index
+  int64_t g0, g1;        // Gaussian range of this launch
+  int accumulate;        // grads += (HGS_FLAG_ACCUMULATE) instead of =
 };
 
 struct ExchangeState {
@@ -663,6 +665,8 @@ cudaError_t launch_composite_bwd(const BwdArgs &b, int kg, int64_t n_tiles, bool
 __global__ void k_det_reduce(const unsigned long long *keys, const uint32_t *vals, const float *pay, int64_t nrec,
                              int kg, acc_t *acc, acc_t *acc_ext);
 cudaError_t launch_chain_rule(const ChainArgs &c, int sh_bases, int grid, size_t smem, cudaStream_t s);
+// the frame's per-Gaussian 3D eigenbasis array (hgs_api.cu layout)
+const float2 *frame_eig(const void *frame, const hgs_frame_info *info);
 template <typename T>
 cudaError_t launch_exchange_scan(int64_t n, const T *log_scale, const uint8_t *type_spec, double theta_e, T *eranks,
                                  ExchangeState *st, int grid, cudaStream_t s);

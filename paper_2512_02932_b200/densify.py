@@ -67,15 +67,16 @@ class DensifyStats:
         return int(self.grad_accum.shape[0])
 
 
-def accumulate(scene, camera, stats, bwd_scratch, kg, touched):
-    """Add one view's statistics (call right after grad.backward_device with
-    the same scratch; kg <= 4)."""
+def accumulate(frame, stats, bwd_scratch, kg, touched):
+    """Add one view's statistics (call right after grad.backward_device on
+    ``frame`` with the same scratch; kg <= 4)."""
+    scene = frame.scene
     if stats.count != scene.count:
         raise ConfigError("densify statistics do not match the scene")
     _lib.check(_lib.lib().hgs_densify_stats(
-        _lib.scene_struct(scene), _lib.camera_struct(camera), _lib.ptr(bwd_scratch), int(kg),
-        _lib.ptr(touched), _lib.ptr(stats.grad_accum), _lib.ptr(stats.obs_count),
-        _lib.current_stream_handle(scene.device)), "hgs_densify_stats")
+        _lib.scene_struct(scene), _lib.camera_struct(frame.camera), _lib.ptr(frame.buf), frame.info,
+        _lib.ptr(bwd_scratch), int(kg), _lib.ptr(touched), _lib.ptr(stats.grad_accum),
+        _lib.ptr(stats.obs_count), _lib.current_stream_handle(scene.device)), "hgs_densify_stats")
 
 
 def densify(scene, stats, config=None, optimizer=None):

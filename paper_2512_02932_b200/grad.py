@@ -121,12 +121,15 @@ _det_hint = {}  # (n, kg, W, H) -> record capacity that sufficed last time
 
 def backward_device(frame, pixel_grads, depth_grads=None, normal_grads=None, alpha_grads=None,
                     grads_out=None, touched_out=None, events=None, flags=None, scratch=None,
-                    deterministic=False):
+                    deterministic=False, accumulate=False, replay_only=False):
     """Device-level backward.  pixel_grads (KG,H,W,3) float32 CUDA; returns
     (grads (KG, n*P) float32, touched (n,) uint8).  ``events`` (3
     torch.cuda.Event) are recorded at the library's stage boundaries.
     ``deterministic``: fixed-order gradient reduction (HGS_FLAG_DETERMINISTIC),
-    bitwise reproducible run to run, at extra memory and time."""
+    bitwise reproducible run to run, at extra memory and time.
+    ``accumulate``: grads_out += this view's gradient (HGS_FLAG_ACCUMULATE).
+    ``replay_only`` (KG <= 4): the back-to-front replay only; the chain rule
+    follows in Gaussian ranges through ``chain_range`` with the same scratch."""
     import torch
     L = _lib.lib()
     ds = frame.scene
@@ -141,6 +144,10 @@ def backward_device(frame, pixel_grads, depth_grads=None, normal_grads=None, alp
     fl = frame.flags if flags is None else flags
     if deterministic:
         fl |= _lib.HGS_FLAG_DETERMINISTIC
+    if accumulate:
+        fl |= _lib.HGS_FLAG_ACCUMULATE
+    if replay_only:
+        fl |= _lib.HGS_FLAG_REPLAY_ONLY
     key = (n, kg, frame.width, frame.height)
     records = _det_hint.get(key, 2 * frame.pair_count + (1 << 16))
     for _ in range(8):
@@ -160,8 +167,27 @@ def backward_device(frame, pixel_grads, depth_grads=None, normal_grads=None, alp
         _lib.check(rc, "hgs_backward")
         if deterministic:
             _det_hint[key] = records
+        if replay_only:
+            frame._replay = (scratch, kg, depth_grads, normal_grads, alpha_grads)
         return grads_out, touched_out[:n]
     raise _lib.ExtensionError("could not size the deterministic backward scratch")
+
+
+def chain_range(frame, g0, g1, grads_out, accumulate=False):
+    """The chain rule of the last ``backward_device(frame, ..., replay_only=True)``
+    for Gaussians [g0, g1) into ``grads_out`` (KG, n*P) (hgs_backward_chain)."""
+    rep = getattr(frame, "_replay", None)
+    if rep is None:
+        raise IntegrityError("chain_range needs a replay_only backward on this frame first")
+    scratch, kg, dg, ng, ag = rep
+    fl = frame.flags | (_lib.HGS_FLAG_ACCUMULATE if accumulate else 0)
+    _lib.check(_lib.lib().hgs_backward_chain(
+        _lib.scene_struct(frame.scene), _lib.camera_struct(frame.camera),
+        _lib.settings_struct(frame.settings, fl), _lib.ptr(frame.buf), frame.info, kg,
+        _lib.ptr(dg), _lib.ptr(ng), _lib.ptr(ag), _lib.ptr(scratch), scratch.numel(), int(g0),
+        int(g1), _lib.ptr(grads_out), _lib.current_stream_handle(frame.buf.device)),
+        "hgs_backward_chain")
+    return grads_out
 
 
 def backward(scene, camera, output, pixel_grad, depth_grad=None, normal_grad=None,

@@ -176,7 +176,7 @@ def train_step(scene, camera, gt, optimizer, weights=None, settings=None, flags=
                                 scratch=ws.bwd_scratch)
     if stats is not None:
         from . import densify
-        densify.accumulate(scene, camera, stats, ws.bwd_scratch, 3, ws.touched)
+        densify.accumulate(frame, stats, ws.bwd_scratch, 3, ws.touched)
     if ev[3] is not None:
         ev[3].record()
     nc = optimizer.step_combined(g[0], g[1], g[2], w.mode)

@@ -15,7 +15,8 @@ sharding and reduction logic with the oracle.
 import math
 
 __all__ = ["shard_views", "allreduce_grads", "replica_checksum", "MultiViewStep",
-           "default_view_grad"]
+           "default_view_grad", "field_slices", "bucket_bounds", "bucketed_allreduce",
+           "view_batch_grads"]
 
 
 def shard_views(n_views, rank, world):
@@ -34,6 +35,91 @@ def allreduce_grads(buf, group=None):
     if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
         dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=group)
     return buf
+
+
+def field_slices(buf, n, sh_bases, g0, g1):
+    """The five slices of a flat field-major gradient buffer (center | log_scale
+    | rotation | opacity | sh, include/hgs.h) that hold Gaussians [g0, g1)."""
+    B3 = 3 * sh_bases
+    out = []
+    off = 0
+    for width in (3, 3, 4, 1, B3):
+        out.append(buf[off + width * g0: off + width * g1])
+        off += width * n
+    return out
+
+
+def bucket_bounds(n, buckets):
+    """[g0, g1) Gaussian ranges of ``buckets`` near-equal buckets (multiples of
+    32, the chain rule's warp step)."""
+    step = -(-max(n, 1) // max(buckets, 1))
+    step = -(-step // 32) * 32
+    return [(g0, min(g0 + step, n)) for g0 in range(0, n, step)]
+
+
+def bucketed_allreduce(out, n, sh_bases, buckets, write_bucket, group=None):
+    """Fill and all-reduce a flat field-major gradient buffer bucket by bucket:
+    ``write_bucket(g0, g1)`` enqueues the writes of Gaussians [g0, g1) (on the
+    GPU: the chain rule over that range), then that bucket's five field slices
+    are all-reduced asynchronously while the next bucket is written.  Waits
+    for every collective before returning (the caller's stream then orders
+    after them)."""
+    import torch.distributed as dist
+    works = []
+    for g0, g1 in bucket_bounds(n, buckets):
+        write_bucket(g0, g1)
+        works += [dist.all_reduce(sl, op=dist.ReduceOp.SUM, group=group, async_op=True)
+                  for sl in field_slices(out, n, sh_bases, g0, g1)]
+    for w in works:
+        w.wait()
+    return out
+
+
+def view_batch_grads(scene, cameras, settings, pixel_grads_of, out, scratch=None, touched=None,
+                     flags=0, buckets=4, group=None, events=None, fwd_events=None, outputs=None,
+                     ext_grads=(None, None, None)):
+    """One data-parallel step's gradient over this rank's views, all-reduced.
+
+    Every view's gradient is added into ``out`` (flat float32 n*P, KG = 1) by
+    the chain rule itself (HGS_FLAG_ACCUMULATE; the first view overwrites).
+    For the last view the chain rule runs in ``buckets`` Gaussian ranges and
+    each range's five field slices are all-reduced asynchronously as soon as
+    it is written, so the collective overlaps the remaining chain rule
+    (NCCL runs on its own stream, ordered after the work already enqueued).
+    ``pixel_grads_of(j, images)`` returns view j's (1, H, W, 3) upstream
+    gradient.  ``fwd_events`` / ``events`` (5 / 3 torch.cuda.Event) time the
+    last view's forward / backward stages; ``outputs`` are reused image
+    buffers; ``ext_grads`` = (depth, normal, alpha) upstream gradients of the
+    extension images (same for every view; each nullable).  Returns the last
+    frame."""
+    import torch.distributed as dist
+
+    from . import grad, raster
+    ready = dist.is_available() and dist.is_initialized()
+    world = dist.get_world_size(group) if ready else 1
+    n, B = scene.count, scene.sh_bases
+    acc = out.view(1, -1)
+    frame = None
+    if not cameras:
+        out.zero_()
+    for j, cam in enumerate(cameras):
+        last = j == len(cameras) - 1
+        imgs, frame = raster.rasterize(scene, cam, settings, flags, outputs=outputs,
+                                       events=fwd_events if last else None)
+        pg = pixel_grads_of(j, imgs)
+        if not last or world == 1:
+            grad.backward_device(frame, pg, *ext_grads, grads_out=acc, touched_out=touched,
+                                 scratch=scratch, accumulate=j > 0, events=events if last else None)
+            continue
+        grad.backward_device(frame, pg, *ext_grads, grads_out=acc, touched_out=touched,
+                             scratch=scratch, replay_only=True, events=events)
+        bucketed_allreduce(out, n, B, buckets,
+                           lambda g0, g1: grad.chain_range(frame, g0, g1, acc, accumulate=j > 0),
+                           group=group)
+        return frame
+    if world > 1:  # no views on this rank: contribute zeros
+        dist.all_reduce(out, op=dist.ReduceOp.SUM, group=group)
+    return frame
 
 
 def replica_checksum(tensors, group=None):

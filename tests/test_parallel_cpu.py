@@ -10,7 +10,8 @@ import pytest
 import torch
 import torch.multiprocessing as mp
 
-from paper_2512_02932_b200.parallel import MultiViewStep, shard_views
+from paper_2512_02932_b200.parallel import (MultiViewStep, bucket_bounds, bucketed_allreduce,
+                                            field_slices, shard_views)
 
 
 def test_shard_views_partition():
@@ -95,3 +96,65 @@ def test_two_rank_allreduce_equals_single_process_sum():
     single = MultiViewStep(scene, cams, st, scene.count * P, view_grad=_oracle_view_grad)
     ref = single.step(_loss_grad).numpy()
     np.testing.assert_allclose(res[0][2], ref, rtol=1e-5, atol=1e-6 * np.abs(ref).max())
+
+
+def test_bucket_slices_partition_the_field_major_buffer():
+    """Every element of the (n*P) field-major buffer is in exactly one
+    bucket's slices, and the slices of Gaussians [g0, g1) hold exactly their
+    rows of each field."""
+    for n, B, nb in ((1000, 16, 4), (37, 1, 3), (64, 4, 8), (5, 9, 1)):
+        P = 11 + 3 * B
+        buf = torch.arange(n * P, dtype=torch.float64)
+        seen = torch.zeros(n * P, dtype=torch.int64)
+        bounds = bucket_bounds(n, nb)
+        assert bounds[0][0] == 0 and bounds[-1][1] == n
+        assert all(b[1] == c[0] for b, c in zip(bounds, bounds[1:]))
+        for g0, g1 in bounds:
+            for sl, width, off in zip(field_slices(buf, n, B, g0, g1), (3, 3, 4, 1, 3 * B),
+                                      (0, 3 * n, 6 * n, 10 * n, 11 * n)):
+                idx = sl.long()
+                assert torch.equal(idx, torch.arange(off + width * g0, off + width * g1))
+                seen[idx] += 1
+        assert bool((seen == 1).all())
+
+
+def _bucket_worker(rank, world, port, n, B, out_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    import torch.distributed as dist
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    P = 11 + 3 * B
+    full = torch.from_numpy(np.random.default_rng(rank).normal(size=n * P)).float()
+    out = torch.full((n * P,), float("nan"))
+    order = []
+
+    def write(g0, g1):  # what the chain rule does for a range: write its rows of each field
+        order.append((g0, g1))
+        for dst, src in zip(field_slices(out, n, B, g0, g1), field_slices(full, n, B, g0, g1)):
+            dst.copy_(src)
+    bucketed_allreduce(out, n, B, 4, write)
+    ref = full.clone()
+    dist.all_reduce(ref)
+    out_q.put((rank, order, out.numpy().copy(), ref.numpy().copy()))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_two_rank_bucketed_allreduce_equals_one_allreduce():
+    """The overlapped, bucketed reduction of the multi-view step
+    (parallel.view_batch_grads) gives the same buffer as one all-reduce."""
+    n, B = 1000, 4
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_bucket_worker, args=(r, 2, port, n, B, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, order, out, ref in res:
+        assert len(order) == 4
+        np.testing.assert_allclose(out, ref, rtol=1e-6, atol=1e-6)
+    assert np.array_equal(res[0][2], res[1][2])
