@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define HGS_ABI_VERSION 2
+#define HGS_ABI_VERSION 3
 
 typedef enum hgs_status {
   HGS_OK = 0,
@@ -86,7 +86,7 @@ typedef struct hgs_camera {
 /* RenderSettings (raster/project.py:34-45) + mode flags. */
 typedef struct hgs_settings {
   float background[3];
-  int32_t tile_size; /* must be 16 */
+  int32_t tile_size; /* 16 (the compositor's tile); see hgs_frame_tile_bins */
   double theta_z, t_z, lambda_z;
   uint32_t flags;
   int32_t n_timing_events;     /* 0, or the length of timing_events            */
@@ -111,6 +111,9 @@ typedef struct hgs_settings {
                                       accumulators stay in the scratch for hgs_backward_chain */
 #define HGS_FLAG_ACCUMULATE 0x40u  /* hgs_backward / hgs_backward_chain: grads += this view's gradient
                                       (multi-view batches) instead of grads = */
+#define HGS_FLAG_FRAME_ONLY 0x80u /* [ABI 3] hgs_forward: build_frame only (project.py:360-379): depth sort,
+                                   * preprocess and binning, no compositing; out may be NULL and the
+                                   * frame cannot be back-propagated */
 
 /* Output images (device, row-major).  Any of normal / alpha may be NULL. */
 typedef struct hgs_images {
@@ -210,6 +213,10 @@ typedef struct hgs_frame_export {
   int64_t *tile_offsets;
   int32_t *tile_ids;
   int32_t *pixel_count; /* (H, W) blend-log entries per pixel */
+  /* [ABI 3] the remaining SplatFrame arrays (project.py:254-257): t_cam (m,3)
+   * camera-space centre, alpha (m) sigmoid(opacity_logit) before modulation,
+   * view_dir (m,3), cam_dist (m) */
+  double *t_cam, *alpha, *view_dir, *cam_dist;
 } hgs_frame_export;
 
 int hgs_frame_export_arrays(const hgs_scene *scene, const hgs_camera *camera, const hgs_settings *settings,
@@ -228,6 +235,49 @@ int hgs_blend_log(const hgs_scene *scene, const hgs_camera *camera, const hgs_se
  *  contributing [7] 2D ray-branch contributing [8] 2D low-pass contributing
  *  [9] pairs evaluated. */
 int hgs_frame_stats(const void *frame, const hgs_frame_info *info, uint64_t *out16, void *stream);
+
+/* [ABI 3] Tile lists of a frame at another tile size.  The compositor always
+ * bins at 16 x 16; the reference bins at settings.tile_size (project.py:37,
+ * _tile_bins :329-357) and only SplatFrame.tile_offsets / tile_ids depend on
+ * it (the image does not).  tile_size in {8, 16, 32, 64}.  Synchronous:
+ * counts the pairs into *k_out and returns HGS_ERR_PAIR_CAPACITY when
+ * ids_capacity < *k_out; otherwise writes tile_offsets ((tiles+1) i64) and
+ * tile_ids (*k_out i32, sorted slots, ascending within a tile).  scratch:
+ * hgs_tile_bins_scratch_bytes(m, W, H, tile_size, ids_capacity). */
+size_t hgs_tile_bins_scratch_bytes(int64_t m, int32_t width, int32_t height, int32_t tile_size, int64_t pair_capacity);
+int hgs_frame_tile_bins(const void *frame, const hgs_frame_info *info, int32_t tile_size, int64_t *tile_offsets,
+                        int32_t *tile_ids, int64_t ids_capacity, void *scratch, size_t scratch_bytes, int64_t *k_out,
+                        void *stream);
+
+/* [ABI 3] Batch forms of the reference's public per-primitive helpers, in
+ * float64 on the device (hgs_helpers.cu), all pointers device pointers.
+ *
+ * evaluate_contribution / ray_splat_intersect (raster/project.py:109-152) for n
+ * (splat, pixel) pairs: typ (n) u8, center2d (n,2), conic (n,3) = (c00, c01,
+ * c11), mrow (n,3,4), opacity (n), pixel (n,2) -> alpha (n) (0 for a degenerate
+ * intersection), u / v (n, nullable: the ray/plane coordinates of 2D pairs,
+ * (dx, dy) for 3D), flags (n, nullable: bit 0 = |den| < 1e-9, the reference's
+ * DegenerateIntersection). */
+int hgs_eval_contributions(int64_t n, const uint8_t *typ, const double *center2d, const double *conic,
+                           const double *mrow, const double *opacity, const double *pixel, double *alpha, double *u,
+                           double *v, int32_t *flags, void *stream);
+/* effective_rank (exchange.py:58-73): log_scale (n,3) -> eranks (n).
+ * Synchronous; HGS_ERR_DEGENERATE_SCALE if any row's squared scales sum to
+ * zero or overflow.  scratch: 256 B of device memory. */
+int hgs_effective_rank_f64(int64_t n, const double *log_scale, double *eranks, void *scratch, void *stream);
+/* choose_permutation + reparameterize_3d_to_2d (exchange.py:76-99):
+ * perm (n) i32 (0 identity, 1 P_x, 2 P_y; nullable), out_log_scale (n,3) /
+ * out_rotation (n,4) (both or neither).  Synchronous; HGS_ERR_INVALID_PARAMETER
+ * for |q| <= 1e-8.  scratch: 256 B. */
+int hgs_reparameterize_f64(int64_t n, const double *log_scale, const double *rotation, double *out_log_scale,
+                           double *out_rotation, int32_t *perm, void *scratch, void *stream);
+/* modulated_z / modulated_opacity / modulated_opacity_grads (exchange.py:
+ * 102-129): opacity (n, the un-modulated alpha; nullable if only sz_star /
+ * d_alpha are wanted), log_scale_z (n) -> sz_star, alpha_eff, d_alpha, d_logz
+ * (each (n), nullable). */
+int hgs_modulation_f64(int64_t n, const double *opacity, const double *log_scale_z, double theta_z, double t_z,
+                       double lambda_z, double *sz_star, double *alpha_eff, double *d_alpha, double *d_logz,
+                       void *stream);
 
 const char *hgs_status_string(int status);
 int hgs_abi_version(void);

@@ -16,8 +16,9 @@ Layout:
 """
 
 from . import errors
-from .core import CameraView, DeviceGaussians, GaussianSet, n_bases
-from .errors import (CheckpointError, ConfigError, DegenerateScaleError, ExtensionError,
+from .core import CameraView, DeviceGaussians, Gaussian, GaussianSet, n_bases
+from .errors import (CheckpointError, ConfigError, DegenerateIntersection, DegenerateScaleError,
+                     ExtensionError,
                      IntegrityError, InvalidParameterError, ManifestError, NumericError,
                      SplatError)
 from .settings import (ALPHA_CLAMP, EARLY_STOP_T, LOWPASS_SIGMA, MIN_ALPHA, SCREEN_DILATION,
@@ -33,10 +34,15 @@ def __getattr__(name):
     import importlib
     if name in ("raster", "grad", "exchange", "parallel", "synthetic"):
         return importlib.import_module("." + name, __name__)
-    if name in ("render", "render_naive", "RenderOutput", "BlendLog", "SplatFrame"):
+    if name in ("render", "render_naive", "RenderOutput", "BlendLog", "SplatFrame", "build_frame",
+                "evaluate_contribution", "ray_splat_intersect", "project_gaussian_3d",
+                "ProjectedSplat"):
         return getattr(importlib.import_module(".raster", __name__), name)
-    if name in ("backward", "ParamGrads", "GradientBundle"):
+    if name in ("backward", "ParamGrads", "GradientBundle", "param_labels", "finite_diff_check",
+                "FiniteDiffReport"):
         return getattr(importlib.import_module(".grad", __name__), name)
-    if name in ("exchange_pass", "ExchangeReport"):
+    if name in ("exchange_pass", "ExchangeReport", "effective_rank", "choose_permutation",
+                "reparameterize_3d_to_2d", "modulated_z", "modulated_opacity",
+                "modulated_opacity_grads", "modulate_opacity"):
         return getattr(importlib.import_module(".exchange", __name__), name)
     raise AttributeError(name)

@@ -13,7 +13,7 @@ from .errors import (ConfigError, DegenerateScaleError, ExtensionError, Integrit
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("HGS_LIB", os.path.join(_HERE, "libhgs.so"))
 
-ABI_VERSION = 2  # include/hgs.h HGS_ABI_VERSION
+ABI_VERSION = 3  # include/hgs.h HGS_ABI_VERSION
 
 HGS_OK = 0
 HGS_ERR_CONFIG = 1
@@ -30,6 +30,8 @@ HGS_FLAG_DETERMINISTIC = 0x8
 HGS_FLAG_DEFER_ALL = 0x10  # tests: with HGS_FLAG_COUNT, every pixel goes through the float64 resume kernel
 HGS_FLAG_REPLAY_ONLY = 0x20  # hgs_backward: replay only, the chain rule follows via hgs_backward_chain
 HGS_FLAG_ACCUMULATE = 0x40   # grads += (multi-view batches)
+HGS_FLAG_FRAME_ONLY = 0x80   # build_frame: no compositing
+COMPOSITOR_TILE = 16         # the compositor's tile; other tile sizes are re-binned on export
 
 # hgs_train.h constants
 HGS_LOSS_L1, HGS_LOSS_SSIM, HGS_LOSS_LOW, HGS_LOSS_HIGH, HGS_LOSS_COLOR = range(5)
@@ -44,7 +46,9 @@ EXPORTS = ("hgs_abi_version", "hgs_status_string", "hgs_frame_bytes", "hgs_forwa
            "hgs_frame_export_arrays", "hgs_blend_log", "hgs_frame_stats",
            "hgs_loss_scratch_bytes", "hgs_image_losses", "hgs_dwt_level1", "hgs_dwt_inverse",
            "hgs_combine_gradients", "hgs_adam_step", "hgs_combine_adam_step",
-           "hgs_densify_stats", "hgs_densify_scratch_bytes", "hgs_densify_plan", "hgs_densify_apply")
+           "hgs_densify_stats", "hgs_densify_scratch_bytes", "hgs_densify_plan", "hgs_densify_apply",
+           "hgs_tile_bins_scratch_bytes", "hgs_frame_tile_bins", "hgs_eval_contributions",
+           "hgs_effective_rank_f64", "hgs_reparameterize_f64", "hgs_modulation_f64")
 
 _vp = ctypes.c_void_p
 _i64 = ctypes.c_int64
@@ -115,7 +119,8 @@ class FrameExport(ctypes.Structure):
     _fields_ = [("idx", _vp), ("typ", _vp), ("depth", _vp), ("center2d", _vp), ("cov2d", _vp),
                 ("conic", _vp), ("mrow", _vp), ("alpha_eff", _vp), ("color", _vp),
                 ("radius", _vp), ("normal", _vp), ("bbox", _vp), ("tile_offsets", _vp),
-                ("tile_ids", _vp), ("pixel_count", _vp)]
+                ("tile_ids", _vp), ("pixel_count", _vp),
+                ("t_cam", _vp), ("alpha", _vp), ("view_dir", _vp), ("cam_dist", _vp)]
 
 
 _lib = None
@@ -162,6 +167,15 @@ def lib():
     L.hgs_blend_log.argtypes = [P(Scene), P(Camera), P(Settings), _vp, P(FrameInfo), _vp, _vp,
                                 _vp, _vp, _vp, _vp]
     L.hgs_frame_stats.argtypes = [_vp, P(FrameInfo), _vp, _vp]
+    L.hgs_tile_bins_scratch_bytes.restype = ctypes.c_size_t
+    L.hgs_tile_bins_scratch_bytes.argtypes = [_i64, _i32, _i32, _i32, _i64]
+    L.hgs_frame_tile_bins.argtypes = [_vp, P(FrameInfo), _i32, _vp, _vp, _i64, _vp, ctypes.c_size_t,
+                                      P(_i64), _vp]
+    L.hgs_eval_contributions.argtypes = [_i64] + [_vp] * 11
+    L.hgs_effective_rank_f64.argtypes = [_i64, _vp, _vp, _vp, _vp]
+    L.hgs_reparameterize_f64.argtypes = [_i64] + [_vp] * 7
+    L.hgs_modulation_f64.argtypes = [_i64, _vp, _vp, ctypes.c_double, ctypes.c_double,
+                                     ctypes.c_double, _vp, _vp, _vp, _vp, _vp]
     L.hgs_loss_scratch_bytes.restype = ctypes.c_size_t
     L.hgs_loss_scratch_bytes.argtypes = [_i32, _i32, _i32]
     L.hgs_image_losses.argtypes = [_i32, _i32, _i32, _vp, _vp, P(LossWeights), _vp, _vp, _vp,
@@ -243,7 +257,9 @@ def settings_struct(st, flags=0, events=None):
     bg = [float(b) for b in st.background]
     if len(bg) != 3:
         raise ConfigError("background must have 3 channels")
-    s = Settings((ctypes.c_float * 3)(*bg), int(st.tile_size), float(st.theta_z),
+    # the compositor always bins at 16 x 16; RenderSettings.tile_size only
+    # selects the tile lists SplatFrame exports (hgs_frame_tile_bins)
+    s = Settings((ctypes.c_float * 3)(*bg), COMPOSITOR_TILE, float(st.theta_z),
                  float(st.t_z), float(st.lambda_z), int(flags), 0, None)
     if events:
         arr = (_vp * len(events))(*[event_handle(e) for e in events])

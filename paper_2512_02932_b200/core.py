@@ -23,6 +23,26 @@ def n_bases(degree):
     return (degree + 1) ** 2
 
 
+@dataclass
+class Gaussian:
+    """One primitive (core/types.py:13-29); type_spec 0 = flat (2D), 1 =
+    volumetric (3D)."""
+    center: np.ndarray          # (3,)
+    log_scale: np.ndarray       # (3,)
+    rotation: np.ndarray        # (4,) w-first
+    opacity_logit: float
+    sh_coeffs: np.ndarray       # (3, B)
+    type_spec: int
+
+    @property
+    def scale(self):
+        return np.exp(self.log_scale)
+
+    @property
+    def opacity(self):
+        return float(1.0 / (1.0 + np.exp(-self.opacity_logit)))
+
+
 class GaussianSet:
     """Host structure-of-arrays scene, float64 like the reference
     (core/types.py:32-142).  ``sh_coeffs`` is (N, 3, B) channel-major;
@@ -85,6 +105,12 @@ class GaussianSet:
         for name in ("center", "log_scale", "rotation", "opacity_logit", "sh_coeffs"):
             if not np.all(np.isfinite(getattr(self, name))):
                 raise InvalidParameterError("non-finite values in %s" % name)
+
+    def get(self, i):
+        """core/types.py:98-101"""
+        return Gaussian(self.center[i].copy(), self.log_scale[i].copy(), self.rotation[i].copy(),
+                        float(self.opacity_logit[i]), self.sh_coeffs[i].copy(),
+                        int(self.type_spec[i]))
 
     def copy(self):
         out = GaussianSet(*(getattr(self, f).copy() for f in self.FIELDS), extent=self.extent)

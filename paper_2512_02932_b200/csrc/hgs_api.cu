@@ -223,7 +223,9 @@ int hgs_forward(const hgs_scene *scene, const hgs_camera *camera, const hgs_sett
                 size_t frame_bytes, const hgs_images *out, hgs_frame_info *info, void *stream) {
   int rc = check_common(scene, camera, settings);
   if (rc) return rc;
-  if (!out || !out->color || !out->depth || !out->transmittance || !info || !frame) return HGS_ERR_CONFIG;
+  if (!info || !frame) return HGS_ERR_CONFIG;
+  if (!(settings->flags & HGS_FLAG_FRAME_ONLY) && (!out || !out->color || !out->depth || !out->transmittance))
+    return HGS_ERR_CONFIG;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int W = camera->width, H = camera->height;
   const int64_t n = scene->n;
@@ -315,7 +317,8 @@ int hgs_forward(const hgs_scene *scene, const hgs_camera *camera, const hgs_sett
   if (K > 0) {
     const int nd = n_tiles > kRadix ? 2 : 1;
     k_duplicate<<<grid_for(m, 256), 256, 0, s>>>(at<SplatRec>(frame, L.recs), at<unsigned long long>(frame, L.pair_off),
-                                                 m, cam.tiles_x, at<uint32_t>(frame, L.pk_a), at<uint32_t>(frame, L.pv_a),
+                                                 m, cam.tiles_x, kTileShift, at<uint32_t>(frame, L.pk_a),
+                                                 at<uint32_t>(frame, L.pv_a),
                                                  nd, at<uint32_t>(frame, L.hist_p));
     HGS_LAUNCHED();
     k_radix_offsets<<<nd, kRadix, 0, s>>>(at<uint32_t>(frame, L.hist_p), at<uint32_t>(frame, L.off_p));
@@ -335,6 +338,7 @@ int hgs_forward(const hgs_scene *scene, const hgs_camera *camera, const hgs_sett
       tile_keys, K, n_tiles, at<uint32_t>(frame, L.tile_off));
   HGS_LAUNCHED();
   HGS_CUDA(record_event(settings, 3, s));
+  if (settings->flags & HGS_FLAG_FRAME_ONLY) return HGS_OK;  // build_frame: no compositing
   // 5. composite
   CompositeArgs a;
   a.recs = at<SplatRec>(frame, L.recs);
@@ -471,6 +475,7 @@ int hgs_backward(const hgs_scene *scene, const hgs_camera *camera, const hgs_set
   if (rc) return rc;
   rc = check_frame(scene, camera, info);
   if (rc) return rc;
+  if (info->flags & HGS_FLAG_FRAME_ONLY) return HGS_ERR_INTEGRITY;  // nothing was composited
   if (kg < 1 || !pixel_grads || (scene->n > 0 && (!grads || !touched))) return HGS_ERR_CONFIG;
   if (scratch_bytes < hgs_backward_scratch_bytes(scene->n, kg)) return HGS_ERR_CONFIG;
   const bool det = settings->flags & HGS_FLAG_DETERMINISTIC;
@@ -668,6 +673,12 @@ __global__ void k_export_frame(SceneView sc, CamD cam, ModD mod, const SplatRec 
     if (o.mrow)
       for (int k = 0; k < 12; ++k) o.mrow[12 * r + k] = p.mrow[k];
     if (o.alpha_eff) o.alpha_eff[r] = p.alpha_eff;
+    if (o.alpha) o.alpha[r] = p.alpha;
+    if (o.cam_dist) o.cam_dist[r] = p.cam_dist;
+    for (int k = 0; k < 3; ++k) {
+      if (o.t_cam) o.t_cam[3 * r + k] = p.t[k];
+      if (o.view_dir) o.view_dir[3 * r + k] = p.view_dir[k];
+    }
     if (o.radius) o.radius[r] = p.radius;
     if (o.bbox)
       for (int k = 0; k < 4; ++k) o.bbox[4 * r + k] = p.bbox[k];
@@ -704,8 +715,22 @@ __global__ void k_blend_log(CompositeArgs a, const int64_t *__restrict__ offsets
       if (!eval_pair<true>(r, a.recs + rk, ix, iy, a.flags, a.st, p)) continue;
       pos[o] = (int32_t)rk;
       alpha[o] = p.at;
-      u[o] = p.u;
-      v[o] = p.v;
+      if (rec_is3d(r)) {
+        u[o] = p.u;
+        v[o] = p.v;
+      } else {
+        // the ray/plane coordinates in float64 (_blend_py.py:38-40): near a
+        // degenerate solve the float32 ones lose every digit (the pair is
+        // then on the low-pass branch, so the image does not depend on them)
+        const Rec64 q = a.st->recs64[rk];
+        const double *m = q.g;
+        const double px = ix + 0.5, py = iy + 0.5;
+        const double hu0 = px * m[6] - m[0], hu1 = px * m[7] - m[1], hu3 = px * m[8] - m[2];
+        const double hv0 = py * m[6] - m[3], hv1 = py * m[7] - m[4], hv3 = py * m[8] - m[5];
+        const double den = hu0 * hv1 - hu1 * hv0;
+        u[o] = (float)((hu1 * hv3 - hu3 * hv1) / den);
+        v[o] = (float)((hu3 * hv0 - hu0 * hv3) / den);
+      }
       ++o;
     }
   }
@@ -769,6 +794,124 @@ int hgs_blend_log(const hgs_scene *scene, const hgs_camera *camera, const hgs_se
   const int64_t HW = (int64_t)info->width * info->height;
   k_blend_log<<<grid_for(HW, 128), 128, 0, s>>>(a, offsets, position, alpha, u, v);
   HGS_LAUNCHED();
+  return HGS_OK;
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------- re-binning
+
+namespace {
+
+struct RebinLayout {
+  size_t state, counts, pair_off, lb_scan, hist, offs, lb_sort, ka, kb, va, vb, tile_off, total;
+};
+
+int tile_shift_of(int t) {
+  switch (t) {
+    case 8: return 3;
+    case 16: return 4;
+    case 32: return 5;
+    case 64: return 6;
+    default: return -1;
+  }
+}
+
+RebinLayout rebin_layout(int64_t m, int W, int H, int tile, int64_t cap) {
+  RebinLayout L;
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    size_t o = off;
+    off += (bytes + 255) & ~(size_t)255;
+    return o;
+  };
+  const int64_t mm = std::max<int64_t>(m, 1), cc = std::max<int64_t>(cap, 1);
+  const int64_t tiles = ceil_div(W, tile) * ceil_div(H, tile);
+  L.state = take(sizeof(FrameState));
+  L.hist = take(3 * kRadix * 4);
+  L.offs = take(3 * kRadix * 4);
+  L.counts = take(mm * 4);
+  L.pair_off = take(mm * 8);
+  L.lb_scan = take((size_t)ceil_div(mm, kScanTile) * 8);
+  L.lb_sort = take((size_t)3 * ceil_div(cc, kSortTile) * kRadix * 4);
+  L.ka = take(cc * 4);
+  L.kb = take(cc * 4);
+  L.va = take(cc * 4);
+  L.vb = take(cc * 4);
+  L.tile_off = take((tiles + 1) * 4);
+  L.total = off;
+  return L;
+}
+
+}  // namespace
+
+extern "C" {
+
+size_t hgs_tile_bins_scratch_bytes(int64_t m, int32_t width, int32_t height, int32_t tile_size,
+                                   int64_t pair_capacity) {
+  if (tile_shift_of(tile_size) < 0 || width <= 0 || height <= 0 || m < 0 || pair_capacity < 0) return 0;
+  return rebin_layout(m, width, height, tile_size, pair_capacity).total;
+}
+
+int hgs_frame_tile_bins(const void *frame, const hgs_frame_info *info, int32_t tile_size, int64_t *tile_offsets,
+                        int32_t *tile_ids, int64_t ids_capacity, void *scratch, size_t scratch_bytes, int64_t *k_out,
+                        void *stream) {
+  const int sh = tile_shift_of(tile_size);
+  if (!frame || !info || sh < 0 || !tile_offsets || !k_out || ids_capacity < 0 || !scratch) return HGS_ERR_CONFIG;
+  const int W = info->width, H = info->height;
+  const int64_t m = info->m;
+  const RebinLayout R = rebin_layout(m, W, H, tile_size, ids_capacity);
+  if (scratch_bytes < R.total) return HGS_ERR_CONFIG;
+  const Layout L = make_layout(info->n, W, H, info->pair_capacity);
+  const SplatRec *recs = at<SplatRec>(frame, L.recs);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int tiles_x = (int)ceil_div(W, tile_size);
+  const int64_t n_tiles = (int64_t)tiles_x * ceil_div(H, tile_size);
+  FrameState *st = at<FrameState>(scratch, R.state);
+  HGS_CUDA(cudaMemsetAsync(scratch, 0, R.counts, s));  // state + histograms
+  int64_t K = 0;
+  if (m > 0) {
+    HGS_CUDA(cudaMemsetAsync(at<char>(scratch, R.lb_scan), 0, (size_t)ceil_div(m, kScanTile) * 8, s));
+    k_rebin_counts<<<grid_for(m, 256), 256, 0, s>>>(recs, m, sh, at<uint32_t>(scratch, R.counts));
+    HGS_LAUNCHED();
+    k_scan_counts<<<(unsigned)ceil_div(m, kScanTile), kScanThreads, 0, s>>>(
+        at<uint32_t>(scratch, R.counts), m, at<unsigned long long>(scratch, R.pair_off),
+        at<unsigned long long>(scratch, R.lb_scan), st);
+    HGS_LAUNCHED();
+    unsigned long long kt;
+    HGS_CUDA(cudaMemcpyAsync(&kt, &st->k_total, 8, cudaMemcpyDeviceToHost, s));
+    HGS_CUDA(cudaStreamSynchronize(s));
+    K = (int64_t)kt;
+  }
+  *k_out = K;
+  if (K > ids_capacity || K >= (1ll << 32)) return HGS_ERR_PAIR_CAPACITY;
+  const uint32_t *keys = at<uint32_t>(scratch, R.ka), *vals = at<uint32_t>(scratch, R.va);
+  if (K > 0) {
+    const int nd = n_tiles > kRadix ? 2 : 1;
+    if (n_tiles > (1 << 16)) return HGS_ERR_CONFIG;  // 2 digit passes cover 65536 tiles
+    k_duplicate<<<grid_for(m, 256), 256, 0, s>>>(recs, at<unsigned long long>(scratch, R.pair_off), m, tiles_x, sh,
+                                                 at<uint32_t>(scratch, R.ka), at<uint32_t>(scratch, R.va),
+                                                 nd, at<uint32_t>(scratch, R.hist));
+    HGS_LAUNCHED();
+    k_radix_offsets<<<nd, kRadix, 0, s>>>(at<uint32_t>(scratch, R.hist), at<uint32_t>(scratch, R.offs));
+    HGS_LAUNCHED();
+    int passes[2] = {0, 1};
+    bool in_b;
+    int rc = radix_sort<uint32_t>(at<uint32_t>(scratch, R.ka), at<uint32_t>(scratch, R.kb),
+                                  at<uint32_t>(scratch, R.va), at<uint32_t>(scratch, R.vb), K, passes, nd,
+                                  at<uint32_t>(scratch, R.offs), at<uint32_t>(scratch, R.lb_sort),
+                                  st->tile_counters + 12, s, &in_b);
+    if (rc) return rc;
+    keys = at<uint32_t>(scratch, in_b ? R.kb : R.ka);
+    vals = at<uint32_t>(scratch, in_b ? R.vb : R.va);
+  }
+  k_tile_ranges<<<grid_for(ceil_div(std::max<int64_t>(K, n_tiles + 1), 4), 256), 256, 0, s>>>(
+      keys, K, n_tiles, at<uint32_t>(scratch, R.tile_off));
+  HGS_LAUNCHED();
+  k_export_u32_to_i64<<<grid_for(n_tiles + 1, 256), 256, 0, s>>>(at<uint32_t>(scratch, R.tile_off), tile_offsets,
+                                                                 n_tiles + 1);
+  HGS_LAUNCHED();
+  if (K > 0 && tile_ids) HGS_CUDA(cudaMemcpyAsync(tile_ids, vals, (size_t)K * 4, cudaMemcpyDeviceToDevice, s));
   return HGS_OK;
 }
 

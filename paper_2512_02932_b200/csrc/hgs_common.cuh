@@ -19,6 +19,7 @@
 namespace hgs {
 
 constexpr int kTile = 16;
+constexpr int kTileShift = 4;  // log2(kTile)
 constexpr int kBlock = kTile * kTile;  // one thread per pixel of a tile
 #ifndef HGS_FIXUP_BLOCKS
 #define HGS_FIXUP_BLOCKS (148 * 4)
@@ -211,6 +212,7 @@ struct ProjD {
   double mrow[12];  // 2D: rows (0, 1, 3) of M, 3 x 4
   double color[3];
   double normal[3];
+  double view_dir[3], cam_dist;  // project.py:247-251 (not with GEOM_ONLY)
   double radius;
   double bb[4];  // continuous bbox before floor/ceil
   int bbox[4];   // inclusive pixel box, bbox[2] = -1 when off screen
@@ -286,6 +288,8 @@ __device__ __forceinline__ void project_d(const SceneView &sc, int64_t i, const 
   double dist = sqrt((dl[0] * dl[0] + dl[1] * dl[1]) + dl[2] * dl[2]);
   double den = dist > 1e-12 ? dist : 1e-12;
   double vx = dl[0] / den, vy = dl[1] / den, vz = dl[2] / den;
+  o.view_dir[0] = vx; o.view_dir[1] = vy; o.view_dir[2] = vz;
+  o.cam_dist = dist;
   const int B = sc.sh_bases;
   const int deg = B == 1 ? 0 : (B == 4 ? 1 : (B == 9 ? 2 : 3));
   const float *shc = sh_row ? sh_row : sc.sh + (int64_t)3 * B * i;  // sh_row: staged copy (shared memory)

@@ -333,7 +333,7 @@ constexpr int kDupOwn = 32;
 
 __global__ void __launch_bounds__(256) k_duplicate(const SplatRec *__restrict__ recs,
                                                    const unsigned long long *__restrict__ pair_off, int64_t m,
-                                                   int tiles_x, uint32_t *__restrict__ pkeys,
+                                                   int tiles_x, int tile_shift, uint32_t *__restrict__ pkeys,
                                                    uint32_t *__restrict__ pvals, int n_digits,
                                                    uint32_t *__restrict__ hist) {
   __shared__ uint32_t sh[2 * kRadix];
@@ -357,9 +357,9 @@ __global__ void __launch_bounds__(256) k_duplicate(const SplatRec *__restrict__ 
       const int4 q = recs[r].r5;
       const int x0 = q.x & 0xffff, y0 = (int)((uint32_t)q.x >> 16), x1 = q.y & 0xffff, y1 = (int)((uint32_t)q.y >> 16);
       if (x1 >= x0) {
-        tx0 = x0 / kTile; ty0 = y0 / kTile;
-        bw = x1 / kTile - tx0 + 1;
-        cnt = (uint32_t)(bw * (y1 / kTile - ty0 + 1));
+        tx0 = x0 >> tile_shift; ty0 = y0 >> tile_shift;
+        bw = (x1 >> tile_shift) - tx0 + 1;
+        cnt = (uint32_t)(bw * ((y1 >> tile_shift) - ty0 + 1));
         o = pair_off[r];
       }
     }
@@ -386,6 +386,19 @@ __global__ void __launch_bounds__(256) k_duplicate(const SplatRec *__restrict__ 
   __syncthreads();
   for (int i = threadIdx.x; i < n_digits * kRadix; i += blockDim.x)
     if (sh[i]) atomicAdd(&hist[i], sh[i]);
+}
+
+// Tiles per splat at another tile size (2^tile_shift px; SplatFrame export at
+// settings.tile_size != 16, project.py:329-343).
+__global__ void __launch_bounds__(256) k_rebin_counts(const SplatRec *__restrict__ recs, int64_t m, int tile_shift,
+                                                      uint32_t *__restrict__ counts) {
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < m; r += (int64_t)gridDim.x * blockDim.x) {
+    const int4 q = recs[r].r5;
+    const int x0 = q.x & 0xffff, y0 = (int)((uint32_t)q.x >> 16), x1 = q.y & 0xffff, y1 = (int)((uint32_t)q.y >> 16);
+    counts[r] = x1 >= x0 ? (uint32_t)(((x1 >> tile_shift) - (x0 >> tile_shift) + 1) *
+                                      ((y1 >> tile_shift) - (y0 >> tile_shift) + 1))
+                         : 0u;
+  }
 }
 
 // tile_offsets (n_tiles + 1) from the tile-sorted keys (project.py:344-345).

@@ -406,14 +406,19 @@ __device__ __forceinline__ int refine_2d(const SplatRec &r, const Geom &g, bool 
   const float B0 = fabsf(g.pyl * m2.z) + fabsf(m1.w), B1 = fabsf(g.pyl * m2.w) + fabsf(m2.x);
   const float B3 = fabsf(g.pyl * m23) + fabsf(m2.y);
   const float ad = fabsf(g.den);
-  const float iad = rcp_approx(ad) * (1.f + 4.f * kEps);
   const float dden = 6.f * kEps * (A0 * B1 + A1 * B0);
+  // |den| is only trusted when its error bound is a small fraction of it
+  // (near-degenerate pairs: the reciprocal below must not blow up); then
+  // |true den| >= ad - dden makes the (u, v) bounds rigorous, not first-order
+  if (!(ad > (float)kDegenerateDen + dden) || !(ad > 32.f * dden)) return kAmbiguous;
+  const float iad = rcp_approx(ad - dden) * (1.f + 4.f * kEps);
   const float du = (6.f * kEps * (A1 * B3 + A3 * B1) + fabsf(g.u) * dden) * iad + 4.f * kEps * fabsf(g.u);
   const float dv = (6.f * kEps * (A3 * B0 + A0 * B3) + fabsf(g.v) * dden) * iad + 4.f * kEps * fabsf(g.v);
-  const float e_ray = 2.f * (fabsf(g.u) * du + fabsf(g.v) * dv) + 4.f * kEps * g.dray;
+  // (|u| + du)^2 - u^2 = 2|u| du + du^2 (likewise v)
+  const float e_ray = fmaf(du, du, dv * dv) + 2.f * (fabsf(g.u) * du + fabsf(g.v) * dv) + 4.f * kEps * g.dray;
   const float e_scr = 8.f * kEps * g.dscr + 1e-6f * (fabsf(g.dx) + fabsf(g.dy));
   const float margin = fmaf(g.ray ? e_ray : e_scr, kHalfLog2e, 1e-5f);
-  if (!(ad > (float)kDegenerateDen + dden) || !(margin < kCoarse2D)) return kAmbiguous;
+  if (!(margin < kCoarse2D)) return kAmbiguous;
   if (!known) {  // known: the forward's exact decision says the pair contributes
     if (g.arg < kArgMinAlpha - margin) return kSkip;
     if (g.arg <= kArgMinAlpha + margin) return kAmbiguous;
@@ -506,7 +511,7 @@ __device__ __forceinline__ int eval_fast(const SplatRec &r, int ix, int iy, uint
     const bool nd = near_degenerate(g);
     if (nd && !exact && fabsf(g.den) < (float)kDegenerateDen) return kSkip;
     geom_2d_solve(r, g);
-    if (!nd && !KNOWN && g.arg < kArgMinAlpha - (exact ? kCoarse2D : 0.f)) return kSkip;
+    if ((!nd || !exact) && !KNOWN && g.arg < kArgMinAlpha - (exact ? kCoarse2D : 0.f)) return kSkip;
     if (exact && (nd || (!KNOWN && g.arg <= kArgMinAlpha + kCoarse2D) ||
                   (BWD && (fabsf(g.arg - kArgClamp) <= kCoarse2D ||
                            fabsf(g.dray - g.dscr) <= 0.02f * (g.dray + g.dscr))))) {
@@ -652,7 +657,9 @@ cudaError_t launch_preprocess(const SceneView &sc, const CamD &cam, const ModD &
                               cudaStream_t s);
 __global__ void k_scan_counts(const uint32_t *counts, int64_t m, unsigned long long *pair_off,
                               unsigned long long *scan_lb, FrameState *st);
+__global__ void k_rebin_counts(const SplatRec *recs, int64_t m, int tile_shift, uint32_t *counts);
 __global__ void k_duplicate(const SplatRec *recs, const unsigned long long *pair_off, int64_t m, int tiles_x,
+                            int tile_shift,
                             uint32_t *pkeys, uint32_t *pvals, int n_digits, uint32_t *hist);
 __global__ void k_tile_ranges(const uint32_t *skeys, int64_t k, int64_t n_tiles, uint32_t *tile_off);
 // Host launchers of the template kernels (each instantiated and launched in

@@ -17,7 +17,9 @@ from . import _lib
 from .core import DeviceGaussians, GaussianSet
 from .errors import IntegrityError
 
-__all__ = ["backward", "ParamGrads", "GradientBundle", "param_labels"]
+# grad/__init__.py:7-8 of the reference
+__all__ = ["backward", "GradientBundle", "ParamGrads", "param_labels", "FiniteDiffReport",
+           "finite_diff_check"]
 
 
 @dataclass
@@ -79,6 +81,11 @@ class GradientBundle:
     g_color: ParamGrads
     g_low: ParamGrads
     g_high: ParamGrads
+
+    @classmethod
+    def zeros_like(cls, scene):
+        return cls(ParamGrads.zeros_like(scene), ParamGrads.zeros_like(scene),
+                   ParamGrads.zeros_like(scene))
 
 
 def param_labels(scene):
@@ -233,3 +240,95 @@ def backward(scene, camera, output, pixel_grad, depth_grad=None, normal_grad=Non
         out = [_views(grads[k], n, B) for k in range(kg)]
         touched = touched.bool()
     return (out[0] if single else out), touched
+
+
+# ---------------------------------------------------------------- finite differences
+
+def _slot_ref(scene, gauss, slot):
+    """(array, index) of flat parameter ``slot`` of Gaussian ``gauss`` in the
+    canonical ParamGrads.flat() order (grad/findiff.py:27-56)."""
+    b = scene.sh_coeffs.shape[2]
+    if slot < 3:
+        return scene.center, (gauss, slot)
+    if slot < 6:
+        return scene.log_scale, (gauss, slot - 3)
+    if slot < 10:
+        return scene.rotation, (gauss, slot - 6)
+    if slot == 10:
+        return scene.opacity_logit, (gauss,)
+    k = slot - 11
+    return scene.sh_coeffs, (gauss, k // b, k % b)
+
+
+@dataclass
+class FiniteDiffReport:
+    """grad/findiff.py:59-75"""
+    rel_err: np.ndarray        # flat over gaussians x params; nan = excluded
+    excluded: np.ndarray       # parameters whose perturbation flips the depth order
+    labels: list
+    analytic: np.ndarray
+    numeric: np.ndarray
+
+    @property
+    def max_rel_err(self):
+        live = self.rel_err[~self.excluded]
+        return float(np.nanmax(live)) if live.size else 0.0
+
+    def pass_fraction(self, tol):
+        live = self.rel_err[~self.excluded]
+        if live.size == 0:
+            return 1.0
+        return float(np.mean(live <= tol))
+
+
+def finite_diff_check(scene, camera, loss, loss_grad, eps, param_subset=None,
+                      settings=None) -> FiniteDiffReport:
+    """Central differences of loss(render(...).color) against the analytic GPU
+    backward (grad/findiff.py:78-133): two GPU renders per scalar parameter;
+    parameters whose perturbation changes the splat depth order are reported
+    as excluded.  eps must lie in [1e-6, 1e-2].  The images are composited
+    in float32, so the central differences carry ~1e-3 relative noise at
+    eps = 1e-4 (the reference's float64 renders ~1e-9)."""
+    from .errors import ConfigError
+    from .raster import render
+    from .settings import RenderSettings
+    if not 1e-6 <= eps <= 1e-2:
+        raise ConfigError("eps must be in [1e-6, 1e-2], got %r" % (eps,))
+    if settings is None:
+        settings = RenderSettings()
+    if not isinstance(scene, GaussianSet):
+        raise ConfigError("finite_diff_check needs a host GaussianSet")
+    out = render(scene, camera, settings)
+    base = loss(out.color)
+    if not np.isfinite(base):
+        raise ConfigError("loss is non-finite at the base point")
+    pixel_grad = np.asarray(loss_grad(out.color), dtype=np.float64)
+    analytic_grads, _ = backward(scene, camera, out, pixel_grad)
+    analytic_flat = analytic_grads.flat()
+    p = 11 + 3 * scene.sh_coeffs.shape[2]
+    slots = list(range(p) if param_subset is None else param_subset)
+    n = scene.count
+    rel = np.full((n, p), np.nan)
+    excluded = np.zeros((n, p), dtype=bool)
+    numeric = np.full((n, p), np.nan)
+    for gi in range(n):
+        for slot in slots:
+            work = scene.copy()
+            arr, ix = _slot_ref(work, gi, slot)
+            theta = float(arr[ix])
+            arr[ix] = theta + eps
+            out_p = render(work, camera, settings)
+            arr[ix] = theta - eps
+            out_m = render(work, camera, settings)
+            if not np.array_equal(out_p.frame.idx, out_m.frame.idx):
+                excluded[gi, slot] = True
+                continue
+            fd = (loss(out_p.color) - loss(out_m.color)) / (2.0 * eps)
+            numeric[gi, slot] = fd
+            rel[gi, slot] = abs(analytic_flat[gi, slot] - fd) / max(abs(fd), 1e-8)
+    mask = np.zeros((n, p), dtype=bool)
+    mask[:, slots] = True
+    labels = param_labels(scene)
+    return FiniteDiffReport(rel_err=rel[mask], excluded=excluded[mask],
+                            labels=[l for l, m in zip(labels, mask.ravel()) if m],
+                            analytic=analytic_flat[mask], numeric=numeric[mask])

@@ -113,7 +113,9 @@ class TrainStepResult:
     losses: object        # float64 CUDA tensor [L1, SSIM, L_low, L_high, L_color]
     n_conflicts: object   # int64 CUDA tensor (1,)
     pair_count: int
-    color: object         # the rendered (H, W, 3) image of this step
+    color: object         # the rendered (H, W, 3) image of this step: a view of the
+                          # per-device workspace, overwritten by the next train_step
+                          # (clone() it to keep it across steps)
 
     def total_loss(self, weights):
         """L = L_color + lambda_low L_low + lambda_high L_high (Eq. 8); syncs."""

@@ -9,6 +9,7 @@ device-resident ``DeviceGaussians`` (float32 CUDA tensors; outputs stay on the
 GPU as torch tensors).  There is no CPU backend.
 """
 
+import ctypes
 from dataclasses import dataclass
 from typing import Optional
 
@@ -16,15 +17,21 @@ import numpy as np
 
 from . import _lib
 from .core import CameraView, DeviceGaussians, GaussianSet
-from .errors import ConfigError, IntegrityError
+from .errors import ConfigError, DegenerateIntersection, IntegrityError
 from .settings import (ALPHA_CLAMP, EARLY_STOP_T, LOWPASS_SIGMA, MIN_ALPHA, SCREEN_DILATION,
                        TILE_SIZE, RenderSettings)
 
 HAVE_EXT = _lib.available()
 
-__all__ = ["ALPHA_CLAMP", "EARLY_STOP_T", "LOWPASS_SIGMA", "MIN_ALPHA", "ProjectedSplat",
-           "RenderSettings", "SCREEN_DILATION", "SplatFrame", "HAVE_EXT", "BlendLog",
-           "RenderOutput", "active_backend", "render", "render_naive", "scene_fingerprint"]
+# raster/__init__.py:12-19 of the reference, in the same order
+__all__ = ["ALPHA_CLAMP", "DegenerateIntersection", "EARLY_STOP_T", "LOWPASS_SIGMA",
+           "MIN_ALPHA", "ProjectedSplat", "RenderSettings", "SCREEN_DILATION",
+           "SplatFrame", "build_frame", "evaluate_contribution",
+           "project_gaussian_3d", "ray_splat_intersect",
+           "HAVE_EXT", "BlendLog", "RenderOutput", "active_backend", "render",
+           "render_naive", "scene_fingerprint"]
+
+TILE_SIZES = (8, 16, 32, 64)  # RenderSettings.tile_size values SplatFrame can export
 
 
 def active_backend(settings: RenderSettings):
@@ -83,7 +90,11 @@ class BlendLog:
 
 
 _FRAME_FIELDS = ("idx", "typ", "depth", "center2d", "cov2d", "conic", "mrow", "alpha_eff",
-                 "color", "radius", "normal", "bbox", "tile_offsets", "tile_ids", "pixel_count")
+                 "color", "radius", "normal", "bbox", "tile_offsets", "tile_ids", "pixel_count",
+                 "t_cam", "alpha", "view_dir", "cam_dist")
+# per-splat (length m) fields; "valid" is all True after build_frame's cull
+_PER_SPLAT = ("idx", "typ", "depth", "center2d", "cov2d", "conic", "mrow", "alpha_eff", "color",
+              "radius", "normal", "bbox", "t_cam", "alpha", "view_dir", "cam_dist")
 
 
 class SplatFrame:
@@ -136,23 +147,57 @@ class SplatFrame:
             tile_offsets=torch.empty(int(self.info.n_tiles) + 1, dtype=torch.int64, device=dev),
             tile_ids=torch.empty(max(k, 1), dtype=torch.int32, device=dev),
             pixel_count=torch.empty((H, W), dtype=torch.int32, device=dev),
+            t_cam=torch.empty((max(m, 1), 3), dtype=torch.float64, device=dev),
+            alpha=torch.empty(max(m, 1), dtype=torch.float64, device=dev),
+            view_dir=torch.empty((max(m, 1), 3), dtype=torch.float64, device=dev),
+            cam_dist=torch.empty(max(m, 1), dtype=torch.float64, device=dev),
         )
+        if self.flags & _lib.HGS_FLAG_FRAME_ONLY:
+            d["pixel_count"] = None  # nothing was composited
         ex = _lib.FrameExport(*(_lib.ptr(d[f]) for f in _FRAME_FIELDS))
         ds = self.scene
         sc = _lib.scene_struct(ds)
         _lib.check(_lib.lib().hgs_frame_export_arrays(
             sc, _lib.camera_struct(self.camera), _lib.settings_struct(self.settings, self.flags),
             _lib.ptr(self.buf), self.info, ex, _lib.current_stream_handle(dev)), "frame export")
-        out = {f: t.cpu().numpy() for f, t in d.items()}
-        for f in _FRAME_FIELDS:
-            if f in ("tile_offsets", "pixel_count"):
-                continue
-            out[f] = out[f][:k] if f == "tile_ids" else out[f][:m]
+        if self.tile_size != _lib.COMPOSITOR_TILE:
+            d["tile_offsets"], d["tile_ids"] = self._rebin(self.tile_size)
+            k = int(d["tile_ids"].shape[0])
+        out = {f: (t.cpu().numpy() if t is not None else None) for f, t in d.items()}
+        for f in _PER_SPLAT:
+            out[f] = out[f][:m]
+        out["tile_ids"] = out["tile_ids"][:k]
+        out["valid"] = np.ones(m, dtype=bool)
         self._host = out
         return out
 
+    def _rebin(self, tile):
+        """Tile lists at another tile size (project.py:329-357) on the GPU."""
+        import torch
+        L = _lib.lib()
+        dev = self.buf.device
+        stream = _lib.current_stream_handle(dev)
+        W, H = self.width, self.height
+        n_tiles = ((W + tile - 1) // tile) * ((H + tile - 1) // tile)
+        offsets = torch.empty(n_tiles + 1, dtype=torch.int64, device=dev)
+        cap = max(self.pair_count * (16 // tile) ** 2 + self.count, 1) if tile < 16 else max(self.pair_count, 1)
+        for _ in range(2):
+            nb = L.hgs_tile_bins_scratch_bytes(self.count, W, H, tile, cap)
+            scratch = torch.empty(nb, dtype=torch.uint8, device=dev)
+            ids = torch.empty(cap, dtype=torch.int32, device=dev)
+            k = _lib._i64(0)
+            rc = L.hgs_frame_tile_bins(_lib.ptr(self.buf), self.info, tile, _lib.ptr(offsets),
+                                       _lib.ptr(ids), cap, _lib.ptr(scratch), nb, ctypes.byref(k),
+                                       stream)
+            if rc == _lib.HGS_ERR_PAIR_CAPACITY:
+                cap = int(k.value)
+                continue
+            _lib.check(rc, "hgs_frame_tile_bins")
+            return offsets, ids[:int(k.value)]
+        raise ConfigError("could not size the tile-bin buffer")
+
     def __getattr__(self, name):
-        if name in _FRAME_FIELDS:
+        if name in _FRAME_FIELDS or name == "valid":
             return self.export()[name]
         raise AttributeError(name)
 
@@ -243,11 +288,14 @@ def rasterize(ds, camera, settings, flags=0, outputs=None, events=None):
     import torch
     L = _lib.lib()
     _check_camera(camera)
-    if settings.tile_size != TILE_SIZE:
-        raise ConfigError("tile_size must be %d for the CUDA compositor" % TILE_SIZE)
+    if settings.tile_size not in TILE_SIZES:
+        raise ConfigError("tile_size must be one of %s (the compositor bins at %d; SplatFrame "
+                          "re-bins its tile lists at the requested size)" % (TILE_SIZES, TILE_SIZE))
     dev = ds.device
     W, H = int(camera.width), int(camera.height)
     n = ds.count
+    if outputs is None and flags & _lib.HGS_FLAG_FRAME_ONLY:
+        outputs = {}
     if outputs is None:
         outputs = dict(
             color=torch.empty((H, W, 3), dtype=torch.float32, device=dev),
@@ -257,6 +305,8 @@ def rasterize(ds, camera, settings, flags=0, outputs=None, events=None):
             normal=torch.empty((H, W, 3), dtype=torch.float32, device=dev))
     imgs = _lib.Images(*(_lib.ptr(outputs.get(k)) for k in
                          ("color", "depth", "transmittance", "alpha", "normal")))
+    if flags & _lib.HGS_FLAG_FRAME_ONLY:
+        imgs = _lib.Images(None, None, None, None, None)
     sc = _lib.scene_struct(ds)
     cam = _lib.camera_struct(camera)
     st = _lib.settings_struct(settings, flags, events)
@@ -321,3 +371,85 @@ def render_naive(scene, camera, settings: RenderSettings = None) -> RenderOutput
     (raster/render.py:101-118) -- the oracle the tile renderer is checked
     against."""
     return _render(scene, camera, settings, True, False)
+
+
+def build_frame(scene, camera, settings: RenderSettings = None) -> SplatFrame:
+    """Screen-space preparation only -- depth sort, float64 preprocess, bounds
+    and tile bins, on the GPU, no compositing (raster/project.py:360-379).
+    The returned frame exports the reference's SplatFrame arrays; it cannot
+    be back-propagated (nothing was blended)."""
+    if settings is None:
+        settings = RenderSettings()
+    flags = _flags(settings) | _lib.HGS_FLAG_FRAME_ONLY
+    if isinstance(scene, DeviceGaussians):
+        return rasterize(scene, camera, settings, flags)[1]
+    if not isinstance(scene, GaussianSet):
+        scene = GaussianSet(scene.center, scene.log_scale, scene.rotation, scene.opacity_logit,
+                            scene.sh_coeffs, scene.type_spec)
+    return rasterize(DeviceGaussians.from_host(scene), camera, settings, flags)[1]
+
+
+def _eval_pairs(splats, pixels, opacities):
+    """hgs_eval_contributions over a list of ProjectedSplat / pixel / opacity
+    triples -> (alpha, u, v, degenerate) numpy arrays."""
+    import torch
+    n = len(splats)
+    typ = np.array([s.type_spec for s in splats], np.uint8)
+    c2 = np.array([s.screen_center for s in splats], np.float64).reshape(n, 2)
+    conic = np.zeros((n, 3))
+    mrow = np.zeros((n, 12))
+    for i, s in enumerate(splats):
+        if s.type_spec == 1:
+            c = np.asarray(s.conic, np.float64)
+            conic[i] = (c[0, 0], c[0, 1], c[1, 1])
+        else:
+            mrow[i] = np.asarray(s.plane_params, np.float64).reshape(12)
+    px = np.array(pixels, np.float64).reshape(n, 2)
+    op = np.array(opacities, np.float64).reshape(n)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    d = [torch.from_numpy(a).to(dev) for a in (typ, c2, conic, mrow, op, px)]
+    alpha = torch.empty(n, dtype=torch.float64, device=dev)
+    u = torch.empty_like(alpha)
+    v = torch.empty_like(alpha)
+    fl = torch.empty(n, dtype=torch.int32, device=dev)
+    _lib.check(_lib.lib().hgs_eval_contributions(
+        n, *(_lib.ptr(t) for t in d), _lib.ptr(alpha), _lib.ptr(u), _lib.ptr(v), _lib.ptr(fl),
+        _lib.current_stream_handle(dev)), "hgs_eval_contributions")
+    return (alpha.cpu().numpy(), u.cpu().numpy(), v.cpu().numpy(), fl.cpu().numpy() != 0)
+
+
+def ray_splat_intersect(splat: ProjectedSplat, pixel):
+    """Tangent-frame coordinates (u, v) where the ray through ``pixel`` meets
+    the plane of a flat splat (raster/project.py:109-126), evaluated on the
+    GPU in float64; raises DegenerateIntersection when |den| < 1e-9."""
+    if splat.plane_params is None:
+        raise ConfigError("ray_splat_intersect needs a flat primitive")
+    _, u, v, deg = _eval_pairs([splat], [(float(pixel[0]), float(pixel[1]))], [1.0])
+    if deg[0]:
+        raise DegenerateIntersection("pixel ray nearly parallel to splat plane")
+    return float(u[0]), float(v[0])
+
+
+def evaluate_contribution(splat: ProjectedSplat, pixel, opacity):
+    """alpha_t = opacity * exp(-d/2) clamped to <= 0.99, d the conic distance
+    (3D) or min(ray/splat, low-pass) distance (2D); 0 for a degenerate
+    intersection (raster/project.py:129-152).  Evaluated on the GPU in
+    float64, with the formulas of the compositors' float64 re-checks."""
+    if splat.type_spec == 0 and splat.plane_params is None:
+        raise ConfigError("flat splat without plane parameters")
+    a, _, _, _ = _eval_pairs([splat], [(float(pixel[0]), float(pixel[1]))], [float(opacity)])
+    return float(a[0])
+
+
+def project_gaussian_3d(g, camera: CameraView, settings: RenderSettings = None):
+    """Affine-project one volumetric primitive (raster/project.py:155-166);
+    None when culled."""
+    if settings is None:
+        settings = RenderSettings()
+    if g.type_spec != 1:
+        raise ConfigError("project_gaussian_3d needs a volumetric primitive")
+    scene = GaussianSet(np.asarray(g.center)[None], np.asarray(g.log_scale)[None],
+                        np.asarray(g.rotation)[None], np.array([g.opacity_logit]),
+                        np.asarray(g.sh_coeffs)[None], np.array([1], np.uint8))
+    frame = build_frame(scene, camera, settings)
+    return frame.splat(0) if frame.count else None

@@ -9,8 +9,9 @@ from paper_2512_02932_b200.settings import RenderSettings
 
 GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 # raw_f64: float64 inputs that are not float32-representable (its float32
-# rounding changes the depth order and tile lists)
-SCENES = ("tiny_sh3", "stress2d", "rotcam_sh2", "c1", "raw_f64")
+# rounding changes the depth order and tile lists); grazing: edge-on 2D surfels
+# (near-degenerate ray/plane solves)
+SCENES = ("tiny_sh3", "stress2d", "rotcam_sh2", "c1", "raw_f64", "grazing")
 
 
 def load(name):

@@ -130,6 +130,68 @@ def rotated_camera_scene(seed=7):
     return sc, synthetic_camera(64, 48, w2c)
 
 
+def _mat_to_quat(R):
+    """Rotation matrix -> w-first unit quaternion (Shepperd, w >= 0)."""
+    q = np.empty(4)
+    tr = np.trace(R)
+    if tr > 0:
+        t = np.sqrt(tr + 1.0) * 2
+        q[:] = [0.25 * t, (R[2, 1] - R[1, 2]) / t, (R[0, 2] - R[2, 0]) / t, (R[1, 0] - R[0, 1]) / t]
+    else:
+        i = int(np.argmax(np.diag(R)))
+        j, k = (i + 1) % 3, (i + 2) % 3
+        t = np.sqrt(1.0 + R[i, i] - R[j, j] - R[k, k]) * 2
+        q[0] = (R[k, j] - R[j, k]) / t
+        q[1 + i] = 0.25 * t
+        q[1 + j] = (R[j, i] + R[i, j]) / t
+        q[1 + k] = (R[k, i] + R[i, k]) / t
+    return q if q[0] >= 0 else -q
+
+
+def grazing_scene(seed=23, n=160, size=64):
+    """2D surfels seen almost edge-on: each surfel's first tangent axis is the
+    view ray through its centre, tilted by 1e-4 .. 0.3 rad, so the ray/plane
+    2x2 solve is near-degenerate (|den| close to its float32 error bound) over
+    much of its footprint.  Mixed with a few 3D Gaussians behind them."""
+    from paper_2512_02932_b200.core import GaussianSet
+    from paper_2512_02932_b200.synthetic import synthetic_camera
+    rng = np.random.default_rng(seed)
+    cam = synthetic_camera(size, size)
+    z = rng.uniform(0.8, 4.0, n)
+    px = rng.uniform(0.1 * size, 0.9 * size, n)
+    py = rng.uniform(0.1 * size, 0.9 * size, n)
+    center = np.stack([(px - cam.cx) * z / cam.fx, (py - cam.cy) * z / cam.fy, z], 1)
+    rot = np.zeros((n, 4))
+    ty = np.zeros(n, np.uint8)
+    ty[n - n // 5:] = 1
+    for i in range(n):
+        if i % 2 == 0:
+            d = center[i] / np.linalg.norm(center[i])
+        else:
+            # the plane contains the ray through a pixel centre near the
+            # splat: that pixel's ray/plane solve is exactly singular
+            qx = np.floor(px[i]) + rng.integers(-3, 4) + 0.5
+            qy = np.floor(py[i]) + rng.integers(-3, 4) + 0.5
+            d = np.array([(qx - cam.cx) / cam.fx, (qy - cam.cy) / cam.fy, 1.0])
+            d /= np.linalg.norm(d)
+        a = rng.normal(size=3)
+        a -= d * (a @ d)
+        a /= np.linalg.norm(a)
+        ang = 10.0 ** rng.uniform(-4, np.log10(0.3)) if i % 2 == 0 else 0.0
+        t0 = np.cos(ang) * d + np.sin(ang) * np.cross(a, d)   # ~ the view ray
+        t1 = a
+        nrm = np.cross(t0, t1)
+        R = np.stack([t0, t1, nrm], 1)
+        if rng.random() < 0.5:
+            R = R[:, [1, 0, 2]] * np.array([1, 1, -1])           # swap tangents (det +1)
+        rot[i] = _mat_to_quat(R)
+    ls = np.log(np.stack([rng.uniform(0.05, 0.4, n), rng.uniform(0.05, 0.4, n),
+                          rng.uniform(0.01, 0.05, n)], 1))
+    sc = GaussianSet(f32_exact(center), f32_exact(ls), f32_exact(rot),
+                     f32_exact(rng.normal(1.0, 1.0, n)), f32_exact(rng.normal(0, .3, (n, 3, 4))), ty)
+    return sc, cam
+
+
 def raw_f64_scene(seed=17):
     """A scene whose float64 inputs are NOT float32-representable, with a
     rotated, translated camera (so view depths are not exact either): the
@@ -214,6 +276,9 @@ def main(which=None):
             "raw_f64", *raw_f64_scene(), RenderSettings(background=(0.3, 0.1, 0.2)), kg=1, with_log=False,
             in_dtype=np.float64),
         "exchange_f64": exchange_f64_fixture,
+        "grazing": lambda: render_fixture(
+            "grazing", *grazing_scene(), RenderSettings(background=(0.2, 0.2, 0.2)), kg=1,
+            naive=True),
     }
     for name, fn in jobs.items():
         if which and name not in which:

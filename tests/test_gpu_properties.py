@@ -196,7 +196,7 @@ def test_errors_match_reference_classes():
     with pytest.raises(errors.ConfigError):
         raster.render(ds, cam, RenderSettings(backend="python"))
     with pytest.raises(errors.ConfigError):
-        raster.render(ds, cam, RenderSettings(tile_size=8))
+        raster.render(ds, cam, RenderSettings(tile_size=12))  # tile sizes 8, 16, 32, 64 only
     bad = scene.copy()
     bad.rotation[3] = 0.0
     with pytest.raises(errors.InvalidParameterError):
