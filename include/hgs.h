@@ -20,8 +20,8 @@
  *    state: the caller provides a frame buffer (hgs_frame_bytes) that holds
  *    everything a forward produces and a backward consumes.
  *  - Work is enqueued on the caller's stream (a cudaStream_t passed as void*).
- *    hgs_forward synchronises that stream once, to read the number of
- *    tile/splat pairs K (data dependent) before binning.
+ *    hgs_forward enqueues the whole frame without a host round trip and then
+ *    synchronises once to report M, K and the status (HGS_FLAG_ASYNC: never).
  *  - Errors are returned as hgs_status codes; the Python layer maps them to
  *    the reference exception classes (hybridsplat/errors.py).
  */
@@ -111,6 +111,10 @@ typedef struct hgs_settings {
                                       accumulators stay in the scratch for hgs_backward_chain */
 #define HGS_FLAG_ACCUMULATE 0x40u  /* hgs_backward / hgs_backward_chain: grads += this view's gradient
                                       (multi-view batches) instead of grads = */
+#define HGS_FLAG_ASYNC 0x100u /* [ABI 3] hgs_forward: no host round trip at all (CUDA-graph capturable);
+                                * info->m = info->k = -1 until hgs_frame_sync_info, which also reports
+                                * the frame's status (bad parameters, pair capacity).  hgs_backward runs
+                                * on such a frame directly; the exports need the synced info. */
 #define HGS_FLAG_FRAME_ONLY 0x80u /* [ABI 3] hgs_forward: build_frame only (project.py:360-379): depth sort,
                                    * preprocess and binning, no compositing; out may be NULL and the
                                    * frame cannot be back-propagated */
@@ -142,10 +146,19 @@ typedef struct hgs_frame_info {
 size_t hgs_frame_bytes(int64_t n, int32_t width, int32_t height, int32_t tile_size, int64_t pair_capacity);
 
 /* render (raster/render.py:83-98): project, depth-sort, bin, composite.
- * Returns HGS_ERR_PAIR_CAPACITY (info->k = required pairs) if the frame buffer
- * cannot hold K pairs; the caller grows the buffer and calls again. */
+ * Every launch is sized from host-known bounds and reads the data-dependent
+ * counts (M, the depth-sort digit plan, K) from the frame on the device; the
+ * call ends with one host round trip that fills info->m / info->k and returns
+ * the frame's status (none with HGS_FLAG_ASYNC).  HGS_ERR_PAIR_CAPACITY
+ * (info->k = required pairs): the frame buffer cannot hold K pairs; the
+ * caller grows the buffer and calls again. */
 int hgs_forward(const hgs_scene *scene, const hgs_camera *camera, const hgs_settings *settings, void *frame,
                 size_t frame_bytes, const hgs_images *out, hgs_frame_info *info, void *stream);
+
+/* [ABI 3] Synchronises the stream, fills info->m, info->k from the frame and
+ * returns its status (HGS_OK, HGS_ERR_INVALID_PARAMETER, HGS_ERR_PAIR_CAPACITY
+ * with info->k = required pairs, ...). */
+int hgs_frame_sync_info(void *frame, hgs_frame_info *info, void *stream);
 
 /* Scratch bytes for hgs_backward with kg stacked upstream gradients. */
 size_t hgs_backward_scratch_bytes(int64_t n, int32_t kg);

@@ -31,6 +31,7 @@ HGS_FLAG_DEFER_ALL = 0x10  # tests: with HGS_FLAG_COUNT, every pixel goes throug
 HGS_FLAG_REPLAY_ONLY = 0x20  # hgs_backward: replay only, the chain rule follows via hgs_backward_chain
 HGS_FLAG_ACCUMULATE = 0x40   # grads += (multi-view batches)
 HGS_FLAG_FRAME_ONLY = 0x80   # build_frame: no compositing
+HGS_FLAG_ASYNC = 0x100       # hgs_forward without a host round trip (hgs_frame_sync_info later)
 COMPOSITOR_TILE = 16         # the compositor's tile; other tile sizes are re-binned on export
 
 # hgs_train.h constants
@@ -48,6 +49,7 @@ EXPORTS = ("hgs_abi_version", "hgs_status_string", "hgs_frame_bytes", "hgs_forwa
            "hgs_combine_gradients", "hgs_adam_step", "hgs_combine_adam_step",
            "hgs_densify_stats", "hgs_densify_scratch_bytes", "hgs_densify_plan", "hgs_densify_apply",
            "hgs_tile_bins_scratch_bytes", "hgs_frame_tile_bins", "hgs_eval_contributions",
+           "hgs_frame_sync_info",
            "hgs_effective_rank_f64", "hgs_reparameterize_f64", "hgs_modulation_f64")
 
 _vp = ctypes.c_void_p
@@ -167,6 +169,7 @@ def lib():
     L.hgs_blend_log.argtypes = [P(Scene), P(Camera), P(Settings), _vp, P(FrameInfo), _vp, _vp,
                                 _vp, _vp, _vp, _vp]
     L.hgs_frame_stats.argtypes = [_vp, P(FrameInfo), _vp, _vp]
+    L.hgs_frame_sync_info.argtypes = [_vp, P(FrameInfo), _vp]
     L.hgs_tile_bins_scratch_bytes.restype = ctypes.c_size_t
     L.hgs_tile_bins_scratch_bytes.argtypes = [_i64, _i32, _i32, _i32, _i64]
     L.hgs_frame_tile_bins.argtypes = [_vp, P(FrameInfo), _i32, _vp, _vp, _i64, _vp, ctypes.c_size_t,

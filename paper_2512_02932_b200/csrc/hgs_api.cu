@@ -14,7 +14,7 @@ namespace {
 constexpr int kMaxGrid = 148 * 8;
 
 struct Layout {
-  size_t state, hist_d, off_d, hist_p, off_p, keys_a, keys_b, vals_a, vals_b, lb_sort, lb_scan, recs, recs64, cull2d, eig, pair_off,
+  size_t state, hist_d, off_d, hist_p, off_p, keys_a, keys_b, vals_a, vals_b, rank, lb_sort, lb_scan, recs, recs64, cull2d, eig, pair_off,
       pk_a, pk_b, pv_a, pv_b, tile_off, pix_T, pix_last, pix_count, fwd_fix, bwd_fix, pix_mask, total;
   size_t small_end;  // [state, small_end) is zeroed at the start of a forward
   size_t lb_sort_bytes, lb_scan_bytes;
@@ -46,6 +46,7 @@ Layout make_layout(int64_t n, int W, int H, int64_t cap) {
   L.keys_b = take(nn * 8);
   L.vals_a = take(nn * 4);
   L.vals_b = take(nn * 4);
+  L.rank = take(nn * 4);  // depth rank of each Gaussian (0xffffffff: culled)
   L.recs = take(nn * sizeof(SplatRec));
   L.recs64 = take(nn * sizeof(Rec64));
   L.cull2d = take(nn * 2 * sizeof(float4));
@@ -165,7 +166,8 @@ int radix_sort(K *ka, K *kb, uint32_t *va, uint32_t *vb, int64_t n, const int *p
   for (int i = 0; i < npass; ++i) {
     const int p = passes[i];
     k_onesweep<K><<<(unsigned)tiles, kSortThreads, 0, s>>>(src, vs, dst, vd, n, p * kRadixBits, offsets + p * kRadix,
-                                                           lookback + (size_t)i * tiles * kRadix, counters + i);
+                                                           lookback + (size_t)i * tiles * kRadix, counters + i,
+                                                           SortDev{nullptr, nullptr, 0, nullptr, nullptr});
     HGS_LAUNCHED();
     std::swap(src, dst);
     std::swap(vs, vd);
@@ -219,6 +221,20 @@ static int64_t capacity_of(size_t frame_bytes, int64_t n, int W, int H) {
   return lo;
 }
 
+// End of a forward: with HGS_FLAG_ASYNC the counts stay on the device (info
+// m = k = -1 until hgs_frame_sync_info); otherwise the one host round trip
+// of the frame reads M, K and the status.
+static int finish_forward(void *frame, const Layout &L, hgs_frame_info *info, const hgs_settings *settings,
+                          cudaStream_t s) {
+  (void)L;
+  if (settings->flags & HGS_FLAG_ASYNC) {
+    info->m = -1;
+    info->k = -1;
+    return HGS_OK;
+  }
+  return hgs_frame_sync_info(frame, info, s);
+}
+
 int hgs_forward(const hgs_scene *scene, const hgs_camera *camera, const hgs_settings *settings, void *frame,
                 size_t frame_bytes, const hgs_images *out, hgs_frame_info *info, void *stream) {
   int rc = check_common(scene, camera, settings);
@@ -246,105 +262,88 @@ int hgs_forward(const hgs_scene *scene, const hgs_camera *camera, const hgs_sett
   HGS_CUDA(cudaMemsetAsync(frame, 0, L.small_end, s));
   k_init_state<<<1, 1, 0, s>>>(sc, cam, mod, at<SplatRec>(frame, L.recs), at<Rec64>(frame, L.recs64), st);
   HGS_LAUNCHED();
-  // 1. depth keys + digit histograms
-  uint32_t *vals_sorted = at<uint32_t>(frame, L.vals_a);
-  uint32_t *rank_of = at<uint32_t>(frame, L.vals_b);
-  int64_t m = 0;
+  // Every launch below is sized from host-known bounds (N, the pair capacity,
+  // the tile count) and reads the data-dependent counts -- M, the depth-sort
+  // digit plan, K, the capacity verdict -- from the frame state on the
+  // device: no host round trip inside a frame (stream-ordered, CUDA-graph
+  // capturable).  Work past the device counts exits at once.
+  const int64_t sort_tiles_n = ceil_div(std::max<int64_t>(n, 1), kSortTile);
+  // 1. depth keys + digit histograms + the pass plan
   if (n > 0) {
     HGS_CUDA(launch_depth_keys(sc, cam, at<unsigned long long>(frame, L.keys_a), at<uint32_t>(frame, L.vals_a),
                                at<uint32_t>(frame, L.hist_d), st, grid_for(n, 256), s));
-    k_radix_offsets<<<8, kRadix, 0, s>>>(at<uint32_t>(frame, L.hist_d), at<uint32_t>(frame, L.off_d));
+    k_sort_plan<<<1, kRadix, 0, s>>>(at<uint32_t>(frame, L.hist_d), n, at<uint32_t>(frame, L.off_d), st);
     HGS_LAUNCHED();
-    // one device-to-host copy: the state block and the digit histograms are
-    // adjacent in the frame (make_layout)
-    static_assert(sizeof(FrameState) <= 4096, "FrameState fits the staging block");
-    alignas(16) unsigned char head[4096 + 8 * kRadix * 4];
-    const size_t head_bytes = L.hist_d + 8 * kRadix * 4;
-    if (head_bytes > sizeof(head)) return HGS_ERR_CONFIG;
-    HGS_CUDA(cudaMemcpyAsync(head, frame, head_bytes, cudaMemcpyDeviceToHost, s));
-    HGS_CUDA(cudaStreamSynchronize(s));
-    FrameState hst;
-    memcpy(&hst, head + L.state, sizeof(hst));
-    uint32_t hist[8 * kRadix];
-    memcpy(hist, head + L.hist_d, sizeof(hist));
-    if (hst.status) return (int)hst.status;
-    m = hst.m_count;
-    // 2. depth sort over the digit passes that are not constant
-    int passes[8], np = 0;
-    for (int p = 0; p < 8; ++p) {
-      bool trivial = false;
-      for (int d = 0; d < kRadix; ++d)
-        if (hist[p * kRadix + d] == (uint32_t)n) trivial = true;
-      if (!trivial) passes[np++] = p;
+    // 2. depth sort: 8 digit passes launched, the constant ones exit at once
+    uint32_t *lb = at<uint32_t>(frame, L.lb_sort);
+    HGS_CUDA(cudaMemsetAsync(lb, 0, (size_t)sort_tiles_n * kRadix * 4 * 8, s));
+    for (int i = 0; i < 8; ++i) {
+      unsigned long long *ka = at<unsigned long long>(frame, (i & 1) ? L.keys_b : L.keys_a);
+      unsigned long long *kb = at<unsigned long long>(frame, (i & 1) ? L.keys_a : L.keys_b);
+      uint32_t *va = at<uint32_t>(frame, (i & 1) ? L.vals_b : L.vals_a);
+      uint32_t *vb = at<uint32_t>(frame, (i & 1) ? L.vals_a : L.vals_b);
+      k_onesweep<unsigned long long><<<(unsigned)sort_tiles_n, kSortThreads, 0, s>>>(
+          ka, va, kb, vb, n, 0, at<uint32_t>(frame, L.off_d), lb + (size_t)i * sort_tiles_n * kRadix,
+          st->tile_counters + 1 + i, SortDev{&st->sort_np, st->sort_digit, i, nullptr, nullptr});
+      HGS_LAUNCHED();
     }
-    bool in_b;
-    rc = radix_sort<unsigned long long>(at<unsigned long long>(frame, L.keys_a), at<unsigned long long>(frame, L.keys_b),
-                                        at<uint32_t>(frame, L.vals_a), at<uint32_t>(frame, L.vals_b), n, passes, np,
-                                        at<uint32_t>(frame, L.off_d), at<uint32_t>(frame, L.lb_sort),
-                                        st->tile_counters + 1, s, &in_b);
-    if (rc) return rc;
-    vals_sorted = at<uint32_t>(frame, in_b ? L.vals_b : L.vals_a);
-    rank_of = at<uint32_t>(frame, in_b ? L.vals_a : L.vals_b);  // the free ping-pong buffer
-    info->internal[2] = (uint32_t)np;  // depth-sort passes (diagnostics / launch count)
   }
-  info->m = m;
   HGS_CUDA(record_event(settings, 1, s));
-  // 3. float64 preprocess per rank + pair-offset scan
-  int64_t K = 0;
-  if (m > 0) {
+  // 3. float64 preprocess per Gaussian (record at its depth rank) + pair-offset scan
+  uint32_t *rank_of = at<uint32_t>(frame, L.rank);
+  if (n > 0) {
     HGS_CUDA(cudaMemsetAsync(at<char>(frame, L.lb_scan), 0, L.lb_scan_bytes, s));
-    // tile counts per rank go to the (now free) depth-key buffer
+    // tile counts per rank go to the depth-key buffer (free after the sort)
     uint32_t *counts = at<uint32_t>(frame, L.keys_a);
-    k_rank_scatter<<<grid_for(n, 256), 256, 0, s>>>(vals_sorted, m, n, rank_of);
+    k_rank_scatter<<<grid_for(n, 256), 256, 0, s>>>(at<uint32_t>(frame, L.vals_a), at<uint32_t>(frame, L.vals_b), st,
+                                                    n, rank_of);
     HGS_LAUNCHED();
     HGS_CUDA(launch_preprocess(sc, cam, mod, rank_of, at<SplatRec>(frame, L.recs), at<Rec64>(frame, L.recs64),
                                at<float4>(frame, L.cull2d), at<float2>(frame, L.eig), counts, s));
     HGS_LAUNCHED();
-    k_scan_counts<<<(unsigned)ceil_div(m, kScanTile), kScanThreads, 0, s>>>(
-        counts, m, at<unsigned long long>(frame, L.pair_off), at<unsigned long long>(frame, L.lb_scan), st);
+    k_scan_counts<<<(unsigned)ceil_div(n, kScanTile), kScanThreads, 0, s>>>(
+        counts, -1, at<unsigned long long>(frame, L.pair_off), at<unsigned long long>(frame, L.lb_scan), st,
+        std::min<int64_t>(cap, 0xffffffffll));
     HGS_LAUNCHED();
-    unsigned long long kt;
-    HGS_CUDA(cudaMemcpyAsync(&kt, &st->k_total, 8, cudaMemcpyDeviceToHost, s));
-    HGS_CUDA(cudaStreamSynchronize(s));
-    K = (int64_t)kt;
   }
-  info->k = K;
   HGS_CUDA(record_event(settings, 2, s));
-  if (K > cap || K >= (1ll << 32)) return HGS_ERR_PAIR_CAPACITY;
-  // 4. duplicate + tile sort + ranges
-  const uint32_t *tile_vals = at<uint32_t>(frame, L.pv_a);
-  const uint32_t *tile_keys = at<uint32_t>(frame, L.pk_a);
-  if (K > 0) {
-    const int nd = n_tiles > kRadix ? 2 : 1;
-    k_duplicate<<<grid_for(m, 256), 256, 0, s>>>(at<SplatRec>(frame, L.recs), at<unsigned long long>(frame, L.pair_off),
-                                                 m, cam.tiles_x, kTileShift, at<uint32_t>(frame, L.pk_a),
-                                                 at<uint32_t>(frame, L.pv_a),
-                                                 nd, at<uint32_t>(frame, L.hist_p));
+  // 4. duplicate + tile sort + ranges (K and the capacity verdict on the device)
+  const int nd = n_tiles > kRadix ? 2 : 1;  // tile-sort digit passes
+  const bool pairs_in_b = (nd & 1) != 0;    // where the sorted pairs land
+  const uint32_t *tile_vals = at<uint32_t>(frame, pairs_in_b ? L.pv_b : L.pv_a);
+  const uint32_t *tile_keys = at<uint32_t>(frame, pairs_in_b ? L.pk_b : L.pk_a);
+  const int64_t sort_tiles_k = ceil_div(std::max<int64_t>(cap, 1), kSortTile);
+  if (n > 0) {
+    k_duplicate<<<grid_for(n, 256), 256, 0, s>>>(at<SplatRec>(frame, L.recs), at<unsigned long long>(frame, L.pair_off),
+                                                 -1, st, cam.tiles_x, kTileShift, at<uint32_t>(frame, L.pk_a),
+                                                 at<uint32_t>(frame, L.pv_a), nd, at<uint32_t>(frame, L.hist_p));
     HGS_LAUNCHED();
     k_radix_offsets<<<nd, kRadix, 0, s>>>(at<uint32_t>(frame, L.hist_p), at<uint32_t>(frame, L.off_p));
     HGS_LAUNCHED();
-    int passes[2] = {0, 1};
-    bool in_b;
-    rc = radix_sort<uint32_t>(at<uint32_t>(frame, L.pk_a), at<uint32_t>(frame, L.pk_b), at<uint32_t>(frame, L.pv_a),
-                              at<uint32_t>(frame, L.pv_b), K, passes, nd, at<uint32_t>(frame, L.off_p),
-                              at<uint32_t>(frame, L.lb_sort), st->tile_counters + 12, s, &in_b);
-    if (rc) return rc;
-    tile_vals = at<uint32_t>(frame, in_b ? L.pv_b : L.pv_a);
-    tile_keys = at<uint32_t>(frame, in_b ? L.pk_b : L.pk_a);
-    info->internal[0] = in_b ? 1u : 0u;
-    info->internal[3] = (uint32_t)nd;  // tile-sort passes
+    uint32_t *lb = at<uint32_t>(frame, L.lb_sort);  // free again after the depth sort
+    HGS_CUDA(cudaMemsetAsync(lb, 0, (size_t)sort_tiles_k * kRadix * 4 * nd, s));
+    for (int i = 0; i < nd; ++i) {
+      k_onesweep<uint32_t><<<(unsigned)sort_tiles_k, kSortThreads, 0, s>>>(
+          at<uint32_t>(frame, (i & 1) ? L.pk_b : L.pk_a), at<uint32_t>(frame, (i & 1) ? L.pv_b : L.pv_a),
+          at<uint32_t>(frame, (i & 1) ? L.pk_a : L.pk_b), at<uint32_t>(frame, (i & 1) ? L.pv_a : L.pv_b), 0,
+          i * kRadixBits, at<uint32_t>(frame, L.off_p) + i * kRadix, lb + (size_t)i * sort_tiles_k * kRadix,
+          st->tile_counters + 12 + i, SortDev{nullptr, nullptr, 0, &st->k_total, &st->status});
+      HGS_LAUNCHED();
+    }
   }
-  k_tile_ranges<<<grid_for(ceil_div(std::max<int64_t>(K, n_tiles + 1), 4), 256), 256, 0, s>>>(
-      tile_keys, K, n_tiles, at<uint32_t>(frame, L.tile_off));
+  info->internal[0] = pairs_in_b ? 1u : 0u;
+  info->internal[3] = (uint32_t)nd;
+  k_tile_ranges<<<grid_for(ceil_div(std::max<int64_t>(cap, n_tiles + 1), 4), 256), 256, 0, s>>>(
+      tile_keys, n > 0 ? -1 : 0, st, n_tiles, at<uint32_t>(frame, L.tile_off));
   HGS_LAUNCHED();
   HGS_CUDA(record_event(settings, 3, s));
-  if (settings->flags & HGS_FLAG_FRAME_ONLY) return HGS_OK;  // build_frame: no compositing
+  if (settings->flags & HGS_FLAG_FRAME_ONLY) return finish_forward(frame, L, info, settings, s);  // build_frame
   // 5. composite
   CompositeArgs a;
   a.recs = at<SplatRec>(frame, L.recs);
   a.tile_off = at<uint32_t>(frame, L.tile_off);
   a.tile_vals = tile_vals;
-  a.m = m;
+  a.m = -1;  // M lives in the frame state
   a.tiles_x = cam.tiles_x; a.width = W; a.height = H;
   a.flags = settings->flags;
   for (int c = 0; c < 3; ++c) a.bg[c] = settings->background[c];
@@ -364,7 +363,20 @@ int hgs_forward(const hgs_scene *scene, const hgs_camera *camera, const hgs_sett
   k_fixup_fwd<<<kFixupBlocks, 256, 0, s>>>(a);
   HGS_LAUNCHED();
   HGS_CUDA(record_event(settings, 4, s));
-  return HGS_OK;
+  return finish_forward(frame, L, info, settings, s);
+}
+
+int hgs_frame_sync_info(void *frame, hgs_frame_info *info, void *stream) {
+  if (!frame || !info) return HGS_ERR_CONFIG;
+  const Layout L = make_layout(info->n, info->width, info->height, info->pair_capacity);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  FrameState h;
+  HGS_CUDA(cudaMemcpyAsync(&h, at<FrameState>(frame, L.state), sizeof(h), cudaMemcpyDeviceToHost, s));
+  HGS_CUDA(cudaStreamSynchronize(s));
+  info->m = h.m_count;
+  info->k = (int64_t)h.k_total;
+  info->internal[2] = h.sort_np;
+  return (int)h.status;
 }
 
 static CompositeArgs composite_args_for(const hgs_scene *scene, const hgs_camera *camera,
@@ -532,7 +544,7 @@ int hgs_backward(const hgs_scene *scene, const hgs_camera *camera, const hgs_set
     b.rec_count = det ? reinterpret_cast<uint32_t *>(scr + DL.count) : nullptr;
     b.rec_cap = (uint32_t)rec_cap;
     if (det) HGS_CUDA(cudaMemsetAsync(b.rec_count, 0, 4, s));
-    if (m > 0) {
+    if (m != 0) {  // m < 0: an asynchronous frame (M on the device)
       HGS_CUDA(launch_composite_bwd(b, (int)kc, info->n_tiles, ext, det, s));
       if (det) {  // sort the records by (Gaussian, tile, sub) and reduce in that order
         uint32_t nrec = 0;
@@ -746,6 +758,7 @@ int hgs_frame_export_arrays(const hgs_scene *scene, const hgs_camera *camera, co
   if (rc) return rc;
   rc = check_frame(scene, camera, info);
   if (rc) return rc;
+  if (info->m < 0 || info->k < 0) return HGS_ERR_INTEGRITY;  // asynchronous frame: hgs_frame_sync_info first
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const CompositeArgs a = composite_args_for(scene, camera, settings, frame, info);
   if (info->m > 0) {
@@ -860,6 +873,7 @@ int hgs_frame_tile_bins(const void *frame, const hgs_frame_info *info, int32_t t
   if (!frame || !info || sh < 0 || !tile_offsets || !k_out || ids_capacity < 0 || !scratch) return HGS_ERR_CONFIG;
   const int W = info->width, H = info->height;
   const int64_t m = info->m;
+  if (m < 0) return HGS_ERR_INTEGRITY;  // asynchronous frame: hgs_frame_sync_info first
   const RebinLayout R = rebin_layout(m, W, H, tile_size, ids_capacity);
   if (scratch_bytes < R.total) return HGS_ERR_CONFIG;
   const Layout L = make_layout(info->n, W, H, info->pair_capacity);
@@ -876,7 +890,7 @@ int hgs_frame_tile_bins(const void *frame, const hgs_frame_info *info, int32_t t
     HGS_LAUNCHED();
     k_scan_counts<<<(unsigned)ceil_div(m, kScanTile), kScanThreads, 0, s>>>(
         at<uint32_t>(scratch, R.counts), m, at<unsigned long long>(scratch, R.pair_off),
-        at<unsigned long long>(scratch, R.lb_scan), st);
+        at<unsigned long long>(scratch, R.lb_scan), st, -1);
     HGS_LAUNCHED();
     unsigned long long kt;
     HGS_CUDA(cudaMemcpyAsync(&kt, &st->k_total, 8, cudaMemcpyDeviceToHost, s));
@@ -889,7 +903,8 @@ int hgs_frame_tile_bins(const void *frame, const hgs_frame_info *info, int32_t t
   if (K > 0) {
     const int nd = n_tiles > kRadix ? 2 : 1;
     if (n_tiles > (1 << 16)) return HGS_ERR_CONFIG;  // 2 digit passes cover 65536 tiles
-    k_duplicate<<<grid_for(m, 256), 256, 0, s>>>(recs, at<unsigned long long>(scratch, R.pair_off), m, tiles_x, sh,
+    k_duplicate<<<grid_for(m, 256), 256, 0, s>>>(recs, at<unsigned long long>(scratch, R.pair_off), m, nullptr,
+                                                 tiles_x, sh,
                                                  at<uint32_t>(scratch, R.ka), at<uint32_t>(scratch, R.va),
                                                  nd, at<uint32_t>(scratch, R.hist));
     HGS_LAUNCHED();
@@ -906,7 +921,7 @@ int hgs_frame_tile_bins(const void *frame, const hgs_frame_info *info, int32_t t
     vals = at<uint32_t>(scratch, in_b ? R.vb : R.va);
   }
   k_tile_ranges<<<grid_for(ceil_div(std::max<int64_t>(K, n_tiles + 1), 4), 256), 256, 0, s>>>(
-      keys, K, n_tiles, at<uint32_t>(scratch, R.tile_off));
+      keys, K, nullptr, n_tiles, at<uint32_t>(scratch, R.tile_off));
   HGS_LAUNCHED();
   k_export_u32_to_i64<<<grid_for(n_tiles + 1, 256), 256, 0, s>>>(at<uint32_t>(scratch, R.tile_off), tile_offsets,
                                                                  n_tiles + 1);

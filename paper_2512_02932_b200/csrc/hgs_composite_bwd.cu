@@ -164,6 +164,7 @@ template <int KG, bool EXT, bool DET>
 __global__ void __launch_bounds__(128, KG == 1 ? 5 : 4) k_composite_bwd_naive(BwdArgs b) {
   constexpr int PPL = 2;
   const CompositeArgs &a = b.c;
+  if (a.st->status) return;  // failed frame
   __shared__ SplatRec s_rec[4][32];
   __shared__ __align__(16) float s_red[4][kRedWarp];
   const int tile = blockIdx.x;
@@ -398,6 +399,7 @@ template <int KG, bool EXT, bool DET, int QP>
 __global__ void __launch_bounds__(256 / QP, HGS_BWDC_MINB(KG, EXT, QP)) k_composite_bwd_c(BwdArgs b) {
   constexpr int NW = 8 / QP;  // warps per tile
   const CompositeArgs &a = b.c;
+  if (a.st->status) return;  // failed frame
   __shared__ SplatRec s_rec[NW][32];
   __shared__ __align__(16) float s_red[NW][kRedWarp];
   extern __shared__ __align__(16) unsigned char s_dyn[];

@@ -18,6 +18,9 @@
 #ifndef HGS_FWD_MINB
 #define HGS_FWD_MINB 4  // CTAs per SM the hot compositor is register-budgeted for
 #endif
+#ifndef HGS_FWD_PF
+#define HGS_FWD_PF 0  // 1, 2: tiled forward stages the next chunk's records with cp.async while walking this one (measured slower)
+#endif
 
 namespace hgs {
 
@@ -29,9 +32,25 @@ namespace hgs {
 // staged in the warp's slice of shared memory and walked in order.  Every
 // lane sees the same splat, so the 2D / 3D branch is warp-uniform; a warp
 // retires as soon as its 32 pixels are saturated or deferred.
-template <bool NAIVE, bool COUNT>
+// 16-byte asynchronous global -> shared copy (L1-allocating: the 8 warps of
+// a tile read the same records) and its group fences.
+__device__ __forceinline__ void cp_async16(uint32_t dst_sa, const void *src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(dst_sa), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// PF (tiled frames only): software-pipelined staging.  The records of chunk
+// c + 1 are copied into the warp's second staging buffer with cp.async while
+// chunk c is walked, and the tile-list ranks two chunks ahead are loaded into
+// a register -- the rank -> record -> bbox gather chain (two dependent L2
+// round trips per chunk) leaves the critical path.  Every entry of the chunk
+// is copied (the bbox test needs the record), the culls then run on the
+// shared-memory copy.
+template <bool NAIVE, bool COUNT, int PF>
 __global__ void __launch_bounds__(kBlock, HGS_FWD_MINB) k_composite_fwd(CompositeArgs a) {
-  __shared__ SplatRec s_rec[kBlock / 32][32];
+  __shared__ SplatRec s_rec[PF ? 2 : 1][kBlock / 32][32];
   const int tile = blockIdx.x;
   const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -42,10 +61,11 @@ __global__ void __launch_bounds__(kBlock, HGS_FWD_MINB) k_composite_fwd(Composit
   const float lox = (float)(lane & 7), loy = (float)(lane >> 3);  // offset in the warp block
   const bool exact = HGS_EXACT_ENABLED && !(a.flags & HGS_FLAG_FAST);
   const bool stress = COUNT && !NAIVE && (a.flags & HGS_FLAG_DEFER_ALL);
+  if (a.st->status) return;  // failed frame (bad parameters / pair capacity): nothing to composite
   uint32_t lo, hi;
   if (NAIVE) {
     lo = 0;
-    hi = (uint32_t)a.m;
+    hi = a.st->m_count;
   } else {
     lo = a.tile_off[tile];
     hi = a.tile_off[tile + 1];
@@ -55,11 +75,36 @@ __global__ void __launch_bounds__(kBlock, HGS_FWD_MINB) k_composite_fwd(Composit
   uint32_t cnt = 0, last = 0;
   bool done = !inside, deferred = false;
   uint32_t n_ev3 = 0, n_ev2 = 0, n_c3 = 0, n_c2 = 0;  // HGS_FLAG_COUNT
-  SplatRec *wrec = s_rec[warp];
+  SplatRec *wrec = s_rec[0][warp];
 #if HGS_FWD_PIN_SA
   uint32_t wrec_sa = (uint32_t)__cvta_generic_to_shared(wrec);
   asm volatile("mov.u32 %0, %0;" : "+r"(wrec_sa));  // opaque: kept, not re-derived per splat
 #endif
+  // PF: rk_c / rk_n / rk_nn = tile-list ranks of chunks c, c + 1, c + 2 of
+  // this lane's entry; q_n = the bbox word (r5) of chunk c + 1's entry
+  // (PF == 2: only entries whose bbox meets the warp block are copied)
+  constexpr uint32_t kNoRank = 0xffffffffu;
+  constexpr uint32_t kBufBytes = (uint32_t)(kBlock / 32) * 32u * (uint32_t)sizeof(SplatRec);
+  uint32_t rk_c = kNoRank, rk_n = kNoRank, rk_nn = kNoRank, slot_sa = 0u;
+  int4 q_n = make_int4(0, -1, 0, 0);
+  bool staged = false;  // this lane's entry of the chunk about to be walked was copied
+  auto stage_async = [&](uint32_t dst_sa, uint32_t rk) {
+    const char *src = reinterpret_cast<const char *>(a.recs + rk);
+#pragma unroll
+    for (int k = 0; k < 6; ++k) cp_async16(dst_sa + 16u * k, src + 16 * k);
+  };
+  auto rank_at = [&](uint32_t e) { return e < hi ? __ldg(a.tile_vals + e) : kNoRank; };
+  if (PF) {
+    slot_sa = (uint32_t)__cvta_generic_to_shared(&s_rec[0][warp][lane]);
+    rk_c = rank_at(lo + lane);
+    rk_n = rank_at(lo + 32u + lane);
+    staged = rk_c != kNoRank && (PF == 1 || pixel_mask(__ldg(&a.recs[rk_c].r5), wx0, wy0));
+    if (staged) stage_async(slot_sa, rk_c);
+    cp_async_commit();
+    if (PF == 2 && rk_n != kNoRank) q_n = __ldg(&a.recs[rk_n].r5);
+    rk_nn = rank_at(lo + 64u + lane);
+  }
+  uint32_t buf = 0u;
 
   auto defer = [&](uint32_t entry, uint32_t mode) {
     FwdFix f;
@@ -78,7 +123,44 @@ __global__ void __launch_bounds__(kBlock, HGS_FWD_MINB) k_composite_fwd(Composit
     // stage: rank + bbox of entry base + lane, pixel mask, record if relevant
     const uint32_t j = base + lane;
     uint32_t pm = 0u;
-    if (j < hi) {
+    if (PF) {
+      // copies of chunk c + 1 into the other buffer (its last reader, the
+      // walk of chunk c - 1, finished at that walk's closing __syncwarp)
+      const uint32_t nb = buf ^ 1u;
+      const bool staged_c = staged;
+      staged = rk_n != kNoRank && (PF == 1 || pixel_mask(q_n, wx0, wy0));
+      if (staged) stage_async(slot_sa + nb * kBufBytes, rk_n);
+      cp_async_commit();
+      // the pipeline's loads for chunk c + 2 (consumed next iteration)
+      if (PF == 2) q_n = rk_nn != kNoRank ? __ldg(&a.recs[rk_nn].r5) : make_int4(0, -1, 0, 0);
+      const uint32_t rk = rk_c;
+      rk_c = rk_n;
+      rk_n = rk_nn;
+      rk_nn = rank_at(base + 96u + lane);
+      cp_async_wait<1>();  // this lane's copies of chunk c have landed
+      wrec = s_rec[buf][warp];
+#if HGS_FWD_PIN_SA
+      wrec_sa = (uint32_t)__cvta_generic_to_shared(wrec);
+      asm volatile("mov.u32 %0, %0;" : "+r"(wrec_sa));
+#endif
+      if (staged_c) {
+        SplatRec &sr = wrec[lane];
+        const int4 q = sr.r5;
+        pm = pixel_mask(q, wx0, wy0);  // PF == 2: copied iff nonzero
+        if (pm) {
+          SplatRec r;
+          r.r0 = sr.r0; r.r1 = sr.r1; r.r2 = sr.r2; r.r3 = sr.r3; r.r4 = sr.r4; r.r5 = q;
+          if (HGS_CULL_PRE ? cull_splat_pre(r, a.cull2d + 2 * (size_t)rk, pm, wx0, wy0) : cull_splat(r, pm, wx0, wy0))
+            pm = 0u;
+          pm &= alive;
+          if (pm && HGS_STAGED_ORIGIN) {
+            stage_block_origin(r, wx0, wy0);
+            sr.r5 = r.r5;
+          }
+        }
+      }
+      buf ^= 1u;
+    } else if (j < hi) {
       const uint32_t rk = NAIVE ? j : __ldg(a.tile_vals + j);
       const SplatRec *g = a.recs + rk;
       const int4 q = __ldg(&g->r5);
@@ -198,6 +280,7 @@ __global__ void __launch_bounds__(kBlock, HGS_FWD_MINB) k_composite_fwd(Composit
       atomicAdd(&a.st->diag[5], (unsigned long long)n_c2);
     }
   }
+  if (PF) cp_async_wait<0>();  // no copy may still target this CTA's shared memory
   if (!inside || deferred) return;  // deferred pixels are written by k_fixup_fwd
   a.color[3 * pix + 0] = cr + a.bg[0] * T;
   a.color[3 * pix + 1] = cg + a.bg[1] * T;
@@ -216,10 +299,11 @@ __global__ void __launch_bounds__(kBlock, HGS_FWD_MINB) k_composite_fwd(Composit
 }
 
 cudaError_t launch_composite_fwd(const CompositeArgs &a, int64_t n_tiles, bool naive, bool count, cudaStream_t s) {
-  if (naive && count) k_composite_fwd<true, true><<<(unsigned)n_tiles, kBlock, 0, s>>>(a);
-  else if (naive) k_composite_fwd<true, false><<<(unsigned)n_tiles, kBlock, 0, s>>>(a);
-  else if (count) k_composite_fwd<false, true><<<(unsigned)n_tiles, kBlock, 0, s>>>(a);
-  else k_composite_fwd<false, false><<<(unsigned)n_tiles, kBlock, 0, s>>>(a);
+  constexpr int PF = HGS_FWD_PF;
+  if (naive && count) k_composite_fwd<true, true, 0><<<(unsigned)n_tiles, kBlock, 0, s>>>(a);
+  else if (naive) k_composite_fwd<true, false, 0><<<(unsigned)n_tiles, kBlock, 0, s>>>(a);
+  else if (count) k_composite_fwd<false, true, PF><<<(unsigned)n_tiles, kBlock, 0, s>>>(a);
+  else k_composite_fwd<false, false, PF><<<(unsigned)n_tiles, kBlock, 0, s>>>(a);
   return cudaGetLastError();
 }
 
@@ -279,7 +363,7 @@ __global__ void __launch_bounds__(256, HGS_FIXUP_MINB) k_fixup_fwd(CompositeArgs
     const int ix = (int)(f.pix % (uint32_t)a.width), iy = (int)(f.pix / (uint32_t)a.width);
     const int tile = (iy / kTile) * a.tiles_x + ix / kTile;
     const uint32_t lo = naive ? 0u : a.tile_off[tile];
-    const uint32_t hi = naive ? (uint32_t)a.m : a.tile_off[tile + 1];
+    const uint32_t hi = naive ? a.st->m_count : a.tile_off[tile + 1];
     float T = f.T;
     float q0 = 0.f, q1 = 0.f, q2 = 0.f, qd = 0.f, qn0 = 0.f, qn1 = 0.f, qn2 = 0.f;  // lane partial sums
     uint32_t cnt = f.cnt, last = f.last;

@@ -186,10 +186,47 @@ __device__ __forceinline__ void write_record(const ProjD &o, uint32_t idx, int W
 
 // Inverse depth permutation over all n sorted slots: culled Gaussians (keys
 // ~0, sorted after the m kept ones) get rank 0xffffffff.
-__global__ void k_rank_scatter(const uint32_t *__restrict__ sorted_idx, int64_t m, int64_t n,
-                               uint32_t *__restrict__ rank_of) {
+// Inverse of the depth permutation.  The sorted indices are in buffer
+// (sort_np & 1) of the ping-pong pair; M = the near-culled count, both from
+// the frame state (no host round trip).
+__global__ void k_rank_scatter(const uint32_t *__restrict__ vals_a, const uint32_t *__restrict__ vals_b,
+                               const FrameState *__restrict__ st, int64_t n, uint32_t *__restrict__ rank_of) {
+  const uint32_t *sorted_idx = (st->sort_np & 1u) ? vals_b : vals_a;
+  const int64_t m = st->m_count;
   for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x)
     rank_of[sorted_idx[r]] = r < m ? (uint32_t)r : 0xffffffffu;
+}
+
+// Depth-sort plan from the fused digit histograms (k_depth_keys): per digit
+// the exclusive offsets (k_radix_offsets) and whether every key has the same
+// digit (that pass is skipped); the non-constant digits, low to high, become
+// the device-side pass list the onesweep passes read.
+__global__ void k_sort_plan(const uint32_t *__restrict__ hist, int64_t n, uint32_t *__restrict__ offsets,
+                            FrameState *__restrict__ st) {
+  __shared__ uint32_t s[kRadix];
+  __shared__ int s_trivial[8];
+  const int t = threadIdx.x;
+  for (int p = 0; p < 8; ++p) {
+    const uint32_t h = hist[p * kRadix + t];
+    const int triv = __syncthreads_or(h == (uint32_t)n);
+    s[t] = h;
+    __syncthreads();
+    for (int d = 1; d < kRadix; d <<= 1) {
+      const uint32_t v = t >= d ? s[t - d] : 0u;
+      __syncthreads();
+      s[t] += v;
+      __syncthreads();
+    }
+    offsets[p * kRadix + t] = s[t] - h;
+    if (t == 0) s_trivial[p] = triv;
+    __syncthreads();
+  }
+  if (t == 0) {
+    uint32_t np = 0;
+    for (int p = 0; p < 8; ++p)
+      if (!s_trivial[p]) st->sort_digit[np++] = (uint32_t)p;
+    st->sort_np = np;
+  }
 }
 
 // One thread per Gaussian in index order, one warp per CTA and 32 consecutive
@@ -291,11 +328,15 @@ cudaError_t launch_preprocess(const SceneView &sc, const CamD &cam, const ModD &
 
 // Exclusive scan of the per-rank tile counts into pair offsets (decoupled
 // look-back, kScanItems counts per thread); the last tile writes K.
+// m < 0: M from the frame state.  cap >= 0: a total above it sets the
+// frame's status to HGS_ERR_PAIR_CAPACITY (the pair buffer is too small).
 __global__ void __launch_bounds__(kScanThreads) k_scan_counts(const uint32_t *__restrict__ counts, int64_t m,
                                                               unsigned long long *__restrict__ pair_off,
                                                               unsigned long long *__restrict__ scan_lb,
-                                                              FrameState *__restrict__ st) {
+                                                              FrameState *__restrict__ st, int64_t cap) {
   __shared__ uint32_t s_tile;
+  if (m < 0) m = st->m_count;
+  if ((int64_t)blockIdx.x * kScanTile >= m) return;  // launched for N, not for M
   __shared__ unsigned long long s_warp[32];
   __shared__ unsigned long long s_excl;
   if (threadIdx.x == 0) s_tile = atomicAdd(&st->tile_counters[0], 1u);
@@ -319,7 +360,10 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_counts(const uint32_t *__
     if (base + k < m) pair_off[base + k] = run;
     run += c[k];
   }
-  if ((int64_t)(tile + 1) * kScanTile >= m && threadIdx.x == 0) st->k_total = s_excl + total;
+  if ((int64_t)(tile + 1) * kScanTile >= m && threadIdx.x == 0) {
+    st->k_total = s_excl + total;
+    if (cap >= 0 && (int64_t)(s_excl + total) > cap) atomicCAS(&st->status, 0u, (uint32_t)HGS_ERR_PAIR_CAPACITY);
+  }
 }
 
 // ------------------------------------------------------------ duplicate
@@ -333,10 +377,14 @@ constexpr int kDupOwn = 32;
 
 __global__ void __launch_bounds__(256) k_duplicate(const SplatRec *__restrict__ recs,
                                                    const unsigned long long *__restrict__ pair_off, int64_t m,
-                                                   int tiles_x, int tile_shift, uint32_t *__restrict__ pkeys,
-                                                   uint32_t *__restrict__ pvals, int n_digits,
-                                                   uint32_t *__restrict__ hist) {
+                                                   const FrameState *__restrict__ st, int tiles_x, int tile_shift,
+                                                   uint32_t *__restrict__ pkeys, uint32_t *__restrict__ pvals,
+                                                   int n_digits, uint32_t *__restrict__ hist) {
   __shared__ uint32_t sh[2 * kRadix];
+  if (m < 0) {  // M and the capacity verdict from the frame state
+    if (st->status) return;
+    m = st->m_count;
+  }
   for (int i = threadIdx.x; i < 2 * kRadix; i += blockDim.x) sh[i] = 0;
   __syncthreads();
   const int lane = threadIdx.x & 31;
@@ -403,8 +451,13 @@ __global__ void __launch_bounds__(256) k_rebin_counts(const SplatRec *__restrict
 
 // tile_offsets (n_tiles + 1) from the tile-sorted keys (project.py:344-345).
 // Four keys per thread (one 16-byte load), grid-stride.
-__global__ void __launch_bounds__(256) k_tile_ranges(const uint32_t *__restrict__ skeys, int64_t k, int64_t n_tiles,
+__global__ void __launch_bounds__(256) k_tile_ranges(const uint32_t *__restrict__ skeys, int64_t k,
+                                                     const FrameState *__restrict__ st, int64_t n_tiles,
                                                      uint32_t *__restrict__ tile_off) {
+  if (k < 0) {  // K from the frame state
+    if (st->status) return;
+    k = (int64_t)st->k_total;
+  }
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (k == 0) {

@@ -25,6 +25,8 @@ struct FrameState {
   uint32_t m_count;
   unsigned long long k_total;
   uint32_t tile_counters[24];
+  uint32_t sort_np;        // depth-sort passes (non-constant digits), set by k_sort_plan
+  uint32_t sort_digit[8];  // their digit indices, low to high
   unsigned long long diag[16];  // see hgs_frame_stats in include/hgs.h
   uint32_t n_fix_fwd, n_fix_bwd;  // deferred pixels (worklist lengths)
   SceneView sc;
@@ -651,17 +653,20 @@ __global__ void k_init_state(SceneView sc, CamD cam, ModD mod, const SplatRec *r
                              FrameState *st);
 cudaError_t launch_depth_keys(const SceneView &sc, const CamD &cam, unsigned long long *keys, uint32_t *vals,
                               uint32_t *hist, FrameState *st, int grid, cudaStream_t s);
-__global__ void k_rank_scatter(const uint32_t *sorted_idx, int64_t m, int64_t n, uint32_t *rank_of);
+__global__ void k_rank_scatter(const uint32_t *vals_a, const uint32_t *vals_b, const FrameState *st, int64_t n,
+                               uint32_t *rank_of);
 cudaError_t launch_preprocess(const SceneView &sc, const CamD &cam, const ModD &mod, const uint32_t *rank_of,
                               SplatRec *recs, Rec64 *recs64, float4 *cull2d, float2 *eig, uint32_t *counts,
                               cudaStream_t s);
 __global__ void k_scan_counts(const uint32_t *counts, int64_t m, unsigned long long *pair_off,
-                              unsigned long long *scan_lb, FrameState *st);
+                              unsigned long long *scan_lb, FrameState *st, int64_t cap);
 __global__ void k_rebin_counts(const SplatRec *recs, int64_t m, int tile_shift, uint32_t *counts);
-__global__ void k_duplicate(const SplatRec *recs, const unsigned long long *pair_off, int64_t m, int tiles_x,
-                            int tile_shift,
-                            uint32_t *pkeys, uint32_t *pvals, int n_digits, uint32_t *hist);
-__global__ void k_tile_ranges(const uint32_t *skeys, int64_t k, int64_t n_tiles, uint32_t *tile_off);
+__global__ void k_duplicate(const SplatRec *recs, const unsigned long long *pair_off, int64_t m, const FrameState *st,
+                            int tiles_x, int tile_shift, uint32_t *pkeys, uint32_t *pvals, int n_digits,
+                            uint32_t *hist);
+__global__ void k_tile_ranges(const uint32_t *skeys, int64_t k, const FrameState *st, int64_t n_tiles,
+                              uint32_t *tile_off);
+__global__ void k_sort_plan(const uint32_t *hist, int64_t n, uint32_t *offsets, FrameState *st);
 // Host launchers of the template kernels (each instantiated and launched in
 // its own translation unit).
 cudaError_t launch_composite_fwd(const CompositeArgs &a, int64_t n_tiles, bool naive, bool count, cudaStream_t s);

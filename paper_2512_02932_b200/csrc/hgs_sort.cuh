@@ -84,6 +84,21 @@ static __global__ void k_radix_offsets(const uint32_t *__restrict__ hist, uint32
 #ifndef HGS_SORT_MINB64
 #define HGS_SORT_MINB64 3
 #endif
+// Device-driven passes (no host round trip, CUDA-graph capturable): with
+// `plan` set, pass `pass` of the depth sort runs digit plan->sort_digit[pass]
+// and exits at once if pass >= plan->sort_np (the digit is constant; the
+// active passes are a prefix, so pass i always reads buffer i & 1); with
+// `n_dev` set the key count is *n_dev (the tile sort's K), and the pass exits
+// if the frame's status is set (pair capacity exceeded).  Blocks whose tile
+// lies past the keys exit after taking their tile id.
+struct SortDev {
+  const unsigned *plan_np;             // &FrameState::sort_np (depth sort) or null
+  const unsigned *plan_digit;          // &FrameState::sort_digit[0]
+  int pass;
+  const unsigned long long *n_dev;     // &FrameState::k_total (tile sort) or null
+  const unsigned *status;              // &FrameState::status (with n_dev)
+};
+
 template <typename K>
 __global__ void __launch_bounds__(kSortThreads, sizeof(K) == 4 ? HGS_SORT_MINB32 : HGS_SORT_MINB64) k_onesweep(const K *__restrict__ keys_in,
                                                            const uint32_t *__restrict__ vals_in,
@@ -91,7 +106,18 @@ __global__ void __launch_bounds__(kSortThreads, sizeof(K) == 4 ? HGS_SORT_MINB32
                                                            int64_t n, int shift,
                                                            const uint32_t *__restrict__ digit_offsets,
                                                            uint32_t *__restrict__ lookback,
-                                                           uint32_t *__restrict__ tile_counter) {
+                                                           uint32_t *__restrict__ tile_counter, SortDev dv) {
+  if (dv.plan_np) {
+    if ((unsigned)dv.pass >= *dv.plan_np) return;
+    const unsigned dg = dv.plan_digit[dv.pass];
+    shift = (int)dg * kRadixBits;
+    digit_offsets += dg * kRadix;
+  }
+  if (dv.n_dev) {
+    if (*dv.status) return;
+    n = (int64_t)*dv.n_dev;
+  }
+  if ((int64_t)blockIdx.x * kSortTile >= n) return;  // launched for a capacity, not for n
   constexpr int W = kSortThreads / 32;
   __shared__ uint32_t s_tile;
   __shared__ uint32_t warp_hist[W][kRadix];

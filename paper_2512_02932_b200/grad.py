@@ -156,7 +156,9 @@ def backward_device(frame, pixel_grads, depth_grads=None, normal_grads=None, alp
     if replay_only:
         fl |= _lib.HGS_FLAG_REPLAY_ONLY
     key = (n, kg, frame.width, frame.height)
-    records = _det_hint.get(key, 2 * frame.pair_count + (1 << 16))
+    # (only the deterministic mode sizes its records from K: an asynchronous
+    # frame's counts stay on the device otherwise)
+    records = _det_hint.get(key) or (2 * frame.pair_count + (1 << 16) if deterministic else 0)
     for _ in range(8):
         nscr = (L.hgs_backward_det_scratch_bytes(n, kg, records) if deterministic
                 else L.hgs_backward_scratch_bytes(n, kg))

@@ -97,15 +97,34 @@ def view_batch_grads(scene, cameras, settings, pixel_grads_of, out, scratch=None
     from . import grad, raster
     ready = dist.is_available() and dist.is_initialized()
     world = dist.get_world_size(group) if ready else 1
+    import torch
     n, B = scene.count, scene.sh_bases
     acc = out.view(1, -1)
     frame = None
     if not cameras:
         out.zero_()
+    # Every view renders into one frame buffer with no host round trip
+    # (HGS_FLAG_ASYNC): the views queue back to back on the stream.  Each
+    # view's status / M / K word (the first 16 bytes of the frame) is copied
+    # to pinned memory; a view that outgrew the pair capacity composited
+    # nothing and back-propagated zeros, so it is simply redone synchronously
+    # (accumulating) once the step's work has drained.
+    dev = scene.device
+    fbuf = torch.empty(raster.frame_bytes(n, int(cameras[0].width), int(cameras[0].height)),
+                       dtype=torch.uint8, device=dev) if cameras else None
+    heads = torch.empty((len(cameras), 16), dtype=torch.uint8, pin_memory=True) if cameras else None
+
+    def view(j, cam, last, async_):
+        imgs, fr = raster.rasterize(scene, cam, settings, flags, outputs=outputs,
+                                    events=fwd_events if last else None, async_=async_,
+                                    frame_buf=fbuf if async_ else None)
+        if async_:
+            heads[j].copy_(fbuf[:16], non_blocking=True)
+        return imgs, fr
+
     for j, cam in enumerate(cameras):
         last = j == len(cameras) - 1
-        imgs, frame = raster.rasterize(scene, cam, settings, flags, outputs=outputs,
-                                       events=fwd_events if last else None)
+        imgs, frame = view(j, cam, last, True)
         pg = pixel_grads_of(j, imgs)
         if not last or world == 1:
             grad.backward_device(frame, pg, *ext_grads, grads_out=acc, touched_out=touched,
@@ -113,13 +132,46 @@ def view_batch_grads(scene, cameras, settings, pixel_grads_of, out, scratch=None
             continue
         grad.backward_device(frame, pg, *ext_grads, grads_out=acc, touched_out=touched,
                              scratch=scratch, replay_only=True, events=events)
+        if _redo_failed(cameras, heads, view, pixel_grads_of, ext_grads, acc, touched, scratch,
+                        last_excluded=True):
+            frame = view(j, cam, True, False)[1]  # the last view again, synchronously
+            grad.backward_device(frame, pg, *ext_grads, grads_out=acc, touched_out=touched,
+                                 scratch=scratch, replay_only=True)
         bucketed_allreduce(out, n, B, buckets,
-                           lambda g0, g1: grad.chain_range(frame, g0, g1, acc, accumulate=j > 0),
+                           lambda g0, g1: grad.chain_range(frame, g0, g1, acc, accumulate=True),
                            group=group)
         return frame
+    if cameras:
+        _redo_failed(cameras, heads, view, pixel_grads_of, ext_grads, acc, touched, scratch)
     if world > 1:  # no views on this rank: contribute zeros
         dist.all_reduce(out, op=dist.ReduceOp.SUM, group=group)
     return frame
+
+
+def _redo_failed(cameras, heads, view, pixel_grads_of, ext_grads, acc, touched, scratch,
+                 last_excluded=False):
+    """Re-render synchronously (growing the frame buffer) and accumulate the
+    views whose asynchronous frame reported a status; True if the last view
+    failed and ``last_excluded`` (the caller redoes it: its chain rule is
+    still pending).  Other statuses raise as the reference exceptions."""
+    import torch
+
+    from . import _lib, grad
+    torch.cuda.current_stream().synchronize()
+    status = heads.view(torch.int32)[:, 0].tolist()
+    last_failed = False
+    for j, st in enumerate(status):
+        if not st:
+            continue
+        if st != _lib.HGS_ERR_PAIR_CAPACITY:
+            _lib.check(st, "hgs_forward (view %d)" % j)
+        if last_excluded and j == len(cameras) - 1:
+            last_failed = True
+            continue
+        imgs, fr = view(j, cameras[j], False, False)
+        grad.backward_device(fr, pixel_grads_of(j, imgs), *ext_grads, grads_out=acc,
+                             touched_out=touched, scratch=scratch, accumulate=True)
+    return last_failed
 
 
 def replica_checksum(tensors, group=None):

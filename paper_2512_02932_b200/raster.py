@@ -117,11 +117,34 @@ class SplatFrame:
 
     @property
     def count(self):
+        self.sync()
         return int(self.info.m)
 
     @property
     def pair_count(self):
+        self.sync()
         return int(self.info.k)
+
+    @property
+    def pending(self):
+        """True for a frame rendered with async=True whose counts are still
+        on the device."""
+        return self.info.m < 0
+
+    def sync(self):
+        """Read M, K and the status of an asynchronous frame (one stream
+        synchronisation); raises the status as the reference exception
+        (ConfigError for an exhausted pair capacity)."""
+        if self.info.m >= 0:
+            return self
+        rc = _lib.lib().hgs_frame_sync_info(_lib.ptr(self.buf), self.info,
+                                            _lib.current_stream_handle(self.buf.device))
+        if rc == _lib.HGS_ERR_PAIR_CAPACITY:
+            key = (self.info.n, self.width, self.height)
+            _pair_hint[key] = max(_pair_hint.get(key, 0), int(self.info.k * 1.25) + 1024)
+            raise ConfigError("frame pair capacity exceeded (K = %d); render again" % self.info.k)
+        _lib.check(rc, "hgs_forward")
+        return self
 
     def export(self):
         """Dict of float64 / int numpy arrays (reference SplatFrame fields)."""
@@ -279,12 +302,17 @@ def _check_camera(camera):
         raise ConfigError("image dimensions above 65535 are not supported")
 
 
-def rasterize(ds, camera, settings, flags=0, outputs=None, events=None):
+def rasterize(ds, camera, settings, flags=0, outputs=None, events=None, async_=False, frame_buf=None):
     """Device-level forward: DeviceGaussians -> (images dict, SplatFrame).
 
     ``outputs`` may pass preallocated image tensors (keys color, depth,
     transmittance, alpha, normal) to avoid per-frame allocation; ``events``
-    (5 torch.cuda.Event) are recorded at the library's stage boundaries."""
+    (5 torch.cuda.Event) are recorded at the library's stage boundaries.
+    ``async_=True``: no host round trip at all (HGS_FLAG_ASYNC; capturable in
+    a CUDA graph); the frame's counts and status are read by
+    ``SplatFrame.sync()`` (a backward can run before that).  ``frame_buf``:
+    a preallocated uint8 CUDA buffer to render into (its size sets the pair
+    capacity)."""
     import torch
     L = _lib.lib()
     _check_camera(camera)
@@ -307,15 +335,28 @@ def rasterize(ds, camera, settings, flags=0, outputs=None, events=None):
                          ("color", "depth", "transmittance", "alpha", "normal")))
     if flags & _lib.HGS_FLAG_FRAME_ONLY:
         imgs = _lib.Images(None, None, None, None, None)
+    if async_:
+        flags |= _lib.HGS_FLAG_ASYNC
     sc = _lib.scene_struct(ds)
     cam = _lib.camera_struct(camera)
     st = _lib.settings_struct(settings, flags, events)
     stream = _lib.current_stream_handle(dev)
     key = (n, W, H)
+    if async_:
+        if frame_buf is None:
+            frame_buf = torch.empty(frame_bytes(n, W, H), dtype=torch.uint8, device=dev)
+        info = _lib.FrameInfo()
+        _lib.check(L.hgs_forward(sc, cam, st, _lib.ptr(frame_buf), frame_buf.numel(), imgs, info, stream),
+                   "hgs_forward")
+        return outputs, SplatFrame(ds, camera, settings, frame_buf, info, flags)
     cap = _pair_hint.get(key, max(8 * n, 1 << 16))
     for _ in range(3):
         nbytes = L.hgs_frame_bytes(n, W, H, TILE_SIZE, cap)
-        buf = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+        if frame_buf is not None and frame_buf.numel() >= nbytes:
+            buf = frame_buf
+            nbytes = frame_buf.numel()
+        else:
+            buf = torch.empty(nbytes, dtype=torch.uint8, device=dev)
         info = _lib.FrameInfo()
         rc = L.hgs_forward(sc, cam, st, _lib.ptr(buf), nbytes, imgs, info, stream)
         if rc == _lib.HGS_ERR_PAIR_CAPACITY:
@@ -327,6 +368,14 @@ def rasterize(ds, camera, settings, flags=0, outputs=None, events=None):
             _pair_hint[key] = max(cap, int(info.k * 1.25) + 1024)
         return outputs, SplatFrame(ds, camera, settings, buf, info, flags)
     raise ConfigError("could not size the pair buffer")
+
+
+def frame_bytes(n, width, height, pairs=None):
+    """Bytes of a frame buffer for n Gaussians at width x height with room for
+    ``pairs`` tile/splat pairs (default: the capacity the last frame of this
+    size needed, with 25% headroom)."""
+    cap = pairs if pairs is not None else _pair_hint.get((n, width, height), max(8 * n, 1 << 16))
+    return int(_lib.lib().hgs_frame_bytes(n, width, height, TILE_SIZE, cap))
 
 
 def _flags(settings, naive=False, fast=False):

@@ -1,0 +1,47 @@
+"""Distribution of the backward compositor's per-visit pixel counts at config 2:
+for every (splat, 8 x 16 warp block) visit, n = the number of the block's
+pixels the splat contributes to (from the blend log).  Also the fraction of
+consecutive visits (in a warp's back-to-front order) that are pixel-disjoint
+and both small -- the candidates for sharing one evaluation pass.  Run on the
+GPU box:  python tools/visit_stats.py"""
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, ".")
+from paper_2512_02932_b200 import raster  # noqa: E402
+from paper_2512_02932_b200.core import DeviceGaussians  # noqa: E402
+from paper_2512_02932_b200.settings import RenderSettings  # noqa: E402
+from paper_2512_02932_b200.synthetic import synthetic_scene  # noqa: E402
+
+W, H = 1920, 1080
+scene, cam = synthetic_scene(1_000_000, W, H, 3, seed=0)
+ds = DeviceGaussians.from_host(scene, "cuda:0")
+imgs, fr = raster.rasterize(ds, cam, RenderSettings())
+out = raster.RenderOutput(imgs["color"], imgs["depth"], imgs["transmittance"], imgs["alpha"],
+                          imgs["normal"], fr, None)
+lg = out.blend_log
+off = torch.from_numpy(lg.offsets).cuda()
+pos = torch.from_numpy(lg.position.astype(np.int64)).cuda()
+cnt = off[1:] - off[:-1]
+pix = torch.repeat_interleave(torch.arange(W * H, device="cuda"), cnt)
+ix, iy = pix % W, pix // W
+block = (iy // 16) * ((W + 15) // 16) * 2 + (ix // 16) * 2 + ((ix % 16) >= 8).long()
+# (block, rank) visits; rank order within a block is the walk order reversed
+key = block * (1 << 24) + pos
+uk, n = torch.unique(key, return_counts=True)
+h = torch.bincount(n, minlength=129).cpu().numpy()
+tot = int(n.numel())
+print("visits", tot, "pairs", int(n.sum()), "mean n", float(n.float().mean()))
+for lo, hi in ((1, 4), (5, 8), (9, 16), (17, 32), (33, 64), (65, 128)):
+    s = int(h[lo:hi + 1].sum())
+    print("n in [%3d, %3d]: %6.2f%% of visits, %6.2f%% of pairs" % (lo, hi, 100.0 * s / tot,
+          100.0 * float((np.arange(129)[lo:hi + 1] * h[lo:hi + 1]).sum()) / float(n.sum())))
+passes = int(((n + 31) // 32).sum())
+print("passes", passes, "lanes per pass", float(n.sum()) / passes)
+# consecutive visits of one block, both n <= 16: pair candidates (ignoring disjointness)
+ub = uk // (1 << 24)
+same = ub[1:] == ub[:-1]
+small = (n[1:] <= 16) & (n[:-1] <= 16)
+print("consecutive same-block visits both n<=16: %.2f%%" % (100.0 * float((same & small).sum()) / tot))
