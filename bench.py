@@ -647,7 +647,7 @@ def main():
     last_frame.sync()  # raises if a timed frame overflowed its pair capacity (none did: same K every step)
     step_ms = float(np.mean([s_ev[i].elapsed_time(e_ev[i]) for i in range(K_)]))
     fwd_ms = float(np.mean([fs[i].elapsed_time(fe[i]) for i in range(K_)]))
-    stage_names = ["depth_keys+sort", "preprocess_f64+scan", "binning(dup+tile sort+ranges)",
+    stage_names = ["depth_keys+sort||preprocess_f64", "scan", "binning(dup+tile sort+ranges)",
                    "composite_fwd"]
     stages = {}
     for j, nm in enumerate(stage_names):
@@ -676,8 +676,10 @@ def main():
     }
     mufu = {"composite_fwd": ev3 + 2 * ev2, "composite_bwd": bev + 2 * (b3 + br + bl)}
     hbm_bytes = {
-        "depth_keys+sort": a.n * (40 + 1) + a.n * 12 * 2 * n_depth_passes,
-        "preprocess_f64+scan": M * (237 + 4 + 96 + 8),
+        # depth keys + sort passes + rank scatter, and the preprocess beside them
+        "depth_keys+sort||preprocess_f64": a.n * (40 + 2) + a.n * 12 * 2 * n_depth_passes + a.n * 12
+        + M * (237 + 96 + 96 + 32 + 8 + 4),
+        "scan": M * (8 + 8),
         "binning(dup+tile sort+ranges)": M * 104 + K * (8 + 16 * n_tile_passes + 4),
         "chain_rule(+touched)": a.n * (4 * (11 + 3 * ds.sh_bases) + 1 + 64 * a.kg
                                        + 4 * P * a.kg),
@@ -701,20 +703,20 @@ def main():
     # the limiter of the compositors is the SM issue rate, not a pipe peak:
     # quote the committed ncu capture of the same kernel (profiles/)
     ncu_file = os.path.join(REPO, "profiles", "ncu_%s_kernels.json" % NCU_TAG)
-    if dom in ("composite_fwd", "composite_bwd") and os.path.exists(ncu_file):
-        pref = "k_composite_fwd<0, 0>" if dom == "composite_fwd" else "k_composite_bwd_c<1, 0, 0, 4>"
+    # the instantiation this run launched (template <NAIVE, COUNT, PF> / <KG, EXT, DET, QP>)
+    kname = {"composite_fwd": "k_composite_fwd<0, 0, 0>",
+             "composite_bwd": "k_composite_bwd_c<%d, 0, 0, 4>" % min(a.kg, 4)}.get(dom)
+    roof["ncu_kernel"] = kname
+    roof["traffic"] = None
+    if kname and os.path.exists(ncu_file):
         for kd in json.load(open(ncu_file)):
-            if kd.get("config") == "c2" and kd.get("kernel") == pref:
+            if kd.get("config") == "c2" and kd.get("kernel") == kname:
                 roof["limiter"] = ("SM instruction issue (ncu, profiles/ncu_%s_kernels.json: issue " % NCU_TAG +
                                    "active %.0f%%, FP32 pipe %.0f%%, DRAM %.0f%%, %.1f of 32 lanes active)"
                                    % (kd.get("issue_active_pct", 0), kd.get("fma_pipe_pct", 0),
                                       kd.get("dram_pct", 0), kd.get("thread_inst_per_inst", 0)))
-    traffic_file = os.path.join(REPO, "profiles", "traffic.json")
-    roof["traffic"] = None
-    if os.path.exists(traffic_file):
-        tr = json.load(open(traffic_file))
-        if dom in tr:
-            roof["traffic"] = tr[dom]
+                # dram__bytes_read.sum + dram__bytes_write.sum of that kernel, one launch
+                roof["traffic"] = int((kd.get("dram_read_MB", 0) + kd.get("dram_write_MB", 0)) * 1e6)
     stage_roofs = {}
     for nm, t_ms in stages.items():
         if nm in flops:
@@ -724,9 +726,10 @@ def main():
             gbs = hbm_bytes[nm] / (t_ms * 1e-3) / 1e9
             stage_roofs[nm] = {"ms": t_ms, "GB/s": gbs, "hbm_frac": gbs / hbm_peak}
 
-    # init_state, depth_keys, radix_offsets, <depth passes>, rank_scatter, preprocess, scan_counts,
-    # duplicate, radix_offsets, <tile passes>, tile_ranges, composite_fwd, fixup_fwd
-    launches_fwd = 11 + n_depth_passes + n_tile_passes
+    # init_state, depth_keys, sort_plan, 8 depth passes (the constant digits' exit at once),
+    # preprocess, rank_scatter, scan_counts, duplicate, radix_offsets, <tile passes>, tile_ranges,
+    # composite_fwd, fixup_fwd
+    launches_fwd = 18 + n_tile_passes
     # init_state + (composite_bwd + fixup_bwd + chain_rule) per chunk of <= 4 gradients; under
     # N ranks the chain rule runs in N_BUCKETS Gaussian ranges (overlapped all-reduce)
     launches_bwd = 1 + 3 * ((a.kg + 3) // 4) + ((N_BUCKETS - 1) if world > 1 else 0)

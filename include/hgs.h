@@ -97,6 +97,12 @@ typedef struct hgs_settings {
                                 *          [4] composite
                                 * backward [0] start [1] composite replay
                                 *          [2] chain rule                     */
+  /* [ABI 3] nullable: an auxiliary cudaStream_t and two caller-created
+   * cudaEvent_t (fork, join).  With all three set, hgs_forward runs the
+   * float64 preprocess on aux_stream beside the depth sort and joins it on
+   * the main stream before binning (graph capture follows the fork). */
+  void *aux_stream;
+  void *aux_events[2];
 } hgs_settings;
 
 #define HGS_FLAG_NAIVE 0x1u /* render_naive: every splat for every pixel, no tiles, no bbox test (render.py:101-118) */

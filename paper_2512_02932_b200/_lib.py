@@ -76,7 +76,8 @@ class Settings(ctypes.Structure):
     _fields_ = [("background", ctypes.c_float * 3), ("tile_size", _i32),
                 ("theta_z", ctypes.c_double), ("t_z", ctypes.c_double),
                 ("lambda_z", ctypes.c_double), ("flags", ctypes.c_uint32),
-                ("n_timing_events", _i32), ("timing_events", ctypes.POINTER(_vp))]
+                ("n_timing_events", _i32), ("timing_events", ctypes.POINTER(_vp)),
+                ("aux_stream", _vp), ("aux_events", _vp * 2)]
 
 
 class Images(ctypes.Structure):
@@ -254,9 +255,31 @@ def camera_struct(cam):
                   int(cam.height), (ctypes.c_double * 16)(*w2c), float(cam.near), float(cam.far))
 
 
-def settings_struct(st, flags=0, events=None):
+_aux = {}  # device index -> (side stream, fork event, join event)
+
+
+def aux_handles(device):
+    """(cudaStream_t, (fork, join) cudaEvent_t) of this process's side stream
+    on ``device``: hgs_forward runs the float64 preprocess on it beside the
+    depth sort."""
+    import torch
+    dev = torch.device(device)
+    idx = dev.index if dev.index is not None else torch.cuda.current_device()
+    if idx not in _aux:
+        stream = torch.cuda.Stream(device=idx)
+        evs = (torch.cuda.Event(), torch.cuda.Event())
+        with torch.cuda.device(idx):
+            for e in evs:
+                e.record()  # creates the CUDA event
+        _aux[idx] = (stream, evs)
+    stream, evs = _aux[idx]
+    return stream.cuda_stream, tuple(e.cuda_event for e in evs)
+
+
+def settings_struct(st, flags=0, events=None, aux=None):
     """hgs_settings; ``events`` = list of torch.cuda.Event(enable_timing=True)
-    recorded by the library at its stage boundaries (include/hgs.h)."""
+    recorded by the library at its stage boundaries (include/hgs.h); ``aux``
+    = (side stream, (fork, join) events) from aux_handles()."""
     bg = [float(b) for b in st.background]
     if len(bg) != 3:
         raise ConfigError("background must have 3 channels")
@@ -269,6 +292,9 @@ def settings_struct(st, flags=0, events=None):
         s.n_timing_events = len(events)
         s.timing_events = ctypes.cast(arr, ctypes.POINTER(_vp))
         s._keep = arr
+    if aux is not None:
+        s.aux_stream = aux[0]
+        s.aux_events[0], s.aux_events[1] = aux[1]
     return s
 
 

@@ -14,7 +14,8 @@ namespace {
 constexpr int kMaxGrid = 148 * 8;
 
 struct Layout {
-  size_t state, hist_d, off_d, hist_p, off_p, keys_a, keys_b, vals_a, vals_b, rank, lb_sort, lb_scan, recs, recs64, cull2d, eig, pair_off,
+  size_t state, hist_d, off_d, hist_p, off_p, keys_a, keys_b, vals_a, vals_b, rank, order, counts, kept, lb_sort, lb_scan,
+      recs, recs64, cull2d, eig, pair_off,
       pk_a, pk_b, pv_a, pv_b, tile_off, pix_T, pix_last, pix_count, fwd_fix, bwd_fix, pix_mask, total;
   size_t small_end;  // [state, small_end) is zeroed at the start of a forward
   size_t lb_sort_bytes, lb_scan_bytes;
@@ -46,7 +47,10 @@ Layout make_layout(int64_t n, int W, int H, int64_t cap) {
   L.keys_b = take(nn * 8);
   L.vals_a = take(nn * 4);
   L.vals_b = take(nn * 4);
-  L.rank = take(nn * 4);  // depth rank of each Gaussian (0xffffffff: culled)
+  L.rank = take(nn * 4);   // depth rank of each Gaussian (0xffffffff: culled)
+  L.order = take(nn * 4);  // the depth order, rank -> Gaussian
+  L.counts = take(nn * 4); // tiles per Gaussian (by index; 0: culled)
+  L.kept = take(nn);       // k_depth_keys' culls, read by the preprocess
   L.recs = take(nn * sizeof(SplatRec));
   L.recs64 = take(nn * sizeof(Rec64));
   L.cull2d = take(nn * 2 * sizeof(float4));
@@ -268,12 +272,31 @@ int hgs_forward(const hgs_scene *scene, const hgs_camera *camera, const hgs_sett
   // device: no host round trip inside a frame (stream-ordered, CUDA-graph
   // capturable).  Work past the device counts exits at once.
   const int64_t sort_tiles_n = ceil_div(std::max<int64_t>(n, 1), kSortTile);
+  uint32_t *rank_of = at<uint32_t>(frame, L.rank);
+  uint32_t *order = at<uint32_t>(frame, L.order);
+  uint32_t *counts = at<uint32_t>(frame, L.counts);
+  // With an auxiliary stream (hgs_settings.aux_stream + two caller events)
+  // the float64 preprocess -- which needs only the scene and the culls --
+  // runs on it beside the depth sort, and the main stream joins it before
+  // the pair-offset scan.
+  cudaStream_t aux = static_cast<cudaStream_t>(settings->aux_stream);
+  const bool fork = aux && settings->aux_events[0] && settings->aux_events[1] && n > 0;
   // 1. depth keys + digit histograms + the pass plan
   if (n > 0) {
     HGS_CUDA(launch_depth_keys(sc, cam, at<unsigned long long>(frame, L.keys_a), at<uint32_t>(frame, L.vals_a),
-                               at<uint32_t>(frame, L.hist_d), st, grid_for(n, 256), s));
+                               at<uint8_t>(frame, L.kept), at<uint32_t>(frame, L.hist_d), st, grid_for(n, 256), s));
     k_sort_plan<<<1, kRadix, 0, s>>>(at<uint32_t>(frame, L.hist_d), n, at<uint32_t>(frame, L.off_d), st);
     HGS_LAUNCHED();
+    if (fork) {
+      HGS_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(settings->aux_events[0]), s));
+      HGS_CUDA(cudaStreamWaitEvent(aux, static_cast<cudaEvent_t>(settings->aux_events[0]), 0));
+    }
+    // 3a. float64 preprocess per Gaussian (record + tile count at its index)
+    HGS_CUDA(launch_preprocess(sc, cam, mod, at<uint8_t>(frame, L.kept), at<SplatRec>(frame, L.recs),
+                               at<Rec64>(frame, L.recs64), at<float4>(frame, L.cull2d), at<float2>(frame, L.eig),
+                               counts, fork ? aux : s));
+    HGS_LAUNCHED();
+    if (fork) HGS_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(settings->aux_events[1]), aux));
     // 2. depth sort: 8 digit passes launched, the constant ones exit at once
     uint32_t *lb = at<uint32_t>(frame, L.lb_sort);
     HGS_CUDA(cudaMemsetAsync(lb, 0, (size_t)sort_tiles_n * kRadix * 4 * 8, s));
@@ -287,22 +310,17 @@ int hgs_forward(const hgs_scene *scene, const hgs_camera *camera, const hgs_sett
           st->tile_counters + 1 + i, SortDev{&st->sort_np, st->sort_digit, i, nullptr, nullptr});
       HGS_LAUNCHED();
     }
+    k_rank_scatter<<<grid_for(n, 256), 256, 0, s>>>(at<uint32_t>(frame, L.vals_a), at<uint32_t>(frame, L.vals_b), st,
+                                                    n, rank_of, order);
+    HGS_LAUNCHED();
   }
   HGS_CUDA(record_event(settings, 1, s));
-  // 3. float64 preprocess per Gaussian (record at its depth rank) + pair-offset scan
-  uint32_t *rank_of = at<uint32_t>(frame, L.rank);
+  // 3b. pair-offset scan over the depth order (joins the preprocess)
   if (n > 0) {
+    if (fork) HGS_CUDA(cudaStreamWaitEvent(s, static_cast<cudaEvent_t>(settings->aux_events[1]), 0));
     HGS_CUDA(cudaMemsetAsync(at<char>(frame, L.lb_scan), 0, L.lb_scan_bytes, s));
-    // tile counts per rank go to the depth-key buffer (free after the sort)
-    uint32_t *counts = at<uint32_t>(frame, L.keys_a);
-    k_rank_scatter<<<grid_for(n, 256), 256, 0, s>>>(at<uint32_t>(frame, L.vals_a), at<uint32_t>(frame, L.vals_b), st,
-                                                    n, rank_of);
-    HGS_LAUNCHED();
-    HGS_CUDA(launch_preprocess(sc, cam, mod, rank_of, at<SplatRec>(frame, L.recs), at<Rec64>(frame, L.recs64),
-                               at<float4>(frame, L.cull2d), at<float2>(frame, L.eig), counts, s));
-    HGS_LAUNCHED();
     k_scan_counts<<<(unsigned)ceil_div(n, kScanTile), kScanThreads, 0, s>>>(
-        counts, -1, at<unsigned long long>(frame, L.pair_off), at<unsigned long long>(frame, L.lb_scan), st,
+        counts, order, -1, at<unsigned long long>(frame, L.pair_off), at<unsigned long long>(frame, L.lb_scan), st,
         std::min<int64_t>(cap, 0xffffffffll));
     HGS_LAUNCHED();
   }
@@ -314,8 +332,9 @@ int hgs_forward(const hgs_scene *scene, const hgs_camera *camera, const hgs_sett
   const uint32_t *tile_keys = at<uint32_t>(frame, pairs_in_b ? L.pk_b : L.pk_a);
   const int64_t sort_tiles_k = ceil_div(std::max<int64_t>(cap, 1), kSortTile);
   if (n > 0) {
-    k_duplicate<<<grid_for(n, 256), 256, 0, s>>>(at<SplatRec>(frame, L.recs), at<unsigned long long>(frame, L.pair_off),
-                                                 -1, st, cam.tiles_x, kTileShift, at<uint32_t>(frame, L.pk_a),
+    k_duplicate<<<grid_for(n, 256), 256, 0, s>>>(at<SplatRec>(frame, L.recs), order,
+                                                 at<unsigned long long>(frame, L.pair_off), -1, st, cam.tiles_x,
+                                                 kTileShift, false, at<uint32_t>(frame, L.pk_a),
                                                  at<uint32_t>(frame, L.pv_a), nd, at<uint32_t>(frame, L.hist_p));
     HGS_LAUNCHED();
     k_radix_offsets<<<nd, kRadix, 0, s>>>(at<uint32_t>(frame, L.hist_p), at<uint32_t>(frame, L.off_p));
@@ -342,7 +361,8 @@ int hgs_forward(const hgs_scene *scene, const hgs_camera *camera, const hgs_sett
   CompositeArgs a;
   a.recs = at<SplatRec>(frame, L.recs);
   a.tile_off = at<uint32_t>(frame, L.tile_off);
-  a.tile_vals = tile_vals;
+  a.tile_vals = (settings->flags & HGS_FLAG_NAIVE) ? order : tile_vals;
+  a.rank_of = rank_of;
   a.m = -1;  // M lives in the frame state
   a.tiles_x = cam.tiles_x; a.width = W; a.height = H;
   a.flags = settings->flags;
@@ -387,7 +407,8 @@ static CompositeArgs composite_args_for(const hgs_scene *scene, const hgs_camera
   memset(&a, 0, sizeof(a));
   a.recs = at<SplatRec>(fr, L.recs);
   a.tile_off = at<uint32_t>(fr, L.tile_off);
-  a.tile_vals = at<uint32_t>(fr, info->internal[0] ? L.pv_b : L.pv_a);
+  a.tile_vals = at<uint32_t>(fr, (info->flags & HGS_FLAG_NAIVE) ? L.order : (info->internal[0] ? L.pv_b : L.pv_a));
+  a.rank_of = at<uint32_t>(fr, L.rank);
   a.m = info->m;
   a.tiles_x = info->tiles_x; a.width = info->width; a.height = info->height;
   a.flags = info->flags;
@@ -664,10 +685,10 @@ int hgs_exchange_f64(int64_t n, double *log_scale, double *rotation, uint8_t *ty
 
 namespace hgs {
 
-__global__ void k_export_frame(SceneView sc, CamD cam, ModD mod, const SplatRec *__restrict__ recs, int64_t m,
+__global__ void k_export_frame(SceneView sc, CamD cam, ModD mod, const uint32_t *__restrict__ order, int64_t m,
                                hgs_frame_export o) {
   for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < m; r += (int64_t)gridDim.x * blockDim.x) {
-    const uint32_t i = __float_as_uint(recs[r].r4.w) & 0x7fffffffu;
+    const uint32_t i = order[r];
     ProjD p;
     if (sc.center64) project_d<true, false, true>(sc, i, cam, mod, p);
     else project_d(sc, i, cam, mod, p);
@@ -697,6 +718,13 @@ __global__ void k_export_frame(SceneView sc, CamD cam, ModD mod, const SplatRec 
   }
 }
 
+// Tile lists hold Gaussian indices; SplatFrame.tile_ids holds slots.
+__global__ void k_export_slots(const uint32_t *__restrict__ vals, const uint32_t *__restrict__ rank_of, int64_t k,
+                               int32_t *__restrict__ out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < k; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = (int32_t)rank_of[vals[i]];
+}
+
 __global__ void k_export_u32_to_i64(const uint32_t *__restrict__ src, int64_t *__restrict__ dst, int64_t n) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     dst[i] = src[i];
@@ -715,7 +743,7 @@ __global__ void k_blend_log(CompositeArgs a, const int64_t *__restrict__ offsets
     const int64_t end = lo + a.pix_last[pix];
     int64_t o = offsets[pix];
     for (int64_t j = lo; j < end; ++j) {
-      const uint32_t rk = naive ? (uint32_t)j : a.tile_vals[j];
+      const uint32_t rk = a.tile_vals[j];  // NAIVE: the depth order
       const SplatRec r = a.recs[rk];
       if (!naive) {
         const int4 q = r.r5;
@@ -725,7 +753,7 @@ __global__ void k_blend_log(CompositeArgs a, const int64_t *__restrict__ offsets
       }
       PairEval p;
       if (!eval_pair<true>(r, a.recs + rk, ix, iy, a.flags, a.st, p)) continue;
-      pos[o] = (int32_t)rk;
+      pos[o] = (int32_t)a.rank_of[rk];  // the SplatFrame slot
       alpha[o] = p.at;
       if (rec_is3d(r)) {
         u[o] = p.u;
@@ -762,8 +790,9 @@ int hgs_frame_export_arrays(const hgs_scene *scene, const hgs_camera *camera, co
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const CompositeArgs a = composite_args_for(scene, camera, settings, frame, info);
   if (info->m > 0) {
+    const Layout FL = make_layout(info->n, info->width, info->height, info->pair_capacity);
     k_export_frame<<<grid_for(info->m, 128), 128, 0, s>>>(make_scene(*scene), make_cam(*camera),
-        ModD{settings->theta_z, settings->t_z, settings->lambda_z}, a.recs, info->m, *out);
+        ModD{settings->theta_z, settings->t_z, settings->lambda_z}, at<uint32_t>(frame, FL.order), info->m, *out);
     HGS_LAUNCHED();
   }
   if (out->tile_offsets) {
@@ -771,8 +800,10 @@ int hgs_frame_export_arrays(const hgs_scene *scene, const hgs_camera *camera, co
                                                                         info->n_tiles + 1);
     HGS_LAUNCHED();
   }
-  if (out->tile_ids && info->k > 0)
-    HGS_CUDA(cudaMemcpyAsync(out->tile_ids, a.tile_vals, (size_t)info->k * 4, cudaMemcpyDeviceToDevice, s));
+  if (out->tile_ids && info->k > 0 && !(info->flags & HGS_FLAG_NAIVE)) {
+    k_export_slots<<<grid_for(info->k, 256), 256, 0, s>>>(a.tile_vals, a.rank_of, info->k, out->tile_ids);
+    HGS_LAUNCHED();
+  }
   if (out->pixel_count) {
     if (info->flags & HGS_FLAG_NAIVE) {
       HGS_CUDA(cudaMemcpyAsync(out->pixel_count, a.pix_count, (size_t)info->width * info->height * 4,
@@ -878,6 +909,7 @@ int hgs_frame_tile_bins(const void *frame, const hgs_frame_info *info, int32_t t
   if (scratch_bytes < R.total) return HGS_ERR_CONFIG;
   const Layout L = make_layout(info->n, W, H, info->pair_capacity);
   const SplatRec *recs = at<SplatRec>(frame, L.recs);
+  const uint32_t *order = at<uint32_t>(frame, L.order);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int tiles_x = (int)ceil_div(W, tile_size);
   const int64_t n_tiles = (int64_t)tiles_x * ceil_div(H, tile_size);
@@ -886,10 +918,10 @@ int hgs_frame_tile_bins(const void *frame, const hgs_frame_info *info, int32_t t
   int64_t K = 0;
   if (m > 0) {
     HGS_CUDA(cudaMemsetAsync(at<char>(scratch, R.lb_scan), 0, (size_t)ceil_div(m, kScanTile) * 8, s));
-    k_rebin_counts<<<grid_for(m, 256), 256, 0, s>>>(recs, m, sh, at<uint32_t>(scratch, R.counts));
+    k_rebin_counts<<<grid_for(m, 256), 256, 0, s>>>(recs, order, m, sh, at<uint32_t>(scratch, R.counts));
     HGS_LAUNCHED();
     k_scan_counts<<<(unsigned)ceil_div(m, kScanTile), kScanThreads, 0, s>>>(
-        at<uint32_t>(scratch, R.counts), m, at<unsigned long long>(scratch, R.pair_off),
+        at<uint32_t>(scratch, R.counts), nullptr, m, at<unsigned long long>(scratch, R.pair_off),
         at<unsigned long long>(scratch, R.lb_scan), st, -1);
     HGS_LAUNCHED();
     unsigned long long kt;
@@ -903,8 +935,8 @@ int hgs_frame_tile_bins(const void *frame, const hgs_frame_info *info, int32_t t
   if (K > 0) {
     const int nd = n_tiles > kRadix ? 2 : 1;
     if (n_tiles > (1 << 16)) return HGS_ERR_CONFIG;  // 2 digit passes cover 65536 tiles
-    k_duplicate<<<grid_for(m, 256), 256, 0, s>>>(recs, at<unsigned long long>(scratch, R.pair_off), m, nullptr,
-                                                 tiles_x, sh,
+    k_duplicate<<<grid_for(m, 256), 256, 0, s>>>(recs, order, at<unsigned long long>(scratch, R.pair_off), m, nullptr,
+                                                 tiles_x, sh, true,
                                                  at<uint32_t>(scratch, R.ka), at<uint32_t>(scratch, R.va),
                                                  nd, at<uint32_t>(scratch, R.hist));
     HGS_LAUNCHED();

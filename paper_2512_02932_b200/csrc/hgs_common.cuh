@@ -203,6 +203,14 @@ __device__ __forceinline__ void cov2d_3d(const CamD &cam, const double *t, const
   c = s11 + kDilation;
 }
 
+// det of the dilated 2D covariance, a c - b^2 with both products rounded
+// (numpy's order, project.py:223): the singular-conic cull is decided by
+// this one expression in k_depth_keys (the depth order / M) and in the
+// preprocess (records / tile counts), so the two can never disagree.
+__device__ __forceinline__ double conic_det(double a, double b, double c) {
+  return __dsub_rn(__dmul_rn(a, c), __dmul_rn(b, b));
+}
+
 // Full float64 projection of one Gaussian: everything SplatFrame holds
 // (project.py:169-326) plus the extension normal.
 struct ProjD {
@@ -251,7 +259,7 @@ __device__ __forceinline__ void project_d(const SceneView &sc, int64_t i, const 
   if (o.typ == 1) {
     double a, b, c;
     cov2d_3d(cam, o.t, R, s, a, b, c);
-    double det = a * c - b * b;
+    double det = conic_det(a, b, c);
     bool ok = det > 1e-18;
     double inv = ok ? 1.0 / det : 0.0;
     o.cov[0] = a; o.cov[1] = b; o.cov[2] = c;

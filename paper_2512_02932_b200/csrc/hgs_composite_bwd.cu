@@ -214,7 +214,7 @@ __global__ void __launch_bounds__(128, KG == 1 ? 5 : 4) k_composite_bwd_naive(Bw
 #pragma unroll
     for (int q = 0; q < PPL; ++q) pm[q] = 0u;
     if (j < top) {
-      const SplatRec *g = a.recs + j;
+      const SplatRec *g = a.recs + a.tile_vals[j];  // NAIVE: tile_vals = the depth order
 #pragma unroll
       for (int q = 0; q < PPL; ++q) pm[q] = 0xffffffffu;
       any_pm = 0xffffffffu;
@@ -398,6 +398,10 @@ constexpr size_t cstate_bytes() {
 template <int KG, bool EXT, bool DET, int QP>
 __global__ void __launch_bounds__(256 / QP, HGS_BWDC_MINB(KG, EXT, QP)) k_composite_bwd_c(BwdArgs b) {
   constexpr int NW = 8 / QP;  // warps per tile
+  // warp block: 8 x (4 QP) pixels, or the whole 16 x 16 tile at QP = 8;
+  // pixel p = lane + 32 q of the block is (p % BW, p / BW)
+  constexpr int BW = QP == 8 ? 16 : 8;
+  constexpr int BSH = QP == 8 ? 4 : 3;
   const CompositeArgs &a = b.c;
   if (a.st->status) return;  // failed frame
   __shared__ SplatRec s_rec[NW][32];
@@ -407,7 +411,7 @@ __global__ void __launch_bounds__(256 / QP, HGS_BWDC_MINB(KG, EXT, QP)) k_compos
   const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   CState<KG, EXT, QP> &cs = *reinterpret_cast<CState<KG, EXT, QP> *>(s_dyn + warp * cstate_bytes<KG, EXT, QP>());
-  const int wx0 = tx * kTile + (warp & 1) * 8, wy0 = ty * kTile + (warp >> 1) * 4 * QP;
+  const int wx0 = tx * kTile + (QP == 8 ? 0 : (warp & 1) * 8), wy0 = ty * kTile + (QP == 8 ? 0 : (warp >> 1) * 4 * QP);
   const uint32_t lo = a.tile_off[tile];
   const int64_t HW = (int64_t)a.width * a.height;
   uint32_t last[QP], mw[QP];
@@ -416,7 +420,7 @@ __global__ void __launch_bounds__(256 / QP, HGS_BWDC_MINB(KG, EXT, QP)) k_compos
 #pragma unroll
   for (int q = 0; q < QP; ++q) {
     const int p = lane + 32 * q;
-    const int ix = wx0 + (lane & 7), iy = wy0 + (lane >> 3) + 4 * q;
+    const int ix = wx0 + (p & (BW - 1)), iy = wy0 + (p >> BSH);
     const bool inside = ix < a.width && iy < a.height;
     const int64_t pix = (int64_t)iy * a.width + ix;
     last[q] = inside ? a.pix_last[pix] : 0u;
@@ -537,12 +541,13 @@ __global__ void __launch_bounds__(256 / QP, HGS_BWDC_MINB(KG, EXT, QP)) k_compos
         bool amb = false;
         if (act) {
           const int p = cs.list[i0 + lane];
-          const int ix = wx0 + (p & 7), iy = wy0 + (p >> 3);
+          const int ix = wx0 + (p & (BW - 1)), iy = wy0 + (p >> BSH);
           const float4 A = cs.a[p];
           PairEval pe;
           if (count) ++n_ev;
           const int c = HGS_STAGED_ORIGIN
-                            ? eval_fast<true, true, true>(r, ix, iy, a.flags, pe, (float)(p & 7), (float)(p >> 3))
+                            ? eval_fast<true, true, true>(r, ix, iy, a.flags, pe, (float)(p & (BW - 1)),
+                                                          (float)(p >> BSH))
                             : eval_fast<true, true>(r, ix, iy, a.flags, pe);
           if (c == kAmbiguous) {
             const float4 E = EXT ? cs.e[p] : make_float4(0.f, 0.f, 0.f, 0.f);
@@ -706,12 +711,12 @@ __global__ void __launch_bounds__(256, HGS_FIXUP_MINB) k_fixup_bwd(BwdArgs b) {
     Suffix S{f.S0, f.S1, f.S2, f.SD, f.SN0, f.SN1, f.SN2};
     // software pipeline: next window's ranks loaded, records prefetched into L2
     const int64_t e0 = (int64_t)f.entry - lane;
-    uint32_t rk_next = e0 >= (int64_t)lo ? (naive ? (uint32_t)e0 : a.tile_vals[e0]) : 0u;
+    uint32_t rk_next = e0 >= (int64_t)lo ? a.tile_vals[e0] : 0u;  // NAIVE: the depth order
     for (int64_t top = (int64_t)f.entry + 1; top > (int64_t)lo; top -= 32) {
       const int64_t e = top - 1 - lane;
       const uint32_t rk_cur = rk_next;
       if (e - 32 >= (int64_t)lo) {
-        rk_next = naive ? (uint32_t)(e - 32) : a.tile_vals[e - 32];
+        rk_next = a.tile_vals[e - 32];
         prefetch_rec(a.recs + rk_next);
       }
       bool con = false;

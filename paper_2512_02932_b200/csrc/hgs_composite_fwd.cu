@@ -161,7 +161,7 @@ __global__ void __launch_bounds__(kBlock, HGS_FWD_MINB) k_composite_fwd(Composit
       }
       buf ^= 1u;
     } else if (j < hi) {
-      const uint32_t rk = NAIVE ? j : __ldg(a.tile_vals + j);
+      const uint32_t rk = __ldg(a.tile_vals + j);  // NAIVE: the depth order
       const SplatRec *g = a.recs + rk;
       const int4 q = __ldg(&g->r5);
       pm = NAIVE ? 0xffffffffu : pixel_mask(q, wx0, wy0);  // a rectangle: the culls rely on it
@@ -392,7 +392,7 @@ __global__ void __launch_bounds__(256, HGS_FIXUP_MINB) k_fixup_fwd(CompositeArgs
         at[i] = 0.f;
         rks[i] = 0u;
         if (e >= start && e < hi) {
-          const uint32_t rk = naive ? e : a.tile_vals[e];
+          const uint32_t rk = a.tile_vals[e];  // NAIVE: the depth order
           rks[i] = rk;
           const SplatRec r = a.recs[rk];
           if (naive || in_bbox(r.r5, ix, iy)) {

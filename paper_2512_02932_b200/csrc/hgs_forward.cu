@@ -4,6 +4,9 @@
 // raster/_blend_py.py:55-123 (paths relative to the reference package).
 #include "hgs_kernels.cuh"
 
+#ifndef HGS_PRE_CTAS
+#define HGS_PRE_CTAS 12  // A/B 8 / 12 / 24 / 48: 12 leaves room for the depth sort beside it
+#endif
 #ifndef HGS_PRE_PREFETCH
 #define HGS_PRE_PREFETCH 1
 #endif
@@ -54,8 +57,8 @@ __device__ __forceinline__ void write_rec64(const ProjD &o, Rec64 *q) {
 // are not counted in M).  Also accumulates the 8 digit histograms.
 template <bool G64>
 __global__ void __launch_bounds__(256) k_depth_keys(SceneView sc, CamD cam, unsigned long long *__restrict__ keys,
-                                                    uint32_t *__restrict__ vals, uint32_t *__restrict__ hist,
-                                                    FrameState *__restrict__ st) {
+                                                    uint32_t *__restrict__ vals, uint8_t *__restrict__ kept,
+                                                    uint32_t *__restrict__ hist, FrameState *__restrict__ st) {
   using G = SceneGeom<G64>;
   __shared__ uint32_t sh[8 * kRadix];
   __shared__ uint32_t s_m;
@@ -79,12 +82,13 @@ __global__ void __launch_bounds__(256) k_depth_keys(SceneView sc, CamD cam, unsi
         double s[3] = {exp(G::log_scale(sc, i, 0)), exp(G::log_scale(sc, i, 1)), exp(G::log_scale(sc, i, 2))};
         double a, b, c;
         cov2d_3d(cam, t, R, s, a, b, c);
-        keep = (a * c - b * b) > 1e-18;
+        keep = conic_det(a, b, c) > 1e-18;
       }
     }
     unsigned long long k = keep ? (unsigned long long)__double_as_longlong(t[2]) : ~0ull;
     keys[i] = k;
     vals[i] = (uint32_t)i;
+    kept[i] = keep ? 1 : 0;  // the preprocess (beside the sort) skips exactly these
     if (keep) atomicAdd(&s_m, 1u);
 #pragma unroll
     for (int pss = 0; pss < 8; ++pss) atomicAdd(&sh[pss * kRadix + digit_of(k, pss * 8)], 1u);
@@ -96,9 +100,9 @@ __global__ void __launch_bounds__(256) k_depth_keys(SceneView sc, CamD cam, unsi
   if (threadIdx.x == 0 && s_m) atomicAdd(&st->m_count, s_m);
 }
 cudaError_t launch_depth_keys(const SceneView &sc, const CamD &cam, unsigned long long *keys, uint32_t *vals,
-                              uint32_t *hist, FrameState *st, int grid, cudaStream_t s) {
-  if (sc.center64) k_depth_keys<true><<<grid, 256, 0, s>>>(sc, cam, keys, vals, hist, st);
-  else k_depth_keys<false><<<grid, 256, 0, s>>>(sc, cam, keys, vals, hist, st);
+                              uint8_t *kept, uint32_t *hist, FrameState *st, int grid, cudaStream_t s) {
+  if (sc.center64) k_depth_keys<true><<<grid, 256, 0, s>>>(sc, cam, keys, vals, kept, hist, st);
+  else k_depth_keys<false><<<grid, 256, 0, s>>>(sc, cam, keys, vals, kept, hist, st);
   return cudaGetLastError();
 }
 
@@ -190,11 +194,15 @@ __device__ __forceinline__ void write_record(const ProjD &o, uint32_t idx, int W
 // (sort_np & 1) of the ping-pong pair; M = the near-culled count, both from
 // the frame state (no host round trip).
 __global__ void k_rank_scatter(const uint32_t *__restrict__ vals_a, const uint32_t *__restrict__ vals_b,
-                               const FrameState *__restrict__ st, int64_t n, uint32_t *__restrict__ rank_of) {
+                               const FrameState *__restrict__ st, int64_t n, uint32_t *__restrict__ rank_of,
+                               uint32_t *__restrict__ order) {
   const uint32_t *sorted_idx = (st->sort_np & 1u) ? vals_b : vals_a;
   const int64_t m = st->m_count;
-  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x)
-    rank_of[sorted_idx[r]] = r < m ? (uint32_t)r : 0xffffffffu;
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t g = sorted_idx[r];
+    rank_of[g] = r < m ? (uint32_t)r : 0xffffffffu;
+    order[r] = g;  // the depth order in a fixed buffer (rank -> Gaussian)
+  }
 }
 
 // Depth-sort plan from the fused digit histograms (k_depth_keys): per digit
@@ -233,10 +241,11 @@ __global__ void k_sort_plan(const uint32_t *__restrict__ hist, int64_t n, uint32
 // Gaussians per warp step: the SH rows (3B floats each) are staged through
 // shared memory as one coalesced segment (per-thread strided rows were
 // LSU-throttled); float64 projection; record + tile count written at the
-// Gaussian's depth rank.
+// Gaussian's index.  Independent of the depth sort (it runs beside it); the
+// culls are k_depth_keys' (kept[]), a culled Gaussian gets count 0.
 template <int B, bool G64>
 __global__ void __launch_bounds__(32, HGS_PRE_MINB) k_preprocess(SceneView sc, CamD cam, ModD mod,
-                                                   const uint32_t *__restrict__ rank_of,
+                                                   const uint8_t *__restrict__ kept,
                                                    SplatRec *__restrict__ recs, Rec64 *__restrict__ recs64,
                                                    float4 *__restrict__ cull2d, float2 *__restrict__ eig,
                                                    uint32_t *__restrict__ counts) {
@@ -273,7 +282,6 @@ __global__ void __launch_bounds__(32, HGS_PRE_MINB) k_preprocess(SceneView sc, C
         else if (lane < 10) ptr = reinterpret_cast<const char *>(sc.rotation + 4 * nb) + 128 * (lane - 6);
         else if (lane == 10) ptr = reinterpret_cast<const char *>(sc.opacity_logit + nb);
         else if (lane == 11) ptr = reinterpret_cast<const char *>(sc.type_spec + nb);
-        else if (lane == 12) ptr = reinterpret_cast<const char *>(rank_of + nb);
         if (ptr) asm volatile("prefetch.global.L1 [%0];" ::"l"(ptr));
       }
 #endif
@@ -297,25 +305,31 @@ __global__ void __launch_bounds__(32, HGS_PRE_MINB) k_preprocess(SceneView sc, C
 #endif
     const int64_t i = base + lane;
     if (lane >= cnt) continue;
-    const uint32_t r = rank_of[i];
-    if (r == 0xffffffffu) continue;
+    // the culls k_depth_keys decided: z <= near (project.py:182), |q| <= 1e-8, singular 3D conic (:225)
+    if (!kept[i]) {
+      counts[i] = 0u;
+      continue;
+    }
     ProjD o;
     project_d<false, false, G64>(sc, i, cam, mod, o, s_sh + lane * SS);
     bbox_d(o, cam.width, cam.height);
-    write_record(o, (uint32_t)i, cam.width, cam.height, recs + r, cull2d + 2 * (size_t)r, eig + i);
-    write_rec64(o, recs64 + r);
-    counts[r] = tile_count_of(o.bbox);
+    write_record(o, (uint32_t)i, cam.width, cam.height, recs + i, cull2d + 2 * (size_t)i, eig + i);
+    write_rec64(o, recs64 + i);
+    counts[i] = tile_count_of(o.bbox);
   }
 }
 // Host launcher (the template is launched from this translation unit).
-cudaError_t launch_preprocess(const SceneView &sc, const CamD &cam, const ModD &mod, const uint32_t *rank_of,
+cudaError_t launch_preprocess(const SceneView &sc, const CamD &cam, const ModD &mod, const uint8_t *kept,
                               SplatRec *recs, Rec64 *recs64, float4 *cull2d, float2 *eig, uint32_t *counts,
                               cudaStream_t s) {
   const int64_t nb = (sc.n + 31) / 32;
-  const int g = (int)(nb < 1 ? 1 : (nb > 148 * 48 ? 148 * 48 : nb));  // one warp per CTA
+  // one warp per CTA; HGS_PRE_CTAS CTAs per SM at most (grid-stride): fewer
+  // than fit leaves registers for the depth sort running beside it
+  const int64_t cap = 148LL * HGS_PRE_CTAS;
+  const int g = (int)(nb < 1 ? 1 : (nb > cap ? cap : nb));
 #define HGS_PRE(B_)                                                                                \
-  (sc.center64 ? k_preprocess<B_, true><<<g, 32, 0, s>>>(sc, cam, mod, rank_of, recs, recs64, cull2d, eig, counts) \
-               : k_preprocess<B_, false><<<g, 32, 0, s>>>(sc, cam, mod, rank_of, recs, recs64, cull2d, eig, counts))
+  (sc.center64 ? k_preprocess<B_, true><<<g, 32, 0, s>>>(sc, cam, mod, kept, recs, recs64, cull2d, eig, counts) \
+               : k_preprocess<B_, false><<<g, 32, 0, s>>>(sc, cam, mod, kept, recs, recs64, cull2d, eig, counts))
   switch (sc.sh_bases) {
     case 1: HGS_PRE(1); break;
     case 4: HGS_PRE(4); break;
@@ -330,7 +344,8 @@ cudaError_t launch_preprocess(const SceneView &sc, const CamD &cam, const ModD &
 // look-back, kScanItems counts per thread); the last tile writes K.
 // m < 0: M from the frame state.  cap >= 0: a total above it sets the
 // frame's status to HGS_ERR_PAIR_CAPACITY (the pair buffer is too small).
-__global__ void __launch_bounds__(kScanThreads) k_scan_counts(const uint32_t *__restrict__ counts, int64_t m,
+__global__ void __launch_bounds__(kScanThreads) k_scan_counts(const uint32_t *__restrict__ counts,
+                                                              const uint32_t *__restrict__ order, int64_t m,
                                                               unsigned long long *__restrict__ pair_off,
                                                               unsigned long long *__restrict__ scan_lb,
                                                               FrameState *__restrict__ st, int64_t cap) {
@@ -347,7 +362,7 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_counts(const uint32_t *__
   unsigned long long sum = 0;
 #pragma unroll
   for (int k = 0; k < kScanItems; ++k) {
-    c[k] = base + k < m ? counts[base + k] : 0u;
+    c[k] = base + k < m ? counts[order ? order[base + k] : base + k] : 0u;  // order: counts by Gaussian
     sum += c[k];
   }
   unsigned long long total;
@@ -375,11 +390,15 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_counts(const uint32_t *__
 // kernel's whole duration).
 constexpr int kDupOwn = 32;
 
+// order: rank -> Gaussian (records are by Gaussian); the pair value is the
+// Gaussian index, or the rank with emit_rank (the SplatFrame export's slots).
 __global__ void __launch_bounds__(256) k_duplicate(const SplatRec *__restrict__ recs,
+                                                   const uint32_t *__restrict__ order,
                                                    const unsigned long long *__restrict__ pair_off, int64_t m,
                                                    const FrameState *__restrict__ st, int tiles_x, int tile_shift,
-                                                   uint32_t *__restrict__ pkeys, uint32_t *__restrict__ pvals,
-                                                   int n_digits, uint32_t *__restrict__ hist) {
+                                                   bool emit_rank, uint32_t *__restrict__ pkeys,
+                                                   uint32_t *__restrict__ pvals, int n_digits,
+                                                   uint32_t *__restrict__ hist) {
   __shared__ uint32_t sh[2 * kRadix];
   if (m < 0) {  // M and the capacity verdict from the frame state
     if (st->status) return;
@@ -401,8 +420,11 @@ __global__ void __launch_bounds__(256) k_duplicate(const SplatRec *__restrict__ 
     int tx0 = 0, ty0 = 0, bw = 1;
     uint32_t cnt = 0;
     unsigned long long o = 0;
+    uint32_t val = 0;
     if (r < m) {
-      const int4 q = recs[r].r5;
+      const uint32_t g = order[r];
+      val = emit_rank ? (uint32_t)r : g;
+      const int4 q = recs[g].r5;
       const int x0 = q.x & 0xffff, y0 = (int)((uint32_t)q.x >> 16), x1 = q.y & 0xffff, y1 = (int)((uint32_t)q.y >> 16);
       if (x1 >= x0) {
         tx0 = x0 >> tile_shift; ty0 = y0 >> tile_shift;
@@ -413,7 +435,7 @@ __global__ void __launch_bounds__(256) k_duplicate(const SplatRec *__restrict__ 
     }
     if (cnt <= (uint32_t)kDupOwn) {
       for (uint32_t j = 0, dy = 0, dx = 0; j < cnt; ++j) {  // row-major over the tile rectangle
-        emit((uint32_t)((ty0 + (int)dy) * tiles_x + tx0 + (int)dx), o + j, (uint32_t)r);
+        emit((uint32_t)((ty0 + (int)dy) * tiles_x + tx0 + (int)dx), o + j, val);
         if (++dx == (uint32_t)bw) { dx = 0; ++dy; }
       }
     }
@@ -425,9 +447,10 @@ __global__ void __launch_bounds__(256) k_duplicate(const SplatRec *__restrict__ 
       const unsigned long long ob = __shfl_sync(0xffffffffu, o, l);
       const int bx = __shfl_sync(0xffffffffu, tx0, l), by = __shfl_sync(0xffffffffu, ty0, l);
       const int w = __shfl_sync(0xffffffffu, bw, l);
+      const uint32_t v = __shfl_sync(0xffffffffu, val, l);
       for (uint32_t j = lane; j < c; j += 32) {
         const uint32_t dy = j / (uint32_t)w, dx = j - dy * (uint32_t)w;
-        emit((uint32_t)((by + (int)dy) * tiles_x + bx + (int)dx), ob + j, (uint32_t)(r0 + l));
+        emit((uint32_t)((by + (int)dy) * tiles_x + bx + (int)dx), ob + j, v);
       }
     }
   }
@@ -438,10 +461,11 @@ __global__ void __launch_bounds__(256) k_duplicate(const SplatRec *__restrict__ 
 
 // Tiles per splat at another tile size (2^tile_shift px; SplatFrame export at
 // settings.tile_size != 16, project.py:329-343).
-__global__ void __launch_bounds__(256) k_rebin_counts(const SplatRec *__restrict__ recs, int64_t m, int tile_shift,
+__global__ void __launch_bounds__(256) k_rebin_counts(const SplatRec *__restrict__ recs,
+                                                      const uint32_t *__restrict__ order, int64_t m, int tile_shift,
                                                       uint32_t *__restrict__ counts) {
   for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < m; r += (int64_t)gridDim.x * blockDim.x) {
-    const int4 q = recs[r].r5;
+    const int4 q = recs[order[r]].r5;
     const int x0 = q.x & 0xffff, y0 = (int)((uint32_t)q.x >> 16), x1 = q.y & 0xffff, y1 = (int)((uint32_t)q.y >> 16);
     counts[r] = x1 >= x0 ? (uint32_t)(((x1 >> tile_shift) - (x0 >> tile_shift) + 1) *
                                       ((y1 >> tile_shift) - (y0 >> tile_shift) + 1))

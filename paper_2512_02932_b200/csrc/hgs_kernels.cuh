@@ -32,7 +32,7 @@ struct FrameState {
   SceneView sc;
   CamD cam;
   ModD mod;
-  const SplatRec *recs;  // float32 records (rank order) ...
+  const SplatRec *recs;  // float32 records (by Gaussian index) ...
   const Rec64 *recs64;   // ... and their float64 counterparts
 };
 
@@ -59,10 +59,14 @@ struct BwdFix {       // resume the backward replay of one pixel, going down
 static_assert(sizeof(BwdFix) == 64, "BwdFix is 64 B");
 
 struct CompositeArgs {
-  // binning
+  // binning.  Records are stored by Gaussian index (the preprocess runs
+  // before / beside the depth sort); tile_vals holds Gaussian indices, each
+  // tile list in depth order.  NAIVE: tile_vals = the depth order itself
+  // (rank -> Gaussian), lo = 0, hi = M.
   const SplatRec *recs;
   const uint32_t *tile_off;
   const uint32_t *tile_vals;
+  const uint32_t *rank_of;  // Gaussian -> depth rank (SplatFrame slot)
   int64_t m;
   int tiles_x, width, height;
   uint32_t flags;
@@ -78,7 +82,7 @@ struct CompositeArgs {
   // bit e of word mask_word(lo, tile, c) * 256 + pixel-in-tile is set iff
   // tile-list entry lo + 32 c + e contributed to the pixel (not NAIVE)
   uint32_t *pix_mask;
-  const float4 *cull2d;  // per rank, 2 x float4: cull2d_prep of 2D splats
+  const float4 *cull2d;  // per Gaussian, 2 x float4: cull2d_prep of 2D splats
 };
 
 // L2 prefetch of one splat record (96 B: at most two 128-B lines).
@@ -580,7 +584,7 @@ static __device__ __noinline__ bool replay_T_below(const SplatRec *recs, const u
     for (int i = 0; i < E; ++i) {
       const uint32_t j = base + (uint32_t)(32 * i + lane);
       if (j <= upto) {
-        const uint32_t rk = naive ? j : tile_vals[j];
+        const uint32_t rk = tile_vals[j];  // NAIVE: the depth order
         const SplatRec *g = recs + rk;
         if (naive || in_bbox(__ldg(&g->r5), ix, iy)) {
           double at64;
@@ -652,18 +656,19 @@ struct ExchangeState {
 __global__ void k_init_state(SceneView sc, CamD cam, ModD mod, const SplatRec *recs, const Rec64 *recs64,
                              FrameState *st);
 cudaError_t launch_depth_keys(const SceneView &sc, const CamD &cam, unsigned long long *keys, uint32_t *vals,
-                              uint32_t *hist, FrameState *st, int grid, cudaStream_t s);
+                              uint8_t *kept, uint32_t *hist, FrameState *st, int grid, cudaStream_t s);
 __global__ void k_rank_scatter(const uint32_t *vals_a, const uint32_t *vals_b, const FrameState *st, int64_t n,
-                               uint32_t *rank_of);
-cudaError_t launch_preprocess(const SceneView &sc, const CamD &cam, const ModD &mod, const uint32_t *rank_of,
+                               uint32_t *rank_of, uint32_t *order);
+cudaError_t launch_preprocess(const SceneView &sc, const CamD &cam, const ModD &mod, const uint8_t *kept,
                               SplatRec *recs, Rec64 *recs64, float4 *cull2d, float2 *eig, uint32_t *counts,
                               cudaStream_t s);
-__global__ void k_scan_counts(const uint32_t *counts, int64_t m, unsigned long long *pair_off,
+__global__ void k_scan_counts(const uint32_t *counts, const uint32_t *order, int64_t m, unsigned long long *pair_off,
                               unsigned long long *scan_lb, FrameState *st, int64_t cap);
-__global__ void k_rebin_counts(const SplatRec *recs, int64_t m, int tile_shift, uint32_t *counts);
-__global__ void k_duplicate(const SplatRec *recs, const unsigned long long *pair_off, int64_t m, const FrameState *st,
-                            int tiles_x, int tile_shift, uint32_t *pkeys, uint32_t *pvals, int n_digits,
-                            uint32_t *hist);
+__global__ void k_rebin_counts(const SplatRec *recs, const uint32_t *order, int64_t m, int tile_shift,
+                               uint32_t *counts);
+__global__ void k_duplicate(const SplatRec *recs, const uint32_t *order, const unsigned long long *pair_off, int64_t m,
+                            const FrameState *st, int tiles_x, int tile_shift, bool emit_rank, uint32_t *pkeys,
+                            uint32_t *pvals, int n_digits, uint32_t *hist);
 __global__ void k_tile_ranges(const uint32_t *skeys, int64_t k, const FrameState *st, int64_t n_tiles,
                               uint32_t *tile_off);
 __global__ void k_sort_plan(const uint32_t *hist, int64_t n, uint32_t *offsets, FrameState *st);

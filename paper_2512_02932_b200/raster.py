@@ -10,6 +10,7 @@ GPU as torch tensors).  There is no CPU backend.
 """
 
 import ctypes
+import os
 from dataclasses import dataclass
 from typing import Optional
 
@@ -31,7 +32,8 @@ __all__ = ["ALPHA_CLAMP", "DegenerateIntersection", "EARLY_STOP_T", "LOWPASS_SIG
            "HAVE_EXT", "BlendLog", "RenderOutput", "active_backend", "render",
            "render_naive", "scene_fingerprint"]
 
-TILE_SIZES = (8, 16, 32, 64)  # RenderSettings.tile_size values SplatFrame can export
+TILE_SIZES = (8, 16, 32, 64)
+_OVERLAP = os.environ.get("HGS_OVERLAP", "1") != "0"  # A/B switch of the preprocess side stream  # RenderSettings.tile_size values SplatFrame can export
 
 
 def active_backend(settings: RenderSettings):
@@ -302,7 +304,8 @@ def _check_camera(camera):
         raise ConfigError("image dimensions above 65535 are not supported")
 
 
-def rasterize(ds, camera, settings, flags=0, outputs=None, events=None, async_=False, frame_buf=None):
+def rasterize(ds, camera, settings, flags=0, outputs=None, events=None, async_=False, frame_buf=None,
+              overlap=None):
     """Device-level forward: DeviceGaussians -> (images dict, SplatFrame).
 
     ``outputs`` may pass preallocated image tensors (keys color, depth,
@@ -312,7 +315,8 @@ def rasterize(ds, camera, settings, flags=0, outputs=None, events=None, async_=F
     a CUDA graph); the frame's counts and status are read by
     ``SplatFrame.sync()`` (a backward can run before that).  ``frame_buf``:
     a preallocated uint8 CUDA buffer to render into (its size sets the pair
-    capacity)."""
+    capacity).  ``overlap``: run the float64 preprocess on a side stream
+    beside the depth sort (hgs_settings.aux_stream)."""
     import torch
     L = _lib.lib()
     _check_camera(camera)
@@ -337,9 +341,12 @@ def rasterize(ds, camera, settings, flags=0, outputs=None, events=None, async_=F
         imgs = _lib.Images(None, None, None, None, None)
     if async_:
         flags |= _lib.HGS_FLAG_ASYNC
+    if overlap is None:
+        overlap = _OVERLAP
     sc = _lib.scene_struct(ds)
     cam = _lib.camera_struct(camera)
-    st = _lib.settings_struct(settings, flags, events)
+    # the float64 preprocess runs on a side stream beside the depth sort
+    st = _lib.settings_struct(settings, flags, events, aux=_lib.aux_handles(dev) if overlap else None)
     stream = _lib.current_stream_handle(dev)
     key = (n, W, H)
     if async_:

@@ -27,17 +27,21 @@ pos = torch.from_numpy(lg.position.astype(np.int64)).cuda()
 cnt = off[1:] - off[:-1]
 pix = torch.repeat_interleave(torch.arange(W * H, device="cuda"), cnt)
 ix, iy = pix % W, pix // W
-block = (iy // 16) * ((W + 15) // 16) * 2 + (ix // 16) * 2 + ((ix % 16) >= 8).long()
+import os
+if os.environ.get("BLOCK", "8x16") == "16x16":
+    block = (iy // 16) * ((W + 15) // 16) + (ix // 16)
+else:
+    block = (iy // 16) * ((W + 15) // 16) * 2 + (ix // 16) * 2 + ((ix % 16) >= 8).long()
 # (block, rank) visits; rank order within a block is the walk order reversed
 key = block * (1 << 24) + pos
 uk, n = torch.unique(key, return_counts=True)
-h = torch.bincount(n, minlength=129).cpu().numpy()
+h = torch.bincount(n, minlength=257).cpu().numpy()
 tot = int(n.numel())
 print("visits", tot, "pairs", int(n.sum()), "mean n", float(n.float().mean()))
-for lo, hi in ((1, 4), (5, 8), (9, 16), (17, 32), (33, 64), (65, 128)):
+for lo, hi in ((1, 4), (5, 8), (9, 16), (17, 32), (33, 64), (65, 128), (129, 256)):
     s = int(h[lo:hi + 1].sum())
     print("n in [%3d, %3d]: %6.2f%% of visits, %6.2f%% of pairs" % (lo, hi, 100.0 * s / tot,
-          100.0 * float((np.arange(129)[lo:hi + 1] * h[lo:hi + 1]).sum()) / float(n.sum())))
+          100.0 * float((np.arange(257)[lo:hi + 1] * h[lo:hi + 1]).sum()) / float(n.sum())))
 passes = int(((n + 31) // 32).sum())
 print("passes", passes, "lanes per pass", float(n.sum()) / passes)
 # consecutive visits of one block, both n <= 16: pair candidates (ignoring disjointness)
