@@ -29,7 +29,7 @@ REPO = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, REPO)
 
 MEASURED_PEAKS = os.path.join(REPO, "MEASURED_PEAKS.json")
-NCU_TAG = "r01i"  # profiles/ncu_<tag>_kernels.json: the committed capture the roofline limiter quotes
+NCU_TAG = "r02"  # profiles/ncu_<tag>_kernels.json: the committed capture the roofline limiter quotes
 METRIC = "hybrid-GS frames/s fwd & iters/s fwd+bwd at 1M Gaussians 1080p; 1/2/4/8 B200"
 N_SM = 148
 FMA_PER_SM_CLK = 128
@@ -709,14 +709,18 @@ def main():
     roof["ncu_kernel"] = kname
     roof["traffic"] = None
     if kname and os.path.exists(ncu_file):
-        for kd in json.load(open(ncu_file)):
-            if kd.get("config") == "c2" and kd.get("kernel") == kname:
-                roof["limiter"] = ("SM instruction issue (ncu, profiles/ncu_%s_kernels.json: issue " % NCU_TAG +
-                                   "active %.0f%%, FP32 pipe %.0f%%, DRAM %.0f%%, %.1f of 32 lanes active)"
-                                   % (kd.get("issue_active_pct", 0), kd.get("fma_pipe_pct", 0),
-                                      kd.get("dram_pct", 0), kd.get("thread_inst_per_inst", 0)))
-                # dram__bytes_read.sum + dram__bytes_write.sum of that kernel, one launch
-                roof["traffic"] = int((kd.get("dram_read_MB", 0) + kd.get("dram_write_MB", 0)) * 1e6)
+        cands = [kd for kd in json.load(open(ncu_file)) if kd.get("kernel") == kname]
+        cands.sort(key=lambda kd: kd.get("config") != "c2")  # this workload's capture first
+        if cands:
+            kd = cands[0]
+            roof["limiter"] = ("SM instruction issue (ncu, profiles/ncu_%s_kernels.json, %s capture: issue "
+                               % (NCU_TAG, kd.get("config")) +
+                               "active %.0f%%, FP32 pipe %.0f%%, DRAM %.0f%%, %.1f of 32 lanes active)"
+                               % (kd.get("issue_active_pct", 0), kd.get("fma_pipe_pct", 0),
+                                  kd.get("dram_pct", 0), kd.get("thread_inst_per_inst", 0)))
+            # dram__bytes_read.sum + dram__bytes_write.sum of that kernel, one launch
+            roof["traffic"] = int((kd.get("dram_read_MB", 0) + kd.get("dram_write_MB", 0)) * 1e6)
+            roof["traffic_config"] = kd.get("config")
     stage_roofs = {}
     for nm, t_ms in stages.items():
         if nm in flops:

@@ -2,7 +2,7 @@
 # summaries -> gpurun_out/sanitize_<tool>.txt
 set -x
 timeout 600 python tools/sanitize_drive.py > gpurun_out/sanitize_plain.txt 2>&1; echo "plain rc=$?"
-for tool in memcheck racecheck synccheck initcheck; do
+for tool in ${TOOLS:-memcheck racecheck synccheck}; do
   extra=""
   [ "$tool" = memcheck ] && extra="--leak-check no --padding 64"
   [ "$tool" = racecheck ] && extra="--racecheck-report all"

@@ -80,8 +80,12 @@ def main():
     json.dump(uniq, open("profiles/ncu_%s_kernels.json" % tag, "w"), indent=1)
     # per-stage DRAM traffic (bytes) of the config-2 kernels, as bench.py names the stages
     stage = {"composite_fwd": ["k_composite_fwd"], "composite_bwd": ["k_composite_bwd"],
-             "chain_rule(+touched)": ["k_chain_rule"], "preprocess_f64+scan": ["k_preprocess", "k_scan_counts",
-                                                                                "k_rank_scatter"]}
+             "chain_rule(+touched)": ["k_chain_rule"],
+             "depth_keys+sort||preprocess_f64": ["k_depth_keys", "k_sort_plan", "k_onesweep<unsigned long long>",
+                                                 "k_rank_scatter", "k_preprocess"],
+             "scan": ["k_scan_counts"],
+             "binning(dup+tile sort+ranges)": ["k_duplicate", "k_radix_offsets", "k_onesweep<unsigned int>",
+                                               "k_tile_ranges"]}
     tr = {"_source": "profiles/ncu_%s_kernels.json (ncu --set full, one launch each, config 2): " % tag +
                      "dram__bytes_read.sum + dram__bytes_write.sum per launch"}
     for st, pref in stage.items():
