@@ -298,6 +298,16 @@ int hgs_modulation_f64(int64_t n, const double *opacity, const double *log_scale
                        double lambda_z, double *sz_star, double *alpha_eff, double *d_alpha, double *d_logz,
                        void *stream);
 
+/* [ABI 3] Host I/O of the reference-facing float64 API (_hostio.py):
+ * page-lock an existing host range (cudaHostRegister), and widen n float32
+ * device values to float64 in `scratch` (device, 8n bytes, 16-byte aligned)
+ * then copy them asynchronously into host memory `dst_host` (registered: the
+ * copy is a DMA), so part of each float64 output never touches the host
+ * cores. */
+int hgs_host_register(void *ptr, size_t bytes);
+int hgs_host_unregister(void *ptr);
+int hgs_widen_d2h(const float *src, double *dst_host, int64_t n, double *scratch, void *stream);
+
 const char *hgs_status_string(int status);
 int hgs_abi_version(void);
 

@@ -26,6 +26,7 @@ allocator recycles device memory.
 """
 
 import ctypes
+import os
 import mmap
 import threading
 import weakref
@@ -39,18 +40,41 @@ _pool_bytes = [0]
 _pool_lock = threading.Lock()
 
 
+_registered = {}  # id(mmap) -> host address of a page-locked (cudaHostRegister) pool mapping
+
+
 def _recycle(mm, nbytes):
     with _pool_lock:
         if _pool_bytes[0] + nbytes <= _POOL_CAP:
             _pool.setdefault(nbytes, []).append(mm)
             _pool_bytes[0] += nbytes
             return
+        addr = _registered.pop(id(mm), None)
+    if addr is not None:
+        from . import _lib
+        _lib.lib().hgs_host_unregister(ctypes.c_void_p(addr))
     mm.close()
 
 
-def host_empty(shape, dtype=np.float64):
+def _register(mm, size):
+    """Page-lock a pool mapping once (it is recycled, so the registration is
+    amortised): copies into it are DMAs."""
+    addr = _registered.get(id(mm))
+    if addr is None:
+        from . import _lib
+        tmp = (ctypes.c_char * size).from_buffer(mm)
+        addr = ctypes.addressof(tmp)
+        del tmp
+        if _lib.lib().hgs_host_register(ctypes.c_void_p(addr), size) != 0:
+            return None
+        _registered[id(mm)] = addr
+    return addr
+
+
+def host_empty(shape, dtype=np.float64, register=False):
     """A new (uninitialised) numpy array; large ones reuse pooled, already
-    faulted-in mappings."""
+    faulted-in mappings (``register``: page-locked, so a device copy into it
+    is a DMA)."""
     dtype = np.dtype(dtype)
     n = int(np.prod(shape)) if len(shape) else 1
     nbytes = n * dtype.itemsize
@@ -64,6 +88,8 @@ def host_empty(shape, dtype=np.float64):
             _pool_bytes[0] -= size
     if mm is None:
         mm = mmap.mmap(-1, size)
+    if register:
+        _register(mm, size)
     # buffer owner of the mapping: a ctypes array exports the buffer protocol
     # on every supported Python (3.10+) and is weak-referenceable, so the
     # finalizer runs when the last numpy view of it is gone
@@ -125,11 +151,22 @@ def upload(arrays, device, tag="up"):
     return outs
 
 
+# share of each large float64 output widened on the GPU and DMA'd as float64
+# into the page-locked destination; the rest crosses as float32 and is
+# widened on the host cores -- both at once (host widening is host-DRAM bound
+# at ~20 B per element, PCIe carries 4 or 8 B per element)
+_GPU_WIDEN = float(os.environ.get("HGS_GPU_WIDEN", "0.4"))
+_GPU_WIDEN_MIN = 1 << 21  # elements; smaller outputs are widened on the host
+
+
 def download(tensors, dtype=np.float64, tag="down"):
     """Device float32 tensors -> list of new numpy arrays of ``dtype``.
 
     DMA into pinned staging in chunks (one event per chunk) and widen each
-    chunk on the host while later chunks are still in flight."""
+    chunk on the host while later chunks are still in flight; for large
+    float64 outputs the leading ``_GPU_WIDEN`` share is widened on the GPU
+    (hgs_widen_d2h) and DMA'd straight into the destination on a side
+    stream, concurrently."""
     import torch
     tdt = {np.float64: torch.float64, np.float32: torch.float32}[dtype]
     metas = []
@@ -143,14 +180,35 @@ def download(tensors, dtype=np.float64, tag="down"):
     stage = ent[0]
     dev = tensors[0].device if tensors else None
     stream = torch.cuda.current_stream(dev)
-    outs, pending = [], []
+    outs, pending, gpu_parts = [], [], []
+    side = None
     for t, off, nb in metas:
         flat = t.reshape(-1)
         hv = stage[off:off + nb].view(t.dtype)
         step = max(_CHUNK // t.element_size(), 1)
-        out = torch.from_numpy(host_empty(tuple(t.shape), dtype))
+        n = flat.numel()
+        split = (int(n * _GPU_WIDEN) & ~1023) if (dtype is np.float64 and t.dtype == torch.float32
+                                                  and n >= _GPU_WIDEN_MIN) else 0
+        out = torch.from_numpy(host_empty(tuple(t.shape), dtype, register=split > 0))
         oflat = out.reshape(-1)
-        for s in range(0, flat.numel(), step):
+        if split:
+            from . import _lib
+            if side is None:
+                side = _side_stream(dev)
+                side.wait_stream(stream)
+            scratch = torch.empty(split, dtype=torch.float64, device=dev)
+            scratch.record_stream(side)
+            flat.record_stream(side)
+            rc = _lib.lib().hgs_widen_d2h(ctypes.c_void_p(flat.data_ptr()), ctypes.c_void_p(oflat.data_ptr()),
+                                          split, ctypes.c_void_p(scratch.data_ptr()),
+                                          ctypes.c_void_p(side.cuda_stream))
+            if rc == 0:
+                gpu_parts.append(scratch)
+            else:
+                split = 0
+        else:
+            split = 0
+        for s in range(split, n, step):
             e = min(s + step, flat.numel())
             hv[s:e].copy_(flat[s:e], non_blocking=True)
             ev = torch.cuda.Event()
@@ -160,5 +218,18 @@ def download(tensors, dtype=np.float64, tag="down"):
     for ev, o, h in pending:
         ev.synchronize()
         o.copy_(h)  # multi-threaded f32 -> f64 while later chunks are in flight
+    if side is not None:
+        side.synchronize()  # the GPU-widened shares have landed
     ent[1] = None
     return [o.numpy() for o in outs]
+
+
+_sides = {}
+
+
+def _side_stream(dev):
+    import torch
+    idx = dev.index if dev.index is not None else torch.cuda.current_device()
+    if idx not in _sides:
+        _sides[idx] = torch.cuda.Stream(device=idx)
+    return _sides[idx]

@@ -49,7 +49,7 @@ EXPORTS = ("hgs_abi_version", "hgs_status_string", "hgs_frame_bytes", "hgs_forwa
            "hgs_combine_gradients", "hgs_adam_step", "hgs_combine_adam_step",
            "hgs_densify_stats", "hgs_densify_scratch_bytes", "hgs_densify_plan", "hgs_densify_apply",
            "hgs_tile_bins_scratch_bytes", "hgs_frame_tile_bins", "hgs_eval_contributions",
-           "hgs_frame_sync_info",
+           "hgs_frame_sync_info", "hgs_host_register", "hgs_host_unregister", "hgs_widen_d2h",
            "hgs_effective_rank_f64", "hgs_reparameterize_f64", "hgs_modulation_f64")
 
 _vp = ctypes.c_void_p
@@ -171,6 +171,9 @@ def lib():
                                 _vp, _vp, _vp, _vp]
     L.hgs_frame_stats.argtypes = [_vp, P(FrameInfo), _vp, _vp]
     L.hgs_frame_sync_info.argtypes = [_vp, P(FrameInfo), _vp]
+    L.hgs_host_register.argtypes = [_vp, ctypes.c_size_t]
+    L.hgs_host_unregister.argtypes = [_vp]
+    L.hgs_widen_d2h.argtypes = [_vp, _vp, _i64, _vp, _vp]
     L.hgs_tile_bins_scratch_bytes.restype = ctypes.c_size_t
     L.hgs_tile_bins_scratch_bytes.argtypes = [_i64, _i32, _i32, _i32, _i64]
     L.hgs_frame_tile_bins.argtypes = [_vp, P(FrameInfo), _i32, _vp, _vp, _i64, _vp, ctypes.c_size_t,

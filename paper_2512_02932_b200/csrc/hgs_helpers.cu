@@ -218,3 +218,49 @@ int hgs_modulation_f64(int64_t n, const double *opacity, const double *log_scale
 }
 
 }  // extern "C"
+
+// ------------------------------------------------------------ host I/O
+// The reference-facing API returns float64 numpy arrays.  Widening on the
+// host cores is host-memory bound (~20 B of DRAM traffic per element); a
+// share of each output is instead widened on the GPU and DMA'd as float64
+// straight into the (registered) destination array, so PCIe and the host
+// cores work in parallel (_hostio.download).
+namespace hgs {
+__global__ void k_widen(const float *__restrict__ src, double *__restrict__ dst, int64_t n) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t n4 = n / 4;
+  const float4 *s4 = reinterpret_cast<const float4 *>(src);
+  double2 *d2 = reinterpret_cast<double2 *>(dst);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += stride) {
+    const float4 v = s4[i];
+    d2[2 * i] = make_double2(v.x, v.y);
+    d2[2 * i + 1] = make_double2(v.z, v.w);
+  }
+  for (int64_t i = 4 * n4 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) dst[i] = src[i];
+}
+}  // namespace hgs
+
+extern "C" {
+
+int hgs_host_register(void *ptr, size_t bytes) {
+  if (!ptr || !bytes) return HGS_ERR_CONFIG;
+  return cudaHostRegister(ptr, bytes, cudaHostRegisterPortable) == cudaSuccess ? HGS_OK : HGS_ERR_CUDA;
+}
+
+int hgs_host_unregister(void *ptr) {
+  if (!ptr) return HGS_ERR_CONFIG;
+  return cudaHostUnregister(ptr) == cudaSuccess ? HGS_OK : HGS_ERR_CUDA;
+}
+
+int hgs_widen_d2h(const float *src, double *dst_host, int64_t n, double *scratch, void *stream) {
+  if (n < 0 || (n > 0 && (!src || !dst_host || !scratch))) return HGS_ERR_CONFIG;
+  if (((uintptr_t)src & 15u) || ((uintptr_t)scratch & 15u)) return HGS_ERR_CONFIG;
+  if (n == 0) return HGS_OK;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  k_widen<<<grid_of(n / 4 + 1), 256, 0, s>>>(src, scratch, n);
+  if (cudaGetLastError() != cudaSuccess) return HGS_ERR_CUDA;
+  return cudaMemcpyAsync(dst_host, scratch, (size_t)n * 8, cudaMemcpyDeviceToHost, s) == cudaSuccess ? HGS_OK
+                                                                                                   : HGS_ERR_CUDA;
+}
+
+}  // extern "C"

@@ -50,7 +50,7 @@ for it in range(4):
     T["total"] = t9 - t0
     print({k: round(v * 1e3, 2) for k, v in T.items()})
 # the public API end to end
-for it in range(3):
+for it in range(8):
     t0 = t()
     out = raster.render(hs, cam, st)
     gr, touched = grad.backward(hs, cam, out, pg)
