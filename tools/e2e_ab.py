@@ -1,0 +1,43 @@
+"""Same-process A/B of the host I/O modes of the reference-facing API at
+config 2 (alternating rounds; the median of each mode's per-step times).
+Run on the GPU box."""
+import sys
+import time
+
+import numpy as np
+import torch
+
+sys.path.insert(0, ".")
+from paper_2512_02932_b200 import _hostio, grad, raster  # noqa: E402
+from paper_2512_02932_b200.core import GaussianSet  # noqa: E402
+from paper_2512_02932_b200.settings import RenderSettings  # noqa: E402
+from paper_2512_02932_b200.synthetic import synthetic_scene  # noqa: E402
+
+scene, cam = synthetic_scene(1_000_000, 1920, 1080, 3, seed=0)
+hs = GaussianSet(scene.center, scene.log_scale, scene.rotation, scene.opacity_logit,
+                 scene.sh_coeffs, scene.type_spec)
+st = RenderSettings()
+pg = np.random.default_rng(0).normal(size=(1080, 1920, 3))
+MODES = {
+    "host only": dict(widen=0.0, narrow=1.0, reg=False),
+    "gpu widen": dict(widen=0.4, narrow=1.0, reg=False),
+    "widen+direct": dict(widen=0.4, narrow=0.85, reg=True),
+    "direct only": dict(widen=0.0, narrow=0.85, reg=True),
+}
+res = {m: [] for m in MODES}
+orig_reg = _hostio._user_registered
+for rnd in range(4):
+    for m, cfg in MODES.items():
+        _hostio._GPU_WIDEN = cfg["widen"]
+        _hostio._HOST_NARROW = cfg["narrow"]
+        _hostio._user_registered = orig_reg if cfg["reg"] else (lambda a: False)
+        for it in range(6):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            out = raster.render(hs, cam, st)
+            gr, touched = grad.backward(hs, cam, out, pg)
+            torch.cuda.synchronize()
+            if it >= 2:
+                res[m].append((time.perf_counter() - t0) * 1e3)
+for m, v in res.items():
+    print("%-14s median %.2f ms  min %.2f ms  (%d steps)" % (m, np.median(v), np.min(v), len(v)))
