@@ -112,3 +112,24 @@ def test_densify_statistics_use_pixel_axis_centre_gradient():
     sel[ofr.idx[k3]] = True
     sel &= ot
     np.testing.assert_allclose(got[sel], want[sel], rtol=2e-3, atol=1e-6 * want.max())
+
+
+def test_view_batch_grads_redoes_views_that_outgrew_the_pair_capacity():
+    """Asynchronous views that overflow the frame's pair capacity composite
+    nothing and back-propagate zeros; the batch redoes them synchronously
+    (the frame buffer grows), so the summed gradient is unchanged."""
+    import torch
+
+    from paper_2512_02932_b200 import parallel, raster
+    ds, cams, pgs, st = _setup()
+    ref = sum(_single(ds, c, st, p)[0] for c, p in zip(cams, pgs))[0]
+    key = (ds.count, int(cams[0].width), int(cams[0].height))
+    for first_bad in (True, False):
+        raster._pair_hint[key] = 1000  # far below K: every asynchronous view overflows
+        out = torch.empty_like(ref)
+        views = cams if first_bad else cams[::-1]
+        grads = pgs if first_bad else pgs[::-1]
+        parallel.view_batch_grads(ds, views, st, lambda j, im: grads[j], out)
+        err = (out - ref).abs().max() / ref.abs().max()
+        assert float(err) < 1e-6
+        assert raster._pair_hint[key] > 1000  # the synchronous redo grew the hint
