@@ -704,8 +704,8 @@ def main():
     # quote the committed ncu capture of the same kernel (profiles/)
     ncu_file = os.path.join(REPO, "profiles", "ncu_%s_kernels.json" % NCU_TAG)
     # the instantiation this run launched (template <NAIVE, COUNT, PF> / <KG, EXT, DET, QP>)
-    kname = {"composite_fwd": "k_composite_fwd<0, 0, 0>",
-             "composite_bwd": "k_composite_bwd_c<%d, 0, 0, 4>" % min(a.kg, 4)}.get(dom)
+    kname = {"composite_fwd": "k_composite_fwd<0, 0, 0, %d>" % (0 if a.fast else 1),
+             "composite_bwd": "k_composite_bwd_c<%d, 0, 0, 4, 0>" % min(a.kg, 4)}.get(dom)
     roof["ncu_kernel"] = kname
     roof["traffic"] = None
     if kname and os.path.exists(ncu_file):

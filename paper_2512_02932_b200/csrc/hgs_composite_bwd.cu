@@ -395,7 +395,7 @@ constexpr size_t cstate_bytes() {
 #define HGS_BWDC_MINB(KG, EXT, QP) \
   (((KG) == 1 ? ((EXT) ? 4 : HGS_BWDC_MINB1) : ((EXT) ? 3 : HGS_BWDC_MINBK)) * (QP) / 2)
 
-template <int KG, bool EXT, bool DET, int QP>
+template <int KG, bool EXT, bool DET, int QP, bool COUNT>
 __global__ void __launch_bounds__(256 / QP, HGS_BWDC_MINB(KG, EXT, QP)) k_composite_bwd_c(BwdArgs b) {
   constexpr int NW = 8 / QP;  // warps per tile
   // warp block: 8 x (4 QP) pixels, or the whole 16 x 16 tile at QP = 8;
@@ -463,7 +463,7 @@ __global__ void __launch_bounds__(256 / QP, HGS_BWDC_MINB(KG, EXT, QP)) k_compos
   asm volatile("mov.u32 %0, %0;" : "+r"(col_sa));
 #endif
   const bool writer = lane < 16;
-  const bool count = a.flags & HGS_FLAG_COUNT;
+  constexpr bool count = COUNT;  // HGS_FLAG_COUNT: a separate instantiation, no per-pass test
   uint32_t n_ev = 0, n_c3 = 0, n_cr = 0, n_cl = 0;
   uint32_t lt;
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(lt));
@@ -841,12 +841,21 @@ static cudaError_t launch_bwd_t(const BwdArgs &b, int64_t n_tiles, cudaStream_t 
     const size_t dyn = (8 / QP) * cstate_bytes<KG, EXT, QP>();
     static bool attr_set = false;
     if (!attr_set) {
-      const cudaError_t err = cudaFuncSetAttribute(k_composite_bwd_c<KG, EXT, DET, QP>,
-                                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
-      if (err != cudaSuccess) return err;
+      // the exact / fast mode stays a per-pair flag test here (templating it
+      // measured 1.748 -> 1.760 ms); HGS_FLAG_COUNT is its own instantiation
+      const void *fns[2] = {(const void *)k_composite_bwd_c<KG, EXT, DET, QP, false>,
+                            (const void *)k_composite_bwd_c<KG, EXT, DET, QP, true>};
+      for (const void *f : fns) {
+        const cudaError_t err = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+        if (err != cudaSuccess) return err;
+      }
       attr_set = true;
     }
-    k_composite_bwd_c<KG, EXT, DET, QP><<<(unsigned)n_tiles, 256 / QP, dyn, s>>>(b);
+    const unsigned g = (unsigned)n_tiles, t = 256 / QP;
+    if (b.c.flags & HGS_FLAG_COUNT)
+      k_composite_bwd_c<KG, EXT, DET, QP, true><<<g, t, dyn, s>>>(b);
+    else
+      k_composite_bwd_c<KG, EXT, DET, QP, false><<<g, t, dyn, s>>>(b);
   }
   k_fixup_bwd<KG, EXT, DET><<<kFixupBlocks, 256, 0, s>>>(b);
   return cudaGetLastError();

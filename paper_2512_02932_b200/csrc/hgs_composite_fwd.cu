@@ -48,7 +48,7 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 // round trips per chunk) leaves the critical path.  Every entry of the chunk
 // is copied (the bbox test needs the record), the culls then run on the
 // shared-memory copy.
-template <bool NAIVE, bool COUNT, int PF>
+template <bool NAIVE, bool COUNT, int PF, bool EXACT>
 __global__ void __launch_bounds__(kBlock, HGS_FWD_MINB) k_composite_fwd(CompositeArgs a) {
   __shared__ SplatRec s_rec[PF ? 2 : 1][kBlock / 32][32];
   const int tile = blockIdx.x;
@@ -59,7 +59,7 @@ __global__ void __launch_bounds__(kBlock, HGS_FWD_MINB) k_composite_fwd(Composit
   const bool inside = ix < a.width && iy < a.height;
   const uint32_t lane_bit = 1u << lane;
   const float lox = (float)(lane & 7), loy = (float)(lane >> 3);  // offset in the warp block
-  const bool exact = HGS_EXACT_ENABLED && !(a.flags & HGS_FLAG_FAST);
+  constexpr bool exact = HGS_EXACT_ENABLED && EXACT;  // HGS_FLAG_FAST: the EXACT = false instantiation
   const bool stress = COUNT && !NAIVE && (a.flags & HGS_FLAG_DEFER_ALL);
   if (a.st->status) return;  // failed frame (bad parameters / pair capacity): nothing to composite
   uint32_t lo, hi;
@@ -203,8 +203,9 @@ __global__ void __launch_bounds__(kBlock, HGS_FWD_MINB) k_composite_fwd(Composit
       const bool is3d = rec_is3d(r);
       if (COUNT) (is3d ? n_ev3 : n_ev2) += 1;
       PairEval p;
-      const int c = (HGS_STAGED_ORIGIN && !NAIVE) ? eval_fast<false, false, true>(r, ix, iy, a.flags, p, lox, loy)
-                                                  : eval_fast<false>(r, ix, iy, a.flags, p);
+      const int c = (HGS_STAGED_ORIGIN && !NAIVE)
+                        ? eval_fast<false, false, true, EXACT ? 1 : 0>(r, ix, iy, a.flags, p, lox, loy)
+                        : eval_fast<false, false, false, EXACT ? 1 : 0>(r, ix, iy, a.flags, p);
       if (c == kSkip) continue;
 #if HGS_FWD_ONE_DEFER
       // one deferral site (the pair's decision or the early-stop decision), so
@@ -300,10 +301,15 @@ __global__ void __launch_bounds__(kBlock, HGS_FWD_MINB) k_composite_fwd(Composit
 
 cudaError_t launch_composite_fwd(const CompositeArgs &a, int64_t n_tiles, bool naive, bool count, cudaStream_t s) {
   constexpr int PF = HGS_FWD_PF;
-  if (naive && count) k_composite_fwd<true, true, 0><<<(unsigned)n_tiles, kBlock, 0, s>>>(a);
-  else if (naive) k_composite_fwd<true, false, 0><<<(unsigned)n_tiles, kBlock, 0, s>>>(a);
-  else if (count) k_composite_fwd<false, true, PF><<<(unsigned)n_tiles, kBlock, 0, s>>>(a);
-  else k_composite_fwd<false, false, PF><<<(unsigned)n_tiles, kBlock, 0, s>>>(a);
+  const bool fast = a.flags & HGS_FLAG_FAST;
+#define HGS_FWD_LAUNCH(NV, CT, P)                                                           \
+  (fast ? k_composite_fwd<NV, CT, P, false><<<(unsigned)n_tiles, kBlock, 0, s>>>(a)         \
+        : k_composite_fwd<NV, CT, P, true><<<(unsigned)n_tiles, kBlock, 0, s>>>(a))
+  if (naive && count) HGS_FWD_LAUNCH(true, true, 0);
+  else if (naive) HGS_FWD_LAUNCH(true, false, 0);
+  else if (count) HGS_FWD_LAUNCH(false, true, PF);
+  else HGS_FWD_LAUNCH(false, false, PF);
+#undef HGS_FWD_LAUNCH
   return cudaGetLastError();
 }
 

@@ -473,7 +473,9 @@ static __device__ __noinline__ Resolved resolve_pair(const SplatRec *rp, int ix,
 // float anchor-relative centre of the warp block's first pixel,
 // (wx0 - ax) + 0.5 (stage_block_origin), and (ox, oy) is the pixel's offset
 // in the block: pxl = that + ox is the same exact value as (ix - ax) + 0.5.
-template <bool BWD, bool KNOWN = false, bool STAGED = false>
+// EXM: 1 exact decisions, 0 HGS_FLAG_FAST, 2 read from flags at run time
+// (the hot compositors are instantiated per mode: no per-pair flag test).
+template <bool BWD, bool KNOWN = false, bool STAGED = false, int EXM = 2>
 __device__ __forceinline__ int eval_fast(const SplatRec &r, int ix, int iy, uint32_t flags, PairEval &p,
                                          float ox = 0.f, float oy = 0.f) {
   Geom g;
@@ -489,7 +491,7 @@ __device__ __forceinline__ int eval_fast(const SplatRec &r, int ix, int iy, uint
   p.dy = g.dy;
   p.pxl = g.pxl;
   p.pyl = g.pyl;
-  const bool exact = HGS_EXACT_ENABLED && !(flags & HGS_FLAG_FAST);
+  const bool exact = HGS_EXACT_ENABLED && (EXM == 2 ? !(flags & HGS_FLAG_FAST) : EXM == 1);
   bool amb = false;
   p.ray = false;
   if (rec_is3d(r)) {
