@@ -106,9 +106,11 @@ __global__ void __launch_bounds__(kBlock, HGS_FWD_MINB) k_composite_fwd(Composit
   }
   uint32_t buf = 0u;
 
-  auto defer = [&](uint32_t entry, uint32_t mode) {
+  // last: one past the last contributor (tile-list position relative to lo);
+  // kept per chunk from the chunk's contribution mask cm, not per pair
+  auto defer = [&](uint32_t entry, uint32_t mode, uint32_t last_now) {
     FwdFix f;
-    f.pix = pix; f.entry = entry; f.mode = mode; f.cnt = cnt; f.last = last;
+    f.pix = pix; f.entry = entry; f.mode = mode; f.cnt = cnt; f.last = last_now;
     f.T = T; f.c0 = cr; f.c1 = cg; f.c2 = cb; f.dep = dep; f.n0 = n0; f.n1 = n1; f.n2 = n2;
     f.pad[0] = f.pad[1] = f.pad[2] = 0;
     a.fwd_fix[atomicAdd(&a.st->n_fix_fwd, 1u)] = f;
@@ -214,15 +216,15 @@ __global__ void __launch_bounds__(kBlock, HGS_FWD_MINB) k_composite_fwd(Composit
       // HGS_FLAG_DEFER_ALL (tests, counting instantiation only): every pixel is
       // deferred at its first contribution, even pixels before it (mode 0),
       // odd pixels after it (mode 1), so the whole image goes through k_fixup_fwd
-      if (c == kAmbiguous || (stress && last == 0u && !(pix & 1u))) {
+      if (c == kAmbiguous || (stress && last == 0u && cm == 0u && !(pix & 1u))) {
         if (COUNT && c == kAmbiguous) atomicAdd(&a.st->diag[is3d ? 12 : 13], 1ull);  // deferral reasons
         dmode = 0u;
       } else {
-        if (stress && last == 0u) dmode = 1u;
+        if (stress && last == 0u && cm == 0u) dmode = 1u;
 #else
       if (c == kAmbiguous) {
         if (COUNT) atomicAdd(&a.st->diag[is3d ? 12 : 13], 1ull);  // deferral reasons
-        defer(base + e, 0u);
+        defer(base + e, 0u, cm ? base - lo + 32u - (uint32_t)__clz(cm) : last);
         continue;
       }
       {
@@ -240,7 +242,6 @@ __global__ void __launch_bounds__(kBlock, HGS_FWD_MINB) k_composite_fwd(Composit
         n2 = fmaf(w, c4.z, n2);
         if (NAIVE) ++cnt;  // tiled frames derive the blend-log counts from the masks
         cm |= 1u << e;
-        last = base + e - lo + 1u;
         T = T * (1.f - at);
         // early stop T < 1e-4 (_blend_py.py:111-113); near the threshold the
         // decision is deferred to the float64 transmittance replay.  One
@@ -251,7 +252,7 @@ __global__ void __launch_bounds__(kBlock, HGS_FWD_MINB) k_composite_fwd(Composit
 #if HGS_FWD_ONE_DEFER
             dmode = 1u;
 #else
-            defer(base + e, 1u);
+            defer(base + e, 1u, cm ? base - lo + 32u - (uint32_t)__clz(cm) : last);
 #endif
           }
           else if (T < (float)kEarlyStopT)
@@ -259,9 +260,10 @@ __global__ void __launch_bounds__(kBlock, HGS_FWD_MINB) k_composite_fwd(Composit
         }
       }
 #if HGS_FWD_ONE_DEFER
-      if (dmode != 2u) defer(base + e, dmode);
+      if (dmode != 2u) defer(base + e, dmode, cm ? base - lo + 32u - (uint32_t)__clz(cm) : last);
 #endif
     }
+    if (cm) last = base - lo + 32u - (uint32_t)__clz(cm);
     if (!NAIVE && walking)
       a.pix_mask[mask_word(lo, tile, (base - lo) >> 5, (uint32_t)((iy & (kTile - 1)) * kTile + (ix & (kTile - 1))))] = cm;
     __syncwarp();  // the next chunk overwrites this warp's staging slots
