@@ -188,6 +188,35 @@ __device__ __forceinline__ void write_record(const ProjD &o, uint32_t idx, int W
   }
 }
 
+// Tile counts of the compositor's lists: a splat whose bbox spans at most
+// kTileCullMax tiles keeps only the tiles tile_culled accepts (k_duplicate
+// emits with the same test on the same record).  A separate, fully occupied
+// pass after the float64 preprocess (inside it the loop over tiles cost the
+// latency-bound preprocess 0.09 ms at config 2).
+__global__ void __launch_bounds__(256) k_tile_counts(const SplatRec *__restrict__ recs,
+                                                     const float4 *__restrict__ cull2d, int64_t n,
+                                                     uint32_t *__restrict__ counts) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t nt = counts[i];  // bbox tiles (0: culled or off screen)
+    if (nt <= 1u || nt > (uint32_t)kTileCullMax) continue;  // one tile: the compositor's warp cull suffices
+    const SplatRec *gp = recs + i;
+    SplatRec r;
+    r.r0 = __ldg(&gp->r0); r.r1 = __ldg(&gp->r1); r.r4 = __ldg(&gp->r4); r.r5 = __ldg(&gp->r5);
+    r.r2 = r.r3 = make_float4(0.f, 0.f, 0.f, 0.f);
+    float4 c2[2] = {make_float4(0.f, 0.f, 0.f, 0.f), make_float4(0.f, 0.f, 0.f, 0.f)};
+    if (!rec_is3d(r)) {
+      c2[0] = __ldg(cull2d + 2 * (size_t)i);
+      c2[1] = __ldg(cull2d + 2 * (size_t)i + 1);
+    }
+    const int4 q = r.r5;
+    const int x0 = q.x & 0xffff, y0 = (int)((uint32_t)q.x >> 16), x1 = q.y & 0xffff, y1 = (int)((uint32_t)q.y >> 16);
+    uint32_t cnt = 0;
+    for (int ty = y0 / kTile; ty <= y1 / kTile; ++ty)
+      for (int tx = x0 / kTile; tx <= x1 / kTile; ++tx) cnt += tile_culled(r, c2, tx, ty, x0, y0, x1, y1) ? 0u : 1u;
+    counts[i] = cnt;
+  }
+}
+
 // Inverse depth permutation over all n sorted slots: culled Gaussians (keys
 // ~0, sorted after the m kept ones) get rank 0xffffffff.
 // Inverse of the depth permutation.  The sorted indices are in buffer
@@ -315,7 +344,7 @@ __global__ void __launch_bounds__(32, HGS_PRE_MINB) k_preprocess(SceneView sc, C
     bbox_d(o, cam.width, cam.height);
     write_record(o, (uint32_t)i, cam.width, cam.height, recs + i, cull2d + 2 * (size_t)i, eig + i);
     write_rec64(o, recs64 + i);
-    counts[i] = tile_count_of(o.bbox);
+    counts[i] = tile_count_of(o.bbox);  // bbox tiles; k_tile_counts culls them
   }
 }
 // Host launcher (the template is launched from this translation unit).
@@ -392,13 +421,16 @@ constexpr int kDupOwn = 32;
 
 // order: rank -> Gaussian (records are by Gaussian); the pair value is the
 // Gaussian index, or the rank with emit_rank (the SplatFrame export's slots).
+// tile_cull (the compositor's lists, 16 x 16 tiles): splats with at most
+// kTileCullMax bbox tiles skip the tiles tile_culled rejects -- the counts
+// the scan used were formed by the same test (write_record).
 __global__ void __launch_bounds__(256) k_duplicate(const SplatRec *__restrict__ recs,
                                                    const uint32_t *__restrict__ order,
                                                    const unsigned long long *__restrict__ pair_off, int64_t m,
                                                    const FrameState *__restrict__ st, int tiles_x, int tile_shift,
-                                                   bool emit_rank, uint32_t *__restrict__ pkeys,
-                                                   uint32_t *__restrict__ pvals, int n_digits,
-                                                   uint32_t *__restrict__ hist) {
+                                                   bool emit_rank, bool tile_cull, const float4 *__restrict__ cull2d,
+                                                   uint32_t *__restrict__ pkeys, uint32_t *__restrict__ pvals,
+                                                   int n_digits, uint32_t *__restrict__ hist) {
   __shared__ uint32_t sh[2 * kRadix];
   if (m < 0) {  // M and the capacity verdict from the frame state
     if (st->status) return;
@@ -420,11 +452,12 @@ __global__ void __launch_bounds__(256) k_duplicate(const SplatRec *__restrict__ 
     int tx0 = 0, ty0 = 0, bw = 1;
     uint32_t cnt = 0;
     unsigned long long o = 0;
-    uint32_t val = 0;
+    uint32_t val = 0, g = 0;
+    int4 q = make_int4(0, 0, 0, 0);
     if (r < m) {
-      const uint32_t g = order[r];
+      g = order[r];
       val = emit_rank ? (uint32_t)r : g;
-      const int4 q = recs[g].r5;
+      q = recs[g].r5;
       const int x0 = q.x & 0xffff, y0 = (int)((uint32_t)q.x >> 16), x1 = q.y & 0xffff, y1 = (int)((uint32_t)q.y >> 16);
       if (x1 >= x0) {
         tx0 = x0 >> tile_shift; ty0 = y0 >> tile_shift;
@@ -433,9 +466,27 @@ __global__ void __launch_bounds__(256) k_duplicate(const SplatRec *__restrict__ 
         o = pair_off[r];
       }
     }
+    static_assert(kTileCullMax <= kDupOwn, "culled splats take the per-lane path");
     if (cnt <= (uint32_t)kDupOwn) {
+      const bool cull = tile_cull && cnt > 1u;  // the k_tile_counts rule
+      SplatRec rc;
+      float4 c2[2] = {make_float4(0.f, 0.f, 0.f, 0.f), make_float4(0.f, 0.f, 0.f, 0.f)};
+      if (cull) {
+        const SplatRec *gp = recs + g;
+        rc.r0 = __ldg(&gp->r0); rc.r1 = __ldg(&gp->r1); rc.r4 = __ldg(&gp->r4); rc.r5 = q;  // r4.w: the type bit
+        rc.r2 = rc.r3 = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (!rec_is3d(rc)) {
+          c2[0] = __ldg(cull2d + 2 * (size_t)g);
+          c2[1] = __ldg(cull2d + 2 * (size_t)g + 1);
+        }
+      }
+      const int bx0 = q.x & 0xffff, by0 = (int)((uint32_t)q.x >> 16), bx1 = q.y & 0xffff,
+                by1 = (int)((uint32_t)q.y >> 16);
+      uint32_t k = 0;
       for (uint32_t j = 0, dy = 0, dx = 0; j < cnt; ++j) {  // row-major over the tile rectangle
-        emit((uint32_t)((ty0 + (int)dy) * tiles_x + tx0 + (int)dx), o + j, val);
+        const int tx = tx0 + (int)dx, ty = ty0 + (int)dy;
+        if (!cull || !tile_culled(rc, c2, tx, ty, bx0, by0, bx1, by1))
+          emit((uint32_t)(ty * tiles_x + tx), o + k++, val);
         if (++dx == (uint32_t)bw) { dx = 0; ++dy; }
       }
     }

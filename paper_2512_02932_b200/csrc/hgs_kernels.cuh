@@ -219,13 +219,16 @@ __device__ __forceinline__ void cull2d_prep(const SplatRec &r, float4 &k0, float
   k1 = make_float4(y0, 1.f, 0.f, 0.f);
 }
 
-__device__ __forceinline__ bool cull_splat_pre(const SplatRec &r, const float4 *c2, uint32_t pm, int wx0, int wy0) {
+// The same test on the inclusive pixel rectangle [x0, x1] x [y0, y1]
+// (absolute pixel indices, inside the splat's bbox): the warp cull of an 8 x 4
+// block and the tile-level cull of the binning (tile lists hold only the
+// (splat, tile) pairs some pixel of which can contribute) share it.
+__device__ __forceinline__ bool cull_rect(const SplatRec &r, const float4 *c2, int x0, int y0, int x1, int y1) {
   const float dstar = (r.r0.w - kArgMinAlpha) * (1.f / kHalfLog2e);
   if (dstar < 0.f) return true;  // alpha_eff < 1/255: never contributes
-  const int c0 = __ffs(pm) - 1, c1 = 31 - __clz(pm);
   const int4 q = r.r5;
-  const float PX0 = (float)(wx0 + (c0 & 7) - q.z) + 0.5f, PX1 = (float)(wx0 + (c1 & 7) - q.z) + 0.5f;
-  const float PY0 = (float)(wy0 + (c0 >> 3) - q.w) + 0.5f, PY1 = (float)(wy0 + (c1 >> 3) - q.w) + 0.5f;
+  const float PX0 = (float)(x0 - q.z) + 0.5f, PX1 = (float)(x1 - q.z) + 0.5f;
+  const float PY0 = (float)(y0 - q.w) + 0.5f, PY1 = (float)(y1 - q.w) + 0.5f;
   float A, B, C, cx, cy, thr;
   if (rec_is3d(r)) {
     const float4 e = r.r1;  // (c, s, lambda_p, lambda_q) -> conic (A, B, C)
@@ -245,6 +248,24 @@ __device__ __forceinline__ bool cull_splat_pre(const SplatRec &r, const float4 *
     thr = 1.05f;
   }
   return rect_min_quad(A, B, C, PX0 - cx, PX1 - cx, PY0 - cy, PY1 - cy) > thr;
+}
+
+__device__ __forceinline__ bool cull_splat_pre(const SplatRec &r, const float4 *c2, uint32_t pm, int wx0, int wy0) {
+  const int c0 = __ffs(pm) - 1, c1 = 31 - __clz(pm);  // pm is a rectangle (pixel_mask)
+  return cull_rect(r, c2, wx0 + (c0 & 7), wy0 + (c0 >> 3), wx0 + (c1 & 7), wy0 + (c1 >> 3));
+}
+
+// Tile-level cull of the binning: splats whose bbox spans at most
+// kTileCullMax tiles list only the tiles whose part of the bbox the support
+// can reach (35% of the bbox pairs at config 2 have no contributing pixel).
+// The preprocess counts and k_duplicate emits with this one function on the
+// same float32 record, so counts and emitted pairs agree exactly.
+constexpr int kTileCullMax = 32;
+__device__ __forceinline__ bool tile_culled(const SplatRec &r, const float4 *c2, int tx, int ty, int bx0, int by0,
+                                            int bx1, int by1) {
+  const int x0 = max(tx * kTile, bx0), x1 = min(tx * kTile + kTile - 1, bx1);
+  const int y0 = max(ty * kTile, by0), y1 = min(ty * kTile + kTile - 1, by1);
+  return cull_rect(r, c2, x0, y0, x1, y1);
 }
 
 #ifndef HGS_CULL_2D
@@ -666,11 +687,12 @@ cudaError_t launch_preprocess(const SceneView &sc, const CamD &cam, const ModD &
                               cudaStream_t s);
 __global__ void k_scan_counts(const uint32_t *counts, const uint32_t *order, int64_t m, unsigned long long *pair_off,
                               unsigned long long *scan_lb, FrameState *st, int64_t cap);
+__global__ void k_tile_counts(const SplatRec *recs, const float4 *cull2d, int64_t n, uint32_t *counts);
 __global__ void k_rebin_counts(const SplatRec *recs, const uint32_t *order, int64_t m, int tile_shift,
                                uint32_t *counts);
 __global__ void k_duplicate(const SplatRec *recs, const uint32_t *order, const unsigned long long *pair_off, int64_t m,
-                            const FrameState *st, int tiles_x, int tile_shift, bool emit_rank, uint32_t *pkeys,
-                            uint32_t *pvals, int n_digits, uint32_t *hist);
+                            const FrameState *st, int tiles_x, int tile_shift, bool emit_rank, bool tile_cull,
+                            const float4 *cull2d, uint32_t *pkeys, uint32_t *pvals, int n_digits, uint32_t *hist);
 __global__ void k_tile_ranges(const uint32_t *skeys, int64_t k, const FrameState *st, int64_t n_tiles,
                               uint32_t *tile_off);
 __global__ void k_sort_plan(const uint32_t *hist, int64_t n, uint32_t *offsets, FrameState *st);

@@ -124,6 +124,9 @@ class SplatFrame:
 
     @property
     def pair_count(self):
+        """Tile/splat pairs of the compositor's 16 x 16 tile lists (the
+        reference's bbox lists, ``len(tile_ids)``, also keep the pairs whose
+        support cannot reach the tile)."""
         self.sync()
         return int(self.info.k)
 
@@ -185,7 +188,10 @@ class SplatFrame:
         _lib.check(_lib.lib().hgs_frame_export_arrays(
             sc, _lib.camera_struct(self.camera), _lib.settings_struct(self.settings, self.flags),
             _lib.ptr(self.buf), self.info, ex, _lib.current_stream_handle(dev)), "frame export")
-        if self.tile_size != _lib.COMPOSITOR_TILE:
+        if not (self.flags & _lib.HGS_FLAG_NAIVE):
+            # the reference's lists (bbox-based, project.py:329-357) at the
+            # settings' tile size; the compositor's own 16 x 16 lists drop the
+            # tiles its support cannot reach (hgs_frame_tile_bins)
             d["tile_offsets"], d["tile_ids"] = self._rebin(self.tile_size)
             k = int(d["tile_ids"].shape[0])
         out = {f: (t.cpu().numpy() if t is not None else None) for f, t in d.items()}
@@ -205,7 +211,8 @@ class SplatFrame:
         W, H = self.width, self.height
         n_tiles = ((W + tile - 1) // tile) * ((H + tile - 1) // tile)
         offsets = torch.empty(n_tiles + 1, dtype=torch.int64, device=dev)
-        cap = max(self.pair_count * (16 // tile) ** 2 + self.count, 1) if tile < 16 else max(self.pair_count, 1)
+        # the compositor's lists are culled: the bbox lists are longer (~1.5x)
+        cap = max(2 * self.pair_count * max(16 // tile, 1) ** 2 + self.count, 1)
         for _ in range(2):
             nb = L.hgs_tile_bins_scratch_bytes(self.count, W, H, tile, cap)
             scratch = torch.empty(nb, dtype=torch.uint8, device=dev)

@@ -69,7 +69,9 @@ def test_config2_full_size():
     from paper_2512_02932_b200.synthetic import synthetic_scene
     scene, cam = synthetic_scene(1_000_000, 1920, 1080, 3, seed=0)
     out, errs = _compare(scene, cam, RenderSettings(), kg=1)
-    assert out.frame.pair_count > 4_000_000
+    # the reference's bbox lists (compared bit-exactly by _compare) hold
+    # 4.56 M pairs; the compositor's culled lists fewer
+    assert out.frame.export()["tile_ids"].size > 4_000_000 > out.frame.pair_count
     print("config2 errors", errs)
 
 

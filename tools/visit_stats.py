@@ -49,3 +49,24 @@ ub = uk // (1 << 24)
 same = ub[1:] == ub[:-1]
 small = (n[1:] <= 16) & (n[:-1] <= 16)
 print("consecutive same-block visits both n<=16: %.2f%%" % (100.0 * float((same & small).sum()) / tot))
+
+# pairing candidates: consecutive visits of one block (walk order), both with
+# <= 16 pixels, the same splat type and disjoint pixel sets
+typ = torch.from_numpy(fr.typ.astype(np.int64)).cuda()  # by slot (rank)
+lx = (ix % 8) if os.environ.get("BLOCK", "8x16") != "16x16" else (ix % 16)
+ly = iy % 16
+bit = (ly * 8 + lx) if os.environ.get("BLOCK", "8x16") != "16x16" else (ly * 16 + lx)
+inv = torch.empty_like(key)
+order = torch.argsort(key)
+ks = key[order]
+vid = torch.searchsorted(uk, ks)  # visit index of each (sorted) pair
+b = bit[order]
+lo_m = torch.zeros(uk.numel(), dtype=torch.int64, device="cuda")
+hi_m = torch.zeros(uk.numel(), dtype=torch.int64, device="cuda")
+one = torch.ones_like(b)
+lo_m.index_put_((vid[b < 64],), torch.bitwise_left_shift(one[b < 64], b[b < 64]), accumulate=True)
+hi_m.index_put_((vid[b >= 64],), torch.bitwise_left_shift(one[b >= 64], b[b >= 64] - 64), accumulate=True)
+vt = typ[uk % (1 << 24)]
+cand = same & small & (vt[1:] == vt[:-1]) & ((lo_m[1:] & lo_m[:-1]) == 0) & ((hi_m[1:] & hi_m[:-1]) == 0)
+print("adjacent pairs: same block, both n<=16, same type, disjoint pixels: %.2f%% of visits"
+      % (100.0 * float(cand.sum()) / tot))
