@@ -18,7 +18,7 @@ constexpr int kMaxGrid = 148 * 8;
 #endif
 
 struct Layout {
-  size_t state, hist_d, off_d, hist_p, off_p, keys_a, keys_b, vals_a, vals_b, rank, order, counts, kept, lb_sort, lb_scan,
+  size_t state, hist_d, off_d, hist_p, off_p, keys_a, keys_b, vals_a, vals_b, rank, order, counts, keep, kept, lb_sort, lb_scan,
       recs, recs64, cull2d, eig, pair_off,
       pk_a, pk_b, pv_a, pv_b, tile_off, pix_T, pix_last, pix_count, fwd_fix, bwd_fix, pix_mask, total;
   size_t small_end;  // [state, small_end) is zeroed at the start of a forward
@@ -54,6 +54,7 @@ Layout make_layout(int64_t n, int W, int H, int64_t cap) {
   L.rank = take(nn * 4);   // depth rank of each Gaussian (0xffffffff: culled)
   L.order = take(nn * 4);  // the depth order, rank -> Gaussian
   L.counts = take(nn * 4); // tiles per Gaussian (by index; 0: culled)
+  L.keep = take(nn * 4);   // bbox tiles kept by the tile-level cull (bit mask, k_tile_counts)
   L.kept = take(nn);       // k_depth_keys' culls, read by the preprocess
   L.recs = take(nn * sizeof(SplatRec));
   L.recs64 = take(nn * sizeof(Rec64));
@@ -302,7 +303,8 @@ int hgs_forward(const hgs_scene *scene, const hgs_camera *camera, const hgs_sett
     HGS_LAUNCHED();
     if (HGS_TILE_COUNTS_AUX) {
       k_tile_counts<<<grid_for(n, 256), 256, 0, fork ? aux : s>>>(at<SplatRec>(frame, L.recs),
-                                                                  at<float4>(frame, L.cull2d), n, counts);
+                                                                  at<float4>(frame, L.cull2d), n, counts,
+                                                                  at<uint32_t>(frame, L.keep));
       HGS_LAUNCHED();
     }
     if (fork) HGS_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(settings->aux_events[1]), aux));
@@ -329,7 +331,7 @@ int hgs_forward(const hgs_scene *scene, const hgs_camera *camera, const hgs_sett
     if (fork) HGS_CUDA(cudaStreamWaitEvent(s, static_cast<cudaEvent_t>(settings->aux_events[1]), 0));
     if (!HGS_TILE_COUNTS_AUX) {  // the tile-level cull of the counts, after the join
       k_tile_counts<<<grid_for(n, 256), 256, 0, s>>>(at<SplatRec>(frame, L.recs), at<float4>(frame, L.cull2d), n,
-                                                     counts);
+                                                     counts, at<uint32_t>(frame, L.keep));
       HGS_LAUNCHED();
     }
     HGS_CUDA(cudaMemsetAsync(at<char>(frame, L.lb_scan), 0, L.lb_scan_bytes, s));
@@ -348,7 +350,7 @@ int hgs_forward(const hgs_scene *scene, const hgs_camera *camera, const hgs_sett
   if (n > 0) {
     k_duplicate<<<grid_for(n, 256), 256, 0, s>>>(at<SplatRec>(frame, L.recs), order,
                                                  at<unsigned long long>(frame, L.pair_off), -1, st, cam.tiles_x,
-                                                 kTileShift, false, true, at<float4>(frame, L.cull2d),
+                                                 kTileShift, false, true, at<uint32_t>(frame, L.keep),
                                                  at<uint32_t>(frame, L.pk_a),
                                                  at<uint32_t>(frame, L.pv_a), nd, at<uint32_t>(frame, L.hist_p));
     HGS_LAUNCHED();

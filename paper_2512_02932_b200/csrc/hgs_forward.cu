@@ -195,7 +195,7 @@ __device__ __forceinline__ void write_record(const ProjD &o, uint32_t idx, int W
 // latency-bound preprocess 0.09 ms at config 2).
 __global__ void __launch_bounds__(256) k_tile_counts(const SplatRec *__restrict__ recs,
                                                      const float4 *__restrict__ cull2d, int64_t n,
-                                                     uint32_t *__restrict__ counts) {
+                                                     uint32_t *__restrict__ counts, uint32_t *__restrict__ keep) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const uint32_t nt = counts[i];  // bbox tiles (0: culled or off screen)
     if (nt <= 1u || nt > (uint32_t)kTileCullMax) continue;  // one tile: the compositor's warp cull suffices
@@ -210,10 +210,12 @@ __global__ void __launch_bounds__(256) k_tile_counts(const SplatRec *__restrict_
     }
     const int4 q = r.r5;
     const int x0 = q.x & 0xffff, y0 = (int)((uint32_t)q.x >> 16), x1 = q.y & 0xffff, y1 = (int)((uint32_t)q.y >> 16);
-    uint32_t cnt = 0;
+    uint32_t bits = 0, b = 1;  // bit j: the j-th bbox tile (row-major) is kept
     for (int ty = y0 / kTile; ty <= y1 / kTile; ++ty)
-      for (int tx = x0 / kTile; tx <= x1 / kTile; ++tx) cnt += tile_culled(r, c2, tx, ty, x0, y0, x1, y1) ? 0u : 1u;
-    counts[i] = cnt;
+      for (int tx = x0 / kTile; tx <= x1 / kTile; ++tx, b <<= 1)
+        if (!tile_culled(r, c2, tx, ty, x0, y0, x1, y1)) bits |= b;
+    counts[i] = (uint32_t)__popc(bits);
+    keep[i] = bits;
   }
 }
 
@@ -421,14 +423,14 @@ constexpr int kDupOwn = 32;
 
 // order: rank -> Gaussian (records are by Gaussian); the pair value is the
 // Gaussian index, or the rank with emit_rank (the SplatFrame export's slots).
-// tile_cull (the compositor's lists, 16 x 16 tiles): splats with at most
-// kTileCullMax bbox tiles skip the tiles tile_culled rejects -- the counts
-// the scan used were formed by the same test (write_record).
+// tile_cull (the compositor's lists, 16 x 16 tiles): splats with 2 ..
+// kTileCullMax bbox tiles emit only the tiles of their k_tile_counts keep
+// mask (the counts the scan used are its popcounts).
 __global__ void __launch_bounds__(256) k_duplicate(const SplatRec *__restrict__ recs,
                                                    const uint32_t *__restrict__ order,
                                                    const unsigned long long *__restrict__ pair_off, int64_t m,
                                                    const FrameState *__restrict__ st, int tiles_x, int tile_shift,
-                                                   bool emit_rank, bool tile_cull, const float4 *__restrict__ cull2d,
+                                                   bool emit_rank, bool tile_cull, const uint32_t *__restrict__ keep,
                                                    uint32_t *__restrict__ pkeys, uint32_t *__restrict__ pvals,
                                                    int n_digits, uint32_t *__restrict__ hist) {
   __shared__ uint32_t sh[2 * kRadix];
@@ -468,25 +470,10 @@ __global__ void __launch_bounds__(256) k_duplicate(const SplatRec *__restrict__ 
     }
     static_assert(kTileCullMax <= kDupOwn, "culled splats take the per-lane path");
     if (cnt <= (uint32_t)kDupOwn) {
-      const bool cull = tile_cull && cnt > 1u;  // the k_tile_counts rule
-      SplatRec rc;
-      float4 c2[2] = {make_float4(0.f, 0.f, 0.f, 0.f), make_float4(0.f, 0.f, 0.f, 0.f)};
-      if (cull) {
-        const SplatRec *gp = recs + g;
-        rc.r0 = __ldg(&gp->r0); rc.r1 = __ldg(&gp->r1); rc.r4 = __ldg(&gp->r4); rc.r5 = q;  // r4.w: the type bit
-        rc.r2 = rc.r3 = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (!rec_is3d(rc)) {
-          c2[0] = __ldg(cull2d + 2 * (size_t)g);
-          c2[1] = __ldg(cull2d + 2 * (size_t)g + 1);
-        }
-      }
-      const int bx0 = q.x & 0xffff, by0 = (int)((uint32_t)q.x >> 16), bx1 = q.y & 0xffff,
-                by1 = (int)((uint32_t)q.y >> 16);
+      const uint32_t bits = (tile_cull && cnt > 1u) ? __ldg(keep + g) : 0xffffffffu;  // the k_tile_counts rule
       uint32_t k = 0;
       for (uint32_t j = 0, dy = 0, dx = 0; j < cnt; ++j) {  // row-major over the tile rectangle
-        const int tx = tx0 + (int)dx, ty = ty0 + (int)dy;
-        if (!cull || !tile_culled(rc, c2, tx, ty, bx0, by0, bx1, by1))
-          emit((uint32_t)(ty * tiles_x + tx), o + k++, val);
+        if ((bits >> j) & 1u) emit((uint32_t)((ty0 + (int)dy) * tiles_x + tx0 + (int)dx), o + k++, val);
         if (++dx == (uint32_t)bw) { dx = 0; ++dy; }
       }
     }

@@ -687,12 +687,13 @@ cudaError_t launch_preprocess(const SceneView &sc, const CamD &cam, const ModD &
                               cudaStream_t s);
 __global__ void k_scan_counts(const uint32_t *counts, const uint32_t *order, int64_t m, unsigned long long *pair_off,
                               unsigned long long *scan_lb, FrameState *st, int64_t cap);
-__global__ void k_tile_counts(const SplatRec *recs, const float4 *cull2d, int64_t n, uint32_t *counts);
+__global__ void k_tile_counts(const SplatRec *recs, const float4 *cull2d, int64_t n, uint32_t *counts,
+                              uint32_t *keep);
 __global__ void k_rebin_counts(const SplatRec *recs, const uint32_t *order, int64_t m, int tile_shift,
                                uint32_t *counts);
 __global__ void k_duplicate(const SplatRec *recs, const uint32_t *order, const unsigned long long *pair_off, int64_t m,
                             const FrameState *st, int tiles_x, int tile_shift, bool emit_rank, bool tile_cull,
-                            const float4 *cull2d, uint32_t *pkeys, uint32_t *pvals, int n_digits, uint32_t *hist);
+                            const uint32_t *keep, uint32_t *pkeys, uint32_t *pvals, int n_digits, uint32_t *hist);
 __global__ void k_tile_ranges(const uint32_t *skeys, int64_t k, const FrameState *st, int64_t n_tiles,
                               uint32_t *tile_off);
 __global__ void k_sort_plan(const uint32_t *hist, int64_t n, uint32_t *offsets, FrameState *st);
