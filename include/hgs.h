@@ -223,7 +223,11 @@ int hgs_exchange_f64(int64_t n, double *log_scale, double *rotation, uint8_t *ty
  * depth (m), center2d (m,2), cov2d (m,3), conic (m,3), mrow (m,3,4),
  * alpha_eff (m), color (m,3), bbox (m,4) i32, radius (m), tile_offsets
  * (n_tiles+1) i64, tile_ids (k) i32.  Values are the float64 preprocess
- * results (bit-for-bit what the binning used). */
+ * results (bit-for-bit what the binning used).  tile_offsets / tile_ids are
+ * the COMPOSITOR's 16 x 16 lists (slots, depth order): they omit the
+ * (splat, tile) pairs whose support cannot reach the tile, so they are a
+ * subset of the reference's bbox lists (project.py:329-357) -- those come
+ * from hgs_frame_tile_bins (any tile size, 16 included). */
 typedef struct hgs_frame_export {
   int32_t *idx;
   uint8_t *typ;
@@ -255,10 +259,12 @@ int hgs_blend_log(const hgs_scene *scene, const hgs_camera *camera, const hgs_se
  *  [9] pairs evaluated. */
 int hgs_frame_stats(const void *frame, const hgs_frame_info *info, uint64_t *out16, void *stream);
 
-/* [ABI 3] Tile lists of a frame at another tile size.  The compositor always
- * bins at 16 x 16; the reference bins at settings.tile_size (project.py:37,
- * _tile_bins :329-357) and only SplatFrame.tile_offsets / tile_ids depend on
- * it (the image does not).  tile_size in {8, 16, 32, 64}.  Synchronous:
+/* [ABI 3] The reference's tile lists of a frame (bbox-based, _tile_bins
+ * project.py:329-357) at any tile size.  The compositor always bins at
+ * 16 x 16 and drops the pairs its support cannot reach; the reference bins
+ * every tile of the bbox at settings.tile_size (project.py:37), and only
+ * SplatFrame.tile_offsets / tile_ids depend on it (the image does not).
+ * tile_size in {8, 16, 32, 64}.  Synchronous:
  * counts the pairs into *k_out and returns HGS_ERR_PAIR_CAPACITY when
  * ids_capacity < *k_out; otherwise writes tile_offsets ((tiles+1) i64) and
  * tile_ids (*k_out i32, sorted slots, ascending within a tile).  scratch:
