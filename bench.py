@@ -793,8 +793,10 @@ def main():
             torch.cuda.synchronize()
             if i >= a.e2e_warmup:
                 ts.append(time.perf_counter() - t0)
-        d2h = (4 * (out.color.size + out.depth.size + out.transmittance.size + out.alpha.size
-                    + out.normal.size + gr.flat().size) + touched.size)
+        # the reference's outputs: colour, depth, transmittance, ParamGrads, touched
+        # (the extension images alpha / normal download on first access)
+        d2h = (4 * (out.color.size + out.depth.size + out.transmittance.size + gr.flat().size)
+               + touched.size)
         tt = float(np.mean(ts))
         if world > 1:
             t = torch.tensor([tt], device=dev, dtype=torch.float64)
@@ -803,7 +805,7 @@ def main():
         e2e = {"value": world / tt, "unit": "iters/s", "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h),
                "path": "raster.render(GaussianSet float64 numpy) + grad.backward(numpy pixel_grad)"
-                       " -> numpy float64 images and ParamGrads (geometry float64, SH / images / gradients float32 over PCIe via pinned staging; conversions on the host cores); wall clock with device syncs"}
+                       " -> numpy float64 colour / depth / transmittance and ParamGrads (the reference's outputs; the extension images download on first access) (geometry float64, SH / images / gradients float32 over PCIe via pinned staging, 40% of the large outputs widened on the GPU; conversions on the host cores); wall clock with device syncs"}
 
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:

@@ -247,19 +247,47 @@ class SplatFrame:
 class RenderOutput:
     """raster/render.py:54-65.  ``color``/``depth``/``transmittance`` are numpy
     float64 for host scenes and float32 CUDA tensors for device scenes;
-    ``alpha`` (1 - T) and ``normal`` are the extension images."""
+    ``alpha`` (1 - T) and ``normal`` are the extension images (for host
+    scenes they are downloaded on first access: the reference has no such
+    outputs, so a drop-in caller never pays for them)."""
 
     def __init__(self, color, depth, transmittance, alpha, normal, frame, fingerprint,
-                 host_scene=None):
+                 host_scene=None, lazy=None):
         self.color = color
         self.depth = depth
         self.transmittance = transmittance
-        self.alpha = alpha
-        self.normal = normal
+        self._alpha = alpha
+        self._normal = normal
+        self._lazy = lazy or {}  # name -> device tensor still to download
         self.frame = frame
         self.scene_fingerprint = fingerprint
         self._host_scene = host_scene
         self._log = None
+
+    def _extension(self, name):
+        t = self._lazy.pop(name, None)
+        if t is not None:
+            from ._hostio import download
+            setattr(self, "_" + name, download([t], tag="ext")[0])
+        return getattr(self, "_" + name)
+
+    @property
+    def alpha(self):
+        return self._extension("alpha")
+
+    @alpha.setter
+    def alpha(self, v):
+        self._lazy.pop("alpha", None)
+        self._alpha = v
+
+    @property
+    def normal(self):
+        return self._extension("normal")
+
+    @normal.setter
+    def normal(self, v):
+        self._lazy.pop("normal", None)
+        self._normal = v
 
     def check_scene(self, scene):
         if scene_fingerprint(scene) != self.scene_fingerprint:
@@ -416,10 +444,11 @@ def _render(scene, camera, settings, naive, fast):
     ds = DeviceGaussians.from_host(scene)
     imgs, frame = rasterize(ds, camera, settings, flags)
     from ._hostio import download
-    keys = ("color", "depth", "transmittance", "alpha", "normal")
+    keys = ("color", "depth", "transmittance")
     host = dict(zip(keys, download([imgs[k] for k in keys], tag="images")))
-    return RenderOutput(host["color"], host["depth"], host["transmittance"], host["alpha"],
-                        host["normal"], frame, scene_fingerprint(scene), host_scene=scene)
+    return RenderOutput(host["color"], host["depth"], host["transmittance"], None, None, frame,
+                        scene_fingerprint(scene), host_scene=scene,
+                        lazy={"alpha": imgs["alpha"], "normal": imgs["normal"]})
 
 
 def render(scene, camera, settings: RenderSettings = None, *, fast=False) -> RenderOutput:
