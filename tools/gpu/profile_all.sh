@@ -7,7 +7,7 @@ set -x
 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file gpurun_out/launches_c2.csv \
   python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline > gpurun_out/launches_c2.log 2>&1
 ncu --set full --clock-control none \
-  -k regex:"k_depth_keys|k_sort_plan|k_onesweep|k_rank_scatter|k_preprocess|k_scan_counts|k_duplicate|k_tile_ranges|k_composite|k_fixup|k_chain_rule" \
+  -k regex:"k_depth_keys|k_sort_plan|k_onesweep|k_rank_scatter|k_preprocess|k_tile_counts|k_scan_counts|k_duplicate|k_tile_ranges|k_composite|k_fixup|k_chain_rule" \
   -s 60 -c 60 -o /tmp/prof_c2 python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/prof_c2.log 2>&1
 ncu -i /tmp/prof_c2.ncu-rep --page raw --csv > gpurun_out/prof_c2_raw.csv
 ncu --set full --clock-control none -k regex:"k_loss|k_optim|k_composite_bwd|k_chain" -s 6 -c 6 \

@@ -82,7 +82,7 @@ def main():
     stage = {"composite_fwd": ["k_composite_fwd"], "composite_bwd": ["k_composite_bwd"],
              "chain_rule(+touched)": ["k_chain_rule"],
              "depth_keys+sort||preprocess_f64": ["k_depth_keys", "k_sort_plan", "k_onesweep<unsigned long long>",
-                                                 "k_rank_scatter", "k_preprocess"],
+                                                 "k_rank_scatter", "k_preprocess", "k_tile_counts"],
              "scan": ["k_scan_counts"],
              "binning(dup+tile sort+ranges)": ["k_duplicate", "k_radix_offsets", "k_onesweep<unsigned int>",
                                                "k_tile_ranges"]}
