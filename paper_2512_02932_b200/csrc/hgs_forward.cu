@@ -189,8 +189,8 @@ __device__ __forceinline__ void write_record(const ProjD &o, uint32_t idx, int W
 }
 
 // Tile counts of the compositor's lists: a splat whose bbox spans at most
-// kTileCullMax tiles keeps only the tiles tile_culled accepts (k_duplicate
-// emits with the same test on the same record).  A separate, fully occupied
+// kTileCullMax tiles keeps only the tiles tile_cull_test keeps (k_duplicate
+// emits exactly those bits).  A separate, fully occupied
 // pass after the float64 preprocess (inside it the loop over tiles cost the
 // latency-bound preprocess 0.09 ms at config 2).
 __global__ void __launch_bounds__(256) k_tile_counts(const SplatRec *__restrict__ recs,
@@ -210,10 +210,14 @@ __global__ void __launch_bounds__(256) k_tile_counts(const SplatRec *__restrict_
     }
     const int4 q = r.r5;
     const int x0 = q.x & 0xffff, y0 = (int)((uint32_t)q.x >> 16), x1 = q.y & 0xffff, y1 = (int)((uint32_t)q.y >> 16);
+    // the splat's side of cull_rect, once (tile_culled per tile repeats it)
+    const TileCull tc = tile_cull_prep(r, c2);
     uint32_t bits = 0, b = 1;  // bit j: the j-th bbox tile (row-major) is kept
     for (int ty = y0 / kTile; ty <= y1 / kTile; ++ty)
       for (int tx = x0 / kTile; tx <= x1 / kTile; ++tx, b <<= 1)
-        if (!tile_culled(r, c2, tx, ty, x0, y0, x1, y1)) bits |= b;
+        if (!tile_cull_test(tc, max(tx * kTile, x0), max(ty * kTile, y0), min(tx * kTile + kTile - 1, x1),
+                            min(ty * kTile + kTile - 1, y1)))
+          bits |= b;
     counts[i] = (uint32_t)__popc(bits);
     keep[i] = bits;
   }

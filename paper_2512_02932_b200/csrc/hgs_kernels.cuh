@@ -255,18 +255,60 @@ __device__ __forceinline__ bool cull_splat_pre(const SplatRec &r, const float4 *
   return cull_rect(r, c2, wx0 + (c0 & 7), wy0 + (c0 >> 3), wx0 + (c1 & 7), wy0 + (c1 >> 3));
 }
 
+// cull_rect split into its per-splat part (once) and its per-rectangle
+// part: the same arithmetic, so the decisions are identical.
+struct TileCull {
+  float A, B, C, cx, cy, thr, dlow, rcx, rcy;
+  int ax, ay;
+  bool never, is3d, conic;
+};
+__device__ __forceinline__ TileCull tile_cull_prep(const SplatRec &r, const float4 *c2) {
+  TileCull t;
+  const float dstar = (r.r0.w - kArgMinAlpha) * (1.f / kHalfLog2e);
+  t.never = dstar < 0.f;
+  t.is3d = rec_is3d(r);
+  t.ax = r.r5.z;
+  t.ay = r.r5.w;
+  t.rcx = r.r0.x;
+  t.rcy = r.r0.y;
+  t.dlow = fmaf(dstar, 1.05f, 1e-3f);
+  t.conic = true;
+  if (t.is3d) {
+    const float4 e = r.r1;
+    t.A = fmaf(e.z * e.x, e.x, e.w * e.y * e.y);
+    t.B = (e.z - e.w) * e.x * e.y;
+    t.C = fmaf(e.z * e.y, e.y, e.w * e.x * e.x);
+    t.cx = r.r0.x; t.cy = r.r0.y;
+    t.thr = fmaf(dstar, 1.001f, 1e-3f);
+  } else {
+    const float4 k0 = c2[0], k1 = c2[1];
+    t.conic = k1.y > 0.f;
+    t.A = k0.x; t.B = k0.y; t.C = k0.z;
+    t.cx = k0.w; t.cy = k1.x;
+    t.thr = 1.05f;
+  }
+  return t;
+}
+// true: no pixel centre of [x0, x1] x [y0, y1] can reach the cutoff
+__device__ __forceinline__ bool tile_cull_test(const TileCull &t, int x0, int y0, int x1, int y1) {
+  if (t.never) return true;
+  const float PX0 = (float)(x0 - t.ax) + 0.5f, PX1 = (float)(x1 - t.ax) + 0.5f;
+  const float PY0 = (float)(y0 - t.ay) + 0.5f, PY1 = (float)(y1 - t.ay) + 0.5f;
+  if (!t.is3d) {
+    const float ex = fmaxf(fmaxf(PX0 - t.rcx, t.rcx - PX1), 0.f);
+    const float ey = fmaxf(fmaxf(PY0 - t.rcy, t.rcy - PY1), 0.f);
+    if (4.f * (ex * ex + ey * ey) <= t.dlow) return false;  // low-pass circle reaches
+    if (!t.conic) return false;                             // no well-conditioned ray conic: keep
+  }
+  return rect_min_quad(t.A, t.B, t.C, PX0 - t.cx, PX1 - t.cx, PY0 - t.cy, PY1 - t.cy) > t.thr;
+}
+
 // Tile-level cull of the binning: splats whose bbox spans at most
 // kTileCullMax tiles list only the tiles whose part of the bbox the support
 // can reach (35% of the bbox pairs at config 2 have no contributing pixel).
-// The preprocess counts and k_duplicate emits with this one function on the
-// same float32 record, so counts and emitted pairs agree exactly.
+// k_tile_counts decides once per tile (tile_cull_prep / tile_cull_test) and
+// k_duplicate emits exactly the kept bits, so counts and pairs agree.
 constexpr int kTileCullMax = 32;
-__device__ __forceinline__ bool tile_culled(const SplatRec &r, const float4 *c2, int tx, int ty, int bx0, int by0,
-                                            int bx1, int by1) {
-  const int x0 = max(tx * kTile, bx0), x1 = min(tx * kTile + kTile - 1, bx1);
-  const int y0 = max(ty * kTile, by0), y1 = min(ty * kTile + kTile - 1, by1);
-  return cull_rect(r, c2, x0, y0, x1, y1);
-}
 
 #ifndef HGS_CULL_2D
 #define HGS_CULL_2D 1
