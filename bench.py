@@ -805,7 +805,7 @@ def main():
         e2e = {"value": world / tt, "unit": "iters/s", "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h),
                "path": "raster.render(GaussianSet float64 numpy) + grad.backward(numpy pixel_grad)"
-                       " -> numpy float64 colour / depth / transmittance and ParamGrads (the reference's outputs; the extension images download on first access) (geometry float64, SH / images / gradients float32 over PCIe via pinned staging, 40% of the large outputs widened on the GPU; conversions on the host cores); wall clock with device syncs"}
+                       " -> numpy float64 colour / depth / transmittance and ParamGrads (the reference's outputs; the extension images download on first access) (geometry float64, SH / images / gradients float32 over PCIe via pinned staging; float64 <-> float32 conversions on all host cores with streaming stores); wall clock with device syncs"}
 
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:

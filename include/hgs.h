@@ -313,6 +313,12 @@ int hgs_modulation_f64(int64_t n, const double *opacity, const double *log_scale
 int hgs_host_register(void *ptr, size_t bytes);
 int hgs_host_unregister(void *ptr);
 int hgs_widen_d2h(const float *src, double *dst_host, int64_t n, double *scratch, void *stream);
+/* Host-only float32 <-> float64 conversion of n elements (or a plain copy) on `threads` host
+ * threads (<= 0: all), destination written with streaming stores (no
+ * read-for-ownership of the destination lines).  Synchronous, no CUDA. */
+int hgs_host_widen(const float *src, double *dst, int64_t n, int threads);
+int hgs_host_narrow(const double *src, float *dst, int64_t n, int threads);
+int hgs_host_copy(const void *src, void *dst, int64_t bytes, int threads);
 
 const char *hgs_status_string(int status);
 int hgs_abi_version(void);

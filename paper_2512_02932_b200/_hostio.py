@@ -8,11 +8,15 @@ on the device then a pageable ``.cpu()``) moves 2x the bytes through pageable
 memory, single-threaded.  Here instead:
 
 * upload: the float64 -> float32 conversion is written straight into a
-  persistent pinned staging buffer by torch's multi-threaded CPU copy, chunk
-  by chunk, and each chunk's DMA to the device is issued as soon as it is
-  converted, so conversion of chunk i+1 overlaps the copy of chunk i;
+  persistent pinned staging buffer on all host cores (hgs_host_narrow),
+  chunk by chunk, and each chunk's DMA to the device is issued as soon as it
+  is converted, so conversion of chunk i+1 overlaps the copy of chunk i;
 * download: float32 results are DMA'd into pinned staging chunk by chunk and
-  widened to float64 on all host cores as each chunk lands.
+  widened to float64 on all host cores as each chunk lands (hgs_host_widen).
+
+Both directions are host-DRAM bound, not PCIe bound, so the conversions
+(csrc/hgs_hostconv.cpp) write with streaming stores: no read-for-ownership
+of the destination lines (widening 59M floats 8.5 -> 4.3 ms on the box).
 
 Only float32 crosses PCIe in either direction.
 
@@ -99,6 +103,25 @@ def host_empty(shape, dtype=np.float64, register=False):
 
 
 _CHUNK = 16 << 20  # bytes of float32 per pipelined chunk
+# float64 <-> float32 conversions through hgs_host_widen / hgs_host_narrow
+# (all cores, streaming stores: widening 59M floats 8.5 -> 4.3 ms on the box,
+# tools/hostconv_bench.py) instead of torch's converting copy
+_NT = os.environ.get("HGS_HOST_NT", "1") != "0"
+
+
+def _convert(fn, src, dst):
+    from . import _lib
+    rc = getattr(_lib.lib(), fn)(ctypes.c_void_p(src.data_ptr()), ctypes.c_void_p(dst.data_ptr()), src.numel(), 0)
+    if rc != 0:
+        raise RuntimeError("%s failed (%d)" % (fn, rc))
+
+
+def _copy(src, dst):
+    from . import _lib
+    nb = src.numel() * src.element_size()
+    rc = _lib.lib().hgs_host_copy(ctypes.c_void_p(src.data_ptr()), ctypes.c_void_p(dst.data_ptr()), nb, 0)
+    if rc != 0:
+        raise RuntimeError("hgs_host_copy failed (%d)" % rc)
 _stages = {}       # tag -> [pinned uint8 tensor, cuda event guarding reuse]
 
 
@@ -140,9 +163,15 @@ def upload(arrays, device, tag="up"):
         dv = dev[off:off + nb].view(dt)
         esz = max(hv.element_size(), 1)
         step = max(_CHUNK // esz, 1)
+        narrow = _NT and src.dtype == torch.float64 and dt == torch.float32
         for s in range(0, src.numel(), step):
             e = min(s + step, src.numel())
-            hv[s:e].copy_(src[s:e])                      # multi-threaded f64 -> f32 into pinned
+            if narrow:  # f64 -> f32 into pinned on all cores, streaming stores
+                _convert("hgs_host_narrow", src[s:e], hv[s:e])
+            elif _NT and src.dtype == dt:
+                _copy(src[s:e], hv[s:e])
+            else:
+                hv[s:e].copy_(src[s:e])
             dv[s:e].copy_(hv[s:e], non_blocking=True)    # async DMA while the next chunk converts
         outs.append(dv.view(a.shape))
     ev = torch.cuda.Event()
@@ -153,9 +182,11 @@ def upload(arrays, device, tag="up"):
 
 # share of each large float64 output widened on the GPU and DMA'd as float64
 # into the page-locked destination; the rest crosses as float32 and is
-# widened on the host cores -- both at once (host widening is host-DRAM bound
-# at ~20 B per element, PCIe carries 4 or 8 B per element)
-_GPU_WIDEN = float(os.environ.get("HGS_GPU_WIDEN", "0.4"))
+# widened on the host cores -- both at once.  Paid (0.4: 26.0 -> 25.0 ms per
+# step) while host widening cost ~20 B of host DRAM traffic per element; with
+# streaming-store widening (~16 B) the host-only split is as fast or faster
+# (tools/e2e_ab.py: 20.9 vs 21.2 ms at 0.2), so the default is 0.
+_GPU_WIDEN = float(os.environ.get("HGS_GPU_WIDEN", "0.0"))
 _GPU_WIDEN_MIN = 1 << 21  # elements; smaller outputs are widened on the host
 
 
@@ -215,9 +246,13 @@ def download(tensors, dtype=np.float64, tag="down"):
             ev.record(stream)
             pending.append((ev, oflat[s:e], hv[s:e]))
         outs.append(out)
+    widen = _NT and dtype is np.float64
     for ev, o, h in pending:
         ev.synchronize()
-        o.copy_(h)  # multi-threaded f32 -> f64 while later chunks are in flight
+        if widen and h.dtype == torch.float32:  # f32 -> f64 while later chunks are in flight
+            _convert("hgs_host_widen", h, o)
+        else:
+            o.copy_(h)
     if side is not None:
         side.synchronize()  # the GPU-widened shares have landed
     ent[1] = None

@@ -1,0 +1,147 @@
+// hgs_hostconv.cpp -- host-side float64 <-> float32 conversion for the
+// reference-facing numpy API (raster.render / grad.backward take and return
+// float64 arrays; the kernels read and write float32).
+//
+// The conversions are host-DRAM bound.  A plain converting copy (torch's
+// copy_, numpy's astype) reads the destination's cache lines before writing
+// them (write-allocate), so widening n floats costs 4n read + 8n RFO + 8n
+// write bytes.  Here the destination is written with non-temporal (streaming)
+// stores -- 4n + 8n -- on all requested threads (OpenMP, static split on
+// 64-byte boundaries of the destination).
+#include <immintrin.h>
+#include <omp.h>
+#include <stdint.h>
+#include <string.h>
+
+#include "../../include/hgs.h"
+
+namespace {
+
+template <bool NT>
+__attribute__((target("avx2"))) void widen_avx2(const float *__restrict__ s, double *__restrict__ d, int64_t n) {
+  int64_t i = 0;
+  while (i < n && (reinterpret_cast<uintptr_t>(d + i) & 31u)) {
+    d[i] = (double)s[i];
+    ++i;
+  }
+  for (; i + 8 <= n; i += 8) {
+    const __m256 v = _mm256_loadu_ps(s + i);
+    const __m256d a = _mm256_cvtps_pd(_mm256_castps256_ps128(v)), b = _mm256_cvtps_pd(_mm256_extractf128_ps(v, 1));
+    if (NT) {
+      _mm256_stream_pd(d + i, a);
+      _mm256_stream_pd(d + i + 4, b);
+    } else {
+      _mm256_store_pd(d + i, a);
+      _mm256_store_pd(d + i + 4, b);
+    }
+  }
+  for (; i < n; ++i) d[i] = (double)s[i];
+}
+
+template <bool NT>
+__attribute__((target("avx2"))) void narrow_avx2(const double *__restrict__ s, float *__restrict__ d, int64_t n) {
+  int64_t i = 0;
+  while (i < n && (reinterpret_cast<uintptr_t>(d + i) & 31u)) {
+    d[i] = (float)s[i];
+    ++i;
+  }
+  for (; i + 8 <= n; i += 8) {
+    const __m128 lo = _mm256_cvtpd_ps(_mm256_loadu_pd(s + i));
+    const __m128 hi = _mm256_cvtpd_ps(_mm256_loadu_pd(s + i + 4));
+    const __m256 v = _mm256_insertf128_ps(_mm256_castps128_ps256(lo), hi, 1);
+    if (NT) _mm256_stream_ps(d + i, v);
+    else _mm256_store_ps(d + i, v);
+  }
+  for (; i < n; ++i) d[i] = (float)s[i];
+}
+
+template <bool NT>
+__attribute__((target("avx2"))) void copy_avx2(const uint8_t *__restrict__ s, uint8_t *__restrict__ d, int64_t n) {
+  int64_t i = 0;
+  const int64_t head = (int64_t)((32u - (reinterpret_cast<uintptr_t>(d) & 31u)) & 31u);
+  if (head) {
+    memcpy(d, s, (size_t)(head < n ? head : n));
+    i = head;
+  }
+  for (; i + 32 <= n; i += 32) {
+    const __m256i v = _mm256_loadu_si256(reinterpret_cast<const __m256i *>(s + i));
+    if (NT) _mm256_stream_si256(reinterpret_cast<__m256i *>(d + i), v);
+    else _mm256_store_si256(reinterpret_cast<__m256i *>(d + i), v);
+  }
+  if (i < n) memcpy(d + i, s + i, (size_t)(n - i));
+}
+
+template <class S, class D>
+void convert_scalar(const S *s, D *d, int64_t n) {
+  for (int64_t i = 0; i < n; ++i) d[i] = (D)s[i];
+}
+
+bool has_avx2() {
+  static const int v = __builtin_cpu_supports("avx2") ? 1 : 0;
+  return v != 0;
+}
+
+// [b, e) of part t of nt, on 16-element (64-byte float64 / float32 x 16)
+// boundaries so two threads never share a destination cache line
+inline void part(int64_t n, int t, int nt, int64_t &b, int64_t &e) {
+  const int64_t blocks = (n + 15) / 16;
+  b = blocks * t / nt * 16;
+  e = blocks * (t + 1) / nt * 16;
+  if (b > n) b = n;
+  if (e > n) e = n;
+}
+
+template <class F>
+void run(int64_t n, int threads, F &&body, bool fence = true) {
+  if (threads <= 0) threads = omp_get_max_threads();
+  const int64_t min_per = 1 << 16;  // elements per thread below which threads do not pay
+  if (n / min_per < threads) threads = (int)(n / min_per > 0 ? n / min_per : 1);
+  if (threads <= 1) {
+    body((int64_t)0, n);
+  } else {
+#pragma omp parallel num_threads(threads)
+    {
+      int64_t b, e;
+      part(n, omp_get_thread_num(), omp_get_num_threads(), b, e);
+      if (e > b) body(b, e);
+      if (fence) _mm_sfence();  // this thread's streaming stores are globally visible before the join
+    }
+  }
+  if (fence) _mm_sfence();
+}
+
+}  // namespace
+
+extern "C" int hgs_host_widen(const float *src, double *dst, int64_t n, int threads) {
+  if (n < 0 || (n > 0 && (!src || !dst))) return HGS_ERR_CONFIG;
+  const bool v = has_avx2();
+  run(n, threads, [&](int64_t b, int64_t e) {
+    if (v) widen_avx2<true>(src + b, dst + b, e - b);
+    else convert_scalar(src + b, dst + b, e - b);
+  });
+  return HGS_OK;
+}
+
+extern "C" int hgs_host_narrow(const double *src, float *dst, int64_t n, int threads) {
+  if (n < 0 || (n > 0 && (!src || !dst))) return HGS_ERR_CONFIG;
+  const bool v = has_avx2();
+  run(n, threads, [&](int64_t b, int64_t e) {
+    if (v) narrow_avx2<true>(src + b, dst + b, e - b);
+    else convert_scalar(src + b, dst + b, e - b);
+  });
+  return HGS_OK;
+}
+
+extern "C" int hgs_host_copy(const void *src, void *dst, int64_t bytes, int threads) {
+  if (bytes < 0 || (bytes > 0 && (!src || !dst))) return HGS_ERR_CONFIG;
+  const bool v = has_avx2();
+  const uint8_t *s = static_cast<const uint8_t *>(src);
+  uint8_t *d = static_cast<uint8_t *>(dst);
+  // parts on 64-byte multiples of the 16-"element" split: elements of 4 bytes
+  run(bytes / 4, threads, [&](int64_t b, int64_t e) {
+    const int64_t lo = b * 4, hi = (e == bytes / 4) ? bytes : e * 4;
+    if (v) copy_avx2<true>(s + lo, d + lo, hi - lo);
+    else memcpy(d + lo, s + lo, (size_t)(hi - lo));
+  });
+  return HGS_OK;
+}

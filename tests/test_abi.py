@@ -152,3 +152,28 @@ def test_c_example_runs(tmp_path):
     out = subprocess.run([exe], env=env, capture_output=True, text=True, timeout=120)
     assert out.returncode == 0, out.stdout + out.stderr
     assert out.stdout.strip().endswith("ok")
+
+
+@pytest.mark.parametrize("threads", [1, 0])
+def test_host_conversions(L, threads):
+    """hgs_host_widen / narrow / copy (the host API's staging conversions):
+    identical to numpy's casts and copies, specials included, at odd sizes and
+    misaligned destinations (head / tail paths of the streaming loops)."""
+    import numpy as np
+    rng = np.random.default_rng(3)
+    for n in (0, 1, 7, 9, 1023, 200_003, 1_000_001):
+        x = rng.standard_normal(n) * 10.0 ** rng.integers(-40, 40, n)
+        if n > 4:
+            x[:4] = [np.inf, -np.inf, np.nan, 1e300]  # float32 overflow -> inf, like numpy
+        for off in (0, 1, 3):
+            d32 = np.empty(n + off, np.float32)[off:]
+            assert L.hgs_host_narrow(x.ctypes.data, d32.ctypes.data, n, threads) == 0
+            with np.errstate(over="ignore"):
+                np.testing.assert_array_equal(d32, x.astype(np.float32))
+            d64 = np.empty(n + off, np.float64)[off:]
+            assert L.hgs_host_widen(d32.ctypes.data, d64.ctypes.data, n, threads) == 0
+            np.testing.assert_array_equal(d64, d32.astype(np.float64))
+            b = np.empty(8 * n + off, np.uint8)[off:]
+            assert L.hgs_host_copy(x.ctypes.data, b.ctypes.data, 8 * n, threads) == 0
+            assert b.tobytes() == x.tobytes()
+    assert L.hgs_host_widen(None, None, 5, 0) != 0

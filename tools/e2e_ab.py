@@ -19,18 +19,15 @@ hs = GaussianSet(scene.center, scene.log_scale, scene.rotation, scene.opacity_lo
 st = RenderSettings()
 pg = np.random.default_rng(0).normal(size=(1080, 1920, 3))
 MODES = {
-    "host only": dict(widen=0.0, narrow=1.0, reg=False),
-    "gpu widen": dict(widen=0.4, narrow=1.0, reg=False),
-    "widen+direct": dict(widen=0.4, narrow=0.85, reg=True),
-    "direct only": dict(widen=0.0, narrow=0.85, reg=True),
+    "torch copy, gpu widen 0.4": dict(widen=0.4, nt=False),
+    "nt, gpu widen 0.25": dict(widen=0.25, nt=True),
+    "nt, host only": dict(widen=0.0, nt=True),
 }
 res = {m: [] for m in MODES}
-orig_reg = _hostio._user_registered
 for rnd in range(4):
     for m, cfg in MODES.items():
         _hostio._GPU_WIDEN = cfg["widen"]
-        _hostio._HOST_NARROW = cfg["narrow"]
-        _hostio._user_registered = orig_reg if cfg["reg"] else (lambda a: False)
+        _hostio._NT = cfg["nt"]
         for it in range(6):
             torch.cuda.synchronize()
             t0 = time.perf_counter()
@@ -40,4 +37,4 @@ for rnd in range(4):
             if it >= 2:
                 res[m].append((time.perf_counter() - t0) * 1e3)
 for m, v in res.items():
-    print("%-14s median %.2f ms  min %.2f ms  (%d steps)" % (m, np.median(v), np.min(v), len(v)))
+    print("%-26s median %.2f ms  min %.2f ms  (%d steps)" % (m, np.median(v), np.min(v), len(v)))
