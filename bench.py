@@ -107,8 +107,8 @@ def parse():
     ap.add_argument("--sh-degree", type=int, default=3)
     ap.add_argument("--kg", type=int, default=1)
     ap.add_argument("--fast", action="store_true", help="HGS_FLAG_FAST (skip f64 re-checks)")
-    ap.add_argument("--e2e-steps", type=int, default=5)
-    ap.add_argument("--e2e-warmup", type=int, default=2)
+    ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--e2e-warmup", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-steps", type=int, default=1, help="full-frame CPU baseline steps")
@@ -798,6 +798,7 @@ def main():
         d2h = (4 * (out.color.size + out.depth.size + out.transmittance.size + gr.flat().size)
                + touched.size)
         tt = float(np.mean(ts))
+        print("e2e step ms: %s" % " ".join("%.1f" % (1e3 * x) for x in ts), file=sys.stderr)
         if world > 1:
             t = torch.tensor([tt], device=dev, dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
