@@ -268,12 +268,14 @@ _aux = {}  # device index -> (side stream, fork event, join event)
 def aux_handles(device):
     """(cudaStream_t, (fork, join) cudaEvent_t) of this process's side stream
     on ``device``: hgs_forward runs the float64 preprocess on it beside the
-    depth sort."""
+    depth sort (HGS_SORT_ON_AUX builds: the other way round)."""
     import torch
     dev = torch.device(device)
     idx = dev.index if dev.index is not None else torch.cuda.current_device()
     if idx not in _aux:
-        stream = torch.cuda.Stream(device=idx)
+        # HGS_AUX_PRIORITY < 0: a higher-priority side stream (for builds with
+        # HGS_SORT_ON_AUX, where the depth sort runs on it)
+        stream = torch.cuda.Stream(device=idx, priority=int(os.environ.get("HGS_AUX_PRIORITY", "0")))
         evs = (torch.cuda.Event(), torch.cuda.Event())
         with torch.cuda.device(idx):
             for e in evs:

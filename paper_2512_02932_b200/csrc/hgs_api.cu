@@ -16,6 +16,9 @@ constexpr int kMaxGrid = 148 * 8;
 #ifndef HGS_TILE_COUNTS_AUX
 #define HGS_TILE_COUNTS_AUX 1  // 0: k_tile_counts on the main stream after the join (A/B: 268.4 vs 269.5 it/s)
 #endif
+#ifndef HGS_SORT_ON_AUX
+#define HGS_SORT_ON_AUX 0  // 1 (+ HGS_PRE_CTAS=64, HGS_AUX_PRIORITY=-5): stage 1 0.359 -> 0.353 ms, neutral end to end
+#endif
 
 struct Layout {
   size_t state, hist_d, off_d, hist_p, off_p, keys_a, keys_b, vals_a, vals_b, rank, order, counts, keep, kept, lb_sort, lb_scan,
@@ -296,39 +299,45 @@ int hgs_forward(const hgs_scene *scene, const hgs_camera *camera, const hgs_sett
       HGS_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(settings->aux_events[0]), s));
       HGS_CUDA(cudaStreamWaitEvent(aux, static_cast<cudaEvent_t>(settings->aux_events[0]), 0));
     }
+    // HGS_SORT_ON_AUX: the depth sort on the side stream and the preprocess
+    // on the caller's (a side stream created with a higher priority then
+    // hands the sort's CTAs the SMs first as the preprocess's retire)
+    cudaStream_t s_pre = (fork && !HGS_SORT_ON_AUX) ? aux : s;
+    cudaStream_t s_sort = (fork && HGS_SORT_ON_AUX) ? aux : s;
     // 3a. float64 preprocess per Gaussian (record + tile count at its index)
     HGS_CUDA(launch_preprocess(sc, cam, mod, at<uint8_t>(frame, L.kept), at<SplatRec>(frame, L.recs),
                                at<Rec64>(frame, L.recs64), at<float4>(frame, L.cull2d), at<float2>(frame, L.eig),
-                               counts, fork ? aux : s));
+                               counts, s_pre));
     HGS_LAUNCHED();
     if (HGS_TILE_COUNTS_AUX) {
-      k_tile_counts<<<grid_for(n, 256), 256, 0, fork ? aux : s>>>(at<SplatRec>(frame, L.recs),
-                                                                  at<float4>(frame, L.cull2d), n, counts,
-                                                                  at<uint32_t>(frame, L.keep));
+      k_tile_counts<<<grid_for(n, 256), 256, 0, s_pre>>>(at<SplatRec>(frame, L.recs), at<float4>(frame, L.cull2d),
+                                                         n, counts, at<uint32_t>(frame, L.keep));
       HGS_LAUNCHED();
     }
-    if (fork) HGS_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(settings->aux_events[1]), aux));
+    if (fork && !HGS_SORT_ON_AUX) HGS_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(settings->aux_events[1]), aux));
     // 2. depth sort: 8 digit passes launched, the constant ones exit at once
     uint32_t *lb = at<uint32_t>(frame, L.lb_sort);
-    HGS_CUDA(cudaMemsetAsync(lb, 0, (size_t)sort_tiles_n * kRadix * 4 * 8, s));
+    HGS_CUDA(cudaMemsetAsync(lb, 0, (size_t)sort_tiles_n * kRadix * 4 * 8, s_sort));
     for (int i = 0; i < 8; ++i) {
       unsigned long long *ka = at<unsigned long long>(frame, (i & 1) ? L.keys_b : L.keys_a);
       unsigned long long *kb = at<unsigned long long>(frame, (i & 1) ? L.keys_a : L.keys_b);
       uint32_t *va = at<uint32_t>(frame, (i & 1) ? L.vals_b : L.vals_a);
       uint32_t *vb = at<uint32_t>(frame, (i & 1) ? L.vals_a : L.vals_b);
-      k_onesweep<unsigned long long><<<(unsigned)sort_tiles_n, kSortThreads, 0, s>>>(
+      k_onesweep<unsigned long long><<<(unsigned)sort_tiles_n, kSortThreads, 0, s_sort>>>(
           ka, va, kb, vb, n, 0, at<uint32_t>(frame, L.off_d), lb + (size_t)i * sort_tiles_n * kRadix,
           st->tile_counters + 1 + i, SortDev{&st->sort_np, st->sort_digit, i, nullptr, nullptr});
       HGS_LAUNCHED();
     }
-    k_rank_scatter<<<grid_for(n, 256), 256, 0, s>>>(at<uint32_t>(frame, L.vals_a), at<uint32_t>(frame, L.vals_b), st,
-                                                    n, rank_of, order);
+    k_rank_scatter<<<grid_for(n, 256), 256, 0, s_sort>>>(at<uint32_t>(frame, L.vals_a), at<uint32_t>(frame, L.vals_b),
+                                                         st, n, rank_of, order);
     HGS_LAUNCHED();
-  }
-  HGS_CUDA(record_event(settings, 1, s));
-  // 3b. pair-offset scan over the depth order (joins the preprocess)
-  if (n > 0) {
+    if (fork && HGS_SORT_ON_AUX) HGS_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(settings->aux_events[1]), aux));
+    // join: the scan below needs both the depth order and the tile counts
     if (fork) HGS_CUDA(cudaStreamWaitEvent(s, static_cast<cudaEvent_t>(settings->aux_events[1]), 0));
+  }
+  HGS_CUDA(record_event(settings, 1, s));  // stage 1 ends at the join
+  // 3b. pair-offset scan over the depth order
+  if (n > 0) {
     if (!HGS_TILE_COUNTS_AUX) {  // the tile-level cull of the counts, after the join
       k_tile_counts<<<grid_for(n, 256), 256, 0, s>>>(at<SplatRec>(frame, L.recs), at<float4>(frame, L.cull2d), n,
                                                      counts, at<uint32_t>(frame, L.keep));
