@@ -53,6 +53,14 @@ __device__ __forceinline__ int64_t field_off(int f, int64_t n) { return (int64_t
 #define HGS_OPT_MINB 4  // 4 CTAs x 256 threads per SM: 64 registers
 #endif
 
+#ifndef HGS_OPT_KU
+#define HGS_OPT_KU 4  // elements per thread per step of the element-wise pass (x 4 loads in flight)
+#endif
+#ifndef HGS_OPT_U1
+#define HGS_OPT_U1 4  // unroll of the g_low / g_high staging loop
+#endif
+constexpr int kU1 = HGS_OPT_U1;
+
 // Templated on the SH basis count so every field width is a compile-time
 // constant (index division becomes multiply-shift; loops unroll).
 template <int OP, int B>
@@ -78,7 +86,7 @@ __global__ void __launch_bounds__(kOThreads, HGS_OPT_MINB) k_optim(OptArgs a) {
       const int cnt = gn * fw;
       const float *const glf = a.gl + base, *const ghf = a.gh + base;
       {
-#pragma unroll 4
+#pragma unroll kU1
         for (int e = tid; e < cnt; e += kOThreads) {
           const int g = e / fw, j = j0 + e - g * fw;
           sl[j][g] = __ldg(glf + e);
@@ -133,7 +141,7 @@ __global__ void __launch_bounds__(kOThreads, HGS_OPT_MINB) k_optim(OptArgs a) {
   //    Per-field base pointers + 32-bit indices keep the address arithmetic
   //    to one IMAD.WIDE per access; the surgery is branch-free:
   //    gh' = mh * (gh - ch gl), gl' = ml * (gl - cl gh)  (surgery.py:83-91)
-  constexpr int kU = 4;
+  constexpr int kU = HGS_OPT_KU;
 #pragma unroll
   for (int f = 0; f < 5; ++f) {
     const int fw = field_width(f, B), j0 = field_j0(f);
