@@ -16,6 +16,14 @@ constexpr int kMaxGrid = 148 * 8;
 #ifndef HGS_TILE_COUNTS_AUX
 #define HGS_TILE_COUNTS_AUX 1  // 0: k_tile_counts on the main stream after the join (A/B: 268.4 vs 269.5 it/s)
 #endif
+// The depth sort's chain is launched without programmatic dependence: its
+// waiting CTAs would hold SM slots the preprocess beside it needs (A/B:
+// stage 1 0.359 -> 0.368 ms with it).  The binning sort, the fixups and the
+// chain rule keep it (binning 0.145 -> 0.139 ms).
+#ifndef HGS_DEPTH_SORT_PDL
+#define HGS_DEPTH_SORT_PDL 0
+#endif
+constexpr bool kDepthSortPdl = HGS_DEPTH_SORT_PDL != 0;
 #ifndef HGS_SORT_ON_AUX
 #define HGS_SORT_ON_AUX 0  // 1 (+ HGS_PRE_CTAS=64, HGS_AUX_PRIORITY=-5): stage 1 0.359 -> 0.353 ms, neutral end to end
 #endif
@@ -177,9 +185,9 @@ int radix_sort(K *ka, K *kb, uint32_t *va, uint32_t *vb, int64_t n, const int *p
   uint32_t *vs = va, *vd = vb;
   for (int i = 0; i < npass; ++i) {
     const int p = passes[i];
-    k_onesweep<K><<<(unsigned)tiles, kSortThreads, 0, s>>>(src, vs, dst, vd, n, p * kRadixBits, offsets + p * kRadix,
-                                                           lookback + (size_t)i * tiles * kRadix, counters + i,
-                                                           SortDev{nullptr, nullptr, 0, nullptr, nullptr});
+    HGS_CUDA(launch_pdl(k_onesweep<K>, dim3((unsigned)tiles), dim3(kSortThreads), 0, s, src, vs, dst, vd, n,
+                        p * kRadixBits, offsets + p * kRadix, lookback + (size_t)i * tiles * kRadix, counters + i,
+                        SortDev{nullptr, nullptr, 0, nullptr, nullptr}));
     HGS_LAUNCHED();
     std::swap(src, dst);
     std::swap(vs, vd);
@@ -291,9 +299,13 @@ int hgs_forward(const hgs_scene *scene, const hgs_camera *camera, const hgs_sett
   const bool fork = aux && settings->aux_events[0] && settings->aux_events[1] && n > 0;
   // 1. depth keys + digit histograms + the pass plan
   if (n > 0) {
+    // the depth sort's look-back slots, zeroed up front so the key ->
+    // plan -> pass chain is kernels only (programmatic dependent launches)
+    HGS_CUDA(cudaMemsetAsync(at<uint32_t>(frame, L.lb_sort), 0, (size_t)sort_tiles_n * kRadix * 4 * 8, s));
     HGS_CUDA(launch_depth_keys(sc, cam, at<unsigned long long>(frame, L.keys_a), at<uint32_t>(frame, L.vals_a),
                                at<uint8_t>(frame, L.kept), at<uint32_t>(frame, L.hist_d), st, grid_for(n, 256), s));
-    k_sort_plan<<<1, kRadix, 0, s>>>(at<uint32_t>(frame, L.hist_d), n, at<uint32_t>(frame, L.off_d), st);
+    HGS_CUDA(launch_ex(kDepthSortPdl, k_sort_plan, dim3(1), dim3(kRadix), 0, s, at<uint32_t>(frame, L.hist_d), n,
+                        at<uint32_t>(frame, L.off_d), st));
     HGS_LAUNCHED();
     if (fork) {
       HGS_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(settings->aux_events[0]), s));
@@ -316,20 +328,19 @@ int hgs_forward(const hgs_scene *scene, const hgs_camera *camera, const hgs_sett
     }
     if (fork && !HGS_SORT_ON_AUX) HGS_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(settings->aux_events[1]), aux));
     // 2. depth sort: 8 digit passes launched, the constant ones exit at once
-    uint32_t *lb = at<uint32_t>(frame, L.lb_sort);
-    HGS_CUDA(cudaMemsetAsync(lb, 0, (size_t)sort_tiles_n * kRadix * 4 * 8, s_sort));
+    uint32_t *lb = at<uint32_t>(frame, L.lb_sort);  // zeroed before the depth keys
     for (int i = 0; i < 8; ++i) {
       unsigned long long *ka = at<unsigned long long>(frame, (i & 1) ? L.keys_b : L.keys_a);
       unsigned long long *kb = at<unsigned long long>(frame, (i & 1) ? L.keys_a : L.keys_b);
       uint32_t *va = at<uint32_t>(frame, (i & 1) ? L.vals_b : L.vals_a);
       uint32_t *vb = at<uint32_t>(frame, (i & 1) ? L.vals_a : L.vals_b);
-      k_onesweep<unsigned long long><<<(unsigned)sort_tiles_n, kSortThreads, 0, s_sort>>>(
-          ka, va, kb, vb, n, 0, at<uint32_t>(frame, L.off_d), lb + (size_t)i * sort_tiles_n * kRadix,
-          st->tile_counters + 1 + i, SortDev{&st->sort_np, st->sort_digit, i, nullptr, nullptr});
+      HGS_CUDA(launch_ex(kDepthSortPdl, k_onesweep<unsigned long long>, dim3((unsigned)sort_tiles_n), dim3(kSortThreads), 0, s_sort,
+                          ka, va, kb, vb, n, 0, at<uint32_t>(frame, L.off_d), lb + (size_t)i * sort_tiles_n * kRadix,
+                          st->tile_counters + 1 + i, SortDev{&st->sort_np, st->sort_digit, i, nullptr, nullptr}));
       HGS_LAUNCHED();
     }
-    k_rank_scatter<<<grid_for(n, 256), 256, 0, s_sort>>>(at<uint32_t>(frame, L.vals_a), at<uint32_t>(frame, L.vals_b),
-                                                         st, n, rank_of, order);
+    HGS_CUDA(launch_ex(kDepthSortPdl, k_rank_scatter, dim3(grid_for(n, 256)), dim3(256), 0, s_sort, at<uint32_t>(frame, L.vals_a),
+                        at<uint32_t>(frame, L.vals_b), st, n, rank_of, order));
     HGS_LAUNCHED();
     if (fork && HGS_SORT_ON_AUX) HGS_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(settings->aux_events[1]), aux));
     // join: the scan below needs both the depth order and the tile counts
@@ -368,11 +379,12 @@ int hgs_forward(const hgs_scene *scene, const hgs_camera *camera, const hgs_sett
     uint32_t *lb = at<uint32_t>(frame, L.lb_sort);  // free again after the depth sort
     HGS_CUDA(cudaMemsetAsync(lb, 0, (size_t)sort_tiles_k * kRadix * 4 * nd, s));
     for (int i = 0; i < nd; ++i) {
-      k_onesweep<uint32_t><<<(unsigned)sort_tiles_k, kSortThreads, 0, s>>>(
-          at<uint32_t>(frame, (i & 1) ? L.pk_b : L.pk_a), at<uint32_t>(frame, (i & 1) ? L.pv_b : L.pv_a),
-          at<uint32_t>(frame, (i & 1) ? L.pk_a : L.pk_b), at<uint32_t>(frame, (i & 1) ? L.pv_a : L.pv_b), 0,
-          i * kRadixBits, at<uint32_t>(frame, L.off_p) + i * kRadix, lb + (size_t)i * sort_tiles_k * kRadix,
-          st->tile_counters + 12 + i, SortDev{nullptr, nullptr, 0, &st->k_total, &st->status});
+      HGS_CUDA(launch_pdl(k_onesweep<uint32_t>, dim3((unsigned)sort_tiles_k), dim3(kSortThreads), 0, s,
+                          at<uint32_t>(frame, (i & 1) ? L.pk_b : L.pk_a), at<uint32_t>(frame, (i & 1) ? L.pv_b : L.pv_a),
+                          at<uint32_t>(frame, (i & 1) ? L.pk_a : L.pk_b), at<uint32_t>(frame, (i & 1) ? L.pv_a : L.pv_b),
+                          (int64_t)0, (int)(i * kRadixBits), at<uint32_t>(frame, L.off_p) + i * kRadix,
+                          lb + (size_t)i * sort_tiles_k * kRadix, st->tile_counters + 12 + i,
+                          SortDev{nullptr, nullptr, 0, &st->k_total, &st->status}));
       HGS_LAUNCHED();
     }
   }
@@ -406,7 +418,7 @@ int hgs_forward(const hgs_scene *scene, const hgs_camera *camera, const hgs_sett
   const bool naive = settings->flags & HGS_FLAG_NAIVE, count = settings->flags & HGS_FLAG_COUNT;
   HGS_CUDA(launch_composite_fwd(a, n_tiles, naive, count, s));
   // deferred (float32-ambiguous) pixels, float64-exact; exits at once if none
-  k_fixup_fwd<<<kFixupBlocks, 256, 0, s>>>(a);
+  HGS_CUDA(launch_pdl(k_fixup_fwd, dim3(kFixupBlocks), dim3(256), 0, s, a));
   HGS_LAUNCHED();
   HGS_CUDA(record_event(settings, 4, s));
   return finish_forward(frame, L, info, settings, s);

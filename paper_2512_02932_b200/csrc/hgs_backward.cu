@@ -107,6 +107,8 @@ constexpr int kChainThreads = 32;
 
 template <int DEG>
 __global__ void __launch_bounds__(kChainThreads, HGS_CHAIN_MINB) k_chain_rule_t(ChainArgs c) {
+  pdl_launch_dependents();
+  pdl_wait();
   constexpr int B = (DEG + 1) * (DEG + 1);
   constexpr int SB = 3 * B, SS = 3 * B + 1;  // row length, padded smem stride
   extern __shared__ float s_chain[];
@@ -431,10 +433,10 @@ __global__ void __launch_bounds__(kChainThreads, HGS_CHAIN_MINB) k_chain_rule_t(
 
 cudaError_t launch_chain_rule(const ChainArgs &c, int sh_bases, int grid, size_t smem, cudaStream_t s) {
   switch (sh_bases) {
-    case 1: k_chain_rule_t<0><<<grid, kChainThreads, smem, s>>>(c); break;
-    case 4: k_chain_rule_t<1><<<grid, kChainThreads, smem, s>>>(c); break;
-    case 9: k_chain_rule_t<2><<<grid, kChainThreads, smem, s>>>(c); break;
-    default: k_chain_rule_t<3><<<grid, kChainThreads, smem, s>>>(c); break;
+    case 1: return launch_pdl(k_chain_rule_t<0>, dim3(grid), dim3(kChainThreads), smem, s, c);
+    case 4: return launch_pdl(k_chain_rule_t<1>, dim3(grid), dim3(kChainThreads), smem, s, c);
+    case 9: return launch_pdl(k_chain_rule_t<2>, dim3(grid), dim3(kChainThreads), smem, s, c);
+    default: return launch_pdl(k_chain_rule_t<3>, dim3(grid), dim3(kChainThreads), smem, s, c);
   }
   return cudaGetLastError();
 }

@@ -12,11 +12,53 @@
 #pragma once
 
 #include <cstdint>
+#include <utility>
 #include <cuda_runtime.h>
 
 #include "../../include/hgs.h"
 
 namespace hgs {
+
+// Programmatic dependent launch (Hopper / Blackwell): a kernel launched with
+// launch_pdl() may be scheduled while its predecessor on the stream drains
+// (each predecessor CTA signals pdl_launch_dependents() when it starts);
+// pdl_wait() then blocks until the predecessor has completed and its writes
+// are visible.  Every PDL-launched kernel calls pdl_wait() before touching
+// global memory, so the ordering is that of a plain launch minus the launch
+// gap.  Both are no-ops for kernels launched without the attribute.
+#ifndef HGS_PDL
+#define HGS_PDL 1
+#endif
+__device__ __forceinline__ void pdl_launch_dependents() {
+#if HGS_PDL
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
+}
+__device__ __forceinline__ void pdl_wait() {
+#if HGS_PDL
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
+}
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_ex(bool pdl, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                             Args &&...args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = (HGS_PDL && pdl) ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                              Args &&...args) {
+  return launch_ex(true, kernel, grid, block, smem, s, std::forward<Args>(args)...);
+}
 
 constexpr int kTile = 16;
 constexpr int kTileShift = 4;  // log2(kTile)

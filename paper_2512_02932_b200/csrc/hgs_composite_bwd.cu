@@ -397,6 +397,7 @@ constexpr size_t cstate_bytes() {
 
 template <int KG, bool EXT, bool DET, int QP, bool COUNT>
 __global__ void __launch_bounds__(256 / QP, HGS_BWDC_MINB(KG, EXT, QP)) k_composite_bwd_c(BwdArgs b) {
+  pdl_launch_dependents();  // k_fixup_bwd may be scheduled into the tail of this grid
   constexpr int NW = 8 / QP;  // warps per tile
   // warp block: 8 x (4 QP) pixels, or the whole 16 x 16 tile at QP = 8;
   // pixel p = lane + 32 q of the block is (p % BW, p / BW)
@@ -693,6 +694,8 @@ __device__ __forceinline__ float scan_add_ex(float x, int lane) {
 // with per-lane atomics.
 template <int KG, bool EXT, bool DET>
 __global__ void __launch_bounds__(256, HGS_FIXUP_MINB) k_fixup_bwd(BwdArgs b) {
+  pdl_launch_dependents();
+  pdl_wait();
   const CompositeArgs &a = b.c;
   const uint32_t nfix = a.st->n_fix_bwd;
   const int lane = threadIdx.x & 31;
@@ -857,7 +860,10 @@ static cudaError_t launch_bwd_t(const BwdArgs &b, int64_t n_tiles, cudaStream_t 
     else
       k_composite_bwd_c<KG, EXT, DET, QP, false><<<g, t, dyn, s>>>(b);
   }
-  k_fixup_bwd<KG, EXT, DET><<<kFixupBlocks, 256, 0, s>>>(b);
+  {
+    const cudaError_t e = launch_pdl(k_fixup_bwd<KG, EXT, DET>, dim3(kFixupBlocks), dim3(256), 0, s, b);
+    if (e != cudaSuccess) return e;
+  }
   return cudaGetLastError();
 }
 

@@ -50,6 +50,8 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 // shared-memory copy.
 template <bool NAIVE, bool COUNT, int PF, bool EXACT>
 __global__ void __launch_bounds__(kBlock, HGS_FWD_MINB) k_composite_fwd(CompositeArgs a) {
+  pdl_launch_dependents();  // k_fixup_fwd may be scheduled into the tail of this grid
+  pdl_wait();
   __shared__ SplatRec s_rec[PF ? 2 : 1][kBlock / 32][32];
   const int tile = blockIdx.x;
   const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
@@ -305,8 +307,8 @@ cudaError_t launch_composite_fwd(const CompositeArgs &a, int64_t n_tiles, bool n
   constexpr int PF = HGS_FWD_PF;
   const bool fast = a.flags & HGS_FLAG_FAST;
 #define HGS_FWD_LAUNCH(NV, CT, P)                                                           \
-  (fast ? k_composite_fwd<NV, CT, P, false><<<(unsigned)n_tiles, kBlock, 0, s>>>(a)         \
-        : k_composite_fwd<NV, CT, P, true><<<(unsigned)n_tiles, kBlock, 0, s>>>(a))
+  (fast ? launch_pdl(k_composite_fwd<NV, CT, P, false>, dim3((unsigned)n_tiles), dim3(kBlock), 0, s, a) \
+        : launch_pdl(k_composite_fwd<NV, CT, P, true>, dim3((unsigned)n_tiles), dim3(kBlock), 0, s, a))
   if (naive && count) HGS_FWD_LAUNCH(true, true, 0);
   else if (naive) HGS_FWD_LAUNCH(true, false, 0);
   else if (count) HGS_FWD_LAUNCH(false, true, PF);
@@ -357,6 +359,8 @@ __device__ __forceinline__ float warp_sum(float x) {
 // chain of windows (the kernel's duration is the longest one): E entries per
 // lane make it E times shorter.
 __global__ void __launch_bounds__(256, HGS_FIXUP_MINB) k_fixup_fwd(CompositeArgs a) {
+  pdl_launch_dependents();
+  pdl_wait();
   constexpr int E = HGS_FIXUP_E;
   constexpr uint32_t WIN = 32u * E;
   constexpr int LPC = 32 / E;  // lanes per 32-entry chunk

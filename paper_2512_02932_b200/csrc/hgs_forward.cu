@@ -59,6 +59,7 @@ template <bool G64>
 __global__ void __launch_bounds__(256) k_depth_keys(SceneView sc, CamD cam, unsigned long long *__restrict__ keys,
                                                     uint32_t *__restrict__ vals, uint8_t *__restrict__ kept,
                                                     uint32_t *__restrict__ hist, FrameState *__restrict__ st) {
+  pdl_launch_dependents();  // k_sort_plan may be scheduled as this grid drains
   using G = SceneGeom<G64>;
   __shared__ uint32_t sh[8 * kRadix];
   __shared__ uint32_t s_m;
@@ -231,6 +232,8 @@ __global__ void __launch_bounds__(256) k_tile_counts(const SplatRec *__restrict_
 __global__ void k_rank_scatter(const uint32_t *__restrict__ vals_a, const uint32_t *__restrict__ vals_b,
                                const FrameState *__restrict__ st, int64_t n, uint32_t *__restrict__ rank_of,
                                uint32_t *__restrict__ order) {
+  pdl_launch_dependents();
+  pdl_wait();
   const uint32_t *sorted_idx = (st->sort_np & 1u) ? vals_b : vals_a;
   const int64_t m = st->m_count;
   for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x) {
@@ -246,6 +249,8 @@ __global__ void k_rank_scatter(const uint32_t *__restrict__ vals_a, const uint32
 // the device-side pass list the onesweep passes read.
 __global__ void k_sort_plan(const uint32_t *__restrict__ hist, int64_t n, uint32_t *__restrict__ offsets,
                             FrameState *__restrict__ st) {
+  pdl_launch_dependents();
+  pdl_wait();
   __shared__ uint32_t s[kRadix];
   __shared__ int s_trivial[8];
   const int t = threadIdx.x;

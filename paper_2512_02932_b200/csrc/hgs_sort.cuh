@@ -107,6 +107,8 @@ __global__ void __launch_bounds__(kSortThreads, sizeof(K) == 4 ? HGS_SORT_MINB32
                                                            const uint32_t *__restrict__ digit_offsets,
                                                            uint32_t *__restrict__ lookback,
                                                            uint32_t *__restrict__ tile_counter, SortDev dv) {
+  pdl_launch_dependents();
+  pdl_wait();
   if (dv.plan_np) {
     if ((unsigned)dv.pass >= *dv.plan_np) return;
     const unsigned dg = dv.plan_digit[dv.pass];
