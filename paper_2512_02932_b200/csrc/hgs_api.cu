@@ -29,11 +29,12 @@ constexpr bool kDepthSortPdl = HGS_DEPTH_SORT_PDL != 0;
 #endif
 
 struct Layout {
-  size_t state, hist_d, off_d, hist_p, off_p, keys_a, keys_b, vals_a, vals_b, rank, order, counts, keep, kept, lb_sort, lb_scan,
+  size_t state, hist_d, off_d, hist_p, off_p, keys_a, keys_b, vals_a, vals_b, rank, order, counts, keep, kept, lb_sort, lb_tile,
+      lb_scan,
       recs, recs64, cull2d, eig, pair_off,
       pk_a, pk_b, pv_a, pv_b, tile_off, pix_T, pix_last, pix_count, fwd_fix, bwd_fix, pix_mask, total;
   size_t small_end;  // [state, small_end) is zeroed at the start of a forward
-  size_t lb_sort_bytes, lb_scan_bytes;
+  size_t lb_sort_bytes, lb_tile_bytes, lb_scan_bytes;  // [lb_sort, lb_scan + lb_scan_bytes): one zeroing
 };
 
 int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
@@ -54,8 +55,12 @@ Layout make_layout(int64_t n, int W, int H, int64_t cap) {
   L.hist_p = take(2 * kRadix * 4);
   L.off_p = take(2 * kRadix * 4);
   L.small_end = off;
-  L.lb_sort_bytes = (size_t)std::max<int64_t>(8 * ceil_div(nn, kSortTile), 2 * ceil_div(cc, kSortTile)) * kRadix * 4;
+  // look-back slots of the depth sort, the tile sort and the pair-offset
+  // scan, adjacent: zeroed by one memset at the start of a forward
+  L.lb_sort_bytes = (size_t)(8 * ceil_div(nn, kSortTile)) * kRadix * 4;
   L.lb_sort = take(L.lb_sort_bytes);
+  L.lb_tile_bytes = (size_t)(2 * ceil_div(cc, kSortTile)) * kRadix * 4;
+  L.lb_tile = take(L.lb_tile_bytes);
   L.lb_scan_bytes = (size_t)ceil_div(nn, kScanThreads) * 8;
   L.lb_scan = take(L.lb_scan_bytes);
   L.keys_a = take(nn * 8);
@@ -299,9 +304,9 @@ int hgs_forward(const hgs_scene *scene, const hgs_camera *camera, const hgs_sett
   const bool fork = aux && settings->aux_events[0] && settings->aux_events[1] && n > 0;
   // 1. depth keys + digit histograms + the pass plan
   if (n > 0) {
-    // the depth sort's look-back slots, zeroed up front so the key ->
-    // plan -> pass chain is kernels only (programmatic dependent launches)
-    HGS_CUDA(cudaMemsetAsync(at<uint32_t>(frame, L.lb_sort), 0, (size_t)sort_tiles_n * kRadix * 4 * 8, s));
+    // every look-back slot of the frame (depth sort, tile sort, scan),
+    // zeroed up front so the sort and binning chains are kernels only
+    HGS_CUDA(cudaMemsetAsync(at<char>(frame, L.lb_sort), 0, L.lb_scan + L.lb_scan_bytes - L.lb_sort, s));
     HGS_CUDA(launch_depth_keys(sc, cam, at<unsigned long long>(frame, L.keys_a), at<uint32_t>(frame, L.vals_a),
                                at<uint8_t>(frame, L.kept), at<uint32_t>(frame, L.hist_d), st, grid_for(n, 256), s));
     HGS_CUDA(launch_ex(kDepthSortPdl, k_sort_plan, dim3(1), dim3(kRadix), 0, s, at<uint32_t>(frame, L.hist_d), n,
@@ -354,7 +359,6 @@ int hgs_forward(const hgs_scene *scene, const hgs_camera *camera, const hgs_sett
                                                      counts, at<uint32_t>(frame, L.keep));
       HGS_LAUNCHED();
     }
-    HGS_CUDA(cudaMemsetAsync(at<char>(frame, L.lb_scan), 0, L.lb_scan_bytes, s));
     k_scan_counts<<<(unsigned)ceil_div(n, kScanTile), kScanThreads, 0, s>>>(
         counts, order, -1, at<unsigned long long>(frame, L.pair_off), at<unsigned long long>(frame, L.lb_scan), st,
         std::min<int64_t>(cap, 0xffffffffll));
@@ -368,16 +372,14 @@ int hgs_forward(const hgs_scene *scene, const hgs_camera *camera, const hgs_sett
   const uint32_t *tile_keys = at<uint32_t>(frame, pairs_in_b ? L.pk_b : L.pk_a);
   const int64_t sort_tiles_k = ceil_div(std::max<int64_t>(cap, 1), kSortTile);
   if (n > 0) {
-    k_duplicate<<<grid_for(n, 256), 256, 0, s>>>(at<SplatRec>(frame, L.recs), order,
-                                                 at<unsigned long long>(frame, L.pair_off), -1, st, cam.tiles_x,
-                                                 kTileShift, false, true, at<uint32_t>(frame, L.keep),
-                                                 at<uint32_t>(frame, L.pk_a),
-                                                 at<uint32_t>(frame, L.pv_a), nd, at<uint32_t>(frame, L.hist_p));
-    HGS_LAUNCHED();
-    k_radix_offsets<<<nd, kRadix, 0, s>>>(at<uint32_t>(frame, L.hist_p), at<uint32_t>(frame, L.off_p));
-    HGS_LAUNCHED();
-    uint32_t *lb = at<uint32_t>(frame, L.lb_sort);  // free again after the depth sort
-    HGS_CUDA(cudaMemsetAsync(lb, 0, (size_t)sort_tiles_k * kRadix * 4 * nd, s));
+    HGS_CUDA(launch_pdl(k_duplicate, dim3(grid_for(n, 256)), dim3(256), 0, s, (const SplatRec *)at<SplatRec>(frame, L.recs),
+                        (const uint32_t *)order, (const unsigned long long *)at<unsigned long long>(frame, L.pair_off),
+                        (int64_t)-1, (const FrameState *)st, (int)cam.tiles_x, (int)kTileShift, false, true,
+                        (const uint32_t *)at<uint32_t>(frame, L.keep), at<uint32_t>(frame, L.pk_a),
+                        at<uint32_t>(frame, L.pv_a), nd, at<uint32_t>(frame, L.hist_p)));
+    HGS_CUDA(launch_pdl(k_radix_offsets, dim3(nd), dim3(kRadix), 0, s, (const uint32_t *)at<uint32_t>(frame, L.hist_p),
+                        at<uint32_t>(frame, L.off_p)));
+    uint32_t *lb = at<uint32_t>(frame, L.lb_tile);  // zeroed at the start of the frame
     for (int i = 0; i < nd; ++i) {
       HGS_CUDA(launch_pdl(k_onesweep<uint32_t>, dim3((unsigned)sort_tiles_k), dim3(kSortThreads), 0, s,
                           at<uint32_t>(frame, (i & 1) ? L.pk_b : L.pk_a), at<uint32_t>(frame, (i & 1) ? L.pv_b : L.pv_a),
@@ -390,9 +392,9 @@ int hgs_forward(const hgs_scene *scene, const hgs_camera *camera, const hgs_sett
   }
   info->internal[0] = pairs_in_b ? 1u : 0u;
   info->internal[3] = (uint32_t)nd;
-  k_tile_ranges<<<grid_for(ceil_div(std::max<int64_t>(cap, n_tiles + 1), 4), 256), 256, 0, s>>>(
-      tile_keys, n > 0 ? -1 : 0, st, n_tiles, at<uint32_t>(frame, L.tile_off));
-  HGS_LAUNCHED();
+  HGS_CUDA(launch_pdl(k_tile_ranges, dim3(grid_for(ceil_div(std::max<int64_t>(cap, n_tiles + 1), 4), 256)), dim3(256), 0,
+                      s, tile_keys, (int64_t)(n > 0 ? -1 : 0), (const FrameState *)st, (int64_t)n_tiles,
+                      at<uint32_t>(frame, L.tile_off)));
   HGS_CUDA(record_event(settings, 3, s));
   if (settings->flags & HGS_FLAG_FRAME_ONLY) return finish_forward(frame, L, info, settings, s);  // build_frame
   // 5. composite

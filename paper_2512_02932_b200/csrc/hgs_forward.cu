@@ -389,6 +389,7 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_counts(const uint32_t *__
                                                               unsigned long long *__restrict__ pair_off,
                                                               unsigned long long *__restrict__ scan_lb,
                                                               FrameState *__restrict__ st, int64_t cap) {
+  pdl_launch_dependents();  // k_duplicate may be scheduled as this grid drains
   __shared__ uint32_t s_tile;
   if (m < 0) m = st->m_count;
   if ((int64_t)blockIdx.x * kScanTile >= m) return;  // launched for N, not for M
@@ -442,6 +443,8 @@ __global__ void __launch_bounds__(256) k_duplicate(const SplatRec *__restrict__ 
                                                    bool emit_rank, bool tile_cull, const uint32_t *__restrict__ keep,
                                                    uint32_t *__restrict__ pkeys, uint32_t *__restrict__ pvals,
                                                    int n_digits, uint32_t *__restrict__ hist) {
+  pdl_launch_dependents();
+  pdl_wait();
   __shared__ uint32_t sh[2 * kRadix];
   if (m < 0) {  // M and the capacity verdict from the frame state
     if (st->status) return;
@@ -525,6 +528,8 @@ __global__ void __launch_bounds__(256) k_rebin_counts(const SplatRec *__restrict
 __global__ void __launch_bounds__(256) k_tile_ranges(const uint32_t *__restrict__ skeys, int64_t k,
                                                      const FrameState *__restrict__ st, int64_t n_tiles,
                                                      uint32_t *__restrict__ tile_off) {
+  pdl_launch_dependents();
+  pdl_wait();
   if (k < 0) {  // K from the frame state
     if (st->status) return;
     k = (int64_t)st->k_total;

@@ -60,6 +60,8 @@ __global__ void __launch_bounds__(256) k_radix_histogram(const K *__restrict__ k
 
 // Exclusive scan of each 256-bin histogram (one block per digit pass).
 static __global__ void k_radix_offsets(const uint32_t *__restrict__ hist, uint32_t *__restrict__ offsets) {
+  pdl_launch_dependents();
+  pdl_wait();
   __shared__ uint32_t s[kRadix];
   const uint32_t *h = hist + blockIdx.x * kRadix;
   uint32_t *o = offsets + blockIdx.x * kRadix;
