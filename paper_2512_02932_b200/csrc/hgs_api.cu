@@ -33,7 +33,7 @@ struct Layout {
       lb_scan,
       recs, recs64, cull2d, eig, pair_off,
       pk_a, pk_b, pv_a, pv_b, tile_off, pix_T, pix_last, pix_count, fwd_fix, bwd_fix, pix_mask, total;
-  size_t small_end;  // [state, small_end) is zeroed at the start of a forward
+  size_t small_end;  // [state, small_end) is zeroed at the start of a forward (with n > 0: up to the look-back end)
   size_t lb_sort_bytes, lb_tile_bytes, lb_scan_bytes;  // [lb_sort, lb_scan + lb_scan_bytes): one zeroing
 };
 
@@ -284,7 +284,10 @@ int hgs_forward(const hgs_scene *scene, const hgs_camera *camera, const hgs_sett
   info->n_tiles = n_tiles; info->pair_capacity = cap; info->sh_bases = scene->sh_bases; info->flags = settings->flags;
 
   HGS_CUDA(record_event(settings, 0, s));
-  HGS_CUDA(cudaMemsetAsync(frame, 0, L.small_end, s));
+  // the frame state and histograms, and (n > 0) every look-back slot of the
+  // frame (depth sort, tile sort, scan: adjacent), zeroed by one memset so
+  // the sort and binning chains are kernels only
+  HGS_CUDA(cudaMemsetAsync(frame, 0, n > 0 ? L.lb_scan + L.lb_scan_bytes : L.small_end, s));
   k_init_state<<<1, 1, 0, s>>>(sc, cam, mod, at<SplatRec>(frame, L.recs), at<Rec64>(frame, L.recs64), st);
   HGS_LAUNCHED();
   // Every launch below is sized from host-known bounds (N, the pair capacity,
@@ -304,9 +307,6 @@ int hgs_forward(const hgs_scene *scene, const hgs_camera *camera, const hgs_sett
   const bool fork = aux && settings->aux_events[0] && settings->aux_events[1] && n > 0;
   // 1. depth keys + digit histograms + the pass plan
   if (n > 0) {
-    // every look-back slot of the frame (depth sort, tile sort, scan),
-    // zeroed up front so the sort and binning chains are kernels only
-    HGS_CUDA(cudaMemsetAsync(at<char>(frame, L.lb_sort), 0, L.lb_scan + L.lb_scan_bytes - L.lb_sort, s));
     HGS_CUDA(launch_depth_keys(sc, cam, at<unsigned long long>(frame, L.keys_a), at<uint32_t>(frame, L.vals_a),
                                at<uint8_t>(frame, L.kept), at<uint32_t>(frame, L.hist_d), st, grid_for(n, 256), s));
     HGS_CUDA(launch_ex(kDepthSortPdl, k_sort_plan, dim3(1), dim3(kRadix), 0, s, at<uint32_t>(frame, L.hist_d), n,
@@ -572,16 +572,9 @@ int hgs_backward(const hgs_scene *scene, const hgs_camera *camera, const hgs_set
   HGS_CUDA(cudaMemsetAsync(touched, 0, (size_t)nn, s));
   BwdArgs b;
   b.c = composite_args_for(scene, camera, settings, frame, info);
-  HGS_CUDA(cudaMemsetAsync(&b.c.st->diag[6], 0, 4 * sizeof(unsigned long long), s));
   const SceneView sc = make_scene(*scene);
   const CamD cam = make_cam(*camera);
   const ModD mod{settings->theta_z, settings->t_z, settings->lambda_z};
-  {
-    const Layout FL = make_layout(info->n, info->width, info->height, info->pair_capacity);
-    k_init_state<<<1, 1, 0, s>>>(sc, cam, mod, at<SplatRec>(const_cast<void *>(frame), FL.recs),
-                                 at<Rec64>(const_cast<void *>(frame), FL.recs64), b.c.st);
-  }
-  HGS_LAUNCHED();
   const Layout FLc = make_layout(info->n, info->width, info->height, info->pair_capacity);
   const bool replay_only = settings->flags & HGS_FLAG_REPLAY_ONLY;
   if (replay_only && kg > 4) return HGS_ERR_CONFIG;
@@ -590,7 +583,6 @@ int hgs_backward(const hgs_scene *scene, const hgs_camera *camera, const hgs_set
   for (int k0 = 0; k0 < kg; k0 += 4) {
     const int kc = std::min(4, kg - k0);
     HGS_CUDA(cudaMemsetAsync(acc, 0, (size_t)nn * kc * 16 * sizeof(acc_t), s));
-    HGS_CUDA(cudaMemsetAsync(&b.c.st->n_fix_bwd, 0, sizeof(uint32_t), s));
     if (ext) HGS_CUDA(cudaMemsetAsync(acc_ext, 0, (size_t)nn * kc * 4 * sizeof(acc_t), s));
     b.pix_grad = pixel_grads + (int64_t)k0 * HW * 3;
     b.depth_grad = depth_grads ? depth_grads + (int64_t)k0 * HW : nullptr;
@@ -604,7 +596,11 @@ int hgs_backward(const hgs_scene *scene, const hgs_camera *camera, const hgs_set
     b.rec_pay = det ? reinterpret_cast<float *>(scr + DL.pay) : nullptr;
     b.rec_count = det ? reinterpret_cast<uint32_t *>(scr + DL.count) : nullptr;
     b.rec_cap = (uint32_t)rec_cap;
-    if (det) HGS_CUDA(cudaMemsetAsync(b.rec_count, 0, 4, s));
+    // frame-state view, worklist count, diagnostics (first round) and the
+    // deterministic record count: one launch, right before the compositor
+    k_init_bwd<<<1, 1, 0, s>>>(sc, cam, mod, at<SplatRec>(const_cast<void *>(frame), FLc.recs),
+                               at<Rec64>(const_cast<void *>(frame), FLc.recs64), b.c.st, b.rec_count, k0 == 0 ? 1 : 0);
+    HGS_LAUNCHED();
     if (m != 0) {  // m < 0: an asynchronous frame (M on the device)
       HGS_CUDA(launch_composite_bwd(b, (int)kc, info->n_tiles, ext, det, s));
       if (det) {  // sort the records by (Gaussian, tile, sub) and reduce in that order

@@ -398,6 +398,7 @@ constexpr size_t cstate_bytes() {
 template <int KG, bool EXT, bool DET, int QP, bool COUNT>
 __global__ void __launch_bounds__(256 / QP, HGS_BWDC_MINB(KG, EXT, QP)) k_composite_bwd_c(BwdArgs b) {
   pdl_launch_dependents();  // k_fixup_bwd may be scheduled into the tail of this grid
+  pdl_wait();
   constexpr int NW = 8 / QP;  // warps per tile
   // warp block: 8 x (4 QP) pixels, or the whole 16 x 16 tile at QP = 8;
   // pixel p = lane + 32 q of the block is (p % BW, p / BW)
@@ -855,10 +856,10 @@ static cudaError_t launch_bwd_t(const BwdArgs &b, int64_t n_tiles, cudaStream_t 
       attr_set = true;
     }
     const unsigned g = (unsigned)n_tiles, t = 256 / QP;
-    if (b.c.flags & HGS_FLAG_COUNT)
-      k_composite_bwd_c<KG, EXT, DET, QP, true><<<g, t, dyn, s>>>(b);
-    else
-      k_composite_bwd_c<KG, EXT, DET, QP, false><<<g, t, dyn, s>>>(b);
+    const cudaError_t e = (b.c.flags & HGS_FLAG_COUNT)
+                              ? launch_pdl(k_composite_bwd_c<KG, EXT, DET, QP, true>, dim3(g), dim3(t), dyn, s, b)
+                              : launch_pdl(k_composite_bwd_c<KG, EXT, DET, QP, false>, dim3(g), dim3(t), dyn, s, b);
+    if (e != cudaSuccess) return e;
   }
   {
     const cudaError_t e = launch_pdl(k_fixup_bwd<KG, EXT, DET>, dim3(kFixupBlocks), dim3(256), 0, s, b);

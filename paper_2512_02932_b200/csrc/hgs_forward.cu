@@ -28,6 +28,24 @@ __global__ void k_init_state(SceneView sc, CamD cam, ModD mod, const SplatRec *r
   st->recs64 = recs64;
 }
 
+// The backward's per-round state: the scene / camera view of the frame
+// state, the deferred-pixel worklist count, the backward's diagnostic
+// counters (first round) and the deterministic record count -- one launch
+// instead of a kernel and three small memsets.
+__global__ void k_init_bwd(SceneView sc, CamD cam, ModD mod, const SplatRec *recs, const Rec64 *recs64,
+                           FrameState *st, uint32_t *rec_count, int zero_diag) {
+  pdl_launch_dependents();  // the backward compositor may be scheduled as this drains
+  st->sc = sc;
+  st->cam = cam;
+  st->mod = mod;
+  st->recs = recs;
+  st->recs64 = recs64;
+  st->n_fix_bwd = 0;
+  if (zero_diag)
+    for (int k = 6; k < 10; ++k) st->diag[k] = 0ull;
+  if (rec_count) *rec_count = 0;
+}
+
 // The float64 projection a pair re-check needs (Rec64).
 __device__ __forceinline__ void write_rec64(const ProjD &o, Rec64 *q) {
   Rec64 r;

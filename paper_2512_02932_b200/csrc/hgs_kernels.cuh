@@ -720,6 +720,8 @@ struct ExchangeState {
 // kernels (defined in hgs_forward.cu / hgs_backward.cu / hgs_exchange.cu)
 __global__ void k_init_state(SceneView sc, CamD cam, ModD mod, const SplatRec *recs, const Rec64 *recs64,
                              FrameState *st);
+__global__ void k_init_bwd(SceneView sc, CamD cam, ModD mod, const SplatRec *recs, const Rec64 *recs64,
+                           FrameState *st, uint32_t *rec_count, int zero_diag);
 cudaError_t launch_depth_keys(const SceneView &sc, const CamD &cam, unsigned long long *keys, uint32_t *vals,
                               uint8_t *kept, uint32_t *hist, FrameState *st, int grid, cudaStream_t s);
 __global__ void k_rank_scatter(const uint32_t *vals_a, const uint32_t *vals_b, const FrameState *st, int64_t n,
