@@ -16,14 +16,20 @@ constexpr int kMaxGrid = 148 * 8;
 #ifndef HGS_TILE_COUNTS_AUX
 #define HGS_TILE_COUNTS_AUX 1  // 0: k_tile_counts on the main stream after the join (A/B: 268.4 vs 269.5 it/s)
 #endif
-// The depth sort's chain is launched without programmatic dependence: its
-// waiting CTAs would hold SM slots the preprocess beside it needs (A/B:
-// stage 1 0.359 -> 0.368 ms with it).  The binning sort, the fixups and the
-// chain rule keep it (binning 0.145 -> 0.139 ms).
+// The depth sort's chain (plan, passes, rank scatter) is launched with
+// programmatic dependence but without early triggers (HGS_DEPTH_SORT_TRIGGER
+// 0): each kernel is set up while its predecessor runs and starts when it
+// completes, and no waiting CTA holds an SM slot the preprocess beside the
+// chain needs (A/B, stage 1: plain launches 0.354 ms, PDL with early
+// triggers 0.368, PDL without them 0.345).  The binning chain, the fixups
+// and the chain rule trigger early (binning 0.145 -> 0.131 ms).
 #ifndef HGS_DEPTH_SORT_PDL
-#define HGS_DEPTH_SORT_PDL 0
+#define HGS_DEPTH_SORT_PDL 1
 #endif
 constexpr bool kDepthSortPdl = HGS_DEPTH_SORT_PDL != 0;
+#ifndef HGS_TILE_COUNTS_PDL
+#define HGS_TILE_COUNTS_PDL 1
+#endif
 #ifndef HGS_SORT_ON_AUX
 #define HGS_SORT_ON_AUX 0  // 1 (+ HGS_PRE_CTAS=64, HGS_AUX_PRIORITY=-5): stage 1 0.359 -> 0.353 ms, neutral end to end
 #endif
@@ -327,9 +333,9 @@ int hgs_forward(const hgs_scene *scene, const hgs_camera *camera, const hgs_sett
                                counts, s_pre));
     HGS_LAUNCHED();
     if (HGS_TILE_COUNTS_AUX) {
-      k_tile_counts<<<grid_for(n, 256), 256, 0, s_pre>>>(at<SplatRec>(frame, L.recs), at<float4>(frame, L.cull2d),
-                                                         n, counts, at<uint32_t>(frame, L.keep));
-      HGS_LAUNCHED();
+      HGS_CUDA(launch_ex(HGS_TILE_COUNTS_PDL != 0, k_tile_counts, dim3(grid_for(n, 256)), dim3(256), 0, s_pre,
+                         (const SplatRec *)at<SplatRec>(frame, L.recs), (const float4 *)at<float4>(frame, L.cull2d),
+                         n, counts, at<uint32_t>(frame, L.keep)));
     }
     if (fork && !HGS_SORT_ON_AUX) HGS_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(settings->aux_events[1]), aux));
     // 2. depth sort: 8 digit passes launched, the constant ones exit at once

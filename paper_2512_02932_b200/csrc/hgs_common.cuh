@@ -29,6 +29,9 @@ namespace hgs {
 #ifndef HGS_PDL
 #define HGS_PDL 1
 #endif
+#ifndef HGS_DEPTH_SORT_TRIGGER
+#define HGS_DEPTH_SORT_TRIGGER 0  // early triggers along the depth sort's chain (see hgs_api.cu)
+#endif
 __device__ __forceinline__ void pdl_launch_dependents() {
 #if HGS_PDL
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");

@@ -77,7 +77,7 @@ template <bool G64>
 __global__ void __launch_bounds__(256) k_depth_keys(SceneView sc, CamD cam, unsigned long long *__restrict__ keys,
                                                     uint32_t *__restrict__ vals, uint8_t *__restrict__ kept,
                                                     uint32_t *__restrict__ hist, FrameState *__restrict__ st) {
-  pdl_launch_dependents();  // k_sort_plan may be scheduled as this grid drains
+  if (HGS_DEPTH_SORT_TRIGGER) pdl_launch_dependents();
   using G = SceneGeom<G64>;
   __shared__ uint32_t sh[8 * kRadix];
   __shared__ uint32_t s_m;
@@ -215,6 +215,7 @@ __device__ __forceinline__ void write_record(const ProjD &o, uint32_t idx, int W
 __global__ void __launch_bounds__(256) k_tile_counts(const SplatRec *__restrict__ recs,
                                                      const float4 *__restrict__ cull2d, int64_t n,
                                                      uint32_t *__restrict__ counts, uint32_t *__restrict__ keep) {
+  pdl_wait();  // launched right behind the preprocess (no early trigger there)
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const uint32_t nt = counts[i];  // bbox tiles (0: culled or off screen)
     if (nt <= 1u || nt > (uint32_t)kTileCullMax) continue;  // one tile: the compositor's warp cull suffices
@@ -250,7 +251,7 @@ __global__ void __launch_bounds__(256) k_tile_counts(const SplatRec *__restrict_
 __global__ void k_rank_scatter(const uint32_t *__restrict__ vals_a, const uint32_t *__restrict__ vals_b,
                                const FrameState *__restrict__ st, int64_t n, uint32_t *__restrict__ rank_of,
                                uint32_t *__restrict__ order) {
-  pdl_launch_dependents();
+  if (HGS_DEPTH_SORT_TRIGGER) pdl_launch_dependents();
   pdl_wait();
   const uint32_t *sorted_idx = (st->sort_np & 1u) ? vals_b : vals_a;
   const int64_t m = st->m_count;
@@ -267,7 +268,7 @@ __global__ void k_rank_scatter(const uint32_t *__restrict__ vals_a, const uint32
 // the device-side pass list the onesweep passes read.
 __global__ void k_sort_plan(const uint32_t *__restrict__ hist, int64_t n, uint32_t *__restrict__ offsets,
                             FrameState *__restrict__ st) {
-  pdl_launch_dependents();
+  if (HGS_DEPTH_SORT_TRIGGER) pdl_launch_dependents();
   pdl_wait();
   __shared__ uint32_t s[kRadix];
   __shared__ int s_trivial[8];

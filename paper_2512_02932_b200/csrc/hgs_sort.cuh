@@ -109,7 +109,10 @@ __global__ void __launch_bounds__(kSortThreads, sizeof(K) == 4 ? HGS_SORT_MINB32
                                                            const uint32_t *__restrict__ digit_offsets,
                                                            uint32_t *__restrict__ lookback,
                                                            uint32_t *__restrict__ tile_counter, SortDev dv) {
-  pdl_launch_dependents();
+  // the depth sort's passes (dv.plan_np) do not trigger early: their
+  // successors would wait on SM slots the preprocess beside them needs
+  if (!HGS_DEPTH_SORT_TRIGGER && dv.plan_np == nullptr) pdl_launch_dependents();
+  if (HGS_DEPTH_SORT_TRIGGER) pdl_launch_dependents();
   pdl_wait();
   if (dv.plan_np) {
     if ((unsigned)dv.pass >= *dv.plan_np) return;
