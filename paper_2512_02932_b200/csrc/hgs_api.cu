@@ -365,10 +365,10 @@ int hgs_forward(const hgs_scene *scene, const hgs_camera *camera, const hgs_sett
                                                      counts, at<uint32_t>(frame, L.keep));
       HGS_LAUNCHED();
     }
-    k_scan_counts<<<(unsigned)ceil_div(n, kScanTile), kScanThreads, 0, s>>>(
-        counts, order, -1, at<unsigned long long>(frame, L.pair_off), at<unsigned long long>(frame, L.lb_scan), st,
-        std::min<int64_t>(cap, 0xffffffffll));
-    HGS_LAUNCHED();
+    HGS_CUDA(launch_pdl(k_scan_counts, dim3((unsigned)ceil_div(n, kScanTile)), dim3(kScanThreads), 0, s,
+                        (const uint32_t *)counts, (const uint32_t *)order, (int64_t)-1,
+                        at<unsigned long long>(frame, L.pair_off), at<unsigned long long>(frame, L.lb_scan), st,
+                        (int64_t)std::min<int64_t>(cap, 0xffffffffll)));
   }
   HGS_CUDA(record_event(settings, 2, s));
   // 4. duplicate + tile sort + ranges (K and the capacity verdict on the device)

@@ -78,6 +78,7 @@ __global__ void __launch_bounds__(256) k_depth_keys(SceneView sc, CamD cam, unsi
                                                     uint32_t *__restrict__ vals, uint8_t *__restrict__ kept,
                                                     uint32_t *__restrict__ hist, FrameState *__restrict__ st) {
   if (HGS_DEPTH_SORT_TRIGGER) pdl_launch_dependents();
+  pdl_wait();
   using G = SceneGeom<G64>;
   __shared__ uint32_t sh[8 * kRadix];
   __shared__ uint32_t s_m;
@@ -120,9 +121,9 @@ __global__ void __launch_bounds__(256) k_depth_keys(SceneView sc, CamD cam, unsi
 }
 cudaError_t launch_depth_keys(const SceneView &sc, const CamD &cam, unsigned long long *keys, uint32_t *vals,
                               uint8_t *kept, uint32_t *hist, FrameState *st, int grid, cudaStream_t s) {
-  if (sc.center64) k_depth_keys<true><<<grid, 256, 0, s>>>(sc, cam, keys, vals, kept, hist, st);
-  else k_depth_keys<false><<<grid, 256, 0, s>>>(sc, cam, keys, vals, kept, hist, st);
-  return cudaGetLastError();
+  // right behind k_init_state under PDL (set up while it runs)
+  if (sc.center64) return launch_pdl(k_depth_keys<true>, dim3(grid), dim3(256), 0, s, sc, cam, keys, vals, kept, hist, st);
+  return launch_pdl(k_depth_keys<false>, dim3(grid), dim3(256), 0, s, sc, cam, keys, vals, kept, hist, st);
 }
 
 // ---------------------------------------------------- preprocess + scan
@@ -409,6 +410,7 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_counts(const uint32_t *__
                                                               unsigned long long *__restrict__ scan_lb,
                                                               FrameState *__restrict__ st, int64_t cap) {
   pdl_launch_dependents();  // k_duplicate may be scheduled as this grid drains
+  pdl_wait();
   __shared__ uint32_t s_tile;
   if (m < 0) m = st->m_count;
   if ((int64_t)blockIdx.x * kScanTile >= m) return;  // launched for N, not for M
