@@ -769,10 +769,10 @@ def main():
             stage_roofs[nm] = {"ms": t_ms, "GB/s": gbs, "hbm_frac": gbs / hbm_peak}
 
     # init_state, depth_keys, sort_plan, 8 depth passes (the constant digits' exit at once),
-    # preprocess, rank_scatter, scan_counts, duplicate, radix_offsets, <tile passes>, tile_ranges,
-    # composite_fwd, fixup_fwd
-    launches_fwd = 18 + n_tile_passes
-    # init_state + (composite_bwd + fixup_bwd + chain_rule) per chunk of <= 4 gradients; under
+    # preprocess, tile_counts, rank_scatter, scan_counts, duplicate, radix_offsets, <tile passes>,
+    # tile_ranges, composite_fwd, fixup_fwd (the launch list in profiles/launches_r02.csv)
+    launches_fwd = 20 + n_tile_passes
+    # init_bwd + (composite_bwd + fixup_bwd + chain_rule) per chunk of <= 4 gradients; under
     # N ranks the chain rule runs in N_BUCKETS Gaussian ranges (overlapped all-reduce)
     launches_bwd = 1 + 3 * ((a.kg + 3) // 4) + ((N_BUCKETS - 1) if world > 1 else 0)
     value = world * 1000.0 / step_ms
