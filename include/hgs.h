@@ -319,6 +319,14 @@ int hgs_widen_d2h(const float *src, double *dst_host, int64_t n, double *scratch
 int hgs_host_widen(const float *src, double *dst, int64_t n, int threads);
 int hgs_host_narrow(const double *src, float *dst, int64_t n, int threads);
 int hgs_host_copy(const void *src, void *dst, int64_t bytes, int threads);
+/* Deterministic float64 sums for the host-scene fingerprint: sums[b] = the
+ * sum of elements [b B, (b + 1) B) in a fixed order (B = hgs_host_sum_block(),
+ * blocks at absolute positions); the caller adds the block sums in order.
+ * The copying form also copies src to dst (the upload's staging pass) and
+ * yields the same sums. */
+int64_t hgs_host_sum_block(void);
+int hgs_host_block_sums(const double *src, int64_t n, double *sums, int threads);
+int hgs_host_copy_block_sums(const double *src, double *dst, int64_t n, double *sums, int threads);
 
 const char *hgs_status_string(int status);
 int hgs_abi_version(void);

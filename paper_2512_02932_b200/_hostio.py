@@ -140,39 +140,81 @@ def _align(n):
     return (n + 255) & ~255
 
 
-def upload(arrays, device, tag="up"):
+def fingerprint_sum(a):
+    """The scene fingerprint's sum of one float64 host array: deterministic
+    block sums (hgs_host_block_sums, all cores) added in order -- the same
+    value ``upload(..., sums_out=)`` produces while it stages the array."""
+    import torch
+    a = np.asarray(a)
+    if a.dtype != np.float64 or not a.flags["C_CONTIGUOUS"]:
+        return float(torch.from_numpy(np.ascontiguousarray(a)).sum())
+    from . import _lib
+    L = _lib.lib()
+    n = a.size
+    sums = np.zeros(max(-(-n // L.hgs_host_sum_block()), 1))
+    if L.hgs_host_block_sums(ctypes.c_void_p(a.ctypes.data), n, ctypes.c_void_p(sums.ctypes.data), 0) != 0:
+        raise RuntimeError("hgs_host_block_sums failed")
+    return _add_in_order(sums)
+
+
+def _add_in_order(sums):
+    t = 0.0
+    for v in sums.tolist():
+        t += v
+    return t
+
+
+def upload(arrays, device, tag="up", sums_out=None):
     """[(numpy array, torch dtype)] -> list of device tensors of those dtypes.
 
-    One pinned staging buffer and one device allocation for the whole list."""
+    One pinned staging buffer and one device allocation for the whole list.
+    ``sums_out``: a dict whose keys are indices of float64 arrays staged as
+    float64; their fingerprint sums (``fingerprint_sum``) are stored under
+    the same keys, computed by the staging pass itself."""
     import torch
     metas = []
     total = 0
-    for a, dt in arrays:
+    for i, (a, dt) in enumerate(arrays):
         a = np.ascontiguousarray(a)
         nb = a.size * torch.empty((), dtype=dt).element_size()
-        metas.append((a, dt, total, nb))
+        metas.append((i, a, dt, total, nb))
         total += _align(nb)
     ent = _stage(tag, total)
     stage = ent[0]
     dev = torch.empty(max(total, 1), dtype=torch.uint8, device=device)
     stream = torch.cuda.current_stream(device)
     outs = []
-    for a, dt, off, nb in metas:
+    for i, a, dt, off, nb in metas:
         src = torch.from_numpy(a).reshape(-1)
         hv = stage[off:off + nb].view(dt)
         dv = dev[off:off + nb].view(dt)
         esz = max(hv.element_size(), 1)
         step = max(_CHUNK // esz, 1)
         narrow = _NT and src.dtype == torch.float64 and dt == torch.float32
+        want_sum = (sums_out is not None and i in sums_out and _NT
+                    and src.dtype == torch.float64 and dt == torch.float64)
+        if want_sum:
+            from . import _lib
+            B = _lib.lib().hgs_host_sum_block()
+            assert step % B == 0, "staging chunks must hold whole fingerprint blocks"
+            bsums = np.zeros(max(-(-src.numel() // B), 1))
         for s in range(0, src.numel(), step):
             e = min(s + step, src.numel())
             if narrow:  # f64 -> f32 into pinned on all cores, streaming stores
                 _convert("hgs_host_narrow", src[s:e], hv[s:e])
+            elif want_sum:  # copy + the fingerprint's block sums in one pass (step is a multiple of B)
+                rc = _lib.lib().hgs_host_copy_block_sums(ctypes.c_void_p(src[s:e].data_ptr()),
+                                                         ctypes.c_void_p(hv[s:e].data_ptr()), e - s,
+                                                         ctypes.c_void_p(bsums.ctypes.data + 8 * (s // B)), 0)
+                if rc != 0:
+                    raise RuntimeError("hgs_host_copy_block_sums failed (%d)" % rc)
             elif _NT and src.dtype == dt:
                 _copy(src[s:e], hv[s:e])
             else:
                 hv[s:e].copy_(src[s:e])
             dv[s:e].copy_(hv[s:e], non_blocking=True)    # async DMA while the next chunk converts
+        if want_sum:
+            sums_out[i] = _add_in_order(bsums)
         outs.append(dv.view(a.shape))
     ev = torch.cuda.Event()
     ev.record(stream)

@@ -172,18 +172,21 @@ class DeviceGaussians:
         self.extent = float(extent)
         self.geom64 = None
         self._geom64_versions = None
+        self.host_fingerprint = None  # from_host(fingerprint=True): raster.scene_fingerprint of the source
         if validate:
             self.validate()
 
     GEOM_FIELDS = ("center", "log_scale", "rotation", "opacity_logit")
 
     @classmethod
-    def from_host(cls, scene, device="cuda", validate=False, geom64=True):
+    def from_host(cls, scene, device="cuda", validate=False, geom64=True, fingerprint=False):
         """Upload a host scene through pinned staging, pipelined with the DMA
         (_hostio.upload).  The geometry crosses as float64 (kept as ``geom64``
         for the exact decisions, its float32 rounding made on the device);
         SH coefficients are converted to float32 on the host cores.
-        ``geom64=False`` uploads float32 geometry only."""
+        ``geom64=False`` uploads float32 geometry only.  ``fingerprint``:
+        also set ``host_fingerprint`` -- raster.scene_fingerprint of the host
+        scene, its sums taken by the staging pass itself (no extra read)."""
         import torch
 
         from ._hostio import upload
@@ -192,10 +195,17 @@ class DeviceGaussians:
         if device.type == "cuda" and device.index is None:
             device = torch.device("cuda", torch.cuda.current_device())
         gdt = torch.float64 if geom64 else torch.float32
+        sums = {0: None, 1: None, 3: None} if fingerprint else None
         t = upload([(scene.center, gdt), (scene.log_scale, gdt), (scene.rotation, gdt),
                     (scene.opacity_logit, gdt), (scene.sh_coeffs, torch.float32),
-                    (scene.type_spec, torch.uint8)], device, tag="scene")
+                    (scene.type_spec, torch.uint8)], device, tag="scene", sums_out=sums)
         out = cls(*t, extent=scene.extent, validate=validate)
+        if fingerprint:
+            from .raster import scene_fingerprint
+            if all(sums[k] is not None for k in (0, 1, 3)):
+                out.host_fingerprint = (scene.count, sums[0], sums[3], sums[1])
+            else:  # not staged as float64: the plain fingerprint
+                out.host_fingerprint = scene_fingerprint(scene)
         if geom64:
             out.geom64 = tuple(t[:4])
             out._geom64_versions = out.versions()

@@ -145,3 +145,99 @@ extern "C" int hgs_host_copy(const void *src, void *dst, int64_t bytes, int thre
   });
   return HGS_OK;
 }
+
+// ---------------------------------------------------------------------------
+// Scene fingerprint sums (raster.scene_fingerprint: the sums of the float64
+// centre / opacity / log-scale arrays, render.py:67-70).  Deterministic: the
+// array is cut into fixed kSumBlock-element blocks at absolute positions,
+// each block summed in one fixed order (8 lanes, then a fixed reduction);
+// the caller adds the block sums in order.  The copying variant produces
+// the same block sums while it copies (the upload's staging pass), so a
+// render's fingerprint costs no extra read of the scene.
+namespace {
+
+constexpr int64_t kSumBlock = 32768;
+
+template <bool COPY>
+__attribute__((target("avx2"))) double block_pass(const double *__restrict__ s, double *__restrict__ d, int64_t n) {
+  __m256d a0 = _mm256_setzero_pd(), a1 = _mm256_setzero_pd();
+  int64_t i = 0;
+  // the copy goes out with streaming stores when the destination allows
+  // (the staging is read by the DMA, not by the CPU); same sums either way
+  const bool nt = COPY && (reinterpret_cast<uintptr_t>(d) & 31u) == 0;
+  for (; i + 8 <= n; i += 8) {
+    const __m256d x0 = _mm256_loadu_pd(s + i), x1 = _mm256_loadu_pd(s + i + 4);
+    a0 = _mm256_add_pd(a0, x0);
+    a1 = _mm256_add_pd(a1, x1);
+    if (COPY) {
+      if (nt) {
+        _mm256_stream_pd(d + i, x0);
+        _mm256_stream_pd(d + i + 4, x1);
+      } else {
+        _mm256_storeu_pd(d + i, x0);
+        _mm256_storeu_pd(d + i + 4, x1);
+      }
+    }
+  }
+  alignas(32) double l0[4], l1[4];
+  _mm256_store_pd(l0, a0);
+  _mm256_store_pd(l1, a1);
+  double t = ((l0[0] + l0[1]) + (l0[2] + l0[3])) + ((l1[0] + l1[1]) + (l1[2] + l1[3]));
+  for (; i < n; ++i) {
+    t += s[i];
+    if (COPY) d[i] = s[i];
+  }
+  return t;
+}
+
+template <bool COPY>
+double block_pass_scalar(const double *s, double *d, int64_t n) {
+  double l0[4] = {0, 0, 0, 0}, l1[4] = {0, 0, 0, 0};
+  int64_t i = 0;
+  for (; i + 8 <= n; i += 8) {
+    for (int k = 0; k < 4; ++k) {
+      l0[k] += s[i + k];
+      l1[k] += s[i + 4 + k];
+      if (COPY) {
+        d[i + k] = s[i + k];
+        d[i + 4 + k] = s[i + 4 + k];
+      }
+    }
+  }
+  double t = ((l0[0] + l0[1]) + (l0[2] + l0[3])) + ((l1[0] + l1[1]) + (l1[2] + l1[3]));
+  for (; i < n; ++i) {
+    t += s[i];
+    if (COPY) d[i] = s[i];
+  }
+  return t;
+}
+
+template <bool COPY>
+int block_sums(const double *src, double *dst, int64_t n, double *sums, int threads) {
+  if (n < 0 || (n > 0 && (!src || !sums || (COPY && !dst)))) return HGS_ERR_CONFIG;
+  const int64_t nb = (n + kSumBlock - 1) / kSumBlock;
+  const bool v = has_avx2();
+  if (threads <= 0) threads = omp_get_max_threads();
+  if (nb < threads) threads = (int)(nb > 0 ? nb : 1);
+#pragma omp parallel for schedule(static) num_threads(threads)
+  for (int64_t b = 0; b < nb; ++b) {
+    const int64_t lo = b * kSumBlock, len = (lo + kSumBlock <= n ? kSumBlock : n - lo);
+    sums[b] = v ? block_pass<COPY>(src + lo, COPY ? dst + lo : nullptr, len)
+                : block_pass_scalar<COPY>(src + lo, COPY ? dst + lo : nullptr, len);
+    if (COPY) _mm_sfence();
+  }
+  return HGS_OK;
+}
+
+}  // namespace
+
+extern "C" int64_t hgs_host_sum_block(void) { return kSumBlock; }
+
+extern "C" int hgs_host_block_sums(const double *src, int64_t n, double *sums, int threads) {
+  return block_sums<false>(src, nullptr, n, sums, threads);
+}
+
+extern "C" int hgs_host_copy_block_sums(const double *src, double *dst, int64_t n, double *sums, int threads) {
+  return block_sums<true>(src, dst, n, sums, threads);
+}
+

@@ -56,9 +56,11 @@ def scene_fingerprint(scene):
     scenes use tensor version counters (no device sync)."""
     if isinstance(scene, DeviceGaussians):
         return ("device", scene.count) + scene.versions()
-    import torch  # multi-threaded sums (numpy's are single-threaded: 5 ms at 1M)
-    return (scene.count,) + tuple(float(torch.from_numpy(np.ascontiguousarray(a)).sum())
-                                  for a in (scene.center, scene.opacity_logit, scene.log_scale))
+    # deterministic block sums on all host cores (numpy's sums are
+    # single-threaded: 5 ms at 1M); render takes the same sums during the
+    # scene's upload (DeviceGaussians.from_host(fingerprint=True))
+    from ._hostio import fingerprint_sum
+    return (scene.count,) + tuple(fingerprint_sum(a) for a in (scene.center, scene.opacity_logit, scene.log_scale))
 
 
 @dataclass
@@ -441,13 +443,13 @@ def _render(scene, camera, settings, naive, fast):
     if not isinstance(scene, GaussianSet):
         scene = GaussianSet(scene.center, scene.log_scale, scene.rotation, scene.opacity_logit,
                             scene.sh_coeffs, scene.type_spec)
-    ds = DeviceGaussians.from_host(scene)
+    ds = DeviceGaussians.from_host(scene, fingerprint=True)
     imgs, frame = rasterize(ds, camera, settings, flags)
     from ._hostio import download
     keys = ("color", "depth", "transmittance")
     host = dict(zip(keys, download([imgs[k] for k in keys], tag="images")))
     return RenderOutput(host["color"], host["depth"], host["transmittance"], None, None, frame,
-                        scene_fingerprint(scene), host_scene=scene,
+                        ds.host_fingerprint, host_scene=scene,
                         lazy={"alpha": imgs["alpha"], "normal": imgs["normal"]})
 
 

@@ -15,7 +15,7 @@ def _header_symbols():
     inc = os.path.join(REPO, "include")
     src = "".join(open(os.path.join(inc, f)).read() for f in sorted(os.listdir(inc))
                   if f.endswith(".h"))
-    return sorted(set(re.findall(r"^\s*(?:int|size_t|const char \*)\s*(hgs_\w+)\s*\(", src, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int|int64_t|size_t|const char \*)\s*(hgs_\w+)\s*\(", src, re.M)))
 
 
 @pytest.fixture(scope="module")
@@ -177,3 +177,31 @@ def test_host_conversions(L, threads):
             assert L.hgs_host_copy(x.ctypes.data, b.ctypes.data, 8 * n, threads) == 0
             assert b.tobytes() == x.tobytes()
     assert L.hgs_host_widen(None, None, 5, 0) != 0
+
+
+def test_host_block_sums(L):
+    """The scene-fingerprint sums: the copying and the plain form give the
+    same block sums (bit for bit), at any thread count and alignment, and
+    the copy is exact."""
+    import numpy as np
+    B = L.hgs_host_sum_block()
+    assert B > 0
+    rng = np.random.default_rng(5)
+    for n in (0, 1, 9, B - 1, B, 3 * B + 17):
+        x = rng.standard_normal(n) * 1e3
+        nb = (n + B - 1) // B
+        ref = None
+        for threads in (1, 0, 3):
+            for off in (0, 1):
+                s1 = np.zeros(max(nb, 1))
+                assert L.hgs_host_block_sums(x.ctypes.data, n, s1.ctypes.data, threads) == 0
+                d = np.empty(n + off)[off:]
+                s2 = np.zeros(max(nb, 1))
+                assert L.hgs_host_copy_block_sums(x.ctypes.data, d.ctypes.data, n, s2.ctypes.data, threads) == 0
+                assert d.tobytes() == x.tobytes()
+                assert s1.tobytes() == s2.tobytes()
+                if ref is None:
+                    ref = s1.copy()
+                assert s1.tobytes() == ref.tobytes()
+        if n:
+            np.testing.assert_allclose(sum(ref[:nb]), x.sum(), rtol=1e-12, atol=1e-9)

@@ -71,3 +71,21 @@ def test_randomised_scenes(case):
     scene.opacity_logit[:] = (scene.opacity_logit + np.float32(rng.uniform(-2, 3))).astype(np.float32)
     bg = tuple(float(x) for x in rng.uniform(0, 1, 3))
     _check(scene, cam, RenderSettings(background=bg))
+
+
+@pytest.mark.gpu
+def test_host_fingerprint_fused_with_upload():
+    """render's scene fingerprint comes from the upload's staging pass; it must
+    equal raster.scene_fingerprint of the same host scene (what backward
+    checks), or backward would raise IntegrityError on an unchanged scene."""
+    from paper_2512_02932_b200 import raster
+    from paper_2512_02932_b200.core import DeviceGaussians, GaussianSet
+    from paper_2512_02932_b200.synthetic import synthetic_scene
+    for n in (1000, 70_000, 300_000):
+        scene, _ = synthetic_scene(n, 64, 48, 3, seed=1)
+        hs = GaussianSet(scene.center, scene.log_scale, scene.rotation, scene.opacity_logit,
+                         scene.sh_coeffs, scene.type_spec)
+        ds = DeviceGaussians.from_host(hs, fingerprint=True)
+        assert ds.host_fingerprint == raster.scene_fingerprint(hs)
+        hs.center[0, 0] += 1.0  # a changed scene no longer matches
+        assert ds.host_fingerprint != raster.scene_fingerprint(hs)
