@@ -27,6 +27,9 @@ constexpr int kMaxGrid = 148 * 8;
 #define HGS_DEPTH_SORT_PDL 1
 #endif
 constexpr bool kDepthSortPdl = HGS_DEPTH_SORT_PDL != 0;
+#ifndef HGS_FUSE_RANK_SCATTER
+#define HGS_FUSE_RANK_SCATTER 0  // 1: the depth order written by the last active depth-sort pass (A/B: neutral, 278.3 vs 278.0 it/s)
+#endif
 #ifndef HGS_TILE_COUNTS_PDL
 #define HGS_TILE_COUNTS_PDL 1
 #endif
@@ -347,11 +350,15 @@ int hgs_forward(const hgs_scene *scene, const hgs_camera *camera, const hgs_sett
       uint32_t *vb = at<uint32_t>(frame, (i & 1) ? L.vals_a : L.vals_b);
       HGS_CUDA(launch_ex(kDepthSortPdl, k_onesweep<unsigned long long>, dim3((unsigned)sort_tiles_n), dim3(kSortThreads), 0, s_sort,
                           ka, va, kb, vb, n, 0, at<uint32_t>(frame, L.off_d), lb + (size_t)i * sort_tiles_n * kRadix,
-                          st->tile_counters + 1 + i, SortDev{&st->sort_np, st->sort_digit, i, nullptr, nullptr}));
+                          st->tile_counters + 1 + i,
+                          HGS_FUSE_RANK_SCATTER ? SortDev{&st->sort_np, st->sort_digit, i, nullptr, nullptr, rank_of, order,
+                                                          &st->m_count}
+                                                : SortDev{&st->sort_np, st->sort_digit, i, nullptr, nullptr}));
       HGS_LAUNCHED();
     }
-    HGS_CUDA(launch_ex(kDepthSortPdl, k_rank_scatter, dim3(grid_for(n, 256)), dim3(256), 0, s_sort, at<uint32_t>(frame, L.vals_a),
-                        at<uint32_t>(frame, L.vals_b), st, n, rank_of, order));
+    if (!HGS_FUSE_RANK_SCATTER)
+      HGS_CUDA(launch_ex(kDepthSortPdl, k_rank_scatter, dim3(grid_for(n, 256)), dim3(256), 0, s_sort,
+                         at<uint32_t>(frame, L.vals_a), at<uint32_t>(frame, L.vals_b), st, n, rank_of, order));
     HGS_LAUNCHED();
     if (fork && HGS_SORT_ON_AUX) HGS_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(settings->aux_events[1]), aux));
     // join: the scan below needs both the depth order and the tile counts

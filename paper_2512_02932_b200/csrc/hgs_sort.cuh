@@ -99,6 +99,12 @@ struct SortDev {
   int pass;
   const unsigned long long *n_dev;     // &FrameState::k_total (tile sort) or null
   const unsigned *status;              // &FrameState::status (with n_dev)
+  // depth sort only (null otherwise): the last active pass also writes the
+  // depth order (order[r] = Gaussian, rank_of[Gaussian] = r, or ~0 past M)
+  // as it stores its output -- the separate rank-scatter pass is not needed
+  uint32_t *rank_of = nullptr;
+  uint32_t *order = nullptr;
+  const uint32_t *m_count = nullptr;
 };
 
 template <typename K>
@@ -114,8 +120,21 @@ __global__ void __launch_bounds__(kSortThreads, sizeof(K) == 4 ? HGS_SORT_MINB32
   if (!HGS_DEPTH_SORT_TRIGGER && dv.plan_np == nullptr) pdl_launch_dependents();
   if (HGS_DEPTH_SORT_TRIGGER) pdl_launch_dependents();
   pdl_wait();
+  bool emit_order = false;  // this pass writes the depth order (the last active one)
   if (dv.plan_np) {
-    if ((unsigned)dv.pass >= *dv.plan_np) return;
+    const unsigned np = *dv.plan_np;
+    if (dv.order && np == 0u && dv.pass == 0) {
+      // every digit constant: the input order is the sorted order
+      const uint32_t m = *dv.m_count;
+      for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t g = vals_in[r];
+        dv.rank_of[g] = r < m ? (uint32_t)r : 0xffffffffu;
+        dv.order[r] = g;
+      }
+      return;
+    }
+    if ((unsigned)dv.pass >= np) return;
+    emit_order = dv.order != nullptr && (unsigned)dv.pass + 1u == np;
     const unsigned dg = dv.plan_digit[dv.pass];
     shift = (int)dg * kRadixBits;
     digit_offsets += dg * kRadix;
@@ -234,12 +253,18 @@ __global__ void __launch_bounds__(kSortThreads, sizeof(K) == 4 ? HGS_SORT_MINB32
   __syncthreads();
   const int64_t rem = n - tile_base;
   const int valid = rem < kSortTile ? (int)rem : kSortTile;
+  const uint32_t m_emit = emit_order ? *dv.m_count : 0u;
   for (int p = tid; p < valid; p += kSortThreads) {
     K k = s_keys[p];
     uint32_t d = digit_of(k, shift);
     uint32_t o = s_gbase[d] + (uint32_t)p - s_lstart[d];
     keys_out[o] = k;
-    vals_out[o] = s_vals[p];
+    const uint32_t g = s_vals[p];
+    vals_out[o] = g;
+    if (emit_order) {
+      dv.rank_of[g] = o < m_emit ? o : 0xffffffffu;
+      dv.order[o] = g;
+    }
   }
 }
 
