@@ -32,8 +32,8 @@ __all__ = ["ALPHA_CLAMP", "DegenerateIntersection", "EARLY_STOP_T", "LOWPASS_SIG
            "HAVE_EXT", "BlendLog", "RenderOutput", "active_backend", "render",
            "render_naive", "scene_fingerprint"]
 
-TILE_SIZES = (8, 16, 32, 64)
-_OVERLAP = os.environ.get("HGS_OVERLAP", "1") != "0"  # A/B switch of the preprocess side stream  # RenderSettings.tile_size values SplatFrame can export
+TILE_SIZES = (8, 16, 32, 64)  # RenderSettings.tile_size values SplatFrame can export
+_OVERLAP = os.environ.get("HGS_OVERLAP", "1") != "0"  # A/B switch of the preprocess side stream
 
 
 def active_backend(settings: RenderSettings):
