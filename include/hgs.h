@@ -324,6 +324,10 @@ int hgs_host_copy(const void *src, void *dst, int64_t bytes, int threads);
  * blocks at absolute positions); the caller adds the block sums in order.
  * The copying form also copies src to dst (the upload's staging pass) and
  * yields the same sums. */
+/* hgs_host_narrow that also counts the non-finite (inf / NaN) float64
+ * inputs into *nonfinite (the reference's upstream-gradient check, on the
+ * float64 values, in the same pass). */
+int hgs_host_narrow_count(const double *src, float *dst, int64_t n, int threads, int64_t *nonfinite);
 int64_t hgs_host_sum_block(void);
 int hgs_host_block_sums(const double *src, int64_t n, double *sums, int threads);
 int hgs_host_copy_block_sums(const double *src, double *dst, int64_t n, double *sums, int threads);

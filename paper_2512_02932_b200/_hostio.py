@@ -164,13 +164,15 @@ def _add_in_order(sums):
     return t
 
 
-def upload(arrays, device, tag="up", sums_out=None):
+def upload(arrays, device, tag="up", sums_out=None, nonfinite_out=None):
     """[(numpy array, torch dtype)] -> list of device tensors of those dtypes.
 
     One pinned staging buffer and one device allocation for the whole list.
     ``sums_out``: a dict whose keys are indices of float64 arrays staged as
     float64; their fingerprint sums (``fingerprint_sum``) are stored under
-    the same keys, computed by the staging pass itself."""
+    the same keys, computed by the staging pass itself.  ``nonfinite_out``:
+    likewise, for float64 arrays narrowed to float32, the number of inf /
+    NaN float64 inputs (counted by the narrowing pass)."""
     import torch
     metas = []
     total = 0
@@ -191,6 +193,8 @@ def upload(arrays, device, tag="up", sums_out=None):
         esz = max(hv.element_size(), 1)
         step = max(_CHUNK // esz, 1)
         narrow = _NT and src.dtype == torch.float64 and dt == torch.float32
+        count_bad = narrow and nonfinite_out is not None and i in nonfinite_out
+        bad = 0
         want_sum = (sums_out is not None and i in sums_out and _NT
                     and src.dtype == torch.float64 and dt == torch.float64)
         if want_sum:
@@ -200,7 +204,15 @@ def upload(arrays, device, tag="up", sums_out=None):
             bsums = np.zeros(max(-(-src.numel() // B), 1))
         for s in range(0, src.numel(), step):
             e = min(s + step, src.numel())
-            if narrow:  # f64 -> f32 into pinned on all cores, streaming stores
+            if count_bad:  # f64 -> f32 and the finiteness check in one pass
+                from . import _lib
+                c = ctypes.c_int64(0)
+                if _lib.lib().hgs_host_narrow_count(ctypes.c_void_p(src[s:e].data_ptr()),
+                                                    ctypes.c_void_p(hv[s:e].data_ptr()), e - s, 0,
+                                                    ctypes.byref(c)) != 0:
+                    raise RuntimeError("hgs_host_narrow_count failed")
+                bad += c.value
+            elif narrow:  # f64 -> f32 into pinned on all cores, streaming stores
                 _convert("hgs_host_narrow", src[s:e], hv[s:e])
             elif want_sum:  # copy + the fingerprint's block sums in one pass (step is a multiple of B)
                 rc = _lib.lib().hgs_host_copy_block_sums(ctypes.c_void_p(src[s:e].data_ptr()),
@@ -215,6 +227,8 @@ def upload(arrays, device, tag="up", sums_out=None):
             dv[s:e].copy_(hv[s:e], non_blocking=True)    # async DMA while the next chunk converts
         if want_sum:
             sums_out[i] = _add_in_order(bsums)
+        if count_bad:
+            nonfinite_out[i] = bad
         outs.append(dv.view(a.shape))
     ev = torch.cuda.Event()
     ev.record(stream)

@@ -50,7 +50,7 @@ EXPORTS = ("hgs_abi_version", "hgs_status_string", "hgs_frame_bytes", "hgs_forwa
            "hgs_densify_stats", "hgs_densify_scratch_bytes", "hgs_densify_plan", "hgs_densify_apply",
            "hgs_tile_bins_scratch_bytes", "hgs_frame_tile_bins", "hgs_eval_contributions",
            "hgs_frame_sync_info", "hgs_host_register", "hgs_host_unregister", "hgs_widen_d2h",
-           "hgs_host_widen", "hgs_host_narrow", "hgs_host_copy",
+           "hgs_host_widen", "hgs_host_narrow", "hgs_host_copy", "hgs_host_narrow_count",
            "hgs_host_sum_block", "hgs_host_block_sums", "hgs_host_copy_block_sums",
            "hgs_effective_rank_f64", "hgs_reparameterize_f64", "hgs_modulation_f64")
 
@@ -179,6 +179,7 @@ def lib():
     L.hgs_host_widen.argtypes = [_vp, _vp, _i64, _i32]
     L.hgs_host_narrow.argtypes = [_vp, _vp, _i64, _i32]
     L.hgs_host_copy.argtypes = [_vp, _vp, _i64, _i32]
+    L.hgs_host_narrow_count.argtypes = [_vp, _vp, _i64, _i32, _vp]
     L.hgs_host_sum_block.restype = _i64
     L.hgs_host_sum_block.argtypes = []
     L.hgs_host_block_sums.argtypes = [_vp, _i64, _vp, _i32]

@@ -241,3 +241,64 @@ extern "C" int hgs_host_copy_block_sums(const double *src, double *dst, int64_t 
   return block_sums<true>(src, dst, n, sums, threads);
 }
 
+// ---------------------------------------------------------------------------
+// Narrowing with the finiteness check the reference applies to its float64
+// upstream gradients (grad/backward.py: non-finite -> IntegrityError) in the
+// same pass: the check reads the float64 values (a finite 1e300 stays
+// finite, although it overflows float32), no second read, no device sync.
+namespace {
+
+__attribute__((target("avx2"))) int64_t narrow_count_avx2(const double *__restrict__ s, float *__restrict__ d, int64_t n) {
+  const __m256d inf = _mm256_set1_pd(__builtin_inf());
+  const __m256d absmask = _mm256_castsi256_pd(_mm256_set1_epi64x(0x7fffffffffffffffll));
+  int64_t bad = 0, i = 0;
+  while (i < n && (reinterpret_cast<uintptr_t>(d + i) & 31u)) {
+    bad += !(__builtin_fabs(s[i]) < __builtin_inf());
+    d[i] = (float)s[i];
+    ++i;
+  }
+  for (; i + 8 <= n; i += 8) {
+    const __m256d a = _mm256_loadu_pd(s + i), b = _mm256_loadu_pd(s + i + 4);
+    // |x| < inf is false for inf and NaN
+    const int ma = _mm256_movemask_pd(_mm256_cmp_pd(_mm256_and_pd(a, absmask), inf, _CMP_LT_OQ));
+    const int mb = _mm256_movemask_pd(_mm256_cmp_pd(_mm256_and_pd(b, absmask), inf, _CMP_LT_OQ));
+    bad += 8 - __builtin_popcount((unsigned)(ma | (mb << 4)));
+    const __m256 v = _mm256_insertf128_ps(_mm256_castps128_ps256(_mm256_cvtpd_ps(a)), _mm256_cvtpd_ps(b), 1);
+    _mm256_stream_ps(d + i, v);
+  }
+  for (; i < n; ++i) {
+    bad += !(__builtin_fabs(s[i]) < __builtin_inf());
+    d[i] = (float)s[i];
+  }
+  return bad;
+}
+
+int64_t narrow_count_scalar(const double *s, float *d, int64_t n) {
+  int64_t bad = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    bad += !(__builtin_fabs(s[i]) < __builtin_inf());
+    d[i] = (float)s[i];
+  }
+  return bad;
+}
+
+}  // namespace
+
+extern "C" int hgs_host_narrow_count(const double *src, float *dst, int64_t n, int threads, int64_t *nonfinite) {
+  if (n < 0 || !nonfinite || (n > 0 && (!src || !dst))) return HGS_ERR_CONFIG;
+  const bool v = has_avx2();
+  int64_t total = 0;
+  if (threads <= 0) threads = omp_get_max_threads();
+  const int64_t min_per = 1 << 16;
+  if (n / min_per < threads) threads = (int)(n / min_per > 0 ? n / min_per : 1);
+#pragma omp parallel num_threads(threads) reduction(+ : total)
+  {
+    int64_t b, e;
+    part(n, omp_get_thread_num(), omp_get_num_threads(), b, e);
+    if (e > b) total += v ? narrow_count_avx2(src + b, dst + b, e - b) : narrow_count_scalar(src + b, dst + b, e - b);
+    _mm_sfence();
+  }
+  *nonfinite = total;
+  return HGS_OK;
+}
+

@@ -107,15 +107,23 @@ def _views(flat_block, n, B):
     return ParamGrads(*out)
 
 
-def _as_device(a, dev, name, shape):
+def _as_device(a, dev, name, shape, nonfinite=None):
+    """``nonfinite``: a list to which the count of non-finite float64 host
+    inputs is appended when the upload could count them (None: not counted,
+    the caller checks on the device)."""
     import torch
     if a is None:
         return None
     if isinstance(a, torch.Tensor):
         t = a.to(device=dev, dtype=torch.float32)
+        if nonfinite is not None:
+            nonfinite.append(None)
     else:
         from ._hostio import upload
-        t = upload([(np.asarray(a), torch.float32)], dev, tag="grad_in." + name)[0]
+        cnt = {0: None}
+        t = upload([(np.asarray(a), torch.float32)], dev, tag="grad_in." + name, nonfinite_out=cnt)[0]
+        if nonfinite is not None:
+            nonfinite.append(cnt[0])
     if t.dim() == len(shape) - 1:
         t = t.unsqueeze(0)
     if tuple(t.shape[1:]) != shape[1:]:
@@ -213,17 +221,24 @@ def backward(scene, camera, output, pixel_grad, depth_grad=None, normal_grad=Non
                              % (tuple(pixel_grad.shape),))
     frame = output.frame
     dev = frame.scene.device
-    pg = _as_device(pixel_grad, dev, "pixel_grad", (0, H, W, 3))
-    dg = _as_device(depth_grad, dev, "depth_grad", (0, H, W))
-    ng = _as_device(normal_grad, dev, "normal_grad", (0, H, W, 3))
-    ag = _as_device(alpha_grad, dev, "alpha_grad", (0, H, W))
+    host_bad = []  # non-finite float64 inputs counted while narrowing (None: check on the device)
+    pg = _as_device(pixel_grad, dev, "pixel_grad", (0, H, W, 3), host_bad)
+    dg = _as_device(depth_grad, dev, "depth_grad", (0, H, W), host_bad)
+    ng = _as_device(normal_grad, dev, "normal_grad", (0, H, W, 3), host_bad)
+    ag = _as_device(alpha_grad, dev, "alpha_grad", (0, H, W), host_bad)
     kg = pg.shape[0]
     for t in (dg, ng, ag):
         if t is not None and t.shape[0] != kg:
             raise IntegrityError("extension gradients must have the same KG as pixel_grad")
     if validate:
-        bad = [~torch.isfinite(t).all() for t in (pg, dg, ng, ag) if t is not None]
-        if bool(torch.stack(bad).any()):
+        # float64 host arrays: checked on their float64 values by the upload
+        # (a finite 1e300 is accepted, as by the reference); device tensors:
+        # checked on the device
+        tens = [t for t in (pg, dg, ng, ag) if t is not None]
+        if any(c for c in host_bad if c is not None):
+            raise IntegrityError("pixel_grad contains non-finite values")
+        dev_check = [t for t, c in zip(tens, host_bad) if c is None]
+        if dev_check and bool(torch.stack([~torch.isfinite(t).all() for t in dev_check]).any()):
             raise IntegrityError("pixel_grad contains non-finite values")
     output.check_scene(scene)
     host = isinstance(scene, GaussianSet)

@@ -205,3 +205,24 @@ def test_host_block_sums(L):
                 assert s1.tobytes() == ref.tobytes()
         if n:
             np.testing.assert_allclose(sum(ref[:nb]), x.sum(), rtol=1e-12, atol=1e-9)
+
+
+def test_host_narrow_count(L):
+    """Narrowing with the float64 finiteness count (the host backward's
+    upstream-gradient check): same float32 values as numpy, inf / NaN counted
+    on the float64 inputs (a finite 1e300 is not counted)."""
+    import ctypes
+    import numpy as np
+    rng = np.random.default_rng(7)
+    for n in (0, 1, 13, 300_001):
+        x = rng.standard_normal(n)
+        if n > 10:
+            x[[1, 4, 9]] = [np.inf, np.nan, -np.inf]
+            x[2] = 1e300
+        for off in (0, 1):
+            d = np.empty(n + off, np.float32)[off:]
+            c = ctypes.c_int64(-1)
+            assert L.hgs_host_narrow_count(x.ctypes.data, d.ctypes.data, n, 0, ctypes.byref(c)) == 0
+            assert c.value == (3 if n > 10 else 0)
+            with np.errstate(over="ignore"):
+                np.testing.assert_array_equal(d, x.astype(np.float32))

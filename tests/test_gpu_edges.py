@@ -89,3 +89,32 @@ def test_host_fingerprint_fused_with_upload():
         assert ds.host_fingerprint == raster.scene_fingerprint(hs)
         hs.center[0, 0] += 1.0  # a changed scene no longer matches
         assert ds.host_fingerprint != raster.scene_fingerprint(hs)
+
+
+@pytest.mark.gpu
+def test_nonfinite_upstream_gradients_rejected():
+    """grad.backward raises IntegrityError for inf / NaN upstream gradients,
+    checked on the float64 host values while they are narrowed for upload
+    and on the device for CUDA tensors (grad/backward.py's validation)."""
+    import torch
+    from paper_2512_02932_b200 import grad, raster
+    from paper_2512_02932_b200.core import GaussianSet
+    from paper_2512_02932_b200.errors import IntegrityError
+    from paper_2512_02932_b200.synthetic import synthetic_scene
+    scene, cam = synthetic_scene(2000, 64, 48, 3, seed=4)
+    hs = GaussianSet(scene.center, scene.log_scale, scene.rotation, scene.opacity_logit,
+                     scene.sh_coeffs, scene.type_spec)
+    out = raster.render(hs, cam)
+    pg = np.random.default_rng(0).normal(size=(48, 64, 3))
+    grad.backward(hs, cam, out, pg)  # finite: fine
+    for bad in (np.nan, np.inf, -np.inf):
+        p = pg.copy()
+        p[7, 9, 1] = bad
+        with pytest.raises(IntegrityError):
+            grad.backward(hs, cam, out, p)
+        with pytest.raises(IntegrityError):
+            grad.backward(hs, cam, out, torch.from_numpy(p).float().cuda())
+    d = np.zeros((48, 64))
+    d[3, 3] = np.nan
+    with pytest.raises(IntegrityError):
+        grad.backward(hs, cam, out, pg, depth_grad=d)
