@@ -658,6 +658,7 @@ int hgs_backward(const hgs_scene *scene, const hgs_camera *camera, const hgs_set
     if (replay_only) break;  // kg <= 4: the accumulators stay for hgs_backward_chain
     ChainArgs c = c0;
     c.kg = kc;
+    c.touched = touched;  // written by this call's replay (and its fixup)
     c.grads = grads + (int64_t)k0 * n * P;
     HGS_CUDA(chain_rule_range(c, scene->sh_bases, 0, n, s));
   }

@@ -101,6 +101,9 @@ constexpr int kChainThreads = 32;
 #ifndef HGS_CHAIN_PREFETCH
 #define HGS_CHAIN_PREFETCH 1
 #endif
+#ifndef HGS_CHAIN_TOUCHED
+#define HGS_CHAIN_TOUCHED 1
+#endif
 #ifndef HGS_CHAIN_MINB
 #define HGS_CHAIN_MINB 16  // 16 warps per SM: 128 registers
 #endif
@@ -150,7 +153,9 @@ __global__ void __launch_bounds__(kChainThreads, HGS_CHAIN_MINB) k_chain_rule_t(
     const int64_t i = base + lane;
     const bool valid = lane < cnt;
     bool any = false;
-    if (valid) {
+    if (valid && HGS_CHAIN_TOUCHED && c.touched) {
+      any = c.touched[i] != 0;  // one byte instead of the 16 (+ 4) accumulator slots
+    } else if (valid) {
       for (int k = 0; k < c.kg; ++k) {
         const double2 *a2 = reinterpret_cast<const double2 *>(c.acc + ((int64_t)i * c.kg + k) * kAcc);
 #pragma unroll

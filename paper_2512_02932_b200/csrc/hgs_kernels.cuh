@@ -710,6 +710,8 @@ struct ChainArgs {
   const float2 *eig;     // (n) a 3D splat's float32 eigenbasis (c, s), by Gaussian index
   int64_t g0, g1;        // Gaussian range of this launch
   int accumulate;        // grads += (HGS_FLAG_ACCUMULATE) instead of =
+  const uint8_t *touched = nullptr;  // hgs_backward: the replay's touched mask (a superset of the
+                                     // Gaussians with a nonzero accumulator), or null: test the slots
 };
 
 struct ExchangeState {
