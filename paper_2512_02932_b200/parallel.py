@@ -13,6 +13,7 @@ sharding and reduction logic with the oracle.
 """
 
 import math
+import os
 
 __all__ = ["shard_views", "allreduce_grads", "replica_checksum", "MultiViewStep",
            "default_view_grad", "field_slices", "bucket_bounds", "bucketed_allreduce",
@@ -77,7 +78,7 @@ def bucketed_allreduce(out, n, sh_bases, buckets, write_bucket, group=None):
 
 def view_batch_grads(scene, cameras, settings, pixel_grads_of, out, scratch=None, touched=None,
                      flags=0, buckets=4, group=None, events=None, fwd_events=None, outputs=None,
-                     ext_grads=(None, None, None)):
+                     ext_grads=(None, None, None), pipeline=None):
     """One data-parallel step's gradient over this rank's views, all-reduced.
 
     Every view's gradient is added into ``out`` (flat float32 n*P, KG = 1) by
@@ -90,8 +91,11 @@ def view_batch_grads(scene, cameras, settings, pixel_grads_of, out, scratch=None
     gradient.  ``fwd_events`` / ``events`` (5 / 3 torch.cuda.Event) time the
     last view's forward / backward stages; ``outputs`` are reused image
     buffers; ``ext_grads`` = (depth, normal, alpha) upstream gradients of the
-    extension images (same for every view; each nullable).  Returns the last
-    frame."""
+    extension images (same for every view; each nullable).  ``pipeline``
+    (0 / 1 / 2, default ``HGS_VIEW_PIPELINE`` or 1): view j + 1's forward
+    is enqueued on a second stream while view j back-propagates (see
+    ``_view_batch_pipelined``, the default; ``pipeline=2`` also moves each
+    view's chain rule to a third stream).  Returns the last frame."""
     import torch.distributed as dist
 
     from . import grad, raster
@@ -122,6 +126,11 @@ def view_batch_grads(scene, cameras, settings, pixel_grads_of, out, scratch=None
             heads[j].copy_(fbuf[:16], non_blocking=True)
         return imgs, fr
 
+    pipe = _PIPELINE if pipeline is None else pipeline
+    if pipe and len(cameras) >= 2:
+        return _view_batch_pipelined(scene, cameras, settings, pixel_grads_of, out, acc, scratch,
+                                     touched, flags, buckets, group, events, fwd_events, outputs,
+                                     ext_grads, fbuf, heads, view, world, pipe)
     for j, cam in enumerate(cameras):
         last = j == len(cameras) - 1
         imgs, frame = view(j, cam, last, True)
@@ -145,6 +154,139 @@ def view_batch_grads(scene, cameras, settings, pixel_grads_of, out, scratch=None
         _redo_failed(cameras, heads, view, pixel_grads_of, ext_grads, acc, touched, scratch)
     if world > 1:  # no views on this rank: contribute zeros
         dist.all_reduce(out, op=dist.ReduceOp.SUM, group=group)
+    return frame
+
+
+_PIPELINE = int(os.environ.get("HGS_VIEW_PIPELINE", "1"))  # 0 off, 1 two streams, 2 three
+_PIPE_PRIO = os.environ.get("HGS_PIPE_PRIO", "none")  # which stream gets the higher priority
+_pipe_streams = {}  # device index -> (forward stream, backward stream)
+
+
+def _streams(dev):
+    import torch
+    idx = dev.index if dev.index is not None else torch.cuda.current_device()
+    if idx not in _pipe_streams:
+        lo, hi = torch.cuda.Stream.priority_range()  # (0, -N): lower number = higher priority
+        pf = hi if _PIPE_PRIO == "fwd" else 0
+        pb = hi if _PIPE_PRIO == "bwd" else 0
+        _pipe_streams[idx] = (torch.cuda.Stream(device=idx, priority=pf),
+                              torch.cuda.Stream(device=idx, priority=pb))
+    return _pipe_streams[idx]
+
+
+_chain_streams = {}
+
+
+def _chain_stream(dev):
+    import torch
+    idx = dev.index if dev.index is not None else torch.cuda.current_device()
+    if idx not in _chain_streams:
+        _chain_streams[idx] = torch.cuda.Stream(device=idx)
+    return _chain_streams[idx]
+
+
+def _view_batch_pipelined(scene, cameras, settings, pixel_grads_of, out, acc, scratch, touched,
+                          flags, buckets, group, events, fwd_events, outputs, ext_grads, fbuf,
+                          heads, view, world, pipe):
+    """Views of one batch are independent given the scene, so the forward of
+    view j + 1 need not wait for the backward of view j: forwards queue on
+    one stream, backwards on another (the higher-priority one), and the
+    latency-bound front end of the next view (depth sort, float64
+    preprocess, binning) fills the SM slots the current view's compositors
+    leave.  Two frame buffers and two image sets alternate (the last view
+    gets the caller's ``outputs``); the forward into a buffer waits for the backward of view j - 2 (its last
+    reader), every backward waits for its own forward, and the backwards
+    stay in view order on their stream (they share the scratch and add into
+    ``out``).  The last view's backward runs on the caller's stream after
+    both streams, exactly as in the sequential loop (replay, then the
+    bucketed chain rule + all-reduce for world > 1)."""
+    import torch
+
+    from . import grad, raster
+    dev = scene.device
+    cur = torch.cuda.current_stream(dev)
+    fs, bs = _streams(dev)
+    fs.wait_stream(cur)
+    bs.wait_stream(cur)
+    W, H = int(cameras[0].width), int(cameras[0].height)
+    fbufs = [fbuf, torch.empty_like(fbuf)]
+    outs = [outputs, None]
+    if outputs is None:
+        outs[0] = {}
+    for k in (0, 1):
+        o = outs[k] if outs[k] is not None else {}
+        outs[k] = {key: o.get(key) if o.get(key) is not None else torch.empty(shape, device=dev)
+                   for key, shape in (("color", (H, W, 3)), ("depth", (H, W)),
+                                      ("transmittance", (H, W)), ("alpha", (H, W)),
+                                      ("normal", (H, W, 3)))}
+    fwd_done = [torch.cuda.Event(), torch.cuda.Event()]
+    bwd_done = [torch.cuda.Event(), torch.cuda.Event()]  # view's last reader of its buffers done
+    rep_done = [torch.cuda.Event(), torch.cuda.Event()]
+    # split: each view's chain rule (HBM-bound) on a third stream, beside the
+    # next view's replay (issue-bound); the two alternate between two scratches
+    split = pipe >= 2
+    if split:
+        if scratch is None:
+            from . import _lib
+            scratch = torch.empty(_lib.lib().hgs_backward_scratch_bytes(scene.count, 1),
+                                  dtype=torch.uint8, device=dev)
+        cs = _chain_stream(dev)
+        cs.wait_stream(cur)
+        scratches = [scratch, torch.empty_like(scratch)]
+    n_views = len(cameras)
+    frame = None
+    for j, cam in enumerate(cameras):
+        last = j == n_views - 1
+        b = (n_views - 1 - j) & 1  # the last view renders into the caller's image set
+        with torch.cuda.stream(fs):
+            if j >= 2:
+                fs.wait_event(bwd_done[b])  # view j - 2's backward read this buffer / image set
+            imgs, frame = raster.rasterize(scene, cam, settings, flags, outputs=outs[b],
+                                           events=fwd_events if last else None, async_=True,
+                                           frame_buf=fbufs[b])
+            heads[j].copy_(fbufs[b][:16], non_blocking=True)
+            fwd_done[b].record(fs)
+        if last:
+            break
+        with torch.cuda.stream(bs):
+            bs.wait_event(fwd_done[b])
+            pg = pixel_grads_of(j, imgs)
+            if not split:
+                grad.backward_device(frame, pg, *ext_grads, grads_out=acc, touched_out=touched,
+                                     scratch=scratch, accumulate=j > 0)
+                bwd_done[b].record(bs)
+                continue
+            if j >= 2:
+                bs.wait_event(bwd_done[b])  # view j - 2's chain rule read this scratch
+            grad.backward_device(frame, pg, *ext_grads, grads_out=acc, touched_out=touched,
+                                 scratch=scratches[b], replay_only=True)
+            rep_done[b].record(bs)
+        with torch.cuda.stream(cs):
+            cs.wait_event(rep_done[b])
+            grad.chain_range(frame, 0, scene.count, acc, accumulate=j > 0)
+            bwd_done[b].record(cs)
+    cur.wait_stream(fs)
+    cur.wait_stream(bs)
+    if split:
+        cur.wait_stream(cs)
+        scratch = scratches[0]  # the last view's set (b = 0)
+    # the sequential loop's epilogue: the last view's backward on the caller's stream
+    pg = pixel_grads_of(n_views - 1, imgs)
+    if world == 1:
+        grad.backward_device(frame, pg, *ext_grads, grads_out=acc, touched_out=touched,
+                             scratch=scratch, accumulate=True, events=events)
+        _redo_failed(cameras, heads, view, pixel_grads_of, ext_grads, acc, touched, scratch)
+        return frame
+    grad.backward_device(frame, pg, *ext_grads, grads_out=acc, touched_out=touched,
+                         scratch=scratch, replay_only=True, events=events)
+    if _redo_failed(cameras, heads, view, pixel_grads_of, ext_grads, acc, touched, scratch,
+                    last_excluded=True):
+        frame = view(n_views - 1, cameras[-1], True, False)[1]
+        grad.backward_device(frame, pg, *ext_grads, grads_out=acc, touched_out=touched,
+                             scratch=scratch, replay_only=True)
+    bucketed_allreduce(out, scene.count, scene.sh_bases, buckets,
+                       lambda g0, g1: grad.chain_range(frame, g0, g1, acc, accumulate=True),
+                       group=group)
     return frame
 
 

@@ -65,16 +65,27 @@ def test_replay_only_then_ranged_chain_rule_equals_full_backward():
     assert torch.equal(out, ref)
 
 
-def test_view_batch_grads_one_rank():
+@pytest.mark.parametrize("pipeline", [0, 1, 2])
+@pytest.mark.parametrize("views", [2, 3, 4])
+def test_view_batch_grads_one_rank(pipeline, views):
+    """Sequential and two-stream pipelined view loops both sum every view's
+    gradient; the caller's image buffers end up holding the last view."""
     import torch
 
-    from paper_2512_02932_b200 import parallel
-    ds, cams, pgs, st = _setup()
+    from paper_2512_02932_b200 import parallel, raster
+    ds, cams, pgs, st = _setup(views=views)
     ref = sum(_single(ds, c, st, p)[0] for c, p in zip(cams, pgs))[0]
     out = torch.empty_like(ref)
-    parallel.view_batch_grads(ds, cams, st, lambda j, im: pgs[j], out)
+    h, w = pgs[0].shape[1:3]
+    outputs = dict(color=torch.empty((h, w, 3), device="cuda"), depth=torch.empty((h, w), device="cuda"),
+                   transmittance=torch.empty((h, w), device="cuda"), alpha=torch.empty((h, w), device="cuda"),
+                   normal=torch.empty((h, w, 3), device="cuda"))
+    parallel.view_batch_grads(ds, cams, st, lambda j, im: pgs[j], out, outputs=outputs, pipeline=pipeline)
     err = (out - ref).abs().max() / ref.abs().max()
     assert float(err) < 1e-6
+    last, _ = raster.rasterize(ds, cams[-1], st)
+    for k in ("color", "depth", "transmittance", "normal"):
+        assert torch.equal(outputs[k], last[k]), k
 
 
 def test_densify_statistics_use_pixel_axis_centre_gradient():
@@ -114,7 +125,8 @@ def test_densify_statistics_use_pixel_axis_centre_gradient():
     np.testing.assert_allclose(got[sel], want[sel], rtol=2e-3, atol=1e-6 * want.max())
 
 
-def test_view_batch_grads_redoes_views_that_outgrew_the_pair_capacity():
+@pytest.mark.parametrize("pipeline", [0, 1, 2])
+def test_view_batch_grads_redoes_views_that_outgrew_the_pair_capacity(pipeline):
     """Asynchronous views that overflow the frame's pair capacity composite
     nothing and back-propagate zeros; the batch redoes them synchronously
     (the frame buffer grows), so the summed gradient is unchanged."""
@@ -129,7 +141,7 @@ def test_view_batch_grads_redoes_views_that_outgrew_the_pair_capacity():
         out = torch.empty_like(ref)
         views = cams if first_bad else cams[::-1]
         grads = pgs if first_bad else pgs[::-1]
-        parallel.view_batch_grads(ds, views, st, lambda j, im: grads[j], out)
+        parallel.view_batch_grads(ds, views, st, lambda j, im: grads[j], out, pipeline=pipeline)
         err = (out - ref).abs().max() / ref.abs().max()
         assert float(err) < 1e-6
         assert raster._pair_hint[key] > 1000  # the synchronous redo grew the hint
