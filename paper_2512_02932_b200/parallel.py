@@ -114,6 +114,10 @@ def view_batch_grads(scene, cameras, settings, pixel_grads_of, out, scratch=None
     # nothing and back-propagated zeros, so it is simply redone synchronously
     # (accumulating) once the step's work has drained.
     dev = scene.device
+    if cameras and any((int(c.width), int(c.height)) != (int(cameras[0].width), int(cameras[0].height))
+                       for c in cameras):
+        from .errors import ConfigError
+        raise ConfigError("view_batch_grads: every camera of a batch must have the same image size")
     fbuf = torch.empty(raster.frame_bytes(n, int(cameras[0].width), int(cameras[0].height)),
                        dtype=torch.uint8, device=dev) if cameras else None
     heads = torch.empty((len(cameras), 16), dtype=torch.uint8, pin_memory=True) if cameras else None

@@ -372,6 +372,7 @@ def rasterize(ds, camera, settings, flags=0, outputs=None, events=None, async_=F
             transmittance=torch.empty((H, W), dtype=torch.float32, device=dev),
             alpha=torch.empty((H, W), dtype=torch.float32, device=dev),
             normal=torch.empty((H, W, 3), dtype=torch.float32, device=dev))
+    _check_outputs(outputs, H, W, dev)
     imgs = _lib.Images(*(_lib.ptr(outputs.get(k)) for k in
                          ("color", "depth", "transmittance", "alpha", "normal")))
     if flags & _lib.HGS_FLAG_FRAME_ONLY:
@@ -412,6 +413,25 @@ def rasterize(ds, camera, settings, flags=0, outputs=None, events=None, async_=F
             _pair_hint[key] = max(cap, int(info.k * 1.25) + 1024)
         return outputs, SplatFrame(ds, camera, settings, buf, info, flags)
     raise ConfigError("could not size the pair buffer")
+
+
+_OUT_SHAPES = {"color": 3, "depth": 0, "transmittance": 0, "alpha": 0, "normal": 3}
+
+
+def _check_outputs(outputs, H, W, dev):
+    """Caller-provided image buffers are written through raw pointers: each
+    must be a contiguous float32 tensor of this camera's shape on the scene's
+    device (a buffer sized for another camera would be overrun)."""
+    import torch
+    for k, t in outputs.items():
+        if t is None:
+            continue
+        if k not in _OUT_SHAPES:
+            raise ConfigError("unknown output image %r" % (k,))
+        want = (H, W, 3) if _OUT_SHAPES[k] else (H, W)
+        if (not isinstance(t, torch.Tensor) or t.dtype != torch.float32 or tuple(t.shape) != want
+                or t.device != dev or not t.is_contiguous()):
+            raise ConfigError("output %r must be a contiguous float32 %s tensor on %s" % (k, want, dev))
 
 
 def frame_bytes(n, width, height, pairs=None):
