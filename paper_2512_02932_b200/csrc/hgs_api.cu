@@ -6,6 +6,7 @@
 #include <cstring>
 
 #include "hgs_kernels.cuh"
+#include "hgs_nvtx.h"
 
 namespace hgs {
 
@@ -271,6 +272,7 @@ static int finish_forward(void *frame, const Layout &L, hgs_frame_info *info, co
 
 int hgs_forward(const hgs_scene *scene, const hgs_camera *camera, const hgs_settings *settings, void *frame,
                 size_t frame_bytes, const hgs_images *out, hgs_frame_info *info, void *stream) {
+  NvtxScope nv("hgs_forward");
   int rc = check_common(scene, camera, settings);
   if (rc) return rc;
   if (!info || !frame) return HGS_ERR_CONFIG;
@@ -293,6 +295,7 @@ int hgs_forward(const hgs_scene *scene, const hgs_camera *camera, const hgs_sett
   info->n_tiles = n_tiles; info->pair_capacity = cap; info->sh_bases = scene->sh_bases; info->flags = settings->flags;
 
   HGS_CUDA(record_event(settings, 0, s));
+  nv.stage("front end: depth sort || float64 preprocess");
   // the frame state and histograms, and (n > 0) every look-back slot of the
   // frame (depth sort, tile sort, scan: adjacent), zeroed by one memset so
   // the sort and binning chains are kernels only
@@ -365,6 +368,7 @@ int hgs_forward(const hgs_scene *scene, const hgs_camera *camera, const hgs_sett
     if (fork) HGS_CUDA(cudaStreamWaitEvent(s, static_cast<cudaEvent_t>(settings->aux_events[1]), 0));
   }
   HGS_CUDA(record_event(settings, 1, s));  // stage 1 ends at the join
+  nv.stage("pair-offset scan");
   // 3b. pair-offset scan over the depth order
   if (n > 0) {
     if (!HGS_TILE_COUNTS_AUX) {  // the tile-level cull of the counts, after the join
@@ -378,6 +382,7 @@ int hgs_forward(const hgs_scene *scene, const hgs_camera *camera, const hgs_sett
                         (int64_t)std::min<int64_t>(cap, 0xffffffffll)));
   }
   HGS_CUDA(record_event(settings, 2, s));
+  nv.stage("binning");
   // 4. duplicate + tile sort + ranges (K and the capacity verdict on the device)
   const int nd = n_tiles > kRadix ? 2 : 1;  // tile-sort digit passes
   const bool pairs_in_b = (nd & 1) != 0;    // where the sorted pairs land
@@ -409,6 +414,7 @@ int hgs_forward(const hgs_scene *scene, const hgs_camera *camera, const hgs_sett
                       s, tile_keys, (int64_t)(n > 0 ? -1 : 0), (const FrameState *)st, (int64_t)n_tiles,
                       at<uint32_t>(frame, L.tile_off)));
   HGS_CUDA(record_event(settings, 3, s));
+  nv.stage("composite + fixup");
   if (settings->flags & HGS_FLAG_FRAME_ONLY) return finish_forward(frame, L, info, settings, s);  // build_frame
   // 5. composite
   CompositeArgs a;
@@ -436,6 +442,7 @@ int hgs_forward(const hgs_scene *scene, const hgs_camera *camera, const hgs_sett
   HGS_CUDA(launch_pdl(k_fixup_fwd, dim3(kFixupBlocks), dim3(256), 0, s, a));
   HGS_LAUNCHED();
   HGS_CUDA(record_event(settings, 4, s));
+  nv.stage("finish");
   return finish_forward(frame, L, info, settings, s);
 }
 
@@ -557,6 +564,7 @@ int hgs_backward(const hgs_scene *scene, const hgs_camera *camera, const hgs_set
                  const hgs_frame_info *info, int32_t kg, const float *pixel_grads, const float *depth_grads,
                  const float *normal_grads, const float *alpha_grads, void *scratch, size_t scratch_bytes,
                  float *grads, uint8_t *touched, void *stream) {
+  NvtxScope nv("hgs_backward");
   int rc = check_common(scene, camera, settings);
   if (rc) return rc;
   rc = check_frame(scene, camera, info);
@@ -582,6 +590,7 @@ int hgs_backward(const hgs_scene *scene, const hgs_camera *camera, const hgs_set
   acc_t *acc_ext =
       reinterpret_cast<acc_t *>(static_cast<char *>(scratch) + ((nn * kc_max * 16 * (int64_t)sizeof(acc_t) + 255) & ~255ll));
   HGS_CUDA(record_event(settings, 0, s));
+  nv.stage("back-to-front replay + fixup");
   HGS_CUDA(cudaMemsetAsync(touched, 0, (size_t)nn, s));
   BwdArgs b;
   b.c = composite_args_for(scene, camera, settings, frame, info);
@@ -653,7 +662,10 @@ int hgs_backward(const hgs_scene *scene, const hgs_camera *camera, const hgs_set
           HGS_LAUNCHED();
         }
       }
-      if (k0 == 0) HGS_CUDA(record_event(settings, 1, s));
+      if (k0 == 0) {
+        HGS_CUDA(record_event(settings, 1, s));
+        nv.stage("chain rule");
+      }
     }
     if (replay_only) break;  // kg <= 4: the accumulators stay for hgs_backward_chain
     ChainArgs c = c0;
@@ -670,6 +682,7 @@ int hgs_backward_chain(const hgs_scene *scene, const hgs_camera *camera, const h
                        const void *frame, const hgs_frame_info *info, int32_t kg, const float *depth_grads,
                        const float *normal_grads, const float *alpha_grads, const void *scratch,
                        size_t scratch_bytes, int64_t g0, int64_t g1, float *grads, void *stream) {
+  NvtxScope nv("hgs_backward_chain");
   int rc = check_common(scene, camera, settings);
   if (rc) return rc;
   rc = check_frame(scene, camera, info);
@@ -721,11 +734,13 @@ extern "C" {
 
 int hgs_exchange(int64_t n, float *log_scale, float *rotation, uint8_t *type_spec, double theta_e, float *eranks,
                  void *scratch, hgs_exchange_report *report, void *stream) {
+  NvtxScope nv("hgs_exchange");
   return exchange_impl<float>(n, log_scale, rotation, type_spec, theta_e, eranks, scratch, report, stream);
 }
 
 int hgs_exchange_f64(int64_t n, double *log_scale, double *rotation, uint8_t *type_spec, double theta_e,
                      double *eranks, void *scratch, hgs_exchange_report *report, void *stream) {
+  NvtxScope nv("hgs_exchange_f64");
   return exchange_impl<double>(n, log_scale, rotation, type_spec, theta_e, eranks, scratch, report, stream);
 }
 

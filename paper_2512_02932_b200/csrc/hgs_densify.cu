@@ -23,6 +23,7 @@
 #include <cmath>
 
 #include "hgs_kernels.cuh"
+#include "hgs_nvtx.h"
 #include "../../include/hgs_train.h"
 
 namespace hgs {
@@ -297,6 +298,7 @@ extern "C" {
 int hgs_densify_stats(const hgs_scene *scene, const hgs_camera *camera, const void *frame,
                       const hgs_frame_info *info, const void *bwd_scratch, int32_t kg, const uint8_t *touched,
                       float *grad_accum, int32_t *obs_count, void *stream) {
+  NvtxScope nv("hgs_densify_stats");
   if (!scene || !camera || scene->n < 0 || kg < 1 || kg > 4) return HGS_ERR_CONFIG;
   if (scene->n == 0) return HGS_OK;
   if (!bwd_scratch || !touched || !grad_accum || !obs_count || !frame || !info) return HGS_ERR_INTEGRITY;
@@ -322,6 +324,7 @@ size_t hgs_densify_scratch_bytes(int64_t n) {
 int hgs_densify_plan(const hgs_scene *scene, const float *grad_accum, const int32_t *obs_count,
                      const hgs_densify_config *cfg, void *scratch, size_t scratch_bytes, int64_t *n_out,
                      int64_t *census, void *stream) {
+  NvtxScope nv("hgs_densify_plan");
   if (!scene || !cfg || !n_out || scene->n < 0) return HGS_ERR_CONFIG;
   if (!(cfg->prune_opacity >= 0.0 && cfg->prune_opacity < 1.0) || !(cfg->split_scale > 0.0) ||
       !(cfg->grad_threshold >= 0.0))
@@ -358,6 +361,7 @@ int hgs_densify_plan(const hgs_scene *scene, const float *grad_accum, const int3
 int hgs_densify_apply(const hgs_scene *scene, const float *exp_avg, const float *exp_avg_sq, const void *scratch,
                       const hgs_densify_config *cfg, const hgs_params *out, uint8_t *out_type_spec,
                       float *out_exp_avg, float *out_exp_avg_sq, void *stream) {
+  NvtxScope nv("hgs_densify_apply");
   if (!scene || !cfg || !out || scene->n < 0 || out->sh_bases != scene->sh_bases) return HGS_ERR_CONFIG;
   if (scene->n == 0 || out->n == 0) return HGS_OK;
   if (!scratch || !out_type_spec || ((out_exp_avg == nullptr) != (out_exp_avg_sq == nullptr)))

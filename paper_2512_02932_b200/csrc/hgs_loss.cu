@@ -21,6 +21,7 @@
 #include <cmath>
 
 #include "hgs_kernels.cuh"
+#include "hgs_nvtx.h"
 #include "../../include/hgs_train.h"
 
 namespace hgs {
@@ -361,6 +362,7 @@ size_t hgs_loss_scratch_bytes(int32_t height, int32_t width, int32_t channels) {
 int hgs_image_losses(int32_t height, int32_t width, int32_t channels, const float *rendered, const float *gt,
                      const hgs_loss_weights *weights, double *losses, float *pixel_grads, void *scratch,
                      size_t scratch_bytes, void *stream) {
+  NvtxScope nv("hgs_image_losses");
   if (height <= 0 || width <= 0 || channels <= 0 || !rendered || !gt || !weights || !losses) return HGS_ERR_CONFIG;
   if (weights->lam < 0.0 || weights->lam > 1.0 || weights->lambda_low < 0.0 || weights->lambda_high < 0.0)
     return HGS_ERR_CONFIG;
@@ -393,6 +395,7 @@ int hgs_image_losses(int32_t height, int32_t width, int32_t channels, const floa
 
 int hgs_dwt_level1(int32_t height, int32_t width, int32_t channels, const float *image, float *ll, float *lh,
                    float *hl, float *hh, void *stream) {
+  NvtxScope nv("hgs_dwt_level1");
   if (height <= 0 || width <= 0 || channels <= 0 || !image || !ll || !lh || !hl || !hh) return HGS_ERR_CONFIG;
   const int64_t total = (int64_t)((height + 1) / 2) * ((width + 1) / 2) * channels;
   const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
@@ -403,6 +406,7 @@ int hgs_dwt_level1(int32_t height, int32_t width, int32_t channels, const float 
 
 int hgs_dwt_inverse(int32_t height, int32_t width, int32_t channels, const float *ll, const float *lh,
                     const float *hl, const float *hh, int32_t adjoint, float *image, void *stream) {
+  NvtxScope nv("hgs_dwt_inverse");
   if (height <= 0 || width <= 0 || channels <= 0 || !image || !ll || !lh || !hl || !hh) return HGS_ERR_CONFIG;
   const int64_t total = (int64_t)height * width * channels;
   const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);

@@ -15,6 +15,7 @@
 #include <cmath>
 
 #include "hgs_kernels.cuh"
+#include "hgs_nvtx.h"
 #include "../../include/hgs_train.h"
 
 namespace hgs {
@@ -267,6 +268,7 @@ extern "C" {
 int hgs_combine_gradients(int64_t n, int32_t sh_bases, const float *g_color, const float *g_low,
                           const float *g_high, const uint8_t *type_spec, int32_t mode, float *out,
                           unsigned long long *n_conflicts, void *stream) {
+  NvtxScope nv("hgs_combine_gradients");
   if (n < 0 || !sh_ok(sh_bases) || mode < 0 || mode > 2) return HGS_ERR_CONFIG;
   if (n > 0 && (!g_color || !g_low || !g_high || !type_spec || !out)) return HGS_ERR_INTEGRITY;
   OptArgs a{};
@@ -278,6 +280,7 @@ int hgs_combine_gradients(int64_t n, int32_t sh_bases, const float *g_color, con
 
 int hgs_adam_step(const hgs_params *params, const float *grads, float *exp_avg, float *exp_avg_sq,
                   const hgs_adam *cfg, void *stream) {
+  NvtxScope nv("hgs_adam_step");
   if (!params || params->n < 0 || !sh_ok(params->sh_bases)) return HGS_ERR_CONFIG;
   OptArgs a{};
   a.n = params->n; a.B = params->sh_bases;
@@ -291,6 +294,7 @@ int hgs_adam_step(const hgs_params *params, const float *grads, float *exp_avg, 
 int hgs_combine_adam_step(const hgs_params *params, const float *g_color, const float *g_low, const float *g_high,
                           const uint8_t *type_spec, int32_t mode, float *exp_avg, float *exp_avg_sq,
                           const hgs_adam *cfg, unsigned long long *n_conflicts, void *stream) {
+  NvtxScope nv("hgs_combine_adam_step");
   if (!params || params->n < 0 || !sh_ok(params->sh_bases) || mode < 0 || mode > 2) return HGS_ERR_CONFIG;
   OptArgs a{};
   a.n = params->n; a.B = params->sh_bases;
