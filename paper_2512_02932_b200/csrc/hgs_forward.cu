@@ -5,7 +5,7 @@
 #include "hgs_kernels.cuh"
 
 #ifndef HGS_PRE_CTAS
-#define HGS_PRE_CTAS 12  // A/B 8 / 12 / 24 / 48: 12 leaves room for the depth sort beside it
+#define HGS_PRE_CTAS 14  // A/B 8 / 12 / 13 / 14 / 15 / 16 / 18 / 24 / 48: 14 still leaves room for the depth sort beside it
 #endif
 #ifndef HGS_PRE_PREFETCH
 #define HGS_PRE_PREFETCH 1
